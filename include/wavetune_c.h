@@ -1,0 +1,295 @@
+/*
+ * wavetune_c.h -- C-ABI of the B200-native WaveTune decision path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no C++ or torch
+ * types.  The C++ drop-in API (include/wavetune/*.hpp, namespace wavetune)
+ * and the Python module are thin layers over these entry points; a
+ * cgo/JNI/ctypes binding would bind exactly this header.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *   wt_engine_create   -- the (tables, registry, hw) triple every query of
+ *                         tune() takes (include/wavetune/tuner.hpp:51-52);
+ *                         validated and resolved once, held on the device.
+ *   wt_tune_batch      -- wavetune::tune() (tuner.hpp:51-52, tuner.cpp:159-166)
+ *                         for n queries at once (Stage I argmin + Stage II).
+ *   wt_predict_batch   -- wavetune::predict_latency() (tuner.hpp:38-40,
+ *                         tuner.cpp:11-42).
+ *   wt_explain         -- the per-table loop inside two_stage_select
+ *                         (tuner.cpp:135-149) for one query, so the host can
+ *                         rebuild Tuned.flags text exactly.
+ *   wt_nearest_anchor_batch -- wavetune::nearest_anchor() (tuner.hpp:44-45).
+ *   wt_grid_* / wt_sweep / wt_gather_batch -- extension (no reference
+ *                         symbol): tune() materialised over a shape grid
+ *                         ("dual lookup tables ... answer online queries")
+ *                         and a table-gather for online queries.
+ *   wt_fit_build       -- wavetune::build_dual_table() (model.hpp:95-98,
+ *                         model.cpp:194-253) incl. select_shared_micro,
+ *                         fit_bucket and fit_extrapolation.
+ *   wt_fit_bucket_batch -- wavetune::fit_bucket() (model.hpp:42).
+ *
+ * Conventions.
+ *   - Every entry point returns wt_status; on failure wt_last_error() holds
+ *     the reference's message text for the same condition (thread-local).
+ *   - "device" pointers are CUDA device (or managed) memory; "host" pointers
+ *     are host memory.  Batched calls are stream-ordered on the given
+ *     cudaStream_t (passed as void*, NULL = legacy default stream) and never
+ *     synchronise the device unless the name ends in _sync.
+ *   - Handles are immutable after creation; any number of host threads may
+ *     issue batched calls on different streams concurrently.
+ *   - Per-query failures (the reference would throw for that query) do not
+ *     fail the batch: they are reported in the query's status byte
+ *     (bits 24..31 of flags, a wt_status value) and its macro_id is -1.
+ */
+#ifndef WAVETUNE_C_H
+#define WAVETUNE_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WT_ABI_VERSION 1
+
+typedef enum {
+    WT_OK = 0,
+    WT_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    WT_RUNTIME_ERROR = 2,    /* std::runtime_error */
+    WT_OUT_OF_RANGE = 3,     /* std::out_of_range */
+    WT_CUDA_ERROR = 4,
+    WT_UNSUPPORTED = 5       /* outside the device path's documented domain */
+} wt_status;
+
+/* Kernel families (kernel_map.hpp:19). */
+enum { WT_FAMILY_DENSE_GEMM = 0, WT_FAMILY_GROUPED_GEMM = 1, WT_FAMILY_FLASH_ATTENTION = 2 };
+
+/* Decision flag bits (wt_decisions.flags). */
+enum {
+    WT_FLAG_EXTRAPOLATED = 1u << 0,   /* Regime.extrapolated of the winner */
+    WT_FLAG_MISSING_WAVE = 1u << 1,   /* some table used a missing_wave_<w>_used_<k> fallback */
+    WT_FLAG_ANCHOR_FALLBACK = 1u << 2 /* winner used anchor_fallback_wave_<k> */
+};
+#define WT_FLAG_STATUS(f) ((int)(((uint32_t)(f)) >> 24))
+
+const char* wt_last_error(void);
+const char* wt_version(void);
+int wt_abi_version(void);
+
+/* ---- inputs ----------------------------------------------------------- */
+
+/* HardwareSpec (kernel_map.hpp:67-73); slots = n_sm * blocks_per_sm. */
+typedef struct {
+    int32_t n_sm;
+    int32_t blocks_per_sm;
+} wt_hw;
+
+/* ConfigRegistry macros (kernel_map.hpp:47-60,81-94), host arrays.  For
+ * FlashAttention registries t_m = t_q, t_k = t_kv and t_n is ignored. */
+typedef struct {
+    int32_t family;
+    int32_t n_macros;
+    const int32_t* id;
+    const int64_t* t_m;
+    const int64_t* t_n;
+    const int64_t* t_k;
+} wt_registry_desc;
+
+/* std::vector<DualTable> (model.hpp:64-77), host arrays.  Every std::map is
+ * a key-ascending CSR slice; tables may be in any order (tune() sorts them
+ * by macro_id, tuner.cpp:127-132). */
+typedef struct {
+    int32_t n_tables;
+    const int32_t* macro_id;   /* [n_tables] */
+    const int32_t* W;          /* [n_tables] */
+    const double* theta_ext;   /* [n_tables*4] alpha, beta, gamma, delta */
+    const int32_t* coeff_off;  /* [n_tables+1] -> coeff_w / coeff_theta */
+    const int32_t* coeff_w;    /* coeff_table keys (wave), ascending per table */
+    const double* coeff_theta; /* [4 per key] */
+    const int32_t* awave_off;  /* [n_tables+1] -> awave_w / awave_aoff */
+    const int32_t* awave_w;    /* anchor_table keys (wave), ascending per table */
+    const int32_t* awave_aoff; /* [n_awave+1] -> anchor_l / anchor_micro */
+    const int64_t* anchor_l;   /* loop anchors, ascending per map */
+    const int32_t* anchor_micro;
+    const int32_t* ext_aoff;   /* [n_tables+1] -> ext_l / ext_micro */
+    const int64_t* ext_l;
+    const int32_t* ext_micro;
+} wt_tables_desc;
+
+/* ---- engine: validated, fallback-resolved device image ------------------ */
+
+typedef struct wt_engine wt_engine;
+
+typedef struct {
+    int32_t n_configs;   /* Stage-I candidates C (= tables) */
+    int32_t n_rows;      /* coefficient rows per config (max W + 1) */
+    int32_t slots;       /* n_sm * blocks_per_sm */
+    int32_t family;
+    int32_t has_fallback_rows; /* any resolved missing-wave / empty-table row */
+    int32_t device;
+    size_t device_bytes; /* bytes of the resident image */
+} wt_engine_info;
+
+/* Validates like the reference (duplicate ids -> INVALID_ARGUMENT, table id
+ * absent from the registry -> OUT_OF_RANGE "no macro config with id N",
+ * no tables -> INVALID_ARGUMENT "no dual tables provided") and uploads.
+ * Synchronous (host -> device copies complete on return). */
+wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc* registry,
+                           const wt_hw* hw, int device, wt_engine** out);
+wt_status wt_engine_destroy(wt_engine* e);
+wt_status wt_engine_info_get(const wt_engine* e, wt_engine_info* out);
+/* Position of macro_id in the engine's ascending config order, or -1. */
+int32_t wt_engine_config_index(const wt_engine* e, int32_t macro_id);
+
+/* ---- outputs ---------------------------------------------------------- */
+
+/* Per-query decision arrays (device).  Required: macro_id, micro_id,
+ * latency_us.  Optional (NULL to skip): g, l, wave, flags, comparisons,
+ * tail_frac, and the top-k block (k >= 1, [n*k] each, extension). */
+typedef struct {
+    int32_t* macro_id;
+    int32_t* micro_id;
+    double* latency_us;
+    int64_t* g;
+    int64_t* l;
+    int32_t* wave;        /* Regime.w */
+    uint32_t* flags;      /* WT_FLAG_* | status << 24 */
+    int32_t* comparisons; /* DecisionStats.anchor_comparisons */
+    double* tail_frac;    /* (g - (w-1)*slots) / slots of the winner (extension) */
+    int32_t topk;         /* 0 = off */
+    int32_t* topk_macro;
+    double* topk_latency;
+} wt_decisions;
+
+/* ---- batched tune (evaluate mode: every query runs full Stage I) -------- */
+
+/* Dense GEMM (M,N,K) / FlashAttention (s_q,n_heads,s_kv) queries, int32
+ * device arrays; dims must be >= 1 (else per-query INVALID_ARGUMENT). */
+wt_status wt_tune_batch(const wt_engine* e, const int32_t* M, const int32_t* N, const int32_t* K,
+                        int64_t n, const wt_decisions* out, void* stream);
+
+/* Grouped GEMM queries: query i has group rows rows[row_off[i] .. row_off[i+1])
+ * (device arrays) and dims (N[i], K[i]) (kernel_map.cpp:244-257). */
+wt_status wt_tune_grouped_batch(const wt_engine* e, const int64_t* row_off, const int32_t* rows,
+                                const int32_t* N, const int32_t* K, int64_t n,
+                                const wt_decisions* out, void* stream);
+
+/* predict_latency for n (config index, g, l) triples (device arrays).
+ * used_w = fallback wave when missing_wave_<w>_used_<k> fired, else -1. */
+wt_status wt_predict_batch(const wt_engine* e, const int32_t* config, const int64_t* g,
+                           const int64_t* l, int64_t n, double* latency_us, int32_t* wave,
+                           int32_t* extrapolated, int32_t* used_w, int32_t* status, void* stream);
+
+/* For one dense query, every config in ascending macro_id order (device
+ * arrays of length n_configs): g, l, wave, used_w, latency. */
+wt_status wt_explain(const wt_engine* e, int64_t M, int64_t N, int64_t K, int64_t* g, int64_t* l,
+                     int32_t* wave, int32_t* used_w, double* latency_us, int32_t* status,
+                     void* stream);
+
+/* Anchor map of (config, row) as resolved at upload: writes up to cap
+ * anchors/micros (host) and returns the count, or -1. */
+int32_t wt_engine_anchor_map(const wt_engine* e, int32_t config, int32_t wave, int32_t extrapolated,
+                             int64_t* anchors, int32_t* micros, int32_t cap, int32_t* fallback_wave);
+
+/* nearest_anchor over a sorted device list, n queries. */
+wt_status wt_nearest_anchor_batch(const int64_t* anchors, int32_t n_anchors, const int64_t* l,
+                                  int64_t n, int64_t* out, int32_t* comparisons, void* stream);
+
+/* ---- decision grid (extension): tune() materialised over shapes --------- */
+
+typedef struct wt_grid wt_grid;
+
+/* Grid over n_pairs (N, K) pairs (host arrays) x M in [m_lo, m_hi].
+ * Entry index = pair * (m_hi - m_lo + 1) + (M - m_lo). */
+typedef struct {
+    int32_t n_pairs;
+    const int32_t* N;
+    const int32_t* K;
+    int32_t m_lo, m_hi;
+    int32_t topk; /* 0 = argmin only */
+} wt_grid_desc;
+
+/* 32-byte grid entry (device layout). */
+typedef struct {
+    double latency_us;
+    int32_t macro_id;
+    int32_t micro_id;
+    int32_t wave;
+    uint32_t flags;
+    int32_t comparisons;
+    float tail_frac;
+} wt_grid_entry;
+
+wt_status wt_grid_create(const wt_engine* e, const wt_grid_desc* desc, wt_grid** out);
+wt_status wt_grid_destroy(wt_grid* g);
+/* Raw device storage (for collectives / inspection). */
+wt_status wt_grid_storage(const wt_grid* g, wt_grid_entry** entries, int64_t* n_entries,
+                          int32_t** topk_macro, double** topk_latency);
+/* Fills entries [begin, end) (flattened index) -- one shard of the sweep. */
+wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, void* stream);
+/* Online queries: on-grid shapes are gathered; off-grid ones are compacted
+ * and evaluated in full (wt_tune_batch semantics).  Needs no host sync. */
+wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M, const int32_t* N,
+                          const int32_t* K, int64_t n, const wt_decisions* out, void* stream);
+
+/* Kernel launch counter (for bench accounting): total launches issued by
+ * this library in this process. */
+int64_t wt_launch_count(void);
+
+/* ---- batched fit / dual-table build (K2) --------------------------------- */
+
+/* ProfileRecord SoA (profiler.hpp:56-63), host arrays. */
+typedef struct {
+    int64_t n;
+    const int64_t* g;
+    const int64_t* l;
+    const int32_t* w;
+    const int32_t* macro_id;
+    const int32_t* micro_id;
+    const double* latency_us;
+} wt_records_desc;
+
+/* Built tables, library-owned host arrays (valid until wt_build_free). */
+typedef struct {
+    int32_t n_tables, W, p;
+    const int32_t* macro_id;
+    const double* theta_ext;
+    const int32_t* ext_flags;    /* bit0 ext_degenerate_fit, bit1 ext_insufficient_waves */
+    const int32_t* coeff_off;
+    const int32_t* coeff_w;
+    const double* coeff_theta;
+    const double* diag_r2;
+    const double* diag_mape;
+    const int32_t* diag_samples;
+    const int32_t* diag_flags;   /* bit0 degenerate_fit, bit1 sparse_bucket */
+    const int32_t* awave_off;
+    const int32_t* awave_w;
+    const int32_t* awave_aoff;
+    const int64_t* anchor_l;
+    const int32_t* anchor_micro;
+    const int32_t* anchor_partial; /* partial_micro_coverage_l<l> */
+    const int32_t* ext_aoff;
+    const int64_t* ext_l;
+    const int32_t* ext_micro;
+    double device_ms;            /* GPU time of the build (CUDA events) */
+} wt_build_result;
+
+typedef struct wt_build wt_build;
+
+/* build_dual_table(records, registry, hw, {W, p}) on the GPU.  registry_ids
+ * is the registry's macro order (tables come out in that order). */
+wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_ids,
+                       int32_t n_macros, int32_t W, int32_t p, int device, wt_build** out,
+                       wt_build_result* result);
+wt_status wt_build_free(wt_build* b);
+
+/* fit_bucket over nb independent buckets in one launch: samples of bucket b
+ * are [off[b], off[b+1]) of g/l/t (host arrays).  coeffs [nb*4]. */
+wt_status wt_fit_bucket_batch(const double* g, const double* l, const double* t,
+                              const int64_t* off, int64_t nb, double* coeffs, double* r2,
+                              double* mape, int32_t* degenerate, int device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WAVETUNE_C_H */

@@ -1,0 +1,281 @@
+"""ctypes binding of the C-ABI in include/wavetune_c.h.
+
+This is the exact binding a Python caller of the boundary would write (see
+INTEGRATION.md).  Device buffers are torch tensors (plumbing only); every
+computation happens in lib/libwtb200.so's sm_100a kernels.  Importing this
+module fails loudly if the library is missing -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libwtb200.so")
+
+WT_OK, WT_INVALID_ARGUMENT, WT_RUNTIME_ERROR, WT_OUT_OF_RANGE, WT_CUDA_ERROR, WT_UNSUPPORTED = range(6)
+WT_FAMILY_DENSE_GEMM, WT_FAMILY_GROUPED_GEMM, WT_FAMILY_FLASH_ATTENTION = range(3)
+WT_FLAG_EXTRAPOLATED, WT_FLAG_MISSING_WAVE, WT_FLAG_ANCHOR_FALLBACK = 1, 2, 4
+
+STATUS_NAMES = {0: "ok", 1: "invalid_argument", 2: "runtime_error", 3: "out_of_range", 4: "cuda_error",
+                5: "unsupported"}
+
+vp = C.c_void_p
+
+
+class WtError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+        self.msg = msg
+
+
+class wt_hw(C.Structure):
+    _fields_ = [("n_sm", C.c_int32), ("blocks_per_sm", C.c_int32)]
+
+
+class wt_registry_desc(C.Structure):
+    _fields_ = [("family", C.c_int32), ("n_macros", C.c_int32), ("id", vp), ("t_m", vp), ("t_n", vp),
+                ("t_k", vp)]
+
+
+_TABLE_FIELDS = ("macro_id W theta_ext coeff_off coeff_w coeff_theta awave_off awave_w awave_aoff "
+                 "anchor_l anchor_micro ext_aoff ext_l ext_micro").split()
+
+
+class wt_tables_desc(C.Structure):
+    _fields_ = [("n_tables", C.c_int32)] + [(n, vp) for n in _TABLE_FIELDS]
+
+
+class wt_engine_info(C.Structure):
+    _fields_ = [("n_configs", C.c_int32), ("n_rows", C.c_int32), ("slots", C.c_int32), ("family", C.c_int32),
+                ("has_fallback_rows", C.c_int32), ("device", C.c_int32), ("device_bytes", C.c_size_t)]
+
+
+class wt_decisions(C.Structure):
+    _fields_ = [("macro_id", vp), ("micro_id", vp), ("latency_us", vp), ("g", vp), ("l", vp), ("wave", vp),
+                ("flags", vp), ("comparisons", vp), ("tail_frac", vp), ("topk", C.c_int32),
+                ("topk_macro", vp), ("topk_latency", vp)]
+
+
+class wt_grid_desc(C.Structure):
+    _fields_ = [("n_pairs", C.c_int32), ("N", vp), ("K", vp), ("m_lo", C.c_int32), ("m_hi", C.c_int32),
+                ("topk", C.c_int32)]
+
+
+class wt_records_desc(C.Structure):
+    _fields_ = [("n", C.c_int64), ("g", vp), ("l", vp), ("w", vp), ("macro_id", vp), ("micro_id", vp),
+                ("latency_us", vp)]
+
+
+_BUILD_FIELDS = ("macro_id theta_ext ext_flags coeff_off coeff_w coeff_theta diag_r2 diag_mape diag_samples "
+                 "diag_flags awave_off awave_w awave_aoff anchor_l anchor_micro anchor_partial ext_aoff ext_l "
+                 "ext_micro").split()
+
+
+class wt_build_result(C.Structure):
+    _fields_ = [("n_tables", C.c_int32), ("W", C.c_int32), ("p", C.c_int32)] + [(n, vp) for n in _BUILD_FIELDS] + [
+        ("device_ms", C.c_double)]
+
+
+# entry points declared in include/wavetune_c.h (tests check they all exist)
+EXPORTS = (
+    "wt_last_error wt_version wt_abi_version wt_engine_create wt_engine_destroy wt_engine_info_get "
+    "wt_engine_config_index wt_tune_batch wt_tune_grouped_batch wt_predict_batch wt_explain "
+    "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_destroy wt_grid_storage wt_sweep "
+    "wt_gather_batch wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch").split()
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        L.wt_last_error.restype = C.c_char_p
+        L.wt_version.restype = C.c_char_p
+        L.wt_launch_count.restype = C.c_int64
+        L.wt_engine_config_index.restype = C.c_int32
+        L.wt_engine_anchor_map.restype = C.c_int32
+        _lib = L
+    return _lib
+
+
+def check(st):
+    if st != WT_OK:
+        raise WtError(st, lib().wt_last_error().decode())
+
+
+def launch_count():
+    return int(lib().wt_launch_count())
+
+
+def _ptr(t):
+    """Raw pointer of a numpy array or torch tensor (None -> NULL)."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+class Engine:
+    """Owns a wt_engine (device image of tables + registry + hardware)."""
+
+    def __init__(self, tables: dict, registry: dict, n_sm: int, blocks_per_sm: int = 1, device: int = 0):
+        L = lib()
+        self._keep = []
+
+        def arr(x, dt):
+            a = np.ascontiguousarray(x, dtype=dt)
+            if a.size == 0:
+                a = np.zeros(1, dt)
+            self._keep.append(a)
+            return a.ctypes.data
+
+        td = wt_tables_desc()
+        td.n_tables = len(tables["macro_id"])
+        dts = dict(macro_id=np.int32, W=np.int32, theta_ext=np.float64, coeff_off=np.int32, coeff_w=np.int32,
+                   coeff_theta=np.float64, awave_off=np.int32, awave_w=np.int32, awave_aoff=np.int32,
+                   anchor_l=np.int64, anchor_micro=np.int32, ext_aoff=np.int32, ext_l=np.int64,
+                   ext_micro=np.int32)
+        for k in _TABLE_FIELDS:
+            setattr(td, k, arr(tables[k], dts[k]))
+        rd = wt_registry_desc()
+        rd.family = registry.get("family", WT_FAMILY_DENSE_GEMM)
+        rd.n_macros = len(registry["id"])
+        rd.id = arr(registry["id"], np.int32)
+        rd.t_m = arr(registry["t_m"], np.int64)
+        rd.t_n = arr(registry["t_n"], np.int64)
+        rd.t_k = arr(registry["t_k"], np.int64)
+        hw = wt_hw(n_sm, blocks_per_sm)
+        h = C.c_void_p()
+        check(L.wt_engine_create(C.byref(td), C.byref(rd), C.byref(hw), C.c_int(device), C.byref(h)))
+        self.handle = h
+        self.device = device
+        self._keep = []
+        info = wt_engine_info()
+        check(L.wt_engine_info_get(h, C.byref(info)))
+        self.info = info
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().wt_engine_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def n_configs(self):
+        return self.info.n_configs
+
+    def config_index(self, macro_id):
+        return int(lib().wt_engine_config_index(self.handle, C.c_int32(macro_id)))
+
+    def anchor_map(self, config, wave, extrapolated):
+        a = np.zeros(64, np.int64)
+        m = np.zeros(64, np.int32)
+        fb = np.zeros(1, np.int32)
+        n = lib().wt_engine_anchor_map(self.handle, C.c_int32(config), C.c_int32(wave), C.c_int32(extrapolated),
+                                       C.c_void_p(a.ctypes.data), C.c_void_p(m.ctypes.data), C.c_int32(64),
+                                       C.c_void_p(fb.ctypes.data))
+        return (a[:n], m[:n], int(fb[0])) if n >= 0 else None
+
+    @staticmethod
+    def decisions(macro, micro, lat, g=None, l=None, wave=None, flags=None, comps=None, tail=None,
+                  topk=0, topk_macro=None, topk_lat=None):
+        d = wt_decisions()
+        for name, t in (("macro_id", macro), ("micro_id", micro), ("latency_us", lat), ("g", g), ("l", l),
+                        ("wave", wave), ("flags", flags), ("comparisons", comps), ("tail_frac", tail),
+                        ("topk_macro", topk_macro), ("topk_latency", topk_lat)):
+            setattr(d, name, _ptr(t))
+        d.topk = topk
+        return d
+
+    def tune_batch(self, M, N, K, out: wt_decisions, stream=None):
+        check(lib().wt_tune_batch(self.handle, vp(_ptr(M)), vp(_ptr(N)), vp(_ptr(K)), C.c_int64(M.numel()),
+                                  C.byref(out), vp(_stream_ptr(stream))))
+
+    def tune_grouped_batch(self, row_off, rows, N, K, out, stream=None):
+        check(lib().wt_tune_grouped_batch(self.handle, vp(_ptr(row_off)), vp(_ptr(rows)), vp(_ptr(N)),
+                                          vp(_ptr(K)), C.c_int64(N.numel()), C.byref(out),
+                                          vp(_stream_ptr(stream))))
+
+    def predict_batch(self, config, g, l, lat, wave=None, extrap=None, used_w=None, status=None, stream=None):
+        check(lib().wt_predict_batch(self.handle, vp(_ptr(config)), vp(_ptr(g)), vp(_ptr(l)),
+                                     C.c_int64(config.numel()), vp(_ptr(lat)), vp(_ptr(wave)), vp(_ptr(extrap)),
+                                     vp(_ptr(used_w)), vp(_ptr(status)), vp(_stream_ptr(stream))))
+
+    def explain(self, M, N, K, g, l, wave, used_w, lat, status, stream=None):
+        check(lib().wt_explain(self.handle, C.c_int64(M), C.c_int64(N), C.c_int64(K), vp(_ptr(g)), vp(_ptr(l)),
+                               vp(_ptr(wave)), vp(_ptr(used_w)), vp(_ptr(lat)), vp(_ptr(status)),
+                               vp(_stream_ptr(stream))))
+
+
+class Grid:
+    """A decision grid: tune() over n_pairs (N, K) x M in [m_lo, m_hi]."""
+
+    def __init__(self, engine: Engine, N, K, m_lo, m_hi, topk=0):
+        self.engine = engine
+        self._N = np.ascontiguousarray(N, np.int32)
+        self._K = np.ascontiguousarray(K, np.int32)
+        d = wt_grid_desc(len(self._N), self._N.ctypes.data, self._K.ctypes.data, m_lo, m_hi, topk)
+        h = C.c_void_p()
+        check(lib().wt_grid_create(engine.handle, C.byref(d), C.byref(h)))
+        self.handle = h
+        self.m_lo, self.m_hi, self.topk = m_lo, m_hi, topk
+        ent, n = C.c_void_p(), C.c_int64()
+        tkm, tkl = C.c_void_p(), C.c_void_p()
+        check(lib().wt_grid_storage(h, C.byref(ent), C.byref(n), C.byref(tkm), C.byref(tkl)))
+        self.entries_ptr, self.n_entries = ent.value, n.value
+        self.topk_macro_ptr, self.topk_lat_ptr = tkm.value, tkl.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().wt_grid_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sweep(self, begin=0, end=None, stream=None):
+        end = self.n_entries if end is None else end
+        check(lib().wt_sweep(self.engine.handle, self.handle, C.c_int64(begin), C.c_int64(end),
+                             vp(_stream_ptr(stream))))
+
+    def gather(self, M, N, K, out: wt_decisions, stream=None):
+        check(lib().wt_gather_batch(self.engine.handle, self.handle, vp(_ptr(M)), vp(_ptr(N)), vp(_ptr(K)),
+                                    C.c_int64(M.numel()), C.byref(out), vp(_stream_ptr(stream))))
+
+    def entries_tensor(self):
+        """The grid's device storage viewed as an int32 [n_entries, 8] torch tensor (no copy)."""
+        import torch
+
+        class _Cuda:
+            pass
+
+        holder = _Cuda()
+        holder.__cuda_array_interface__ = {
+            "shape": (self.n_entries, 8), "typestr": "<i4", "data": (self.entries_ptr, False), "version": 3,
+            "strides": None,
+        }
+        return torch.as_tensor(holder, device=f"cuda:{self.engine.device}")

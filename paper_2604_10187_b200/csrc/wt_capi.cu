@@ -1,0 +1,515 @@
+// wt_capi.cu -- the extern "C" boundary declared in include/wavetune_c.h.
+// Owns device images (engines) and decision grids, validates inputs the way
+// the reference does, and launches the sm_100a kernels of wt_decide.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "wavetune_c.h"
+#include "wt_decide.h"
+#include "wt_internal.h"
+
+using namespace wtb;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+wt_status set_err(wt_status st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+
+wt_status cuda_err(cudaError_t e, const char* where) {
+    return set_err(WT_CUDA_ERROR, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int d) {
+        cudaGetDevice(&prev);
+        if (prev != d) cudaSetDevice(d);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// One device allocation carved into 256-byte aligned pieces.
+struct Arena {
+    size_t used = 0;
+    size_t take(size_t bytes) {
+        size_t off = used;
+        used += (bytes + 255) & ~size_t(255);
+        return off;
+    }
+};
+
+int sm_count(int device) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+    return n;
+}
+
+}  // namespace
+
+struct wt_engine {
+    int device = 0;
+    HostImage host;
+    DevImage dev{};
+    void* mem = nullptr;
+    size_t bytes = 0;
+    int eval_chunk = 0;
+    int eval_grid = 0;
+};
+
+struct wt_grid {
+    const wt_engine* eng = nullptr;
+    int32_t n_pairs = 0;
+    int32_t m_lo = 1, m_hi = 0;
+    int64_t mcount = 0, n_entries = 0;
+    int32_t topk = 0;
+    bool wide = false;
+    int sweep_chunk = 0;
+    void* mem = nullptr;
+    int32_t* dN = nullptr;
+    int32_t* dK = nullptr;
+    uint64_t* dkeys = nullptr;
+    int32_t* dpid = nullptr;
+    wt_grid_entry* entries = nullptr;
+    int32_t* tk_macro = nullptr;
+    double* tk_lat = nullptr;
+    int32_t n_keys = 0;
+};
+
+extern "C" {
+
+const char* wt_last_error(void) { return g_err.c_str(); }
+const char* wt_version(void) { return "wavetune-b200 0.1 (sm_100a)"; }
+int wt_abi_version(void) { return WT_ABI_VERSION; }
+int64_t wt_launch_count(void) { return g_launches.load(); }
+
+wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc* registry,
+                           const wt_hw* hw, int device, wt_engine** out) {
+    if (!tables || !registry || !hw || !out) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    auto* e = new wt_engine;
+    e->device = device;
+    std::string err;
+    wt_status st = build_image(*tables, *registry, *hw, &e->host, &err);
+    if (st != WT_OK) {
+        delete e;
+        return set_err(st, err);
+    }
+    DeviceGuard guard(device);
+    const HostImage& h = e->host;
+    const size_t C = h.C, R = h.R;
+    Arena ar;
+    size_t o_mid = ar.take(C * 4), o_til = ar.take(C * 16), o_mag = ar.take(C * 16),
+           o_th = ar.take(C * R * 32), o_meta = ar.take(C * R * 4), o_used = ar.take(C * R * 4),
+           o_amap = ar.take(C * R * 8), o_afb = ar.take(C * R * 4),
+           o_al = ar.take(h.anchor_l.size() * 8), o_am = ar.take(h.anchor_micro.size() * 4);
+    cudaError_t ce = cudaMalloc(&e->mem, ar.used);
+    if (ce != cudaSuccess) {
+        delete e;
+        return cuda_err(ce, "wt_engine_create: cudaMalloc");
+    }
+    e->bytes = ar.used;
+    char* base = static_cast<char*>(e->mem);
+    struct Piece {
+        size_t off;
+        const void* src;
+        size_t n;
+    } pieces[] = {
+        {o_mid, h.macro_id.data(), C * 4},        {o_til, h.tiles.data(), C * 16},
+        {o_mag, h.magic.data(), C * 16},          {o_th, h.theta.data(), C * R * 32},
+        {o_meta, h.rowmeta.data(), C * R * 4},    {o_used, h.used_w.data(), C * R * 4},
+        {o_amap, h.amap.data(), C * R * 8},       {o_afb, h.afb.data(), C * R * 4},
+        {o_al, h.anchor_l.data(), h.anchor_l.size() * 8},
+        {o_am, h.anchor_micro.data(), h.anchor_micro.size() * 4},
+    };
+    for (const Piece& p : pieces) {
+        ce = cudaMemcpy(base + p.off, p.src, p.n, cudaMemcpyHostToDevice);
+        if (ce != cudaSuccess) {
+            cudaFree(e->mem);
+            delete e;
+            return cuda_err(ce, "wt_engine_create: upload");
+        }
+    }
+    DevImage& d = e->dev;
+    d.C = h.C;
+    d.R = h.R;
+    d.S = h.S;
+    d.RS = uint32_t(h.R) * uint32_t(h.S);
+    Magic ms = make_magic(uint32_t(h.S));
+    d.mS = ms.m;
+    d.sS = ms.s;
+    d.special = h.special ? 1 : 0;
+    d.macro_id = reinterpret_cast<const int32_t*>(base + o_mid);
+    d.tiles = reinterpret_cast<const int4*>(base + o_til);
+    d.magic = reinterpret_cast<const uint4*>(base + o_mag);
+    d.theta = reinterpret_cast<const double4*>(base + o_th);
+    d.rowmeta = reinterpret_cast<const uint32_t*>(base + o_meta);
+    d.used_w = reinterpret_cast<const int32_t*>(base + o_used);
+    d.amap = reinterpret_cast<const int2*>(base + o_amap);
+    d.afb = reinterpret_cast<const int32_t*>(base + o_afb);
+    d.anchor_l = reinterpret_cast<const int64_t*>(base + o_al);
+    d.anchor_micro = reinterpret_cast<const int32_t*>(base + o_am);
+    d.tm_min = h.tm_min;
+    d.tn_min = h.tn_min;
+    // list-mode chunk: keep the staged rows near 40 KB so several CTAs fit per SM
+    e->eval_chunk = int(std::max<size_t>(1, std::min<size_t>(C, 40960 / (R * 36 + 32))));
+    e->eval_grid = sm_count(device) * 4;
+    *out = e;
+    return WT_OK;
+}
+
+wt_status wt_engine_destroy(wt_engine* e) {
+    if (!e) return WT_OK;
+    DeviceGuard guard(e->device);
+    cudaFree(e->mem);
+    delete e;
+    return WT_OK;
+}
+
+wt_status wt_engine_info_get(const wt_engine* e, wt_engine_info* out) {
+    if (!e || !out) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    out->n_configs = e->host.C;
+    out->n_rows = e->host.R;
+    out->slots = e->host.S;
+    out->family = e->host.family;
+    out->has_fallback_rows = e->host.special ? 1 : 0;
+    out->device = e->device;
+    out->device_bytes = e->bytes;
+    return WT_OK;
+}
+
+int32_t wt_engine_config_index(const wt_engine* e, int32_t macro_id) {
+    if (!e) return -1;
+    auto it = std::lower_bound(e->host.macro_id.begin(), e->host.macro_id.end(), macro_id);
+    if (it == e->host.macro_id.end() || *it != macro_id) return -1;
+    return int32_t(it - e->host.macro_id.begin());
+}
+
+int32_t wt_engine_anchor_map(const wt_engine* e, int32_t config, int32_t wave, int32_t extrapolated,
+                             int64_t* anchors, int32_t* micros, int32_t cap, int32_t* fallback_wave) {
+    if (!e || config < 0 || config >= e->host.C) return -1;
+    const HostImage& h = e->host;
+    int32_t row;
+    if (extrapolated) row = h.R - 1;
+    else if (wave >= 1 && wave < h.R) row = wave - 1;
+    else return -1;
+    const size_t rr = size_t(config) * h.R + row;
+    if (h.rowmeta[rr] & ROW_NO_ANCHOR) return -1;
+    const int32_t off = h.amap[2 * rr], cnt = h.amap[2 * rr + 1];
+    for (int32_t i = 0; i < cnt && i < cap; ++i) {
+        if (anchors) anchors[i] = h.anchor_l[off + i];
+        if (micros) micros[i] = h.anchor_micro[off + i];
+    }
+    if (fallback_wave) fallback_wave[0] = h.afb[rr];
+    return cnt;
+}
+
+static DecOut to_out(const wt_decisions* o) {
+    DecOut d{};
+    d.macro = o->macro_id;
+    d.micro = o->micro_id;
+    d.lat = o->latency_us;
+    d.g = o->g;
+    d.l = o->l;
+    d.wave = o->wave;
+    d.flags = o->flags;
+    d.comps = o->comparisons;
+    d.tail = o->tail_frac;
+    d.topk = o->topk;
+    d.topk_macro = o->topk_macro;
+    d.topk_lat = o->topk_latency;
+    return d;
+}
+
+static wt_status check_out(const wt_decisions* o) {
+    if (!o || !o->macro_id || !o->micro_id || !o->latency_us)
+        return set_err(WT_INVALID_ARGUMENT, "decision outputs macro_id, micro_id, latency_us are required");
+    if (o->topk < 0 || o->topk > 8) return set_err(WT_UNSUPPORTED, "topk must be in [0, 8]");
+    if (o->topk > 0 && (!o->topk_macro || !o->topk_latency))
+        return set_err(WT_INVALID_ARGUMENT, "topk outputs missing");
+    return WT_OK;
+}
+
+wt_status wt_tune_batch(const wt_engine* e, const int32_t* M, const int32_t* N, const int32_t* K,
+                        int64_t n, const wt_decisions* out, void* stream) {
+    if (!e) return set_err(WT_INVALID_ARGUMENT, "null engine");
+    if (n < 0) return set_err(WT_INVALID_ARGUMENT, "negative batch size");
+    wt_status st = check_out(out);
+    if (st) return st;
+    if (n == 0) return WT_OK;
+    if (e->host.family == WT_FAMILY_GROUPED_GEMM)
+        return set_err(WT_INVALID_ARGUMENT, "dense_gemm workload needs gemm tiles");
+    DeviceGuard guard(e->device);
+    EvalArgs a{};
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.n = n;
+    a.chunk = e->eval_chunk;
+    a.out = to_out(out);
+    const int64_t tiles = (n + kEvalThreads - 1) / kEvalThreads;
+    const int grid = int(std::min<int64_t>(tiles, e->eval_grid));
+    cudaError_t ce = launch_eval(e->dev, a, grid, static_cast<cudaStream_t>(stream));
+    g_launches++;
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_tune_batch");
+    return WT_OK;
+}
+
+wt_status wt_tune_grouped_batch(const wt_engine* e, const int64_t* row_off, const int32_t* rows,
+                                const int32_t* N, const int32_t* K, int64_t n,
+                                const wt_decisions* out, void* stream) {
+    if (!e) return set_err(WT_INVALID_ARGUMENT, "null engine");
+    wt_status st = check_out(out);
+    if (st) return st;
+    if (out->topk) return set_err(WT_UNSUPPORTED, "topk is not available for grouped queries");
+    if (n <= 0) return n == 0 ? WT_OK : set_err(WT_INVALID_ARGUMENT, "negative batch size");
+    if (e->host.family == WT_FAMILY_FLASH_ATTENTION)
+        return set_err(WT_INVALID_ARGUMENT, "grouped_gemm workload needs gemm tiles");
+    DeviceGuard guard(e->device);
+    GroupedArgs a{};
+    a.row_off = row_off;
+    a.rows = rows;
+    a.N = N;
+    a.K = K;
+    a.n = n;
+    a.out = to_out(out);
+    const int grid = int(std::min<int64_t>((n * 32 + 255) / 256, int64_t(sm_count(e->device)) * 8));
+    cudaError_t ce = launch_grouped(e->dev, a, grid, static_cast<cudaStream_t>(stream));
+    g_launches++;
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_tune_grouped_batch");
+    return WT_OK;
+}
+
+wt_status wt_predict_batch(const wt_engine* e, const int32_t* config, const int64_t* g,
+                           const int64_t* l, int64_t n, double* latency_us, int32_t* wave,
+                           int32_t* extrapolated, int32_t* used_w, int32_t* status, void* stream) {
+    if (!e || !latency_us) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    if (n <= 0) return WT_OK;
+    DeviceGuard guard(e->device);
+    PredictArgs a{config, g, l, n, latency_us, wave, extrapolated, used_w, status};
+    cudaError_t ce = launch_predict(e->dev, a, static_cast<cudaStream_t>(stream));
+    g_launches++;
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_predict_batch");
+    return WT_OK;
+}
+
+wt_status wt_explain(const wt_engine* e, int64_t M, int64_t N, int64_t K, int64_t* g, int64_t* l,
+                     int32_t* wave, int32_t* used_w, double* latency_us, int32_t* status,
+                     void* stream) {
+    if (!e || !g || !l || !wave || !used_w || !latency_us || !status)
+        return set_err(WT_INVALID_ARGUMENT, "null argument");
+    if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
+        return set_err(WT_UNSUPPORTED, "dims above 2^31-1 are outside the device path's range");
+    DeviceGuard guard(e->device);
+    ExplainArgs a{M, N, K, g, l, wave, used_w, latency_us, status};
+    cudaError_t ce = launch_explain(e->dev, a, static_cast<cudaStream_t>(stream));
+    g_launches++;
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_explain");
+    return WT_OK;
+}
+
+wt_status wt_nearest_anchor_batch(const int64_t* anchors, int32_t n_anchors, const int64_t* l,
+                                  int64_t n, int64_t* out, int32_t* comparisons, void* stream) {
+    if (n_anchors <= 0) return set_err(WT_INVALID_ARGUMENT, "nearest_anchor: empty anchor list");
+    if (n <= 0) return WT_OK;
+    NearestArgs a{anchors, n_anchors, l, n, out, comparisons};
+    cudaError_t ce = launch_nearest(a, static_cast<cudaStream_t>(stream));
+    g_launches++;
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_nearest_anchor_batch");
+    return WT_OK;
+}
+
+// ------------------------------------------------------------------ grid
+wt_status wt_grid_create(const wt_engine* e, const wt_grid_desc* desc, wt_grid** out) {
+    if (!e || !desc || !out) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    if (desc->n_pairs <= 0) return set_err(WT_INVALID_ARGUMENT, "grid needs at least one (N, K) pair");
+    if (desc->m_lo < 1 || desc->m_hi < desc->m_lo)
+        return set_err(WT_INVALID_ARGUMENT, "grid M range must satisfy 1 <= m_lo <= m_hi");
+    if (desc->topk < 0 || desc->topk > 8) return set_err(WT_UNSUPPORTED, "topk must be in [0, 8]");
+    if (e->host.family == WT_FAMILY_GROUPED_GEMM)
+        return set_err(WT_UNSUPPORTED, "decision grids cover dense / attention shapes");
+    for (int32_t p = 0; p < desc->n_pairs; ++p)
+        if (desc->N[p] < 1 || desc->K[p] < 1)
+            return set_err(WT_INVALID_ARGUMENT, "dense_gemm dims must be >= 1");
+    DeviceGuard guard(e->device);
+    auto* g = new wt_grid;
+    g->eng = e;
+    g->n_pairs = desc->n_pairs;
+    g->m_lo = desc->m_lo;
+    g->m_hi = desc->m_hi;
+    g->mcount = int64_t(desc->m_hi) - desc->m_lo + 1;
+    g->n_entries = g->mcount * desc->n_pairs;
+    g->topk = desc->topk;
+    // narrow (32-bit g) sweep whenever every g fits
+    uint64_t nt_max = 0;
+    for (int32_t p = 0; p < desc->n_pairs; ++p)
+        nt_max = std::max<uint64_t>(nt_max, (uint64_t(desc->N[p]) + e->host.tn_min - 1) / e->host.tn_min);
+    const uint64_t mt_max = (uint64_t(desc->m_hi) + e->host.tm_min - 1) / e->host.tm_min;
+    g->wide = mt_max * nt_max >= (uint64_t(1) << 32);
+    // sorted unique (N, K) keys for the gather; first occurrence wins
+    std::vector<std::pair<uint64_t, int32_t>> keys;
+    for (int32_t p = 0; p < desc->n_pairs; ++p)
+        keys.push_back({(uint64_t(uint32_t(desc->N[p])) << 32) | uint32_t(desc->K[p]), p});
+    std::stable_sort(keys.begin(), keys.end(),
+                     [](const auto& a, const auto& b) { return a.first < b.first; });
+    keys.erase(std::unique(keys.begin(), keys.end(),
+                           [](const auto& a, const auto& b) { return a.first == b.first; }),
+               keys.end());
+    g->n_keys = int32_t(keys.size());
+    Arena ar;
+    const size_t o_n = ar.take(size_t(g->n_pairs) * 4), o_k = ar.take(size_t(g->n_pairs) * 4),
+                 o_keys = ar.take(keys.size() * 8), o_pid = ar.take(keys.size() * 4),
+                 o_ent = ar.take(size_t(g->n_entries) * sizeof(wt_grid_entry)),
+                 o_tkm = ar.take(size_t(g->n_entries) * g->topk * 4),
+                 o_tkl = ar.take(size_t(g->n_entries) * g->topk * 8);
+    cudaError_t ce = cudaMalloc(&g->mem, ar.used);
+    if (ce != cudaSuccess) {
+        delete g;
+        return cuda_err(ce, "wt_grid_create: cudaMalloc");
+    }
+    char* base = static_cast<char*>(g->mem);
+    g->dN = reinterpret_cast<int32_t*>(base + o_n);
+    g->dK = reinterpret_cast<int32_t*>(base + o_k);
+    g->dkeys = reinterpret_cast<uint64_t*>(base + o_keys);
+    g->dpid = reinterpret_cast<int32_t*>(base + o_pid);
+    g->entries = reinterpret_cast<wt_grid_entry*>(base + o_ent);
+    g->tk_macro = g->topk ? reinterpret_cast<int32_t*>(base + o_tkm) : nullptr;
+    g->tk_lat = g->topk ? reinterpret_cast<double*>(base + o_tkl) : nullptr;
+    std::vector<uint64_t> kk;
+    std::vector<int32_t> pid;
+    for (auto& k : keys) {
+        kk.push_back(k.first);
+        pid.push_back(k.second);
+    }
+    cudaMemcpy(g->dN, desc->N, size_t(g->n_pairs) * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(g->dK, desc->K, size_t(g->n_pairs) * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(g->dkeys, kk.data(), kk.size() * 8, cudaMemcpyHostToDevice);
+    ce = cudaMemcpy(g->dpid, pid.data(), pid.size() * 4, cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) {
+        cudaFree(g->mem);
+        delete g;
+        return cuda_err(ce, "wt_grid_create: upload");
+    }
+    const size_t per_cfg = size_t(e->host.R) * (32 + (e->host.special ? 4 : 0)) + 24;
+    g->sweep_chunk = int(std::max<size_t>(1, std::min<size_t>(e->host.C, 49152 / per_cfg)));
+    *out = g;
+    return WT_OK;
+}
+
+wt_status wt_grid_destroy(wt_grid* g) {
+    if (!g) return WT_OK;
+    DeviceGuard guard(g->eng->device);
+    cudaFree(g->mem);
+    delete g;
+    return WT_OK;
+}
+
+wt_status wt_grid_storage(const wt_grid* g, wt_grid_entry** entries, int64_t* n_entries,
+                          int32_t** topk_macro, double** topk_latency) {
+    if (!g) return set_err(WT_INVALID_ARGUMENT, "null grid");
+    if (entries) *entries = g->entries;
+    if (n_entries) *n_entries = g->n_entries;
+    if (topk_macro) *topk_macro = g->tk_macro;
+    if (topk_latency) *topk_latency = g->tk_lat;
+    return WT_OK;
+}
+
+wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, void* stream) {
+    if (!e || !g) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    if (g->eng != e) return set_err(WT_INVALID_ARGUMENT, "grid was created for another engine");
+    if (begin < 0 || end > g->n_entries || begin > end)
+        return set_err(WT_OUT_OF_RANGE, "sweep range outside the grid");
+    if (begin == end) return WT_OK;
+    DeviceGuard guard(e->device);
+    SweepArgs a{};
+    a.N = g->dN;
+    a.K = g->dK;
+    a.m_lo = g->m_lo;
+    a.mcount = g->mcount;
+    a.begin = begin;
+    a.end = end;
+    a.chunk = g->sweep_chunk;
+    a.entries = g->entries;
+    a.topk = g->topk;
+    a.topk_macro = g->tk_macro;
+    a.topk_lat = g->tk_lat;
+    cudaError_t ce = launch_sweep(e->dev, a, g->wide, static_cast<cudaStream_t>(stream));
+    g_launches++;
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep");
+    return WT_OK;
+}
+
+wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M, const int32_t* N,
+                          const int32_t* K, int64_t n, const wt_decisions* out, void* stream) {
+    if (!e || !g) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    if (g->eng != e) return set_err(WT_INVALID_ARGUMENT, "grid was created for another engine");
+    wt_status st = check_out(out);
+    if (st) return st;
+    if (out->topk && out->topk != g->topk)
+        return set_err(WT_INVALID_ARGUMENT, "topk must match the grid's topk");
+    if (n <= 0) return n == 0 ? WT_OK : set_err(WT_INVALID_ARGUMENT, "negative batch size");
+    DeviceGuard guard(e->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    void* scratch = nullptr;
+    cudaError_t ce = cudaMallocAsync(&scratch, size_t(n + 2) * sizeof(int64_t), s);
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_gather_batch: scratch");
+    int64_t* count = static_cast<int64_t*>(scratch);
+    int64_t* idx = count + 2;
+    cudaMemsetAsync(count, 0, sizeof(int64_t), s);
+    GatherArgs a{};
+    a.pair_keys = g->dkeys;
+    a.pair_ids = g->dpid;
+    a.n_pairs = g->n_keys;
+    a.m_lo = g->m_lo;
+    a.m_hi = g->m_hi;
+    a.mcount = g->mcount;
+    a.entries = g->entries;
+    a.topk_macro = g->tk_macro;
+    a.topk_lat = g->tk_lat;
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.n = n;
+    a.out = to_out(out);
+    a.off_count = count;
+    a.off_idx = idx;
+    const int grid = int(std::min<int64_t>((n + kGatherThreads - 1) / kGatherThreads,
+                                           int64_t(sm_count(e->device)) * 8));
+    ce = launch_gather(e->dev, a, grid, s);
+    g_launches++;
+    if (ce == cudaSuccess) {
+        EvalArgs ea{};
+        ea.M = M;
+        ea.N = N;
+        ea.K = K;
+        ea.n = n;
+        ea.idx = idx;
+        ea.count = count;
+        ea.chunk = e->eval_chunk;
+        ea.out = to_out(out);
+        if (g->topk == 0) ea.out.topk = 0;
+        ce = launch_eval(e->dev, ea, e->eval_grid, s);
+        g_launches++;
+    }
+    cudaFreeAsync(scratch, s);
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_gather_batch");
+    return WT_OK;
+}
+
+// K2 entry points live in wt_fit.cu.
+
+}  // extern "C"

@@ -1,0 +1,743 @@
+// wt_decide.cu -- sm_100a kernels of the WaveTune decision path.
+//
+//   k_sweep   (K1, grid mode)  tune() over every (pair, M) of a shape grid:
+//             lanes = shapes, configs + coefficient rows staged per pair in
+//             shared memory with gamma*l folded in, integer magic division
+//             for tiles and waves, register argmin per lane.
+//   k_eval    (K1, list mode)  tune() for arbitrary dense/attention queries
+//             (optionally a device-compacted index list from k_gather).
+//   k_grouped tune() for grouped-GEMM queries: one warp per query, lanes over
+//             configs, warp-shuffle argmin.
+//   k_gather  (K3) online queries against a filled grid; off-grid queries are
+//             compacted (warp-aggregated atomics) for k_eval.
+//   k_predict / k_explain / k_nearest  per-table helpers for the drop-in API.
+//
+// Arithmetic is binary64 with explicit _rn intrinsics (no contraction) and
+// exact 32-bit magic division, so results are bit-identical to the
+// reference's C++ (SURVEY.md Appendix A).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "wt_decide.h"
+#include "wt_device.cuh"
+
+namespace wtb {
+
+// ---------------------------------------------------------------- Stage II
+struct Stage2 {
+    int32_t micro;
+    int32_t comps;
+    uint32_t flags;  // WT_FLAG_* bits and status << 24
+};
+
+__device__ __forceinline__ Stage2 stage2(const DevImage& im, int c, uint32_t row, int64_t l) {
+    const size_t rr = size_t(c) * im.R + row;
+    const uint32_t meta = __ldg(im.rowmeta + rr);
+    Stage2 s;
+    s.flags = (meta & ROW_EXTRAP) ? WT_FLAG_EXTRAPOLATED : 0u;
+    if (meta & ROW_ANCHOR_FB) s.flags |= WT_FLAG_ANCHOR_FALLBACK;
+    if (meta & ROW_NO_ANCHOR) {
+        s.micro = -1;
+        s.comps = 0;
+        s.flags |= uint32_t(WT_RUNTIME_ERROR) << 24;
+        return s;
+    }
+    const int2 am = __ldg(im.amap + rr);
+    int comps;
+    int k = nearest_anchor_idx(im.anchor_l + am.x, am.y, l, &comps);
+    s.micro = __ldg(im.anchor_micro + am.x + k);
+    s.comps = comps;
+    return s;
+}
+
+// Winner epilogue shared by every mode: w (true wave count), regime,
+// Stage II, tail fraction.
+struct Final {
+    int32_t macro, micro, wave, comps;
+    uint32_t flags;
+    float tail;
+};
+
+__device__ __forceinline__ Final finish(const DevImage& im, int c, double best, uint64_t g,
+                                        int64_t l, uint32_t acc_meta) {
+    Final f;
+    f.tail = 0.f;
+    if (c < 0) {  // every candidate NaN or +inf: the reference dereferences null
+        f.macro = f.micro = f.wave = -1;
+        f.comps = 0;
+        f.flags = uint32_t(WT_RUNTIME_ERROR) << 24;
+        return f;
+    }
+    if (acc_meta & ROW_NO_COEFF) {  // predict_latency threw for some table
+        f.macro = f.micro = f.wave = -1;
+        f.comps = 0;
+        f.flags = uint32_t(WT_RUNTIME_ERROR) << 24;
+        return f;
+    }
+    const uint64_t S = uint64_t(im.S);
+    const uint64_t w64 = (g + S - 1) / S;
+    const uint32_t row = uint32_t(w64 < uint64_t(im.R) ? w64 : uint64_t(im.R)) - 1u;
+    Stage2 s = stage2(im, c, row, l);
+    f.macro = __ldg(im.macro_id + c);
+    f.micro = s.micro;
+    f.wave = int32_t(uint32_t(w64));
+    f.comps = s.comps;
+    f.flags = s.flags | ((acc_meta & ROW_MISSING) ? WT_FLAG_MISSING_WAVE : 0u);
+    f.tail = float(double(g - (w64 - 1) * S) / double(S));
+    if (f.flags >> 24) f.macro = -1;
+    (void)best;
+    return f;
+}
+
+__device__ __forceinline__ void write_decision(const DecOut& o, int64_t q, const Final& f,
+                                               double lat, uint64_t g, int64_t l) {
+    const bool ok = (f.flags >> 24) == 0;
+    o.macro[q] = ok ? f.macro : -1;
+    o.micro[q] = ok ? f.micro : -1;
+    o.lat[q] = ok ? lat : __longlong_as_double(0x7ff8000000000000LL);
+    if (o.g) o.g[q] = ok ? int64_t(g) : 0;
+    if (o.l) o.l[q] = ok ? l : 0;
+    if (o.wave) o.wave[q] = ok ? f.wave : 0;
+    if (o.flags) o.flags[q] = f.flags;
+    if (o.comps) o.comps[q] = ok ? f.comps : 0;
+    if (o.tail) o.tail[q] = ok ? double(f.tail) : 0.0;
+}
+
+// ------------------------------------------------------------- K1: sweep
+// Shared-memory chunk of configs for one (N, K) pair.
+struct SweepCfg {
+    uint32_t mM, sM, nt, pad;
+};
+
+template <int RPT, bool SPECIAL, bool WIDE, int KM>
+__global__ void __launch_bounds__(kSweepThreads) k_sweep(DevImage im, SweepArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int CC = a.chunk;
+    SweepCfg* scfg = reinterpret_cast<SweepCfg*>(smem);
+    double* sld = reinterpret_cast<double*>(scfg + CC);
+    double4* sth = reinterpret_cast<double4*>(sld + CC);
+    uint32_t* smeta = reinterpret_cast<uint32_t*>(sth + size_t(CC) * im.R);
+
+    const int tid = threadIdx.x;
+    const int64_t tile = int64_t(kSweepThreads) * RPT;
+    const int64_t t0 = a.begin + int64_t(blockIdx.x) * tile;
+    const int64_t t1 = min(t0 + tile, a.end);
+    const uint32_t RS = im.RS, mS = im.mS, sS = im.sS;
+    const int R = im.R;
+
+    // A tile may straddle pair boundaries: process one pair segment at a time.
+    for (int64_t seg = t0; seg < t1;) {
+        const int32_t p = int32_t(seg / a.mcount);
+        const int64_t seg_end = min(t1, int64_t(p + 1) * a.mcount);
+        const uint32_t Np = uint32_t(a.N[p]), Kp = uint32_t(a.K[p]);
+
+        double best[RPT];
+        int bc[RPT];
+        uint32_t acc[RPT];
+        uint32_t y2[RPT];
+        double tkL[KM > 0 ? KM : 1][RPT];
+        int tkI[KM > 0 ? KM : 1][RPT];
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            const int64_t idx = seg + int64_t(j) * kSweepThreads + tid;
+            const int64_t mi = (idx < seg_end) ? idx - int64_t(p) * a.mcount : 0;
+            const uint32_t M = uint32_t(a.m_lo + mi);
+            y2[j] = 2u * (M - 1u);
+            best[j] = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+            bc[j] = -1;
+            acc[j] = 0;
+            if constexpr (KM > 0) {
+#pragma unroll
+                for (int q = 0; q < KM; ++q) {
+                    tkL[q][j] = __longlong_as_double(0x7ff0000000000000LL);
+                    tkI[q][j] = -1;
+                }
+            }
+        }
+
+        for (int c0 = 0; c0 < im.C; c0 += CC) {
+            const int cc = min(CC, im.C - c0);
+            __syncthreads();
+            // stage per-config scalars: ceil(N/t_n), ceil(K/t_k), magic for t_m
+            for (int i = tid; i < cc; i += kSweepThreads) {
+                const int c = c0 + i;
+                const int4 tl = __ldg(im.tiles + c);
+                const uint4 mg = __ldg(im.magic + c);
+                SweepCfg s;
+                s.mM = mg.x;
+                s.sM = mg.w & 0xffu;
+                s.nt = uint32_t((uint64_t(Np) + uint32_t(tl.y) - 1) / uint32_t(tl.y));
+                s.pad = 0;
+                scfg[i] = s;
+                const uint32_t lk = uint32_t((uint64_t(Kp) + uint32_t(tl.z) - 1) / uint32_t(tl.z));
+                sld[i] = u32_to_f64(lk);
+            }
+            __syncthreads();
+            // stage coefficient rows with gamma*l folded in (bit-identical
+            // product: the reference forms gamma*l as one rounded DMUL)
+            const int nrow = cc * R;
+            const double4* gth = im.theta + size_t(c0) * R;
+            for (int i = tid; i < nrow; i += kSweepThreads) {
+                double4 th = ldg_row(gth + i);
+                th.z = __dmul_rn(th.z, sld[i / R]);
+                sth[i] = th;
+                if constexpr (SPECIAL) smeta[i] = __ldg(im.rowmeta + size_t(c0) * R + i);
+            }
+            __syncthreads();
+
+#pragma unroll 2
+            for (int i = 0; i < cc; ++i) {
+                const SweepCfg s = scfg[i];
+                const double ld = sld[i];
+                const double4* rows = sth + size_t(i) * R;
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) {
+                    const uint32_t q = mdiv2(y2[j], s.mM, s.sM);
+                    uint32_t gc;
+                    double gd;
+                    if constexpr (WIDE) {
+                        const uint64_t g = uint64_t(q) * s.nt + s.nt;
+                        gc = g > RS ? RS : uint32_t(g);
+                        gd = u64_to_f64(g);
+                    } else {
+                        const uint32_t g = q * s.nt + s.nt;
+                        gc = min(g, RS);
+                        gd = u32_to_f64(g);
+                    }
+                    const uint32_t row = row_of(gc, mS, sS);
+                    const double4 th = rows[row];
+                    const double t = bilinear(th.x, th.y, th.z, th.w, gd, ld);
+                    if (t < best[j]) {
+                        best[j] = t;
+                        bc[j] = c0 + i;
+                    }
+                    if constexpr (SPECIAL) acc[j] |= smeta[size_t(i) * R + row];
+                    if constexpr (KM > 0) {
+                        double L[KM];
+                        int I[KM];
+#pragma unroll
+                        for (int z = 0; z < KM; ++z) {
+                            L[z] = tkL[z][j];
+                            I[z] = tkI[z][j];
+                        }
+                        topk_insert<KM>(L, I, t, c0 + i);
+#pragma unroll
+                        for (int z = 0; z < KM; ++z) {
+                            tkL[z][j] = L[z];
+                            tkI[z][j] = I[z];
+                        }
+                    }
+                }
+            }
+        }
+
+        // epilogue: Stage II for each winner, one 32-byte entry per shape
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            const int64_t idx = seg + int64_t(j) * kSweepThreads + tid;
+            if (idx >= seg_end) continue;
+            const int c = bc[j];
+            uint64_t g = 0;
+            int64_t l = 0;
+            if (c >= 0) {
+                const int4 tl = __ldg(im.tiles + c);
+                const uint32_t M = y2[j] / 2u + 1u;
+                g = uint64_t((M + uint32_t(tl.x) - 1) / uint32_t(tl.x)) *
+                    uint64_t((uint64_t(Np) + uint32_t(tl.y) - 1) / uint32_t(tl.y));
+                l = int64_t((uint64_t(Kp) + uint32_t(tl.z) - 1) / uint32_t(tl.z));
+            }
+            const Final f = finish(im, c, best[j], g, l, acc[j]);
+            const bool ok = (f.flags >> 24) == 0;
+            int4 lo, hi;
+            const double lat = ok ? best[j] : __longlong_as_double(0x7ff8000000000000LL);
+            lo.x = __double2loint(lat);
+            lo.y = __double2hiint(lat);
+            lo.z = f.macro;
+            lo.w = f.micro;
+            hi.x = f.wave;
+            hi.y = int(f.flags);
+            hi.z = f.comps;
+            hi.w = __float_as_int(f.tail);
+            int4* e = reinterpret_cast<int4*>(a.entries + idx);
+            e[0] = lo;
+            e[1] = hi;
+            if constexpr (KM > 0) {
+                for (int z = 0; z < a.topk; ++z) {
+                    const int ci = ok ? tkI[z][j] : -1;
+                    a.topk_macro[idx * a.topk + z] = ci >= 0 ? __ldg(im.macro_id + ci) : -1;
+                    a.topk_lat[idx * a.topk + z] =
+                        ci >= 0 ? tkL[z][j] : __longlong_as_double(0x7ff8000000000000LL);
+                }
+            }
+        }
+        seg = seg_end;
+    }
+}
+
+// --------------------------------------------------------- K1: list mode
+template <bool SPECIAL, int KM>
+__global__ void __launch_bounds__(kEvalThreads) k_eval(DevImage im, EvalArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int CC = a.chunk;
+    int4* stile = reinterpret_cast<int4*>(smem);
+    uint4* smag = reinterpret_cast<uint4*>(stile + CC);
+    double4* sth = reinterpret_cast<double4*>(smag + CC);
+    uint32_t* smeta = reinterpret_cast<uint32_t*>(sth + size_t(CC) * im.R);
+
+    const int64_t n = a.count ? *a.count : a.n;
+    const int64_t ntiles = (n + kEvalThreads - 1) / kEvalThreads;
+    const uint32_t RS = im.RS, mS = im.mS, sS = im.sS;
+    const int R = im.R;
+    const int tid = threadIdx.x;
+
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t slot = tile * kEvalThreads + tid;
+        const bool live = slot < n;
+        const int64_t q = live ? (a.idx ? a.idx[slot] : slot) : 0;
+        uint32_t M = 1, N = 1, K = 1;
+        uint32_t status = 0;
+        if (live) {
+            const int32_t m = a.M[q], nn = a.N[q], k = a.K[q];
+            if (m < 1 || nn < 1 || k < 1) status = WT_INVALID_ARGUMENT;  // kernel_map.cpp:238-239
+            else {
+                M = uint32_t(m);
+                N = uint32_t(nn);
+                K = uint32_t(k);
+                // guard: every wave count must fit the reference's int
+                const uint64_t gmax = uint64_t((M + uint32_t(im.tm_min) - 1) / uint32_t(im.tm_min)) *
+                                      uint64_t((N + uint32_t(im.tn_min) - 1) / uint32_t(im.tn_min));
+                if ((gmax + uint64_t(im.S) - 1) / uint64_t(im.S) >= (uint64_t(1) << 31))
+                    status = WT_UNSUPPORTED;
+            }
+        }
+        const uint32_t y2M = 2u * (M - 1u), y2N = 2u * (N - 1u), y2K = 2u * (K - 1u);
+        double best = __longlong_as_double(0x7ff0000000000000LL);
+        int bc = -1;
+        uint32_t acc = 0;
+        double tkL[KM > 0 ? KM : 1];
+        int tkI[KM > 0 ? KM : 1];
+        if constexpr (KM > 0) {
+#pragma unroll
+            for (int z = 0; z < KM; ++z) {
+                tkL[z] = __longlong_as_double(0x7ff0000000000000LL);
+                tkI[z] = -1;
+            }
+        }
+        for (int c0 = 0; c0 < im.C; c0 += CC) {
+            const int cc = min(CC, im.C - c0);
+            __syncthreads();
+            for (int i = tid; i < cc; i += kEvalThreads) {
+                stile[i] = __ldg(im.tiles + c0 + i);
+                smag[i] = __ldg(im.magic + c0 + i);
+            }
+            const int nrow = cc * R;
+            for (int i = tid; i < nrow; i += kEvalThreads) {
+                sth[i] = ldg_row(im.theta + size_t(c0) * R + i);
+                if constexpr (SPECIAL) smeta[i] = __ldg(im.rowmeta + size_t(c0) * R + i);
+            }
+            __syncthreads();
+            for (int i = 0; i < cc; ++i) {
+                const uint4 mg = smag[i];
+                const uint32_t mt = mdiv2(y2M, mg.x, mg.w & 0xffu) + 1u;
+                const uint32_t nt = mdiv2(y2N, mg.y, (mg.w >> 8) & 0xffu) + 1u;
+                const uint32_t lk = mdiv2(y2K, mg.z, (mg.w >> 16) & 0xffu) + 1u;
+                const uint64_t g = uint64_t(mt) * nt;
+                const uint32_t gc = g > RS ? RS : uint32_t(g);
+                const uint32_t row = row_of(gc, mS, sS);
+                const double4 th = sth[size_t(i) * R + row];
+                const double gd = u64_to_f64(g), ld = u32_to_f64(lk);
+                const double t = bilinear(th.x, th.y, __dmul_rn(th.z, ld), th.w, gd, ld);
+                if (t < best) {
+                    best = t;
+                    bc = c0 + i;
+                }
+                if constexpr (SPECIAL) acc |= smeta[size_t(i) * R + row];
+                if constexpr (KM > 0) topk_insert<KM>(tkL, tkI, t, c0 + i);
+            }
+        }
+        if (live) {
+            if (status) {
+                Final f;
+                f.flags = status << 24;
+                f.macro = f.micro = f.wave = -1;
+                f.comps = 0;
+                f.tail = 0.f;
+                write_decision(a.out, q, f, 0.0, 0, 0);
+                if constexpr (KM > 0)
+                    for (int z = 0; z < a.out.topk; ++z) {
+                        a.out.topk_macro[q * a.out.topk + z] = -1;
+                        a.out.topk_lat[q * a.out.topk + z] = __longlong_as_double(0x7ff8000000000000LL);
+                    }
+            } else {
+                uint64_t g = 0;
+                int64_t l = 0;
+                if (bc >= 0) {
+                    const int4 tl = __ldg(im.tiles + bc);
+                    g = uint64_t((M + uint32_t(tl.x) - 1) / uint32_t(tl.x)) *
+                        uint64_t((N + uint32_t(tl.y) - 1) / uint32_t(tl.y));
+                    l = int64_t((K + uint32_t(tl.z) - 1) / uint32_t(tl.z));
+                }
+                const Final f = finish(im, bc, best, g, l, acc);
+                write_decision(a.out, q, f, best, g, l);
+                if constexpr (KM > 0) {
+                    const bool ok = (f.flags >> 24) == 0;
+                    for (int z = 0; z < a.out.topk; ++z) {
+                        const int ci = ok ? tkI[z] : -1;
+                        a.out.topk_macro[q * a.out.topk + z] = ci >= 0 ? __ldg(im.macro_id + ci) : -1;
+                        a.out.topk_lat[q * a.out.topk + z] =
+                            ci >= 0 ? tkL[z] : __longlong_as_double(0x7ff8000000000000LL);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------ grouped GEMM (warp/query)
+__global__ void __launch_bounds__(256) k_grouped(DevImage im, GroupedArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t q = warp; q < a.n; q += nwarps) {
+        const int64_t r0 = a.row_off[q], r1 = a.row_off[q + 1];
+        const int32_t N = a.N[q], K = a.K[q];
+        uint32_t status = 0;
+        if (N < 1 || K < 1) status = WT_INVALID_ARGUMENT;  // kernel_map.cpp:247-248
+        for (int64_t r = r0 + lane; r < r1 && !status; r += 32)
+            if (a.rows[r] < 0) status = WT_INVALID_ARGUMENT;  // :251
+        status = __reduce_max_sync(0xffffffffu, status);
+        double best = __longlong_as_double(0x7ff0000000000000LL);
+        int bc = -1;
+        uint32_t acc = 0;
+        uint64_t bg = 0;
+        if (!status) {
+            for (int c = lane; c < im.C; c += 32) {
+                const int4 tl = __ldg(im.tiles + c);
+                const uint4 mg = __ldg(im.magic + c);
+                uint64_t sum = 0;  // sum_i ceil(rows_i / t_m) over non-empty groups
+                for (int64_t r = r0; r < r1; ++r) {
+                    const int32_t rows = a.rows[r];
+                    if (rows > 0) sum += cdiv_m(uint32_t(rows), mg.x, mg.w & 0xffu);
+                }
+                const uint32_t nt = cdiv_m(uint32_t(N), mg.y, (mg.w >> 8) & 0xffu);
+                const uint32_t lk = cdiv_m(uint32_t(K), mg.z, (mg.w >> 16) & 0xffu);
+                const uint64_t g = sum * nt;
+                if (g == 0) {  // kernel_map.cpp:254-255: empty grid
+                    acc |= 0x80000000u;
+                    continue;
+                }
+                const uint32_t gc = g > im.RS ? im.RS : uint32_t(g);
+                const uint32_t row = row_of(gc, im.mS, im.sS);
+                const double4 th = ldg_row(im.theta + size_t(c) * im.R + row);
+                const double gd = u64_to_f64(g), ld = u32_to_f64(lk);
+                const double t = bilinear(th.x, th.y, __dmul_rn(th.z, ld), th.w, gd, ld);
+                acc |= __ldg(im.rowmeta + size_t(c) * im.R + row);
+                if (t < best) {  // lane-local scan is ascending in c
+                    best = t;
+                    bc = c;
+                    bg = g;
+                }
+                (void)tl;
+            }
+            // warp-shuffle argmin: smaller latency, ties -> smaller config
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+                const int oc = __shfl_xor_sync(0xffffffffu, bc, off);
+                const uint64_t og = __shfl_xor_sync(0xffffffffu, bg, off);
+                const bool take = (ob < best) || (ob == best && oc >= 0 && (bc < 0 || oc < bc));
+                if (take) {
+                    best = ob;
+                    bc = oc;
+                    bg = og;
+                }
+            }
+            acc = __reduce_or_sync(0xffffffffu, acc);
+            if (acc & 0x80000000u) status = WT_INVALID_ARGUMENT;
+        }
+        if (lane == 0) {
+            if (status) {
+                Final f;
+                f.flags = status << 24;
+                f.macro = f.micro = f.wave = -1;
+                f.comps = 0;
+                f.tail = 0.f;
+                write_decision(a.out, q, f, 0.0, 0, 0);
+            } else {
+                int64_t l = 0;
+                if (bc >= 0) {
+                    const int4 tl = __ldg(im.tiles + bc);
+                    l = int64_t((uint32_t(K) + uint32_t(tl.z) - 1) / uint32_t(tl.z));
+                }
+                const Final f = finish(im, bc, best, bg, l, acc);
+                write_decision(a.out, q, f, best, bg, l);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------ K3: gather
+// config index of a macro id (im.macro_id is ascending).
+__device__ __forceinline__ int config_of(const DevImage& im, int32_t macro) {
+    int lo = 0, hi = im.C;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(im.macro_id + mid) < macro)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kGatherThreads) k_gather(DevImage im, GatherArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
+    int32_t* pid = reinterpret_cast<int32_t*>(keys + a.n_pairs);
+    for (int i = threadIdx.x; i < a.n_pairs; i += blockDim.x) {
+        keys[i] = a.pair_keys[i];
+        pid[i] = a.pair_ids[i];
+    }
+    __syncthreads();
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    const int64_t n = a.n;
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
+        const int64_t q = base + threadIdx.x;
+        const bool live = q < n;
+        int32_t M = 0, N = 0, K = 0;
+        if (live) {
+            M = __ldcs(a.M + q);
+            N = __ldcs(a.N + q);
+            K = __ldcs(a.K + q);
+        }
+        // pair lookup: binary search over sorted (N, K) keys
+        const uint64_t key = (uint64_t(uint32_t(N)) << 32) | uint32_t(K);
+        int lo = 0, hi = a.n_pairs;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (keys[mid] < key)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        const bool on = live && lo < a.n_pairs && keys[lo] == key && M >= a.m_lo && M <= a.m_hi;
+        if (on) {
+            const int64_t e = int64_t(pid[lo]) * a.mcount + (M - a.m_lo);
+            const int4* src = reinterpret_cast<const int4*>(a.entries + e);
+            const int4 lo4 = __ldg(src), hi4 = __ldg(src + 1);
+            const DecOut& o = a.out;
+            __stcs(o.macro + q, lo4.z);
+            __stcs(o.micro + q, lo4.w);
+            __stcs(o.lat + q, __hiloint2double(lo4.y, lo4.x));
+            if (o.wave) o.wave[q] = hi4.x;
+            if (o.flags) o.flags[q] = uint32_t(hi4.y);
+            if (o.comps) o.comps[q] = hi4.z;
+            if (o.tail) o.tail[q] = double(__int_as_float(hi4.w));
+            if (o.g || o.l) {
+                const int c = lo4.z >= 0 ? config_of(im, lo4.z) : -1;
+                uint64_t g = 0;
+                int64_t l = 0;
+                if (c >= 0) {
+                    const int4 tl = __ldg(im.tiles + c);
+                    g = uint64_t((uint32_t(M) + uint32_t(tl.x) - 1) / uint32_t(tl.x)) *
+                        uint64_t((uint32_t(N) + uint32_t(tl.y) - 1) / uint32_t(tl.y));
+                    l = int64_t((uint32_t(K) + uint32_t(tl.z) - 1) / uint32_t(tl.z));
+                }
+                if (o.g) o.g[q] = int64_t(g);
+                if (o.l) o.l[q] = l;
+            }
+            if (o.topk_macro)
+                for (int z = 0; z < o.topk; ++z) {
+                    o.topk_macro[q * o.topk + z] = a.topk_macro[e * o.topk + z];
+                    o.topk_lat[q * o.topk + z] = a.topk_lat[e * o.topk + z];
+                }
+        }
+        // off-grid: warp-aggregated append to the compaction list
+        const bool off = live && !on;
+        const unsigned mask = __ballot_sync(0xffffffffu, off);
+        if (mask) {
+            const int lane = threadIdx.x & 31;
+            const int leader = __ffs(mask) - 1;
+            unsigned long long basep = 0;
+            if (lane == leader) basep = atomicAdd(reinterpret_cast<unsigned long long*>(a.off_count),
+                                                  (unsigned long long)__popc(mask));
+            basep = __shfl_sync(0xffffffffu, basep, leader);
+            if (off) a.off_idx[basep + __popc(mask & ((1u << lane) - 1u))] = q;
+        }
+    }
+}
+
+// ------------------------------------------------- drop-in per-table helpers
+__global__ void k_predict(DevImage im, PredictArgs a) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    const int c = a.config[i];
+    const int64_t g = a.g[i], l = a.l[i];
+    int32_t st = 0;
+    if (c < 0 || c >= im.C) st = WT_OUT_OF_RANGE;
+    else if (g < 1 || l < 1) st = WT_INVALID_ARGUMENT;  // tuner.cpp:14-15
+    double lat = __longlong_as_double(0x7ff8000000000000LL);
+    int32_t w = 0, ex = 0, used = -1;
+    if (!st) {
+        const uint64_t S = uint64_t(im.S);
+        const uint64_t w64 = (uint64_t(g) + S - 1) / S;
+        const uint32_t row = uint32_t(w64 < uint64_t(im.R) ? w64 : uint64_t(im.R)) - 1u;
+        const size_t rr = size_t(c) * im.R + row;
+        const uint32_t meta = im.rowmeta[rr];
+        w = int32_t(uint32_t(w64));
+        if (meta & ROW_NO_COEFF) {
+            st = WT_RUNTIME_ERROR;
+        } else {
+            const double4 th = im.theta[rr];
+            const double gd = u64_to_f64(uint64_t(g)), ld = u64_to_f64(uint64_t(l));
+            lat = bilinear(th.x, th.y, __dmul_rn(th.z, ld), th.w, gd, ld);
+            ex = (meta & ROW_EXTRAP) ? 1 : 0;
+            used = im.used_w[rr];
+        }
+    }
+    a.lat[i] = lat;
+    if (a.wave) a.wave[i] = w;
+    if (a.extrap) a.extrap[i] = ex;
+    if (a.used_w) a.used_w[i] = used;
+    if (a.status) a.status[i] = st;
+}
+
+// Per-config prediction for one dense query (the loop body of
+// two_stage_select, tuner.cpp:135-149), for Tuned.flags reconstruction.
+__global__ void k_explain(DevImage im, ExplainArgs a) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= im.C) return;
+    int32_t st = 0;
+    if (a.M < 1 || a.N < 1 || a.K < 1) st = WT_INVALID_ARGUMENT;
+    const int4 tl = __ldg(im.tiles + c);
+    uint64_t g = 0;
+    int64_t l = 0;
+    double lat = __longlong_as_double(0x7ff8000000000000LL);
+    int32_t w = 0, used = -1;
+    if (!st) {
+        g = uint64_t((uint64_t(a.M) + tl.x - 1) / uint64_t(tl.x)) *
+            uint64_t((uint64_t(a.N) + tl.y - 1) / uint64_t(tl.y));
+        l = int64_t((uint64_t(a.K) + tl.z - 1) / uint64_t(tl.z));
+        const uint64_t S = uint64_t(im.S);
+        const uint64_t w64 = (g + S - 1) / S;
+        const uint32_t row = uint32_t(w64 < uint64_t(im.R) ? w64 : uint64_t(im.R)) - 1u;
+        const size_t rr = size_t(c) * im.R + row;
+        const uint32_t meta = im.rowmeta[rr];
+        w = int32_t(uint32_t(w64));
+        if (meta & ROW_NO_COEFF) {
+            st = WT_RUNTIME_ERROR;
+        } else {
+            const double4 th = im.theta[rr];
+            const double gd = u64_to_f64(g), ld = u64_to_f64(uint64_t(l));
+            lat = bilinear(th.x, th.y, __dmul_rn(th.z, ld), th.w, gd, ld);
+            used = im.used_w[rr];
+        }
+    }
+    a.g[c] = int64_t(g);
+    a.l[c] = l;
+    a.wave[c] = w;
+    a.used_w[c] = used;
+    a.lat[c] = lat;
+    a.status[c] = st;
+}
+
+__global__ void k_nearest(NearestArgs a) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    int comps = 0;
+    const int k = nearest_anchor_idx(a.anchors, a.n_anchors, a.l[i], &comps);
+    a.out[i] = a.anchors[k];
+    if (a.comps) a.comps[i] = comps;
+}
+
+// ------------------------------------------------------------- launchers
+template <int RPT, bool SPECIAL, bool WIDE, int KM>
+static cudaError_t launch_sweep_t(const DevImage& im, const SweepArgs& a, int grid, size_t smem,
+                                  cudaStream_t st) {
+    auto fn = k_sweep<RPT, SPECIAL, WIDE, KM>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    fn<<<grid, kSweepThreads, smem, st>>>(im, a);
+    return cudaGetLastError();
+}
+
+size_t sweep_smem_bytes(const DevImage& im, int chunk, bool special) {
+    size_t b = size_t(chunk) * (sizeof(SweepCfg) + sizeof(double)) + size_t(chunk) * im.R * sizeof(double4);
+    if (special) b += size_t(chunk) * im.R * sizeof(uint32_t);
+    return b;
+}
+
+cudaError_t launch_sweep(const DevImage& im, const SweepArgs& a, bool wide, cudaStream_t st) {
+    const int64_t n = a.end - a.begin;
+    if (n <= 0) return cudaSuccess;
+    const bool sp = im.special != 0;
+    const size_t smem = sweep_smem_bytes(im, a.chunk, sp);
+    const bool tk = a.topk > 0;
+    const int rpt = tk ? 1 : kSweepRPT;
+    const int grid = int((n + int64_t(kSweepThreads) * rpt - 1) / (int64_t(kSweepThreads) * rpt));
+    if (tk) {
+        if (wide) return sp ? launch_sweep_t<1, true, true, 8>(im, a, grid, smem, st)
+                            : launch_sweep_t<1, false, true, 8>(im, a, grid, smem, st);
+        return sp ? launch_sweep_t<1, true, false, 8>(im, a, grid, smem, st)
+                  : launch_sweep_t<1, false, false, 8>(im, a, grid, smem, st);
+    }
+    if (wide) return sp ? launch_sweep_t<kSweepRPT, true, true, 0>(im, a, grid, smem, st)
+                        : launch_sweep_t<kSweepRPT, false, true, 0>(im, a, grid, smem, st);
+    return sp ? launch_sweep_t<kSweepRPT, true, false, 0>(im, a, grid, smem, st)
+              : launch_sweep_t<kSweepRPT, false, false, 0>(im, a, grid, smem, st);
+}
+
+size_t eval_smem_bytes(const DevImage& im, int chunk, bool special) {
+    size_t b = size_t(chunk) * (sizeof(int4) + sizeof(uint4)) + size_t(chunk) * im.R * sizeof(double4);
+    if (special) b += size_t(chunk) * im.R * sizeof(uint32_t);
+    return b;
+}
+
+template <bool SPECIAL, int KM>
+static cudaError_t launch_eval_t(const DevImage& im, const EvalArgs& a, int grid, size_t smem,
+                                 cudaStream_t st) {
+    auto fn = k_eval<SPECIAL, KM>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    fn<<<grid, kEvalThreads, smem, st>>>(im, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eval(const DevImage& im, const EvalArgs& a, int grid, cudaStream_t st) {
+    const bool sp = im.special != 0;
+    const size_t smem = eval_smem_bytes(im, a.chunk, sp);
+    if (a.out.topk > 0)
+        return sp ? launch_eval_t<true, 8>(im, a, grid, smem, st) : launch_eval_t<false, 8>(im, a, grid, smem, st);
+    return sp ? launch_eval_t<true, 0>(im, a, grid, smem, st) : launch_eval_t<false, 0>(im, a, grid, smem, st);
+}
+
+cudaError_t launch_grouped(const DevImage& im, const GroupedArgs& a, int grid, cudaStream_t st) {
+    k_grouped<<<grid, 256, 0, st>>>(im, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const DevImage& im, const GatherArgs& a, int grid, cudaStream_t st) {
+    const size_t smem = size_t(a.n_pairs) * (sizeof(uint64_t) + sizeof(int32_t)) + 16;
+    k_gather<<<grid, kGatherThreads, smem, st>>>(im, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_predict(const DevImage& im, const PredictArgs& a, cudaStream_t st) {
+    const int grid = int((a.n + 255) / 256);
+    if (grid > 0) k_predict<<<grid, 256, 0, st>>>(im, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_explain(const DevImage& im, const ExplainArgs& a, cudaStream_t st) {
+    k_explain<<<(im.C + 127) / 128, 128, 0, st>>>(im, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_nearest(const NearestArgs& a, cudaStream_t st) {
+    const int grid = int((a.n + 255) / 256);
+    if (grid > 0) k_nearest<<<grid, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace wtb

@@ -1,0 +1,124 @@
+// wt_decide.h -- launch interface between the C-ABI layer and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "wt_internal.h"
+
+namespace wtb {
+
+constexpr int kSweepThreads = 256;
+constexpr int kSweepRPT = 4;  // shapes per thread in the sweep
+constexpr int kEvalThreads = 256;
+constexpr int kGatherThreads = 256;
+
+struct DecOut {
+    int32_t* macro;
+    int32_t* micro;
+    double* lat;
+    int64_t* g;
+    int64_t* l;
+    int32_t* wave;
+    uint32_t* flags;
+    int32_t* comps;
+    double* tail;
+    int32_t topk;
+    int32_t* topk_macro;
+    double* topk_lat;
+};
+
+struct SweepArgs {
+    const int32_t* N;  // [n_pairs] device
+    const int32_t* K;
+    int32_t m_lo;
+    int64_t mcount;    // M values per pair
+    int64_t begin, end;
+    int32_t chunk;     // configs per shared-memory chunk
+    wt_grid_entry* entries;
+    int32_t topk;
+    int32_t* topk_macro;
+    double* topk_lat;
+};
+
+struct EvalArgs {
+    const int32_t* M;
+    const int32_t* N;
+    const int32_t* K;
+    int64_t n;
+    const int64_t* idx;    // optional compacted query indices
+    const int64_t* count;  // optional device count of idx
+    int32_t chunk;
+    DecOut out;
+};
+
+struct GroupedArgs {
+    const int64_t* row_off;
+    const int32_t* rows;
+    const int32_t* N;
+    const int32_t* K;
+    int64_t n;
+    DecOut out;
+};
+
+struct GatherArgs {
+    const uint64_t* pair_keys;  // sorted (N << 32 | K)
+    const int32_t* pair_ids;
+    int32_t n_pairs;
+    int32_t m_lo, m_hi;
+    int64_t mcount;
+    const wt_grid_entry* entries;
+    const int32_t* topk_macro;
+    const double* topk_lat;
+    const int32_t* M;
+    const int32_t* N;
+    const int32_t* K;
+    int64_t n;
+    DecOut out;
+    int64_t* off_count;
+    int64_t* off_idx;
+};
+
+struct PredictArgs {
+    const int32_t* config;
+    const int64_t* g;
+    const int64_t* l;
+    int64_t n;
+    double* lat;
+    int32_t* wave;
+    int32_t* extrap;
+    int32_t* used_w;
+    int32_t* status;
+};
+
+struct ExplainArgs {
+    int64_t M, N, K;
+    int64_t* g;
+    int64_t* l;
+    int32_t* wave;
+    int32_t* used_w;
+    double* lat;
+    int32_t* status;
+};
+
+struct NearestArgs {
+    const int64_t* anchors;
+    int32_t n_anchors;
+    const int64_t* l;
+    int64_t n;
+    int64_t* out;
+    int32_t* comps;
+};
+
+size_t sweep_smem_bytes(const DevImage& im, int chunk, bool special);
+size_t eval_smem_bytes(const DevImage& im, int chunk, bool special);
+cudaError_t launch_sweep(const DevImage& im, const SweepArgs& a, bool wide, cudaStream_t st);
+cudaError_t launch_eval(const DevImage& im, const EvalArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_grouped(const DevImage& im, const GroupedArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_gather(const DevImage& im, const GatherArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_predict(const DevImage& im, const PredictArgs& a, cudaStream_t st);
+cudaError_t launch_explain(const DevImage& im, const ExplainArgs& a, cudaStream_t st);
+cudaError_t launch_nearest(const NearestArgs& a, cudaStream_t st);
+
+}  // namespace wtb

@@ -1,0 +1,107 @@
+// wt_device.cuh -- exact integer / fp64 building blocks for the sm_100a
+// decision kernels.  Every helper reproduces the reference's C++ arithmetic
+// bit for bit.
+#pragma once
+
+#include <cstdint>
+
+#include "wt_internal.h"
+
+namespace wtb {
+
+// floor(y2/2 / d) for y2 = 2*y, y < 2^31 (see make_magic): IMAD.HI + SHF.
+__device__ __forceinline__ uint32_t mdiv2(uint32_t y2, uint32_t m, uint32_t s) {
+    return __umulhi(y2, m) >> s;
+}
+
+// ceil_div(x, d) = (x + d - 1) / d for 1 <= x < 2^31 (kernel_map.hpp:17).
+__device__ __forceinline__ uint32_t cdiv_m(uint32_t x, uint32_t m, uint32_t s) {
+    return mdiv2(2u * (x - 1u), m, s) + 1u;
+}
+
+// Exact (double)x for x < 2^32: one DADD, no I2F (the conversion pipe runs
+// at a quarter of the DADD rate).
+__device__ __forceinline__ double u32_to_f64(uint32_t x) {
+    return __dsub_rn(__hiloint2double(0x43300000, int(x)), 4503599627370496.0);
+}
+
+// (double)x for x < 2^63 with the reference's rounding (i64 -> double, RN).
+__device__ __forceinline__ double u64_to_f64(uint64_t x) {
+    if (x < (uint64_t(1) << 52))
+        return __dsub_rn(__longlong_as_double((long long)(0x4330000000000000ULL | x)),
+                         4503599627370496.0);
+    return __ull2double_rn(x);
+}
+
+// BilinearCoeffs::predict (model.hpp:20-23) as the reference evaluates it:
+//   ((((alpha*g)*l) + (beta*g)) + (gamma*l)) + delta, binary64, no FMA.
+// gl = gamma * l may be precomputed (same rounded product).
+__device__ __forceinline__ double bilinear(double a, double b, double gl, double d, double gd,
+                                           double ld) {
+    double t = __dmul_rn(__dmul_rn(a, gd), ld);
+    t = __dadd_rn(t, __dmul_rn(b, gd));
+    t = __dadd_rn(t, gl);
+    return __dadd_rn(t, d);
+}
+
+// Row of the dense image for grid size g (w = ceil(g/S), rows clamp at R-1).
+__device__ __forceinline__ uint32_t row_of(uint32_t g_clamped, uint32_t mS, uint32_t sS) {
+    return mdiv2(2u * g_clamped - 2u, mS, sS);
+}
+
+// Read-only 32-byte row load (two 16-byte LDG.E.128.CONSTANT).
+__device__ __forceinline__ double4 ldg_row(const double4* p) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// nearest_anchor (tuner.cpp:44-70): lower_bound, then the closer neighbour,
+// ties to the smaller anchor.  Returns the index; *comps = comparisons.
+__device__ __forceinline__ int nearest_anchor_idx(const int64_t* a, int n, int64_t l, int* comps) {
+    int c = 0, lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        ++c;
+        if (a[mid] < l)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    int r;
+    if (lo == 0) {
+        r = 0;
+    } else if (lo == n) {
+        r = n - 1;
+    } else {
+        ++c;
+        r = (l - a[lo - 1] <= a[lo] - l) ? lo - 1 : lo;
+    }
+    *comps = c;
+    return r;
+}
+
+// Top-k insertion into an ascending list; equal latencies keep the earlier
+// (smaller macro_id) entry first; NaN and +inf never enter.
+template <int KM>
+__device__ __forceinline__ void topk_insert(double (&L)[KM], int (&I)[KM], double v, int c) {
+    if (!(v < L[KM - 1])) return;
+    bool placed = false;
+#pragma unroll
+    for (int q = KM - 1; q > 0; --q) {
+        if (v < L[q - 1]) {
+            L[q] = L[q - 1];
+            I[q] = I[q - 1];
+        } else if (!placed) {
+            L[q] = v;
+            I[q] = c;
+            placed = true;
+        }
+    }
+    if (!placed) {
+        L[0] = v;
+        I[0] = c;
+    }
+}
+
+}  // namespace wtb

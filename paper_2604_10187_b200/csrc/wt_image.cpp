@@ -1,0 +1,224 @@
+// wt_image.cpp -- resolves a std::vector<DualTable> (flattened as
+// wt_tables_desc) into the dense device image the kernels read.
+//
+// Every data-dependent rule of the reference's query path is decided here,
+// once, instead of per query:
+//   * tables sorted by macro_id (tuner.cpp:127-132); duplicate ids are
+//     rejected because std::sort leaves their order unspecified;
+//   * registry.macro(id) join (kernel_map.cpp:96-100), out_of_range text;
+//   * the W-horizon switch (tuner.cpp:17-18): row w-1 for w <= W_c holds
+//     coeff_table[w], rows for w > W_c hold theta_ext;
+//   * the missing-wave fallback (tuner.cpp:20-39): nearest key over ALL
+//     keys, ties to the smaller key, source wave kept for the flag text;
+//   * the Stage-II map choice and its fallback (tuner.cpp:80-103): ext
+//     anchors when extrapolated and non-empty, else anchor_table[w] when
+//     non-empty, else the nearest non-empty wave map to (W_c if
+//     extrapolated else w), ties to the smaller wave.
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+#include <map>
+#include <numeric>
+
+#include "wt_internal.h"
+
+namespace wtb {
+
+namespace {
+
+wt_status fail(std::string* err, wt_status st, const std::string& msg) {
+    *err = msg;
+    return st;
+}
+
+}  // namespace
+
+wt_status build_image(const wt_tables_desc& T, const wt_registry_desc& reg, const wt_hw& hw,
+                      HostImage* out, std::string* err) {
+    if (hw.n_sm < 1 || hw.blocks_per_sm < 1)
+        return fail(err, WT_INVALID_ARGUMENT, "hardware spec must have positive capacities");
+    if (T.n_tables <= 0) return fail(err, WT_INVALID_ARGUMENT, "no dual tables provided");
+    const int64_t S64 = int64_t(hw.n_sm) * hw.blocks_per_sm;
+    if (S64 >= (int64_t(1) << 30))
+        return fail(err, WT_UNSUPPORTED, "slots = n_sm * blocks_per_sm exceeds the device path's range");
+
+    // registry.macro(id): first macro with that id wins (linear scan order).
+    std::map<int32_t, int32_t> reg_pos;
+    for (int32_t i = reg.n_macros - 1; i >= 0; --i) reg_pos[reg.id[i]] = i;
+
+    std::vector<int32_t> order(T.n_tables);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return T.macro_id[a] < T.macro_id[b]; });
+    for (int32_t i = 1; i < T.n_tables; ++i)
+        if (T.macro_id[order[i]] == T.macro_id[order[i - 1]])
+            return fail(err, WT_INVALID_ARGUMENT,
+                        "duplicate macro_id " + std::to_string(T.macro_id[order[i]]) +
+                            " in dual tables");
+
+    HostImage& im = *out;
+    im.C = T.n_tables;
+    im.S = int32_t(S64);
+    im.family = reg.family;
+    int32_t wmax = 0;
+    for (int32_t i = 0; i < T.n_tables; ++i) wmax = std::max(wmax, T.W[i]);
+    if (wmax > 4096)
+        return fail(err, WT_UNSUPPORTED, "table W above 4096 is outside the device path's range");
+    im.R = wmax + 1;
+    if (int64_t(im.R) * S64 >= (int64_t(1) << 31))
+        return fail(err, WT_UNSUPPORTED, "W * slots exceeds the device path's range");
+
+    const int32_t C = im.C, R = im.R;
+    im.macro_id.resize(C);
+    im.W.resize(C);
+    im.tiles.assign(size_t(C) * 4, 0);
+    im.magic.assign(size_t(C) * 4, 0);
+    im.theta.assign(size_t(C) * R * 4, 0.0);
+    im.rowmeta.assign(size_t(C) * R, 0);
+    im.used_w.assign(size_t(C) * R, -1);
+    im.amap.assign(size_t(C) * R * 2, 0);
+    im.afb.assign(size_t(C) * R, -1);
+    im.anchor_l.clear();
+    im.anchor_micro.clear();
+    im.tm_min = INT32_MAX;
+    im.tn_min = INT32_MAX;
+
+    for (int32_t c = 0; c < C; ++c) {
+        const int32_t t = order[c];
+        const int32_t id = T.macro_id[t];
+        im.macro_id[c] = id;
+        im.W[c] = T.W[t];
+        auto it = reg_pos.find(id);
+        if (it == reg_pos.end())
+            return fail(err, WT_OUT_OF_RANGE, "no macro config with id " + std::to_string(id));
+        int64_t tm = reg.t_m[it->second], tn = reg.t_n[it->second], tk = reg.t_k[it->second];
+        if (reg.family == WT_FAMILY_FLASH_ATTENTION) tn = 1;  // g = n_heads * ceil(s_q / t_q)
+        if (tm < 1 || tn < 1 || tk < 1) return fail(err, WT_INVALID_ARGUMENT, "tile dims must be >= 1");
+        if (tm > INT32_MAX || tn > INT32_MAX || tk > INT32_MAX)
+            return fail(err, WT_UNSUPPORTED, "tile dims above 2^31-1 are outside the device path's range");
+        im.tiles[4 * c + 0] = int32_t(tm);
+        im.tiles[4 * c + 1] = int32_t(tn);
+        im.tiles[4 * c + 2] = int32_t(tk);
+        Magic a = make_magic(uint32_t(tm)), b = make_magic(uint32_t(tn)), k = make_magic(uint32_t(tk));
+        im.magic[4 * c + 0] = a.m;
+        im.magic[4 * c + 1] = b.m;
+        im.magic[4 * c + 2] = k.m;
+        im.magic[4 * c + 3] = a.s | (b.s << 8) | (k.s << 16);
+        im.tm_min = std::min<int32_t>(im.tm_min, int32_t(tm));
+        im.tn_min = std::min<int32_t>(im.tn_min, int32_t(tn));
+
+        // Anchor maps of this table, stored once in the pool.
+        const int32_t aw_lo = T.awave_off[t], aw_hi = T.awave_off[t + 1];
+        std::vector<std::pair<int32_t, int32_t>> wave_map;  // (wave, pool offset) non-empty only
+        std::vector<int32_t> wave_cnt;
+        for (int32_t i = aw_lo; i < aw_hi; ++i) {
+            int32_t lo = T.awave_aoff[i], hi = T.awave_aoff[i + 1];
+            if (hi <= lo) continue;
+            wave_map.push_back({T.awave_w[i], int32_t(im.anchor_l.size())});
+            wave_cnt.push_back(hi - lo);
+            for (int32_t q = lo; q < hi; ++q) {
+                im.anchor_l.push_back(T.anchor_l[q]);
+                im.anchor_micro.push_back(T.anchor_micro[q]);
+            }
+        }
+        int32_t ext_off = int32_t(im.anchor_l.size());
+        int32_t ext_cnt = T.ext_aoff[t + 1] - T.ext_aoff[t];
+        for (int32_t q = T.ext_aoff[t]; q < T.ext_aoff[t + 1]; ++q) {
+            im.anchor_l.push_back(T.ext_l[q]);
+            im.anchor_micro.push_back(T.ext_micro[q]);
+        }
+        // nearest non-empty wave map to target (ties -> smaller wave)
+        auto nearest_map = [&](int32_t target, int32_t* off, int32_t* cnt, int32_t* wave) {
+            int best = INT_MAX;
+            int32_t best_w = 0;
+            bool found = false;
+            for (size_t i = 0; i < wave_map.size(); ++i) {
+                int d = std::abs(wave_map[i].first - target);
+                if (d < best || (d == best && wave_map[i].first < best_w)) {
+                    best = d;
+                    best_w = wave_map[i].first;
+                    *off = wave_map[i].second;
+                    *cnt = wave_cnt[i];
+                    found = true;
+                }
+            }
+            *wave = best_w;
+            return found;
+        };
+
+        const int32_t co_lo = T.coeff_off[t], co_hi = T.coeff_off[t + 1];
+        const int32_t Wc = T.W[t];
+        for (int32_t r = 0; r < R; ++r) {
+            const int32_t w = r + 1;  // last row stands for every w >= R > W_c
+            const size_t row = size_t(c) * R + r;
+            uint32_t meta = 0;
+            const double* th = nullptr;
+            bool extrap = (r == R - 1) || (w > Wc);
+            if (extrap) {
+                meta |= ROW_EXTRAP;
+                th = T.theta_ext + 4 * size_t(t);
+            } else {
+                for (int32_t i = co_lo; i < co_hi; ++i)
+                    if (T.coeff_w[i] == w) th = T.coeff_theta + 4 * size_t(i);
+                if (!th) {
+                    if (co_hi == co_lo) {
+                        meta |= ROW_NO_COEFF;
+                    } else {
+                        int best = INT_MAX;
+                        int32_t best_w = 0, best_i = -1;
+                        for (int32_t i = co_lo; i < co_hi; ++i) {
+                            int d = std::abs(T.coeff_w[i] - w);
+                            if (d < best || (d == best && T.coeff_w[i] < best_w)) {
+                                best = d;
+                                best_w = T.coeff_w[i];
+                                best_i = i;
+                            }
+                        }
+                        meta |= ROW_MISSING;
+                        im.used_w[row] = best_w;
+                        th = T.coeff_theta + 4 * size_t(best_i);
+                    }
+                }
+            }
+            if (th)
+                for (int q = 0; q < 4; ++q) im.theta[4 * row + q] = th[q];
+            // Stage-II map
+            int32_t off = 0, cnt = 0, fbw = -1;
+            bool have = false;
+            if (extrap) {
+                if (ext_cnt > 0) {
+                    off = ext_off;
+                    cnt = ext_cnt;
+                    have = true;
+                }
+            } else {
+                for (size_t i = 0; i < wave_map.size(); ++i)
+                    if (wave_map[i].first == w) {
+                        off = wave_map[i].second;
+                        cnt = wave_cnt[i];
+                        have = true;
+                    }
+            }
+            if (!have) {
+                int32_t target = extrap ? Wc : w;
+                if (nearest_map(target, &off, &cnt, &fbw)) {
+                    meta |= ROW_ANCHOR_FB;
+                    im.afb[row] = fbw;
+                } else {
+                    meta |= ROW_NO_ANCHOR;
+                }
+            }
+            im.amap[2 * row] = off;
+            im.amap[2 * row + 1] = cnt;
+            im.rowmeta[row] = meta;
+            if (meta & ROW_SPECIAL) im.special = true;
+        }
+    }
+    if (im.anchor_l.empty()) {  // keep the pool non-empty for the device
+        im.anchor_l.push_back(0);
+        im.anchor_micro.push_back(-1);
+    }
+    return WT_OK;
+}
+
+}  // namespace wtb

@@ -1,0 +1,84 @@
+// wt_internal.h -- shared between the host image builder, the C-ABI layer
+// and the sm_100a kernels.  Not part of the public boundary.
+#pragma once
+
+#include <vector_types.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "wavetune_c.h"
+
+namespace wtb {
+
+// Row metadata bits (one u32 per (config, row)).
+enum : uint32_t {
+    ROW_EXTRAP = 1u << 0,       // row serves w > W_c: theta_ext, ext anchors
+    ROW_MISSING = 1u << 1,      // coefficient fallback (missing_wave_<w>_used_<k>)
+    ROW_NO_COEFF = 1u << 2,     // coeff_table empty and w <= W_c: runtime_error
+    ROW_ANCHOR_FB = 1u << 3,    // anchor_fallback_wave_<k>
+    ROW_NO_ANCHOR = 1u << 4,    // no non-empty anchor map: runtime_error
+};
+constexpr uint32_t ROW_SPECIAL = ROW_MISSING | ROW_NO_COEFF;
+
+// Exact floor(y / d) for 0 <= y < 2^31 and 1 <= d < 2^31:
+//   floor(y / d) = umulhi(2y, m) >> s,  s = ceil(log2 d), m = ceil(2^(31+s) / d)
+// (m < 2^32; error y * (m*d - 2^(31+s)) < 2^31 * d <= 2^(31+s)).
+struct Magic {
+    uint32_t m;
+    uint32_t s;
+};
+inline Magic make_magic(uint32_t d) {
+    uint32_t s = 0;
+    while ((uint64_t(1) << s) < d) ++s;
+    unsigned __int128 num = (unsigned __int128)1 << (31 + s);
+    uint64_t m = (uint64_t)((num + d - 1) / d);
+    return Magic{(uint32_t)m, s};
+}
+
+// POD image handed to kernels by value.
+struct DevImage {
+    int32_t C;          // configs (tables), ascending macro_id
+    int32_t R;          // rows per config: waves 1..R-1 then row R-1 = every w >= R
+    int32_t S;          // slots
+    uint32_t RS;        // R * S  (< 2^31)
+    uint32_t mS, sS;    // magic for / S
+    int32_t special;    // any ROW_SPECIAL row exists
+    const int32_t* macro_id;  // [C]
+    const int4* tiles;        // [C] {t_m, t_n, t_k, 0} (attention: t_n = 1)
+    const uint4* magic;       // [C] {m_m, m_n, m_k, s_m | s_n << 8 | s_k << 16}
+    const double4* theta;     // [C*R]
+    const uint32_t* rowmeta;  // [C*R]
+    const int32_t* used_w;    // [C*R] coefficient fallback source wave or -1
+    const int2* amap;         // [C*R] {offset, count} into the anchor pool
+    const int32_t* afb;       // [C*R] anchor fallback wave or -1
+    const int64_t* anchor_l;  // pool
+    const int32_t* anchor_micro;
+    int32_t tm_min, tn_min;   // for the per-query wide-range guard
+};
+
+// Host-side resolved image (built by build_image, uploaded by the C-ABI).
+struct HostImage {
+    int32_t C = 0, R = 0, S = 0, family = 0;
+    bool special = false;
+    std::vector<int32_t> macro_id;
+    std::vector<int32_t> W;  // per config
+    std::vector<int32_t> tiles;   // 4 per config
+    std::vector<uint32_t> magic;  // 4 per config
+    std::vector<double> theta;    // 4 per row
+    std::vector<uint32_t> rowmeta;
+    std::vector<int32_t> used_w;
+    std::vector<int32_t> amap;    // 2 per row
+    std::vector<int32_t> afb;
+    std::vector<int64_t> anchor_l;
+    std::vector<int32_t> anchor_micro;
+    int32_t tm_min = 0, tn_min = 0;
+};
+
+// Resolves every reference fallback rule into dense rows; returns WT_OK or
+// an error status with *err set to the reference's message.
+wt_status build_image(const wt_tables_desc& t, const wt_registry_desc& r, const wt_hw& hw,
+                      HostImage* out, std::string* err);
+
+}  // namespace wtb

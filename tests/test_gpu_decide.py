@@ -1,0 +1,359 @@
+"""GPU parity: the sm_100a decision kernels (through the C-ABI) against the
+reference compiled verbatim (oracle/_ref) and the C restatement (oracle/).
+
+Bar: macro / micro / wave / regime / comparisons / g / l bit-exact, predicted
+latency bit-exact (BASELINE.json allows 1e-5 relative; the kernels use the
+reference's exact fp64 operation order, so we assert bitwise equality).
+"""
+import numpy as np
+import pytest
+
+import pyoracle as po
+import wtutil as U
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def capi():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_10187_b200 import capi as c
+
+    c.lib()
+    return c
+
+
+@pytest.fixture(scope="module")
+def ref():
+    return po.Reference()
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return po.Oracle()
+
+
+def dev(a, dt=torch.int32):
+    return torch.as_tensor(np.ascontiguousarray(a)).to(dtype=dt, device="cuda")
+
+
+def tune_gpu(capi, eng, M, N, K, topk=0, grid=None):
+    n = len(M)
+    o = dict(macro=torch.empty(n, dtype=torch.int32, device="cuda"),
+             micro=torch.empty(n, dtype=torch.int32, device="cuda"),
+             lat=torch.empty(n, dtype=torch.float64, device="cuda"),
+             g=torch.empty(n, dtype=torch.int64, device="cuda"),
+             l=torch.empty(n, dtype=torch.int64, device="cuda"),
+             wave=torch.empty(n, dtype=torch.int32, device="cuda"),
+             flags=torch.empty(n, dtype=torch.int32, device="cuda"),
+             comps=torch.empty(n, dtype=torch.int32, device="cuda"),
+             tail=torch.empty(n, dtype=torch.float64, device="cuda"))
+    if topk:
+        o["tkm"] = torch.empty(n * topk, dtype=torch.int32, device="cuda")
+        o["tkl"] = torch.empty(n * topk, dtype=torch.float64, device="cuda")
+    d = capi.Engine.decisions(o["macro"], o["micro"], o["lat"], o["g"], o["l"], o["wave"], o["flags"], o["comps"],
+                              o["tail"], topk, o.get("tkm"), o.get("tkl"))
+    Md, Nd, Kd = dev(M), dev(N), dev(K)
+    if grid is None:
+        eng.tune_batch(Md, Nd, Kd, d)
+    else:
+        grid.gather(Md, Nd, Kd, d)
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in o.items()}
+
+
+def assert_same(gpu, want, status_key="status"):
+    st = want[status_key]
+    gst = (gpu["flags"].astype(np.uint32) >> 24).astype(np.int32)
+    np.testing.assert_array_equal(gst, st)
+    ok = st == 0
+    for k_g, k_w in (("macro", "macro"), ("micro", "micro"), ("g", "g"), ("l", "l"), ("wave", "w"),
+                     ("comps", "comps")):
+        np.testing.assert_array_equal(gpu[k_g][ok], want[k_w][ok], err_msg=k_g)
+    np.testing.assert_array_equal(U.bits(gpu["lat"][ok]), U.bits(want["lat"][ok]))
+    ex = (gpu["flags"] & 1) != 0
+    np.testing.assert_array_equal(ex[ok], want["extrap"][ok] != 0)
+
+
+# ------------------------------------------------------------------ fixtures
+@pytest.fixture(scope="module")
+def landscape(ref, tmpdir_session):
+    reg, rec, tab = U.reference_fixture(ref, tmpdir_session)
+    fam, tabs = po.parse_tables_json(tab)
+    tiles, order = po.parse_registry_json(reg)
+    return dict(reg=reg, rec=rec, tab=tab, tabs=tabs, tiles=tiles, arrays=U.arrays_from_pytables(tabs),
+                registry=U.registry_from_json(reg))
+
+
+@pytest.fixture(scope="module")
+def synth256():
+    from paper_2604_10187_b200 import synthetic as S
+
+    cfg = S.config_space(full=False)
+    t = S.synthetic_tables(cfg)
+    return cfg, t, S.registry_arrays(cfg)
+
+
+# --------------------------------------------------------------------- tests
+def test_tune_matches_reference_on_its_landscape(capi, ref, orc, landscape):
+    """Reference acceptance landscape (6x8 configs, W=10, sigma=5): GPU tune vs
+    the reference's own tune() on 50k random shapes (acceptance.cpp:246-259
+    style draws) plus the boundary shapes of every wave."""
+    L = landscape
+    eng = capi.Engine(L["arrays"], L["registry"], n_sm=132)
+    rng = np.random.default_rng(33)
+    n = 50000
+    M = rng.integers(1, 9000, n)
+    N = rng.integers(1, 9000, n)
+    K = rng.integers(1, 9000, n)
+    # wave boundaries: g = w*132 and w*132+1 for 64x64 tiles
+    wb = np.array([w * 132 + d for w in range(1, 14) for d in (0, 1)])
+    M = np.concatenate([M, wb * 64, np.full(len(wb), 64)])
+    N = np.concatenate([N, np.full(len(wb), 64), wb * 64])
+    K = np.concatenate([K, np.full(2 * len(wb), 1024)])
+    h = ref.open(L["tab"], L["reg"], 132)
+    want = ref.tune(h, M, N, K, nthreads=8)
+    got = tune_gpu(capi, eng, M, N, K)
+    assert (want["status"] == 0).all()
+    assert_same(got, want)
+    assert (want["evals"] == eng.n_configs).all()
+    # restatement agrees with the reference too (pinning)
+    flat = po.FlatTables(L["tabs"], L["tiles"])
+    w2 = orc.tune(flat, 132, 1, M, N, K)
+    assert_same(got, w2)
+    ref.close(h)
+
+
+def test_sweep_grid_config1_bitexact(capi, orc, synth256):
+    """Config 1: 4 Llama-3-8B pairs x M=1..8192 x 256 configs, every entry vs
+    the oracle tune()."""
+    from paper_2604_10187_b200 import synthetic as S
+
+    cfg, t, reg = synth256
+    eng = capi.Engine(t, reg, n_sm=148)
+    pairs = S.LLAMA3_8B
+    grid = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 8192)
+    grid.sweep()
+    torch.cuda.synchronize()
+    ent = grid.entries_tensor().cpu().numpy()
+    lat = ent[:, 0:2].copy().view(np.float64)[:, 0]
+    M = np.tile(np.arange(1, 8193), len(pairs))
+    N = np.repeat([p[0] for p in pairs], 8192)
+    K = np.repeat([p[1] for p in pairs], 8192)
+    tiles = {int(i): (int(a), int(b), int(c)) for i, a, b, c in zip(cfg["id"], cfg["t_m"], cfg["t_n"], cfg["t_k"])}
+    flat = po.FlatTables(U.pytables_from_arrays(t), tiles)
+    want = orc.tune(flat, 148, 1, M, N, K)
+    assert (want["status"] == 0).all()
+    np.testing.assert_array_equal(ent[:, 2], want["macro"])
+    np.testing.assert_array_equal(ent[:, 3], want["micro"])
+    np.testing.assert_array_equal(ent[:, 4], want["w"])
+    np.testing.assert_array_equal(ent[:, 6], want["comps"])
+    np.testing.assert_array_equal(U.bits(lat), U.bits(want["lat"]))
+    np.testing.assert_array_equal(ent[:, 5] & 1, want["extrap"])
+    # tail fraction of the winner (extension): (g - (w-1)*S)/S
+    tail = ent[:, 7].copy().view(np.float32)
+    exp = ((want["g"] - (want["w"] - 1) * 148) / 148.0).astype(np.float32)
+    np.testing.assert_array_equal(tail, exp)
+
+
+def test_gather_matches_tune_with_offgrid(capi, orc, synth256):
+    """Config 2 stream (decode/prefill mix + 1% off-grid): gather answers ==
+    evaluate-mode answers == oracle."""
+    from paper_2604_10187_b200 import synthetic as S
+
+    cfg, t, reg = synth256
+    eng = capi.Engine(t, reg, n_sm=148)
+    pairs = S.LLAMA3_8B
+    grid = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 8192)
+    grid.sweep()
+    M, N, K = S.query_stream(300000, pairs, seed=55, off_grid_frac=0.02)
+    got = tune_gpu(capi, eng, M, N, K, grid=grid)
+    direct = tune_gpu(capi, eng, M, N, K)
+    for k in ("macro", "micro", "wave", "comps", "flags", "g", "l"):
+        np.testing.assert_array_equal(got[k], direct[k], err_msg=k)
+    np.testing.assert_array_equal(U.bits(got["lat"]), U.bits(direct["lat"]))
+    tiles = {int(i): (int(a), int(b), int(c)) for i, a, b, c in zip(cfg["id"], cfg["t_m"], cfg["t_n"], cfg["t_k"])}
+    flat = po.FlatTables(U.pytables_from_arrays(t), tiles)
+    sub = np.random.default_rng(0).choice(len(M), 40000, replace=False)
+    want = orc.tune(flat, 148, 1, M[sub], N[sub], K[sub])
+    assert_same({k: v[sub] for k, v in got.items()}, want)
+
+
+def test_topk_matches_oracle(capi, orc, synth256):
+    from paper_2604_10187_b200 import synthetic as S
+
+    cfg, t, reg = synth256
+    eng = capi.Engine(t, reg, n_sm=148)
+    rng = np.random.default_rng(5)
+    n = 3000
+    M = rng.integers(1, 8193, n)
+    P = np.array(S.LLAMA3_8B)[rng.integers(0, 4, n)]
+    N, K = P[:, 0], P[:, 1]
+    k = 4
+    got = tune_gpu(capi, eng, M, N, K, topk=k)
+    grid = capi.Grid(eng, [p[0] for p in S.LLAMA3_8B], [p[1] for p in S.LLAMA3_8B], 1, 8192, topk=k)
+    grid.sweep()
+    got_g = tune_gpu(capi, eng, M, N, K, topk=k, grid=grid)
+    tiles = {int(i): (int(a), int(b), int(c)) for i, a, b, c in zip(cfg["id"], cfg["t_m"], cfg["t_n"], cfg["t_k"])}
+    flat = po.FlatTables(U.pytables_from_arrays(t), tiles)
+    for i in range(0, n, 7):
+        st, mac, lat = orc.topk(flat, 148, 1, int(M[i]), int(N[i]), int(K[i]), k)
+        assert st == 0
+        np.testing.assert_array_equal(got["tkm"][i * k:(i + 1) * k], mac)
+        np.testing.assert_array_equal(U.bits(got["tkl"][i * k:(i + 1) * k]), U.bits(lat))
+        np.testing.assert_array_equal(got_g["tkm"][i * k:(i + 1) * k], mac)
+        assert got["macro"][i] == mac[0]
+
+
+def _mutilate(t, rng):
+    """Tables exercising every fallback rule: erased coefficient waves,
+    erased / emptied anchor maps, per-table W, an empty coeff table, NaN and
+    +inf coefficients, ties."""
+    tabs = U.pytables_from_arrays(t)
+    for i, tb in enumerate(tabs):
+        r = i % 9
+        if r == 1:
+            for w in rng.choice(sorted(tb.coeffs), 5, replace=False):
+                del tb.coeffs[int(w)]
+        elif r == 2:
+            for w in rng.choice(sorted(tb.anchors), 6, replace=False):
+                del tb.anchors[int(w)]
+        elif r == 3:
+            tb.ext_anchors = {}
+        elif r == 4:
+            tb.W = int(rng.integers(3, 40))
+        elif r == 5:
+            w = int(rng.integers(1, 41))
+            tb.coeffs[w] = (float("nan"),) * 4
+        elif r == 6:
+            tb.coeffs = {w: c for w, c in tb.coeffs.items() if w % 3 == 0}
+            tb.anchors = {w: d for w, d in tb.anchors.items() if w % 4 == 0}
+        elif r == 7:
+            tb.theta_ext = (0.0, 0.0, 0.0, float("inf"))
+        elif r == 8 and i < 40:
+            tb.coeffs[7] = tabs[i - 1].coeffs.get(7, (0.0, 0.0, 0.0, 1.0))  # exact ties across ids
+    return tabs
+
+
+def test_fallback_rules_and_errors(capi, orc, ref, synth256, tmpdir_session):
+    cfg, t, reg = synth256
+    rng = np.random.default_rng(9)
+    tabs = _mutilate(t, rng)
+    arr = U.arrays_from_pytables(tabs)
+    eng = capi.Engine(arr, reg, n_sm=148)
+    assert eng.info.has_fallback_rows == 1
+    n = 60000
+    M = rng.integers(1, 70000, n)
+    N = rng.integers(1, 70000, n)
+    K = rng.integers(1, 20000, n)
+    M[:50] = 0  # invalid dims -> invalid_argument
+    K[50:60] = -3
+    got = tune_gpu(capi, eng, M, N, K)
+    tiles = {int(i): (int(a), int(b), int(c)) for i, a, b, c in zip(cfg["id"], cfg["t_m"], cfg["t_n"], cfg["t_k"])}
+    want = orc.tune(po.FlatTables(tabs, tiles), 148, 1, M, N, K)
+    assert_same(got, want)
+    ok = want["status"] == 0
+    np.testing.assert_array_equal(((got["flags"] >> 1) & 1)[ok], (want["n_missing"] > 0)[ok])
+    np.testing.assert_array_equal(((got["flags"] >> 2) & 1)[ok], (want["anchor_fb"] >= 0)[ok])
+    # the same artefact through the reference itself (JSON round trip)
+    tab = str(tmpdir_session / "mutilated.json")
+    regp = str(tmpdir_session / "reg256.json")
+    U.write_tables_json(tabs, tab)
+    U.write_registry_json(reg, regp)
+    h = ref.open(tab, regp, 148)
+    sub = slice(60, 20060)
+    wr = ref.tune(h, M[sub], N[sub], K[sub], nthreads=8)
+    assert_same({k: v[sub] for k, v in got.items()}, wr)
+    ref.close(h)
+
+
+def test_empty_coeff_table_is_runtime_error(capi, orc, synth256):
+    cfg, t, reg = synth256
+    tabs = U.pytables_from_arrays(t)
+    tabs[3].coeffs = {}
+    eng = capi.Engine(U.arrays_from_pytables(tabs), reg, n_sm=148)
+    M = np.array([1, 100000, 8192]); N = np.array([4096, 4096, 4096]); K = np.array([4096, 4096, 4096])
+    got = tune_gpu(capi, eng, M, N, K)
+    tiles = {int(i): (int(a), int(b), int(c)) for i, a, b, c in zip(cfg["id"], cfg["t_m"], cfg["t_n"], cfg["t_k"])}
+    want = orc.tune(po.FlatTables(tabs, tiles), 148, 1, M, N, K)
+    assert_same(got, want)
+    assert want["status"][0] == 2  # w <= W for table 3 -> runtime_error
+
+
+def test_attention_family(capi, orc):
+    """FlashAttention registries: g = n_heads*ceil(s_q/t_q), l = ceil(s_kv/t_kv)
+    (kernel_map.cpp:258-263) -- the oracle evaluates it as dense with t_n=1."""
+    from paper_2604_10187_b200 import synthetic as S
+
+    cfg = S.config_space(False)
+    t = S.synthetic_tables(cfg)
+    reg = dict(family=2, id=cfg["id"], t_m=cfg["t_m"], t_n=cfg["t_n"], t_k=cfg["t_k"])
+    eng = capi.Engine(t, reg, n_sm=148)
+    rng = np.random.default_rng(3)
+    n = 20000
+    sq, heads, skv = rng.integers(1, 32768, n), rng.integers(1, 129, n), rng.integers(1, 65536, n)
+    got = tune_gpu(capi, eng, sq, heads, skv)
+    tiles = {int(i): (int(a), 1, int(c)) for i, a, c in zip(cfg["id"], cfg["t_m"], cfg["t_k"])}
+    want = orc.tune(po.FlatTables(U.pytables_from_arrays(t), tiles), 148, 1, sq, heads, skv)
+    assert_same(got, want)
+
+
+def test_predict_and_nearest_anchor(capi, ref, landscape):
+    L = landscape
+    eng = capi.Engine(L["arrays"], L["registry"], n_sm=132)
+    h = ref.open(L["tab"], L["reg"], 132)
+    rng = np.random.default_rng(2)
+    n = 4000
+    cfgi = rng.integers(0, eng.n_configs, n).astype(np.int32)
+    g = rng.integers(1, 3000, n)
+    l = rng.integers(1, 200, n)
+    lat = torch.empty(n, dtype=torch.float64, device="cuda")
+    wave = torch.empty(n, dtype=torch.int32, device="cuda")
+    ex = torch.empty(n, dtype=torch.int32, device="cuda")
+    st = torch.empty(n, dtype=torch.int32, device="cuda")
+    eng.predict_batch(dev(cfgi), dev(g, torch.int64), dev(l, torch.int64), lat, wave, ex, None, st)
+    torch.cuda.synchronize()
+    # engine configs are in ascending macro_id order; the artefact order may differ
+    order = np.argsort([t.macro_id for t in L["tabs"]], kind="stable")
+    lat, wave, ex = lat.cpu().numpy(), wave.cpu().numpy(), ex.cpu().numpy()
+    for i in range(n):
+        s, v, e, w, _ = ref.predict(h, int(order[cfgi[i]]), int(g[i]), int(l[i]))
+        assert s == 0
+        assert U.bits(np.array([v]))[0] == U.bits(lat[i:i + 1])[0]
+        assert (e, w) == (ex[i], wave[i])
+    ref.close(h)
+    anchors = np.array([16, 32, 48, 64, 80], np.int64)
+    ls = np.arange(0, 120, dtype=np.int64)
+    out = torch.empty(len(ls), dtype=torch.int64, device="cuda")
+    comps = torch.empty(len(ls), dtype=torch.int32, device="cuda")
+    import ctypes as C
+
+    capi.check(capi.lib().wt_nearest_anchor_batch(C.c_void_p(dev(anchors, torch.int64).data_ptr()), 5,
+                                                   C.c_void_p(dev(ls, torch.int64).data_ptr()), C.c_int64(len(ls)),
+                                                   C.c_void_p(out.data_ptr()), C.c_void_p(comps.data_ptr()),
+                                                   C.c_void_p(0)))
+    torch.cuda.synchronize()
+    for i, lv in enumerate(ls):
+        r, c = ref.nearest_anchor(anchors, int(lv))
+        assert (r, c) == (out[i].item(), comps[i].item())
+
+
+def test_sharded_sweep_equals_full(capi, synth256):
+    """Any split of the flattened shape index (the multi-GPU shard unit)
+    fills identical entries."""
+    from paper_2604_10187_b200 import synthetic as S
+
+    cfg, t, reg = synth256
+    eng = capi.Engine(t, reg, n_sm=148)
+    pairs = S.LLAMA3_8B
+    g1 = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 5000)
+    g2 = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 5000)
+    g1.sweep()
+    cuts = [0, 777, 5000, 5001, 12345, g2.n_entries]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        g2.sweep(a, b)
+    torch.cuda.synchronize()
+    assert torch.equal(g1.entries_tensor(), g2.entries_tensor())
