@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark of the WaveTune decision path on B200 (BASELINE.json configs[1]).
+
+Headline workload (config 2): a stream of 10^8 random (M, N, K) online queries
+(Llama-3-8B linear layers, 50% decode M~U[1,256], 50% prefill M~U[257,8192],
+1% off-grid (N, K) ~ U[256, 32768]) answered against prebuilt dual tables of
+256 tile configs (synthetic sampled-latency tables, W=40, 148-SM wave model).
+A step = one pass of wt_gather_batch over all queries resident in HBM
+(on-grid: table gather, off-grid: full Stage-I evaluation).  Under torchrun
+each rank answers its own stream (replicas, weak scaling); time = max over
+ranks of CUDA-event time.
+
+`--impl reference` times the reference's own tune() (compiled verbatim into
+oracle/_ref) on the host cores over a bounded sample of the same stream.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        try:
+            p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                  "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                 stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            return
+        while not self._stop.is_set():
+            line = p.stdout.readline()
+            if not line:
+                break
+            self.rows.append([x.strip() for x in line.split(",")])
+        p.terminate()
+        try:
+            p.wait(timeout=2)
+        except Exception:
+            p.kill()
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        time.sleep(0.25)
+        self._stop.set()
+        self._t.join(timeout=3)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ helpers
+def write_artifacts(cfg, tables, tmpdir, n_micros=4):
+    """The reference's own on-disk formats: registry JSON (kernel_map.cpp:151-
+    231) and tables JSON with %a hex floats (model.cpp:255-302)."""
+    reg = {"version": 1, "family": "dense_gemm", "macros": [], "micros": [], "feasible": []}
+    for i, mid in enumerate(cfg["id"]):
+        reg["macros"].append({"id": int(mid), "t_m": int(cfg["t_m"][i]), "t_n": int(cfg["t_n"][i]),
+                              "t_k": int(cfg["t_k"][i])})
+        for k in range(n_micros):
+            reg["micros"].append({"id": int(mid) * n_micros + k, "n_stages": 2 + k, "n_warps": 4})
+            reg["feasible"].append([int(mid), int(mid) * n_micros + k])
+    t = tables
+    th = t["coeff_theta"].reshape(-1, 4)
+    te = t["theta_ext"].reshape(-1, 4)
+    art = {"schema_version": 1, "kernel_family": "dense_gemm", "tables": []}
+    for i in range(len(t["macro_id"])):
+        co = {str(int(t["coeff_w"][j])): [float(x).hex() for x in th[j]]
+              for j in range(t["coeff_off"][i], t["coeff_off"][i + 1])}
+        an = {}
+        for j in range(t["awave_off"][i], t["awave_off"][i + 1]):
+            an[str(int(t["awave_w"][j]))] = {str(int(t["anchor_l"][q])): int(t["anchor_micro"][q])
+                                             for q in range(t["awave_aoff"][j], t["awave_aoff"][j + 1])}
+        ex = {str(int(t["ext_l"][q])): int(t["ext_micro"][q]) for q in range(t["ext_aoff"][i], t["ext_aoff"][i + 1])}
+        art["tables"].append({"macro_id": int(t["macro_id"][i]), "hardware": "b200", "W": int(t["W"][i]), "p": 10,
+                              "coeffs": co, "theta_ext": [float(x).hex() for x in te[i]], "anchors": an,
+                              "ext_anchors": ex, "diagnostics": {}, "ext_flags": []})
+    rp, tp = os.path.join(tmpdir, "registry.json"), os.path.join(tmpdir, "tables.json")
+    with open(rp, "w") as f:
+        json.dump(reg, f)
+    with open(tp, "w") as f:
+        json.dump(art, f)
+    return rp, tp
+
+
+def reference_rate(M, N, K, cfg, tables, seconds, threads, steps=1, warmup=0):
+    """queries/s of the reference's tune() (oracle/_ref/libwtref.so) on host
+    cores over a sample of the stream sized to ~`seconds` per step."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+
+    ref = po.Reference()
+    with tempfile.TemporaryDirectory() as td:
+        rp, tp = write_artifacts(cfg, tables, td)
+        h = ref.open(tp, rp, 148)
+        cal = min(len(M), 400 * threads)
+        t0 = time.perf_counter()
+        ref.tune(h, M[:cal], N[:cal], K[:cal], nthreads=threads)
+        rate0 = cal / (time.perf_counter() - t0)
+        n = int(min(len(M), max(cal, rate0 * seconds)))
+        for _ in range(warmup):
+            ref.tune(h, M[:cal], N[:cal], K[:cal], nthreads=threads)
+        times = []
+        for s in range(steps):
+            off = (s * n) % max(1, len(M) - n + 1)
+            t0 = time.perf_counter()
+            out = ref.tune(h, M[off:off + n], N[off:off + n], K[off:off + n], nthreads=threads)
+            times.append(time.perf_counter() - t0)
+            assert (out["status"] == 0).all()
+        ref.close(h)
+    return n / max(times), n, times
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------ arms
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2604_10187_b200 import synthetic as S
+
+    cfg = S.config_space(full=False)
+    tables = S.synthetic_tables(cfg)
+    n = min(args.queries, 4_000_000)
+    M, N, K = S.query_stream(n, S.LLAMA3_8B, seed=21)
+    thr = host_threads()
+    rate, sample, times = reference_rate(M, N, K, cfg, tables, args.ref_seconds, thr, steps=args.steps,
+                                         warmup=min(args.warmup, 1))
+    line = {
+        "impl": "reference", "metric": "queries/s", "value": rate, "unit": "queries/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * max(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config2: online queries vs prebuilt Llama-3-8B dual tables (C=256, W=40, 148 SMs)",
+                   "sample_queries_per_step": sample, "parallelism": f"{thr} host threads"},
+        "cpu_baseline": {"value": rate, "unit": "queries/s", "cores": thr, "kind": "reference",
+                         "sample": f"{sample} queries of the config-2 stream per step, reference tune() "
+                                   f"(oracle/_ref, -O2 -ffp-contract=off) on {thr} threads"},
+        "e2e": {"value": rate, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_wavetune(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2604_10187_b200 import capi, synthetic as S
+
+    peaks, peaks_kind = load_peaks()
+    cfg = S.config_space(full=False)
+    tables = S.synthetic_tables(cfg)
+    eng = capi.Engine(tables, S.registry_arrays(cfg), n_sm=148, device=local)
+    pairs = S.LLAMA3_8B
+    grid = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 8192)
+    stream = torch.cuda.current_stream(dev)
+    # table fill (config 1 sweep) -- part of "prebuilt", timed for the record
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(2):
+        grid.sweep(stream=stream)
+    e0.record(stream)
+    grid.sweep(stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    sweep_ms = e0.elapsed_time(e1)
+
+    n = args.queries
+    Mh, Nh, Kh = S.query_stream(n, pairs, seed=21 + rank)
+    Md, Nd, Kd = (torch.from_numpy(x).to(dev) for x in (Mh, Nh, Kh))
+    mac = torch.empty(n, dtype=torch.int32, device=dev)
+    mic = torch.empty(n, dtype=torch.int32, device=dev)
+    lat = torch.empty(n, dtype=torch.float64, device=dev)
+    dec = capi.Engine.decisions(mac, mic, lat)
+
+    def step():
+        grid.gather(Md, Nd, Kd, dec, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    l0 = capi.launch_count()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        ev[0].record(stream)
+        for _ in range(args.steps):
+            step()
+        ev[1].record(stream)
+        torch.cuda.synchronize(dev)
+    launches = capi.launch_count() - l0
+    t_ms = ev[0].elapsed_time(ev[1]) / args.steps
+    if ws > 1:
+        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+        dist.barrier()
+    value = ws * n / (t_ms * 1e-3)
+
+    # dominant kernel (k_gather) alone: the on-grid queries only
+    on = ~((Nh[:, None] == np.array(pairs)[None, :, 0]) & (Kh[:, None] == np.array(pairs)[None, :, 1])).any(1)
+    n_on = int((~on).sum())
+    Mo, No, Ko = (torch.from_numpy(np.ascontiguousarray(x[~on])).to(dev) for x in (Mh, Nh, Kh))
+    d_on = capi.Engine.decisions(mac[:n_on], mic[:n_on], lat[:n_on])
+    for _ in range(2):
+        grid.gather(Mo, No, Ko, d_on, stream=stream)
+    ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    reps = 5
+    ev2[0].record(stream)
+    for _ in range(reps):
+        grid.gather(Mo, No, Ko, d_on, stream=stream)
+    ev2[1].record(stream)
+    torch.cuda.synchronize(dev)
+    gather_ms = ev2[0].elapsed_time(ev2[1]) / reps
+    alg_bytes = 28.0 * n_on  # 12 B (M,N,K) read + 16 B (macro, micro, latency) written per decision
+    achieved = alg_bytes / (gather_ms * 1e-3) / 1e9
+
+    # e2e through the public API with host buffers (pinned), copies inside
+    Mp, Np, Kp = (torch.from_numpy(x).pin_memory() for x in (Mh, Nh, Kh))
+    macp = torch.empty(n, dtype=torch.int32).pin_memory()
+    micp = torch.empty(n, dtype=torch.int32).pin_memory()
+    latp = torch.empty(n, dtype=torch.float64).pin_memory()
+    e2e_steps = max(1, min(args.steps, 3))
+    grid.decide_host(Mp, Np, Kp, macp, micp, latp)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        grid.decide_host(Mp, Np, Kp, macp, micp, latp)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if ws > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    # the host path must reproduce the device-resident answers exactly
+    step()
+    torch.cuda.synchronize(dev)
+    assert torch.equal(macp, mac.cpu()) and torch.equal(latp.view(torch.int64), lat.cpu().view(torch.int64))
+
+    # secondary: config-3 sweep (4608 configs x 6 pairs x M=1..65536) evals/s
+    sec = {}
+    if not args.skip_secondary:
+        cfg3 = S.config_space(full=True)
+        t3 = S.synthetic_tables(cfg3)
+        eng3 = capi.Engine(t3, S.registry_arrays(cfg3), n_sm=148, device=local)
+        p3 = S.unique_pairs(S.LLAMA3_70B, S.QWEN2_72B)
+        g3 = capi.Grid(eng3, [p[0] for p in p3], [p[1] for p in p3], 1, 65536)
+        g3.sweep(stream=stream)
+        e0.record(stream)
+        g3.sweep(stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms3 = e0.elapsed_time(e1)
+        evals3 = g3.n_entries * eng3.n_configs
+        sec = {
+            "config1_sweep": {"ms": sweep_ms, "evals": grid.n_entries * eng.n_configs,
+                              "evals_per_s": grid.n_entries * eng.n_configs / (sweep_ms * 1e-3)},
+            "config3_sweep": {"ms": ms3, "evals": evals3, "evals_per_s": evals3 / (ms3 * 1e-3),
+                              "fp64_flop_per_s": 7.0 * evals3 / (ms3 * 1e-3),
+                              "shapes": g3.n_entries, "configs": eng3.n_configs},
+        }
+        g3.close()
+        eng3.close()
+
+    if rank == 0:
+        cpu = None
+        if ws == 1 and not args.skip_cpu:
+            thr = host_threads()
+            rate, sample, _ = reference_rate(Mh, Nh, Kh, cfg, tables, args.ref_seconds, thr)
+            cpu = {"value": rate, "unit": "queries/s", "cores": thr, "kind": "reference",
+                   "sample": f"{sample} queries of this stream, reference tune() (oracle/_ref) on {thr} threads"}
+        line = {
+            "metric": "queries/s", "value": value, "unit": "queries/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config2: 1e8 online (M,N,K) queries vs prebuilt Llama-3-8B dual tables "
+                                   "(C=256 tile configs, W=40, 148-SM wave model), 1% off-grid",
+                       "queries_per_rank": n, "configs": eng.n_configs, "grid_shapes": grid.n_entries,
+                       "l2": "inputs 1.2 GB/rank > L2 (no flush needed)", "parallelism": f"replicas x{ws}"},
+            "e2e": {"value": ws * n / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": 12 * n,
+                    "d2h_bytes_per_step": 16 * n},
+            "roofline": {"kernel": "k_gather", "bound": "hbm", "achieved": achieved,
+                         "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                         "traffic": None, "peak_kind": peaks_kind,
+                         "alg_bytes_per_launch": alg_bytes, "launch_ms": gather_ms,
+                         "share_of_step": gather_ms / t_ms},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "secondary": sec,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="wavetune", choices=["wavetune", "reference"])
+    ap.add_argument("--queries", type=int, default=100_000_000)
+    ap.add_argument("--ref-seconds", type=float, default=6.0)
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-secondary", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_wavetune(args)
+
+
+if __name__ == "__main__":
+    main()

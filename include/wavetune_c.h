@@ -232,6 +232,15 @@ wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, v
 wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M, const int32_t* N,
                           const int32_t* K, int64_t n, const wt_decisions* out, void* stream);
 
+/* End-to-end convenience over HOST buffers (the call an application makes):
+ * queries M/N/K and the outputs macro/micro/latency live in host memory
+ * (pinned for full overlap).  The batch is cut into chunks of `chunk`
+ * queries and pipelined over two internal streams: H2D copy, gather (grid
+ * != NULL) or full evaluation (grid == NULL), D2H copy.  Synchronous. */
+wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_t* M,
+                              const int32_t* N, const int32_t* K, int64_t n, int32_t* macro_id,
+                              int32_t* micro_id, double* latency_us, int64_t chunk);
+
 /* Kernel launch counter (for bench accounting): total launches issued by
  * this library in this process. */
 int64_t wt_launch_count(void);

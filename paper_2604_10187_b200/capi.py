@@ -85,7 +85,7 @@ EXPORTS = (
     "wt_last_error wt_version wt_abi_version wt_engine_create wt_engine_destroy wt_engine_info_get "
     "wt_engine_config_index wt_tune_batch wt_tune_grouped_batch wt_predict_batch wt_explain "
     "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_destroy wt_grid_storage wt_sweep "
-    "wt_gather_batch wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch").split()
+    "wt_gather_batch wt_decide_host_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch").split()
 
 _lib = None
 
@@ -265,6 +265,12 @@ class Grid:
     def gather(self, M, N, K, out: wt_decisions, stream=None):
         check(lib().wt_gather_batch(self.engine.handle, self.handle, vp(_ptr(M)), vp(_ptr(N)), vp(_ptr(K)),
                                     C.c_int64(M.numel()), C.byref(out), vp(_stream_ptr(stream))))
+
+    def decide_host(self, M, N, K, macro, micro, lat, chunk=1 << 22):
+        """End-to-end over host (pinned) buffers: H2D, gather, D2H, pipelined."""
+        check(lib().wt_decide_host_sync(self.engine.handle, self.handle, vp(_ptr(M)), vp(_ptr(N)), vp(_ptr(K)),
+                                        C.c_int64(M.numel()), vp(_ptr(macro)), vp(_ptr(micro)), vp(_ptr(lat)),
+                                        C.c_int64(chunk)))
 
     def entries_tensor(self):
         """The grid's device storage viewed as an int32 [n_entries, 8] torch tensor (no copy)."""

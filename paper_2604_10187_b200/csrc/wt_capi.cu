@@ -510,6 +510,60 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
     return WT_OK;
 }
 
+wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_t* M,
+                              const int32_t* N, const int32_t* K, int64_t n, int32_t* macro_id,
+                              int32_t* micro_id, double* latency_us, int64_t chunk) {
+    if (!e || !M || !N || !K || !macro_id || !micro_id || !latency_us)
+        return set_err(WT_INVALID_ARGUMENT, "null argument");
+    if (n <= 0) return n == 0 ? WT_OK : set_err(WT_INVALID_ARGUMENT, "negative batch size");
+    if (chunk <= 0) chunk = int64_t(1) << 22;
+    chunk = std::min(chunk, n);
+    DeviceGuard guard(e->device);
+    constexpr int kSlots = 2;
+    cudaStream_t st[kSlots] = {};
+    void* buf[kSlots] = {};
+    const size_t per = size_t(chunk) * (3 * 4 + 4 + 4 + 8);
+    cudaError_t ce = cudaSuccess;
+    for (int s = 0; s < kSlots && ce == cudaSuccess; ++s) {
+        ce = cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking);
+        if (ce == cudaSuccess) ce = cudaMalloc(&buf[s], per);
+    }
+    wt_status rs = WT_OK;
+    for (int64_t i = 0, k = 0; ce == cudaSuccess && rs == WT_OK && i < n; i += chunk, ++k) {
+        const int s = int(k % kSlots);
+        const int64_t m = std::min(chunk, n - i);
+        char* b = static_cast<char*>(buf[s]);
+        int32_t* dM = reinterpret_cast<int32_t*>(b);
+        int32_t* dN = dM + chunk;
+        int32_t* dK = dN + chunk;
+        int32_t* dmac = dK + chunk;
+        int32_t* dmic = dmac + chunk;
+        double* dlat = reinterpret_cast<double*>(dmic + chunk);
+        cudaMemcpyAsync(dM, M + i, size_t(m) * 4, cudaMemcpyHostToDevice, st[s]);
+        cudaMemcpyAsync(dN, N + i, size_t(m) * 4, cudaMemcpyHostToDevice, st[s]);
+        cudaMemcpyAsync(dK, K + i, size_t(m) * 4, cudaMemcpyHostToDevice, st[s]);
+        wt_decisions d{};
+        d.macro_id = dmac;
+        d.micro_id = dmic;
+        d.latency_us = dlat;
+        rs = g ? wt_gather_batch(e, g, dM, dN, dK, m, &d, st[s]) : wt_tune_batch(e, dM, dN, dK, m, &d, st[s]);
+        cudaMemcpyAsync(macro_id + i, dmac, size_t(m) * 4, cudaMemcpyDeviceToHost, st[s]);
+        cudaMemcpyAsync(micro_id + i, dmic, size_t(m) * 4, cudaMemcpyDeviceToHost, st[s]);
+        ce = cudaMemcpyAsync(latency_us + i, dlat, size_t(m) * 8, cudaMemcpyDeviceToHost, st[s]);
+    }
+    for (int s = 0; s < kSlots; ++s) {
+        if (st[s]) {
+            cudaError_t e2 = cudaStreamSynchronize(st[s]);
+            if (ce == cudaSuccess) ce = e2;
+        }
+        if (buf[s]) cudaFree(buf[s]);
+        if (st[s]) cudaStreamDestroy(st[s]);
+    }
+    if (rs != WT_OK) return rs;
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_decide_host_sync");
+    return WT_OK;
+}
+
 // K2 entry points live in wt_fit.cu.
 
 }  // extern "C"

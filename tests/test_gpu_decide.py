@@ -331,8 +331,9 @@ def test_predict_and_nearest_anchor(capi, ref, landscape):
     comps = torch.empty(len(ls), dtype=torch.int32, device="cuda")
     import ctypes as C
 
-    capi.check(capi.lib().wt_nearest_anchor_batch(C.c_void_p(dev(anchors, torch.int64).data_ptr()), 5,
-                                                   C.c_void_p(dev(ls, torch.int64).data_ptr()), C.c_int64(len(ls)),
+    a_d, l_d = dev(anchors, torch.int64), dev(ls, torch.int64)  # keep alive across the launch
+    capi.check(capi.lib().wt_nearest_anchor_batch(C.c_void_p(a_d.data_ptr()), 5,
+                                                   C.c_void_p(l_d.data_ptr()), C.c_int64(len(ls)),
                                                    C.c_void_p(out.data_ptr()), C.c_void_p(comps.data_ptr()),
                                                    C.c_void_p(0)))
     torch.cuda.synchronize()
