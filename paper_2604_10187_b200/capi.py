@@ -285,3 +285,72 @@ class Grid:
             "strides": None,
         }
         return torch.as_tensor(holder, device=f"cuda:{self.engine.device}")
+
+
+def _np_from(ptr, n, dt):
+    if n == 0 or not ptr:
+        return np.zeros(0, dt)
+    ct = {np.int32: C.c_int32, np.int64: C.c_int64, np.float64: C.c_double}[dt]
+    return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ct)), shape=(n,)).copy()
+
+
+def fit_build(records: dict, registry_ids, W: int = 0, p: int = 10, device: int = 0):
+    """build_dual_table on the GPU (K2).  records: dict of numpy arrays
+    g, l (int64), w, macro, micro (int32), lat (float64).  Returns the built
+    tables as CSR numpy arrays (same layout as the engine's input) plus
+    diagnostics and the device time."""
+    keep = []
+
+    def arr(x, dt):
+        a = np.ascontiguousarray(x, dtype=dt)
+        keep.append(a)
+        return a.ctypes.data
+
+    rd = wt_records_desc()
+    rd.n = len(records["g"])
+    rd.g, rd.l = arr(records["g"], np.int64), arr(records["l"], np.int64)
+    rd.w = arr(records["w"], np.int32)
+    rd.macro_id, rd.micro_id = arr(records["macro"], np.int32), arr(records["micro"], np.int32)
+    rd.latency_us = arr(records["lat"], np.float64)
+    ids = np.ascontiguousarray(registry_ids, np.int32)
+    h = C.c_void_p()
+    res = wt_build_result()
+    check(lib().wt_fit_build(C.byref(rd), C.c_void_p(ids.ctypes.data), C.c_int32(len(ids)), C.c_int32(W),
+                             C.c_int32(p), C.c_int(device), C.byref(h), C.byref(res)))
+    nt = res.n_tables
+    co_off = _np_from(res.coeff_off, nt + 1, np.int32)
+    aw_off = _np_from(res.awave_off, nt + 1, np.int32)
+    ex_off = _np_from(res.ext_aoff, nt + 1, np.int32)
+    ncoef, naw, next_ = int(co_off[-1]), int(aw_off[-1]), int(ex_off[-1])
+    aw_aoff = _np_from(res.awave_aoff, naw + 1, np.int32)
+    nan = int(aw_aoff[-1])
+    out = dict(
+        n_tables=nt, W=res.W, p=res.p, device_ms=res.device_ms,
+        macro_id=_np_from(res.macro_id, nt, np.int32), theta_ext=_np_from(res.theta_ext, 4 * nt, np.float64),
+        ext_flags=_np_from(res.ext_flags, nt, np.int32), coeff_off=co_off,
+        coeff_w=_np_from(res.coeff_w, ncoef, np.int32), coeff_theta=_np_from(res.coeff_theta, 4 * ncoef, np.float64),
+        diag_r2=_np_from(res.diag_r2, ncoef, np.float64), diag_mape=_np_from(res.diag_mape, ncoef, np.float64),
+        diag_samples=_np_from(res.diag_samples, ncoef, np.int32),
+        diag_flags=_np_from(res.diag_flags, ncoef, np.int32), awave_off=aw_off,
+        awave_w=_np_from(res.awave_w, naw, np.int32), awave_aoff=aw_aoff,
+        anchor_l=_np_from(res.anchor_l, nan, np.int64), anchor_micro=_np_from(res.anchor_micro, nan, np.int32),
+        anchor_partial=_np_from(res.anchor_partial, nan, np.int32), ext_aoff=ex_off,
+        ext_l=_np_from(res.ext_l, next_, np.int64), ext_micro=_np_from(res.ext_micro, next_, np.int32))
+    out["W_arr"] = np.full(nt, res.W, np.int32)
+    lib().wt_build_free(h)
+    return out
+
+
+def fit_bucket_batch(g, l, t, off, device: int = 0):
+    """fit_bucket for many buckets at once: bucket b = samples [off[b], off[b+1])."""
+    g, l, t = (np.ascontiguousarray(x, np.float64) for x in (g, l, t))
+    off = np.ascontiguousarray(off, np.int64)
+    nb = len(off) - 1
+    co = np.zeros(4 * nb, np.float64)
+    r2 = np.zeros(nb, np.float64)
+    mape = np.zeros(nb, np.float64)
+    dg = np.zeros(nb, np.int32)
+    check(lib().wt_fit_bucket_batch(vp(g.ctypes.data), vp(l.ctypes.data), vp(t.ctypes.data), vp(off.ctypes.data),
+                                    C.c_int64(nb), vp(co.ctypes.data), vp(r2.ctypes.data), vp(mape.ctypes.data),
+                                    vp(dg.ctypes.data), C.c_int(device)))
+    return co.reshape(nb, 4), r2, mape, dg

@@ -60,6 +60,8 @@ int sm_count(int device) {
 
 }  // namespace
 
+void wtb::set_last_error(const std::string& msg) { g_err = msg; }
+
 struct wt_engine {
     int device = 0;
     HostImage host;

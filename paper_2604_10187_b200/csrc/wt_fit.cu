@@ -1,14 +1,1075 @@
-// wt_fit.cu -- K2 batched least-squares / dual-table build (in progress).
+// wt_fit.cu -- K2: build_dual_table on the GPU (model.cpp:194-253).
+//
+// Pipeline over the profile records resident in HBM:
+//   1. registry position of every record (group_records visits registry
+//      macros only, model.cpp:131-136); invalid records dropped (order kept)
+//   2. two stable radix sorts (CUB, LSD over packed field keys):
+//        order A by (macro_pos, w, l, micro, g, record index)
+//        order B by (macro_pos, w, l, g, record index)
+//      record index order is preserved by stability, so the last write of a
+//      duplicated (micro, g) wins exactly like by_micro[micro][g] = t
+//   3. k_select     thread / (macro, w, l) group: select_shared_micro
+//                   (model.cpp:81-120) -- full-coverage argmin of the
+//                   sequential mean, else widest coverage
+//   4. k_samples    selected (g, l, t) samples laid out group after group, so
+//                   every (macro, w) bucket and every extrapolation window is
+//                   one contiguous slice in (w asc, l asc, g asc) order
+//   5. k_fit        warp / bucket: column-scaled ColPivHouseholderQR +
+//                   reduced HouseholderQR, R^2, MAPE (model.cpp:20-77)
+//   6. k_extrap     warp / macro: fit_extrapolation (model.cpp:140-192)
+// The QR reproduces oracle/wt_fit_core.h's operation order exactly: every
+// reduction is lane-strided accumulation (lane j owns rows j, j+32, ...) then
+// a xor-butterfly, all binary64 _rn arithmetic, correctly rounded sqrt/div.
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+#include <cstring>
+#include <string>
+#include <vector>
+
 #include "wavetune_c.h"
+#include "wt_internal.h"
+
+namespace wtb {
+namespace fit {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// ------------------------------------------------------------ warp algebra
+__device__ __forceinline__ double butterfly(double p) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) p = __dadd_rn(p, __shfl_xor_sync(FULL, p, off));
+    return p;
+}
+
+// sum over rows [r0, n) of a[r]*b[r] (b == nullptr: of a[r])
+__device__ __forceinline__ double wdot(const double* a, const double* b, int r0, int n, int lane) {
+    double p = 0.0;
+    for (int r = r0 + ((lane - r0) & 31); r < n; r += 32) p = __dadd_rn(p, b ? __dmul_rn(a[r], b[r]) : a[r]);
+    return butterfly(p);
+}
+
+__device__ __forceinline__ double wmaxabs(const double* a, int n, int lane) {
+    double m = -1.0;
+    for (int r = lane; r < n; r += 32) m = fmax(m, fabs(a[r]));
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, off));
+    return m;
+}
+
+// Householder reflector on col[k..n) (makeHouseholderInPlace).
+__device__ double whouse(double* col, int k, int n, double* beta, int lane) {
+    const double c0 = col[k];
+    const double tailsq = (n - k == 1) ? 0.0 : wdot(col, col, k + 1, n, lane);
+    __syncwarp();
+    if (tailsq <= DBL_MIN) {
+        *beta = c0;
+        for (int r = k + 1 + lane; r < n; r += 32) col[r] = 0.0;
+        __syncwarp();
+        return 0.0;
+    }
+    double b = __dsqrt_rn(__dadd_rn(__dmul_rn(c0, c0), tailsq));
+    if (c0 >= 0.0) b = -b;
+    const double d = __dadd_rn(c0, -b);
+    for (int r = k + 1 + lane; r < n; r += 32) col[r] = __ddiv_rn(col[r], d);
+    __syncwarp();
+    *beta = b;
+    return __ddiv_rn(__dadd_rn(b, -c0), b);
+}
+
+// y[k..n) -= tau * v * (v . y[k..n)), v = [1; ess[k+1..n)] (applyHouseholderOnTheLeft)
+__device__ void wapply(const double* ess, double tau, double* y, int k, int n, int lane) {
+    if (n - k == 1) {
+        __syncwarp();
+        if (lane == 0) y[k] = __dmul_rn(y[k], __dadd_rn(1.0, -tau));
+        __syncwarp();
+        return;
+    }
+    if (tau == 0.0) return;
+    double tmp = wdot(ess, y, k + 1, n, lane);
+    tmp = __dadd_rn(tmp, y[k]);
+    __syncwarp();
+    if (lane == 0) y[k] = __dadd_rn(y[k], -__dmul_rn(tau, tmp));
+    for (int r = k + 1 + lane; r < n; r += 32) y[r] = __dadd_rn(y[r], -__dmul_rn(__dmul_rn(tau, ess[r]), tmp));
+    __syncwarp();
+}
+
+// upper back-substitution on c[0..m) (single-panel triangular_solve_vector)
+__device__ void wbacksolve(const double* A, int n, int m, double* c, int lane) {
+    __syncwarp();
+    if (lane == 0) {
+        for (int i = m - 1; i >= 0; --i) {
+            if (c[i] != 0.0) {
+                c[i] = __ddiv_rn(c[i], A[size_t(i) * n + i]);
+                for (int j = 0; j < i; ++j) c[j] = __dadd_rn(c[j], -__dmul_rn(c[i], A[size_t(i) * n + j]));
+            }
+        }
+    }
+    __syncwarp();
+}
+
+struct FitOut {
+    double c[4];
+    double r2, mape;
+    int degenerate;
+};
+
+// fit_bucket on samples (g, l, t)[0..n) with scratch of 18*n doubles.
+__device__ FitOut warp_fit(const double* g, const double* l, const double* t, int n, double* scr, int lane) {
+    double* D = scr;            // design, 4 columns
+    double* Sc = D + 4 * size_t(n);   // scaled design (kept for the reduced fit)
+    double* A = Sc + 4 * size_t(n);   // QR workspace
+    double* Sub = A + 4 * size_t(n);  // reduced-fit columns
+    double* Wk = Sub + 4 * size_t(n);
+    double* F = Wk + size_t(n);
+    for (int r = lane; r < n; r += 32) {
+        D[r] = __dmul_rn(g[r], l[r]);
+        D[n + r] = g[r];
+        D[2 * size_t(n) + r] = l[r];
+        D[3 * size_t(n) + r] = 1.0;
+    }
+    __syncwarp();
+    double scale[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const double m = wmaxabs(D + size_t(c) * n, n, lane);
+        scale[c] = (m > 0) ? m : 1.0;
+        for (int r = lane; r < n; r += 32) {
+            const double v = __ddiv_rn(D[size_t(c) * n + r], scale[c]);
+            Sc[size_t(c) * n + r] = v;
+            A[size_t(c) * n + r] = v;
+        }
+    }
+    __syncwarp();
+    // ---- ColPivHouseholderQR
+    const int size = n < 4 ? n : 4;
+    double upd[4], direct[4], tau[4];
+    int trans[4], perm[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        direct[c] = __dsqrt_rn(wdot(A + size_t(c) * n, A + size_t(c) * n, 0, n, lane));
+        upd[c] = direct[c];
+    }
+    double mx = upd[0];
+#pragma unroll
+    for (int c = 1; c < 4; ++c)
+        if (upd[c] > mx) mx = upd[c];
+    const double th_help = __ddiv_rn(__dmul_rn(__dmul_rn(mx, DBL_EPSILON), __dmul_rn(mx, DBL_EPSILON)), double(n));
+    const double downdate_th = __dsqrt_rn(DBL_EPSILON);
+    int nz = size;
+    double maxpiv = 0.0;
+    for (int k = 0; k < size; ++k) {
+        int big = k;
+        double bigv = upd[k];
+        for (int c = k + 1; c < 4; ++c)
+            if (upd[c] > bigv) {
+                bigv = upd[c];
+                big = c;
+            }
+        const double big_sq = __dmul_rn(bigv, bigv);
+        if (nz == size && big_sq < __dmul_rn(th_help, double(n - k))) nz = k;
+        trans[k] = big;
+        if (big != k) {
+            double* ck = A + size_t(k) * n;
+            double* cb = A + size_t(big) * n;
+            for (int r = lane; r < n; r += 32) {
+                const double tv = ck[r];
+                ck[r] = cb[r];
+                cb[r] = tv;
+            }
+            __syncwarp();
+            double tv = upd[k];
+            upd[k] = upd[big];
+            upd[big] = tv;
+            tv = direct[k];
+            direct[k] = direct[big];
+            direct[big] = tv;
+        }
+        double* colk = A + size_t(k) * n;
+        double beta;
+        tau[k] = whouse(colk, k, n, &beta, lane);
+        if (lane == 0) colk[k] = beta;
+        __syncwarp();
+        if (fabs(beta) > maxpiv) maxpiv = fabs(beta);
+        for (int j = k + 1; j < 4; ++j) wapply(colk, tau[k], A + size_t(j) * n, k, n, lane);
+        for (int j = k + 1; j < 4; ++j) {
+            if (upd[j] != 0.0) {
+                double tq = __ddiv_rn(fabs(A[size_t(j) * n + k]), upd[j]);
+                tq = __dmul_rn(__dadd_rn(1.0, tq), __dadd_rn(1.0, -tq));
+                if (tq < 0.0) tq = 0.0;
+                const double ratio = __ddiv_rn(upd[j], direct[j]);
+                const double t2 = __dmul_rn(tq, __dmul_rn(ratio, ratio));
+                if (t2 <= downdate_th) {
+                    direct[j] = __dsqrt_rn(wdot(A + size_t(j) * n, A + size_t(j) * n, k + 1, n, lane));
+                    upd[j] = direct[j];
+                } else {
+                    upd[j] = __dmul_rn(upd[j], __dsqrt_rn(tq));
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) perm[c] = c;
+    for (int k = 0; k < size; ++k) {
+        const int tv = perm[k];
+        perm[k] = perm[trans[k]];
+        perm[trans[k]] = tv;
+    }
+    const double pre = __dmul_rn(fabs(maxpiv), 1e-10);
+    int rank = 0;
+    for (int i = 0; i < nz; ++i) rank += fabs(A[size_t(i) * n + i]) > pre;
+
+    FitOut o;
+    double x[4] = {0.0, 0.0, 0.0, 0.0};
+    o.degenerate = 0;
+    if (rank >= 4 && n >= 4) {
+        for (int r = lane; r < n; r += 32) Wk[r] = t[r];
+        __syncwarp();
+        for (int k = 0; k < nz; ++k) wapply(A + size_t(k) * n, tau[k], Wk, k, n, lane);
+        wbacksolve(A, n, nz, Wk, lane);
+        for (int i = 0; i < nz; ++i) x[perm[i]] = Wk[i];
+    } else {
+        o.degenerate = 1;
+        int keep = rank < n ? rank : n;
+        if (keep < 1) keep = 1;
+        for (int c = 0; c < keep; ++c)
+            for (int r = lane; r < n; r += 32) Sub[size_t(c) * n + r] = Sc[size_t(perm[c]) * n + r];
+        __syncwarp();
+        const int hs = n < keep ? n : keep;
+        double ht[4];
+        for (int k = 0; k < hs; ++k) {
+            double* colk = Sub + size_t(k) * n;
+            double beta;
+            ht[k] = whouse(colk, k, n, &beta, lane);
+            if (lane == 0) colk[k] = beta;
+            __syncwarp();
+            for (int j = k + 1; j < keep; ++j) wapply(colk, ht[k], Sub + size_t(j) * n, k, n, lane);
+        }
+        for (int r = lane; r < n; r += 32) Wk[r] = t[r];
+        __syncwarp();
+        for (int k = 0; k < hs; ++k) wapply(Sub + size_t(k) * n, ht[k], Wk, k, n, lane);
+        wbacksolve(Sub, n, hs, Wk, lane);
+        for (int c = 0; c < hs; ++c) x[perm[c]] = Wk[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        x[c] = __ddiv_rn(x[c], scale[c]);
+        o.c[c] = x[c];
+    }
+    // residuals (model.cpp:64-75)
+    for (int r = lane; r < n; r += 32) {
+        double acc = __dmul_rn(D[r], x[0]);
+        acc = __dadd_rn(acc, __dmul_rn(D[n + r], x[1]));
+        acc = __dadd_rn(acc, __dmul_rn(D[2 * size_t(n) + r], x[2]));
+        acc = __dadd_rn(acc, __dmul_rn(D[3 * size_t(n) + r], x[3]));
+        F[r] = acc;
+        const double d = __dadd_rn(t[r], -acc);
+        Wk[r] = __dmul_rn(d, d);
+    }
+    __syncwarp();
+    const double ss_res = wdot(Wk, nullptr, 0, n, lane);
+    const double mean = __ddiv_rn(wdot(t, nullptr, 0, n, lane), double(n));
+    __syncwarp();
+    for (int r = lane; r < n; r += 32) {
+        const double d = __dadd_rn(t[r], -mean);
+        Wk[r] = __dmul_rn(d, d);
+    }
+    __syncwarp();
+    const double ss_tot = wdot(Wk, nullptr, 0, n, lane);
+    o.r2 = ss_tot > 0 ? __dadd_rn(1.0, -__ddiv_rn(ss_res, ss_tot)) : (ss_res < 1e-18 ? 1.0 : 0.0);
+    double mp = 0.0;
+    if (lane == 0)
+        for (int r = 0; r < n; ++r) mp = __dadd_rn(mp, __ddiv_rn(fabs(__dadd_rn(t[r], -F[r])), fabs(t[r])));
+    mp = __shfl_sync(FULL, mp, 0);
+    o.mape = __ddiv_rn(mp, double(n));
+    __syncwarp();
+    return o;
+}
+
+// --------------------------------------------------------- build pipeline
+struct Rec {
+    const int64_t* g;
+    const int64_t* l;
+    const int32_t* w;
+    const int32_t* macro;
+    const int32_t* micro;
+    const double* lat;
+};
+
+__global__ void k_mpos(Rec rc, int64_t n, const int32_t* ids_sorted, const int32_t* pos_sorted, int nm,
+                       int32_t* mpos, int32_t* valid) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t id = rc.macro[i];
+    int lo = 0, hi = nm;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ids_sorted[mid] < id)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    const bool ok = lo < nm && ids_sorted[lo] == id;
+    mpos[i] = ok ? pos_sorted[lo] : INT_MAX;
+    valid[i] = ok ? 1 : 0;
+}
+
+struct Ranges {
+    unsigned long long gmin, gmax, lmin, lmax;
+    int wmin, wmax, umin, umax;
+};
+
+__global__ void k_ranges(Rec rc, const int64_t* idx, int64_t n, Ranges* out) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t r = idx[i];
+    // offsets by 2^63 make signed order unsigned
+    const unsigned long long g = (unsigned long long)rc.g[r] ^ 0x8000000000000000ULL;
+    const unsigned long long l = (unsigned long long)rc.l[r] ^ 0x8000000000000000ULL;
+    atomicMin(&out->gmin, g);
+    atomicMax(&out->gmax, g);
+    atomicMin(&out->lmin, l);
+    atomicMax(&out->lmax, l);
+    atomicMin(&out->wmin, rc.w[r]);
+    atomicMax(&out->wmax, rc.w[r]);
+    atomicMin(&out->umin, rc.micro[r]);
+    atomicMax(&out->umax, rc.micro[r]);
+}
+
+// One key field: value - base, `bits` wide, placed at `shift`.
+struct Field {
+    int which;  // 0 g, 1 micro, 2 l, 3 w, 4 mpos
+    unsigned long long base;
+    int bits, shift;
+};
+struct Pass {
+    Field f[5];
+    int nf, bits;
+};
+
+__global__ void k_pack(Rec rc, const int32_t* mpos, const int64_t* perm, int64_t n, Pass ps,
+                       unsigned long long* key) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t r = perm[i];
+    unsigned long long k = 0;
+    for (int q = 0; q < ps.nf; ++q) {
+        const Field& f = ps.f[q];
+        unsigned long long v;
+        switch (f.which) {
+            case 0: v = ((unsigned long long)rc.g[r] ^ 0x8000000000000000ULL) - f.base; break;
+            case 1: v = (unsigned long long)(long long)(rc.micro[r]) - f.base; break;
+            case 2: v = ((unsigned long long)rc.l[r] ^ 0x8000000000000000ULL) - f.base; break;
+            case 3: v = (unsigned long long)(long long)(rc.w[r]) - f.base; break;
+            default: v = (unsigned long long)mpos[r]; break;
+        }
+        k |= v << f.shift;
+    }
+    key[i] = k;
+}
+
+__device__ __forceinline__ bool same_group(const Rec& rc, const int32_t* mpos, int64_t a, int64_t b) {
+    return mpos[a] == mpos[b] && rc.w[a] == rc.w[b] && rc.l[a] == rc.l[b];
+}
+
+__global__ void k_group_flags(Rec rc, const int32_t* mpos, const int64_t* ordA, int64_t n, int32_t* gflag) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    gflag[i] = (i == 0 || !same_group(rc, mpos, ordA[i], ordA[i - 1])) ? 1 : 0;
+}
+
+__global__ void k_group_starts(const int32_t* gflag, const int32_t* gid, int64_t n, int64_t* gstart) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (gflag[i]) gstart[gid[i]] = i;
+}
+
+struct Groups {
+    const int64_t* start;  // [G+1]
+    int32_t* micro;
+    int32_t* partial;
+    int64_t* sel_lo;
+    int64_t* sel_hi;
+    int32_t* nsamp;
+};
+
+// select_shared_micro (model.cpp:81-120) on group q = [start[q], start[q+1])
+__global__ void k_select(Rec rc, const int64_t* ordA, const int64_t* ordB, int64_t G, Groups gr) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= G) return;
+    const int64_t s = gr.start[q], e = gr.start[q + 1];
+    int32_t n_g = 0;  // |all_g|
+    for (int64_t i = s; i < e; ++i)
+        if (i == s || rc.g[ordB[i]] != rc.g[ordB[i - 1]]) ++n_g;
+    int32_t best_micro = -1, best_cover = 0, part = 0;
+    int64_t blo = s, bhi = s;
+    for (int pass = 0; pass < 2 && best_micro < 0; ++pass) {
+        const bool full = pass == 0;
+        double best_mean = 0.0;
+        for (int64_t i = s; i < e;) {
+            const int32_t mu = rc.micro[ordA[i]];
+            int64_t j = i;
+            while (j < e && rc.micro[ordA[j]] == mu) ++j;
+            int32_t cover = 0;
+            double mean = 0.0;
+            for (int64_t k = i; k < j; ++k)
+                if (k + 1 == j || rc.g[ordA[k + 1]] != rc.g[ordA[k]]) {  // last write of this g
+                    mean = __dadd_rn(mean, rc.lat[ordA[k]]);
+                    ++cover;
+                }
+            mean = __ddiv_rn(mean, double(cover));
+            if (!(full && cover != n_g)) {
+                const bool better = best_micro < 0 || (full ? mean < best_mean : cover > best_cover);
+                if (better) {
+                    best_micro = mu;
+                    best_mean = mean;
+                    best_cover = cover;
+                    blo = i;
+                    bhi = j;
+                }
+            }
+            i = j;
+        }
+        part = full ? 0 : 1;
+    }
+    gr.micro[q] = best_micro;
+    gr.partial[q] = part;
+    gr.sel_lo[q] = blo;
+    gr.sel_hi[q] = bhi;
+    gr.nsamp[q] = best_cover;
+}
+
+__global__ void k_samples(Rec rc, const int64_t* ordA, int64_t G, Groups gr, const int64_t* soff, double* sg,
+                          double* sl, double* st) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= G) return;
+    int64_t o = soff[q];
+    const int64_t lo = gr.sel_lo[q], hi = gr.sel_hi[q];
+    for (int64_t k = lo; k < hi; ++k)
+        if (k + 1 == hi || rc.g[ordA[k + 1]] != rc.g[ordA[k]]) {
+            const int64_t r = ordA[k];
+            sg[o] = double(rc.g[r]);
+            sl[o] = double(rc.l[r]);
+            st[o] = rc.lat[r];
+            ++o;
+        }
+}
+
+struct Buckets {
+    int64_t nb;
+    const int64_t* slo;  // sample range per bucket
+    const int64_t* shi;
+    double* coeff;       // [nb*4]
+    double* r2;
+    double* mape;
+    int32_t* degen;
+};
+
+__global__ void k_fit(const double* sg, const double* sl, const double* st, Buckets b, double* scratch) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t q = warp; q < b.nb; q += nw) {
+        const int64_t lo = b.slo[q], n = b.shi[q] - lo;
+        if (n <= 0) continue;
+        FitOut o = warp_fit(sg + lo, sl + lo, st + lo, int(n), scratch + 18 * lo, lane);
+        if (lane == 0) {
+            for (int c = 0; c < 4; ++c) b.coeff[4 * q + c] = o.c[c];
+            b.r2[q] = o.r2;
+            b.mape[q] = o.mape;
+            b.degen[q] = o.degenerate;
+        }
+    }
+}
+
+struct Macros {
+    int64_t nmac;
+    const int64_t* bstart;  // [nmac+1] bucket range per macro
+    const int64_t* bw;      // wave of each bucket
+    const int64_t* gstart_of_bucket;  // [nb+1] group range per bucket
+    int32_t W, p;
+    double* theta;          // [nmac*4]
+    int32_t* flags;
+    int32_t* next;          // ext anchor count per macro
+    int64_t* el;            // [G] ext anchors, slice at the macro's first group
+    int32_t* em;
+};
+
+__global__ void k_extrap(Rec rc, const double* sg, const double* sl, const double* st, Buckets b,
+                         const int64_t* slo_group, Groups gr, const int64_t* ordA, Macros m, double* scratch) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t q = warp; q < m.nmac; q += nw) {
+        const int64_t b0 = m.bstart[q], b1 = m.bstart[q + 1];
+        const int w_lo = max(1, m.W - m.p + 1);
+        int64_t wb0 = -1, wb1 = -1;
+        int used = 0;
+        for (int64_t k = b0; k < b1; ++k)
+            if (m.bw[k] >= w_lo && m.bw[k] <= m.W) {
+                if (wb0 < 0) wb0 = k;
+                wb1 = k + 1;
+                ++used;
+            }
+        const int64_t gslice = m.gstart_of_bucket[b0];  // ext anchors slice for this macro
+        if (used >= 2) {
+            const int64_t lo = b.slo[wb0], n = b.shi[wb1 - 1] - lo;
+            FitOut o = warp_fit(sg + lo, sl + lo, st + lo, int(n), scratch + 18 * lo, lane);
+            if (lane == 0) {
+                for (int c = 0; c < 4; ++c) m.theta[4 * q + c] = o.c[c];
+                m.flags[q] = o.degenerate ? 1 : 0;
+                // majority vote per l over window groups, ties -> smaller micro
+                const int64_t g0 = m.gstart_of_bucket[wb0], g1 = m.gstart_of_bucket[wb1];
+                int cnt = 0;
+                int64_t prev_l = 0;
+                bool have_prev = false;
+                for (;;) {  // distinct l ascending
+                    bool found = false;
+                    int64_t lv = 0;
+                    for (int64_t k = g0; k < g1; ++k) {
+                        const int64_t gl = rc.l[ordA[gr.start[k]]];
+                        if ((!have_prev || gl > prev_l) && (!found || gl < lv)) {
+                            lv = gl;
+                            found = true;
+                        }
+                    }
+                    if (!found) break;
+                    int32_t best_micro = -1, best_count = -1, cur = INT_MIN;
+                    for (;;) {
+                        int32_t nxt = INT_MAX;
+                        for (int64_t k = g0; k < g1; ++k) {
+                            const int64_t gl = rc.l[ordA[gr.start[k]]];
+                            if (gl == lv && gr.micro[k] > cur && gr.micro[k] < nxt) nxt = gr.micro[k];
+                        }
+                        if (nxt == INT_MAX) break;
+                        int32_t c = 0;
+                        for (int64_t k = g0; k < g1; ++k)
+                            if (rc.l[ordA[gr.start[k]]] == lv && gr.micro[k] == nxt) ++c;
+                        if (c > best_count) {
+                            best_count = c;
+                            best_micro = nxt;
+                        }
+                        cur = nxt;
+                    }
+                    m.el[gslice + cnt] = lv;
+                    m.em[gslice + cnt] = best_micro;
+                    ++cnt;
+                    prev_l = lv;
+                    have_prev = true;
+                }
+                m.next[q] = cnt;
+            }
+        } else if (lane == 0) {
+            // fewer than two window waves: the highest wave's fit and anchors
+            const int64_t top = b1 - 1;
+            for (int c = 0; c < 4; ++c) m.theta[4 * q + c] = b.coeff[4 * top + c];
+            m.flags[q] = 2;
+            const int64_t g0 = m.gstart_of_bucket[top], g1 = m.gstart_of_bucket[top + 1];
+            int cnt = 0;
+            for (int64_t k = g0; k < g1; ++k) {
+                m.el[gslice + cnt] = rc.l[ordA[gr.start[k]]];
+                m.em[gslice + cnt] = gr.micro[k];
+                ++cnt;
+            }
+            m.next[q] = cnt;
+        }
+        __syncwarp();
+    }
+    (void)slo_group;
+}
+
+}  // namespace fit
+}  // namespace wtb
+
+// ------------------------------------------------------------------ C-ABI
+using namespace wtb::fit;
+
+namespace {
+// errors surface through wt_last_error() (wt_capi.cu)
+struct FitErr {
+    FitErr& operator=(const std::string& m) {
+        wtb::set_last_error(m);
+        return *this;
+    }
+    FitErr& operator=(const char* m) {
+        wtb::set_last_error(m);
+        return *this;
+    }
+} g_fit_err;
+}
+
+struct wt_build {
+    std::vector<int32_t> macro_id, ext_flags, coeff_off, coeff_w, diag_samples, diag_flags, awave_off, awave_w,
+        awave_aoff, anchor_micro, anchor_partial, ext_aoff, ext_micro;
+    std::vector<double> theta_ext, coeff_theta, diag_r2, diag_mape;
+    std::vector<int64_t> anchor_l, ext_l;
+};
+
+
+#define CK(x)                                                                          \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess) {                                                       \
+            g_fit_err = std::string(#x) + ": " + cudaGetErrorString(e_);              \
+            return WT_CUDA_ERROR;                                                      \
+        }                                                                              \
+    } while (0)
+
+namespace {
+
+template <typename T>
+T* dalloc(std::vector<void*>& owned, size_t n) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) return nullptr;
+    owned.push_back(p);
+    return static_cast<T*>(p);
+}
+
+int bits_for(unsigned long long range) {
+    int b = 0;
+    while (b < 64 && (range >> b) != 0) ++b;
+    return b;
+}
+
+// Plan LSD passes over fields (least significant first), packing greedily.
+std::vector<Pass> plan_passes(const std::vector<Field>& fields) {
+    std::vector<Pass> out;
+    Pass cur{};
+    cur.nf = 0;
+    cur.bits = 0;
+    for (const Field& f0 : fields) {
+        Field f = f0;
+        if (cur.bits + f.bits > 64 && cur.nf > 0) {
+            out.push_back(cur);
+            cur = Pass{};
+        }
+        f.shift = cur.bits;
+        cur.f[cur.nf++] = f;
+        cur.bits += f.bits;
+    }
+    if (cur.nf > 0) out.push_back(cur);
+    return out;
+}
+
+wt_status run_sort(const Rec& rc, const int32_t* mpos, int64_t* perm, int64_t* perm_alt, int64_t n,
+                   const std::vector<Pass>& passes, unsigned long long* keys, unsigned long long* keys_alt,
+                   void*& tmp, size_t& tmp_bytes, cudaStream_t s) {
+    for (const Pass& ps : passes) {
+        const int blocks = int((n + 255) / 256);
+        k_pack<<<blocks, 256, 0, s>>>(rc, mpos, perm, n, ps, keys);
+        size_t need = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, need, keys, keys_alt, perm, perm_alt, n, 0,
+                                        std::max(1, ps.bits), s);
+        if (need > tmp_bytes) {
+            if (tmp) cudaFreeAsync(tmp, s);
+            CK(cudaMallocAsync(&tmp, need, s));
+            tmp_bytes = need;
+        }
+        CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_alt, perm, perm_alt, n, 0,
+                                           std::max(1, ps.bits), s));
+        CK(cudaMemcpyAsync(perm, perm_alt, size_t(n) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    }
+    return WT_OK;
+}
+
+}  // namespace
 
 extern "C" {
-wt_status wt_fit_build(const wt_records_desc*, const int32_t*, int32_t, int32_t, int32_t, int,
-                       wt_build**, wt_build_result*) {
-    return WT_UNSUPPORTED;
+
+wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_ids, int32_t n_macros,
+                       int32_t W, int32_t p, int device, wt_build** out, wt_build_result* result) {
+    if (!records || !out || !result || (n_macros > 0 && !registry_ids)) {
+        g_fit_err = "null argument";
+        return WT_INVALID_ARGUMENT;
+    }
+    *out = nullptr;
+    const int64_t n_all = records->n;
+    if (n_all <= 0) {
+        g_fit_err = "build_dual_table: empty record set";
+        return WT_INVALID_ARGUMENT;
+    }
+    int prev_dev = 0;
+    cudaGetDevice(&prev_dev);
+    cudaSetDevice(device);
+    struct Restore {
+        int d;
+        ~Restore() { cudaSetDevice(d); }
+    } restore{prev_dev};
+    std::vector<void*> owned;
+    struct Free {
+        std::vector<void*>* v;
+        ~Free() {
+            for (void* q : *v) cudaFree(q);
+        }
+    } freer{&owned};
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct SD {
+        cudaStream_t s;
+        ~SD() { cudaStreamDestroy(s); }
+    } sd{s};
+
+    // W = params.W or the highest wave in the data (model.cpp:201-203)
+    if (W <= 0)
+        for (int64_t i = 0; i < n_all; ++i) W = std::max(W, records->w[i]);
+
+    // upload records
+    Rec rc{};
+    int64_t* dg = dalloc<int64_t>(owned, n_all);
+    int64_t* dl = dalloc<int64_t>(owned, n_all);
+    int32_t* dw = dalloc<int32_t>(owned, n_all);
+    int32_t* dma = dalloc<int32_t>(owned, n_all);
+    int32_t* dmi = dalloc<int32_t>(owned, n_all);
+    double* dt = dalloc<double>(owned, n_all);
+    if (!dg || !dl || !dw || !dma || !dmi || !dt) {
+        g_fit_err = "cudaMalloc failed";
+        return WT_CUDA_ERROR;
+    }
+    CK(cudaMemcpyAsync(dg, records->g, n_all * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dl, records->l, n_all * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dw, records->w, n_all * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dma, records->macro_id, n_all * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dmi, records->micro_id, n_all * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dt, records->latency_us, n_all * 8, cudaMemcpyHostToDevice, s));
+    rc.g = dg;
+    rc.l = dl;
+    rc.w = dw;
+    rc.macro = dma;
+    rc.micro = dmi;
+    rc.lat = dt;
+
+    cudaEvent_t ev0, ev1;
+    cudaEventCreate(&ev0);
+    cudaEventCreate(&ev1);
+    CK(cudaEventRecord(ev0, s));
+
+    // 1. registry positions (first occurrence of a duplicated id wins)
+    std::vector<std::pair<int32_t, int32_t>> ids;
+    for (int32_t i = 0; i < n_macros; ++i) ids.push_back({registry_ids[i], i});
+    std::stable_sort(ids.begin(), ids.end(), [](auto& a, auto& b) { return a.first < b.first; });
+    ids.erase(std::unique(ids.begin(), ids.end(), [](auto& a, auto& b) { return a.first == b.first; }), ids.end());
+    std::vector<int32_t> hid, hpos;
+    for (auto& x : ids) {
+        hid.push_back(x.first);
+        hpos.push_back(x.second);
+    }
+    int32_t* did = dalloc<int32_t>(owned, hid.size());
+    int32_t* dpos = dalloc<int32_t>(owned, hid.size());
+    CK(cudaMemcpyAsync(did, hid.data(), hid.size() * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dpos, hpos.data(), hpos.size() * 4, cudaMemcpyHostToDevice, s));
+    int32_t* mpos = dalloc<int32_t>(owned, n_all);
+    int32_t* valid = dalloc<int32_t>(owned, n_all);
+    const int blocks_all = int((n_all + 255) / 256);
+    k_mpos<<<blocks_all, 256, 0, s>>>(rc, n_all, did, dpos, int(hid.size()), mpos, valid);
+    // compact valid record indices, order preserved
+    int64_t* idx = dalloc<int64_t>(owned, n_all);
+    int64_t* idx2 = dalloc<int64_t>(owned, n_all);
+    int64_t* nvalid_d = dalloc<int64_t>(owned, 1);
+    {
+        cub::CountingInputIterator<int64_t> it(0);
+        size_t need = 0;
+        cub::DeviceSelect::Flagged(nullptr, need, it, valid, idx, nvalid_d, n_all, s);
+        void* t = nullptr;
+        CK(cudaMallocAsync(&t, need, s));
+        CK(cub::DeviceSelect::Flagged(t, need, it, valid, idx, nvalid_d, n_all, s));
+        cudaFreeAsync(t, s);
+    }
+    int64_t n = 0;
+    CK(cudaMemcpyAsync(&n, nvalid_d, 8, cudaMemcpyDeviceToHost, s));
+    Ranges* dr = dalloc<Ranges>(owned, 1);
+    Ranges init{~0ULL, 0ULL, ~0ULL, 0ULL, INT_MAX, INT_MIN, INT_MAX, INT_MIN};
+    CK(cudaStreamSynchronize(s));
+    if (n == 0) {
+        g_fit_err = "build_dual_table: no macro produced a table";
+        return WT_RUNTIME_ERROR;
+    }
+    CK(cudaMemcpyAsync(dr, &init, sizeof(Ranges), cudaMemcpyHostToDevice, s));
+    k_ranges<<<int((n + 255) / 256), 256, 0, s>>>(rc, idx, n, dr);
+    Ranges hr;
+    CK(cudaMemcpyAsync(&hr, dr, sizeof(Ranges), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+
+    const int bits_g = bits_for(hr.gmax - hr.gmin), bits_l = bits_for(hr.lmax - hr.lmin);
+    const int bits_w = bits_for((unsigned long long)((long long)hr.wmax - hr.wmin));
+    const int bits_u = bits_for((unsigned long long)((long long)hr.umax - hr.umin));
+    const int bits_m = bits_for((unsigned long long)std::max(1, n_macros));
+    Field fg{0, hr.gmin, bits_g, 0}, fu{1, (unsigned long long)(long long)hr.umin, bits_u, 0},
+        fl{2, hr.lmin, bits_l, 0}, fw{3, (unsigned long long)(long long)hr.wmin, bits_w, 0},
+        fm{4, 0, bits_m, 0};
+    auto passA = plan_passes({fg, fu, fl, fw, fm});
+    auto passB = plan_passes({fg, fl, fw, fm});
+
+    // 2. stable sorts
+    int64_t* ordA = dalloc<int64_t>(owned, n);
+    int64_t* ordB = dalloc<int64_t>(owned, n);
+    int64_t* alt = dalloc<int64_t>(owned, n);
+    unsigned long long* keys = dalloc<unsigned long long>(owned, n);
+    unsigned long long* keys2 = dalloc<unsigned long long>(owned, n);
+    CK(cudaMemcpyAsync(ordA, idx, n * 8, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(ordB, idx, n * 8, cudaMemcpyDeviceToDevice, s));
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    wt_status st = run_sort(rc, mpos, ordA, alt, n, passA, keys, keys2, tmp, tmp_bytes, s);
+    if (st) return st;
+    st = run_sort(rc, mpos, ordB, alt, n, passB, keys, keys2, tmp, tmp_bytes, s);
+    if (st) return st;
+    if (tmp) cudaFreeAsync(tmp, s);
+
+    // 3. groups
+    const int blocks = int((n + 255) / 256);
+    int32_t* gflag = dalloc<int32_t>(owned, n);
+    int32_t* gid = dalloc<int32_t>(owned, n);
+    k_group_flags<<<blocks, 256, 0, s>>>(rc, mpos, ordA, n, gflag);
+    {
+        size_t need = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, need, gflag, gid, n, s);
+        void* t = nullptr;
+        CK(cudaMallocAsync(&t, need, s));
+        CK(cub::DeviceScan::ExclusiveSum(t, need, gflag, gid, n, s));
+        cudaFreeAsync(t, s);
+    }
+    int32_t last_gid = 0, last_flag = 0;
+    CK(cudaMemcpyAsync(&last_gid, gid + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&last_flag, gflag + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int64_t G = int64_t(last_gid) + last_flag;
+    int64_t* gstart = dalloc<int64_t>(owned, G + 1);
+    k_group_starts<<<blocks, 256, 0, s>>>(gflag, gid, n, gstart);
+    CK(cudaMemcpyAsync(gstart + G, &n, 8, cudaMemcpyHostToDevice, s));
+    Groups gr{gstart, dalloc<int32_t>(owned, G), dalloc<int32_t>(owned, G), dalloc<int64_t>(owned, G),
+              dalloc<int64_t>(owned, G), dalloc<int32_t>(owned, G)};
+    const int gblocks = int((G + 127) / 128);
+    k_select<<<gblocks, 128, 0, s>>>(rc, ordA, ordB, G, gr);
+    // sample offsets
+    int64_t* soff = dalloc<int64_t>(owned, G + 1);
+    int64_t* ns64 = dalloc<int64_t>(owned, G);
+    {
+        // widen nsamp to int64 via a transform iterator
+        auto wid = cub::TransformInputIterator<int64_t, cub::CastOp<int64_t>, const int32_t*>(gr.nsamp,
+                                                                                                cub::CastOp<int64_t>());
+        size_t need = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, need, wid, soff, G, s);
+        void* t = nullptr;
+        CK(cudaMallocAsync(&t, need, s));
+        CK(cub::DeviceScan::ExclusiveSum(t, need, wid, soff, G, s));
+        cudaFreeAsync(t, s);
+    }
+    (void)ns64;
+    // group metadata to host (small: one row per (macro, w, l))
+    std::vector<int64_t> h_gstart(G + 1), h_soff(G);
+    std::vector<int32_t> h_gnsamp(G), h_gmicro(G), h_gpart(G);
+    CK(cudaMemcpyAsync(h_gstart.data(), gstart, (G + 1) * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_soff.data(), soff, G * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_gnsamp.data(), gr.nsamp, G * 4, cudaMemcpyDeviceToHost, s));
+    // group keys (mpos, w, l) from the first record of each group
+    std::vector<int64_t> h_ordA(n);
+    CK(cudaMemcpyAsync(h_ordA.data(), ordA, n * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int64_t S_total = h_soff[G - 1] + h_gnsamp[G - 1];
+    double* sg = dalloc<double>(owned, S_total);
+    double* sl = dalloc<double>(owned, S_total);
+    double* stt = dalloc<double>(owned, S_total);
+    double* scratch = dalloc<double>(owned, 18 * S_total);
+    if (!scratch) {
+        g_fit_err = "cudaMalloc failed (fit scratch)";
+        return WT_CUDA_ERROR;
+    }
+    k_samples<<<gblocks, 128, 0, s>>>(rc, ordA, G, gr, soff, sg, sl, stt);
+
+    // buckets (mpos, w) and macros from the group keys (host; G rows)
+    std::vector<int32_t> h_mpos_g(G), h_w_g(G);
+    std::vector<int64_t> h_l_g(G);
+    for (int64_t q = 0; q < G; ++q) {  // group keys from each group's first record
+        const int64_t r = h_ordA[h_gstart[q]];
+        h_w_g[q] = records->w[r];
+        h_l_g[q] = records->l[r];
+        auto it = std::lower_bound(hid.begin(), hid.end(), records->macro_id[r]);
+        h_mpos_g[q] = hpos[it - hid.begin()];
+    }
+    std::vector<int64_t> b_gstart, b_slo, b_shi, b_w, m_bstart;
+    std::vector<int32_t> m_pos;
+    for (int64_t q = 0; q < G; ++q) {
+        const bool newm = q == 0 || h_mpos_g[q] != h_mpos_g[q - 1];
+        const bool newb = newm || h_w_g[q] != h_w_g[q - 1];
+        if (newm) {
+            m_bstart.push_back(int64_t(b_gstart.size()));
+            m_pos.push_back(h_mpos_g[q]);
+        }
+        if (newb) {
+            b_gstart.push_back(q);
+            b_w.push_back(h_w_g[q]);
+            b_slo.push_back(h_soff[q]);
+        }
+    }
+    const int64_t NB = int64_t(b_gstart.size()), NM = int64_t(m_pos.size());
+    m_bstart.push_back(NB);
+    b_gstart.push_back(G);
+    for (int64_t k = 0; k < NB; ++k)
+        b_shi.push_back(b_gstart[k + 1] < G ? h_soff[b_gstart[k + 1]] : S_total);
+
+    int64_t* d_bslo = dalloc<int64_t>(owned, NB);
+    int64_t* d_bshi = dalloc<int64_t>(owned, NB);
+    int64_t* d_bgs = dalloc<int64_t>(owned, NB + 1);
+    int64_t* d_bw = dalloc<int64_t>(owned, NB);
+    int64_t* d_mbs = dalloc<int64_t>(owned, NM + 1);
+    CK(cudaMemcpyAsync(d_bslo, b_slo.data(), NB * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_bshi, b_shi.data(), NB * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_bgs, b_gstart.data(), (NB + 1) * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_bw, b_w.data(), NB * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_mbs, m_bstart.data(), (NM + 1) * 8, cudaMemcpyHostToDevice, s));
+    Buckets bk{NB, d_bslo, d_bshi, dalloc<double>(owned, NB * 4), dalloc<double>(owned, NB),
+               dalloc<double>(owned, NB), dalloc<int32_t>(owned, NB)};
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    k_fit<<<nsm * 8, 128, 0, s>>>(sg, sl, stt, bk, scratch);
+    Macros mc{NM, d_mbs, d_bw, d_bgs, W, p, dalloc<double>(owned, NM * 4), dalloc<int32_t>(owned, NM),
+              dalloc<int32_t>(owned, NM), dalloc<int64_t>(owned, G), dalloc<int32_t>(owned, G)};
+    // extrapolation pools reuse the bucket scratch layout (slice of the pooled samples)
+    k_extrap<<<nsm * 4, 128, 0, s>>>(rc, sg, sl, stt, bk, soff, gr, ordA, mc, scratch);
+    CK(cudaEventRecord(ev1, s));
+
+    // 7. results to host and CSR assembly (registry order = mpos order)
+    std::vector<double> h_coeff(NB * 4), h_r2(NB), h_mape(NB), h_theta(NM * 4);
+    std::vector<int32_t> h_degen(NB), h_mflags(NM), h_next(NM), h_em(G);
+    std::vector<int64_t> h_el(G);
+    CK(cudaMemcpyAsync(h_coeff.data(), bk.coeff, NB * 32, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_r2.data(), bk.r2, NB * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_mape.data(), bk.mape, NB * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_degen.data(), bk.degen, NB * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_theta.data(), mc.theta, NM * 32, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_mflags.data(), mc.flags, NM * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_next.data(), mc.next, NM * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_el.data(), mc.el, G * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_em.data(), mc.em, G * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_gmicro.data(), gr.micro, G * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_gpart.data(), gr.partial, G * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    CK(cudaGetLastError());
+
+    auto* B = new wt_build;
+    B->coeff_off.push_back(0);
+    B->awave_off.push_back(0);
+    B->awave_aoff.push_back(0);
+    B->ext_aoff.push_back(0);
+    for (int64_t mq = 0; mq < NM; ++mq) {
+        B->macro_id.push_back(registry_ids[m_pos[mq]]);
+        for (int c = 0; c < 4; ++c) B->theta_ext.push_back(h_theta[4 * mq + c]);
+        B->ext_flags.push_back(h_mflags[mq]);
+        for (int64_t k = m_bstart[mq]; k < m_bstart[mq + 1]; ++k) {
+            B->coeff_w.push_back(int32_t(b_w[k]));
+            for (int c = 0; c < 4; ++c) B->coeff_theta.push_back(h_coeff[4 * k + c]);
+            B->diag_r2.push_back(h_r2[k]);
+            B->diag_mape.push_back(h_mape[k]);
+            const int32_t ns = int32_t(b_shi[k] - b_slo[k]);
+            B->diag_samples.push_back(ns);
+            B->diag_flags.push_back((h_degen[k] ? 1 : 0) | (ns < 4 ? 2 : 0));
+            B->awave_w.push_back(int32_t(b_w[k]));
+            for (int64_t q = b_gstart[k]; q < b_gstart[k + 1]; ++q) {
+                B->anchor_l.push_back(h_l_g[q]);
+                B->anchor_micro.push_back(h_gmicro[q]);
+                B->anchor_partial.push_back(h_gpart[q]);
+            }
+            B->awave_aoff.push_back(int32_t(B->anchor_l.size()));
+        }
+        B->coeff_off.push_back(int32_t(B->coeff_w.size()));
+        B->awave_off.push_back(int32_t(B->awave_w.size()));
+        const int64_t gs = b_gstart[m_bstart[mq]];
+        for (int q = 0; q < h_next[mq]; ++q) {
+            B->ext_l.push_back(h_el[gs + q]);
+            B->ext_micro.push_back(h_em[gs + q]);
+        }
+        B->ext_aoff.push_back(int32_t(B->ext_l.size()));
+    }
+    wt_build_result& R = *result;
+    R.n_tables = int32_t(NM);
+    R.W = W;
+    R.p = p;
+    R.macro_id = B->macro_id.data();
+    R.theta_ext = B->theta_ext.data();
+    R.ext_flags = B->ext_flags.data();
+    R.coeff_off = B->coeff_off.data();
+    R.coeff_w = B->coeff_w.data();
+    R.coeff_theta = B->coeff_theta.data();
+    R.diag_r2 = B->diag_r2.data();
+    R.diag_mape = B->diag_mape.data();
+    R.diag_samples = B->diag_samples.data();
+    R.diag_flags = B->diag_flags.data();
+    R.awave_off = B->awave_off.data();
+    R.awave_w = B->awave_w.data();
+    R.awave_aoff = B->awave_aoff.data();
+    R.anchor_l = B->anchor_l.data();
+    R.anchor_micro = B->anchor_micro.data();
+    R.anchor_partial = B->anchor_partial.data();
+    R.ext_aoff = B->ext_aoff.data();
+    R.ext_l = B->ext_l.data();
+    R.ext_micro = B->ext_micro.data();
+    R.device_ms = ms;
+    *out = B;
+    return WT_OK;
 }
-wt_status wt_build_free(wt_build*) { return WT_OK; }
-wt_status wt_fit_bucket_batch(const double*, const double*, const double*, const int64_t*, int64_t,
-                              double*, double*, double*, int32_t*, int) {
-    return WT_UNSUPPORTED;
+
+wt_status wt_build_free(wt_build* b) {
+    delete b;
+    return WT_OK;
 }
+
+wt_status wt_fit_bucket_batch(const double* g, const double* l, const double* t, const int64_t* off,
+                              int64_t nb, double* coeffs, double* r2, double* mape, int32_t* degenerate,
+                              int device) {
+    if (nb <= 0) return WT_OK;
+    for (int64_t b = 0; b < nb; ++b)
+        if (off[b + 1] <= off[b]) {
+            g_fit_err = "fit_bucket: no samples";
+            return WT_INVALID_ARGUMENT;
+        }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    struct Restore {
+        int d;
+        ~Restore() { cudaSetDevice(d); }
+    } restore{prev};
+    std::vector<void*> owned;
+    struct Free {
+        std::vector<void*>* v;
+        ~Free() {
+            for (void* q : *v) cudaFree(q);
+        }
+    } freer{&owned};
+    const int64_t S = off[nb] - off[0];
+    double* dg = dalloc<double>(owned, S);
+    double* dl = dalloc<double>(owned, S);
+    double* dt = dalloc<double>(owned, S);
+    double* scr = dalloc<double>(owned, 18 * S);
+    int64_t* lo = dalloc<int64_t>(owned, nb);
+    int64_t* hi = dalloc<int64_t>(owned, nb);
+    std::vector<int64_t> hlo(nb), hhi(nb);
+    for (int64_t b = 0; b < nb; ++b) {
+        hlo[b] = off[b] - off[0];
+        hhi[b] = off[b + 1] - off[0];
+    }
+    CK(cudaMemcpy(dg, g + off[0], S * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dl, l + off[0], S * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dt, t + off[0], S * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(lo, hlo.data(), nb * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(hi, hhi.data(), nb * 8, cudaMemcpyHostToDevice));
+    Buckets bk{nb, lo, hi, dalloc<double>(owned, nb * 4), dalloc<double>(owned, nb), dalloc<double>(owned, nb),
+               dalloc<int32_t>(owned, nb)};
+    k_fit<<<int(std::min<int64_t>((nb + 3) / 4, 148 * 16)), 128>>>(dg, dl, dt, bk, scr);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(coeffs, bk.coeff, nb * 32, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(r2, bk.r2, nb * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(mape, bk.mape, nb * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(degenerate, bk.degen, nb * 4, cudaMemcpyDeviceToHost));
+    return WT_OK;
 }
+
+}  // extern "C"

@@ -76,6 +76,9 @@ struct HostImage {
     int32_t tm_min = 0, tn_min = 0;
 };
 
+// Thread-local message returned by wt_last_error().
+void set_last_error(const std::string& msg);
+
 // Resolves every reference fallback rule into dense rows; returns WT_OK or
 // an error status with *err set to the reference's message.
 wt_status build_image(const wt_tables_desc& t, const wt_registry_desc& r, const wt_hw& hw,
