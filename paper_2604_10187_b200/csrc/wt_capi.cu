@@ -70,6 +70,7 @@ struct wt_engine {
     size_t bytes = 0;
     int eval_chunk = 0;
     int eval_grid = 0;
+    int eval_grid2 = 0;
 };
 
 struct wt_grid {
@@ -118,6 +119,9 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
            o_th = ar.take(C * R * 32), o_meta = ar.take(C * R * 4), o_used = ar.take(C * R * 4),
            o_amap = ar.take(C * R * 8), o_afb = ar.take(C * R * 4),
            o_al = ar.take(h.anchor_l.size() * 8), o_am = ar.take(h.anchor_micro.size() * 4);
+    const size_t NS = h.seg_pos.size();
+    size_t o_st = ar.take(NS * 16), o_sm = ar.take(NS * 16), o_sp = ar.take(NS * 4), o_cc = ar.take(C * 4),
+           o_th2 = ar.take(C * R * 32), o_m2 = ar.take(C * R * 4);
     cudaError_t ce = cudaMalloc(&e->mem, ar.used);
     if (ce != cudaSuccess) {
         delete e;
@@ -136,6 +140,9 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
         {o_amap, h.amap.data(), C * R * 8},       {o_afb, h.afb.data(), C * R * 4},
         {o_al, h.anchor_l.data(), h.anchor_l.size() * 8},
         {o_am, h.anchor_micro.data(), h.anchor_micro.size() * 4},
+        {o_st, h.seg_tiles.data(), NS * 16},      {o_sm, h.seg_magic.data(), NS * 16},
+        {o_sp, h.seg_pos.data(), NS * 4},         {o_cc, h.cls_cfg.data(), C * 4},
+        {o_th2, h.theta2.data(), C * R * 32},     {o_m2, h.meta2.data(), C * R * 4},
     };
     for (const Piece& p : pieces) {
         ce = cudaMemcpy(base + p.off, p.src, p.n, cudaMemcpyHostToDevice);
@@ -166,9 +173,17 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
     d.anchor_micro = reinterpret_cast<const int32_t*>(base + o_am);
     d.tm_min = h.tm_min;
     d.tn_min = h.tn_min;
+    d.nseg = int32_t(NS);
+    d.seg_tiles = reinterpret_cast<const int4*>(base + o_st);
+    d.seg_magic = reinterpret_cast<const uint4*>(base + o_sm);
+    d.seg_pos = reinterpret_cast<const int32_t*>(base + o_sp);
+    d.cls_cfg = reinterpret_cast<const int32_t*>(base + o_cc);
+    d.theta2 = reinterpret_cast<const double4*>(base + o_th2);
+    d.meta2 = reinterpret_cast<const uint32_t*>(base + o_m2);
     // list-mode chunk: keep the staged rows near 40 KB so several CTAs fit per SM
     e->eval_chunk = int(std::max<size_t>(1, std::min<size_t>(C, 40960 / (R * 36 + 32))));
     e->eval_grid = sm_count(device) * 4;
+    e->eval_grid2 = sm_count(device) * 2;  // 96 KB of shared memory per CTA
     *out = e;
     return WT_OK;
 }
@@ -262,9 +277,14 @@ wt_status wt_tune_batch(const wt_engine* e, const int32_t* M, const int32_t* N, 
     a.n = n;
     a.chunk = e->eval_chunk;
     a.out = to_out(out);
-    const int64_t tiles = (n + kEvalThreads - 1) / kEvalThreads;
-    const int grid = int(std::min<int64_t>(tiles, e->eval_grid));
-    cudaError_t ce = launch_eval(e->dev, a, grid, static_cast<cudaStream_t>(stream));
+    cudaError_t ce;
+    if (a.out.topk > 0) {  // per-config order kernel keeps the top-k list
+        const int64_t tiles = (n + kEvalThreads - 1) / kEvalThreads;
+        ce = launch_eval(e->dev, a, int(std::min<int64_t>(tiles, e->eval_grid)), static_cast<cudaStream_t>(stream));
+    } else {
+        const int64_t tiles = (n + eval2_tile() - 1) / eval2_tile();
+        ce = launch_eval2(e->dev, a, int(std::min<int64_t>(tiles, e->eval_grid2)), static_cast<cudaStream_t>(stream));
+    }
     g_launches++;
     if (ce != cudaSuccess) return cuda_err(ce, "wt_tune_batch");
     return WT_OK;
@@ -449,7 +469,8 @@ wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, v
     a.topk = g->topk;
     a.topk_macro = g->tk_macro;
     a.topk_lat = g->tk_lat;
-    cudaError_t ce = launch_sweep(e->dev, a, g->wide, static_cast<cudaStream_t>(stream));
+    cudaError_t ce = g->topk > 0 ? launch_sweep(e->dev, a, g->wide, static_cast<cudaStream_t>(stream))
+                                 : launch_sweep2(e->dev, a, g->wide, static_cast<cudaStream_t>(stream));
     g_launches++;
     if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep");
     return WT_OK;
@@ -504,7 +525,7 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
         ea.chunk = e->eval_chunk;
         ea.out = to_out(out);
         if (g->topk == 0) ea.out.topk = 0;
-        ce = launch_eval(e->dev, ea, e->eval_grid, s);
+        ce = ea.out.topk > 0 ? launch_eval(e->dev, ea, e->eval_grid, s) : launch_eval2(e->dev, ea, e->eval_grid2, s);
         g_launches++;
     }
     cudaFreeAsync(scratch, s);

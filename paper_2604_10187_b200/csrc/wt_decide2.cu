@@ -1,0 +1,455 @@
+// wt_decide2.cu -- tile-class K1 kernels (argmin path, no top-k).
+//
+// Configs that share (t_m, t_n, t_k) give every shape the same (G, L, w), so
+// the integer part of the evaluation (magic divisions, wave row, int->fp64
+// conversion of G) is done once per (shape, tile class) and only the bilinear
+// evaluation + compare runs per (shape, config):
+//     3 DMUL + 3 DADD (+1 DMUL for gamma*l in list mode) + DSETP + 3 SEL.
+// Classes are cut into segments of <= kSegCfg configs kept in ascending
+// macro_id order, so the segment-local argmin is the reference's strict-<
+// scan; segments are merged with the lexicographic (latency, config index)
+// order, which is exactly "first minimum in ascending macro_id"
+// (tuner.cpp:135-149): NaN never wins, -0 == +0 keeps the smaller id.
+//
+//   k_sweep2  grid mode: lanes = consecutive M of one (N, K) pair; per tile
+//             only the coefficient rows the tile's G range can touch are
+//             staged (row-range staging), gamma*l folded in.
+//   k_eval2   list mode: lanes = arbitrary queries; every row of a segment is
+//             staged in a [row][config] layout whose row stride is an odd
+//             number of 16-byte slots, so lanes hitting random rows spread
+//             over all shared-memory banks.
+#include <cuda_runtime.h>
+
+#include <cub/block/block_scan.cuh>
+#include <cstdint>
+
+#include "wt_decide.h"
+#include "wt_device.cuh"
+
+namespace wtb {
+
+
+namespace {
+
+constexpr int kT2 = 256;  // threads per CTA for both kernels
+
+struct SegHdr {  // one staged segment
+    uint32_t mM, sM, nt, rowlo;
+    int32_t ncfg, pos, off, stride;  // off/stride in double4 units
+    double ld;
+    uint32_t mN, mK, sNK, pad;
+};
+
+__device__ __forceinline__ bool lex_less(double a, int ia, double b, int ib) {
+    return a < b || (a == b && ia < ib);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- sweep (grid)
+template <int RPT, bool SPECIAL, bool WIDE>
+__global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int cap_rows) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    SegHdr* hdr = reinterpret_cast<SegHdr*>(smem);
+    double4* rows = reinterpret_cast<double4*>(hdr + kT2);
+    uint32_t* meta = reinterpret_cast<uint32_t*>(rows + cap_rows);
+    using Scan = cub::BlockScan<int, kT2>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+
+    const int tid = threadIdx.x;
+    const int64_t tile = int64_t(kT2) * RPT;
+    const int64_t t0 = a.begin + int64_t(blockIdx.x) * tile;
+    const int64_t t1 = min(t0 + tile, a.end);
+    const uint32_t RS = im.RS, mS = im.mS, sS = im.sS;
+    const int R = im.R;
+
+    for (int64_t seg0 = t0; seg0 < t1;) {
+        const int32_t p = int32_t(seg0 / a.mcount);
+        const int64_t seg_end = min(t1, int64_t(p + 1) * a.mcount);
+        const uint32_t Np = uint32_t(a.N[p]), Kp = uint32_t(a.K[p]);
+        const uint32_t Mlo = uint32_t(a.m_lo + (seg0 - int64_t(p) * a.mcount));
+        const uint32_t Mhi = uint32_t(a.m_lo + (seg_end - 1 - int64_t(p) * a.mcount));
+
+        double best[RPT];
+        int bc[RPT];
+        uint32_t acc[RPT], y2[RPT];
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            const int64_t idx = seg0 + int64_t(j) * kT2 + tid;
+            const uint32_t M = idx < seg_end ? uint32_t(a.m_lo + (idx - int64_t(p) * a.mcount)) : Mlo;
+            y2[j] = 2u * (M - 1u);
+            best[j] = __longlong_as_double(0x7ff0000000000000LL);
+            bc[j] = -1;
+            acc[j] = 0;
+        }
+
+        for (int s0 = 0; s0 < im.nseg;) {
+            // -- plan this staging round: segments s0.. whose row ranges fit
+            const int s = s0 + tid;
+            int need = 0;
+            uint32_t rlo = 0, nt = 0, mM = 0, sM = 0, lk = 1;
+            int4 st = make_int4(0, 0, 0, 0);
+            if (s < im.nseg) {
+                st = __ldg(im.seg_tiles + s);
+                const uint4 mg = __ldg(im.seg_magic + s);
+                mM = mg.x;
+                sM = mg.w & 0xffu;
+                nt = uint32_t((uint64_t(Np) + uint32_t(st.y) - 1) / uint32_t(st.y));
+                lk = uint32_t((uint64_t(Kp) + uint32_t(st.z) - 1) / uint32_t(st.z));
+                const uint64_t glo = uint64_t(cdiv_m(Mlo, mM, sM)) * nt;
+                const uint64_t ghi = uint64_t(cdiv_m(Mhi, mM, sM)) * nt;
+                rlo = row_of(uint32_t(glo > RS ? RS : glo), mS, sS);
+                const uint32_t rhi = row_of(uint32_t(ghi > RS ? RS : ghi), mS, sS);
+                need = int(rhi - rlo + 1) * st.w;
+            }
+            int off;
+            Scan(scan_tmp).ExclusiveSum(need, off);
+            const int fits = (s < im.nseg) && (off + need <= cap_rows);
+            const int count = max(1, __syncthreads_count(fits));
+            if (tid < count && s < im.nseg) {
+                SegHdr h;
+                h.mM = mM;
+                h.sM = sM;
+                h.nt = nt;
+                h.rowlo = rlo;
+                h.ncfg = st.w;
+                h.pos = __ldg(im.seg_pos + s);
+                h.off = off;
+                h.stride = need / max(st.w, 1);  // rows per config in this tile
+                h.ld = u32_to_f64(lk);
+                hdr[tid] = h;
+            }
+            __syncthreads();
+            // -- stage rows [rowlo, rowlo+stride) of every config, gamma*l folded
+            for (int k = 0; k < count; ++k) {
+                const SegHdr h = hdr[k];
+                const int n = h.stride * h.ncfg;
+                for (int i = tid; i < n; i += kT2) {
+                    const int j = i / h.stride, r = i - j * h.stride;
+                    const size_t src = size_t(h.pos + j) * R + h.rowlo + r;
+                    double4 th = ldg_row(im.theta2 + src);
+                    th.z = __dmul_rn(th.z, h.ld);
+                    rows[h.off + i] = th;
+                    if constexpr (SPECIAL) meta[h.off + i] = __ldg(im.meta2 + src);
+                }
+            }
+            __syncthreads();
+            // -- evaluate
+            for (int k = 0; k < count; ++k) {
+                const SegHdr h = hdr[k];
+                int base[RPT];
+                double gd[RPT], sb[RPT];
+                int sj[RPT];
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) {
+                    const uint32_t q = mdiv2(y2[j], h.mM, h.sM);
+                    uint32_t gc;
+                    if constexpr (WIDE) {
+                        const uint64_t g = uint64_t(q) * h.nt + h.nt;
+                        gc = g > RS ? RS : uint32_t(g);
+                        gd[j] = u64_to_f64(g);
+                    } else {
+                        const uint32_t g = q * h.nt + h.nt;
+                        gc = min(g, RS);
+                        gd[j] = u32_to_f64(g);
+                    }
+                    base[j] = h.off + int(row_of(gc, mS, sS) - h.rowlo);
+                    sb[j] = __longlong_as_double(0x7ff0000000000000LL);
+                    sj[j] = -1;
+                }
+                const double ld = h.ld;
+#pragma unroll 2
+                for (int c = 0; c < h.ncfg; ++c) {
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) {
+                        const double4 th = rows[base[j] + c * h.stride];
+                        const double t = bilinear(th.x, th.y, th.z, th.w, gd[j], ld);
+                        if (t < sb[j]) {
+                            sb[j] = t;
+                            sj[j] = c;
+                        }
+                        if constexpr (SPECIAL) acc[j] |= meta[base[j] + c * h.stride];
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) {
+                    if (sj[j] >= 0) {
+                        const int ci = __ldg(im.cls_cfg + h.pos + sj[j]);
+                        if (lex_less(sb[j], ci, best[j], bc[j] < 0 ? INT32_MAX : bc[j])) {
+                            best[j] = sb[j];
+                            bc[j] = ci;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            s0 += count;
+        }
+
+        // epilogue: Stage II per winner, one 32-byte entry per shape
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            const int64_t idx = seg0 + int64_t(j) * kT2 + tid;
+            if (idx >= seg_end) continue;
+            const int c = bc[j];
+            uint64_t g = 0;
+            int64_t l = 0;
+            if (c >= 0) {
+                const int4 tl = __ldg(im.tiles + c);
+                const uint32_t M = y2[j] / 2u + 1u;
+                g = uint64_t((M + uint32_t(tl.x) - 1) / uint32_t(tl.x)) *
+                    uint64_t((uint64_t(Np) + uint32_t(tl.y) - 1) / uint32_t(tl.y));
+                l = int64_t((uint64_t(Kp) + uint32_t(tl.z) - 1) / uint32_t(tl.z));
+            }
+            const Final f = finish(im, c, 0.0, g, l, acc[j]);
+            const bool ok = (f.flags >> 24) == 0;
+            const double lat = ok ? best[j] : __longlong_as_double(0x7ff8000000000000LL);
+            int4 lo, hi;
+            lo.x = __double2loint(lat);
+            lo.y = __double2hiint(lat);
+            lo.z = f.macro;
+            lo.w = f.micro;
+            hi.x = f.wave;
+            hi.y = int(f.flags);
+            hi.z = f.comps;
+            hi.w = __float_as_int(f.tail);
+            int4* e = reinterpret_cast<int4*>(a.entries + idx);
+            e[0] = lo;
+            e[1] = hi;
+        }
+        seg0 = seg_end;
+    }
+}
+
+// --------------------------------------------------------------- eval (list)
+template <int RPT, bool SPECIAL>
+__global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_rows) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    SegHdr* hdr = reinterpret_cast<SegHdr*>(smem);
+    double4* rows = reinterpret_cast<double4*>(hdr + kT2);
+    uint32_t* meta = reinterpret_cast<uint32_t*>(rows + cap_rows);
+    using Scan = cub::BlockScan<int, kT2>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+
+    const int64_t n = a.count ? *a.count : a.n;
+    const int64_t tile = int64_t(kT2) * RPT;
+    const int64_t ntiles = (n + tile - 1) / tile;
+    const uint32_t RS = im.RS, mS = im.mS, sS = im.sS;
+    const int R = im.R;
+    const int tid = threadIdx.x;
+
+    for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+        int64_t q[RPT];
+        uint32_t y2M[RPT], y2N[RPT], y2K[RPT], status[RPT], acc[RPT];
+        double best[RPT];
+        int bc[RPT];
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            const int64_t slot = tl * tile + int64_t(j) * kT2 + tid;
+            const bool live = slot < n;
+            q[j] = live ? (a.idx ? a.idx[slot] : slot) : -1;
+            uint32_t M = 1, N = 1, K = 1, st = 0;
+            if (live) {
+                const int32_t m = a.M[q[j]], nn = a.N[q[j]], k = a.K[q[j]];
+                if (m < 1 || nn < 1 || k < 1) {
+                    st = WT_INVALID_ARGUMENT;  // kernel_map.cpp:238-239
+                } else {
+                    M = uint32_t(m);
+                    N = uint32_t(nn);
+                    K = uint32_t(k);
+                    const uint64_t gmax = uint64_t((M + uint32_t(im.tm_min) - 1) / uint32_t(im.tm_min)) *
+                                          uint64_t((N + uint32_t(im.tn_min) - 1) / uint32_t(im.tn_min));
+                    if ((gmax + uint64_t(im.S) - 1) / uint64_t(im.S) >= (uint64_t(1) << 31)) st = WT_UNSUPPORTED;
+                }
+            }
+            if (st) M = N = K = 1;
+            y2M[j] = 2u * (M - 1u);
+            y2N[j] = 2u * (N - 1u);
+            y2K[j] = 2u * (K - 1u);
+            status[j] = st;
+            best[j] = __longlong_as_double(0x7ff0000000000000LL);
+            bc[j] = -1;
+            acc[j] = 0;
+        }
+        for (int s0 = 0; s0 < im.nseg;) {
+            const int s = s0 + tid;
+            int need = 0;
+            int4 st = make_int4(0, 0, 0, 0);
+            uint4 mg = make_uint4(0, 0, 0, 0);
+            if (s < im.nseg) {
+                st = __ldg(im.seg_tiles + s);
+                mg = __ldg(im.seg_magic + s);
+                need = R * (2 * st.w + 1);  // [row][config] double4 halves + one pad slot per row
+            }
+            int off;
+            Scan(scan_tmp).ExclusiveSum(need, off);
+            const int fits = (s < im.nseg) && (off + need <= 2 * cap_rows);
+            const int count = max(1, __syncthreads_count(fits));
+            if (tid < count && s < im.nseg) {
+                SegHdr h;
+                h.mM = mg.x;
+                h.mN = mg.y;
+                h.mK = mg.z;
+                h.sM = mg.w;
+                h.ncfg = st.w;
+                h.pos = __ldg(im.seg_pos + s);
+                h.off = off;                // in 16-byte slots
+                h.stride = 2 * st.w + 1;    // slots per row (odd)
+                hdr[tid] = h;
+            }
+            __syncthreads();
+            double2* slots = reinterpret_cast<double2*>(rows);
+            for (int k = 0; k < count; ++k) {
+                const SegHdr h = hdr[k];
+                const int n2 = R * h.ncfg;
+                for (int i = tid; i < n2; i += kT2) {
+                    const int r = i / h.ncfg, c = i - r * h.ncfg;
+                    const size_t src = size_t(h.pos + c) * R + r;
+                    const double4 th = ldg_row(im.theta2 + src);
+                    const int d = h.off + r * h.stride + 2 * c;
+                    slots[d] = make_double2(th.x, th.y);
+                    slots[d + 1] = make_double2(th.z, th.w);
+                    if constexpr (SPECIAL) meta[h.off / 2 + r * h.ncfg + c] = __ldg(im.meta2 + src);
+                }
+            }
+            __syncthreads();
+            for (int k = 0; k < count; ++k) {
+                const SegHdr h = hdr[k];
+                const uint32_t sMv = h.sM & 0xffu, sNv = (h.sM >> 8) & 0xffu, sKv = (h.sM >> 16) & 0xffu;
+                int base[RPT];
+                double gd[RPT], ld[RPT], sb[RPT];
+                int sj[RPT];
+                int rowi[RPT];
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) {
+                    const uint32_t mt = mdiv2(y2M[j], h.mM, sMv) + 1u;
+                    const uint32_t nt = mdiv2(y2N[j], h.mN, sNv) + 1u;
+                    const uint32_t lk = mdiv2(y2K[j], h.mK, sKv) + 1u;
+                    const uint64_t g = uint64_t(mt) * nt;
+                    const uint32_t gc = g > RS ? RS : uint32_t(g);
+                    rowi[j] = int(row_of(gc, mS, sS));
+                    base[j] = h.off + rowi[j] * h.stride;
+                    gd[j] = u64_to_f64(g);
+                    ld[j] = u32_to_f64(lk);
+                    sb[j] = __longlong_as_double(0x7ff0000000000000LL);
+                    sj[j] = -1;
+                }
+#pragma unroll 2
+                for (int c = 0; c < h.ncfg; ++c) {
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) {
+                        const double2 ab = slots[base[j] + 2 * c];
+                        const double2 gd2 = slots[base[j] + 2 * c + 1];
+                        const double t = bilinear(ab.x, ab.y, __dmul_rn(gd2.x, ld[j]), gd2.y, gd[j], ld[j]);
+                        if (t < sb[j]) {
+                            sb[j] = t;
+                            sj[j] = c;
+                        }
+                        if constexpr (SPECIAL) acc[j] |= meta[h.off / 2 + rowi[j] * h.ncfg + c];
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) {
+                    if (sj[j] >= 0) {
+                        const int ci = __ldg(im.cls_cfg + h.pos + sj[j]);
+                        if (lex_less(sb[j], ci, best[j], bc[j] < 0 ? INT32_MAX : bc[j])) {
+                            best[j] = sb[j];
+                            bc[j] = ci;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            s0 += count;
+        }
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            if (q[j] < 0) continue;
+            Final f;
+            uint64_t g = 0;
+            int64_t l = 0;
+            if (status[j]) {
+                f.flags = status[j] << 24;
+                f.macro = f.micro = f.wave = -1;
+                f.comps = 0;
+                f.tail = 0.f;
+            } else {
+                if (bc[j] >= 0) {
+                    const int4 tl4 = __ldg(im.tiles + bc[j]);
+                    const uint32_t M = y2M[j] / 2u + 1u, N = y2N[j] / 2u + 1u, K = y2K[j] / 2u + 1u;
+                    g = uint64_t((M + uint32_t(tl4.x) - 1) / uint32_t(tl4.x)) *
+                        uint64_t((N + uint32_t(tl4.y) - 1) / uint32_t(tl4.y));
+                    l = int64_t((K + uint32_t(tl4.z) - 1) / uint32_t(tl4.z));
+                }
+                f = finish(im, bc[j], 0.0, g, l, acc[j]);
+            }
+            const DecOut& o = a.out;
+            const int64_t qi = q[j];
+            const bool ok = (f.flags >> 24) == 0;
+            o.macro[qi] = ok ? f.macro : -1;
+            o.micro[qi] = ok ? f.micro : -1;
+            o.lat[qi] = ok ? best[j] : __longlong_as_double(0x7ff8000000000000LL);
+            if (o.g) o.g[qi] = ok ? int64_t(g) : 0;
+            if (o.l) o.l[qi] = ok ? l : 0;
+            if (o.wave) o.wave[qi] = ok ? f.wave : 0;
+            if (o.flags) o.flags[qi] = f.flags;
+            if (o.comps) o.comps[qi] = ok ? f.comps : 0;
+            if (o.tail) o.tail[qi] = ok ? double(f.tail) : 0.0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- launchers
+namespace {
+constexpr int kSweepRPT2 = 4;
+constexpr int kEvalRPT2 = 4;
+constexpr size_t kSmem2 = 96 * 1024;  // per CTA: 2 CTAs per SM
+}
+
+size_t sweep2_smem(const DevImage& im, int* cap_rows) {
+    const size_t avail = kSmem2 - kT2 * sizeof(SegHdr);
+    const size_t per_row = sizeof(double4) + (im.special ? 4 : 0);
+    *cap_rows = int(avail / per_row);
+    return kSmem2;
+}
+
+template <int RPT, bool SP, bool WIDE>
+static cudaError_t go_sweep2(const DevImage& im, const SweepArgs& a, int grid, cudaStream_t st) {
+    int cap;
+    const size_t smem = sweep2_smem(im, &cap);
+    auto fn = k_sweep2<RPT, SP, WIDE>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    fn<<<grid, kT2, smem, st>>>(im, a, cap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sweep2(const DevImage& im, const SweepArgs& a, bool wide, cudaStream_t st) {
+    const int64_t n = a.end - a.begin;
+    if (n <= 0) return cudaSuccess;
+    const int grid = int((n + int64_t(kT2) * kSweepRPT2 - 1) / (int64_t(kT2) * kSweepRPT2));
+    const bool sp = im.special != 0;
+    if (wide) return sp ? go_sweep2<kSweepRPT2, true, true>(im, a, grid, st) : go_sweep2<kSweepRPT2, false, true>(im, a, grid, st);
+    return sp ? go_sweep2<kSweepRPT2, true, false>(im, a, grid, st) : go_sweep2<kSweepRPT2, false, false>(im, a, grid, st);
+}
+
+template <int RPT, bool SP>
+static cudaError_t go_eval2(const DevImage& im, const EvalArgs& a, int grid, cudaStream_t st) {
+    const size_t avail = kSmem2 - kT2 * sizeof(SegHdr);
+    // rows are counted in double4 units; the list layout uses 16-byte slots
+    const size_t per_row = sizeof(double4) + (SP ? 8 : 0);
+    const int cap = int(avail / per_row);
+    auto fn = k_eval2<RPT, SP>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem2));
+    if (e != cudaSuccess) return e;
+    fn<<<grid, kT2, kSmem2, st>>>(im, a, cap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eval2(const DevImage& im, const EvalArgs& a, int grid, cudaStream_t st) {
+    return im.special ? go_eval2<kEvalRPT2, true>(im, a, grid, st) : go_eval2<kEvalRPT2, false>(im, a, grid, st);
+}
+
+int eval2_tile() { return kT2 * kEvalRPT2; }
+
+}  // namespace wtb

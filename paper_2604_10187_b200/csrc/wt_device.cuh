@@ -104,4 +104,71 @@ __device__ __forceinline__ void topk_insert(double (&L)[KM], int (&I)[KM], doubl
     }
 }
 
+// ---------------------------------------------------------------- Stage II
+struct Stage2 {
+    int32_t micro;
+    int32_t comps;
+    uint32_t flags;  // WT_FLAG_* bits and status << 24
+};
+
+__device__ __forceinline__ Stage2 stage2(const DevImage& im, int c, uint32_t row, int64_t l) {
+    const size_t rr = size_t(c) * im.R + row;
+    const uint32_t meta = __ldg(im.rowmeta + rr);
+    Stage2 s;
+    s.flags = (meta & ROW_EXTRAP) ? WT_FLAG_EXTRAPOLATED : 0u;
+    if (meta & ROW_ANCHOR_FB) s.flags |= WT_FLAG_ANCHOR_FALLBACK;
+    if (meta & ROW_NO_ANCHOR) {
+        s.micro = -1;
+        s.comps = 0;
+        s.flags |= uint32_t(WT_RUNTIME_ERROR) << 24;
+        return s;
+    }
+    const int2 am = __ldg(im.amap + rr);
+    int comps;
+    int k = nearest_anchor_idx(im.anchor_l + am.x, am.y, l, &comps);
+    s.micro = __ldg(im.anchor_micro + am.x + k);
+    s.comps = comps;
+    return s;
+}
+
+// Winner epilogue shared by every mode: w (true wave count), regime,
+// Stage II, tail fraction.
+struct Final {
+    int32_t macro, micro, wave, comps;
+    uint32_t flags;
+    float tail;
+};
+
+__device__ __forceinline__ Final finish(const DevImage& im, int c, double best, uint64_t g,
+                                        int64_t l, uint32_t acc_meta) {
+    Final f;
+    f.tail = 0.f;
+    if (c < 0) {  // every candidate NaN or +inf: the reference dereferences null
+        f.macro = f.micro = f.wave = -1;
+        f.comps = 0;
+        f.flags = uint32_t(WT_RUNTIME_ERROR) << 24;
+        return f;
+    }
+    if (acc_meta & ROW_NO_COEFF) {  // predict_latency threw for some table
+        f.macro = f.micro = f.wave = -1;
+        f.comps = 0;
+        f.flags = uint32_t(WT_RUNTIME_ERROR) << 24;
+        return f;
+    }
+    const uint64_t S = uint64_t(im.S);
+    const uint64_t w64 = (g + S - 1) / S;
+    const uint32_t row = uint32_t(w64 < uint64_t(im.R) ? w64 : uint64_t(im.R)) - 1u;
+    Stage2 s = stage2(im, c, row, l);
+    f.macro = __ldg(im.macro_id + c);
+    f.micro = s.micro;
+    f.wave = int32_t(uint32_t(w64));
+    f.comps = s.comps;
+    f.flags = s.flags | ((acc_meta & ROW_MISSING) ? WT_FLAG_MISSING_WAVE : 0u);
+    f.tail = float(double(g - (w64 - 1) * S) / double(S));
+    if (f.flags >> 24) f.macro = -1;
+    (void)best;
+    return f;
+}
+
+
 }  // namespace wtb

@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <map>
 #include <numeric>
+#include <tuple>
 
 #include "wt_internal.h"
 
@@ -62,8 +63,8 @@ wt_status build_image(const wt_tables_desc& T, const wt_registry_desc& reg, cons
     im.family = reg.family;
     int32_t wmax = 0;
     for (int32_t i = 0; i < T.n_tables; ++i) wmax = std::max(wmax, T.W[i]);
-    if (wmax > 4096)
-        return fail(err, WT_UNSUPPORTED, "table W above 4096 is outside the device path's range");
+    if (wmax > 2048)
+        return fail(err, WT_UNSUPPORTED, "table W above 2048 is outside the device path's range");
     im.R = wmax + 1;
     if (int64_t(im.R) * S64 >= (int64_t(1) << 31))
         return fail(err, WT_UNSUPPORTED, "W * slots exceeds the device path's range");
@@ -212,6 +213,42 @@ wt_status build_image(const wt_tables_desc& T, const wt_registry_desc& reg, cons
             im.amap[2 * row + 1] = cnt;
             im.rowmeta[row] = meta;
             if (meta & ROW_SPECIAL) im.special = true;
+        }
+    }
+    // Tile classes (first-appearance order) cut into segments of <= kSegCfg.
+    {
+        std::map<std::tuple<int32_t, int32_t, int32_t>, std::vector<int32_t>> cls;
+        std::vector<std::tuple<int32_t, int32_t, int32_t>> first;
+        for (int32_t c = 0; c < C; ++c) {
+            auto key = std::make_tuple(im.tiles[4 * c], im.tiles[4 * c + 1], im.tiles[4 * c + 2]);
+            auto& v = cls[key];
+            if (v.empty()) first.push_back(key);
+            v.push_back(c);
+        }
+        im.cls_cfg.clear();
+        im.seg_tiles.clear();
+        im.seg_magic.clear();
+        im.seg_pos.clear();
+        for (const auto& key : first) {
+            const auto& v = cls[key];
+            for (size_t s = 0; s < v.size(); s += kSegCfg) {
+                const int32_t n = int32_t(std::min<size_t>(kSegCfg, v.size() - s));
+                const int32_t c0 = v[s];
+                im.seg_pos.push_back(int32_t(im.cls_cfg.size()));
+                for (int32_t q = 0; q < 3; ++q) im.seg_tiles.push_back(im.tiles[4 * c0 + q]);
+                im.seg_tiles.push_back(n);
+                for (int32_t q = 0; q < 4; ++q) im.seg_magic.push_back(im.magic[4 * c0 + q]);
+                for (int32_t q = 0; q < n; ++q) im.cls_cfg.push_back(v[s + q]);
+            }
+        }
+        im.theta2.resize(im.theta.size());
+        im.meta2.resize(im.rowmeta.size());
+        for (int32_t pos = 0; pos < C; ++pos) {
+            const int32_t c = im.cls_cfg[pos];
+            std::copy(im.theta.begin() + size_t(c) * R * 4, im.theta.begin() + size_t(c + 1) * R * 4,
+                      im.theta2.begin() + size_t(pos) * R * 4);
+            std::copy(im.rowmeta.begin() + size_t(c) * R, im.rowmeta.begin() + size_t(c + 1) * R,
+                      im.meta2.begin() + size_t(pos) * R);
         }
     }
     if (im.anchor_l.empty()) {  // keep the pool non-empty for the device

@@ -56,7 +56,20 @@ struct DevImage {
     const int64_t* anchor_l;  // pool
     const int32_t* anchor_micro;
     int32_t tm_min, tn_min;   // for the per-query wide-range guard
+    // Tile-class view: configs with identical (t_m, t_n, t_k) map every shape
+    // to the same (G, L, w), so the integer work is done once per class.
+    // Classes are cut into segments of <= kSegCfg configs; within a segment
+    // configs keep ascending macro_id order.
+    int32_t nseg;
+    const int4* seg_tiles;    // [nseg] {t_m, t_n, t_k, ncfg}
+    const uint4* seg_magic;   // [nseg] as magic
+    const int32_t* seg_pos;   // [nseg] first position in the class-ordered list
+    const int32_t* cls_cfg;   // [C] class-ordered position -> config index
+    const double4* theta2;    // [C*R] rows in class order
+    const uint32_t* meta2;    // [C*R] rowmeta in class order
 };
+
+constexpr int kSegCfg = 32;
 
 // Host-side resolved image (built by build_image, uploaded by the C-ABI).
 struct HostImage {
@@ -74,6 +87,12 @@ struct HostImage {
     std::vector<int64_t> anchor_l;
     std::vector<int32_t> anchor_micro;
     int32_t tm_min = 0, tn_min = 0;
+    std::vector<int32_t> seg_tiles;  // 4 per segment
+    std::vector<uint32_t> seg_magic; // 4 per segment
+    std::vector<int32_t> seg_pos;
+    std::vector<int32_t> cls_cfg;
+    std::vector<double> theta2;
+    std::vector<uint32_t> meta2;
 };
 
 // Thread-local message returned by wt_last_error().
