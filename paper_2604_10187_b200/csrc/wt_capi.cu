@@ -7,6 +7,8 @@
 #include <atomic>
 #include <cstring>
 #include <string>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "wavetune_c.h"
@@ -51,6 +53,29 @@ struct Arena {
         return off;
     }
 };
+
+// Library-owned stream-ordered pool: scratch stays mapped between calls
+// (release threshold = max), so per-call compaction buffers cost nothing
+// after the first call and need no host synchronisation.
+cudaMemPool_t lib_pool(int device) {
+    static std::mutex mu;
+    static std::map<int, cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = pools.find(device);
+    if (it != pools.end()) return it->second;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+        cudaDeviceGetDefaultMemPool(&pool, device);
+    }
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    pools[device] = pool;
+    return pool;
+}
 
 int sm_count(int device) {
     int n = 148;
@@ -488,7 +513,7 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
     DeviceGuard guard(e->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     void* scratch = nullptr;
-    cudaError_t ce = cudaMallocAsync(&scratch, size_t(n + 2) * sizeof(int64_t), s);
+    cudaError_t ce = cudaMallocFromPoolAsync(&scratch, size_t(n + 2) * sizeof(int64_t), lib_pool(e->device), s);
     if (ce != cudaSuccess) return cuda_err(ce, "wt_gather_batch: scratch");
     int64_t* count = static_cast<int64_t*>(scratch);
     int64_t* idx = count + 2;

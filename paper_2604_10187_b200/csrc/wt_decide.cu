@@ -425,17 +425,41 @@ __device__ __forceinline__ int config_of(const DevImage& im, int32_t macro) {
     return lo;
 }
 
+// Off-grid compaction: each CTA buffers indices in shared memory and makes
+// one global atomicAdd per flush (instead of one per warp), so the 1%
+// off-grid slice costs no global atomic contention.
+constexpr int kGBuf = 2048;
+
 __global__ void __launch_bounds__(kGatherThreads) k_gather(DevImage im, GatherArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
     int32_t* pid = reinterpret_cast<int32_t*>(keys + a.n_pairs);
+    __shared__ int64_t buf[kGBuf];
+    __shared__ int cnt;
+    __shared__ unsigned long long gbase;
     for (int i = threadIdx.x; i < a.n_pairs; i += blockDim.x) {
         keys[i] = a.pair_keys[i];
         pid[i] = a.pair_ids[i];
     }
+    if (threadIdx.x == 0) cnt = 0;
     __syncthreads();
+    const DecOut& o = a.out;
+    const bool full = o.wave || o.flags || o.comps || o.tail;  // second half of the entry needed
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     const int64_t n = a.n;
+    const int lane = threadIdx.x & 31;
+
+    auto flush = [&]() {
+        // caller guarantees a preceding __syncthreads()
+        if (threadIdx.x == 0)
+            gbase = atomicAdd(reinterpret_cast<unsigned long long*>(a.off_count), (unsigned long long)cnt);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) a.off_idx[gbase + i] = buf[i];
+        __syncthreads();
+        if (threadIdx.x == 0) cnt = 0;
+        __syncthreads();
+    };
+
     for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
         const int64_t q = base + threadIdx.x;
         const bool live = q < n;
@@ -445,7 +469,6 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(DevImage im, GatherAr
             N = __ldcs(a.N + q);
             K = __ldcs(a.K + q);
         }
-        // pair lookup: binary search over sorted (N, K) keys
         const uint64_t key = (uint64_t(uint32_t(N)) << 32) | uint32_t(K);
         int lo = 0, hi = a.n_pairs;
         while (lo < hi) {
@@ -459,15 +482,17 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(DevImage im, GatherAr
         if (on) {
             const int64_t e = int64_t(pid[lo]) * a.mcount + (M - a.m_lo);
             const int4* src = reinterpret_cast<const int4*>(a.entries + e);
-            const int4 lo4 = __ldg(src), hi4 = __ldg(src + 1);
-            const DecOut& o = a.out;
+            const int4 lo4 = __ldg(src);
             __stcs(o.macro + q, lo4.z);
             __stcs(o.micro + q, lo4.w);
             __stcs(o.lat + q, __hiloint2double(lo4.y, lo4.x));
-            if (o.wave) o.wave[q] = hi4.x;
-            if (o.flags) o.flags[q] = uint32_t(hi4.y);
-            if (o.comps) o.comps[q] = hi4.z;
-            if (o.tail) o.tail[q] = double(__int_as_float(hi4.w));
+            if (full) {
+                const int4 hi4 = __ldg(src + 1);
+                if (o.wave) o.wave[q] = hi4.x;
+                if (o.flags) o.flags[q] = uint32_t(hi4.y);
+                if (o.comps) o.comps[q] = hi4.z;
+                if (o.tail) o.tail[q] = double(__int_as_float(hi4.w));
+            }
             if (o.g || o.l) {
                 const int c = lo4.z >= 0 ? config_of(im, lo4.z) : -1;
                 uint64_t g = 0;
@@ -487,19 +512,20 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(DevImage im, GatherAr
                     o.topk_lat[q * o.topk + z] = a.topk_lat[e * o.topk + z];
                 }
         }
-        // off-grid: warp-aggregated append to the compaction list
         const bool off = live && !on;
         const unsigned mask = __ballot_sync(0xffffffffu, off);
         if (mask) {
-            const int lane = threadIdx.x & 31;
             const int leader = __ffs(mask) - 1;
-            unsigned long long basep = 0;
-            if (lane == leader) basep = atomicAdd(reinterpret_cast<unsigned long long*>(a.off_count),
-                                                  (unsigned long long)__popc(mask));
-            basep = __shfl_sync(0xffffffffu, basep, leader);
-            if (off) a.off_idx[basep + __popc(mask & ((1u << lane) - 1u))] = q;
+            int b = 0;
+            if (lane == leader) b = atomicAdd(&cnt, __popc(mask));
+            b = __shfl_sync(0xffffffffu, b, leader);
+            if (off) buf[b + __popc(mask & ((1u << lane) - 1u))] = q;
         }
+        __syncthreads();
+        if (cnt > kGBuf - int(blockDim.x)) flush();
     }
+    __syncthreads();
+    if (cnt > 0) flush();
 }
 
 // ------------------------------------------------- drop-in per-table helpers
