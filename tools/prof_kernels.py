@@ -1,0 +1,38 @@
+"""Drives one kernel family for an ncu capture (diagnostic; not a bench line).
+usage: python tools/prof_kernels.py {sweep3|eval|gather} [n]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2604_10187_b200 import capi, synthetic as S  # noqa: E402
+
+mode = sys.argv[1]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 1_000_000
+if mode == "sweep3":
+    cfg = S.config_space(True)
+    eng = capi.Engine(S.synthetic_tables(cfg), S.registry_arrays(cfg), n_sm=148)
+    p3 = S.unique_pairs(S.LLAMA3_70B, S.QWEN2_72B)
+    g = capi.Grid(eng, [p[0] for p in p3], [p[1] for p in p3], 1, 65536)
+    for _ in range(3):
+        g.sweep()
+    torch.cuda.synchronize()
+else:
+    cfg = S.config_space(False)
+    eng = capi.Engine(S.synthetic_tables(cfg), S.registry_arrays(cfg), n_sm=148)
+    pairs = S.LLAMA3_8B
+    grid = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 8192)
+    grid.sweep()
+    frac = 1.0 if mode == "eval" else 0.0
+    M, N, K = (torch.from_numpy(x).cuda() for x in S.query_stream(n, pairs, seed=3, off_grid_frac=frac))
+    o = [torch.empty(n, dtype=d, device="cuda") for d in (torch.int32, torch.int32, torch.float64)]
+    d = capi.Engine.decisions(*o)
+    for _ in range(3):
+        if mode == "eval":
+            eng.tune_batch(M, N, K, d)
+        else:
+            grid.gather(M, N, K, d)
+    torch.cuda.synchronize()
+print("done", mode, n)
