@@ -494,8 +494,21 @@ wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, v
     a.topk = g->topk;
     a.topk_macro = g->tk_macro;
     a.topk_lat = g->tk_lat;
-    cudaError_t ce = g->topk > 0 ? launch_sweep(e->dev, a, g->wide, static_cast<cudaStream_t>(stream))
-                                 : launch_sweep2(e->dev, a, g->wide, static_cast<cudaStream_t>(stream));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t ce;
+    if (g->topk > 0) {
+        ce = launch_sweep(e->dev, a, g->wide, s);
+    } else {
+        void* scratch = nullptr;
+        const size_t sb = sweep2_scratch_bytes(e->dev, a);
+        if (sb) {
+            ce = cudaMallocFromPoolAsync(&scratch, sb, lib_pool(e->device), s);
+            if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep: scratch");
+        }
+        ce = launch_sweep2(e->dev, a, g->wide, scratch, s);
+        if (scratch) cudaFreeAsync(scratch, s);
+        if (sb) g_launches++;  // split merge
+    }
     g_launches++;
     if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep");
     return WT_OK;

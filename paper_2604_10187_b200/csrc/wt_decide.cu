@@ -425,107 +425,169 @@ __device__ __forceinline__ int config_of(const DevImage& im, int32_t macro) {
     return lo;
 }
 
-// Off-grid compaction: each CTA buffers indices in shared memory and makes
-// one global atomicAdd per flush (instead of one per warp), so the 1%
-// off-grid slice costs no global atomic contention.
-constexpr int kGBuf = 2048;
+// Off-grid compaction: each warp buffers its off-grid query indices in a
+// shared-memory slice and appends them with one global atomicAdd per ~32
+// entries -- no block-wide barrier and no per-warp atomic on a hot address.
+constexpr int kWarpBuf = 64;
 
+__device__ __forceinline__ void wbuf_push(bool off, int64_t q, int64_t* slice, int& wcnt, const GatherArgs& a,
+                                          int lane) {
+    const unsigned mask = __ballot_sync(0xffffffffu, off);
+    if (off) slice[wcnt + __popc(mask & ((1u << lane) - 1u))] = q;
+    wcnt += __popc(mask);
+    if (wcnt > 32) {
+        __syncwarp();
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(reinterpret_cast<unsigned long long*>(a.off_count), (unsigned long long)wcnt);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (int i = lane; i < wcnt; i += 32) a.off_idx[base + i] = slice[i];
+        __syncwarp();
+        wcnt = 0;
+    }
+}
+
+__device__ __forceinline__ void wbuf_flush(int64_t* slice, int& wcnt, const GatherArgs& a, int lane) {
+    if (wcnt == 0) return;
+    __syncwarp();
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(reinterpret_cast<unsigned long long*>(a.off_count), (unsigned long long)wcnt);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int i = lane; i < wcnt; i += 32) a.off_idx[base + i] = slice[i];
+    __syncwarp();
+    wcnt = 0;
+}
+
+// One query: returns true when answered from the grid (writes optional
+// outputs); the caller stores the required three.
+__device__ __forceinline__ bool gather_one(const DevImage& im, const GatherArgs& a, const uint64_t* keys,
+                                           const int32_t* pid, int64_t q, int32_t M, int32_t N, int32_t K,
+                                           bool full, int4* lo_out) {
+    const uint64_t key = (uint64_t(uint32_t(N)) << 32) | uint32_t(K);
+    int lo = 0, hi = a.n_pairs;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (keys[mid] < key)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    if (!(lo < a.n_pairs && keys[lo] == key && M >= a.m_lo && M <= a.m_hi)) return false;
+    const int64_t e = int64_t(pid[lo]) * a.mcount + (M - a.m_lo);
+    const int4* src = reinterpret_cast<const int4*>(a.entries + e);
+    *lo_out = __ldg(src);
+    const DecOut& o = a.out;
+    if (full) {
+        const int4 hi4 = __ldg(src + 1);
+        if (o.wave) o.wave[q] = hi4.x;
+        if (o.flags) o.flags[q] = uint32_t(hi4.y);
+        if (o.comps) o.comps[q] = hi4.z;
+        if (o.tail) o.tail[q] = double(__int_as_float(hi4.w));
+    }
+    if (o.g || o.l) {
+        const int c = lo_out->z >= 0 ? config_of(im, lo_out->z) : -1;
+        uint64_t g = 0;
+        int64_t l = 0;
+        if (c >= 0) {
+            const int4 tl = __ldg(im.tiles + c);
+            g = uint64_t((uint32_t(M) + uint32_t(tl.x) - 1) / uint32_t(tl.x)) *
+                uint64_t((uint32_t(N) + uint32_t(tl.y) - 1) / uint32_t(tl.y));
+            l = int64_t((uint32_t(K) + uint32_t(tl.z) - 1) / uint32_t(tl.z));
+        }
+        if (o.g) o.g[q] = int64_t(g);
+        if (o.l) o.l[q] = l;
+    }
+    if (o.topk_macro)
+        for (int z = 0; z < o.topk; ++z) {
+            o.topk_macro[q * o.topk + z] = a.topk_macro[e * o.topk + z];
+            o.topk_lat[q * o.topk + z] = a.topk_lat[e * o.topk + z];
+        }
+    return true;
+}
+
+// V = 4: four consecutive queries per thread with 16-byte loads/stores
+// (requires 16-byte aligned arrays); V = 1: scalar.
+template <int V>
 __global__ void __launch_bounds__(kGatherThreads) k_gather(DevImage im, GatherArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
     int32_t* pid = reinterpret_cast<int32_t*>(keys + a.n_pairs);
-    __shared__ int64_t buf[kGBuf];
-    __shared__ int cnt;
-    __shared__ unsigned long long gbase;
+    __shared__ int64_t wbuf[kGatherThreads / 32][kWarpBuf];
     for (int i = threadIdx.x; i < a.n_pairs; i += blockDim.x) {
         keys[i] = a.pair_keys[i];
         pid[i] = a.pair_ids[i];
     }
-    if (threadIdx.x == 0) cnt = 0;
     __syncthreads();
     const DecOut& o = a.out;
-    const bool full = o.wave || o.flags || o.comps || o.tail;  // second half of the entry needed
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    const int64_t n = a.n;
+    const bool full = o.wave || o.flags || o.comps || o.tail;
     const int lane = threadIdx.x & 31;
-
-    auto flush = [&]() {
-        // caller guarantees a preceding __syncthreads()
-        if (threadIdx.x == 0)
-            gbase = atomicAdd(reinterpret_cast<unsigned long long*>(a.off_count), (unsigned long long)cnt);
-        __syncthreads();
-        for (int i = threadIdx.x; i < cnt; i += blockDim.x) a.off_idx[gbase + i] = buf[i];
-        __syncthreads();
-        if (threadIdx.x == 0) cnt = 0;
-        __syncthreads();
-    };
-
-    for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
-        const int64_t q = base + threadIdx.x;
-        const bool live = q < n;
-        int32_t M = 0, N = 0, K = 0;
+    int64_t* slice = wbuf[threadIdx.x >> 5];
+    int wcnt = 0;
+    const int64_t n = a.n;
+    const int64_t nv = n / V;  // full vectors
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < nv; base += stride) {
+        const int64_t v = base + threadIdx.x;
+        const bool live = v < nv;
+        int32_t M[V], N[V], K[V];
+        if constexpr (V == 4) {
+            int4 m4 = make_int4(0, 0, 0, 0), n4 = m4, k4 = m4;
+            if (live) {
+                m4 = __ldcs(reinterpret_cast<const int4*>(a.M) + v);
+                n4 = __ldcs(reinterpret_cast<const int4*>(a.N) + v);
+                k4 = __ldcs(reinterpret_cast<const int4*>(a.K) + v);
+            }
+            M[0] = m4.x; M[1] = m4.y; M[2] = m4.z; M[3] = m4.w;
+            N[0] = n4.x; N[1] = n4.y; N[2] = n4.z; N[3] = n4.w;
+            K[0] = k4.x; K[1] = k4.y; K[2] = k4.z; K[3] = k4.w;
+        } else {
+            M[0] = live ? __ldcs(a.M + v) : 0;
+            N[0] = live ? __ldcs(a.N + v) : 0;
+            K[0] = live ? __ldcs(a.K + v) : 0;
+        }
+        int32_t mac[V], mic[V];
+        double lat[V];
+        bool on[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            int4 lo4 = make_int4(0, 0, -1, -1);
+            on[j] = live && gather_one(im, a, keys, pid, v * V + j, M[j], N[j], K[j], full, &lo4);
+            mac[j] = lo4.z;
+            mic[j] = lo4.w;
+            lat[j] = __hiloint2double(lo4.y, lo4.x);
+        }
         if (live) {
-            M = __ldcs(a.M + q);
-            N = __ldcs(a.N + q);
-            K = __ldcs(a.K + q);
-        }
-        const uint64_t key = (uint64_t(uint32_t(N)) << 32) | uint32_t(K);
-        int lo = 0, hi = a.n_pairs;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (keys[mid] < key)
-                lo = mid + 1;
-            else
-                hi = mid;
-        }
-        const bool on = live && lo < a.n_pairs && keys[lo] == key && M >= a.m_lo && M <= a.m_hi;
-        if (on) {
-            const int64_t e = int64_t(pid[lo]) * a.mcount + (M - a.m_lo);
-            const int4* src = reinterpret_cast<const int4*>(a.entries + e);
-            const int4 lo4 = __ldg(src);
-            __stcs(o.macro + q, lo4.z);
-            __stcs(o.micro + q, lo4.w);
-            __stcs(o.lat + q, __hiloint2double(lo4.y, lo4.x));
-            if (full) {
-                const int4 hi4 = __ldg(src + 1);
-                if (o.wave) o.wave[q] = hi4.x;
-                if (o.flags) o.flags[q] = uint32_t(hi4.y);
-                if (o.comps) o.comps[q] = hi4.z;
-                if (o.tail) o.tail[q] = double(__int_as_float(hi4.w));
+            if constexpr (V == 4) {
+                // off-grid lanes are overwritten later by the evaluation kernel
+                __stcs(reinterpret_cast<int4*>(o.macro) + v, make_int4(mac[0], mac[1], mac[2], mac[3]));
+                __stcs(reinterpret_cast<int4*>(o.micro) + v, make_int4(mic[0], mic[1], mic[2], mic[3]));
+                __stcs(reinterpret_cast<double2*>(o.lat) + 2 * v, make_double2(lat[0], lat[1]));
+                __stcs(reinterpret_cast<double2*>(o.lat) + 2 * v + 1, make_double2(lat[2], lat[3]));
+            } else if (on[0]) {
+                __stcs(o.macro + v, mac[0]);
+                __stcs(o.micro + v, mic[0]);
+                __stcs(o.lat + v, lat[0]);
             }
-            if (o.g || o.l) {
-                const int c = lo4.z >= 0 ? config_of(im, lo4.z) : -1;
-                uint64_t g = 0;
-                int64_t l = 0;
-                if (c >= 0) {
-                    const int4 tl = __ldg(im.tiles + c);
-                    g = uint64_t((uint32_t(M) + uint32_t(tl.x) - 1) / uint32_t(tl.x)) *
-                        uint64_t((uint32_t(N) + uint32_t(tl.y) - 1) / uint32_t(tl.y));
-                    l = int64_t((uint32_t(K) + uint32_t(tl.z) - 1) / uint32_t(tl.z));
-                }
-                if (o.g) o.g[q] = int64_t(g);
-                if (o.l) o.l[q] = l;
-            }
-            if (o.topk_macro)
-                for (int z = 0; z < o.topk; ++z) {
-                    o.topk_macro[q * o.topk + z] = a.topk_macro[e * o.topk + z];
-                    o.topk_lat[q * o.topk + z] = a.topk_lat[e * o.topk + z];
-                }
         }
-        const bool off = live && !on;
-        const unsigned mask = __ballot_sync(0xffffffffu, off);
-        if (mask) {
-            const int leader = __ffs(mask) - 1;
-            int b = 0;
-            if (lane == leader) b = atomicAdd(&cnt, __popc(mask));
-            b = __shfl_sync(0xffffffffu, b, leader);
-            if (off) buf[b + __popc(mask & ((1u << lane) - 1u))] = q;
-        }
-        __syncthreads();
-        if (cnt > kGBuf - int(blockDim.x)) flush();
+#pragma unroll
+        for (int j = 0; j < V; ++j) wbuf_push(live && !on[j], v * V + j, slice, wcnt, a, lane);
     }
-    __syncthreads();
-    if (cnt > 0) flush();
+    // scalar tail (n % V queries), handled by the first warp of block 0
+    if (V > 1 && blockIdx.x == 0 && threadIdx.x < 32) {
+        const int64_t q = nv * V + threadIdx.x;
+        const bool live = q < n;
+        bool on = false;
+        if (live) {
+            int4 lo4;
+            on = gather_one(im, a, keys, pid, q, a.M[q], a.N[q], a.K[q], full, &lo4);
+            if (on) {
+                o.macro[q] = lo4.z;
+                o.micro[q] = lo4.w;
+                o.lat[q] = __hiloint2double(lo4.y, lo4.x);
+            }
+        }
+        wbuf_push(live && !on, q, slice, wcnt, a, lane);
+    }
+    wbuf_flush(slice, wcnt, a, lane);
 }
 
 // ------------------------------------------------- drop-in per-table helpers
@@ -679,7 +741,11 @@ cudaError_t launch_grouped(const DevImage& im, const GroupedArgs& a, int grid, c
 
 cudaError_t launch_gather(const DevImage& im, const GatherArgs& a, int grid, cudaStream_t st) {
     const size_t smem = size_t(a.n_pairs) * (sizeof(uint64_t) + sizeof(int32_t)) + 16;
-    k_gather<<<grid, kGatherThreads, smem, st>>>(im, a);
+    const auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+    if (al16(a.M) && al16(a.N) && al16(a.K) && al16(a.out.macro) && al16(a.out.micro) && al16(a.out.lat))
+        k_gather<4><<<grid, kGatherThreads, smem, st>>>(im, a);
+    else
+        k_gather<1><<<grid, kGatherThreads, smem, st>>>(im, a);
     return cudaGetLastError();
 }
 

@@ -118,7 +118,8 @@ cudaError_t launch_eval(const DevImage& im, const EvalArgs& a, int grid, cudaStr
 cudaError_t launch_grouped(const DevImage& im, const GroupedArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_gather(const DevImage& im, const GatherArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_predict(const DevImage& im, const PredictArgs& a, cudaStream_t st);
-cudaError_t launch_sweep2(const DevImage& im, const SweepArgs& a, bool wide, cudaStream_t st);
+size_t sweep2_scratch_bytes(const DevImage& im, const SweepArgs& a);
+cudaError_t launch_sweep2(const DevImage& im, const SweepArgs& a, bool wide, void* scratch, cudaStream_t st);
 cudaError_t launch_eval2(const DevImage& im, const EvalArgs& a, int grid, cudaStream_t st);
 int eval2_tile();
 cudaError_t launch_explain(const DevImage& im, const ExplainArgs& a, cudaStream_t st);

@@ -7,17 +7,21 @@
 //     3 DMUL + 3 DADD (+1 DMUL for gamma*l in list mode) + DSETP + 3 SEL.
 // Classes are cut into segments of <= kSegCfg configs kept in ascending
 // macro_id order, so the segment-local argmin is the reference's strict-<
-// scan; segments are merged with the lexicographic (latency, config index)
-// order, which is exactly "first minimum in ascending macro_id"
-// (tuner.cpp:135-149): NaN never wins, -0 == +0 keeps the smaller id.
+// scan; segments (and config splits) are merged with the lexicographic
+// (latency, config index) order, which is exactly "first minimum in ascending
+// macro_id" (tuner.cpp:135-149): NaN never wins, -0 == +0 keeps the smaller id.
 //
 //   k_sweep2  grid mode: lanes = consecutive M of one (N, K) pair; per tile
 //             only the coefficient rows the tile's G range can touch are
-//             staged (row-range staging), gamma*l folded in.
+//             staged ([row][config] layout, gamma*l folded in).  Work units
+//             are (shape tile, config split) so the grid has several waves of
+//             equal units; splits are merged by k_merge.
 //   k_eval2   list mode: lanes = arbitrary queries; every row of a segment is
 //             staged in a [row][config] layout whose row stride is an odd
 //             number of 16-byte slots, so lanes hitting random rows spread
 //             over all shared-memory banks.
+// Inner loops are written phase by phase across the RPT independent shapes so
+// the dependent DMUL/DADD chains of different shapes interleave.
 #include <cuda_runtime.h>
 
 #include <cub/block/block_scan.cuh>
@@ -28,27 +32,36 @@
 
 namespace wtb {
 
-
 namespace {
 
-constexpr int kT2 = 256;  // threads per CTA for both kernels
+constexpr int kT2 = 256;  // threads per CTA
 
 struct SegHdr {  // one staged segment
     uint32_t mM, sM, nt, rowlo;
-    int32_t ncfg, pos, off, stride;  // off/stride in double4 units
+    int32_t ncfg, pos, off, stride;
     double ld;
-    uint32_t mN, mK, sNK, pad;
+    uint32_t mN, mK, pad0, pad1;
 };
 
 __device__ __forceinline__ bool lex_less(double a, int ia, double b, int ib) {
     return a < b || (a == b && ia < ib);
 }
 
+constexpr double kInf = __builtin_huge_val();
+
 }  // namespace
+
+struct Part {  // per-split partial argmins, [S][n]
+    int32_t S;
+    double* lat;
+    int32_t* cfg;
+    uint32_t* acc;
+};
 
 // ------------------------------------------------------------- sweep (grid)
 template <int RPT, bool SPECIAL, bool WIDE>
-__global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int cap_rows) {
+__global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int cap_rows, Part part,
+                                                int64_t ntiles) {
     extern __shared__ __align__(16) unsigned char smem[];
     SegHdr* hdr = reinterpret_cast<SegHdr*>(smem);
     double4* rows = reinterpret_cast<double4*>(hdr + kT2);
@@ -57,8 +70,13 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
     __shared__ typename Scan::TempStorage scan_tmp;
 
     const int tid = threadIdx.x;
+    const int64_t unit = blockIdx.x;
+    const int64_t tl = unit % ntiles;
+    const int split = int(unit / ntiles);
+    const int seg_lo = int(int64_t(im.nseg) * split / part.S);
+    const int seg_hi = int(int64_t(im.nseg) * (split + 1) / part.S);
     const int64_t tile = int64_t(kT2) * RPT;
-    const int64_t t0 = a.begin + int64_t(blockIdx.x) * tile;
+    const int64_t t0 = a.begin + tl * tile;
     const int64_t t1 = min(t0 + tile, a.end);
     const uint32_t RS = im.RS, mS = im.mS, sS = im.sS;
     const int R = im.R;
@@ -78,18 +96,18 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
             const int64_t idx = seg0 + int64_t(j) * kT2 + tid;
             const uint32_t M = idx < seg_end ? uint32_t(a.m_lo + (idx - int64_t(p) * a.mcount)) : Mlo;
             y2[j] = 2u * (M - 1u);
-            best[j] = __longlong_as_double(0x7ff0000000000000LL);
+            best[j] = kInf;
             bc[j] = -1;
             acc[j] = 0;
         }
 
-        for (int s0 = 0; s0 < im.nseg;) {
+        for (int s0 = seg_lo; s0 < seg_hi;) {
             // -- plan this staging round: segments s0.. whose row ranges fit
             const int s = s0 + tid;
             int need = 0;
             uint32_t rlo = 0, nt = 0, mM = 0, sM = 0, lk = 1;
             int4 st = make_int4(0, 0, 0, 0);
-            if (s < im.nseg) {
+            if (s < seg_hi) {
                 st = __ldg(im.seg_tiles + s);
                 const uint4 mg = __ldg(im.seg_magic + s);
                 mM = mg.x;
@@ -104,9 +122,9 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
             }
             int off;
             Scan(scan_tmp).ExclusiveSum(need, off);
-            const int fits = (s < im.nseg) && (off + need <= cap_rows);
+            const int fits = (s < seg_hi) && (off + need <= cap_rows);
             const int count = max(1, __syncthreads_count(fits));
-            if (tid < count && s < im.nseg) {
+            if (tid < count && s < seg_hi) {
                 SegHdr h;
                 h.mM = mM;
                 h.sM = sM;
@@ -115,18 +133,18 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
                 h.ncfg = st.w;
                 h.pos = __ldg(im.seg_pos + s);
                 h.off = off;
-                h.stride = need / max(st.w, 1);  // rows per config in this tile
+                h.stride = need / max(st.w, 1);  // rows of this segment in the tile
                 h.ld = u32_to_f64(lk);
                 hdr[tid] = h;
             }
             __syncthreads();
-            // -- stage rows [rowlo, rowlo+stride) of every config, gamma*l folded
+            // -- stage rows [rowlo, rowlo + nrows) as [row][config], gamma*l folded
             for (int k = 0; k < count; ++k) {
                 const SegHdr h = hdr[k];
                 const int n = h.stride * h.ncfg;
                 for (int i = tid; i < n; i += kT2) {
-                    const int j = i / h.stride, r = i - j * h.stride;
-                    const size_t src = size_t(h.pos + j) * R + h.rowlo + r;
+                    const int r = i / h.ncfg, c = i - r * h.ncfg;
+                    const size_t src = size_t(h.pos + c) * R + h.rowlo + r;
                     double4 th = ldg_row(im.theta2 + src);
                     th.z = __dmul_rn(th.z, h.ld);
                     rows[h.off + i] = th;
@@ -137,7 +155,8 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
             // -- evaluate
             for (int k = 0; k < count; ++k) {
                 const SegHdr h = hdr[k];
-                int base[RPT];
+                const double4* pr[RPT];
+                const uint32_t* pm[RPT];
                 double gd[RPT], sb[RPT];
                 int sj[RPT];
 #pragma unroll
@@ -153,22 +172,38 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
                         gc = min(g, RS);
                         gd[j] = u32_to_f64(g);
                     }
-                    base[j] = h.off + int(row_of(gc, mS, sS) - h.rowlo);
-                    sb[j] = __longlong_as_double(0x7ff0000000000000LL);
+                    const int r = int(row_of(gc, mS, sS) - h.rowlo);
+                    pr[j] = rows + h.off + r * h.ncfg;
+                    pm[j] = meta + h.off + r * h.ncfg;
+                    sb[j] = kInf;
                     sj[j] = -1;
                 }
                 const double ld = h.ld;
 #pragma unroll 2
                 for (int c = 0; c < h.ncfg; ++c) {
+                    double4 th[RPT];
+                    double t[RPT], u[RPT];
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) th[j] = pr[j][c];
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) t[j] = __dmul_rn(th[j].x, gd[j]);
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) u[j] = __dmul_rn(th[j].y, gd[j]);
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) t[j] = __dmul_rn(t[j], ld);
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) t[j] = __dadd_rn(t[j], u[j]);
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) t[j] = __dadd_rn(t[j], th[j].z);
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) t[j] = __dadd_rn(t[j], th[j].w);
 #pragma unroll
                     for (int j = 0; j < RPT; ++j) {
-                        const double4 th = rows[base[j] + c * h.stride];
-                        const double t = bilinear(th.x, th.y, th.z, th.w, gd[j], ld);
-                        if (t < sb[j]) {
-                            sb[j] = t;
+                        if (t[j] < sb[j]) {
+                            sb[j] = t[j];
                             sj[j] = c;
                         }
-                        if constexpr (SPECIAL) acc[j] |= meta[base[j] + c * h.stride];
+                        if constexpr (SPECIAL) acc[j] |= pm[j][c];
                     }
                 }
 #pragma unroll
@@ -186,20 +221,26 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
             s0 += count;
         }
 
-        // epilogue: Stage II per winner, one 32-byte entry per shape
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
             const int64_t idx = seg0 + int64_t(j) * kT2 + tid;
             if (idx >= seg_end) continue;
+            if (part.S > 1) {  // partial argmin of this config split
+                const size_t o = size_t(split) * size_t(a.end - a.begin) + size_t(idx - a.begin);
+                part.lat[o] = best[j];
+                part.cfg[o] = bc[j];
+                part.acc[o] = acc[j];
+                continue;
+            }
             const int c = bc[j];
             uint64_t g = 0;
             int64_t l = 0;
             if (c >= 0) {
-                const int4 tl = __ldg(im.tiles + c);
+                const int4 tl4 = __ldg(im.tiles + c);
                 const uint32_t M = y2[j] / 2u + 1u;
-                g = uint64_t((M + uint32_t(tl.x) - 1) / uint32_t(tl.x)) *
-                    uint64_t((uint64_t(Np) + uint32_t(tl.y) - 1) / uint32_t(tl.y));
-                l = int64_t((uint64_t(Kp) + uint32_t(tl.z) - 1) / uint32_t(tl.z));
+                g = uint64_t((M + uint32_t(tl4.x) - 1) / uint32_t(tl4.x)) *
+                    uint64_t((uint64_t(Np) + uint32_t(tl4.y) - 1) / uint32_t(tl4.y));
+                l = int64_t((uint64_t(Kp) + uint32_t(tl4.z) - 1) / uint32_t(tl4.z));
             }
             const Final f = finish(im, c, 0.0, g, l, acc[j]);
             const bool ok = (f.flags >> 24) == 0;
@@ -221,13 +262,60 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
     }
 }
 
+// Merge of the config splits + Stage II epilogue (grid mode).
+__global__ void k_sweep_merge(DevImage im, SweepArgs a, Part part) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t n = a.end - a.begin;
+    if (i >= n) return;
+    double best = kInf;
+    int bc = -1;
+    uint32_t acc = 0;
+    for (int s = 0; s < part.S; ++s) {
+        const size_t o = size_t(s) * size_t(n) + size_t(i);
+        const int c = part.cfg[o];
+        const double v = part.lat[o];
+        acc |= part.acc[o];
+        if (c >= 0 && lex_less(v, c, best, bc < 0 ? INT32_MAX : bc)) {
+            best = v;
+            bc = c;
+        }
+    }
+    const int64_t idx = a.begin + i;
+    const int32_t p = int32_t(idx / a.mcount);
+    const uint32_t M = uint32_t(a.m_lo + (idx - int64_t(p) * a.mcount));
+    const uint32_t Np = uint32_t(a.N[p]), Kp = uint32_t(a.K[p]);
+    uint64_t g = 0;
+    int64_t l = 0;
+    if (bc >= 0) {
+        const int4 tl4 = __ldg(im.tiles + bc);
+        g = uint64_t((M + uint32_t(tl4.x) - 1) / uint32_t(tl4.x)) *
+            uint64_t((uint64_t(Np) + uint32_t(tl4.y) - 1) / uint32_t(tl4.y));
+        l = int64_t((uint64_t(Kp) + uint32_t(tl4.z) - 1) / uint32_t(tl4.z));
+    }
+    const Final f = finish(im, bc, 0.0, g, l, acc);
+    const bool ok = (f.flags >> 24) == 0;
+    const double lat = ok ? best : __longlong_as_double(0x7ff8000000000000LL);
+    int4 lo, hi;
+    lo.x = __double2loint(lat);
+    lo.y = __double2hiint(lat);
+    lo.z = f.macro;
+    lo.w = f.micro;
+    hi.x = f.wave;
+    hi.y = int(f.flags);
+    hi.z = f.comps;
+    hi.w = __float_as_int(f.tail);
+    int4* e = reinterpret_cast<int4*>(a.entries + idx);
+    e[0] = lo;
+    e[1] = hi;
+}
+
 // --------------------------------------------------------------- eval (list)
 template <int RPT, bool SPECIAL>
 __global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_rows) {
     extern __shared__ __align__(16) unsigned char smem[];
     SegHdr* hdr = reinterpret_cast<SegHdr*>(smem);
-    double4* rows = reinterpret_cast<double4*>(hdr + kT2);
-    uint32_t* meta = reinterpret_cast<uint32_t*>(rows + cap_rows);
+    double2* slots = reinterpret_cast<double2*>(hdr + kT2);
+    uint32_t* meta = reinterpret_cast<uint32_t*>(slots + 2 * size_t(cap_rows));
     using Scan = cub::BlockScan<int, kT2>;
     __shared__ typename Scan::TempStorage scan_tmp;
 
@@ -248,26 +336,26 @@ __global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_
             const int64_t slot = tl * tile + int64_t(j) * kT2 + tid;
             const bool live = slot < n;
             q[j] = live ? (a.idx ? a.idx[slot] : slot) : -1;
-            uint32_t M = 1, N = 1, K = 1, st = 0;
+            uint32_t M = 1, N = 1, K = 1, stv = 0;
             if (live) {
                 const int32_t m = a.M[q[j]], nn = a.N[q[j]], k = a.K[q[j]];
                 if (m < 1 || nn < 1 || k < 1) {
-                    st = WT_INVALID_ARGUMENT;  // kernel_map.cpp:238-239
+                    stv = WT_INVALID_ARGUMENT;  // kernel_map.cpp:238-239
                 } else {
                     M = uint32_t(m);
                     N = uint32_t(nn);
                     K = uint32_t(k);
                     const uint64_t gmax = uint64_t((M + uint32_t(im.tm_min) - 1) / uint32_t(im.tm_min)) *
                                           uint64_t((N + uint32_t(im.tn_min) - 1) / uint32_t(im.tn_min));
-                    if ((gmax + uint64_t(im.S) - 1) / uint64_t(im.S) >= (uint64_t(1) << 31)) st = WT_UNSUPPORTED;
+                    if ((gmax + uint64_t(im.S) - 1) / uint64_t(im.S) >= (uint64_t(1) << 31)) stv = WT_UNSUPPORTED;
                 }
             }
-            if (st) M = N = K = 1;
+            if (stv) M = N = K = 1;
             y2M[j] = 2u * (M - 1u);
             y2N[j] = 2u * (N - 1u);
             y2K[j] = 2u * (K - 1u);
-            status[j] = st;
-            best[j] = __longlong_as_double(0x7ff0000000000000LL);
+            status[j] = stv;
+            best[j] = kInf;
             bc[j] = -1;
             acc[j] = 0;
         }
@@ -279,7 +367,7 @@ __global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_
             if (s < im.nseg) {
                 st = __ldg(im.seg_tiles + s);
                 mg = __ldg(im.seg_magic + s);
-                need = R * (2 * st.w + 1);  // [row][config] double4 halves + one pad slot per row
+                need = R * (2 * st.w + 1);  // 16-byte slots: [row][config] halves + one pad per row
             }
             int off;
             Scan(scan_tmp).ExclusiveSum(need, off);
@@ -293,12 +381,11 @@ __global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_
                 h.sM = mg.w;
                 h.ncfg = st.w;
                 h.pos = __ldg(im.seg_pos + s);
-                h.off = off;                // in 16-byte slots
-                h.stride = 2 * st.w + 1;    // slots per row (odd)
+                h.off = off;
+                h.stride = 2 * st.w + 1;  // odd
                 hdr[tid] = h;
             }
             __syncthreads();
-            double2* slots = reinterpret_cast<double2*>(rows);
             for (int k = 0; k < count; ++k) {
                 const SegHdr h = hdr[k];
                 const int n2 = R * h.ncfg;
@@ -316,10 +403,10 @@ __global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_
             for (int k = 0; k < count; ++k) {
                 const SegHdr h = hdr[k];
                 const uint32_t sMv = h.sM & 0xffu, sNv = (h.sM >> 8) & 0xffu, sKv = (h.sM >> 16) & 0xffu;
-                int base[RPT];
+                const double2* pr[RPT];
+                const uint32_t* pm[RPT];
                 double gd[RPT], ld[RPT], sb[RPT];
                 int sj[RPT];
-                int rowi[RPT];
 #pragma unroll
                 for (int j = 0; j < RPT; ++j) {
                     const uint32_t mt = mdiv2(y2M[j], h.mM, sMv) + 1u;
@@ -327,25 +414,43 @@ __global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_
                     const uint32_t lk = mdiv2(y2K[j], h.mK, sKv) + 1u;
                     const uint64_t g = uint64_t(mt) * nt;
                     const uint32_t gc = g > RS ? RS : uint32_t(g);
-                    rowi[j] = int(row_of(gc, mS, sS));
-                    base[j] = h.off + rowi[j] * h.stride;
+                    const int r = int(row_of(gc, mS, sS));
+                    pr[j] = slots + h.off + r * h.stride;
+                    pm[j] = meta + h.off / 2 + r * h.ncfg;
                     gd[j] = u64_to_f64(g);
                     ld[j] = u32_to_f64(lk);
-                    sb[j] = __longlong_as_double(0x7ff0000000000000LL);
+                    sb[j] = kInf;
                     sj[j] = -1;
                 }
 #pragma unroll 2
                 for (int c = 0; c < h.ncfg; ++c) {
+                    double2 ab[RPT], gw[RPT];
+                    double t[RPT], u[RPT], v[RPT];
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) ab[j] = pr[j][2 * c];
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) gw[j] = pr[j][2 * c + 1];
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) t[j] = __dmul_rn(ab[j].x, gd[j]);
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) u[j] = __dmul_rn(ab[j].y, gd[j]);
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) v[j] = __dmul_rn(gw[j].x, ld[j]);
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) t[j] = __dmul_rn(t[j], ld[j]);
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) t[j] = __dadd_rn(t[j], u[j]);
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) t[j] = __dadd_rn(t[j], v[j]);
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) t[j] = __dadd_rn(t[j], gw[j].y);
 #pragma unroll
                     for (int j = 0; j < RPT; ++j) {
-                        const double2 ab = slots[base[j] + 2 * c];
-                        const double2 gd2 = slots[base[j] + 2 * c + 1];
-                        const double t = bilinear(ab.x, ab.y, __dmul_rn(gd2.x, ld[j]), gd2.y, gd[j], ld[j]);
-                        if (t < sb[j]) {
-                            sb[j] = t;
+                        if (t[j] < sb[j]) {
+                            sb[j] = t[j];
                             sj[j] = c;
                         }
-                        if constexpr (SPECIAL) acc[j] |= meta[h.off / 2 + rowi[j] * h.ncfg + c];
+                        if constexpr (SPECIAL) acc[j] |= pm[j][c];
                     }
                 }
 #pragma unroll
@@ -404,41 +509,74 @@ namespace {
 constexpr int kSweepRPT2 = 4;
 constexpr int kEvalRPT2 = 4;
 constexpr size_t kSmem2 = 96 * 1024;  // per CTA: 2 CTAs per SM
+int n_sms() {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+}
+}  // namespace
+
+// Work decomposition of a sweep: tiles x config splits, sized so the grid is
+// several waves of equal units (2 CTAs / SM resident).
+void sweep2_plan(const DevImage& im, const SweepArgs& a, int64_t* ntiles, int* splits) {
+    const int64_t n = a.end - a.begin;
+    *ntiles = (n + int64_t(kT2) * kSweepRPT2 - 1) / (int64_t(kT2) * kSweepRPT2);
+    const int64_t target = int64_t(n_sms()) * 2 * 4;
+    int S = int((target + *ntiles - 1) / *ntiles);
+    S = max(1, min(S, im.nseg));
+    *splits = S;
 }
 
-size_t sweep2_smem(const DevImage& im, int* cap_rows) {
-    const size_t avail = kSmem2 - kT2 * sizeof(SegHdr);
-    const size_t per_row = sizeof(double4) + (im.special ? 4 : 0);
-    *cap_rows = int(avail / per_row);
-    return kSmem2;
+size_t sweep2_scratch_bytes(const DevImage& im, const SweepArgs& a) {
+    int64_t nt;
+    int S;
+    sweep2_plan(im, a, &nt, &S);
+    if (S <= 1) return 0;
+    return size_t(S) * size_t(a.end - a.begin) * (sizeof(double) + 2 * sizeof(int32_t)) + 256;
 }
 
 template <int RPT, bool SP, bool WIDE>
-static cudaError_t go_sweep2(const DevImage& im, const SweepArgs& a, int grid, cudaStream_t st) {
-    int cap;
-    const size_t smem = sweep2_smem(im, &cap);
+static cudaError_t go_sweep2(const DevImage& im, const SweepArgs& a, int64_t units, int cap, Part part,
+                             int64_t ntiles, cudaStream_t st) {
     auto fn = k_sweep2<RPT, SP, WIDE>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem2));
     if (e != cudaSuccess) return e;
-    fn<<<grid, kT2, smem, st>>>(im, a, cap);
+    fn<<<unsigned(units), kT2, kSmem2, st>>>(im, a, cap, part, ntiles);
     return cudaGetLastError();
 }
 
-cudaError_t launch_sweep2(const DevImage& im, const SweepArgs& a, bool wide, cudaStream_t st) {
+cudaError_t launch_sweep2(const DevImage& im, const SweepArgs& a, bool wide, void* scratch, cudaStream_t st) {
     const int64_t n = a.end - a.begin;
     if (n <= 0) return cudaSuccess;
-    const int grid = int((n + int64_t(kT2) * kSweepRPT2 - 1) / (int64_t(kT2) * kSweepRPT2));
+    int64_t ntiles;
+    int S;
+    sweep2_plan(im, a, &ntiles, &S);
+    Part part{S, nullptr, nullptr, nullptr};
+    if (S > 1) {
+        char* b = static_cast<char*>(scratch);
+        part.lat = reinterpret_cast<double*>(b);
+        part.cfg = reinterpret_cast<int32_t*>(part.lat + size_t(S) * n);
+        part.acc = reinterpret_cast<uint32_t*>(part.cfg + size_t(S) * n);
+    }
+    const size_t avail = kSmem2 - kT2 * sizeof(SegHdr);
+    const int cap = int(avail / (sizeof(double4) + (im.special ? 4 : 0)));
+    const int64_t units = ntiles * S;
     const bool sp = im.special != 0;
-    if (wide) return sp ? go_sweep2<kSweepRPT2, true, true>(im, a, grid, st) : go_sweep2<kSweepRPT2, false, true>(im, a, grid, st);
-    return sp ? go_sweep2<kSweepRPT2, true, false>(im, a, grid, st) : go_sweep2<kSweepRPT2, false, false>(im, a, grid, st);
+    cudaError_t e;
+    if (wide) e = sp ? go_sweep2<kSweepRPT2, true, true>(im, a, units, cap, part, ntiles, st)
+                     : go_sweep2<kSweepRPT2, false, true>(im, a, units, cap, part, ntiles, st);
+    else e = sp ? go_sweep2<kSweepRPT2, true, false>(im, a, units, cap, part, ntiles, st)
+                : go_sweep2<kSweepRPT2, false, false>(im, a, units, cap, part, ntiles, st);
+    if (e != cudaSuccess || S <= 1) return e;
+    k_sweep_merge<<<unsigned((n + 255) / 256), 256, 0, st>>>(im, a, part);
+    return cudaGetLastError();
 }
 
 template <int RPT, bool SP>
 static cudaError_t go_eval2(const DevImage& im, const EvalArgs& a, int grid, cudaStream_t st) {
     const size_t avail = kSmem2 - kT2 * sizeof(SegHdr);
-    // rows are counted in double4 units; the list layout uses 16-byte slots
-    const size_t per_row = sizeof(double4) + (SP ? 8 : 0);
-    const int cap = int(avail / per_row);
+    const int cap = int(avail / (sizeof(double4) + (SP ? 8 : 0)));  // 32-byte units (2 slots)
     auto fn = k_eval2<RPT, SP>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem2));
     if (e != cudaSuccess) return e;
