@@ -138,8 +138,9 @@ def test_errors_match_reference(wt, registry):
         wt.tune(wt.DenseGemm(64, 64, 64), art, registry, hw)
     with pytest.raises(ValueError, match="empty anchor list"):
         wt.nearest_anchor([], 1)
-    assert wt.nearest_anchor([16, 32, 64], 40) == (32, 2)
-    assert wt.nearest_anchor([32, 64], 48)[0] == 32
+    ref = po.Reference()
+    for anchors, l in (([16, 32, 64], 40), ([32, 64], 48), ([32, 64], 5), ([32, 64], 500), ([7], 1000)):
+        assert wt.nearest_anchor(anchors, l) == ref.nearest_anchor(anchors, l)
     lat, regime = wt.predict_latency(t, 100, 50, wt.HardwareSpec(4096))
     assert abs(lat - 120.0) < 1e-9
 
