@@ -24,6 +24,7 @@
 // the dependent DMUL/DADD chains of different shapes interleave.
 #include <cuda_runtime.h>
 
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 #include <cstdint>
 
@@ -317,7 +318,9 @@ __global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_
     double2* slots = reinterpret_cast<double2*>(hdr + kT2);
     uint32_t* meta = reinterpret_cast<uint32_t*>(slots + 2 * size_t(cap_rows));
     using Scan = cub::BlockScan<int, kT2>;
+    using Sort = cub::BlockRadixSort<uint32_t, kT2, RPT, int32_t>;
     __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ typename Sort::TempStorage sort_tmp;
 
     const int64_t n = a.count ? *a.count : a.n;
     const int64_t tile = int64_t(kT2) * RPT;
@@ -327,13 +330,34 @@ __global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_
     const int tid = threadIdx.x;
 
     for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+        // Order the tile's queries by M*N: lanes of a warp then hold shapes
+        // with near-equal G for every tile class, so their coefficient rows
+        // coincide and the shared-memory loads become broadcasts.
+        int32_t perm[RPT];
+        {
+            uint32_t key[RPT];
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) {
+                const int64_t slot = tl * tile + int64_t(tid) * RPT + j;
+                uint32_t k = 0xffffffffu;
+                if (slot < n) {
+                    const int64_t qq = a.idx ? a.idx[slot] : slot;
+                    const int32_t m = a.M[qq], nn = a.N[qq];
+                    if (m >= 1 && nn >= 1) k = __float_as_uint(__fmul_rn(float(m), float(nn)));
+                }
+                key[j] = k;
+                perm[j] = tid * RPT + j;
+            }
+            __syncthreads();  // sort_tmp is reused across tiles
+            Sort(sort_tmp).SortBlockedToStriped(key, perm, 14, 32);
+        }
         int64_t q[RPT];
         uint32_t y2M[RPT], y2N[RPT], y2K[RPT], status[RPT], acc[RPT];
         double best[RPT];
         int bc[RPT];
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
-            const int64_t slot = tl * tile + int64_t(j) * kT2 + tid;
+            const int64_t slot = tl * tile + perm[j];
             const bool live = slot < n;
             q[j] = live ? (a.idx ? a.idx[slot] : slot) : -1;
             uint32_t M = 1, N = 1, K = 1, stv = 0;
