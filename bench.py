@@ -303,24 +303,57 @@ def run_wavetune(args):
     # secondary: config-3 sweep (4608 configs x 6 pairs x M=1..65536) evals/s
     sec = {}
     if not args.skip_secondary:
+        # config 4: batched fit of the 4608-config table set from ~3.0M
+        # wave-structured samples (K2; device time from records in HBM)
         cfg3 = S.config_space(full=True)
-        t3 = S.synthetic_tables(cfg3)
+        rec4 = S.synthetic_records(cfg3, micros_per_macro=1)
+        fit = capi.fit_build(rec4, cfg3["id"], 40, 10, device=local)  # warm-up
+        fit = capi.fit_build(rec4, cfg3["id"], 40, 10, device=local)
+        t3 = {k: fit[k] for k in ("macro_id", "theta_ext", "coeff_off", "coeff_w", "coeff_theta", "awave_off",
+                                   "awave_w", "awave_aoff", "anchor_l", "anchor_micro", "ext_aoff", "ext_l",
+                                   "ext_micro")}
+        t3["W"] = fit["W_arr"]
+        # config 3: sweep of the fitted tables over 6 pairs x M=1..65536,
+        # shape index sharded across ranks + NCCL all-gather when N > 1
         eng3 = capi.Engine(t3, S.registry_arrays(cfg3), n_sm=148, device=local)
         p3 = S.unique_pairs(S.LLAMA3_70B, S.QWEN2_72B)
         g3 = capi.Grid(eng3, [p[0] for p in p3], [p[1] for p in p3], 1, 65536)
-        g3.sweep(stream=stream)
-        e0.record(stream)
-        g3.sweep(stream=stream)
-        e1.record(stream)
+        if ws > 1:
+            from paper_2604_10187_b200.dist import sharded_sweep
+
+            sharded_sweep(g3, stream=stream)
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            e0.record(stream)
+            sharded_sweep(g3, stream=stream)
+            e1.record(stream)
+        else:
+            g3.sweep(stream=stream)
+            e0.record(stream)
+            g3.sweep(stream=stream)
+            e1.record(stream)
         torch.cuda.synchronize(dev)
         ms3 = e0.elapsed_time(e1)
+        if ws > 1:
+            t = torch.tensor([ms3, fit["device_ms"]], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms3, fit_ms = (float(x) for x in t.tolist())
+        else:
+            fit_ms = fit["device_ms"]
         evals3 = g3.n_entries * eng3.n_configs
         sec = {
             "config1_sweep": {"ms": sweep_ms, "evals": grid.n_entries * eng.n_configs,
                               "evals_per_s": grid.n_entries * eng.n_configs / (sweep_ms * 1e-3)},
             "config3_sweep": {"ms": ms3, "evals": evals3, "evals_per_s": evals3 / (ms3 * 1e-3),
                               "fp64_flop_per_s": 7.0 * evals3 / (ms3 * 1e-3),
-                              "shapes": g3.n_entries, "configs": eng3.n_configs},
+                              "fp64_frac_of_18.6TF": 7.0 * evals3 / (ms3 * 1e-3) / 18.6e12,
+                              "shapes": g3.n_entries, "configs": eng3.n_configs,
+                              "sharding": f"shape slices x{ws} + NCCL all_gather" if ws > 1 else "single GPU"},
+            "config4_fit": {"ms": fit_ms, "records": int(len(rec4["g"])), "tables": int(fit["n_tables"]),
+                            "buckets": int(len(fit["coeff_w"])),
+                            "median_bucket_mape": float(np.median(fit["diag_mape"])),
+                            "median_bucket_r2": float(np.median(fit["diag_r2"]))},
+            "full_build_ms": fit_ms + ms3,
         }
         g3.close()
         eng3.close()

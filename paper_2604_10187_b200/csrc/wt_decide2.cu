@@ -383,6 +383,14 @@ __global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_
             bc[j] = -1;
             acc[j] = 0;
         }
+        uint32_t cM = 0, cN = 0, cS = 0, cK = 0, cSK = 0;  // magic m is never 0: "nothing cached"
+        int rowc[RPT];
+        double gd[RPT], ld[RPT];
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            rowc[j] = 0;
+            gd[j] = ld[j] = 0.0;
+        }
         for (int s0 = 0; s0 < im.nseg;) {
             const int s = s0 + tid;
             int need = 0;
@@ -427,22 +435,36 @@ __global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_
             for (int k = 0; k < count; ++k) {
                 const SegHdr h = hdr[k];
                 const uint32_t sMv = h.sM & 0xffu, sNv = (h.sM >> 8) & 0xffu, sKv = (h.sM >> 16) & 0xffu;
+                // G / row / (double)G change only with (t_m, t_n); L only with t_k
+                // (classes are ordered by (t_m, t_n, t_k)): segment-uniform branches
+                if (h.mM != cM || h.mN != cN || (h.sM & 0xffffu) != cS) {
+                    cM = h.mM;
+                    cN = h.mN;
+                    cS = h.sM & 0xffffu;
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) {
+                        const uint32_t mt = mdiv2(y2M[j], h.mM, sMv) + 1u;
+                        const uint32_t nt = mdiv2(y2N[j], h.mN, sNv) + 1u;
+                        const uint64_t g = uint64_t(mt) * nt;
+                        const uint32_t gc = g > RS ? RS : uint32_t(g);
+                        rowc[j] = int(row_of(gc, mS, sS));
+                        gd[j] = u64_to_f64(g);
+                    }
+                }
+                if (h.mK != cK || sKv != cSK) {
+                    cK = h.mK;
+                    cSK = sKv;
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) ld[j] = u32_to_f64(mdiv2(y2K[j], h.mK, sKv) + 1u);
+                }
                 const double2* pr[RPT];
                 const uint32_t* pm[RPT];
-                double gd[RPT], ld[RPT], sb[RPT];
+                double sb[RPT];
                 int sj[RPT];
 #pragma unroll
                 for (int j = 0; j < RPT; ++j) {
-                    const uint32_t mt = mdiv2(y2M[j], h.mM, sMv) + 1u;
-                    const uint32_t nt = mdiv2(y2N[j], h.mN, sNv) + 1u;
-                    const uint32_t lk = mdiv2(y2K[j], h.mK, sKv) + 1u;
-                    const uint64_t g = uint64_t(mt) * nt;
-                    const uint32_t gc = g > RS ? RS : uint32_t(g);
-                    const int r = int(row_of(gc, mS, sS));
-                    pr[j] = slots + h.off + r * h.stride;
-                    pm[j] = meta + h.off / 2 + r * h.ncfg;
-                    gd[j] = u64_to_f64(g);
-                    ld[j] = u32_to_f64(lk);
+                    pr[j] = slots + h.off + rowc[j] * h.stride;
+                    pm[j] = meta + h.off / 2 + rowc[j] * h.ncfg;
                     sb[j] = kInf;
                     sj[j] = -1;
                 }

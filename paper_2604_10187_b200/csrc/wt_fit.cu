@@ -459,6 +459,52 @@ __global__ void k_samples(Rec rc, const int64_t* ordA, int64_t G, Groups gr, con
         }
 }
 
+__global__ void k_group_meta(Rec rc, const int32_t* mpos, const int64_t* ordA, int64_t G, Groups gr, int64_t* gm,
+                             int64_t* gw, int64_t* gl, int32_t* bflag, int32_t* mflag) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= G) return;
+    const int64_t r = ordA[gr.start[q]];
+    gm[q] = mpos[r];
+    gw[q] = rc.w[r];
+    gl[q] = rc.l[r];
+    int nb = 1, nm = 1;
+    if (q > 0) {
+        const int64_t r0 = ordA[gr.start[q - 1]];
+        nm = mpos[r0] != mpos[r];
+        nb = nm || rc.w[r0] != rc.w[r];
+    }
+    bflag[q] = nb;
+    mflag[q] = nm;
+}
+
+__global__ void k_bucket_meta(int64_t G, const int64_t* gm, const int64_t* gw, const int64_t* soff,
+                              const int32_t* bflag, const int32_t* bid, const int32_t* mflag, const int32_t* mid,
+                              int64_t* b_gstart, int64_t* b_w, int64_t* b_slo, int64_t* m_bstart, int64_t* m_pos) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= G) return;
+    if (bflag[q]) {
+        const int b = bid[q];
+        b_gstart[b] = q;
+        b_w[b] = gw[q];
+        b_slo[b] = soff[q];
+    }
+    if (mflag[q]) {
+        m_bstart[mid[q]] = bid[q];
+        m_pos[mid[q]] = gm[q];
+    }
+}
+
+__global__ void k_bucket_tail(int64_t NB, int64_t NM, int64_t G, int64_t S_total, const int64_t* soff,
+                              int64_t* b_gstart, int64_t* b_shi, int64_t* m_bstart) {
+    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b == 0) {
+        b_gstart[NB] = G;
+        m_bstart[NM] = NB;
+    }
+    if (b >= NB) return;
+    b_shi[b] = b + 1 < NB ? soff[b_gstart[b + 1]] : S_total;
+}
+
 struct Buckets {
     int64_t nb;
     const int64_t* slo;  // sample range per bucket
@@ -859,17 +905,35 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
         cudaFreeAsync(t, s);
     }
     (void)ns64;
-    // group metadata to host (small: one row per (macro, w, l))
-    std::vector<int64_t> h_gstart(G + 1), h_soff(G);
-    std::vector<int32_t> h_gnsamp(G), h_gmicro(G), h_gpart(G);
-    CK(cudaMemcpyAsync(h_gstart.data(), gstart, (G + 1) * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_soff.data(), soff, G * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_gnsamp.data(), gr.nsamp, G * 4, cudaMemcpyDeviceToHost, s));
-    // group keys (mpos, w, l) from the first record of each group
-    std::vector<int64_t> h_ordA(n);
-    CK(cudaMemcpyAsync(h_ordA.data(), ordA, n * 8, cudaMemcpyDeviceToHost, s));
+    // group keys and bucket / macro boundaries, all on the device
+    int64_t* gm = dalloc<int64_t>(owned, G);
+    int64_t* gw = dalloc<int64_t>(owned, G);
+    int64_t* gl = dalloc<int64_t>(owned, G);
+    int32_t* bflag = dalloc<int32_t>(owned, G);
+    int32_t* mflag = dalloc<int32_t>(owned, G);
+    int32_t* bid = dalloc<int32_t>(owned, G);
+    int32_t* mid = dalloc<int32_t>(owned, G);
+    k_group_meta<<<gblocks, 128, 0, s>>>(rc, mpos, ordA, G, gr, gm, gw, gl, bflag, mflag);
+    for (auto [in, out] : {std::pair<int32_t*, int32_t*>{bflag, bid}, std::pair<int32_t*, int32_t*>{mflag, mid}}) {
+        size_t need = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, need, in, out, G, s);
+        void* t = nullptr;
+        CK(cudaMallocAsync(&t, need, s));
+        CK(cub::DeviceScan::ExclusiveSum(t, need, in, out, G, s));
+        cudaFreeAsync(t, s);
+    }
+    int32_t tail4[4];
+    int64_t tail2[2];
+    CK(cudaMemcpyAsync(&tail4[0], bid + G - 1, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&tail4[1], bflag + G - 1, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&tail4[2], mid + G - 1, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&tail4[3], mflag + G - 1, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&tail2[0], soff + G - 1, 8, cudaMemcpyDeviceToHost, s));
+    int32_t last_ns = 0;
+    CK(cudaMemcpyAsync(&last_ns, gr.nsamp + G - 1, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    const int64_t S_total = h_soff[G - 1] + h_gnsamp[G - 1];
+    const int64_t NB = int64_t(tail4[0]) + tail4[1], NM = int64_t(tail4[2]) + tail4[3];
+    const int64_t S_total = tail2[0] + last_ns;
     double* sg = dalloc<double>(owned, S_total);
     double* sl = dalloc<double>(owned, S_total);
     double* stt = dalloc<double>(owned, S_total);
@@ -879,48 +943,15 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
         return WT_CUDA_ERROR;
     }
     k_samples<<<gblocks, 128, 0, s>>>(rc, ordA, G, gr, soff, sg, sl, stt);
-
-    // buckets (mpos, w) and macros from the group keys (host; G rows)
-    std::vector<int32_t> h_mpos_g(G), h_w_g(G);
-    std::vector<int64_t> h_l_g(G);
-    for (int64_t q = 0; q < G; ++q) {  // group keys from each group's first record
-        const int64_t r = h_ordA[h_gstart[q]];
-        h_w_g[q] = records->w[r];
-        h_l_g[q] = records->l[r];
-        auto it = std::lower_bound(hid.begin(), hid.end(), records->macro_id[r]);
-        h_mpos_g[q] = hpos[it - hid.begin()];
-    }
-    std::vector<int64_t> b_gstart, b_slo, b_shi, b_w, m_bstart;
-    std::vector<int32_t> m_pos;
-    for (int64_t q = 0; q < G; ++q) {
-        const bool newm = q == 0 || h_mpos_g[q] != h_mpos_g[q - 1];
-        const bool newb = newm || h_w_g[q] != h_w_g[q - 1];
-        if (newm) {
-            m_bstart.push_back(int64_t(b_gstart.size()));
-            m_pos.push_back(h_mpos_g[q]);
-        }
-        if (newb) {
-            b_gstart.push_back(q);
-            b_w.push_back(h_w_g[q]);
-            b_slo.push_back(h_soff[q]);
-        }
-    }
-    const int64_t NB = int64_t(b_gstart.size()), NM = int64_t(m_pos.size());
-    m_bstart.push_back(NB);
-    b_gstart.push_back(G);
-    for (int64_t k = 0; k < NB; ++k)
-        b_shi.push_back(b_gstart[k + 1] < G ? h_soff[b_gstart[k + 1]] : S_total);
-
     int64_t* d_bslo = dalloc<int64_t>(owned, NB);
     int64_t* d_bshi = dalloc<int64_t>(owned, NB);
     int64_t* d_bgs = dalloc<int64_t>(owned, NB + 1);
     int64_t* d_bw = dalloc<int64_t>(owned, NB);
     int64_t* d_mbs = dalloc<int64_t>(owned, NM + 1);
-    CK(cudaMemcpyAsync(d_bslo, b_slo.data(), NB * 8, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d_bshi, b_shi.data(), NB * 8, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d_bgs, b_gstart.data(), (NB + 1) * 8, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d_bw, b_w.data(), NB * 8, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d_mbs, m_bstart.data(), (NM + 1) * 8, cudaMemcpyHostToDevice, s));
+    int64_t* d_mpos = dalloc<int64_t>(owned, NM);
+    k_bucket_meta<<<gblocks, 128, 0, s>>>(G, gm, gw, soff, bflag, bid, mflag, mid, d_bgs, d_bw, d_bslo, d_mbs,
+                                          d_mpos);
+    k_bucket_tail<<<int((NB + 127) / 128), 128, 0, s>>>(NB, NM, G, S_total, soff, d_bgs, d_bshi, d_mbs);
     Buckets bk{NB, d_bslo, d_bshi, dalloc<double>(owned, NB * 4), dalloc<double>(owned, NB),
                dalloc<double>(owned, NB), dalloc<int32_t>(owned, NB)};
     int nsm = 148;
@@ -933,6 +964,15 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
     CK(cudaEventRecord(ev1, s));
 
     // 7. results to host and CSR assembly (registry order = mpos order)
+    std::vector<int64_t> b_gstart(NB + 1), b_slo(NB), b_shi(NB), b_w(NB), m_bstart(NM + 1), m_pos(NM), h_l_g(G);
+    std::vector<int32_t> h_gmicro(G), h_gpart(G);
+    CK(cudaMemcpyAsync(b_gstart.data(), d_bgs, (NB + 1) * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(b_slo.data(), d_bslo, NB * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(b_shi.data(), d_bshi, NB * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(b_w.data(), d_bw, NB * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(m_bstart.data(), d_mbs, (NM + 1) * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(m_pos.data(), d_mpos, NM * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_l_g.data(), gl, G * 8, cudaMemcpyDeviceToHost, s));
     std::vector<double> h_coeff(NB * 4), h_r2(NB), h_mape(NB), h_theta(NM * 4);
     std::vector<int32_t> h_degen(NB), h_mflags(NM), h_next(NM), h_em(G);
     std::vector<int64_t> h_el(G);

@@ -229,7 +229,11 @@ wt_status build_image(const wt_tables_desc& T, const wt_registry_desc& reg, cons
         im.seg_tiles.clear();
         im.seg_magic.clear();
         im.seg_pos.clear();
-        for (const auto& key : first) {
+        // classes in (t_m, t_n, t_k) order: consecutive segments share t_m / t_n,
+        // so the kernels recompute the per-shape G (and its wave row) only when
+        // the tile footprint changes
+        (void)first;
+        for (const auto& [key, unused] : cls) {
             const auto& v = cls[key];
             for (size_t s = 0; s < v.size(); s += kSegCfg) {
                 const int32_t n = int32_t(std::min<size_t>(kSegCfg, v.size() - s));
