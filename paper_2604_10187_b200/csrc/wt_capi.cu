@@ -580,7 +580,9 @@ wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_
     if (chunk <= 0) chunk = int64_t(1) << 22;
     chunk = std::min(chunk, n);
     DeviceGuard guard(e->device);
-    constexpr int kSlots = 2;
+    // 4 slots: the H2D copy of chunk k+1..k+3 never waits behind the D2H of
+    // chunk k on the same stream, so both copy engines stay busy
+    constexpr int kSlots = 4;
     cudaStream_t st[kSlots] = {};
     void* buf[kSlots] = {};
     const size_t per = size_t(chunk) * (3 * 4 + 4 + 4 + 8);

@@ -11,7 +11,13 @@ from paper_2604_10187_b200 import capi, synthetic as S  # noqa: E402
 
 mode = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1_000_000
-if mode == "sweep3":
+if mode == "fit":
+    cfg = S.config_space(True)
+    rec = S.synthetic_records(cfg, micros_per_macro=1)
+    for _ in range(2):
+        r = capi.fit_build(rec, cfg["id"], 40, 10)
+    print("fit device ms", r["device_ms"])
+elif mode == "sweep3":
     cfg = S.config_space(True)
     eng = capi.Engine(S.synthetic_tables(cfg), S.registry_arrays(cfg), n_sm=148)
     p3 = S.unique_pairs(S.LLAMA3_70B, S.QWEN2_72B)
