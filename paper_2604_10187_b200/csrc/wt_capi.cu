@@ -526,10 +526,15 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
     DeviceGuard guard(e->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     void* scratch = nullptr;
-    cudaError_t ce = cudaMallocFromPoolAsync(&scratch, size_t(n + 2) * sizeof(int64_t), lib_pool(e->device), s);
+    // [count | idx (n) | M (n) | N (n) | K (n)] -- the off-grid compaction list
+    const size_t bytes = size_t(n + 2) * sizeof(int64_t) + 3 * size_t(n + 4) * sizeof(int32_t);
+    cudaError_t ce = cudaMallocFromPoolAsync(&scratch, bytes, lib_pool(e->device), s);
     if (ce != cudaSuccess) return cuda_err(ce, "wt_gather_batch: scratch");
     int64_t* count = static_cast<int64_t*>(scratch);
     int64_t* idx = count + 2;
+    int32_t* offM = reinterpret_cast<int32_t*>(idx + n);
+    int32_t* offN = offM + (n + 4);
+    int32_t* offK = offN + (n + 4);
     cudaMemsetAsync(count, 0, sizeof(int64_t), s);
     GatherArgs a{};
     a.pair_keys = g->dkeys;
@@ -548,6 +553,9 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
     a.out = to_out(out);
     a.off_count = count;
     a.off_idx = idx;
+    a.off_M = offM;
+    a.off_N = offN;
+    a.off_K = offK;
     const int grid = int(std::min<int64_t>((n + kGatherThreads - 1) / kGatherThreads,
                                            int64_t(sm_count(e->device)) * 8));
     ce = launch_gather(e->dev, a, grid, s);
@@ -563,6 +571,12 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
         ea.chunk = e->eval_chunk;
         ea.out = to_out(out);
         if (g->topk == 0) ea.out.topk = 0;
+        if (ea.out.topk == 0) {  // list kernel reads the compacted dims contiguously
+            ea.M = offM;
+            ea.N = offN;
+            ea.K = offK;
+            ea.inputs_compact = 1;
+        }
         ce = ea.out.topk > 0 ? launch_eval(e->dev, ea, e->eval_grid, s) : launch_eval2(e->dev, ea, e->eval_grid2, s);
         g_launches++;
     }

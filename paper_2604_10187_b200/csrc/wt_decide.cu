@@ -430,31 +430,42 @@ __device__ __forceinline__ int config_of(const DevImage& im, int32_t macro) {
 // entries -- no block-wide barrier and no per-warp atomic on a hot address.
 constexpr int kWarpBuf = 64;
 
-__device__ __forceinline__ void wbuf_push(bool off, int64_t q, int64_t* slice, int& wcnt, const GatherArgs& a,
-                                          int lane) {
-    const unsigned mask = __ballot_sync(0xffffffffu, off);
-    if (off) slice[wcnt + __popc(mask & ((1u << lane) - 1u))] = q;
-    wcnt += __popc(mask);
-    if (wcnt > 32) {
-        __syncwarp();
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(reinterpret_cast<unsigned long long*>(a.off_count), (unsigned long long)wcnt);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        for (int i = lane; i < wcnt; i += 32) a.off_idx[base + i] = slice[i];
-        __syncwarp();
-        wcnt = 0;
-    }
-}
+struct WarpBuf {  // one warp's pending off-grid queries (index + dims)
+    int64_t q[kWarpBuf];
+    int32_t m[kWarpBuf], n[kWarpBuf], k[kWarpBuf];
+};
 
-__device__ __forceinline__ void wbuf_flush(int64_t* slice, int& wcnt, const GatherArgs& a, int lane) {
-    if (wcnt == 0) return;
+__device__ __forceinline__ void wbuf_drain(WarpBuf& b, int& wcnt, const GatherArgs& a, int lane) {
     __syncwarp();
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(reinterpret_cast<unsigned long long*>(a.off_count), (unsigned long long)wcnt);
     base = __shfl_sync(0xffffffffu, base, 0);
-    for (int i = lane; i < wcnt; i += 32) a.off_idx[base + i] = slice[i];
+    for (int i = lane; i < wcnt; i += 32) {
+        a.off_idx[base + i] = b.q[i];
+        a.off_M[base + i] = b.m[i];
+        a.off_N[base + i] = b.n[i];
+        a.off_K[base + i] = b.k[i];
+    }
     __syncwarp();
     wcnt = 0;
+}
+
+__device__ __forceinline__ void wbuf_push(bool off, int64_t q, int32_t M, int32_t N, int32_t K, WarpBuf& b,
+                                          int& wcnt, const GatherArgs& a, int lane) {
+    const unsigned mask = __ballot_sync(0xffffffffu, off);
+    if (off) {
+        const int at = wcnt + __popc(mask & ((1u << lane) - 1u));
+        b.q[at] = q;
+        b.m[at] = M;
+        b.n[at] = N;
+        b.k[at] = K;
+    }
+    wcnt += __popc(mask);
+    if (wcnt > 32) wbuf_drain(b, wcnt, a, lane);
+}
+
+__device__ __forceinline__ void wbuf_flush(WarpBuf& b, int& wcnt, const GatherArgs& a, int lane) {
+    if (wcnt > 0) wbuf_drain(b, wcnt, a, lane);
 }
 
 // One query: returns true when answered from the grid (writes optional
@@ -511,7 +522,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(DevImage im, GatherAr
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
     int32_t* pid = reinterpret_cast<int32_t*>(keys + a.n_pairs);
-    __shared__ int64_t wbuf[kGatherThreads / 32][kWarpBuf];
+    __shared__ WarpBuf wbuf[kGatherThreads / 32];
     for (int i = threadIdx.x; i < a.n_pairs; i += blockDim.x) {
         keys[i] = a.pair_keys[i];
         pid[i] = a.pair_ids[i];
@@ -520,7 +531,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(DevImage im, GatherAr
     const DecOut& o = a.out;
     const bool full = o.wave || o.flags || o.comps || o.tail;
     const int lane = threadIdx.x & 31;
-    int64_t* slice = wbuf[threadIdx.x >> 5];
+    WarpBuf& slice = wbuf[threadIdx.x >> 5];
     int wcnt = 0;
     const int64_t n = a.n;
     const int64_t nv = n / V;  // full vectors
@@ -569,23 +580,27 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(DevImage im, GatherAr
             }
         }
 #pragma unroll
-        for (int j = 0; j < V; ++j) wbuf_push(live && !on[j], v * V + j, slice, wcnt, a, lane);
+        for (int j = 0; j < V; ++j) wbuf_push(live && !on[j], v * V + j, M[j], N[j], K[j], slice, wcnt, a, lane);
     }
     // scalar tail (n % V queries), handled by the first warp of block 0
     if (V > 1 && blockIdx.x == 0 && threadIdx.x < 32) {
         const int64_t q = nv * V + threadIdx.x;
         const bool live = q < n;
         bool on = false;
+        int32_t tM = 0, tN = 0, tK = 0;
         if (live) {
+            tM = a.M[q];
+            tN = a.N[q];
+            tK = a.K[q];
             int4 lo4;
-            on = gather_one(im, a, keys, pid, q, a.M[q], a.N[q], a.K[q], full, &lo4);
+            on = gather_one(im, a, keys, pid, q, tM, tN, tK, full, &lo4);
             if (on) {
                 o.macro[q] = lo4.z;
                 o.micro[q] = lo4.w;
                 o.lat[q] = __hiloint2double(lo4.y, lo4.x);
             }
         }
-        wbuf_push(live && !on, q, slice, wcnt, a, lane);
+        wbuf_push(live && !on, q, tM, tN, tK, slice, wcnt, a, lane);
     }
     wbuf_flush(slice, wcnt, a, lane);
 }

@@ -49,6 +49,7 @@ struct EvalArgs {
     int64_t n;
     const int64_t* idx;    // optional compacted query indices
     const int64_t* count;  // optional device count of idx
+    int32_t inputs_compact;  // M/N/K indexed by list slot (idx only scatters outputs)
     int32_t chunk;
     DecOut out;
 };
@@ -78,6 +79,9 @@ struct GatherArgs {
     DecOut out;
     int64_t* off_count;
     int64_t* off_idx;
+    int32_t* off_M;  // compacted copies of the off-grid queries' dims
+    int32_t* off_N;
+    int32_t* off_K;
 };
 
 struct PredictArgs {

@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_
                 const int64_t slot = tl * tile + int64_t(tid) * RPT + j;
                 uint32_t k = 0xffffffffu;
                 if (slot < n) {
-                    const int64_t qq = a.idx ? a.idx[slot] : slot;
+                    const int64_t qq = (a.idx && !a.inputs_compact) ? a.idx[slot] : slot;
                     const int32_t m = a.M[qq], nn = a.N[qq];
                     if (m >= 1 && nn >= 1) k = __float_as_uint(__fmul_rn(float(m), float(nn)));
                 }
@@ -362,7 +362,8 @@ __global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_
             q[j] = live ? (a.idx ? a.idx[slot] : slot) : -1;
             uint32_t M = 1, N = 1, K = 1, stv = 0;
             if (live) {
-                const int32_t m = a.M[q[j]], nn = a.N[q[j]], k = a.K[q[j]];
+                const int64_t src = a.inputs_compact ? slot : q[j];
+                const int32_t m = a.M[src], nn = a.N[src], k = a.K[src];
                 if (m < 1 || nn < 1 || k < 1) {
                     stv = WT_INVALID_ARGUMENT;  // kernel_map.cpp:238-239
                 } else {

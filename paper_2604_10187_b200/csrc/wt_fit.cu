@@ -323,21 +323,46 @@ struct Ranges {
     int wmin, wmax, umin, umax;
 };
 
+// Field ranges for the sort-key packing: grid-stride, warp reductions, one
+// set of atomics per warp (a per-record atomic on 8 hot words serialises).
 __global__ void k_ranges(Rec rc, const int64_t* idx, int64_t n, Ranges* out) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int64_t r = idx[i];
-    // offsets by 2^63 make signed order unsigned
-    const unsigned long long g = (unsigned long long)rc.g[r] ^ 0x8000000000000000ULL;
-    const unsigned long long l = (unsigned long long)rc.l[r] ^ 0x8000000000000000ULL;
-    atomicMin(&out->gmin, g);
-    atomicMax(&out->gmax, g);
-    atomicMin(&out->lmin, l);
-    atomicMax(&out->lmax, l);
-    atomicMin(&out->wmin, rc.w[r]);
-    atomicMax(&out->wmax, rc.w[r]);
-    atomicMin(&out->umin, rc.micro[r]);
-    atomicMax(&out->umax, rc.micro[r]);
+    unsigned long long gmin = ~0ULL, gmax = 0, lmin = ~0ULL, lmax = 0;
+    int wmin = INT_MAX, wmax = INT_MIN, umin = INT_MAX, umax = INT_MIN;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = idx[i];
+        // offset by 2^63 so signed order becomes unsigned order
+        const unsigned long long g = (unsigned long long)rc.g[r] ^ 0x8000000000000000ULL;
+        const unsigned long long l = (unsigned long long)rc.l[r] ^ 0x8000000000000000ULL;
+        gmin = min(gmin, g);
+        gmax = max(gmax, g);
+        lmin = min(lmin, l);
+        lmax = max(lmax, l);
+        wmin = min(wmin, rc.w[r]);
+        wmax = max(wmax, rc.w[r]);
+        umin = min(umin, rc.micro[r]);
+        umax = max(umax, rc.micro[r]);
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        gmin = min(gmin, __shfl_xor_sync(FULL, gmin, off));
+        gmax = max(gmax, __shfl_xor_sync(FULL, gmax, off));
+        lmin = min(lmin, __shfl_xor_sync(FULL, lmin, off));
+        lmax = max(lmax, __shfl_xor_sync(FULL, lmax, off));
+    }
+    wmin = __reduce_min_sync(FULL, wmin);
+    wmax = __reduce_max_sync(FULL, wmax);
+    umin = __reduce_min_sync(FULL, umin);
+    umax = __reduce_max_sync(FULL, umax);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&out->gmin, gmin);
+        atomicMax(&out->gmax, gmax);
+        atomicMin(&out->lmin, lmin);
+        atomicMax(&out->lmax, lmax);
+        atomicMin(&out->wmin, wmin);
+        atomicMax(&out->wmax, wmax);
+        atomicMin(&out->umin, umin);
+        atomicMax(&out->umax, umax);
+    }
 }
 
 // One key field: value - base, `bits` wide, placed at `shift`.
@@ -515,14 +540,20 @@ struct Buckets {
     int32_t* degen;
 };
 
-__global__ void k_fit(const double* sg, const double* sl, const double* st, Buckets b, double* scratch) {
+constexpr int kFitWarps = 4;     // 128-thread CTAs
+constexpr int kFitSmemRows = 32;  // buckets up to 32 samples run entirely in shared memory
+
+__global__ void __launch_bounds__(32 * kFitWarps) k_fit(const double* sg, const double* sl, const double* st,
+                                                        Buckets b, double* scratch) {
+    __shared__ double wscr[kFitWarps][18 * kFitSmemRows];
     const int lane = threadIdx.x & 31;
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
     for (int64_t q = warp; q < b.nb; q += nw) {
         const int64_t lo = b.slo[q], n = b.shi[q] - lo;
         if (n <= 0) continue;
-        FitOut o = warp_fit(sg + lo, sl + lo, st + lo, int(n), scratch + 18 * lo, lane);
+        double* scr = n <= kFitSmemRows ? wscr[threadIdx.x >> 5] : scratch + 18 * lo;
+        FitOut o = warp_fit(sg + lo, sl + lo, st + lo, int(n), scr, lane);
         if (lane == 0) {
             for (int c = 0; c < 4; ++c) b.coeff[4 * q + c] = o.c[c];
             b.r2[q] = o.r2;
@@ -834,7 +865,7 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
         return WT_RUNTIME_ERROR;
     }
     CK(cudaMemcpyAsync(dr, &init, sizeof(Ranges), cudaMemcpyHostToDevice, s));
-    k_ranges<<<int((n + 255) / 256), 256, 0, s>>>(rc, idx, n, dr);
+    k_ranges<<<int(std::min<int64_t>((n + 255) / 256, 148 * 4)), 256, 0, s>>>(rc, idx, n, dr);
     Ranges hr;
     CK(cudaMemcpyAsync(&hr, dr, sizeof(Ranges), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
