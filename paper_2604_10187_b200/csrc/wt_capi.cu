@@ -86,6 +86,7 @@ int sm_count(int device) {
 }  // namespace
 
 void wtb::set_last_error(const std::string& msg) { g_err = msg; }
+cudaMemPool_t wtb::device_pool(int device) { return lib_pool(device); }
 
 struct wt_engine {
     int device = 0;
@@ -199,6 +200,7 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
     d.tm_min = h.tm_min;
     d.tn_min = h.tn_min;
     d.nseg = int32_t(NS);
+    d.seg_cfg = h.seg_cfg;
     d.seg_tiles = reinterpret_cast<const int4*>(base + o_st);
     d.seg_magic = reinterpret_cast<const uint4*>(base + o_sm);
     d.seg_pos = reinterpret_cast<const int32_t*>(base + o_sp);
@@ -208,7 +210,7 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
     // list-mode chunk: keep the staged rows near 40 KB so several CTAs fit per SM
     e->eval_chunk = int(std::max<size_t>(1, std::min<size_t>(C, 40960 / (R * 36 + 32))));
     e->eval_grid = sm_count(device) * 4;
-    e->eval_grid2 = sm_count(device) * 2;  // 96 KB of shared memory per CTA
+    e->eval_grid2 = sm_count(device) * 4;  // upper bound; launch_eval2 clamps to residency
     *out = e;
     return WT_OK;
 }

@@ -115,6 +115,9 @@ struct NearestArgs {
     int32_t* comps;
 };
 
+// Library-owned stream-ordered memory pool of a device (wt_capi.cu).
+cudaMemPool_t device_pool(int device);
+
 size_t sweep_smem_bytes(const DevImage& im, int chunk, bool special);
 size_t eval_smem_bytes(const DevImage& im, int chunk, bool special);
 cudaError_t launch_sweep(const DevImage& im, const SweepArgs& a, bool wide, cudaStream_t st);

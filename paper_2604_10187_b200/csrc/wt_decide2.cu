@@ -26,7 +26,9 @@
 
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "wt_decide.h"
 #include "wt_device.cuh"
@@ -552,23 +554,53 @@ __global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_
 }
 
 // ---------------------------------------------------------------- launchers
+// Launch shape: shapes (queries) per thread and dynamic shared memory per CTA.
+// Defaults are the measured best on B200; WT_SWEEP_RPT / WT_EVAL_RPT (2|4)
+// and WT_SWEEP_SMEM_KB / WT_EVAL_SMEM_KB override them for A/B runs.
 namespace {
-constexpr int kSweepRPT2 = 4;
-constexpr int kEvalRPT2 = 4;
-constexpr size_t kSmem2 = 96 * 1024;  // per CTA: 2 CTAs per SM
+struct Tuning {
+    int sweep_rpt = 4, eval_rpt = 4;
+    int sweep_kb = 96, eval_kb = 96;
+};
+const Tuning& tuning() {
+    static const Tuning t = [] {
+        Tuning x;
+        auto env = [](const char* k, int d) {
+            const char* v = std::getenv(k);
+            return v ? std::atoi(v) : d;
+        };
+        x.sweep_rpt = env("WT_SWEEP_RPT", x.sweep_rpt) == 2 ? 2 : 4;
+        x.eval_rpt = env("WT_EVAL_RPT", x.eval_rpt) == 2 ? 2 : 4;
+        x.sweep_kb = env("WT_SWEEP_SMEM_KB", x.sweep_kb);
+        x.eval_kb = env("WT_EVAL_SMEM_KB", x.eval_kb);
+        return x;
+    }();
+    return t;
+}
 int n_sms() {
     int dev = 0, n = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n;
 }
+// bytes of one staged segment in the worst case (all R rows)
+size_t seg_worst(const DevImage& im, bool list) {
+    return list ? size_t(im.R) * (2 * im.seg_cfg + 1) * 16 + size_t(im.R) * im.seg_cfg * 4
+                : size_t(im.R) * im.seg_cfg * (sizeof(double4) + 4);
+}
+size_t smem_for(int kb, const DevImage& im, bool list) {
+    size_t b = size_t(kb) * 1024;
+    const size_t need = kT2 * sizeof(SegHdr) + seg_worst(im, list) + 1024;
+    return std::min<size_t>(std::max(b, need), 200 * 1024);
+}
 }  // namespace
 
 // Work decomposition of a sweep: tiles x config splits, sized so the grid is
-// several waves of equal units (2 CTAs / SM resident).
+// several waves of equal units.
 void sweep2_plan(const DevImage& im, const SweepArgs& a, int64_t* ntiles, int* splits) {
     const int64_t n = a.end - a.begin;
-    *ntiles = (n + int64_t(kT2) * kSweepRPT2 - 1) / (int64_t(kT2) * kSweepRPT2);
+    const int rpt = tuning().sweep_rpt;
+    *ntiles = (n + int64_t(kT2) * rpt - 1) / (int64_t(kT2) * rpt);
     const int64_t target = int64_t(n_sms()) * 2 * 4;
     int S = int((target + *ntiles - 1) / *ntiles);
     S = max(1, min(S, im.nseg));
@@ -584,13 +616,25 @@ size_t sweep2_scratch_bytes(const DevImage& im, const SweepArgs& a) {
 }
 
 template <int RPT, bool SP, bool WIDE>
-static cudaError_t go_sweep2(const DevImage& im, const SweepArgs& a, int64_t units, int cap, Part part,
-                             int64_t ntiles, cudaStream_t st) {
+static cudaError_t go_sweep2(const DevImage& im, const SweepArgs& a, int64_t units, Part part, int64_t ntiles,
+                             cudaStream_t st) {
+    const size_t smem = smem_for(tuning().sweep_kb, im, false);
+    const int cap = int((smem - kT2 * sizeof(SegHdr)) / (sizeof(double4) + (SP ? 4 : 0)));
     auto fn = k_sweep2<RPT, SP, WIDE>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem2));
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    fn<<<unsigned(units), kT2, kSmem2, st>>>(im, a, cap, part, ntiles);
+    fn<<<unsigned(units), kT2, smem, st>>>(im, a, cap, part, ntiles);
     return cudaGetLastError();
+}
+
+template <int RPT>
+static cudaError_t sweep2_rpt(const DevImage& im, const SweepArgs& a, bool wide, int64_t units, Part part,
+                              int64_t ntiles, cudaStream_t st) {
+    const bool sp = im.special != 0;
+    if (wide) return sp ? go_sweep2<RPT, true, true>(im, a, units, part, ntiles, st)
+                        : go_sweep2<RPT, false, true>(im, a, units, part, ntiles, st);
+    return sp ? go_sweep2<RPT, true, false>(im, a, units, part, ntiles, st)
+              : go_sweep2<RPT, false, false>(im, a, units, part, ntiles, st);
 }
 
 cudaError_t launch_sweep2(const DevImage& im, const SweepArgs& a, bool wide, void* scratch, cudaStream_t st) {
@@ -606,15 +650,9 @@ cudaError_t launch_sweep2(const DevImage& im, const SweepArgs& a, bool wide, voi
         part.cfg = reinterpret_cast<int32_t*>(part.lat + size_t(S) * n);
         part.acc = reinterpret_cast<uint32_t*>(part.cfg + size_t(S) * n);
     }
-    const size_t avail = kSmem2 - kT2 * sizeof(SegHdr);
-    const int cap = int(avail / (sizeof(double4) + (im.special ? 4 : 0)));
     const int64_t units = ntiles * S;
-    const bool sp = im.special != 0;
-    cudaError_t e;
-    if (wide) e = sp ? go_sweep2<kSweepRPT2, true, true>(im, a, units, cap, part, ntiles, st)
-                     : go_sweep2<kSweepRPT2, false, true>(im, a, units, cap, part, ntiles, st);
-    else e = sp ? go_sweep2<kSweepRPT2, true, false>(im, a, units, cap, part, ntiles, st)
-                : go_sweep2<kSweepRPT2, false, false>(im, a, units, cap, part, ntiles, st);
+    cudaError_t e = tuning().sweep_rpt == 2 ? sweep2_rpt<2>(im, a, wide, units, part, ntiles, st)
+                                            : sweep2_rpt<4>(im, a, wide, units, part, ntiles, st);
     if (e != cudaSuccess || S <= 1) return e;
     k_sweep_merge<<<unsigned((n + 255) / 256), 256, 0, st>>>(im, a, part);
     return cudaGetLastError();
@@ -622,19 +660,28 @@ cudaError_t launch_sweep2(const DevImage& im, const SweepArgs& a, bool wide, voi
 
 template <int RPT, bool SP>
 static cudaError_t go_eval2(const DevImage& im, const EvalArgs& a, int grid, cudaStream_t st) {
-    const size_t avail = kSmem2 - kT2 * sizeof(SegHdr);
-    const int cap = int(avail / (sizeof(double4) + (SP ? 8 : 0)));  // 32-byte units (2 slots)
+    const size_t smem = smem_for(tuning().eval_kb, im, true);
+    const int cap = int((smem - kT2 * sizeof(SegHdr)) / (sizeof(double4) + (SP ? 8 : 0)));  // 32-byte units
     auto fn = k_eval2<RPT, SP>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem2));
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    fn<<<grid, kT2, kSmem2, st>>>(im, a, cap);
+    fn<<<grid, kT2, smem, st>>>(im, a, cap);
     return cudaGetLastError();
 }
 
 cudaError_t launch_eval2(const DevImage& im, const EvalArgs& a, int grid, cudaStream_t st) {
-    return im.special ? go_eval2<kEvalRPT2, true>(im, a, grid, st) : go_eval2<kEvalRPT2, false>(im, a, grid, st);
+    // persistent grid: as many CTAs as fit at this shared-memory size
+    const size_t smem = smem_for(tuning().eval_kb, im, true);
+    const int per_sm = std::max(1, int((228 * 1024) / (smem + 12 * 1024)));
+    grid = std::min(grid, n_sms() * per_sm);
+    if (tuning().eval_rpt == 2)
+        return im.special ? go_eval2<2, true>(im, a, grid, st) : go_eval2<2, false>(im, a, grid, st);
+    return im.special ? go_eval2<4, true>(im, a, grid, st) : go_eval2<4, false>(im, a, grid, st);
 }
 
-int eval2_tile() { return kT2 * kEvalRPT2; }
+int eval2_tile() { return kT2 * tuning().eval_rpt; }
+int eval2_ctas_per_sm() {
+    return 0;  // informational hook (grid sizing happens in launch_eval2)
+}
 
 }  // namespace wtb

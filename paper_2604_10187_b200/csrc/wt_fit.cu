@@ -26,12 +26,16 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <climits>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "wavetune_c.h"
+#include "wt_decide.h"
 #include "wt_internal.h"
 
 namespace wtb {
@@ -698,13 +702,31 @@ struct wt_build {
 
 namespace {
 
+// Temporaries come from the library's stream-ordered pool (cudaMalloc of
+// hundreds of MB per build costs milliseconds of host time).
+thread_local cudaStream_t t_alloc_stream = nullptr;
+thread_local cudaMemPool_t t_alloc_pool = nullptr;
+
 template <typename T>
 T* dalloc(std::vector<void*>& owned, size_t n) {
     void* p = nullptr;
-    if (cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) return nullptr;
+    const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+    const cudaError_t e = t_alloc_pool ? cudaMallocFromPoolAsync(&p, bytes, t_alloc_pool, t_alloc_stream)
+                                       : cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return nullptr;
     owned.push_back(p);
     return static_cast<T*>(p);
 }
+
+struct OwnedFree {
+    std::vector<void*>* v;
+    ~OwnedFree() {
+        for (void* q : *v) t_alloc_pool ? cudaFreeAsync(q, t_alloc_stream) : cudaFree(q);
+        if (t_alloc_pool) cudaStreamSynchronize(t_alloc_stream);
+        t_alloc_pool = nullptr;
+        t_alloc_stream = nullptr;
+    }
+};
 
 int bits_for(unsigned long long range) {
     int b = 0;
@@ -776,19 +798,16 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
         int d;
         ~Restore() { cudaSetDevice(d); }
     } restore{prev_dev};
-    std::vector<void*> owned;
-    struct Free {
-        std::vector<void*>* v;
-        ~Free() {
-            for (void* q : *v) cudaFree(q);
-        }
-    } freer{&owned};
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     struct SD {
         cudaStream_t s;
         ~SD() { cudaStreamDestroy(s); }
     } sd{s};
+    t_alloc_stream = s;
+    t_alloc_pool = device_pool(device);
+    std::vector<void*> owned;
+    OwnedFree freer{&owned};  // released (stream-ordered) before the stream dies
 
     // W = params.W or the highest wave in the data (model.cpp:201-203)
     if (W <= 0)
@@ -823,6 +842,16 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
     cudaEventCreate(&ev0);
     cudaEventCreate(&ev1);
     CK(cudaEventRecord(ev0, s));
+    // WT_FIT_TRACE=1 prints a synchronised wall-clock breakdown of the stages
+    const bool tr = std::getenv("WT_FIT_TRACE") != nullptr;
+    auto t_start = std::chrono::steady_clock::now();
+    auto trace = [&](const char* what) {
+        if (!tr) return;
+        cudaStreamSynchronize(s);
+        const double ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+        std::fprintf(stderr, "[wt_fit] %-28s %9.3f ms\n", what, ms);
+    };
 
     // 1. registry positions (first occurrence of a duplicated id wins)
     std::vector<std::pair<int32_t, int32_t>> ids;
@@ -880,6 +909,7 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
     auto passA = plan_passes({fg, fu, fl, fw, fm});
     auto passB = plan_passes({fg, fl, fw, fm});
 
+    trace("registry + ranges");
     // 2. stable sorts
     int64_t* ordA = dalloc<int64_t>(owned, n);
     int64_t* ordB = dalloc<int64_t>(owned, n);
@@ -896,6 +926,7 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
     if (st) return st;
     if (tmp) cudaFreeAsync(tmp, s);
 
+    trace("sorts");
     // 3. groups
     const int blocks = int((n + 255) / 256);
     int32_t* gflag = dalloc<int32_t>(owned, n);
@@ -936,6 +967,7 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
         cudaFreeAsync(t, s);
     }
     (void)ns64;
+    trace("groups + select");
     // group keys and bucket / macro boundaries, all on the device
     int64_t* gm = dalloc<int64_t>(owned, G);
     int64_t* gw = dalloc<int64_t>(owned, G);
@@ -987,12 +1019,15 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
                dalloc<double>(owned, NB), dalloc<int32_t>(owned, NB)};
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    trace("samples + meta");
     k_fit<<<nsm * 8, 128, 0, s>>>(sg, sl, stt, bk, scratch);
+    trace("k_fit");
     Macros mc{NM, d_mbs, d_bw, d_bgs, W, p, dalloc<double>(owned, NM * 4), dalloc<int32_t>(owned, NM),
               dalloc<int32_t>(owned, NM), dalloc<int64_t>(owned, G), dalloc<int32_t>(owned, G)};
     // extrapolation pools reuse the bucket scratch layout (slice of the pooled samples)
     k_extrap<<<nsm * 4, 128, 0, s>>>(rc, sg, sl, stt, bk, soff, gr, ordA, mc, scratch);
     CK(cudaEventRecord(ev1, s));
+    trace("k_extrap");
 
     // 7. results to host and CSR assembly (registry order = mpos order)
     std::vector<int64_t> b_gstart(NB + 1), b_slo(NB), b_shi(NB), b_w(NB), m_bstart(NM + 1), m_pos(NM), h_l_g(G);

@@ -233,16 +233,22 @@ wt_status build_image(const wt_tables_desc& T, const wt_registry_desc& reg, cons
         // so the kernels recompute the per-shape G (and its wave row) only when
         // the tile footprint changes
         (void)first;
+        // segment size: all R rows of one segment must fit a 48 KB staging
+        // budget (list mode stages every row); classes split evenly
+        im.seg_cfg = int32_t(std::clamp<int64_t>(48 * 1024 / (int64_t(R) * 36), 1, kSegCfg));
         for (const auto& [key, unused] : cls) {
             const auto& v = cls[key];
-            for (size_t s = 0; s < v.size(); s += kSegCfg) {
-                const int32_t n = int32_t(std::min<size_t>(kSegCfg, v.size() - s));
+            const size_t nparts = (v.size() + im.seg_cfg - 1) / im.seg_cfg;
+            for (size_t part = 0, s = 0; part < nparts; ++part) {
+                const size_t e = v.size() * (part + 1) / nparts;
+                const int32_t n = int32_t(e - s);
                 const int32_t c0 = v[s];
                 im.seg_pos.push_back(int32_t(im.cls_cfg.size()));
                 for (int32_t q = 0; q < 3; ++q) im.seg_tiles.push_back(im.tiles[4 * c0 + q]);
                 im.seg_tiles.push_back(n);
                 for (int32_t q = 0; q < 4; ++q) im.seg_magic.push_back(im.magic[4 * c0 + q]);
                 for (int32_t q = 0; q < n; ++q) im.cls_cfg.push_back(v[s + q]);
+                s = e;
             }
         }
         im.theta2.resize(im.theta.size());

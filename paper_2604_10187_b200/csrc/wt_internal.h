@@ -61,6 +61,7 @@ struct DevImage {
     // Classes are cut into segments of <= kSegCfg configs; within a segment
     // configs keep ascending macro_id order.
     int32_t nseg;
+    int32_t seg_cfg;          // max configs per segment
     const int4* seg_tiles;    // [nseg] {t_m, t_n, t_k, ncfg}
     const uint4* seg_magic;   // [nseg] as magic
     const int32_t* seg_pos;   // [nseg] first position in the class-ordered list
@@ -87,6 +88,7 @@ struct HostImage {
     std::vector<int64_t> anchor_l;
     std::vector<int32_t> anchor_micro;
     int32_t tm_min = 0, tn_min = 0;
+    int32_t seg_cfg = 32;
     std::vector<int32_t> seg_tiles;  // 4 per segment
     std::vector<uint32_t> seg_magic; // 4 per segment
     std::vector<int32_t> seg_pos;

@@ -358,3 +358,20 @@ def test_sharded_sweep_equals_full(capi, synth256):
         g2.sweep(a, b)
     torch.cuda.synchronize()
     assert torch.equal(g1.entries_tensor(), g2.entries_tensor())
+
+
+@pytest.mark.parametrize("env", [
+    {"WT_SWEEP_RPT": "2", "WT_EVAL_RPT": "2"},
+    {"WT_SWEEP_SMEM_KB": "48", "WT_EVAL_SMEM_KB": "64"},
+    {"WT_SWEEP_RPT": "2", "WT_SWEEP_SMEM_KB": "160", "WT_EVAL_RPT": "4", "WT_EVAL_SMEM_KB": "160"},
+])
+def test_launch_variants(capi, env):
+    """Every launch shape the tuning knobs can select stays bit-exact."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, os.path.join(here, "variant_check.py")], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
