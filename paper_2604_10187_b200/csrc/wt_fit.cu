@@ -805,7 +805,7 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
         ~SD() { cudaStreamDestroy(s); }
     } sd{s};
     t_alloc_stream = s;
-    t_alloc_pool = device_pool(device);
+    t_alloc_pool = wtb::device_pool(device);
     std::vector<void*> owned;
     OwnedFree freer{&owned};  // released (stream-ordered) before the stream dies
 
