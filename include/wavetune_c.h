@@ -298,6 +298,41 @@ wt_status wt_fit_bucket_batch(const double* g, const double* l, const double* t,
                               const int64_t* off, int64_t nb, double* coeffs, double* r2,
                               double* mape, int32_t* degenerate, int device);
 
+/* ---- synthetic-profile generator (wave simulator) ----- */
+
+/* simulate() (wave_sim.cpp:80-117) for n independent jobs on `slots` slots:
+ * job i dispatches g[i] blocks of duration max(eps, mean + sigma*N(0,1)),
+ * N drawn from SplitMix64(mix_seed(seed[i], block)); gap = dispatch gap.
+ * Host arrays in and out (synchronous). */
+wt_status wt_simulate_batch(const int64_t* g, const double* mean, const double* sigma, const double* eps,
+                            const double* gap, const uint64_t* seed, int64_t n, int32_t slots,
+                            double* makespan, int device);
+
+/* SimulatorBackend sweep of run_profile (profiler.cpp:192-218, 286-329):
+ * records in (point, anchor, feasible pair) order, pairs in (macro_id,
+ * micro_id) ascending order with their ground-truth entry. */
+typedef struct {
+    int64_t n_points;
+    const int64_t* point_g;
+    int64_t n_anchors;
+    const int64_t* anchor_l;
+    int64_t n_pairs;
+    const int32_t* pair_macro;
+    const int32_t* pair_micro;
+    const double* pair_base;     /* GroundEntry.base */
+    const double* pair_per_iter; /* GroundEntry.per_iter */
+    const double* pair_gap;      /* GroundEntry.dispatch_gap */
+    double sigma;
+    double floor_frac;           /* BlockLatencyModel.floor_frac (0.01) */
+    uint64_t seed;
+    int32_t warmup, measured;
+    int32_t slots;               /* n_sm * blocks_per_sm */
+} wt_sim_profile_desc;
+
+/* latency_us / status: host arrays of n_points*n_anchors*n_pairs. */
+wt_status wt_profile_sim(const wt_sim_profile_desc* desc, double* latency_us, int32_t* status, int device,
+                         double* device_ms);
+
 #ifdef __cplusplus
 }
 #endif

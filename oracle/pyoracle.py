@@ -337,3 +337,32 @@ def read_records_csv(path):
         lat = np.array([float(line.rsplit(",", 1)[1]) for line in f if line.strip()], F64)
     return dict(g=d[:, 0].astype(I64), l=d[:, 1].astype(I64), w=d[:, 2].astype(I32),
                 macro=d[:, 3].astype(I32), micro=d[:, 4].astype(I32), lat=lat)
+
+
+def _ref_extra(ref):
+    L = ref.lib
+    return L
+
+
+def ref_ground(ref, n_macros, n_micros, out):
+    if ref.lib.wtref_ground(C.c_int(n_macros), C.c_int(n_micros), out.encode()):
+        raise RuntimeError(ref.err())
+
+
+def ref_simulate(ref, n_sm, g, l, mu, sigma=0.0, seed=0):
+    out = C.c_double()
+    st = ref.lib.wtref_simulate(C.c_int(n_sm), C.c_int64(g), C.c_int64(l), C.c_double(mu), C.c_double(sigma),
+                                C.c_uint64(seed), C.byref(out))
+    if st:
+        raise RuntimeError(ref.err())
+    return out.value
+
+
+def ref_oracle_best(ref, registry_json, ground_json, n_sm, seed, M, N, K, sigma, reps):
+    ma, mi, lat = C.c_int32(), C.c_int32(), C.c_double()
+    st = ref.lib.wtref_oracle_best(registry_json.encode(), ground_json.encode(), C.c_int(n_sm), C.c_uint64(seed),
+                                   C.c_int64(M), C.c_int64(N), C.c_int64(K), C.c_double(sigma), C.c_int(reps),
+                                   C.byref(ma), C.byref(mi), C.byref(lat))
+    if st:
+        raise RuntimeError(ref.err())
+    return ma.value, mi.value, lat.value

@@ -270,3 +270,42 @@ WTREF_API int wtref_fixture(int n_sm, int n_macros, int n_micros, int W, int I, 
         return fail(e);
     }
 }
+
+// Ground truth of the reference fixture (helpers.hpp:40-56), saved as JSON.
+WTREF_API int wtref_ground(int n_macros, int n_micros, const char* out) {
+    try {
+        ConfigRegistry reg = testing::small_gemm_registry(n_macros, n_micros);
+        testing::two_regime_ground(reg).save(out);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// simulate() with a constant block model (bindings.cpp:119-128 semantics).
+WTREF_API int wtref_simulate(int n_sm, int64_t g, int64_t l, double mu, double sigma, uint64_t seed, double* out) {
+    try {
+        *out = simulate(SimMachine{HardwareSpec{n_sm, 1, ""}, seed}, g, l, BlockLatencyModel::constant(mu, sigma));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// oracle_best (wave_sim.cpp:136-161) for one dense query on the fixture ground.
+WTREF_API int wtref_oracle_best(const char* registry_json, const char* ground_json, int n_sm, uint64_t seed,
+                                int64_t M, int64_t N, int64_t K, double sigma, int reps, int32_t* macro,
+                                int32_t* micro, double* lat) {
+    try {
+        auto reg = ConfigRegistry::load(registry_json);
+        auto ground = SyntheticKernelGround::load(ground_json);
+        OracleResult r = oracle_best(SimMachine{HardwareSpec{n_sm, 1, ""}, seed}, DenseGemm{M, N, K}, reg, ground,
+                                     sigma, reps);
+        *macro = r.macro_id;
+        *micro = r.micro_id;
+        *lat = r.latency_us;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}

@@ -85,7 +85,8 @@ EXPORTS = (
     "wt_last_error wt_version wt_abi_version wt_engine_create wt_engine_destroy wt_engine_info_get "
     "wt_engine_config_index wt_tune_batch wt_tune_grouped_batch wt_predict_batch wt_explain "
     "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_destroy wt_grid_storage wt_sweep "
-    "wt_gather_batch wt_decide_host_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch").split()
+    "wt_gather_batch wt_decide_host_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
+    "wt_simulate_batch wt_profile_sim").split()
 
 _lib = None
 
@@ -354,3 +355,48 @@ def fit_bucket_batch(g, l, t, off, device: int = 0):
                                     C.c_int64(nb), vp(co.ctypes.data), vp(r2.ctypes.data), vp(mape.ctypes.data),
                                     vp(dg.ctypes.data), C.c_int(device)))
     return co.reshape(nb, 4), r2, mape, dg
+
+
+# ---------------------------------------------------------------- simulator
+class wt_sim_profile_desc(C.Structure):
+    _fields_ = [("n_points", C.c_int64), ("point_g", vp), ("n_anchors", C.c_int64), ("anchor_l", vp),
+                ("n_pairs", C.c_int64), ("pair_macro", vp), ("pair_micro", vp), ("pair_base", vp),
+                ("pair_per_iter", vp), ("pair_gap", vp), ("sigma", C.c_double), ("floor_frac", C.c_double),
+                ("seed", C.c_uint64), ("warmup", C.c_int32), ("measured", C.c_int32), ("slots", C.c_int32)]
+
+
+def simulate_batch(g, mean, sigma, eps, gap, seed, slots, device=0):
+    """Makespans of independent wave simulations (wave_sim.cpp:80-117)."""
+    g = np.ascontiguousarray(g, np.int64)
+    arrs = [np.ascontiguousarray(np.broadcast_to(x, g.shape), np.float64) for x in (mean, sigma, eps, gap)]
+    seed = np.ascontiguousarray(np.broadcast_to(seed, g.shape), np.uint64)
+    out = np.zeros(len(g), np.float64)
+    check(lib().wt_simulate_batch(vp(g.ctypes.data), *[vp(a.ctypes.data) for a in arrs], vp(seed.ctypes.data),
+                                  C.c_int64(len(g)), C.c_int32(slots), vp(out.ctypes.data), C.c_int(device)))
+    return out
+
+
+def profile_sim(point_g, anchors, pair_macro, pair_micro, base, per_iter, gap, sigma, seed, slots, warmup=3,
+                measured=5, floor_frac=0.01, device=0):
+    """SimulatorBackend sweep: latencies for (point, anchor, pair) in run_profile order."""
+    keep = []
+
+    def arr(x, dt):
+        a = np.ascontiguousarray(x, dtype=dt)
+        keep.append(a)
+        return a.ctypes.data
+
+    d = wt_sim_profile_desc()
+    d.n_points, d.point_g = len(point_g), arr(point_g, np.int64)
+    d.n_anchors, d.anchor_l = len(anchors), arr(anchors, np.int64)
+    d.n_pairs = len(pair_macro)
+    d.pair_macro, d.pair_micro = arr(pair_macro, np.int32), arr(pair_micro, np.int32)
+    d.pair_base, d.pair_per_iter, d.pair_gap = arr(base, np.float64), arr(per_iter, np.float64), arr(gap, np.float64)
+    d.sigma, d.floor_frac, d.seed = sigma, floor_frac, seed
+    d.warmup, d.measured, d.slots = warmup, measured, slots
+    total = d.n_points * d.n_anchors * d.n_pairs
+    lat = np.zeros(total, np.float64)
+    st = np.zeros(total, np.int32)
+    ms = C.c_double()
+    check(lib().wt_profile_sim(C.byref(d), vp(lat.ctypes.data), vp(st.ctypes.data), C.c_int(device), C.byref(ms)))
+    return lat, st, ms.value
