@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <optional>
 #include <set>
@@ -101,6 +102,51 @@ struct GridFactoring {
 KernelWorkload instantiate_workload(GridFactoring f, i64 l, const MacroConfig& c);
 KernelWorkload instantiate_workload_attention(i64 g, i64 l, const MacroConfig& c, i64 n_heads);
 
+// ============================================================ wave simulator
+// Synthetic ground truth + discrete-event wave simulator (reference
+// wave_sim.hpp).  The latency-model callbacks are evaluated on the host to
+// obtain (mean, gap) per (macro, micro, l); the dispatch simulation itself
+// runs on the GPU (wt_simulate_batch / wt_profile_sim).
+struct BlockLatencyModel {
+    std::function<double(int macro_id, int micro_id, i64 l)> mean_fn;
+    double sigma = 0.0;
+    double floor_frac = 0.01;
+    std::function<double(int, int)> dispatch_gap;
+    static BlockLatencyModel constant(double mu, double sigma = 0.0);
+};
+struct GroundEntry {
+    double base = 0.0;
+    double per_iter = 0.0;
+    double dispatch_gap = 0.0;
+};
+struct SyntheticKernelGround {
+    std::map<std::pair<int, int>, GroundEntry> entries;
+    const GroundEntry& at(int macro_id, int micro_id) const;
+    double mean(int macro_id, int micro_id, i64 l) const;
+    BlockLatencyModel latency_model(double sigma) const;
+    static SyntheticKernelGround load(const std::string& path);
+    void save(const std::string& path) const;
+};
+struct SimMachine {
+    HardwareSpec hw;
+    std::uint64_t seed = 0;
+};
+double simulate(const SimMachine& machine, i64 g, i64 l, const BlockLatencyModel& blm, int macro_id = 0,
+                int micro_id = 0);
+struct SweepPoint {
+    i64 g;
+    double latency_us;
+};
+std::vector<SweepPoint> sweep_profile(const SimMachine& machine, const std::vector<i64>& g_list, i64 l,
+                                      const BlockLatencyModel& blm, int macro_id = 0, int micro_id = 0);
+struct OracleResult {
+    int macro_id;
+    int micro_id;
+    double latency_us;
+};
+OracleResult oracle_best(const SimMachine& machine, const KernelWorkload& x, const ConfigRegistry& registry,
+                         const SyntheticKernelGround& ground, double sigma, int reps = 3);
+
 // ============================================================ sampling
 struct GridPoint {
     int w = 0;
@@ -147,6 +193,22 @@ public:
     virtual ~MeasurementBackend() = default;
     virtual double measure(const KernelWorkload& x, const MacroConfig& macro, const MicroConfig& micro) = 0;
     virtual bool concurrency_safe() const { return false; }
+};
+class SimulatorBackend : public MeasurementBackend {
+public:
+    SimulatorBackend(HardwareSpec hw, SyntheticKernelGround ground, double sigma, std::uint64_t seed,
+                     int warmup = 3, int measured = 5);
+    double measure(const KernelWorkload& x, const MacroConfig& macro, const MicroConfig& micro) override;
+    bool concurrency_safe() const override { return true; }
+    // the whole run_profile sweep in one device launch (used by run_profile)
+    std::vector<ProfileRecord> profile(const struct SamplingPlan& plan, const ConfigRegistry& registry) const;
+
+private:
+    HardwareSpec hw_;
+    SyntheticKernelGround ground_;
+    double sigma_;
+    std::uint64_t seed_;
+    int warmup_, measured_;
 };
 class CsvReplayBackend : public MeasurementBackend {
 public:

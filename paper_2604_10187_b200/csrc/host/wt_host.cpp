@@ -521,6 +521,8 @@ std::vector<ProfileRecord> run_profile(const SamplingPlan& plan, const ConfigReg
                                        MeasurementBackend& backend) {
     registry.validate();
     if (registry.family != plan.family) throw std::invalid_argument("registry family does not match plan family");
+    // the simulator backend runs the whole sweep in one device launch
+    if (const auto* sim = dynamic_cast<const SimulatorBackend*>(&backend)) return sim->profile(plan, registry);
     std::vector<MacroConfig> macros = registry.macros;
     std::sort(macros.begin(), macros.end(), [](const MacroConfig& a, const MacroConfig& b) { return a.id < b.id; });
     std::vector<ProfileRecord> out;
@@ -545,6 +547,227 @@ std::vector<ProfileRecord> run_profile(const SamplingPlan& plan, const ConfigReg
             }
     if (tried > 0 && failed * 10 > tried)
         throw std::runtime_error("profiling aborted: " + std::to_string(failed) + " of " + std::to_string(tried) +
+                                 " measurements failed (>10%)");
+    return out;
+}
+
+// --------------------------------------------------------------- simulator
+BlockLatencyModel BlockLatencyModel::constant(double mu, double sigma) {
+    if (mu <= 0) throw std::invalid_argument("mean block latency must be positive");
+    BlockLatencyModel b;
+    b.mean_fn = [mu](int, int, i64) { return mu; };
+    b.sigma = sigma;
+    return b;
+}
+
+const GroundEntry& SyntheticKernelGround::at(int macro_id, int micro_id) const {
+    auto it = entries.find({macro_id, micro_id});
+    if (it == entries.end())
+        throw std::out_of_range("no ground-truth entry for (" + std::to_string(macro_id) + ", " +
+                                std::to_string(micro_id) + ")");
+    return it->second;
+}
+
+double SyntheticKernelGround::mean(int macro_id, int micro_id, i64 l) const {
+    const GroundEntry& e = at(macro_id, micro_id);
+    return e.base + e.per_iter * static_cast<double>(l);
+}
+
+BlockLatencyModel SyntheticKernelGround::latency_model(double sigma) const {
+    BlockLatencyModel b;
+    b.mean_fn = [this](int a, int m, i64 l) { return mean(a, m, l); };
+    b.dispatch_gap = [this](int a, int m) { return at(a, m).dispatch_gap; };
+    b.sigma = sigma;
+    return b;
+}
+
+SyntheticKernelGround SyntheticKernelGround::load(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw std::runtime_error("cannot open ground-truth file: " + path);
+    json j;
+    in >> j;
+    SyntheticKernelGround g;
+    for (const auto& je : j.at("entries")) {
+        GroundEntry e{je.at("base").get<double>(), je.at("per_iter").get<double>(), je.value("dispatch_gap", 0.0)};
+        if (e.base <= 0 || e.per_iter < 0 || e.dispatch_gap < 0)
+            throw std::invalid_argument("ground-truth costs must be positive");
+        g.entries[{je.at("macro_id").get<int>(), je.at("micro_id").get<int>()}] = e;
+    }
+    return g;
+}
+
+void SyntheticKernelGround::save(const std::string& path) const {
+    json j;
+    j["entries"] = json::array();
+    for (const auto& [k, e] : entries)
+        j["entries"].push_back({{"macro_id", k.first}, {"micro_id", k.second}, {"base", e.base},
+                                {"per_iter", e.per_iter}, {"dispatch_gap", e.dispatch_gap}});
+    std::ofstream out(path);
+    if (!out) throw std::runtime_error("cannot write ground-truth file: " + path);
+    out << j.dump(2) << "\n";
+}
+
+namespace {
+uint64_t host_splitmix(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+uint64_t host_mix(uint64_t a, uint64_t b) { return host_splitmix(a ^ host_splitmix(b)); }
+
+std::vector<double> run_sims(const std::vector<int64_t>& g, const std::vector<double>& mean, double sigma,
+                             const std::vector<double>& eps, const std::vector<double>& gap,
+                             const std::vector<uint64_t>& seed, int slots) {
+    std::vector<double> sig(g.size(), sigma), out(g.size());
+    int dev = 0;
+    cudaGetDevice(&dev);
+    ok(wt_simulate_batch(g.data(), mean.data(), sig.data(), eps.data(), gap.data(), seed.data(), int64_t(g.size()),
+                         slots, out.data(), dev));
+    return out;
+}
+}  // namespace
+
+double simulate(const SimMachine& machine, i64 g, i64 l, const BlockLatencyModel& blm, int macro_id, int micro_id) {
+    if (g < 1 || l < 1) throw std::invalid_argument("grid size and loop count must be >= 1");
+    if (!blm.mean_fn) throw std::invalid_argument("latency model has no mean_fn");
+    const double mean = blm.mean_fn(macro_id, micro_id, l);
+    if (mean <= 0) throw std::invalid_argument("mean block duration must be positive");
+    const double gap = blm.dispatch_gap ? blm.dispatch_gap(macro_id, micro_id) : 0.0;
+    return run_sims({g}, {mean}, blm.sigma, {blm.floor_frac * mean}, {gap}, {machine.seed}, machine.hw.slots())[0];
+}
+
+std::vector<SweepPoint> sweep_profile(const SimMachine& machine, const std::vector<i64>& g_list, i64 l,
+                                      const BlockLatencyModel& blm, int macro_id, int micro_id) {
+    if (g_list.empty()) throw std::invalid_argument("g_list must be non-empty");
+    if (!std::is_sorted(g_list.begin(), g_list.end())) throw std::invalid_argument("g_list must be ascending");
+    if (!blm.mean_fn) throw std::invalid_argument("latency model has no mean_fn");
+    const double mean = blm.mean_fn(macro_id, micro_id, l);
+    if (mean <= 0) throw std::invalid_argument("mean block duration must be positive");
+    const double gap = blm.dispatch_gap ? blm.dispatch_gap(macro_id, micro_id) : 0.0;
+    const size_t n = g_list.size();
+    std::vector<uint64_t> seeds(n);
+    for (size_t i = 0; i < n; ++i) seeds[i] = host_mix(machine.seed, uint64_t(g_list[i]));
+    auto m = run_sims(std::vector<int64_t>(g_list.begin(), g_list.end()), std::vector<double>(n, mean), blm.sigma,
+                      std::vector<double>(n, blm.floor_frac * mean), std::vector<double>(n, gap), seeds,
+                      machine.hw.slots());
+    std::vector<SweepPoint> out;
+    for (size_t i = 0; i < n; ++i) out.push_back({g_list[i], m[i]});
+    return out;
+}
+
+OracleResult oracle_best(const SimMachine& machine, const KernelWorkload& x, const ConfigRegistry& registry,
+                         const SyntheticKernelGround& ground, double sigma, int reps) {
+    if (registry.feasible.empty()) throw std::invalid_argument("registry has no feasible pairs");
+    if (reps < 1) throw std::invalid_argument("reps must be >= 1");
+    std::vector<int64_t> g;
+    std::vector<double> mean, eps, gap;
+    std::vector<uint64_t> seed;
+    std::vector<std::pair<int, int>> pairs(registry.feasible.begin(), registry.feasible.end());
+    for (const auto& [ma, mi] : pairs) {
+        const auto [gg, l] = map_workload(x, registry.macro(ma));
+        const double mu = ground.mean(ma, mi, l);
+        if (mu <= 0) throw std::invalid_argument("mean block duration must be positive");
+        for (int r = 0; r < reps; ++r) {
+            g.push_back(gg);
+            mean.push_back(mu);
+            eps.push_back(0.01 * mu);
+            gap.push_back(ground.at(ma, mi).dispatch_gap);
+            seed.push_back(host_mix(host_mix(host_mix(machine.seed, uint64_t(int64_t(ma))), uint64_t(int64_t(mi))),
+                                    uint64_t(r)));
+        }
+    }
+    const auto m = run_sims(g, mean, sigma, eps, gap, seed, machine.hw.slots());
+    OracleResult best{-1, -1, std::numeric_limits<double>::infinity()};
+    for (size_t p = 0; p < pairs.size(); ++p) {
+        double total = 0.0;
+        for (int r = 0; r < reps; ++r) total += m[p * reps + r];
+        const double lat = total / reps;
+        if (lat < best.latency_us) best = {pairs[p].first, pairs[p].second, lat};
+    }
+    return best;
+}
+
+SimulatorBackend::SimulatorBackend(HardwareSpec hw, SyntheticKernelGround ground, double sigma, std::uint64_t seed,
+                                   int warmup, int measured)
+    : hw_(std::move(hw)), ground_(std::move(ground)), sigma_(sigma), seed_(seed), warmup_(warmup),
+      measured_(measured) {
+    if (measured_ < 1) throw std::invalid_argument("measured iterations must be >= 1");
+}
+
+double SimulatorBackend::measure(const KernelWorkload& x, const MacroConfig& macro, const MicroConfig& micro) {
+    const auto [g, l] = map_workload(x, macro);
+    const double mean = ground_.mean(macro.id, micro.id, l);
+    if (mean <= 0) throw std::invalid_argument("mean block duration must be positive");
+    const int iters = warmup_ + measured_;
+    const uint64_t inner = host_mix(host_mix(uint64_t(l), uint64_t(int64_t(macro.id))), uint64_t(int64_t(micro.id)));
+    const uint64_t base = host_mix(host_mix(seed_, uint64_t(g)), inner);
+    std::vector<uint64_t> seeds(iters);
+    for (int it = 0; it < iters; ++it) seeds[it] = host_mix(base, uint64_t(it));
+    const auto m = run_sims(std::vector<int64_t>(iters, g), std::vector<double>(iters, mean), sigma_,
+                            std::vector<double>(iters, 0.01 * mean),
+                            std::vector<double>(iters, ground_.at(macro.id, micro.id).dispatch_gap), seeds,
+                            hw_.slots());
+    double total = 0.0;
+    for (int it = warmup_; it < iters; ++it) total += m[it];
+    return total / measured_;
+}
+
+std::vector<ProfileRecord> SimulatorBackend::profile(const SamplingPlan& plan, const ConfigRegistry& registry) const {
+    std::vector<int64_t> pg, al(plan.loop_anchors.begin(), plan.loop_anchors.end());
+    for (const auto& p : plan.grid_points) pg.push_back(p.g);
+    std::vector<MacroConfig> macros = registry.macros;
+    std::sort(macros.begin(), macros.end(), [](const MacroConfig& a, const MacroConfig& b) { return a.id < b.id; });
+    std::vector<int32_t> pm, pu;
+    std::vector<double> base, per, gap;
+    for (const auto& mc : macros)
+        for (int mu : registry.feasible_micros(mc.id)) {
+            const GroundEntry& e = ground_.at(mc.id, mu);
+            pm.push_back(mc.id);
+            pu.push_back(mu);
+            base.push_back(e.base);
+            per.push_back(e.per_iter);
+            gap.push_back(e.dispatch_gap);
+        }
+    wt_sim_profile_desc d{};
+    d.n_points = int64_t(pg.size());
+    d.point_g = pg.data();
+    d.n_anchors = int64_t(al.size());
+    d.anchor_l = al.data();
+    d.n_pairs = int64_t(pm.size());
+    d.pair_macro = pm.data();
+    d.pair_micro = pu.data();
+    d.pair_base = base.data();
+    d.pair_per_iter = per.data();
+    d.pair_gap = gap.data();
+    d.sigma = sigma_;
+    d.floor_frac = 0.01;
+    d.seed = seed_;
+    d.warmup = warmup_;
+    d.measured = measured_;
+    d.slots = hw_.slots();
+    const size_t total = pg.size() * al.size() * pm.size();
+    std::vector<double> lat(total);
+    std::vector<int32_t> st(total);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    double ms = 0;
+    ok(wt_profile_sim(&d, lat.data(), st.data(), dev, &ms));
+    std::vector<ProfileRecord> out;
+    size_t r = 0, failed = 0;
+    for (size_t p = 0; p < pg.size(); ++p)
+        for (size_t a = 0; a < al.size(); ++a)
+            for (size_t f = 0; f < pm.size(); ++f, ++r) {
+                if (st[r]) {
+                    ++failed;
+                    std::cerr << "profile: skipped g=" << pg[p] << " l=" << al[a] << " macro=" << pm[f]
+                              << " micro=" << pu[f] << ": mean block duration must be positive\n";
+                    continue;
+                }
+                out.push_back({pg[p], al[a], wave_count(pg[p], plan.hw), pm[f], pu[f], lat[r]});
+            }
+    if (total > 0 && failed * 10 > total)
+        throw std::runtime_error("profiling aborted: " + std::to_string(failed) + " of " + std::to_string(total) +
                                  " measurements failed (>10%)");
     return out;
 }

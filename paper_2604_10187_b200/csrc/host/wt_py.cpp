@@ -115,6 +115,46 @@ PYBIND11_MODULE(_core, m) {
         },
         py::arg("hw"), py::arg("family"), py::arg("W"), py::arg("I"), py::arg("tau"), py::arg("loop_anchors"),
         py::arg("n_heads") = std::nullopt);
+    // simulator (reference bindings.cpp:104-128, 165-174)
+    py::class_<GroundEntry>(m, "GroundEntry")
+        .def(py::init([](double base, double per_iter, double gap) { return GroundEntry{base, per_iter, gap}; }),
+             py::arg("base"), py::arg("per_iter"), py::arg("dispatch_gap") = 0.0)
+        .def_readwrite("base", &GroundEntry::base)
+        .def_readwrite("per_iter", &GroundEntry::per_iter)
+        .def_readwrite("dispatch_gap", &GroundEntry::dispatch_gap);
+    py::class_<SyntheticKernelGround>(m, "SyntheticKernelGround")
+        .def(py::init<>())
+        .def("set_entry", [](SyntheticKernelGround& g, int a, int b, const GroundEntry& e) { g.entries[{a, b}] = e; })
+        .def("mean", &SyntheticKernelGround::mean)
+        .def_static("load", &SyntheticKernelGround::load)
+        .def("save", &SyntheticKernelGround::save);
+    m.def(
+        "simulate",
+        [](const HardwareSpec& hw, i64 g, i64 l, double mu, double sigma, std::uint64_t seed) {
+            return simulate(SimMachine{hw, seed}, g, l, BlockLatencyModel::constant(mu, sigma));
+        },
+        py::arg("hw"), py::arg("g"), py::arg("l"), py::arg("mu"), py::arg("sigma") = 0.0, py::arg("seed") = 0,
+        "makespan of g blocks with Normal(mu, sigma) durations (GPU wave simulator)");
+    m.def(
+        "run_profile_sim",
+        [](const SamplingPlan& plan, const ConfigRegistry& reg, const SyntheticKernelGround& ground, double sigma,
+           std::uint64_t seed) {
+            SimulatorBackend b(plan.hw, ground, sigma, seed);
+            return run_profile(plan, reg, b);
+        },
+        py::arg("plan"), py::arg("registry"), py::arg("ground"), py::arg("sigma") = 0.0, py::arg("seed") = 0);
+    py::class_<OracleResult>(m, "OracleResult")
+        .def_readonly("macro_id", &OracleResult::macro_id)
+        .def_readonly("micro_id", &OracleResult::micro_id)
+        .def_readonly("latency_us", &OracleResult::latency_us);
+    m.def(
+        "oracle_best",
+        [](const HardwareSpec& hw, std::uint64_t seed, const KernelWorkload& x, const ConfigRegistry& reg,
+           const SyntheticKernelGround& ground, double sigma, int reps) {
+            return oracle_best(SimMachine{hw, seed}, x, reg, ground, sigma, reps);
+        },
+        py::arg("hw"), py::arg("seed"), py::arg("workload"), py::arg("registry"), py::arg("ground"),
+        py::arg("sigma") = 0.0, py::arg("reps") = 3);
     m.def("write_records", &write_records);
     m.def("read_records", &read_records);
     m.def(

@@ -175,3 +175,49 @@ def test_engine_batch_host(wt, ref, tmpdir_session):
     ref.close(h)
     t = eng.tune(wt.DenseGemm(int(M[0]), int(N[0]), int(K[0])))
     assert t.macro_id == ma[0]
+
+
+def test_reference_smoke_suite_verbatim_semantics(wt, registry, tmp_path):
+    """tests/python/test_smoke.py of the reference, statement for statement,
+    against this module (simulator + profile + fit + tune all on the GPU)."""
+    import math
+
+    g = wt.SyntheticKernelGround()
+    g.set_entry(0, 0, wt.GroundEntry(20.0, 2.0))
+    g.set_entry(0, 1, wt.GroundEntry(22.0, 1.8))
+    g.set_entry(1, 0, wt.GroundEntry(70.0, 5.0))
+    g.set_entry(1, 1, wt.GroundEntry(77.0, 4.5))
+    hw = wt.HardwareSpec(132)
+    # test_mapping_and_waves
+    macro = wt.MacroConfig(0, wt.GemmTiles(128, 256, 64))
+    gg, l = wt.map_workload(wt.DenseGemm(4096, 4096, 4096), macro)
+    assert (gg, l) == (32 * 16, 64) and wt.wave_count(gg, hw) == math.ceil(512 / 132)
+    # test_simulate_step_law
+    assert wt.simulate(hw, 132, 1, 50.0) == 50.0
+    assert wt.simulate(hw, 133, 1, 50.0) == 100.0
+    noisy = wt.simulate(hw, 264, 1, 50.0, sigma=10.0, seed=3)
+    assert noisy == wt.simulate(hw, 264, 1, 50.0, sigma=10.0, seed=3)
+    # test_full_pipeline
+    plan = wt.build_plan(hw, "dense_gemm", W=4, I=4, tau=1.5, loop_anchors=[8, 16, 32])
+    assert 0 < len(plan.grid_points) <= 16
+    records = wt.run_profile_sim(plan, registry, g, sigma=0.0, seed=9)
+    assert len(records) == len(plan.grid_points) * 3 * 4
+    tables = wt.build_tables(records, registry, hw, W=4)
+    assert len(tables.tables) == 2
+    path = str(tmp_path / "tables.json")
+    wt.save_tables(tables, path)
+    loaded = wt.load_tables(path)
+    assert [t.macro_id for t in loaded.tables] == [0, 1]
+    decision = wt.tune(wt.DenseGemm(2000, 2000, 2048), loaded, registry, hw)
+    assert decision.macro_id in (0, 1) and decision.stats.model_evals == 2
+    latency, regime = wt.predict_latency(loaded.tables[0], 200, 16, hw)
+    assert latency > 0 and not regime.extrapolated
+    # test_records_csv_roundtrip
+    plan2 = wt.build_plan(hw, "dense_gemm", W=2, I=2, tau=1.5, loop_anchors=[8])
+    recs = wt.run_profile_sim(plan2, registry, g, sigma=2.0, seed=1)
+    p2 = str(tmp_path / "records.csv")
+    wt.write_records(recs, p2)
+    assert [r.latency_us for r in wt.read_records(p2)] == [r.latency_us for r in recs]
+    # exhaustive oracle on the GPU simulator
+    best = wt.oracle_best(hw, 3, wt.DenseGemm(2000, 2000, 2048), registry, g, sigma=0.0, reps=1)
+    assert (best.macro_id, best.micro_id) in {(0, 0), (0, 1), (1, 0), (1, 1)}
