@@ -605,7 +605,7 @@ wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_
     cudaError_t ce = cudaSuccess;
     for (int s = 0; s < kSlots && ce == cudaSuccess; ++s) {
         ce = cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking);
-        if (ce == cudaSuccess) ce = cudaMalloc(&buf[s], per);
+        if (ce == cudaSuccess) ce = cudaMallocFromPoolAsync(&buf[s], per, lib_pool(e->device), st[s]);
     }
     wt_status rs = WT_OK;
     for (int64_t i = 0, k = 0; ce == cudaSuccess && rs == WT_OK && i < n; i += chunk, ++k) {
@@ -635,7 +635,10 @@ wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_
             cudaError_t e2 = cudaStreamSynchronize(st[s]);
             if (ce == cudaSuccess) ce = e2;
         }
-        if (buf[s]) cudaFree(buf[s]);
+        if (buf[s]) {
+            cudaFreeAsync(buf[s], st[s]);
+            cudaStreamSynchronize(st[s]);
+        }
         if (st[s]) cudaStreamDestroy(st[s]);
     }
     if (rs != WT_OK) return rs;
