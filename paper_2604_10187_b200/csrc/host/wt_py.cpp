@@ -5,6 +5,7 @@
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
+#include "wavetune/gemm_backend.hpp"
 #include "wavetune/wavetune.hpp"
 #include "wavetune_c.h"
 
@@ -315,6 +316,21 @@ PYBIND11_MODULE(_core, m) {
                                       py::array_t<double>(lat.size(), lat.data()));
             },
             py::arg("M"), py::arg("N"), py::arg("K"));
+    // ---- B200 validation GEMM family behind MeasurementBackend (new)
+    m.def("gemm_registry", &gemm_registry);
+    py::class_<B200GemmBackend>(m, "B200GemmBackend")
+        .def(py::init<int, int, std::uint64_t>(), py::arg("warmup") = 3, py::arg("measured") = 10,
+             py::arg("seed") = 0)
+        .def("measure", &B200GemmBackend::measure, py::arg("workload"), py::arg("macro"), py::arg("micro"),
+             py::call_guard<py::gil_scoped_release>())
+        .def_static("family_config", &B200GemmBackend::family_config, py::arg("macro"), py::arg("micro"))
+        .def(
+            "profile",
+            [](B200GemmBackend& b, const SamplingPlan& plan, const ConfigRegistry& reg) {
+                py::gil_scoped_release nogil;
+                return run_profile(plan, reg, b);
+            },
+            py::arg("plan"), py::arg("registry"));
     m.def("abi_version", &wt_abi_version);
     m.def("version", []() { return std::string(wt_version()); });
 }

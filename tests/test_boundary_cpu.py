@@ -164,3 +164,29 @@ def test_records_replay_profile(core, tmp_path):
     # ... and more than 10% misses abort the run (:324-327)
     with pytest.raises(RuntimeError, match="profiling aborted"):
         wt.run_profile_replay(plan, reg, recs[: len(recs) // 2])
+
+
+def test_gemm_family_symbols_and_registry(core):
+    """lib/libwtgemm.so exports every entry point include/wavetune_gemm.h
+    declares; the family registry is valid and maps back onto instantiations."""
+    from paper_2604_10187_b200 import gemm
+
+    text = open(os.path.join(ROOT, "include", "wavetune_gemm.h")).read()
+    decl = set(re.findall(r"^\s*int\s+(wt_gemm_\w+)\(", text, re.M))
+    assert len(decl) == 6
+    lib = gemm.lib()
+    assert not [s for s in decl if not hasattr(lib, s)]
+    fam = gemm.family()
+    assert len(fam) == lib.wt_gemm_family_size() >= 10
+    assert all(bk == 64 and bm in (128, 256) for bm, bn, bk, st in fam)
+    reg = core.gemm_registry()
+    assert len(reg.feasible) == 4 * len(fam)
+    for ma, mi in reg.feasible:
+        cfg = core.B200GemmBackend.family_config(reg.macro(ma), reg.micro(mi))
+        bm, bn, bk, st = fam[cfg]
+        t = reg.macro(ma).tiles
+        assert (t.t_m, t.t_n, t.t_k, reg.micro(mi).n_stages) == (bm, bn, bk, st)
+    # argument validation happens before any device work
+    assert lib.wt_gemm_config(len(fam), None, None, None, None) == 3
+    assert lib.wt_gemm_run(0, 3, 128, 128, 64, 1, 1, 1, None) == 1
+    assert lib.wt_gemm_run(0, 1, 0, 128, 64, 1, 1, 1, None) == 1
