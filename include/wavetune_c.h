@@ -11,6 +11,7 @@
  *                         tune() takes (include/wavetune/tuner.hpp:51-52);
  *                         validated and resolved once, held on the device.
  *   wt_tune_batch      -- wavetune::tune() (tuner.hpp:51-52, tuner.cpp:159-166)
+ *   wt_tune_one        -- the same for one query at minimum latency
  *                         for n queries at once (Stage I argmin + Stage II).
  *   wt_predict_batch   -- wavetune::predict_latency() (tuner.hpp:38-40,
  *                         tuner.cpp:11-42).
@@ -160,6 +161,27 @@ typedef struct {
     int32_t* topk_macro;
     double* topk_latency;
 } wt_decisions;
+
+/* ---- one query, lowest latency ----------------------------------------- */
+
+/* tune() for a single query, synchronously (tuner.cpp:159-166 with n = 1):
+ * the query travels as kernel arguments, one warp evaluates every config,
+ * and the decision is written straight into engine-owned pinned host memory
+ * that the caller polls -- no copies and no stream synchronisation on the
+ * happy path.  Calls on one engine are serialised.  The per-query status
+ * (INVALID_ARGUMENT / RUNTIME_ERROR / UNSUPPORTED) is returned in
+ * flags >> 24 exactly as in wt_tune_batch; the return value reports only
+ * API and CUDA errors. */
+typedef struct wt_decision_one {
+    double latency_us;
+    int64_t g, l;
+    double tail_frac;
+    int32_t macro_id, micro_id, wave;
+    uint32_t flags;
+    int32_t comparisons;
+} wt_decision_one;
+
+wt_status wt_tune_one(const wt_engine* e, int32_t M, int32_t N, int32_t K, wt_decision_one* out);
 
 /* ---- batched tune (evaluate mode: every query runs full Stage I) -------- */
 

@@ -60,6 +60,12 @@ class wt_decisions(C.Structure):
                 ("topk_macro", vp), ("topk_latency", vp)]
 
 
+class wt_decision_one(C.Structure):
+    _fields_ = [("latency_us", C.c_double), ("g", C.c_int64), ("l", C.c_int64), ("tail_frac", C.c_double),
+                ("macro_id", C.c_int32), ("micro_id", C.c_int32), ("wave", C.c_int32), ("flags", C.c_uint32),
+                ("comparisons", C.c_int32)]
+
+
 class wt_grid_desc(C.Structure):
     _fields_ = [("n_pairs", C.c_int32), ("N", vp), ("K", vp), ("m_lo", C.c_int32), ("m_hi", C.c_int32),
                 ("topk", C.c_int32)]
@@ -86,7 +92,7 @@ EXPORTS = (
     "wt_engine_config_index wt_tune_batch wt_tune_grouped_batch wt_predict_batch wt_explain "
     "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_destroy wt_grid_storage wt_sweep "
     "wt_gather_batch wt_decide_host_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
-    "wt_simulate_batch wt_profile_sim").split()
+    "wt_simulate_batch wt_profile_sim wt_tune_one").split()
 
 _lib = None
 
@@ -212,6 +218,12 @@ class Engine:
     def tune_batch(self, M, N, K, out: wt_decisions, stream=None):
         check(lib().wt_tune_batch(self.handle, vp(_ptr(M)), vp(_ptr(N)), vp(_ptr(K)), C.c_int64(M.numel()),
                                   C.byref(out), vp(_stream_ptr(stream))))
+
+    def tune_one(self, M, N, K) -> wt_decision_one:
+        """One query, synchronously, at minimum latency (wt_tune_one)."""
+        o = wt_decision_one()
+        check(lib().wt_tune_one(self.handle, C.c_int32(M), C.c_int32(N), C.c_int32(K), C.byref(o)))
+        return o
 
     def tune_grouped_batch(self, row_off, rows, N, K, out, stream=None):
         check(lib().wt_tune_grouped_batch(self.handle, vp(_ptr(row_off)), vp(_ptr(rows)), vp(_ptr(N)),

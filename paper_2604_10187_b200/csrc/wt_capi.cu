@@ -97,6 +97,12 @@ struct wt_engine {
     int eval_chunk = 0;
     int eval_grid = 0;
     int eval_grid2 = 0;
+    // wt_tune_one: private stream + pinned, device-mapped mailbox
+    mutable std::mutex one_mu;
+    mutable cudaStream_t one_st = nullptr;
+    mutable OneOut* one_h = nullptr;
+    mutable OneOut* one_d = nullptr;
+    mutable uint32_t one_seq = 0;
 };
 
 struct wt_grid {
@@ -218,6 +224,8 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
 wt_status wt_engine_destroy(wt_engine* e) {
     if (!e) return WT_OK;
     DeviceGuard guard(e->device);
+    if (e->one_st) cudaStreamDestroy(e->one_st);
+    if (e->one_h) cudaFreeHost(e->one_h);
     cudaFree(e->mem);
     delete e;
     return WT_OK;
@@ -314,6 +322,51 @@ wt_status wt_tune_batch(const wt_engine* e, const int32_t* M, const int32_t* N, 
     }
     g_launches++;
     if (ce != cudaSuccess) return cuda_err(ce, "wt_tune_batch");
+    return WT_OK;
+}
+
+wt_status wt_tune_one(const wt_engine* e, int32_t M, int32_t N, int32_t K, wt_decision_one* out) {
+    if (!e || !out) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    if (e->host.family == WT_FAMILY_GROUPED_GEMM)
+        return set_err(WT_INVALID_ARGUMENT, "dense_gemm workload needs gemm tiles");
+    std::lock_guard<std::mutex> lk(e->one_mu);
+    DeviceGuard guard(e->device);
+    if (!e->one_h) {
+        cudaError_t ce = cudaStreamCreateWithFlags(&e->one_st, cudaStreamNonBlocking);
+        if (ce == cudaSuccess)
+            ce = cudaHostAlloc(reinterpret_cast<void**>(&e->one_h), sizeof(OneOut), cudaHostAllocMapped);
+        if (ce == cudaSuccess) ce = cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->one_d), e->one_h, 0);
+        if (ce != cudaSuccess) {
+            if (e->one_h) cudaFreeHost(e->one_h);
+            e->one_h = nullptr;
+            return cuda_err(ce, "wt_tune_one setup");
+        }
+        e->one_h->seq = 0;
+    }
+    const uint32_t seq = ++e->one_seq == 0 ? ++e->one_seq : e->one_seq;
+    cudaError_t ce = launch_one(e->dev, M, N, K, e->one_d, seq, e->one_st);
+    g_launches++;
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_tune_one");
+    // poll the mailbox; every 4096 spins ask the stream whether the kernel
+    // ended without writing (a fault), so a broken launch cannot hang here
+    for (uint32_t spin = 1; e->one_h->seq != seq; ++spin) {
+        if ((spin & 4095u) == 0) {
+            ce = cudaStreamQuery(e->one_st);
+            if (ce == cudaSuccess && e->one_h->seq != seq) return set_err(WT_CUDA_ERROR, "wt_tune_one: no result");
+            if (ce != cudaSuccess && ce != cudaErrorNotReady) return cuda_err(ce, "wt_tune_one");
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    const OneOut& o = *e->one_h;
+    out->latency_us = o.lat;
+    out->g = o.g;
+    out->l = o.l;
+    out->tail_frac = o.tail;
+    out->macro_id = o.macro;
+    out->micro_id = o.micro;
+    out->wave = o.wave;
+    out->flags = o.flags;
+    out->comparisons = o.comps;
     return WT_OK;
 }
 
@@ -598,10 +651,11 @@ wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_
     DeviceGuard guard(e->device);
     // 4 slots: the H2D copy of chunk k+1..k+3 never waits behind the D2H of
     // chunk k on the same stream, so both copy engines stay busy
-    constexpr int kSlots = 4;
-    cudaStream_t st[kSlots] = {};
-    void* buf[kSlots] = {};
-    const size_t per = size_t(chunk) * (3 * 4 + 4 + 4 + 8);
+    constexpr int kMaxSlots = 4;
+    const int kSlots = int(std::min<int64_t>(kMaxSlots, (n + chunk - 1) / chunk));
+    cudaStream_t st[kMaxSlots] = {};
+    void* buf[kMaxSlots] = {};
+    const size_t per = size_t(chunk) * (8 + 3 * 4 + 4 + 4);
     cudaError_t ce = cudaSuccess;
     for (int s = 0; s < kSlots && ce == cudaSuccess; ++s) {
         ce = cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking);
@@ -611,13 +665,13 @@ wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_
     for (int64_t i = 0, k = 0; ce == cudaSuccess && rs == WT_OK && i < n; i += chunk, ++k) {
         const int s = int(k % kSlots);
         const int64_t m = std::min(chunk, n - i);
-        char* b = static_cast<char*>(buf[s]);
-        int32_t* dM = reinterpret_cast<int32_t*>(b);
+        // doubles first: every sub-array stays naturally aligned for any chunk
+        double* dlat = static_cast<double*>(buf[s]);
+        int32_t* dM = reinterpret_cast<int32_t*>(dlat + chunk);
         int32_t* dN = dM + chunk;
         int32_t* dK = dN + chunk;
         int32_t* dmac = dK + chunk;
         int32_t* dmic = dmac + chunk;
-        double* dlat = reinterpret_cast<double*>(dmic + chunk);
         cudaMemcpyAsync(dM, M + i, size_t(m) * 4, cudaMemcpyHostToDevice, st[s]);
         cudaMemcpyAsync(dN, N + i, size_t(m) * 4, cudaMemcpyHostToDevice, st[s]);
         cudaMemcpyAsync(dK, K + i, size_t(m) * 4, cudaMemcpyHostToDevice, st[s]);

@@ -699,6 +699,99 @@ static cudaError_t launch_sweep_t(const DevImage& im, const SweepArgs& a, int gr
     return cudaGetLastError();
 }
 
+// ------------------------------------------ one query, one warp (latency)
+// tune() for a single query: the lanes stride the configs (ascending index),
+// each keeping its own strict-< winner; a shuffle reduction on (latency,
+// index) then picks the smallest latency with the smallest index among ties
+// -- the reference's ascending strict-< scan (tuner.cpp:114-124).  The
+// result goes straight to pinned host memory, then the sequence number the
+// host polls.
+__global__ void __launch_bounds__(32) k_one(DevImage im, int32_t m, int32_t nn, int32_t k, OneOut* out,
+                                            uint32_t seq) {
+    const int lane = threadIdx.x;
+    uint32_t status = 0;
+    uint32_t M = 1, N = 1, K = 1;
+    if (m < 1 || nn < 1 || k < 1) status = WT_INVALID_ARGUMENT;  // kernel_map.cpp:238-239
+    else {
+        M = uint32_t(m);
+        N = uint32_t(nn);
+        K = uint32_t(k);
+        const uint64_t gmax = uint64_t((M + uint32_t(im.tm_min) - 1) / uint32_t(im.tm_min)) *
+                              uint64_t((N + uint32_t(im.tn_min) - 1) / uint32_t(im.tn_min));
+        if ((gmax + uint64_t(im.S) - 1) / uint64_t(im.S) >= (uint64_t(1) << 31)) status = WT_UNSUPPORTED;
+    }
+    const uint32_t y2M = 2u * (M - 1u), y2N = 2u * (N - 1u), y2K = 2u * (K - 1u);
+    double best = __longlong_as_double(0x7ff0000000000000LL);
+    int bc = -1;
+    uint32_t acc = 0;
+    if (!status) {
+#pragma unroll 4
+        for (int c = lane; c < im.C; c += 32) {
+            const uint4 mg = __ldg(im.magic + c);
+            const uint32_t mt = mdiv2(y2M, mg.x, mg.w & 0xffu) + 1u;
+            const uint32_t nt = mdiv2(y2N, mg.y, (mg.w >> 8) & 0xffu) + 1u;
+            const uint32_t lk = mdiv2(y2K, mg.z, (mg.w >> 16) & 0xffu) + 1u;
+            const uint64_t g = uint64_t(mt) * nt;
+            const uint32_t gc = g > im.RS ? im.RS : uint32_t(g);
+            const uint32_t row = row_of(gc, im.mS, im.sS);
+            const size_t rr = size_t(c) * im.R + row;
+            const double4 th = ldg_row(im.theta + rr);
+            const double gd = u64_to_f64(g), ld = u32_to_f64(lk);
+            const double t = bilinear(th.x, th.y, __dmul_rn(th.z, ld), th.w, gd, ld);
+            if (t < best) {
+                best = t;
+                bc = c;
+            }
+            if (im.special) acc |= __ldg(im.rowmeta + rr);
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+        const int oc = __shfl_xor_sync(0xffffffffu, bc, off);
+        acc |= __shfl_xor_sync(0xffffffffu, acc, off);
+        if (oc >= 0 && (bc < 0 || ob < best || (ob == best && oc < bc))) {
+            best = ob;
+            bc = oc;
+        }
+    }
+    if (lane != 0) return;
+    Final f;
+    uint64_t g = 0;
+    int64_t l = 0;
+    if (status) {
+        f.flags = status << 24;
+        f.macro = f.micro = f.wave = -1;
+        f.comps = 0;
+        f.tail = 0.f;
+    } else {
+        if (bc >= 0) {
+            const int4 tl = __ldg(im.tiles + bc);
+            g = uint64_t((M + uint32_t(tl.x) - 1) / uint32_t(tl.x)) * uint64_t((N + uint32_t(tl.y) - 1) / uint32_t(tl.y));
+            l = int64_t((K + uint32_t(tl.z) - 1) / uint32_t(tl.z));
+        }
+        f = finish(im, bc, best, g, l, acc);
+    }
+    const bool ok = (f.flags >> 24) == 0;
+    out->lat = ok ? best : __longlong_as_double(0x7ff8000000000000LL);
+    out->g = ok ? int64_t(g) : 0;
+    out->l = ok ? l : 0;
+    out->tail = ok ? double(f.tail) : 0.0;
+    out->macro = ok ? f.macro : -1;
+    out->micro = ok ? f.micro : -1;
+    out->wave = ok ? f.wave : 0;
+    out->flags = f.flags;
+    out->comps = ok ? f.comps : 0;
+    __threadfence_system();
+    out->seq = seq;
+}
+
+cudaError_t launch_one(const DevImage& im, int32_t M, int32_t N, int32_t K, OneOut* out, uint32_t seq,
+                       cudaStream_t st) {
+    k_one<<<1, 32, 0, st>>>(im, M, N, K, out, seq);
+    return cudaGetLastError();
+}
+
 size_t sweep_smem_bytes(const DevImage& im, int chunk, bool special) {
     size_t b = size_t(chunk) * (sizeof(SweepCfg) + sizeof(double)) + size_t(chunk) * im.R * sizeof(double4);
     if (special) b += size_t(chunk) * im.R * sizeof(uint32_t);

@@ -125,6 +125,18 @@ cudaError_t launch_eval(const DevImage& im, const EvalArgs& a, int grid, cudaStr
 cudaError_t launch_grouped(const DevImage& im, const GroupedArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_gather(const DevImage& im, const GatherArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_predict(const DevImage& im, const PredictArgs& a, cudaStream_t st);
+// one query, one warp; result + sequence number written to (pinned) `out`
+struct OneOut {
+    double lat;
+    int64_t g, l;
+    double tail;
+    int32_t macro, micro, wave;
+    uint32_t flags;
+    int32_t comps;
+    volatile uint32_t seq;
+};
+cudaError_t launch_one(const DevImage& im, int32_t M, int32_t N, int32_t K, OneOut* out, uint32_t seq,
+                       cudaStream_t st);
 size_t sweep2_scratch_bytes(const DevImage& im, const SweepArgs& a);
 cudaError_t launch_sweep2(const DevImage& im, const SweepArgs& a, bool wide, void* scratch, cudaStream_t st);
 cudaError_t launch_eval2(const DevImage& im, const EvalArgs& a, int grid, cudaStream_t st);

@@ -375,3 +375,27 @@ def test_launch_variants(capi, env):
     r = subprocess.run([sys.executable, os.path.join(here, "variant_check.py")], env={**os.environ, **env},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_tune_one_matches_batch(capi, landscape, synth256):
+    """wt_tune_one (one warp, pinned mailbox) returns exactly the batch
+    kernel's answer, field for field, including per-query error statuses and
+    the reference landscape's fallback rows."""
+    from paper_2604_10187_b200 import synthetic as S
+
+    cfg, t, reg = synth256
+    engines = [capi.Engine(t, reg, n_sm=148), capi.Engine(landscape["arrays"], landscape["registry"], n_sm=132)]
+    rng = np.random.default_rng(11)
+    M = np.concatenate([rng.integers(1, 70000, 400), [0, -3, 1, 2**31 - 1, 5]]).astype(np.int32)
+    N = np.concatenate([rng.integers(1, 70000, 400), [5, 5, 0, 2**31 - 1, 2**31 - 1]]).astype(np.int32)
+    K = np.concatenate([rng.integers(1, 70000, 400), [5, 5, 5, 7, 2**31 - 1]]).astype(np.int32)
+    for eng in engines:
+        want = tune_gpu(capi, eng, M, N, K)
+        for i in range(len(M)):
+            o = eng.tune_one(int(M[i]), int(N[i]), int(K[i]))
+            assert o.flags == np.uint32(want["flags"][i]), i
+            got = (o.macro_id, o.micro_id, o.wave, o.comparisons, o.g, o.l)
+            exp = tuple(int(want[k][i]) for k in ("macro", "micro", "wave", "comps", "g", "l"))
+            assert got == exp, (i, got, exp)
+            assert U.bits(np.array([o.latency_us]))[0] == U.bits(want["lat"][i:i + 1])[0]
+    assert engines[0].tune_one(4096, 4096, 4096).macro_id >= 0
