@@ -349,6 +349,9 @@ public:
     int n_configs() const { return n_configs_; }
     // One full tune() with flags (single query).
     Tuned tune_one(const KernelWorkload& x) const;
+    // idle_us > 0: single queries are answered by a resident polling CTA
+    // (no launch per query) that leaves after idle_us without queries.
+    void set_resident(int idle_us);
     // Batched dense/attention decisions on host vectors (copies inside).
     void tune_host(const std::vector<int32_t>& M, const std::vector<int32_t>& N, const std::vector<int32_t>& K,
                    std::vector<int32_t>& macro, std::vector<int32_t>& micro, std::vector<double>& latency) const;

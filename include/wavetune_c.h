@@ -183,6 +183,14 @@ typedef struct wt_decision_one {
 
 wt_status wt_tune_one(const wt_engine* e, int32_t M, int32_t N, int32_t K, wt_decision_one* out);
 
+/* Resident mode for wt_tune_one.  idle_us > 0: the first call starts one
+ * resident CTA that polls the engine's pinned mailbox and answers each query
+ * without a kernel launch; it leaves by itself after idle_us microseconds
+ * without a query and the next call restarts it.  While it is resident a
+ * device-wide synchronisation waits for it to leave (at most idle_us).
+ * idle_us = 0 stops it and returns to one launch per query (the default). */
+wt_status wt_engine_set_resident(wt_engine* e, int32_t idle_us);
+
 /* ---- batched tune (evaluate mode: every query runs full Stage I) -------- */
 
 /* Dense GEMM (M,N,K) / FlashAttention (s_q,n_heads,s_kv) queries, int32

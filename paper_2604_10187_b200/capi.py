@@ -92,7 +92,7 @@ EXPORTS = (
     "wt_engine_config_index wt_tune_batch wt_tune_grouped_batch wt_predict_batch wt_explain "
     "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_destroy wt_grid_storage wt_sweep "
     "wt_gather_batch wt_decide_host_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
-    "wt_simulate_batch wt_profile_sim wt_tune_one").split()
+    "wt_simulate_batch wt_profile_sim wt_tune_one wt_engine_set_resident").split()
 
 _lib = None
 
@@ -224,6 +224,10 @@ class Engine:
         o = wt_decision_one()
         check(lib().wt_tune_one(self.handle, C.c_int32(M), C.c_int32(N), C.c_int32(K), C.byref(o)))
         return o
+
+    def set_resident(self, idle_us: int):
+        """idle_us > 0: answer tune_one() from a resident polling CTA."""
+        check(lib().wt_engine_set_resident(self.handle, C.c_int32(idle_us)))
 
     def tune_grouped_batch(self, row_off, rows, N, K, out, stream=None):
         check(lib().wt_tune_grouped_batch(self.handle, vp(_ptr(row_off)), vp(_ptr(rows)), vp(_ptr(N)),

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <iostream>
@@ -1276,6 +1277,8 @@ Tuned Engine::tune_one(const KernelWorkload& x) const {
     return t;
 }
 
+void Engine::set_resident(int idle_us) { ok(wt_engine_set_resident(static_cast<wt_engine*>(handle_), idle_us)); }
+
 void Engine::tune_host(const std::vector<int32_t>& M, const std::vector<int32_t>& N, const std::vector<int32_t>& K,
                        std::vector<int32_t>& macro, std::vector<int32_t>& micro, std::vector<double>& latency) const {
     const size_t n = M.size();
@@ -1358,6 +1361,8 @@ std::shared_ptr<Engine> cached_engine(const std::vector<DualTable>& tables, cons
     int dev = 0;
     cudaGetDevice(&dev);
     auto e = std::make_shared<Engine>(tables, reg, hw, dev);
+    // WT_RESIDENT_US=<idle us>: answer tune() from a resident polling CTA
+    if (const char* r = std::getenv("WT_RESIDENT_US"); r && std::atoi(r) > 0) e->set_resident(std::atoi(r));
     std::lock_guard<std::mutex> lock(mu);
     if (cache.size() > 64) cache.clear();
     cache[key] = e;

@@ -300,6 +300,7 @@ PYBIND11_MODULE(_core, m) {
         .def_property_readonly("n_configs", &Engine::n_configs)
         .def_property_readonly("handle", [](const Engine& e) { return reinterpret_cast<uintptr_t>(e.handle()); })
         .def("tune", &Engine::tune_one, py::arg("workload"))
+        .def("set_resident", &Engine::set_resident, py::arg("idle_us"))
         .def(
             "tune_batch",
             [](const Engine& e, py::array_t<int32_t> M, py::array_t<int32_t> N, py::array_t<int32_t> K) {

@@ -137,6 +137,25 @@ struct OneOut {
 };
 cudaError_t launch_one(const DevImage& im, int32_t M, int32_t N, int32_t K, OneOut* out, uint32_t seq,
                        cudaStream_t st);
+// Resident decision server (wt_serve.cu): one CTA polls a pinned mailbox.
+struct alignas(64) Mailbox {
+    // host -> device: one 16-byte record, read by the server in one load
+    // (the host stores M, N, K before req; all four share a cache line)
+    volatile int32_t M, N, K;
+    volatile uint32_t req;    // request sequence number
+    volatile uint32_t stop;   // host -> device: leave now
+    volatile uint32_t alive;  // 1 from launch until the server has left
+    uint32_t pad[10];
+    // device -> host: the decision as four 16-byte stores, each carrying the
+    // sequence number in .w, so no fence is needed before the host reads:
+    //   {lat lo, lat hi, macro, seq} {g lo, g hi, micro, seq}
+    //   {l lo, l hi, wave, seq}      {flags, comps, tail (f32 bits), seq}
+    volatile int4 resp[4];
+};
+// `last` = the last request already answered; idle_ns = leave after this
+// long without a request.  Stages the image in shared memory when it fits.
+cudaError_t launch_serve(const DevImage& im, int64_t n_anchor, Mailbox* mb, uint32_t last, int64_t idle_ns,
+                         cudaStream_t st);
 size_t sweep2_scratch_bytes(const DevImage& im, const SweepArgs& a);
 cudaError_t launch_sweep2(const DevImage& im, const SweepArgs& a, bool wide, void* scratch, cudaStream_t st);
 cudaError_t launch_eval2(const DevImage& im, const EvalArgs& a, int grid, cudaStream_t st);

@@ -104,6 +104,14 @@ __device__ __forceinline__ void topk_insert(double (&L)[KM], int (&I)[KM], doubl
     }
 }
 
+// Read-only load: the non-coherent path for global memory (G), a plain
+// generic load for images staged into shared memory (!G).
+template <bool G, class T>
+__device__ __forceinline__ T rd(const T* p) {
+    if constexpr (G) return __ldg(p);
+    else return *p;
+}
+
 // ---------------------------------------------------------------- Stage II
 struct Stage2 {
     int32_t micro;
@@ -111,9 +119,10 @@ struct Stage2 {
     uint32_t flags;  // WT_FLAG_* bits and status << 24
 };
 
+template <bool G = true>
 __device__ __forceinline__ Stage2 stage2(const DevImage& im, int c, uint32_t row, int64_t l) {
     const size_t rr = size_t(c) * im.R + row;
-    const uint32_t meta = __ldg(im.rowmeta + rr);
+    const uint32_t meta = rd<G>(im.rowmeta + rr);
     Stage2 s;
     s.flags = (meta & ROW_EXTRAP) ? WT_FLAG_EXTRAPOLATED : 0u;
     if (meta & ROW_ANCHOR_FB) s.flags |= WT_FLAG_ANCHOR_FALLBACK;
@@ -123,10 +132,10 @@ __device__ __forceinline__ Stage2 stage2(const DevImage& im, int c, uint32_t row
         s.flags |= uint32_t(WT_RUNTIME_ERROR) << 24;
         return s;
     }
-    const int2 am = __ldg(im.amap + rr);
+    const int2 am = rd<G>(im.amap + rr);
     int comps;
     int k = nearest_anchor_idx(im.anchor_l + am.x, am.y, l, &comps);
-    s.micro = __ldg(im.anchor_micro + am.x + k);
+    s.micro = rd<G>(im.anchor_micro + am.x + k);
     s.comps = comps;
     return s;
 }
@@ -139,6 +148,7 @@ struct Final {
     float tail;
 };
 
+template <bool G = true>
 __device__ __forceinline__ Final finish(const DevImage& im, int c, double best, uint64_t g,
                                         int64_t l, uint32_t acc_meta) {
     Final f;
@@ -158,8 +168,8 @@ __device__ __forceinline__ Final finish(const DevImage& im, int c, double best, 
     const uint64_t S = uint64_t(im.S);
     const uint64_t w64 = (g + S - 1) / S;
     const uint32_t row = uint32_t(w64 < uint64_t(im.R) ? w64 : uint64_t(im.R)) - 1u;
-    Stage2 s = stage2(im, c, row, l);
-    f.macro = __ldg(im.macro_id + c);
+    Stage2 s = stage2<G>(im, c, row, l);
+    f.macro = rd<G>(im.macro_id + c);
     f.micro = s.micro;
     f.wave = int32_t(uint32_t(w64));
     f.comps = s.comps;

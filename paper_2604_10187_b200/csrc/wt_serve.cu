@@ -1,0 +1,221 @@
+// wt_serve.cu -- resident single-query decision server.
+//
+// A launch costs more than the decision itself (a few us of launch latency
+// against well under a microsecond of evaluation), so latency-critical
+// callers can keep one CTA resident: it polls a mailbox in pinned host
+// memory (mapped into the device), answers each request with the same
+// arithmetic as k_one (Stage I strict-< scan, Stage II nearest anchor;
+// tuner.cpp:108-166) and leaves on its own after an idle period, so it never
+// holds the device indefinitely.  The image is staged into shared memory
+// when it fits, which turns every load of a decision into an SMEM access.
+#include <cuda_runtime.h>
+
+#include "wt_decide.h"
+#include "wt_device.cuh"
+
+namespace wtb {
+namespace {
+
+constexpr int kServeThreads = 256;
+constexpr int kServeWarps = kServeThreads / 32;
+constexpr size_t kServeSmemMax = 200 * 1024;
+
+// the whole request record in one system-scope load (one PCIe read)
+__device__ __forceinline__ int4 ld_request(const Mailbox* mb) {
+    int4 v;
+    asm volatile("ld.relaxed.sys.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(mb)
+                 : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_sys(volatile uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_sys4(volatile int4* p, int x, int y, int z, int w) {
+    asm volatile("st.relaxed.sys.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(x), "r"(y), "r"(z), "r"(w)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+size_t staged_bytes(const DevImage& im, int64_t n_anchor) {
+    const size_t C = size_t(im.C), CR = size_t(im.C) * im.R, A = size_t(n_anchor);
+    return CR * sizeof(double4) + A * sizeof(int64_t) + C * (sizeof(uint4) + sizeof(int4)) + CR * sizeof(int2) +
+           CR * sizeof(uint32_t) + A * sizeof(int32_t) + C * sizeof(int32_t) + 64;
+}
+
+template <class T>
+__device__ __forceinline__ const T* stage(unsigned char*& cur, const T* src, size_t n) {
+    T* dst = reinterpret_cast<T*>(cur);
+    for (size_t i = threadIdx.x; i < n; i += kServeThreads) dst[i] = src[i];
+    cur += (n * sizeof(T) + 15) & ~size_t(15);
+    return dst;
+}
+
+template <bool G>
+__global__ void __launch_bounds__(kServeThreads, 1) k_serve(DevImage im, int64_t n_anchor, Mailbox* mb,
+                                                            uint32_t last, int64_t idle_ns) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int32_t q[4];
+    __shared__ double wbest[kServeWarps];
+    __shared__ int32_t wbc[kServeWarps];
+    __shared__ uint32_t wacc[kServeWarps];
+    if constexpr (!G) {  // the whole image into shared memory, 16-byte arrays first
+        unsigned char* cur = smem;
+        const size_t CR = size_t(im.C) * im.R;
+        im.theta = stage(cur, im.theta, CR);
+        im.anchor_l = stage(cur, im.anchor_l, size_t(n_anchor));
+        im.magic = stage(cur, im.magic, size_t(im.C));
+        im.tiles = stage(cur, im.tiles, size_t(im.C));
+        im.amap = stage(cur, im.amap, CR);
+        im.rowmeta = stage(cur, im.rowmeta, CR);
+        im.anchor_micro = stage(cur, im.anchor_micro, size_t(n_anchor));
+        im.macro_id = stage(cur, im.macro_id, size_t(im.C));
+        __syncthreads();
+    }
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t seq = last;
+    for (;;) {
+        if (tid == 0) {
+            int cmd = 0;
+            const uint64_t t0 = global_ns();
+            for (uint32_t spin = 1;; ++spin) {
+                const int4 r = ld_request(mb);
+                if (uint32_t(r.w) != seq) {
+                    seq = uint32_t(r.w);
+                    q[0] = r.x;
+                    q[1] = r.y;
+                    q[2] = r.z;
+                    cmd = 1;
+                    break;
+                }
+                if ((spin & 63u) == 0 && (mb->stop || int64_t(global_ns() - t0) > idle_ns)) {
+                    cmd = 2;
+                    break;
+                }
+            }
+            q[3] = cmd;
+        }
+        __syncthreads();
+        if (q[3] == 2) break;
+        const int32_t m = q[0], nn = q[1], k = q[2];
+        uint32_t status = 0, M = 1, N = 1, K = 1;
+        if (m < 1 || nn < 1 || k < 1) status = WT_INVALID_ARGUMENT;  // kernel_map.cpp:238-239
+        else {
+            M = uint32_t(m);
+            N = uint32_t(nn);
+            K = uint32_t(k);
+            const uint64_t gmax = uint64_t((M + uint32_t(im.tm_min) - 1) / uint32_t(im.tm_min)) *
+                                  uint64_t((N + uint32_t(im.tn_min) - 1) / uint32_t(im.tn_min));
+            if ((gmax + uint64_t(im.S) - 1) / uint64_t(im.S) >= (uint64_t(1) << 31)) status = WT_UNSUPPORTED;
+        }
+        const uint32_t y2M = 2u * (M - 1u), y2N = 2u * (N - 1u), y2K = 2u * (K - 1u);
+        double best = __longlong_as_double(0x7ff0000000000000LL);
+        int bc = -1;
+        uint32_t acc = 0;
+        if (!status)
+            for (int c = tid; c < im.C; c += kServeThreads) {
+                const uint4 mg = rd<G>(im.magic + c);
+                const uint32_t mt = mdiv2(y2M, mg.x, mg.w & 0xffu) + 1u;
+                const uint32_t nt = mdiv2(y2N, mg.y, (mg.w >> 8) & 0xffu) + 1u;
+                const uint32_t lk = mdiv2(y2K, mg.z, (mg.w >> 16) & 0xffu) + 1u;
+                const uint64_t g = uint64_t(mt) * nt;
+                const uint32_t gc = g > im.RS ? im.RS : uint32_t(g);
+                const uint32_t row = row_of(gc, im.mS, im.sS);
+                const size_t rr = size_t(c) * im.R + row;
+                double4 th;
+                if constexpr (G) th = ldg_row(im.theta + rr);
+                else th = im.theta[rr];
+                const double gd = u64_to_f64(g), ld = u32_to_f64(lk);
+                const double t = bilinear(th.x, th.y, __dmul_rn(th.z, ld), th.w, gd, ld);
+                if (t < best) {
+                    best = t;
+                    bc = c;
+                }
+                if (im.special) acc |= rd<G>(im.rowmeta + rr);
+            }
+        // (latency, index) minimum: smallest latency, smallest index on ties
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+            const int oc = __shfl_xor_sync(0xffffffffu, bc, off);
+            acc |= __shfl_xor_sync(0xffffffffu, acc, off);
+            if (oc >= 0 && (bc < 0 || ob < best || (ob == best && oc < bc))) {
+                best = ob;
+                bc = oc;
+            }
+        }
+        if (lane == 0) {
+            wbest[warp] = best;
+            wbc[warp] = bc;
+            wacc[warp] = acc;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 0; w < kServeWarps; ++w) {
+                acc |= wacc[w];
+                const double ob = wbest[w];
+                const int oc = wbc[w];
+                if (oc >= 0 && (bc < 0 || ob < best || (ob == best && oc < bc))) {
+                    best = ob;
+                    bc = oc;
+                }
+            }
+            Final f;
+            uint64_t g = 0;
+            int64_t l = 0;
+            if (status) {
+                f.flags = status << 24;
+                f.macro = f.micro = f.wave = -1;
+                f.comps = 0;
+                f.tail = 0.f;
+            } else {
+                if (bc >= 0) {
+                    const int4 tl = rd<G>(im.tiles + bc);
+                    g = uint64_t((M + uint32_t(tl.x) - 1) / uint32_t(tl.x)) *
+                        uint64_t((N + uint32_t(tl.y) - 1) / uint32_t(tl.y));
+                    l = int64_t((K + uint32_t(tl.z) - 1) / uint32_t(tl.z));
+                }
+                f = finish<G>(im, bc, best, g, l, acc);
+            }
+            const bool ok = (f.flags >> 24) == 0;
+            const double lat = ok ? best : __longlong_as_double(0x7ff8000000000000LL);
+            const int64_t go = ok ? int64_t(g) : 0, lo = ok ? l : 0;
+            const int s32 = int(seq);
+            st_sys4(&mb->resp[0], __double2loint(lat), __double2hiint(lat), ok ? f.macro : -1, s32);
+            st_sys4(&mb->resp[1], int(uint64_t(go)), int(uint64_t(go) >> 32), ok ? f.micro : -1, s32);
+            st_sys4(&mb->resp[2], int(uint64_t(lo)), int(uint64_t(lo) >> 32), ok ? f.wave : 0, s32);
+            st_sys4(&mb->resp[3], int(f.flags), ok ? f.comps : 0, __float_as_int(ok ? f.tail : 0.f), s32);
+        }
+        // no barrier needed here: q and the warp slots are rewritten only
+        // after the next top-of-loop barrier, which thread 0 reaches last
+    }
+    if (tid == 0) {
+        __threadfence_system();
+        st_sys(&mb->alive, 0u);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_serve(const DevImage& im, int64_t n_anchor, Mailbox* mb, uint32_t last, int64_t idle_ns,
+                         cudaStream_t st) {
+    const size_t smem = staged_bytes(im, n_anchor);
+    if (smem <= kServeSmemMax) {
+        cudaError_t e = cudaFuncSetAttribute(k_serve<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        k_serve<false><<<1, kServeThreads, smem, st>>>(im, n_anchor, mb, last, idle_ns);
+    } else {
+        k_serve<true><<<1, kServeThreads, 0, st>>>(im, n_anchor, mb, last, idle_ns);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace wtb

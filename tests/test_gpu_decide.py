@@ -399,3 +399,31 @@ def test_tune_one_matches_batch(capi, landscape, synth256):
             assert got == exp, (i, got, exp)
             assert U.bits(np.array([o.latency_us]))[0] == U.bits(want["lat"][i:i + 1])[0]
     assert engines[0].tune_one(4096, 4096, 4096).macro_id >= 0
+
+
+def test_resident_server_matches_batch(capi, landscape, synth256):
+    """wt_engine_set_resident: the polling CTA answers exactly as the batch
+    kernel, restarts after its idle exit, and stops on request (so a device
+    synchronisation afterwards returns at once)."""
+    import time
+
+    cfg, t, reg = synth256
+    for eng in (capi.Engine(t, reg, n_sm=148), capi.Engine(landscape["arrays"], landscape["registry"], n_sm=132)):
+        rng = np.random.default_rng(5)
+        M = np.concatenate([rng.integers(1, 70000, 300), [0, 2**31 - 1]]).astype(np.int32)
+        N = np.concatenate([rng.integers(1, 70000, 300), [7, 2**31 - 1]]).astype(np.int32)
+        K = np.concatenate([rng.integers(1, 70000, 300), [7, 9]]).astype(np.int32)
+        want = tune_gpu(capi, eng, M, N, K)
+        eng.set_resident(2000)  # 2 ms idle exit: the sleeps below force restarts
+        for i in range(len(M)):
+            if i % 50 == 49:
+                time.sleep(0.01)
+            o = eng.tune_one(int(M[i]), int(N[i]), int(K[i]))
+            assert o.flags == np.uint32(want["flags"][i]), i
+            got = (o.macro_id, o.micro_id, o.wave, o.comparisons, o.g, o.l)
+            assert got == tuple(int(want[k][i]) for k in ("macro", "micro", "wave", "comps", "g", "l")), i
+            assert U.bits(np.array([o.latency_us]))[0] == U.bits(want["lat"][i:i + 1])[0]
+        eng.set_resident(0)
+        t0 = time.perf_counter()
+        torch.cuda.synchronize()
+        assert time.perf_counter() - t0 < 0.5

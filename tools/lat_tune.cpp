@@ -37,6 +37,10 @@ int main(int argc, char** argv) {
     report("C-ABI wt_tune_one", [&] { wt_tune_one(e, int32_t(x.m), int32_t(x.n), int32_t(x.k), &one); });
     report("C++ Engine::tune_one", [&] { (void)eng.tune_one(x); });
     report("C++ tune() (cached engine)", [&] { (void)tune(x, art.tables, reg, hw); });
+    eng.set_resident(20000);
+    report("C-ABI wt_tune_one, resident", [&] { wt_tune_one(e, int32_t(x.m), int32_t(x.n), int32_t(x.k), &one); });
+    report("C++ Engine::tune_one, resident", [&] { (void)eng.tune_one(x); });
+    eng.set_resident(0);
     const Tuned t = tune(x, art.tables, reg, hw);
     std::printf("decision: macro %d micro %d predicted %.3f us (C-ABI macro %d)\n", t.macro_id, t.micro_id,
                 t.predicted_latency_us, one.macro_id);

@@ -47,6 +47,12 @@ def main():
     cfg = S.config_space(full=False)
     ce = capi.Engine(S.synthetic_tables(cfg), S.registry_arrays(cfg), n_sm=148)
     print("ctypes wt_tune_one (C=256)  :", lat_us(lambda: ce.tune_one(3000, 6144, 4096)))
+    ce.set_resident(20000)
+    print("ctypes resident (C=256)     :", lat_us(lambda: ce.tune_one(3000, 6144, 4096)))
+    ce.set_resident(0)
+    eng.set_resident(20000)
+    print("Engine.tune() resident      :", lat_us(lambda: eng.tune(x)))
+    eng.set_resident(0)
     out = os.path.join(ROOT, "gpurun_out")
     os.makedirs(out, exist_ok=True)
     wt.save_tables(art, os.path.join(out, "lat_tables.json"))
@@ -56,7 +62,6 @@ def main():
     subprocess.run([os.path.join(ROOT, "tools", "bin", "lat_tune"), os.path.join(out, "lat_tables.json"),
                     os.path.join(out, "lat_registry.json"), "148", "3000", "6144", "4096"], check=False)
 
-    os.environ["WT_FIT_TRACE"] = "1"
     cfg3 = S.config_space(full=True)
     rec4 = S.synthetic_records(cfg3, micros_per_macro=1)
     for _ in range(2):
