@@ -333,6 +333,25 @@ i64 nearest_anchor(const std::vector<i64>& sorted_anchors, i64 l, int* compariso
 Tuned tune(const KernelWorkload& x, const std::vector<DualTable>& tables, const ConfigRegistry& registry,
            const HardwareSpec& hw);
 
+// ---- ablation baselines (reference tuner.hpp:54-85): fitted by K2 on the
+// GPU from the same selected samples, evaluated by the baseline kernels.
+struct StepPredictor {
+    std::map<std::pair<int, i64>, double> t_wave;  // (macro_id, loop anchor) -> per-wave latency
+};
+struct GlobalLinearPredictor {
+    std::map<int, BilinearCoeffs> theta;  // macro_id -> single global fit
+};
+struct BaselinePredictor {
+    enum class Kind { Step, GlobalLinear } kind = Kind::Step;
+    StepPredictor step;
+    GlobalLinearPredictor linear;
+};
+BaselinePredictor fit_step_baseline(const std::vector<ProfileRecord>& records);
+BaselinePredictor fit_linear_baseline(const std::vector<ProfileRecord>& records);
+double baseline_predict(const BaselinePredictor& bp, int macro_id, i64 g, i64 l, const HardwareSpec& hw);
+Tuned baseline_tune(const KernelWorkload& x, const BaselinePredictor& bp, const std::vector<DualTable>& tables,
+                    const ConfigRegistry& registry, const HardwareSpec& hw);
+
 // ============================================================ batched (new)
 // A device-resident engine: the (tables, registry, hw) triple validated and
 // uploaded once; queries go straight to the kernels.

@@ -191,6 +191,36 @@ wt_status wt_tune_one(const wt_engine* e, int32_t M, int32_t N, int32_t K, wt_de
  * idle_us = 0 stops it and returns to one launch per query (the default). */
 wt_status wt_engine_set_resident(wt_engine* e, int32_t idle_us);
 
+/* ---- ablation baselines (tuner.hpp:54-85, tuner.cpp:168-250) ----------- */
+
+#define WT_BASELINE_STEP 0   /* T = t_wave[(macro, nearest anchor)] * wave_count(g) */
+#define WT_BASELINE_LINEAR 1 /* T = one bilinear fit per macro, no wave regimes */
+
+typedef struct wt_baseline wt_baseline;
+
+/* A baseline predictor on the device.  Step: n entries (macro_id[i],
+ * anchor_l[i], values[i] = t_wave) sorted by (macro_id, anchor_l) -- the
+ * StepPredictor map order.  Linear: n entries macro_id[i] (ascending),
+ * values[4i..4i+3] = (alpha, beta, gamma, delta); anchor_l unused.
+ * e != NULL binds the baseline to that engine's configs (needed for
+ * wt_baseline_tune_batch); an engine table without an entry makes every
+ * valid query fail with OUT_OF_RANGE, as baseline_predict throws. */
+wt_status wt_baseline_create(const wt_engine* e, int device, int32_t kind, const int32_t* macro_id,
+                             const int64_t* anchor_l, const double* values, int64_t n, wt_baseline** out);
+wt_status wt_baseline_destroy(wt_baseline* b);
+
+/* baseline_tune() for dense/attention queries (device arrays): Stage I with
+ * the baseline predictor, Stage II on the engine's dual tables.  Same output
+ * contract as wt_tune_batch (no top-k). */
+wt_status wt_baseline_tune_batch(const wt_engine* e, const wt_baseline* b, const int32_t* M, const int32_t* N,
+                                 const int32_t* K, int64_t n, const wt_decisions* out, void* stream);
+
+/* baseline_predict(bp, macro_id, g, l, hw) for n device-array triples;
+ * status[i] = OK / OUT_OF_RANGE (no entry) / INVALID_ARGUMENT (step, g < 1). */
+wt_status wt_baseline_predict_batch(const wt_baseline* b, const int32_t* macro_id, const int64_t* g,
+                                    const int64_t* l, int64_t n, const wt_hw* hw, double* latency, int32_t* status,
+                                    void* stream);
+
 /* ---- batched tune (evaluate mode: every query runs full Stage I) -------- */
 
 /* Dense GEMM (M,N,K) / FlashAttention (s_q,n_heads,s_kv) queries, int32
@@ -311,6 +341,17 @@ typedef struct {
     const int64_t* ext_l;
     const int32_t* ext_micro;
     double device_ms;            /* GPU time of the build (CUDA events) */
+    /* Ablation baselines fitted from the same shared-micro-selected samples
+     * (tuner.cpp:191-220), per table in the order above.  Step: t_wave of
+     * anchors [step_off[i], step_off[i+1]) (ascending l).  Linear: one
+     * bilinear fit of all the table's samples, theta [4 per table]. */
+    const int32_t* step_off;
+    const int64_t* step_l;
+    const double* step_t;
+    const double* lin_theta;
+    const double* lin_r2;
+    const double* lin_mape;
+    const int32_t* lin_degenerate;
 } wt_build_result;
 
 typedef struct wt_build wt_build;

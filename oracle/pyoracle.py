@@ -366,3 +366,47 @@ def ref_oracle_best(ref, registry_json, ground_json, n_sm, seed, M, N, K, sigma,
     if st:
         raise RuntimeError(ref.err())
     return ma.value, mi.value, lat.value
+
+
+# ---- ablation baselines through the reference (tuner.cpp:168-250) ----------
+def ref_fit_baselines(ref, records_csv, cap=1 << 20):
+    sm, sl, st = np.zeros(cap, I32), np.zeros(cap, I64), np.zeros(cap, F64)
+    lm, lt = np.zeros(cap, I32), np.zeros(4 * cap, F64)
+    ns, nl = C.c_int64(), C.c_int64()
+    if ref.lib.wtref_fit_baselines(records_csv.encode(), C.c_int64(cap), _p(sm, C.c_int32), _p(sl, C.c_int64),
+                                   _p(st, C.c_double), C.byref(ns), _p(lm, C.c_int32), _p(lt, C.c_double),
+                                   C.byref(nl)):
+        raise RuntimeError(ref.err())
+    k, j = ns.value, nl.value
+    return dict(step_macro=sm[:k], step_l=sl[:k], step_t=st[:k], lin_macro=lm[:j], lin_theta=lt[:4 * j])
+
+
+def _bp_arrays(kind, bp):
+    if kind == 0:
+        return (np.ascontiguousarray(bp["step_macro"], I32), np.ascontiguousarray(bp["step_l"], I64),
+                np.ascontiguousarray(bp["step_t"], F64), len(bp["step_macro"]))
+    m = np.ascontiguousarray(bp["lin_macro"], I32)
+    return m, np.zeros(len(m), I64), np.ascontiguousarray(bp["lin_theta"], F64), len(m)
+
+
+def ref_baseline_predict(ref, kind, bp, n_sm, bps, macro, g, l):
+    m, ls, t, n = _bp_arrays(kind, bp)
+    out = C.c_double()
+    st = ref.lib.wtref_baseline_predict(C.c_int(kind), _p(m, C.c_int32), _p(ls, C.c_int64), _p(t, C.c_double),
+                                        C.c_int64(n), C.c_int(n_sm), C.c_int(bps), C.c_int32(macro),
+                                        C.c_int64(g), C.c_int64(l), C.byref(out))
+    return st, out.value
+
+
+def ref_baseline_tune(ref, h, kind, bp, M, N, K, nthreads=8):
+    m, ls, t, nb = _bp_arrays(kind, bp)
+    M, N, K = (np.ascontiguousarray(x, I64) for x in (M, N, K))
+    n = len(M)
+    o = {k: np.zeros(n, I32) for k in ("macro", "micro", "w", "extrap", "comps", "flag_count", "status")}
+    o["lat"] = np.zeros(n, F64)
+    ref.lib.wtref_baseline_tune(
+        C.c_void_p(h), C.c_int(kind), _p(m, C.c_int32), _p(ls, C.c_int64), _p(t, C.c_double), C.c_int64(nb),
+        _p(M, C.c_int64), _p(N, C.c_int64), _p(K, C.c_int64), C.c_int64(n), _p(o["macro"], C.c_int32),
+        _p(o["micro"], C.c_int32), _p(o["lat"], C.c_double), _p(o["w"], C.c_int32), _p(o["extrap"], C.c_int32),
+        _p(o["comps"], C.c_int32), _p(o["flag_count"], C.c_int32), _p(o["status"], C.c_int32), C.c_int(nthreads))
+    return o

@@ -309,3 +309,94 @@ WTREF_API int wtref_oracle_best(const char* registry_json, const char* ground_js
         return fail(e);
     }
 }
+
+// ---- ablation baselines (tuner.cpp:168-250) ---------------------------------
+
+// fit_step_baseline + fit_linear_baseline from a records CSV.  Step entries in
+// map order ((macro, l) ascending); linear thetas in macro order.
+WTREF_API int wtref_fit_baselines(const char* records_csv, int64_t cap, int32_t* step_macro, int64_t* step_l,
+                                  double* step_t, int64_t* n_step, int32_t* lin_macro, double* lin_theta,
+                                  int64_t* n_lin) {
+    try {
+        auto recs = read_records(records_csv);
+        BaselinePredictor s = fit_step_baseline(recs);
+        BaselinePredictor l = fit_linear_baseline(recs);
+        int64_t k = 0;
+        for (const auto& [key, t] : s.step.t_wave) {
+            if (k >= cap) throw std::runtime_error("wtref_fit_baselines: cap too small");
+            step_macro[k] = key.first;
+            step_l[k] = key.second;
+            step_t[k] = t;
+            ++k;
+        }
+        *n_step = k;
+        k = 0;
+        for (const auto& [m, th] : l.linear.theta) {
+            if (k >= cap) throw std::runtime_error("wtref_fit_baselines: cap too small");
+            lin_macro[k] = m;
+            lin_theta[4 * k + 0] = th.alpha;
+            lin_theta[4 * k + 1] = th.beta;
+            lin_theta[4 * k + 2] = th.gamma;
+            lin_theta[4 * k + 3] = th.delta;
+            ++k;
+        }
+        *n_lin = k;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+namespace {
+// kind 0 = step: entries (macro[i], l[i], t[i]); kind 1 = linear: macro[i], theta[4i..4i+3]
+BaselinePredictor make_bp(int kind, const int32_t* macro, const int64_t* l, const double* t, int64_t n) {
+    BaselinePredictor bp;
+    bp.kind = kind == 0 ? BaselinePredictor::Kind::Step : BaselinePredictor::Kind::GlobalLinear;
+    for (int64_t i = 0; i < n; ++i) {
+        if (kind == 0) bp.step.t_wave[{macro[i], l[i]}] = t[i];
+        else bp.linear.theta[macro[i]] = BilinearCoeffs{t[4 * i], t[4 * i + 1], t[4 * i + 2], t[4 * i + 3]};
+    }
+    return bp;
+}
+}  // namespace
+
+WTREF_API int wtref_baseline_predict(int kind, const int32_t* macro, const int64_t* l, const double* t, int64_t n,
+                                     int n_sm, int bps, int32_t qmacro, int64_t qg, int64_t ql, double* out) {
+    try {
+        *out = baseline_predict(make_bp(kind, macro, l, t, n), qmacro, qg, ql, HardwareSpec{n_sm, bps, ""});
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// Batched baseline_tune() over dense queries against an opened handle's tables.
+WTREF_API int wtref_baseline_tune(void* hp, int kind, const int32_t* bmacro, const int64_t* bl, const double* bt,
+                                  int64_t nb, const int64_t* M, const int64_t* N, const int64_t* K, int64_t n,
+                                  int32_t* macro, int32_t* micro, double* lat, int32_t* w, int32_t* extrap,
+                                  int32_t* comps, int32_t* flag_count, int32_t* status, int nthreads) {
+    const Handle& h = *static_cast<Handle*>(hp);
+    const BaselinePredictor bp = make_bp(kind, bmacro, bl, bt, nb);
+    if (nthreads < 1) nthreads = 1;
+    auto work = [&](int tid) {
+        for (int64_t i = tid; i < n; i += nthreads) {
+            try {
+                Tuned t = baseline_tune(DenseGemm{M[i], N[i], K[i]}, bp, h.artifact.tables, h.registry, h.hw);
+                macro[i] = t.macro_id;
+                micro[i] = t.micro_id;
+                lat[i] = t.predicted_latency_us;
+                w[i] = t.regime.w;
+                extrap[i] = t.regime.extrapolated ? 1 : 0;
+                comps[i] = t.stats.anchor_comparisons;
+                flag_count[i] = static_cast<int32_t>(t.flags.size());
+                status[i] = 0;
+            } catch (const std::exception& e) {
+                status[i] = fail(e);
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nthreads; ++t) pool.emplace_back(work, t);
+    for (auto& th : pool) th.join();
+    return 0;
+}

@@ -81,9 +81,12 @@ _BUILD_FIELDS = ("macro_id theta_ext ext_flags coeff_off coeff_w coeff_theta dia
                  "ext_micro").split()
 
 
+_BASELINE_FIELDS = "step_off step_l step_t lin_theta lin_r2 lin_mape lin_degenerate".split()
+
+
 class wt_build_result(C.Structure):
     _fields_ = [("n_tables", C.c_int32), ("W", C.c_int32), ("p", C.c_int32)] + [(n, vp) for n in _BUILD_FIELDS] + [
-        ("device_ms", C.c_double)]
+        ("device_ms", C.c_double)] + [(n, vp) for n in _BASELINE_FIELDS]
 
 
 # entry points declared in include/wavetune_c.h (tests check they all exist)
@@ -92,7 +95,8 @@ EXPORTS = (
     "wt_engine_config_index wt_tune_batch wt_tune_grouped_batch wt_predict_batch wt_explain "
     "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_destroy wt_grid_storage wt_sweep "
     "wt_gather_batch wt_decide_host_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
-    "wt_simulate_batch wt_profile_sim wt_tune_one wt_engine_set_resident").split()
+    "wt_simulate_batch wt_profile_sim wt_tune_one wt_engine_set_resident wt_baseline_create "
+    "wt_baseline_destroy wt_baseline_tune_batch wt_baseline_predict_batch").split()
 
 _lib = None
 
@@ -245,6 +249,44 @@ class Engine:
                                vp(_stream_ptr(stream))))
 
 
+class Baseline:
+    """A device baseline predictor (wt_baseline): kind 0 = step, 1 = linear.
+    Step entries sorted by (macro, l); linear: one theta row per macro."""
+
+    def __init__(self, engine, kind, macro_id, anchor_l, values, device=0):
+        self.engine = engine
+        self._keep = [np.ascontiguousarray(macro_id, np.int32), np.ascontiguousarray(anchor_l, np.int64),
+                      np.ascontiguousarray(values, np.float64)]
+        h = C.c_void_p()
+        m, l, v = self._keep
+        check(lib().wt_baseline_create(engine.handle if engine is not None else None, C.c_int(device),
+                                       C.c_int32(kind), vp(m.ctypes.data), vp(l.ctypes.data), vp(v.ctypes.data),
+                                       C.c_int64(len(m)), C.byref(h)))
+        self.handle = h.value
+
+    def close(self):
+        if self.handle:
+            lib().wt_baseline_destroy(vp(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def tune_batch(self, M, N, K, out: wt_decisions, stream=None):
+        check(lib().wt_baseline_tune_batch(self.engine.handle, vp(self.handle), vp(_ptr(M)), vp(_ptr(N)),
+                                           vp(_ptr(K)), C.c_int64(M.numel()), C.byref(out),
+                                           vp(_stream_ptr(stream))))
+
+    def predict_batch(self, macro, g, l, n_sm, bps, lat, status, stream=None):
+        hw = wt_hw(n_sm, bps)
+        check(lib().wt_baseline_predict_batch(vp(self.handle), vp(_ptr(macro)), vp(_ptr(g)), vp(_ptr(l)),
+                                              C.c_int64(macro.numel()), C.byref(hw), vp(_ptr(lat)),
+                                              vp(_ptr(status)), vp(_stream_ptr(stream))))
+
+
 class Grid:
     """A decision grid: tune() over n_pairs (N, K) x M in [m_lo, m_hi]."""
 
@@ -354,6 +396,13 @@ def fit_build(records: dict, registry_ids, W: int = 0, p: int = 10, device: int 
         anchor_partial=_np_from(res.anchor_partial, nan, np.int32), ext_aoff=ex_off,
         ext_l=_np_from(res.ext_l, next_, np.int64), ext_micro=_np_from(res.ext_micro, next_, np.int32))
     out["W_arr"] = np.full(nt, res.W, np.int32)
+    # ablation baselines from the same selected samples (tuner.cpp:191-220)
+    s_off = _np_from(res.step_off, nt + 1, np.int32)
+    out.update(step_off=s_off, step_l=_np_from(res.step_l, int(s_off[-1]), np.int64),
+               step_t=_np_from(res.step_t, int(s_off[-1]), np.float64),
+               lin_theta=_np_from(res.lin_theta, 4 * nt, np.float64), lin_r2=_np_from(res.lin_r2, nt, np.float64),
+               lin_mape=_np_from(res.lin_mape, nt, np.float64),
+               lin_degenerate=_np_from(res.lin_degenerate, nt, np.int32))
     lib().wt_build_free(h)
     return out
 

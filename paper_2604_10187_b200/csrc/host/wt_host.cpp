@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <set>
+#include <limits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1429,6 +1431,217 @@ i64 nearest_anchor(const std::vector<i64>& sorted_anchors, i64 l, int* compariso
     cu(cudaMemcpy(&c, dc, 4, cudaMemcpyDeviceToHost), "anchor out");
     if (comparisons) *comparisons = c;
     return r;
+}
+
+// -------------------------------------------------------------- baselines
+namespace {
+
+BaselinePredictor device_baselines(const std::vector<ProfileRecord>& records, BaselinePredictor::Kind kind) {
+    BaselinePredictor bp;
+    bp.kind = kind;
+    if (records.empty()) return bp;
+    // every macro of the records: selected_samples() has no registry filter
+    std::set<int> macros;
+    for (const auto& r : records) macros.insert(r.macro_id);
+    const size_t n = records.size();
+    std::vector<int64_t> g(n), l(n);
+    std::vector<int32_t> w(n), ma(n), mi(n);
+    std::vector<double> t(n);
+    for (size_t i = 0; i < n; ++i) {
+        g[i] = records[i].g;
+        l[i] = records[i].l;
+        w[i] = records[i].w;
+        ma[i] = records[i].macro_id;
+        mi[i] = records[i].micro_id;
+        t[i] = records[i].latency_us;
+    }
+    wt_records_desc rd{int64_t(n), g.data(), l.data(), w.data(), ma.data(), mi.data(), t.data()};
+    std::vector<int32_t> ids(macros.begin(), macros.end());
+    wt_build* b = nullptr;
+    wt_build_result R{};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    ok(wt_fit_build(&rd, ids.data(), int32_t(ids.size()), 0, 10, dev, &b, &R));
+    std::unique_ptr<wt_build, wt_status (*)(wt_build*)> guard(b, wt_build_free);
+    for (int32_t q = 0; q < R.n_tables; ++q) {
+        const int m = R.macro_id[q];
+        if (kind == BaselinePredictor::Kind::Step)
+            for (int32_t k = R.step_off[q]; k < R.step_off[q + 1]; ++k) bp.step.t_wave[{m, R.step_l[k]}] = R.step_t[k];
+        else
+            bp.linear.theta[m] = {R.lin_theta[4 * q], R.lin_theta[4 * q + 1], R.lin_theta[4 * q + 2],
+                                  R.lin_theta[4 * q + 3]};
+    }
+    return bp;
+}
+
+// Flattened entries in the C-ABI's order (step: (macro, l); linear: macro).
+struct BaselineArrays {
+    int32_t kind;
+    std::vector<int32_t> macro;
+    std::vector<int64_t> l;
+    std::vector<double> v;
+};
+BaselineArrays flatten(const BaselinePredictor& bp) {
+    BaselineArrays a;
+    a.kind = bp.kind == BaselinePredictor::Kind::Step ? WT_BASELINE_STEP : WT_BASELINE_LINEAR;
+    if (a.kind == WT_BASELINE_STEP)
+        for (const auto& [key, t] : bp.step.t_wave) {
+            a.macro.push_back(key.first);
+            a.l.push_back(key.second);
+            a.v.push_back(t);
+        }
+    else
+        for (const auto& [m, th] : bp.linear.theta) {
+            a.macro.push_back(m);
+            a.v.insert(a.v.end(), {th.alpha, th.beta, th.gamma, th.delta});
+        }
+    return a;
+}
+
+uint64_t bp_fingerprint(const BaselineArrays& a) {
+    uint64_t h = fnv(0xcbf29ce484222325ULL, &a.kind, sizeof a.kind);
+    h = fnv(h, a.macro.data(), a.macro.size() * 4);
+    h = fnv(h, a.l.data(), a.l.size() * 8);
+    return fnv(h, a.v.data(), a.v.size() * 8);
+}
+
+struct DeviceBaseline {
+    std::shared_ptr<Engine> engine;  // keeps the bound engine alive
+    wt_baseline* b = nullptr;
+    ~DeviceBaseline() { wt_baseline_destroy(b); }
+};
+
+std::shared_ptr<DeviceBaseline> cached_baseline(const BaselinePredictor& bp, std::shared_ptr<Engine> eng) {
+    static std::mutex mu;
+    static std::map<std::pair<uint64_t, const void*>, std::shared_ptr<DeviceBaseline>> cache;
+    const BaselineArrays a = flatten(bp);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_pair(bp_fingerprint(a) ^ uint64_t(dev), eng ? eng->handle() : nullptr);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    auto d = std::make_shared<DeviceBaseline>();
+    d->engine = eng;
+    ok(wt_baseline_create(eng ? static_cast<const wt_engine*>(eng->handle()) : nullptr, dev, a.kind, a.macro.data(),
+                          a.l.data(), a.v.data(), int64_t(a.macro.size()), &d->b));
+    std::lock_guard<std::mutex> lock(mu);
+    if (cache.size() > 64) cache.clear();
+    cache[key] = d;
+    return d;
+}
+
+const char* baseline_name(const BaselinePredictor& bp) {
+    return bp.kind == BaselinePredictor::Kind::GlobalLinear ? "linear" : "step";
+}
+
+bool has_entry(const BaselinePredictor& bp, int macro_id) {
+    if (bp.kind == BaselinePredictor::Kind::GlobalLinear) return bp.linear.theta.count(macro_id) != 0;
+    auto it = bp.step.t_wave.lower_bound({macro_id, std::numeric_limits<i64>::min()});
+    return it != bp.step.t_wave.end() && it->first.first == macro_id;
+}
+
+}  // namespace
+
+BaselinePredictor fit_step_baseline(const std::vector<ProfileRecord>& records) {
+    return device_baselines(records, BaselinePredictor::Kind::Step);
+}
+
+BaselinePredictor fit_linear_baseline(const std::vector<ProfileRecord>& records) {
+    return device_baselines(records, BaselinePredictor::Kind::GlobalLinear);
+}
+
+double baseline_predict(const BaselinePredictor& bp, int macro_id, i64 g, i64 l, const HardwareSpec& hw) {
+    auto d = cached_baseline(bp, nullptr);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    char* base = static_cast<char*>(t_scratch.get(256, dev));
+    int32_t* dm = reinterpret_cast<int32_t*>(base);
+    int64_t* dg = reinterpret_cast<int64_t*>(base + 64);
+    int64_t* dl = dg + 1;
+    double* dlat = reinterpret_cast<double*>(base + 128);
+    int32_t* dst = reinterpret_cast<int32_t*>(base + 192);
+    const int64_t gl[2] = {g, l};
+    cu(cudaMemcpy(dm, &macro_id, 4, cudaMemcpyHostToDevice), "baseline upload");
+    cu(cudaMemcpy(dg, gl, 16, cudaMemcpyHostToDevice), "baseline upload");
+    const wt_hw h{hw.n_sm, hw.blocks_per_sm};
+    ok(wt_baseline_predict_batch(d->b, dm, dg, dl, 1, &h, dlat, dst, nullptr));
+    double v;
+    int32_t st;
+    cu(cudaMemcpy(&v, dlat, 8, cudaMemcpyDeviceToHost), "baseline download");
+    cu(cudaMemcpy(&st, dst, 4, cudaMemcpyDeviceToHost), "baseline download");
+    if (st == WT_OUT_OF_RANGE)
+        throw std::out_of_range(std::string("no ") + baseline_name(bp) + " baseline for macro " +
+                                std::to_string(macro_id));
+    if (st == WT_INVALID_ARGUMENT) (void)wave_count(g, hw);  // throws the reference's message
+    if (st != WT_OK) rethrow(wt_status(st), "baseline_predict failed");
+    return v;
+}
+
+Tuned baseline_tune(const KernelWorkload& x, const BaselinePredictor& bp, const std::vector<DualTable>& tables,
+                    const ConfigRegistry& registry, const HardwareSpec& hw) {
+    if (tables.empty()) throw std::invalid_argument("no dual tables provided");
+    if (std::holds_alternative<GroupedGemm>(x))
+        throw std::invalid_argument("baseline_tune: grouped_gemm queries are not supported by the device path");
+    auto eng = cached_engine(tables, registry, hw);
+    // the reference's exception order: map_workload's argument checks on the
+    // first table, then baseline_predict's missing entry in ascending macro order
+    i64 M, N, K;
+    if (const auto* d = std::get_if<DenseGemm>(&x)) M = d->m, N = d->n, K = d->k;
+    else {
+        const auto& a = std::get<FlashAttention>(x);
+        M = a.s_q, N = a.n_heads, K = a.s_kv;
+    }
+    std::vector<int> ids;
+    for (const auto& t : tables) ids.push_back(t.macro_id);
+    std::sort(ids.begin(), ids.end());
+    (void)map_workload(x, registry.macro(ids.front()));
+    for (int id : ids)
+        if (!has_entry(bp, id))
+            throw std::out_of_range(std::string("no ") + baseline_name(bp) + " baseline for macro " +
+                                    std::to_string(id));
+    if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
+        throw std::invalid_argument("dims above 2^31-1 are outside the device path's range");
+    auto d = cached_baseline(bp, eng);
+    auto* e = static_cast<const wt_engine*>(eng->handle());
+    char* base = static_cast<char*>(t_scratch.get(4096, eng->device()));
+    int32_t* q = reinterpret_cast<int32_t*>(base);
+    QueryOut* o = reinterpret_cast<QueryOut*>(base + 128);
+    const int32_t hq[3] = {int32_t(M), int32_t(N), int32_t(K)};
+    cu(cudaMemcpy(q, hq, sizeof hq, cudaMemcpyHostToDevice), "baseline upload");
+    wt_decisions dd{};
+    dd.macro_id = &o->macro;
+    dd.micro_id = &o->micro;
+    dd.latency_us = &o->lat;
+    dd.g = &o->g;
+    dd.l = &o->l;
+    dd.wave = &o->wave;
+    dd.flags = &o->flags;
+    dd.comparisons = &o->comps;
+    dd.tail_frac = &o->tail;
+    ok(wt_baseline_tune_batch(e, d->b, q, q + 1, q + 2, 1, &dd, nullptr));
+    QueryOut h{};
+    cu(cudaMemcpy(&h, o, sizeof h, cudaMemcpyDeviceToHost), "baseline download");
+    const int st = WT_FLAG_STATUS(h.flags);
+    if (st != 0) rethrow(wt_status(st), "baseline_tune: decision failed (no finite prediction or no anchor entries)");
+    Tuned t;
+    t.macro_id = h.macro;
+    t.micro_id = h.micro;
+    t.predicted_latency_us = h.lat;
+    t.g = h.g;
+    t.l = h.l;
+    t.regime = Regime{(h.flags & WT_FLAG_EXTRAPOLATED) != 0, h.wave};
+    t.stats.model_evals = int(tables.size());
+    t.stats.anchor_comparisons = h.comps;
+    if (h.flags & WT_FLAG_ANCHOR_FALLBACK) {
+        const int cfg = wt_engine_config_index(e, h.macro);
+        int32_t fb = -1;
+        wt_engine_anchor_map(e, cfg, h.wave, (h.flags & WT_FLAG_EXTRAPOLATED) ? 1 : 0, nullptr, nullptr, 0, &fb);
+        t.flags.push_back("anchor_fallback_wave_" + std::to_string(fb));
+    }
+    return t;
 }
 
 }  // namespace wavetune

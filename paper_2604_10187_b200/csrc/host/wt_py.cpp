@@ -274,6 +274,35 @@ PYBIND11_MODULE(_core, m) {
             return tune(x, a.tables, reg, hw);
         },
         py::arg("workload"), py::arg("tables"), py::arg("registry"), py::arg("hw"));
+    // ---- ablation baselines (tuner.hpp:54-85)
+    py::class_<StepPredictor>(m, "StepPredictor")
+        .def(py::init<>())
+        .def_readwrite("t_wave", &StepPredictor::t_wave);
+    py::class_<GlobalLinearPredictor>(m, "GlobalLinearPredictor")
+        .def(py::init<>())
+        .def_readwrite("theta", &GlobalLinearPredictor::theta);
+    py::class_<BaselinePredictor>(m, "BaselinePredictor")
+        .def(py::init<>())
+        .def_property(
+            "kind",
+            [](const BaselinePredictor& b) {
+                return std::string(b.kind == BaselinePredictor::Kind::Step ? "step" : "linear");
+            },
+            [](BaselinePredictor& b, const std::string& k) {
+                if (k != "step" && k != "linear") throw std::invalid_argument("kind must be 'step' or 'linear'");
+                b.kind = k == "step" ? BaselinePredictor::Kind::Step : BaselinePredictor::Kind::GlobalLinear;
+            })
+        .def_readwrite("step", &BaselinePredictor::step)
+        .def_readwrite("linear", &BaselinePredictor::linear);
+    m.def("fit_step_baseline", &fit_step_baseline, py::arg("records"));
+    m.def("fit_linear_baseline", &fit_linear_baseline, py::arg("records"));
+    m.def("baseline_predict", &baseline_predict, py::arg("bp"), py::arg("macro_id"), py::arg("g"), py::arg("l"),
+          py::arg("hw"));
+    m.def(
+        "baseline_tune",
+        [](const KernelWorkload& x, const BaselinePredictor& bp, const TableArtifact& a, const ConfigRegistry& reg,
+           const HardwareSpec& hw) { return baseline_tune(x, bp, a.tables, reg, hw); },
+        py::arg("workload"), py::arg("bp"), py::arg("tables"), py::arg("registry"), py::arg("hw"));
     m.def(
         "predict_latency",
         [](const DualTable& t, i64 g, i64 l, const HardwareSpec& hw) {

@@ -456,6 +456,150 @@ wt_status wt_engine_set_resident(wt_engine* e, int32_t idle_us) {
     return WT_OK;
 }
 
+// ------------------------------------------------------- ablation baselines
+struct wt_baseline {
+    int device = 0;
+    const wt_engine* eng = nullptr;
+    BaseImage img{};
+    void* mem = nullptr;
+};
+
+wt_status wt_baseline_create(const wt_engine* e, int device, int32_t kind, const int32_t* macro_id,
+                             const int64_t* anchor_l, const double* values, int64_t n, wt_baseline** out) {
+    if (!out) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    if (kind != WT_BASELINE_STEP && kind != WT_BASELINE_LINEAR) return set_err(WT_INVALID_ARGUMENT, "unknown baseline kind");
+    if (n < 0 || (n > 0 && (!macro_id || !values || (kind == WT_BASELINE_STEP && !anchor_l))))
+        return set_err(WT_INVALID_ARGUMENT, "null or negative baseline arrays");
+    for (int64_t i = 1; i < n; ++i) {
+        const bool asc = kind == WT_BASELINE_STEP
+                             ? (macro_id[i - 1] < macro_id[i] ||
+                                (macro_id[i - 1] == macro_id[i] && anchor_l[i - 1] < anchor_l[i]))
+                             : macro_id[i - 1] < macro_id[i];
+        if (!asc) return set_err(WT_INVALID_ARGUMENT, "baseline entries must be strictly ascending");
+    }
+    if (e) device = e->device;
+    std::vector<int32_t> cfg;  // config macro ids, ascending
+    if (e) cfg = e->host.macro_id;
+    else
+        for (int64_t i = 0; i < n; ++i)
+            if (cfg.empty() || cfg.back() != macro_id[i]) cfg.push_back(macro_id[i]);
+    const int C = int(cfg.size());
+    std::vector<int32_t> has(C, 0), off(C + 1, 0);
+    std::vector<double> theta(size_t(C) * 4, 0.0), tw;
+    std::vector<int64_t> al;
+    int missing = 0;
+    int64_t i = 0;
+    for (int c = 0; c < C; ++c) {
+        while (i < n && macro_id[i] < cfg[c]) ++i;
+        off[c] = int32_t(al.size());
+        int64_t j = i;
+        while (j < n && macro_id[j] == cfg[c]) {
+            if (kind == WT_BASELINE_STEP) {
+                al.push_back(anchor_l[j]);
+                tw.push_back(values[j]);
+            } else {
+                for (int q = 0; q < 4; ++q) theta[size_t(c) * 4 + q] = values[4 * j + q];
+            }
+            ++j;
+        }
+        has[c] = j > i ? 1 : 0;
+        if (!has[c]) missing = 1;
+        i = j;
+    }
+    off[C] = int32_t(al.size());
+    DeviceGuard guard(device);
+    Arena ar;
+    const size_t o_mac = ar.take(size_t(C) * 4), o_has = ar.take(size_t(C) * 4), o_th = ar.take(theta.size() * 8),
+                 o_off = ar.take(off.size() * 4), o_al = ar.take(al.size() * 8), o_tw = ar.take(tw.size() * 8);
+    auto* b = new wt_baseline;
+    b->device = device;
+    b->eng = e;
+    cudaError_t ce = cudaMalloc(&b->mem, std::max<size_t>(ar.used, 256));
+    if (ce != cudaSuccess) {
+        delete b;
+        return cuda_err(ce, "wt_baseline_create");
+    }
+    char* base = static_cast<char*>(b->mem);
+    auto up = [&](size_t o, const void* src, size_t bytes) {
+        if (bytes && ce == cudaSuccess) ce = cudaMemcpy(base + o, src, bytes, cudaMemcpyHostToDevice);
+    };
+    up(o_mac, cfg.data(), size_t(C) * 4);
+    up(o_has, has.data(), size_t(C) * 4);
+    up(o_th, theta.data(), theta.size() * 8);
+    up(o_off, off.data(), off.size() * 4);
+    up(o_al, al.data(), al.size() * 8);
+    up(o_tw, tw.data(), tw.size() * 8);
+    if (ce != cudaSuccess) {
+        cudaFree(b->mem);
+        delete b;
+        return cuda_err(ce, "wt_baseline_create upload");
+    }
+    BaseImage& im = b->img;
+    im.kind = kind;
+    im.C = C;
+    im.missing = e ? missing : 0;
+    im.S = e ? e->host.S : 0;
+    im.macro = reinterpret_cast<const int32_t*>(base + o_mac);
+    im.has = reinterpret_cast<const int32_t*>(base + o_has);
+    im.theta = reinterpret_cast<const double4*>(base + o_th);
+    im.off = reinterpret_cast<const int32_t*>(base + o_off);
+    im.al = reinterpret_cast<const int64_t*>(base + o_al);
+    im.tw = reinterpret_cast<const double*>(base + o_tw);
+    *out = b;
+    return WT_OK;
+}
+
+wt_status wt_baseline_destroy(wt_baseline* b) {
+    if (!b) return WT_OK;
+    DeviceGuard guard(b->device);
+    cudaFree(b->mem);
+    delete b;
+    return WT_OK;
+}
+
+wt_status wt_baseline_tune_batch(const wt_engine* e, const wt_baseline* b, const int32_t* M, const int32_t* N,
+                                 const int32_t* K, int64_t n, const wt_decisions* out, void* stream) {
+    if (!e || !b) return set_err(WT_INVALID_ARGUMENT, "null engine or baseline");
+    if (b->eng != e) return set_err(WT_INVALID_ARGUMENT, "baseline was not created for this engine");
+    if (n < 0) return set_err(WT_INVALID_ARGUMENT, "negative batch size");
+    wt_status st = check_out(out);
+    if (st) return st;
+    if (out->topk) return set_err(WT_UNSUPPORTED, "topk is not available for baseline queries");
+    if (n == 0) return WT_OK;
+    if (e->host.family == WT_FAMILY_GROUPED_GEMM)
+        return set_err(WT_INVALID_ARGUMENT, "dense_gemm workload needs gemm tiles");
+    DeviceGuard guard(e->device);
+    EvalArgs a{};
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.n = n;
+    a.out = to_out(out);
+    const cudaError_t ce = launch_btune(e->dev, b->img, a, static_cast<cudaStream_t>(stream));
+    g_launches++;
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_baseline_tune_batch");
+    return WT_OK;
+}
+
+wt_status wt_baseline_predict_batch(const wt_baseline* b, const int32_t* macro_id, const int64_t* g,
+                                    const int64_t* l, int64_t n, const wt_hw* hw, double* latency, int32_t* status,
+                                    void* stream) {
+    if (!b || !hw) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    if (n < 0) return set_err(WT_INVALID_ARGUMENT, "negative batch size");
+    if (n == 0) return WT_OK;
+    if (!macro_id || !g || !l || !latency || !status) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    DeviceGuard guard(b->device);
+    BaseImage im = b->img;
+    const int64_t S = int64_t(hw->n_sm) * hw->blocks_per_sm;
+    im.S = (hw->n_sm < 1 || hw->blocks_per_sm < 1 || S > INT32_MAX) ? 0 : int32_t(S);
+    BPredictArgs a{macro_id, g, l, n, latency, status};
+    const cudaError_t ce = launch_bpredict(im, a, static_cast<cudaStream_t>(stream));
+    g_launches++;
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_baseline_predict_batch");
+    return WT_OK;
+}
+
 wt_status wt_tune_grouped_batch(const wt_engine* e, const int64_t* row_off, const int32_t* rows,
                                 const int32_t* N, const int32_t* K, int64_t n,
                                 const wt_decisions* out, void* stream) {

@@ -24,19 +24,6 @@
 
 namespace wtb {
 
-__device__ __forceinline__ void write_decision(const DecOut& o, int64_t q, const Final& f,
-                                               double lat, uint64_t g, int64_t l) {
-    const bool ok = (f.flags >> 24) == 0;
-    o.macro[q] = ok ? f.macro : -1;
-    o.micro[q] = ok ? f.micro : -1;
-    o.lat[q] = ok ? lat : __longlong_as_double(0x7ff8000000000000LL);
-    if (o.g) o.g[q] = ok ? int64_t(g) : 0;
-    if (o.l) o.l[q] = ok ? l : 0;
-    if (o.wave) o.wave[q] = ok ? f.wave : 0;
-    if (o.flags) o.flags[q] = f.flags;
-    if (o.comps) o.comps[q] = ok ? f.comps : 0;
-    if (o.tail) o.tail[q] = ok ? double(f.tail) : 0.0;
-}
 
 // ------------------------------------------------------------- K1: sweep
 // Shared-memory chunk of configs for one (N, K) pair.

@@ -137,6 +137,29 @@ struct OneOut {
 };
 cudaError_t launch_one(const DevImage& im, int32_t M, int32_t N, int32_t K, OneOut* out, uint32_t seq,
                        cudaStream_t st);
+// Ablation baselines (wt_baseline.cu, reference tuner.cpp:168-250).
+struct BaseImage {
+    int32_t kind;            // WT_BASELINE_STEP / WT_BASELINE_LINEAR
+    int32_t C;               // configs (engine order, or the baseline's own macros)
+    int32_t missing;         // some config has no entry: every valid query fails
+    int32_t S;               // slots (predict: per call)
+    const int32_t* macro;    // [C] ascending (predict lookup)
+    const int32_t* has;      // [C] 1 if the config has an entry
+    const double4* theta;    // linear: [C]
+    const int32_t* off;      // step: [C+1] into al / tw
+    const int64_t* al;       // step: anchors, ascending per config
+    const double* tw;        // step: per-wave latency per anchor
+};
+cudaError_t launch_btune(const DevImage& im, const BaseImage& b, const EvalArgs& a, cudaStream_t st);
+struct BPredictArgs {
+    const int32_t* macro;
+    const int64_t* g;
+    const int64_t* l;
+    int64_t n;
+    double* lat;
+    int32_t* status;
+};
+cudaError_t launch_bpredict(const BaseImage& b, const BPredictArgs& a, cudaStream_t st);
 // Resident decision server (wt_serve.cu): one CTA polls a pinned mailbox.
 struct alignas(64) Mailbox {
     // host -> device: one 16-byte record, read by the server in one load

@@ -567,6 +567,63 @@ __global__ void __launch_bounds__(32 * kFitWarps) k_fit(const double* sg, const 
     }
 }
 
+// ---- ablation baselines (tuner.cpp:168-220) from the selected samples.
+// Sample range of each macro: its groups are contiguous and in (w, l) order,
+// exactly the order selected_samples() appends them (tuner.cpp:174-187).
+__global__ void k_macro_samples(int64_t NM, const int64_t* mbs, const int64_t* bgs, const int64_t* soff,
+                                int64_t G, int64_t S_total, int64_t* mslo, int64_t* mshi) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= NM) return;
+    const int64_t g0 = bgs[mbs[q]], g1 = bgs[mbs[q + 1]];
+    mslo[q] = soff[g0];
+    mshi[q] = g1 < G ? soff[g1] : S_total;
+}
+
+// fit_step_baseline: per (macro, l), num += w*t, den += w*w in sample order,
+// t_wave = num/den.  One thread per macro walks its groups sequentially (the
+// reference's summation order); slots live at the macro's first group index
+// and come out sorted by l (the std::map order).
+__global__ void k_step(int64_t NM, const int64_t* mbs, const int64_t* bgs, const int64_t* gw, const int64_t* gl,
+                       const int64_t* soff, const int32_t* nsamp, const double* st, int64_t* slot_l,
+                       double* slot_num, double* slot_den, int32_t* nslot) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= NM) return;
+    const int64_t g0 = bgs[mbs[q]], g1 = bgs[mbs[q + 1]];
+    int n = 0;
+    for (int64_t grp = g0; grp < g1; ++grp) {
+        const int64_t l = gl[grp];
+        int s = 0;
+        while (s < n && slot_l[g0 + s] != l) ++s;
+        if (s == n) {
+            slot_l[g0 + n] = l;
+            slot_num[g0 + n] = 0.0;
+            slot_den[g0 + n] = 0.0;
+            ++n;
+        }
+        const double w = __ll2double_rn(gw[grp]);
+        double num = slot_num[g0 + s], den = slot_den[g0 + s];
+        for (int64_t i = soff[grp], e = soff[grp] + nsamp[grp]; i < e; ++i) {
+            num = __dadd_rn(num, __dmul_rn(w, st[i]));
+            den = __dadd_rn(den, __dmul_rn(w, w));
+        }
+        slot_num[g0 + s] = num;
+        slot_den[g0 + s] = den;
+    }
+    for (int a = 1; a < n; ++a)  // insertion sort by l (distinct keys)
+        for (int b = a; b > 0 && slot_l[g0 + b - 1] > slot_l[g0 + b]; --b) {
+            const int64_t tl = slot_l[g0 + b];
+            slot_l[g0 + b] = slot_l[g0 + b - 1];
+            slot_l[g0 + b - 1] = tl;
+            const double tn = slot_num[g0 + b], td = slot_den[g0 + b];
+            slot_num[g0 + b] = slot_num[g0 + b - 1];
+            slot_den[g0 + b] = slot_den[g0 + b - 1];
+            slot_num[g0 + b - 1] = tn;
+            slot_den[g0 + b - 1] = td;
+        }
+    for (int a = 0; a < n; ++a) slot_num[g0 + a] = __ddiv_rn(slot_num[g0 + a], slot_den[g0 + a]);
+    nslot[q] = n;
+}
+
 struct Macros {
     int64_t nmac;
     const int64_t* bstart;  // [nmac+1] bucket range per macro
@@ -685,9 +742,9 @@ struct FitErr {
 
 struct wt_build {
     std::vector<int32_t> macro_id, ext_flags, coeff_off, coeff_w, diag_samples, diag_flags, awave_off, awave_w,
-        awave_aoff, anchor_micro, anchor_partial, ext_aoff, ext_micro;
-    std::vector<double> theta_ext, coeff_theta, diag_r2, diag_mape;
-    std::vector<int64_t> anchor_l, ext_l;
+        awave_aoff, anchor_micro, anchor_partial, ext_aoff, ext_micro, step_off, lin_degen;
+    std::vector<double> theta_ext, coeff_theta, diag_r2, diag_mape, step_t, lin_theta, lin_r2, lin_mape;
+    std::vector<int64_t> anchor_l, ext_l, step_l;
 };
 
 
@@ -1026,8 +1083,22 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
               dalloc<int32_t>(owned, NM), dalloc<int64_t>(owned, G), dalloc<int32_t>(owned, G)};
     // extrapolation pools reuse the bucket scratch layout (slice of the pooled samples)
     k_extrap<<<nsm * 4, 128, 0, s>>>(rc, sg, sl, stt, bk, soff, gr, ordA, mc, scratch);
-    CK(cudaEventRecord(ev1, s));
     trace("k_extrap");
+    // ablation baselines from the same selected samples
+    int64_t* d_mslo = dalloc<int64_t>(owned, NM);
+    int64_t* d_mshi = dalloc<int64_t>(owned, NM);
+    k_macro_samples<<<int((NM + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, soff, G, S_total, d_mslo, d_mshi);
+    Buckets lin{NM, d_mslo, d_mshi, dalloc<double>(owned, NM * 4), dalloc<double>(owned, NM),
+                dalloc<double>(owned, NM), dalloc<int32_t>(owned, NM)};
+    k_fit<<<nsm * 8, 128, 0, s>>>(sg, sl, stt, lin, scratch);
+    int64_t* d_sll = dalloc<int64_t>(owned, G);
+    double* d_snum = dalloc<double>(owned, G);
+    double* d_sden = dalloc<double>(owned, G);
+    int32_t* d_nslot = dalloc<int32_t>(owned, NM);
+    k_step<<<int((NM + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, gw, gl, soff, gr.nsamp, stt, d_sll, d_snum,
+                                                  d_sden, d_nslot);
+    CK(cudaEventRecord(ev1, s));
+    trace("baselines");
 
     // 7. results to host and CSR assembly (registry order = mpos order)
     std::vector<int64_t> b_gstart(NB + 1), b_slo(NB), b_shi(NB), b_w(NB), m_bstart(NM + 1), m_pos(NM), h_l_g(G);
@@ -1053,6 +1124,16 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
     CK(cudaMemcpyAsync(h_em.data(), mc.em, G * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(h_gmicro.data(), gr.micro, G * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(h_gpart.data(), gr.partial, G * 4, cudaMemcpyDeviceToHost, s));
+    std::vector<double> h_lth(NM * 4), h_lr2(NM), h_lmape(NM), h_snum(G);
+    std::vector<int32_t> h_ldeg(NM), h_nslot(NM);
+    std::vector<int64_t> h_sll(G);
+    CK(cudaMemcpyAsync(h_lth.data(), lin.coeff, NM * 32, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_lr2.data(), lin.r2, NM * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_lmape.data(), lin.mape, NM * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_ldeg.data(), lin.degen, NM * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_nslot.data(), d_nslot, NM * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_sll.data(), d_sll, G * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_snum.data(), d_snum, G * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ev0, ev1);
@@ -1093,7 +1174,17 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
             B->ext_micro.push_back(h_em[gs + q]);
         }
         B->ext_aoff.push_back(int32_t(B->ext_l.size()));
+        B->step_off.push_back(int32_t(B->step_l.size()));
+        for (int q = 0; q < h_nslot[mq]; ++q) {
+            B->step_l.push_back(h_sll[gs + q]);
+            B->step_t.push_back(h_snum[gs + q]);
+        }
+        for (int c = 0; c < 4; ++c) B->lin_theta.push_back(h_lth[4 * mq + c]);
+        B->lin_r2.push_back(h_lr2[mq]);
+        B->lin_mape.push_back(h_lmape[mq]);
+        B->lin_degen.push_back(h_ldeg[mq]);
     }
+    B->step_off.push_back(int32_t(B->step_l.size()));
     wt_build_result& R = *result;
     R.n_tables = int32_t(NM);
     R.W = W;
@@ -1118,6 +1209,13 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
     R.ext_l = B->ext_l.data();
     R.ext_micro = B->ext_micro.data();
     R.device_ms = ms;
+    R.step_off = B->step_off.data();
+    R.step_l = B->step_l.data();
+    R.step_t = B->step_t.data();
+    R.lin_theta = B->lin_theta.data();
+    R.lin_r2 = B->lin_r2.data();
+    R.lin_mape = B->lin_mape.data();
+    R.lin_degenerate = B->lin_degen.data();
     *out = B;
     return WT_OK;
 }
