@@ -75,6 +75,12 @@ def main():
     t0 = time.perf_counter()
     art = wt.build_tables(records, reg, hw, W=args.W)
     t_fit = time.perf_counter() - t0
+    # ablation baselines from the same records (tuner.cpp:191-220)
+    step_bp = wt.fit_step_baseline(records)
+    linear_bp = wt.fit_linear_baseline(records)
+    # eval.cpp:48-52: the default heuristic = smallest macro id, its smallest feasible micro
+    d_macro = min(m.id for m in reg.macros)
+    d_micro = min(reg.feasible_micros(d_macro))
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     wt.write_records(records, os.path.splitext(args.out)[0] + "_records.csv")
     wt.save_tables(art, os.path.splitext(args.out)[0] + "_tables.json")
@@ -97,7 +103,18 @@ def main():
             d = wt.tune(x, art, reg, hw)
             t_decide = (time.perf_counter() - q0) * 1e6
             pick = (d.macro_id, d.micro_id)
+            sd = wt.baseline_tune(x, step_bp, art, reg, hw)
+            ld = wt.baseline_tune(x, linear_bp, art, reg, hw)
+            methods = {
+                "wavetune": (pick, d.predicted_latency_us),
+                "step": ((sd.macro_id, sd.micro_id), sd.predicted_latency_us),
+                "linear": ((ld.macro_id, ld.micro_id), ld.predicted_latency_us),
+                "oracle": (best, None),
+                "default": ((d_macro, d_micro), None),
+            }
             rows.append({
+                "methods": {k: {"config": label(*c), "measured_us": t_all[c], "predicted_us": pr}
+                            for k, (c, pr) in methods.items()},
                 "layer": layer, "M": M, "N": N, "K": K,
                 "oracle": label(*best), "oracle_us": t_all[best],
                 "wavetune": label(*pick), "wavetune_us": t_all[pick], "predicted_us": d.predicted_latency_us,
@@ -110,6 +127,40 @@ def main():
                   f"{r['wavetune']:22s} {r['wavetune_us']:9.1f} us (pred {r['predicted_us']:9.1f}) | "
                   f"cuBLAS {r['cublas_us']:9.1f} us", flush=True)
 
+    # eval.cpp:106-116: geomean speedup over the default heuristic, MAPE of
+    # each method's predicted latency against the measured one
+    eval_report = {"geomean_speedup_vs_default": {}, "mape": {}}
+    for meth in rows[0]["methods"]:
+        eval_report["geomean_speedup_vs_default"][meth] = geomean(
+            [r["methods"]["default"]["measured_us"] / r["methods"][meth]["measured_us"] for r in rows])
+        pr = [r["methods"][meth] for r in rows if r["methods"][meth]["predicted_us"] is not None]
+        if pr:
+            eval_report["mape"][meth] = float(np.mean([abs(p["predicted_us"] - p["measured_us"]) / p["measured_us"]
+                                                       for p in pr]))
+    eval_report["default_config"] = label(d_macro, d_micro)
+    sub = [r for r in rows if 512 <= r["M"] <= 8192]
+    eval_report["geomean_speedup_vs_default_M512_8192"] = {
+        meth: geomean([r["methods"]["default"]["measured_us"] / r["methods"][meth]["measured_us"] for r in sub])
+        for meth in rows[0]["methods"]}
+    # decision overhead on this registry: Engine (one launch) and resident server
+    eng = wt.Engine(art, reg, hw)
+    xq = wt.DenseGemm(3000, 6144, 4096)
+
+    def p50_us(fn, n=3000):
+        for _ in range(100):
+            fn()
+        ts = []
+        for _ in range(n):
+            q0 = time.perf_counter_ns()
+            fn()
+            ts.append((time.perf_counter_ns() - q0) / 1e3)
+        return float(np.median(ts))
+
+    overhead = {"tune_cached_engine": p50_us(lambda: wt.tune(xq, art, reg, hw)),
+                "engine_tune_one": p50_us(lambda: eng.tune(xq))}
+    eng.set_resident(20000)
+    overhead["engine_tune_one_resident"] = p50_us(lambda: eng.tune(xq))
+    eng.set_resident(0)
     labels = list(rows[0]["all_us"])
     # the best single static config in hindsight (a strong default) and a
     # common hand-picked default
@@ -135,6 +186,8 @@ def main():
         "decide_us_host_median": float(np.median([r["decide_us_host"] for r in rows])),
         "prediction_mape": float(np.mean([abs(r["predicted_us"] - r["wavetune_us"]) / r["wavetune_us"]
                                           for r in rows])),
+        "eval": eval_report,
+        "decision_overhead_us_p50_python": overhead,
     }
     with open(args.out, "w") as f:
         json.dump({"summary": summary, "rows": rows}, f, indent=1)
