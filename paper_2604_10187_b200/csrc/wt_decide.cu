@@ -17,7 +17,9 @@
 // reference's C++ (SURVEY.md Appendix A).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "wt_decide.h"
 #include "wt_device.cuh"
@@ -504,8 +506,11 @@ __device__ __forceinline__ bool gather_one(const DevImage& im, const GatherArgs&
 
 // V = 4: four consecutive queries per thread with 16-byte loads/stores
 // (requires 16-byte aligned arrays); V = 1: scalar.
-template <int V>
-__global__ void __launch_bounds__(kGatherThreads) k_gather(DevImage im, GatherArgs a) {
+// PF: software pipelining -- the next grid-stride iteration's M/N/K vectors
+// are loaded before the current ones are looked up, so HBM reads overlap the
+// dependent L2 grid reads and the stores.
+template <int V, bool PF, int MINB>
+__global__ void __launch_bounds__(kGatherThreads, MINB) k_gather(DevImage im, GatherArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
     int32_t* pid = reinterpret_cast<int32_t*>(keys + a.n_pairs);
@@ -523,13 +528,32 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(DevImage im, GatherAr
     const int64_t n = a.n;
     const int64_t nv = n / V;  // full vectors
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    int4 pm = make_int4(0, 0, 0, 0), pn = pm, pk = pm;  // prefetched vectors (PF)
+    if constexpr (PF && V == 4) {
+        const int64_t v0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+        if (v0 < nv) {
+            pm = __ldcs(reinterpret_cast<const int4*>(a.M) + v0);
+            pn = __ldcs(reinterpret_cast<const int4*>(a.N) + v0);
+            pk = __ldcs(reinterpret_cast<const int4*>(a.K) + v0);
+        }
+    }
     for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < nv; base += stride) {
         const int64_t v = base + threadIdx.x;
         const bool live = v < nv;
         int32_t M[V], N[V], K[V];
         if constexpr (V == 4) {
             int4 m4 = make_int4(0, 0, 0, 0), n4 = m4, k4 = m4;
-            if (live) {
+            if constexpr (PF) {
+                m4 = pm;
+                n4 = pn;
+                k4 = pk;
+                const int64_t v2 = v + stride;
+                if (v2 < nv) {
+                    pm = __ldcs(reinterpret_cast<const int4*>(a.M) + v2);
+                    pn = __ldcs(reinterpret_cast<const int4*>(a.N) + v2);
+                    pk = __ldcs(reinterpret_cast<const int4*>(a.K) + v2);
+                }
+            } else if (live) {
                 m4 = __ldcs(reinterpret_cast<const int4*>(a.M) + v);
                 n4 = __ldcs(reinterpret_cast<const int4*>(a.N) + v);
                 k4 = __ldcs(reinterpret_cast<const int4*>(a.K) + v);
@@ -834,14 +858,40 @@ cudaError_t launch_grouped(const DevImage& im, const GroupedArgs& a, int grid, c
     return cudaGetLastError();
 }
 
+// Persistent grid: exactly the CTAs that are co-resident (a grid-stride loop
+// over a partly non-resident grid leaves a half-occupied second wave).
+// WT_GATHER_VARIANT (A/B runs): 0 = prefetch, 4 CTAs/SM; 1 = prefetch, 5
+// CTAs/SM (register cap); 2 = no prefetch, 5 CTAs/SM (cap); 3 = no prefetch,
+// no cap.
+template <int V, bool PF, int MINB>
+static cudaError_t go_gather(const DevImage& im, const GatherArgs& a, int grid, size_t smem, cudaStream_t st) {
+    static int occ = 0, sms = 0;
+    if (!occ) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather<V, PF, MINB>, kGatherThreads, 4096);
+        if (occ < 1) occ = 1;
+    }
+    grid = std::min(grid, sms * occ);
+    k_gather<V, PF, MINB><<<grid, kGatherThreads, smem, st>>>(im, a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gather(const DevImage& im, const GatherArgs& a, int grid, cudaStream_t st) {
     const size_t smem = size_t(a.n_pairs) * (sizeof(uint64_t) + sizeof(int32_t)) + 16;
     const auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
-    if (al16(a.M) && al16(a.N) && al16(a.K) && al16(a.out.macro) && al16(a.out.micro) && al16(a.out.lat))
-        k_gather<4><<<grid, kGatherThreads, smem, st>>>(im, a);
-    else
-        k_gather<1><<<grid, kGatherThreads, smem, st>>>(im, a);
-    return cudaGetLastError();
+    static const int variant = [] {
+        const char* v = std::getenv("WT_GATHER_VARIANT");
+        return v ? std::atoi(v) : 0;
+    }();
+    if (al16(a.M) && al16(a.N) && al16(a.K) && al16(a.out.macro) && al16(a.out.micro) && al16(a.out.lat)) {
+        if (variant == 1) return go_gather<4, true, 5>(im, a, grid, smem, st);
+        if (variant == 2) return go_gather<4, false, 5>(im, a, grid, smem, st);
+        if (variant == 3) return go_gather<4, false, 0>(im, a, grid, smem, st);
+        return go_gather<4, true, 0>(im, a, grid, smem, st);
+    }
+    return go_gather<1, false, 0>(im, a, grid, smem, st);
 }
 
 cudaError_t launch_predict(const DevImage& im, const PredictArgs& a, cudaStream_t st) {

@@ -34,7 +34,8 @@ eng = capi.Engine(S.synthetic_tables(cfg), S.registry_arrays(cfg), n_sm=148)
 pairs = S.LLAMA3_8B
 grid = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 8192)
 res["sweep1_ms"] = timeit(lambda: grid.sweep())
-for name, n, frac in (("eval_1M_ms", 1_000_000, 1.0), ("gather_100M_ms", 100_000_000, 0.01)):
+for name, n, frac in (("eval_1M_ms", 1_000_000, 1.0), ("gather_100M_ms", 100_000_000, 0.01),
+                      ("gather_ongrid_100M_ms", 100_000_000, 0.0)):
     M, N, K = (torch.from_numpy(x).cuda() for x in S.query_stream(n, pairs, seed=21, off_grid_frac=frac))
     o = [torch.empty(n, dtype=d, device="cuda") for d in (torch.int32, torch.int32, torch.float64)]
     d = capi.Engine.decisions(*o)
