@@ -166,34 +166,8 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
            o_amap = ar.take(C * R * 8), o_afb = ar.take(C * R * 4),
            o_al = ar.take(h.anchor_l.size() * 8), o_am = ar.take(h.anchor_micro.size() * 4);
     const size_t NS = h.seg_pos.size();
-    // cluster list mode: cut the class-ordered segments into <= 8 slices of
-    // at most kSliceBudget staged bytes (odd-stride rows + row metadata)
-    std::vector<int32_t> slices{0};
-    int32_t slice_smem = 0, slice_maxseg = 0;
-    {
-        const size_t kSliceBudget = 80 * 1024;
-        size_t cur = 0;
-        int32_t nseg_cur = 0;
-        for (size_t k = 0; k < NS; ++k) {
-            const size_t ncfg = size_t(h.seg_tiles[4 * k + 3]);
-            const size_t b = R * (2 * ncfg + 1) * 16 + R * ncfg * 4;
-            if (nseg_cur > 0 && cur + b > kSliceBudget) {
-                slices.push_back(int32_t(k));
-                slice_smem = std::max<int32_t>(slice_smem, int32_t(cur));
-                slice_maxseg = std::max(slice_maxseg, nseg_cur);
-                cur = 0;
-                nseg_cur = 0;
-            }
-            cur += b;
-            ++nseg_cur;
-        }
-        slices.push_back(int32_t(NS));
-        slice_smem = std::max<int32_t>(slice_smem, int32_t(cur));
-        slice_maxseg = std::max(slice_maxseg, nseg_cur);
-        if (slices.size() - 1 > 8 || size_t(slice_smem) > kSliceBudget) slices.assign(1, 0);
-    }
     size_t o_st = ar.take(NS * 16), o_sm = ar.take(NS * 16), o_sp = ar.take(NS * 4), o_cc = ar.take(C * 4),
-           o_th2 = ar.take(C * R * 32), o_m2 = ar.take(C * R * 4), o_sl = ar.take(slices.size() * 4);
+           o_th2 = ar.take(C * R * 32), o_m2 = ar.take(C * R * 4);
     cudaError_t ce = cudaMalloc(&e->mem, ar.used);
     if (ce != cudaSuccess) {
         delete e;
@@ -215,7 +189,6 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
         {o_st, h.seg_tiles.data(), NS * 16},      {o_sm, h.seg_magic.data(), NS * 16},
         {o_sp, h.seg_pos.data(), NS * 4},         {o_cc, h.cls_cfg.data(), C * 4},
         {o_th2, h.theta2.data(), C * R * 32},     {o_m2, h.meta2.data(), C * R * 4},
-        {o_sl, slices.data(), slices.size() * 4},
     };
     for (const Piece& p : pieces) {
         ce = cudaMemcpy(base + p.off, p.src, p.n, cudaMemcpyHostToDevice);
@@ -254,10 +227,6 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
     d.cls_cfg = reinterpret_cast<const int32_t*>(base + o_cc);
     d.theta2 = reinterpret_cast<const double4*>(base + o_th2);
     d.meta2 = reinterpret_cast<const uint32_t*>(base + o_m2);
-    d.nslice = int32_t(slices.size()) - 1;
-    d.slice_smem = slice_smem;
-    d.slice_maxseg = slice_maxseg;
-    d.slice_seg = reinterpret_cast<const int32_t*>(base + o_sl);
     // list-mode chunk: keep the staged rows near 40 KB so several CTAs fit per SM
     e->eval_chunk = int(std::max<size_t>(1, std::min<size_t>(C, 40960 / (R * 36 + 32))));
     e->eval_grid = sm_count(device) * 4;

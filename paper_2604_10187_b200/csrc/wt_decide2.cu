@@ -24,7 +24,6 @@
 // the dependent DMUL/DADD chains of different shapes interleave.
 #include <cuda_runtime.h>
 
-#include <cooperative_groups.h>
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 #include <algorithm>
@@ -573,193 +572,6 @@ __global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_
 }
 
 
-// ------------------------------------------------ eval (list), cluster mode
-// The image's class-ordered segments are cut into nslice slices at engine
-// creation (<= 8, each <= 80 KB staged).  One thread-block cluster = nslice
-// CTAs; each CTA stages ITS slice into shared memory once and keeps it for
-// the whole launch.  Every tile of 1024 queries is sorted identically by all
-// CTAs of the cluster (deterministic block radix sort), evaluated by each
-// CTA against its slice, and the partial (latency, config, row metadata) per
-// query is left in that CTA's shared memory.  After a cluster barrier each
-// CTA merges 1/nslice of the tile by reading the other CTAs' partials over
-// distributed shared memory, in ascending rank order with the lexicographic
-// (latency, config index) rule, and runs Stage II.  Compared to k_eval2 the
-// image is staged once per CTA instead of once per tile.
-template <int RPT, bool SPECIAL>
-__global__ void __launch_bounds__(kT2) k_evalc(DevImage im, EvalArgs a) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cluster = cg::this_cluster();
-    const int S = int(cluster.num_blocks());
-    const int rank = int(cluster.block_rank());
-    constexpr int kTile = kT2 * RPT;
-    extern __shared__ __align__(16) unsigned char smem[];
-    SegHdr* hdr = reinterpret_cast<SegHdr*>(smem);
-    double* plat = reinterpret_cast<double*>(hdr + im.slice_maxseg);
-    int32_t* pcfg = reinterpret_cast<int32_t*>(plat + kTile);
-    uint32_t* pacc = reinterpret_cast<uint32_t*>(pcfg + kTile);
-    double2* slots = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(pacc + kTile) + 15) & ~uintptr_t(15));
-    using Sort = cub::BlockRadixSort<uint32_t, kT2, RPT, int32_t>;
-    __shared__ typename Sort::TempStorage sort_tmp;
-    __shared__ int total_slots;
-
-    const int tid = threadIdx.x;
-    const int R = im.R;
-    const int s0 = im.slice_seg[rank], ns = im.slice_seg[rank + 1] - s0;
-    if (tid == 0) {  // headers: slot offsets (16-byte units) and meta offsets (in `rowlo`)
-        int off = 0, moff = 0;
-        for (int k = 0; k < ns; ++k) {
-            const int4 st = __ldg(im.seg_tiles + s0 + k);
-            const uint4 mg = __ldg(im.seg_magic + s0 + k);
-            SegHdr h;
-            h.mM = mg.x;
-            h.mN = mg.y;
-            h.mK = mg.z;
-            h.sM = mg.w;
-            h.ncfg = st.w;
-            h.pos = __ldg(im.seg_pos + s0 + k);
-            h.off = off;
-            h.stride = 2 * st.w + 1;  // odd
-            h.rowlo = uint32_t(moff);
-            hdr[k] = h;
-            off += R * h.stride;
-            moff += R * st.w;
-        }
-        total_slots = off;
-    }
-    __syncthreads();
-    uint32_t* meta = reinterpret_cast<uint32_t*>(slots + total_slots);
-    for (int k = 0; k < ns; ++k) {
-        const SegHdr h = hdr[k];
-        const int n2 = R * h.ncfg;
-        for (int i = tid; i < n2; i += kT2) {
-            const int r = i / h.ncfg, c = i - r * h.ncfg;
-            const size_t src = size_t(h.pos + c) * R + r;
-            const double4 th = ldg_row(im.theta2 + src);
-            const int d = h.off + r * h.stride + 2 * c;
-            slots[d] = make_double2(th.x, th.y);
-            slots[d + 1] = make_double2(th.z, th.w);
-            if constexpr (SPECIAL) meta[h.rowlo + r * h.ncfg + c] = __ldg(im.meta2 + src);
-        }
-    }
-    __syncthreads();
-
-    const int64_t n = a.count ? *a.count : a.n;
-    const int64_t ntiles = (n + kTile - 1) / kTile;
-    const int64_t cid = blockIdx.x / S, ncl = gridDim.x / S;
-    const int chunk = (kTile + S - 1) / S;
-    for (int64_t tl = cid; tl < ntiles; tl += ncl) {
-        int32_t perm[RPT];
-        {
-            uint32_t key[RPT];
-#pragma unroll
-            for (int j = 0; j < RPT; ++j) {
-                const int64_t slot = tl * kTile + int64_t(tid) * RPT + j;
-                uint32_t k = 0xffffffffu;
-                if (slot < n) {
-                    const int64_t qq = (a.idx && !a.inputs_compact) ? a.idx[slot] : slot;
-                    const int32_t m = a.M[qq], nn = a.N[qq];
-                    if (m >= 1 && nn >= 1) k = __float_as_uint(__fmul_rn(float(m), float(nn)));
-                }
-                key[j] = k;
-                perm[j] = tid * RPT + j;
-            }
-            __syncthreads();  // sort_tmp is reused across tiles
-            Sort(sort_tmp).SortBlockedToStriped(key, perm, 14, 32);
-        }
-        uint32_t y2M[RPT], y2N[RPT], y2K[RPT], acc[RPT];
-        double best[RPT];
-        int bc[RPT];
-#pragma unroll
-        for (int j = 0; j < RPT; ++j) {
-            const int64_t slot = tl * kTile + perm[j];
-            uint32_t M = 1, N = 1, K = 1;
-            if (slot < n) {
-                const int64_t src = a.inputs_compact ? slot : (a.idx ? a.idx[slot] : slot);
-                const int32_t m = a.M[src], nn = a.N[src], k = a.K[src];
-                if (m >= 1 && nn >= 1 && k >= 1) {
-                    M = uint32_t(m);
-                    N = uint32_t(nn);
-                    K = uint32_t(k);
-                }
-            }
-            y2M[j] = 2u * (M - 1u);
-            y2N[j] = 2u * (N - 1u);
-            y2K[j] = 2u * (K - 1u);
-            best[j] = kInf;
-            bc[j] = -1;
-            acc[j] = 0;
-        }
-        ClassCache cc;
-        int rowc[RPT];
-        double gd[RPT], ld[RPT];
-#pragma unroll
-        for (int j = 0; j < RPT; ++j) {
-            rowc[j] = 0;
-            gd[j] = ld[j] = 0.0;
-        }
-        for (int k = 0; k < ns; ++k) {
-            const SegHdr h = hdr[k];
-            eval_seg<RPT, SPECIAL>(im, h, slots + h.off, meta + h.rowlo, y2M, y2N, y2K, cc, rowc, gd, ld, best, bc,
-                                   acc);
-        }
-#pragma unroll
-        for (int j = 0; j < RPT; ++j) {
-            plat[perm[j]] = best[j];
-            pcfg[perm[j]] = bc[j];
-            pacc[perm[j]] = acc[j];
-        }
-        cluster.sync();
-        // merge this CTA's share of the tile across the cluster's slices
-        const int p_end = min(kTile, (rank + 1) * chunk);
-        for (int p = rank * chunk + tid; p < p_end; p += kT2) {
-            const int64_t slot = tl * kTile + p;
-            if (slot >= n) continue;
-            const int64_t qi = a.idx ? a.idx[slot] : slot;
-            const int64_t src = a.inputs_compact ? slot : qi;
-            const int32_t m = a.M[src], nn = a.N[src], k = a.K[src];
-            uint32_t stv = 0;
-            if (m < 1 || nn < 1 || k < 1) {
-                stv = WT_INVALID_ARGUMENT;  // kernel_map.cpp:238-239
-            } else {
-                const uint64_t gmax = uint64_t((uint32_t(m) + uint32_t(im.tm_min) - 1) / uint32_t(im.tm_min)) *
-                                      uint64_t((uint32_t(nn) + uint32_t(im.tn_min) - 1) / uint32_t(im.tn_min));
-                if ((gmax + uint64_t(im.S) - 1) / uint64_t(im.S) >= (uint64_t(1) << 31)) stv = WT_UNSUPPORTED;
-            }
-            double b = kInf;
-            int c = -1;
-            uint32_t ac = 0;
-            for (int r = 0; r < S; ++r) {
-                const double rb = cluster.map_shared_rank(plat, r)[p];
-                const int rc = cluster.map_shared_rank(pcfg, r)[p];
-                if constexpr (SPECIAL) ac |= cluster.map_shared_rank(pacc, r)[p];
-                if (rc >= 0 && lex_less(rb, rc, b, c < 0 ? INT32_MAX : c)) {
-                    b = rb;
-                    c = rc;
-                }
-            }
-            Final f;
-            uint64_t g = 0;
-            int64_t l = 0;
-            if (stv) {
-                f.flags = stv << 24;
-                f.macro = f.micro = f.wave = -1;
-                f.comps = 0;
-                f.tail = 0.f;
-            } else {
-                if (c >= 0) {
-                    const int4 tl4 = __ldg(im.tiles + c);
-                    g = uint64_t((uint32_t(m) + uint32_t(tl4.x) - 1) / uint32_t(tl4.x)) *
-                        uint64_t((uint32_t(nn) + uint32_t(tl4.y) - 1) / uint32_t(tl4.y));
-                    l = int64_t((uint32_t(k) + uint32_t(tl4.z) - 1) / uint32_t(tl4.z));
-                }
-                f = finish(im, c, 0.0, g, l, ac);
-            }
-            write_decision(a.out, qi, f, b, g, l);
-        }
-        cluster.sync();  // the partials are rewritten by the next tile
-    }
-}
-
 // ---------------------------------------------------------------- launchers
 // Launch shape: shapes (queries) per thread and dynamic shared memory per CTA.
 // Defaults are the measured best on B200; WT_SWEEP_RPT / WT_EVAL_RPT (2|4)
@@ -876,52 +688,7 @@ static cudaError_t go_eval2(const DevImage& im, const EvalArgs& a, int grid, cud
     return cudaGetLastError();
 }
 
-template <int RPT, bool SP>
-static cudaError_t go_evalc(const DevImage& im, const EvalArgs& a, cudaStream_t st) {
-    const int S = im.nslice;
-    const size_t smem = size_t(im.slice_maxseg) * sizeof(SegHdr) + size_t(kT2) * RPT * 16 + size_t(im.slice_smem) + 64;
-    auto fn = k_evalc<RPT, SP>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    if (S > 8) {
-        e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-    }
-    cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = unsigned(S);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(kT2);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    // as many clusters as can be co-resident
-    static int max_clusters[2][9] = {};
-    int& mc = max_clusters[SP ? 1 : 0][S];
-    if (!mc) {
-        cfg.gridDim = dim3(unsigned(S * n_sms()));
-        if (cudaOccupancyMaxActiveClusters(&mc, fn, &cfg) != cudaSuccess || mc < 1) mc = std::max(1, n_sms() / S);
-    }
-    cfg.gridDim = dim3(unsigned(S * mc));
-    e = cudaLaunchKernelEx(&cfg, fn, im, a);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
-}
-
-static bool use_cluster_eval(const DevImage& im) {
-    static const int mode = [] {
-        const char* v = std::getenv("WT_EVAL_CLUSTER");
-        return v ? std::atoi(v) : 1;
-    }();
-    return mode != 0 && im.nslice >= 1 && im.nslice <= 8;
-}
-
 cudaError_t launch_eval2(const DevImage& im, const EvalArgs& a, int grid, cudaStream_t st) {
-    if (use_cluster_eval(im))
-        return im.special ? go_evalc<4, true>(im, a, st) : go_evalc<4, false>(im, a, st);
     // persistent grid: as many CTAs as fit at this shared-memory size
     const size_t smem = smem_for(tuning().eval_kb, im, true);
     const int per_sm = std::max(1, int((228 * 1024) / (smem + 12 * 1024)));

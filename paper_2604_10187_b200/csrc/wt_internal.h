@@ -68,12 +68,6 @@ struct DevImage {
     const int32_t* cls_cfg;   // [C] class-ordered position -> config index
     const double4* theta2;    // [C*R] rows in class order
     const uint32_t* meta2;    // [C*R] rowmeta in class order
-    // Cluster list mode (k_evalc): segments cut into nslice consecutive
-    // slices, each staged once into one CTA of a thread-block cluster.
-    int32_t nslice;           // 0 = image too large for a cluster
-    int32_t slice_smem;       // bytes of the largest staged slice (slots + meta)
-    int32_t slice_maxseg;     // most segments in one slice
-    const int32_t* slice_seg; // [nslice+1] first segment of each slice
 };
 
 constexpr int kSegCfg = 32;
