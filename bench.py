@@ -43,6 +43,20 @@ def load_peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
+def gather_traffic(n_decisions):
+    """DRAM bytes per k_gather launch from the committed ncu --set full capture
+    (dram__bytes_read.sum + dram__bytes_write.sum per decision, scaled to this
+    launch's decisions); None when no capture is committed."""
+    import glob
+
+    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic_gather.json")))
+    if not caps:
+        return None, None
+    with open(caps[-1]) as f:
+        d = json.load(f)
+    return d["dram_bytes_per_decision"] * n_decisions, os.path.relpath(caps[-1], ROOT)
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -279,6 +293,7 @@ def run_wavetune(args):
     gather_ms = ev2[0].elapsed_time(ev2[1]) / reps
     alg_bytes = 28.0 * n_on  # 12 B (M,N,K) read + 16 B (macro, micro, latency) written per decision
     achieved = alg_bytes / (gather_ms * 1e-3) / 1e9
+    traffic, traffic_src = gather_traffic(n_on)
 
     # e2e through the public API with host buffers (pinned), copies inside
     Mp, Np, Kp = (torch.from_numpy(x).pin_memory() for x in (Mh, Nh, Kh))
@@ -377,7 +392,7 @@ def run_wavetune(args):
                     "d2h_bytes_per_step": 16 * n},
             "roofline": {"kernel": "k_gather", "bound": "hbm", "achieved": achieved,
                          "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                         "traffic": None, "peak_kind": peaks_kind,
+                         "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peaks_kind,
                          "alg_bytes_per_launch": alg_bytes, "launch_ms": gather_ms,
                          "share_of_step": gather_ms / t_ms},
             "gpu_launches": launches,
