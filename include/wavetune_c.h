@@ -282,11 +282,18 @@ typedef struct {
 
 wt_status wt_grid_create(const wt_engine* e, const wt_grid_desc* desc, wt_grid** out);
 wt_status wt_grid_destroy(wt_grid* g);
-/* Raw device storage (for collectives / inspection). */
+/* Raw device storage (for collectives / inspection).  After writing entries
+ * through it (e.g. an all-gather of sweep shards) call wt_grid_finalize. */
 wt_status wt_grid_storage(const wt_grid* g, wt_grid_entry** entries, int64_t* n_entries,
                           int32_t** topk_macro, double** topk_latency);
-/* Fills entries [begin, end) (flattened index) -- one shard of the sweep. */
+/* Fills entries [begin, end) (flattened index) -- one shard of the sweep.
+ * A full-range sweep also rebuilds the grid's run index (below); a partial
+ * one invalidates it until wt_grid_finalize. */
 wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, void* stream);
+/* Rebuilds the run-compressed copy of the entries' heads (latency, macro,
+ * micro are piecewise constant along M) that wt_gather_batch serves from
+ * shared memory when it fits.  Stream-ordered, no host sync. */
+wt_status wt_grid_finalize(const wt_engine* e, wt_grid* g, void* stream);
 /* Online queries: on-grid shapes are gathered; off-grid ones are compacted
  * and evaluated in full (wt_tune_batch semantics).  Needs no host sync. */
 wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M, const int32_t* N,

@@ -93,7 +93,7 @@ class wt_build_result(C.Structure):
 EXPORTS = (
     "wt_last_error wt_version wt_abi_version wt_engine_create wt_engine_destroy wt_engine_info_get "
     "wt_engine_config_index wt_tune_batch wt_tune_grouped_batch wt_predict_batch wt_explain "
-    "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_destroy wt_grid_storage wt_sweep "
+    "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_destroy wt_grid_storage wt_sweep wt_grid_finalize "
     "wt_gather_batch wt_decide_host_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
     "wt_simulate_batch wt_profile_sim wt_tune_one wt_engine_set_resident wt_baseline_create "
     "wt_baseline_destroy wt_baseline_tune_batch wt_baseline_predict_batch").split()
@@ -320,6 +320,11 @@ class Grid:
         end = self.n_entries if end is None else end
         check(lib().wt_sweep(self.engine.handle, self.handle, C.c_int64(begin), C.c_int64(end),
                              vp(_stream_ptr(stream))))
+
+    def finalize(self, stream=None):
+        """Rebuild the run index after entries were written directly (e.g. the
+        all-gather of a sharded sweep); a full sweep() does it itself."""
+        check(lib().wt_grid_finalize(self.engine.handle, self.handle, vp(_stream_ptr(stream))))
 
     def gather(self, M, N, K, out: wt_decisions, stream=None):
         check(lib().wt_gather_batch(self.engine.handle, self.handle, vp(_ptr(M)), vp(_ptr(N)), vp(_ptr(K)),

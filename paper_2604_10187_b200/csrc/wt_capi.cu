@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <map>
@@ -136,6 +137,9 @@ struct wt_grid {
     int32_t* tk_macro = nullptr;
     double* tk_lat = nullptr;
     int32_t n_keys = 0;
+    int4* dhash = nullptr;  // (N, K) -> pair open-addressing table (k_gather_h)
+    int32_t hbits = 0;
+    RunIndex runs{};        // run-compressed heads (k_gather_h); budget 0 = none
 };
 
 extern "C" {
@@ -708,6 +712,35 @@ wt_status wt_grid_create(const wt_engine* e, const wt_grid_desc* desc, wt_grid**
                  o_ent = ar.take(size_t(g->n_entries) * sizeof(wt_grid_entry)),
                  o_tkm = ar.take(size_t(g->n_entries) * g->topk * 4),
                  o_tkl = ar.take(size_t(g->n_entries) * g->topk * 8);
+    // hash table: load factor <= 1/2, linear probing, inserted in key order
+    // (deterministic); only for tables that fit shared memory comfortably
+    std::vector<int4> htab;
+    if (keys.size() <= 2048) {
+        int bits = 3;
+        while ((size_t(1) << bits) < 2 * keys.size()) ++bits;
+        htab.assign(size_t(1) << bits, make_int4(0, 0, -1, 0));
+        for (auto& k : keys) {
+            const uint32_t N = uint32_t(k.first >> 32), K = uint32_t(k.first);
+            uint32_t h = pair_slot(N, K, bits);
+            while (htab[h].z >= 0) h = (h + 1) & ((1u << bits) - 1u);
+            htab[h] = make_int4(int(N), int(K), k.second, 0);
+        }
+        g->hbits = bits;
+    }
+    const size_t o_hash = ar.take(htab.size() * sizeof(int4));
+    // run index storage (worst case: every entry its own run) when its block
+    // table alone leaves room in the shared-memory budget
+    static const int runs_kb = [] {
+        const char* v = std::getenv("WT_GATHER_RUNS_KB");
+        return v ? std::atoi(v) : 40;
+    }();
+    const int64_t nblk = (g->mcount + (1 << kRunBlkShift) - 1) >> kRunBlkShift;
+    const bool want_runs = !htab.empty() && runs_kb > 0 && g->n_entries < int64_t(0xfffffff0u) &&
+                           int64_t(g->n_pairs) * nblk * 16 <= int64_t(runs_kb) * 1024;
+    const size_t o_rhdr = ar.take(want_runs ? 16 : 0),
+                 o_rbidx = ar.take(want_runs ? size_t(g->n_pairs) * nblk * 16 : 0),
+                 o_rkey = ar.take(want_runs ? size_t(g->n_entries + 1) * 4 : 0),
+                 o_rval = ar.take(want_runs ? size_t(g->n_entries) * 16 : 0);
     cudaError_t ce = cudaMalloc(&g->mem, ar.used);
     if (ce != cudaSuccess) {
         delete g;
@@ -721,6 +754,18 @@ wt_status wt_grid_create(const wt_engine* e, const wt_grid_desc* desc, wt_grid**
     g->entries = reinterpret_cast<wt_grid_entry*>(base + o_ent);
     g->tk_macro = g->topk ? reinterpret_cast<int32_t*>(base + o_tkm) : nullptr;
     g->tk_lat = g->topk ? reinterpret_cast<double*>(base + o_tkl) : nullptr;
+    g->dhash = htab.empty() ? nullptr : reinterpret_cast<int4*>(base + o_hash);
+    if (g->dhash) cudaMemcpy(g->dhash, htab.data(), htab.size() * sizeof(int4), cudaMemcpyHostToDevice);
+    if (want_runs) {
+        g->runs.hdr = reinterpret_cast<int32_t*>(base + o_rhdr);
+        g->runs.bhead = reinterpret_cast<int4*>(base + o_rbidx);
+        g->runs.rkey = reinterpret_cast<uint32_t*>(base + o_rkey);
+        g->runs.rval = reinterpret_cast<int4*>(base + o_rval);
+        g->runs.nblk = int32_t(nblk);
+        g->runs.nbtot = int32_t(int64_t(g->n_pairs) * nblk);
+        g->runs.budget = runs_kb * 1024;
+        cudaMemset(g->runs.hdr, 0, 16);
+    }
     std::vector<uint64_t> kk;
     std::vector<int32_t> pid;
     for (auto& k : keys) {
@@ -796,6 +841,29 @@ wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, v
     }
     g_launches++;
     if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep");
+    // the run index follows the entries: rebuilt after a full sweep,
+    // invalidated by a partial one (wt_grid_finalize rebuilds it)
+    if (g->runs.budget > 0) {
+        if (begin == 0 && end == g->n_entries) return wt_grid_finalize(e, g, stream);
+        ce = cudaMemsetAsync(g->runs.hdr, 0, 4, s);
+        if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep: run index");
+    }
+    return WT_OK;
+}
+
+wt_status wt_grid_finalize(const wt_engine* e, wt_grid* g, void* stream) {
+    if (!e || !g) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    if (g->eng != e) return set_err(WT_INVALID_ARGUMENT, "grid was created for another engine");
+    if (g->runs.budget <= 0) return WT_OK;
+    DeviceGuard guard(e->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    void* temp = nullptr;
+    cudaError_t ce = cudaMallocFromPoolAsync(&temp, runs_temp_bytes(g->n_entries), lib_pool(e->device), s);
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_grid_finalize: scratch");
+    ce = launch_runs_build(g->entries, g->n_entries, g->mcount, g->runs, temp, s);
+    cudaFreeAsync(temp, s);
+    g_launches += 5;
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_grid_finalize");
     return WT_OK;
 }
 
@@ -841,6 +909,9 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
     a.off_M = offM;
     a.off_N = offN;
     a.off_K = offK;
+    a.htab = g->dhash;
+    a.hbits = g->hbits;
+    a.runs = g->runs;
     const int grid = int(std::min<int64_t>((n + kGatherThreads - 1) / kGatherThreads,
                                            int64_t(sm_count(e->device)) * 8));
     ce = launch_gather(e->dev, a, grid, s);

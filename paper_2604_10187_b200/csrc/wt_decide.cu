@@ -17,6 +17,8 @@
 // reference's C++ (SURVEY.md Appendix A).
 #include <cuda_runtime.h>
 
+#include <cub/device/device_scan.cuh>
+
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
@@ -616,6 +618,281 @@ __global__ void __launch_bounds__(kGatherThreads, MINB) k_gather(DevImage im, Ga
     wbuf_flush(slice, wcnt, a, lane);
 }
 
+// Hashed gather: the common call (macro / micro / latency outputs only,
+// 16-byte aligned arrays, pair table hashed at grid creation).  Per query one
+// LDS.128 probe of the open-addressing (N, K) table (linear probing, load
+// factor <= 1/2: almost always the only probe), an unsigned range check on M,
+// then the 16-byte head of the grid entry: from the run-compressed copy in
+// shared memory when it fits (RUNS; the scattered 16-byte L2 reads otherwise
+// cost one L1 wavefront per lane and bound the kernel), else from L2.
+// Off-grid queries take the same per-warp compaction as k_gather, but only
+// in warps that hold one.
+struct RunSmem {
+    const int4* head;
+    const int4* val;
+    const uint32_t* key;
+};
+
+template <bool RUNS>
+__device__ __forceinline__ bool hlookup(const int4* tab, uint32_t hmask, int bits, const GatherArgs& a,
+                                        const RunSmem& rs, uint32_t mlo, uint32_t mcnt, int32_t M, int32_t N,
+                                        int32_t K, int4* out) {
+    uint32_t h = pair_slot(uint32_t(N), uint32_t(K), bits);
+    int4 e = tab[h];
+    while (e.z >= 0 && (e.x != N || e.y != K)) {
+        h = (h + 1u) & hmask;
+        e = tab[h];
+    }
+    const uint32_t dm = uint32_t(M) - mlo;
+    const bool hit = e.z >= 0 && dm < mcnt;
+    *out = make_int4(0, 0, -1, -1);
+    if (hit) {
+        if constexpr (RUNS) {
+            int4 hd = rs.head[uint32_t(e.z) * uint32_t(a.runs.nblk) + (dm >> kRunBlkShift)];
+            if (hd.z == INT32_MIN) {  // block with several runs
+                const uint32_t flat = uint32_t(e.z) * mcnt + dm;
+                uint32_t r = uint32_t(hd.x);
+                while (rs.key[r + 1] <= flat) ++r;
+                hd = rs.val[r];
+            }
+            *out = hd;
+        } else {
+            *out = __ldg(reinterpret_cast<const int4*>(a.entries + (int64_t(e.z) * mcnt + dm)));
+        }
+    }
+    return hit;
+}
+
+template <bool RUNS>
+__device__ __forceinline__ void gather_h_loop(const GatherArgs& a, const int4* tab, const RunSmem& rs,
+                                              WarpBuf& slice) {
+    const int bits = a.hbits;
+    const uint32_t hmask = (1u << bits) - 1u;
+    const uint32_t mlo = uint32_t(a.m_lo), mcnt = uint32_t(a.mcount);
+    const int lane = threadIdx.x & 31;
+    int wcnt = 0;
+    const int64_t n = a.n, nv = n / 4;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    const int4* M4 = reinterpret_cast<const int4*>(a.M);
+    const int4* N4 = reinterpret_cast<const int4*>(a.N);
+    const int4* K4 = reinterpret_cast<const int4*>(a.K);
+    int4 pm = make_int4(0, 0, 0, 0), pn = pm, pk = pm;
+    {
+        const int64_t v0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+        if (v0 < nv) {
+            pm = __ldcs(M4 + v0);
+            pn = __ldcs(N4 + v0);
+            pk = __ldcs(K4 + v0);
+        }
+    }
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < nv; base += stride) {
+        const int64_t v = base + threadIdx.x;
+        const bool live = v < nv;
+        const int32_t M[4] = {pm.x, pm.y, pm.z, pm.w}, N[4] = {pn.x, pn.y, pn.z, pn.w},
+                      K[4] = {pk.x, pk.y, pk.z, pk.w};
+        if (v + stride < nv) {
+            pm = __ldcs(M4 + v + stride);
+            pn = __ldcs(N4 + v + stride);
+            pk = __ldcs(K4 + v + stride);
+        }
+        // phase 1: the four first probes, issued back to back
+        uint32_t h[4];
+        int4 e[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            h[j] = pair_slot(uint32_t(N[j]), uint32_t(K[j]), bits);
+            e[j] = tab[h[j]];
+        }
+        // rare: collision chains
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            while (e[j].z >= 0 && (e[j].x != N[j] || e[j].y != K[j])) {
+                h[j] = (h[j] + 1u) & hmask;
+                e[j] = tab[h[j]];
+            }
+        }
+        // phase 2: the four heads, issued back to back
+        int4 r[4];
+        uint32_t offm = 0;
+        uint32_t dm[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            dm[j] = uint32_t(M[j]) - mlo;
+            const bool hit = e[j].z >= 0 && dm[j] < mcnt;
+            offm |= hit ? 0u : (1u << j);
+            r[j] = make_int4(0, 0, -1, -1);
+            if constexpr (RUNS) {
+                if (hit) r[j] = rs.head[uint32_t(e[j].z) * uint32_t(a.runs.nblk) + (dm[j] >> kRunBlkShift)];
+            } else {
+                if (hit) r[j] = __ldg(reinterpret_cast<const int4*>(a.entries + (int64_t(e[j].z) * mcnt + dm[j])));
+            }
+        }
+        if constexpr (RUNS) {  // rare: blocks holding several runs
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (r[j].z == INT32_MIN && !((offm >> j) & 1u)) {
+                    const uint32_t flat = uint32_t(e[j].z) * mcnt + dm[j];
+                    uint32_t q = uint32_t(r[j].x);
+                    while (rs.key[q + 1] <= flat) ++q;
+                    r[j] = rs.val[q];
+                }
+            }
+        }
+        if (live) {
+            // off-grid lanes are overwritten later by the evaluation kernel
+            __stcs(reinterpret_cast<int4*>(a.out.macro) + v, make_int4(r[0].z, r[1].z, r[2].z, r[3].z));
+            __stcs(reinterpret_cast<int4*>(a.out.micro) + v, make_int4(r[0].w, r[1].w, r[2].w, r[3].w));
+            __stcs(reinterpret_cast<double2*>(a.out.lat) + 2 * v,
+                   make_double2(__hiloint2double(r[0].y, r[0].x), __hiloint2double(r[1].y, r[1].x)));
+            __stcs(reinterpret_cast<double2*>(a.out.lat) + 2 * v + 1,
+                   make_double2(__hiloint2double(r[2].y, r[2].x), __hiloint2double(r[3].y, r[3].x)));
+        } else {
+            offm = 0;
+        }
+        if (__any_sync(0xffffffffu, offm != 0)) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) wbuf_push((offm >> j) & 1u, v * 4 + j, M[j], N[j], K[j], slice, wcnt, a, lane);
+        }
+    }
+    // scalar tail (n % 4 queries), first warp of block 0
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        const int64_t q = nv * 4 + threadIdx.x;
+        const bool live = q < n;
+        bool on = false;
+        int32_t tM = 0, tN = 0, tK = 0;
+        if (live) {
+            tM = a.M[q];
+            tN = a.N[q];
+            tK = a.K[q];
+            int4 lo4;
+            on = hlookup<RUNS>(tab, hmask, bits, a, rs, mlo, mcnt, tM, tN, tK, &lo4);
+            if (on) {
+                a.out.macro[q] = lo4.z;
+                a.out.micro[q] = lo4.w;
+                a.out.lat[q] = __hiloint2double(lo4.y, lo4.x);
+            }
+        }
+        wbuf_push(live && !on, q, tM, tN, tK, slice, wcnt, a, lane);
+    }
+    wbuf_flush(slice, wcnt, a, lane);
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kGatherThreads, MINB) k_gather_h(GatherArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    int4* tab = reinterpret_cast<int4*>(smem);
+    __shared__ WarpBuf wbuf[kGatherThreads / 32];
+    const int H = 1 << a.hbits;
+    for (int i = threadIdx.x; i < H; i += blockDim.x) tab[i] = a.htab[i];
+    // run index: usable when built and within the reserved shared memory
+    const RunIndex& ri = a.runs;
+    int nr = 0;
+    bool runs = false, multi = false;
+    if (ri.budget > 0) {
+        const int4 hd = *reinterpret_cast<const int4*>(ri.hdr);
+        nr = hd.y;
+        multi = hd.z != 0;
+        const int64_t need = int64_t(ri.nbtot) * 16 + (multi ? int64_t(nr) * 20 + 4 : 0);
+        runs = hd.x != 0 && need <= ri.budget;
+    }
+    RunSmem rs{};
+    if (runs) {
+        int4* head = tab + H;
+        int4* val = head + ri.nbtot;
+        uint32_t* key = reinterpret_cast<uint32_t*>(val + (multi ? nr : 0));
+        for (int i = threadIdx.x; i < ri.nbtot; i += blockDim.x) head[i] = ri.bhead[i];
+        if (multi) {
+            for (int i = threadIdx.x; i < nr; i += blockDim.x) val[i] = ri.rval[i];
+            for (int i = threadIdx.x; i <= nr; i += blockDim.x) key[i] = ri.rkey[i];
+        }
+        rs = RunSmem{head, val, key};
+    }
+    __syncthreads();
+    WarpBuf& slice = wbuf[threadIdx.x >> 5];
+    if (runs)
+        gather_h_loop<true>(a, tab, rs, slice);
+    else
+        gather_h_loop<false>(a, tab, rs, slice);
+}
+
+// ---- run index build (after a full sweep / wt_grid_finalize)
+__device__ __forceinline__ int4 head_of(const wt_grid_entry* e, int64_t i) {
+    return __ldg(reinterpret_cast<const int4*>(e + i));
+}
+
+__global__ void k_runflags(const wt_grid_entry* ent, int64_t n, int64_t mcount, uint32_t* flags, int32_t* hdr) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int4 a = head_of(ent, i);
+    uint32_t f = 1;
+    if (i % mcount != 0) {
+        const int4 b = head_of(ent, i - 1);
+        f = (a.x != b.x || a.y != b.y || a.z != b.z || a.w != b.w) ? 1u : 0u;
+    }
+    flags[i] = f;
+    if (a.z == INT32_MIN) atomicOr(hdr + 3, 1);  // the block marker would be ambiguous
+}
+
+__global__ void k_runscatter(const wt_grid_entry* ent, int64_t n, const uint32_t* flags, const uint32_t* ids,
+                             RunIndex ri) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t f = flags[i], id = ids[i];
+    if (f) {
+        ri.rkey[id] = uint32_t(i);
+        ri.rval[id] = head_of(ent, i);
+    }
+    if (i == n - 1) {
+        const uint32_t nr = id + f;
+        ri.rkey[nr] = 0xffffffffu;
+        ri.hdr[1] = int32_t(nr);
+    }
+}
+
+// one thread per block of M values: its head, or the multi-run marker
+__global__ void k_runheads(int64_t mcount, const uint32_t* flags, const uint32_t* ids, RunIndex ri) {
+    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b == 0) ri.hdr[0] = ri.hdr[3] ? 0 : 1;
+    if (b >= ri.nbtot) return;
+    const int64_t p = b / ri.nblk, blk = b - p * ri.nblk;
+    const int64_t i0 = p * mcount + (blk << kRunBlkShift);
+    const int64_t i1 = p * mcount + min(mcount, (blk + 1) << kRunBlkShift);  // exclusive
+    const uint32_t r = ids[i0] + flags[i0] - 1u;  // run holding the block's first entry
+    const bool single = ri.rkey[r + 1] >= uint64_t(i1);
+    if (single) {
+        ri.bhead[b] = ri.rval[r];
+    } else {
+        ri.bhead[b] = make_int4(int(r), 0, INT32_MIN, 0);
+        atomicOr(ri.hdr + 2, 1);
+    }
+}
+
+size_t runs_temp_bytes(int64_t n) {
+    size_t b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b, static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                  int(n));
+    return b + 2 * ((size_t(n) * 4 + 255) & ~size_t(255));
+}
+
+cudaError_t launch_runs_build(const wt_grid_entry* entries, int64_t n, int64_t mcount, const RunIndex& ri,
+                              void* temp, cudaStream_t st) {
+    char* t = static_cast<char*>(temp);
+    const size_t arr = (size_t(n) * 4 + 255) & ~size_t(255);
+    uint32_t* flags = reinterpret_cast<uint32_t*>(t);
+    uint32_t* ids = reinterpret_cast<uint32_t*>(t + arr);
+    const unsigned g = unsigned((n + 255) / 256);
+    cudaError_t e = cudaMemsetAsync(ri.hdr, 0, 16, st);
+    if (e != cudaSuccess) return e;
+    k_runflags<<<g, 256, 0, st>>>(entries, n, mcount, flags, ri.hdr);
+    size_t b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b, flags, ids, int(n), st);
+    e = cub::DeviceScan::ExclusiveSum(t + 2 * arr, b, flags, ids, int(n), st);
+    if (e != cudaSuccess) return e;
+    k_runscatter<<<g, 256, 0, st>>>(entries, n, flags, ids, ri);
+    k_runheads<<<unsigned((ri.nbtot + 255) / 256), 256, 0, st>>>(mcount, flags, ids, ri);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------- drop-in per-table helpers
 __global__ void k_predict(DevImage im, PredictArgs a) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -860,9 +1137,10 @@ cudaError_t launch_grouped(const DevImage& im, const GroupedArgs& a, int grid, c
 
 // Persistent grid: exactly the CTAs that are co-resident (a grid-stride loop
 // over a partly non-resident grid leaves a half-occupied second wave).
-// WT_GATHER_VARIANT (A/B runs): 0 = prefetch, 4 CTAs/SM; 1 = prefetch, 5
+// WT_GATHER_VARIANT (A/B runs): 0 = hashed kernel when the call allows it
+// (else prefetching binary-search kernel, 4 CTAs/SM); 1 = prefetch, 5
 // CTAs/SM (register cap); 2 = no prefetch, 5 CTAs/SM (cap); 3 = no prefetch,
-// no cap.
+// no cap; 4 = never hashed; 5 = hashed, 4 CTAs/SM (register cap).
 template <int V, bool PF, int MINB>
 static cudaError_t go_gather(const DevImage& im, const GatherArgs& a, int grid, size_t smem, cudaStream_t st) {
     static int occ = 0, sms = 0;
@@ -878,6 +1156,30 @@ static cudaError_t go_gather(const DevImage& im, const GatherArgs& a, int grid, 
     return cudaGetLastError();
 }
 
+// Hashed gather launch: persistent grid of co-resident CTAs; the hash table
+// and the run-index budget are dynamic shared memory.
+template <int MINB>
+static cudaError_t go_gather_h(const GatherArgs& a, int grid, cudaStream_t st) {
+    static int occ = 0, sms = 0;
+    static size_t occ_hs = 0, attr_hs = 0;
+    const size_t hs = (size_t(1) << a.hbits) * sizeof(int4) + size_t(a.runs.budget);
+    if (hs > attr_hs) {  // static + dynamic may exceed the 48 KB default
+        cudaError_t e = cudaFuncSetAttribute(k_gather_h<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hs));
+        if (e != cudaSuccess) return e;
+        attr_hs = hs;
+    }
+    if (!occ || occ_hs != hs) {
+        occ_hs = hs;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather_h<MINB>, kGatherThreads, hs);
+        if (occ < 1) occ = 1;
+    }
+    k_gather_h<MINB><<<std::min(grid, sms * occ), kGatherThreads, hs, st>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gather(const DevImage& im, const GatherArgs& a, int grid, cudaStream_t st) {
     const size_t smem = size_t(a.n_pairs) * (sizeof(uint64_t) + sizeof(int32_t)) + 16;
     const auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
@@ -885,7 +1187,13 @@ cudaError_t launch_gather(const DevImage& im, const GatherArgs& a, int grid, cud
         const char* v = std::getenv("WT_GATHER_VARIANT");
         return v ? std::atoi(v) : 0;
     }();
-    if (al16(a.M) && al16(a.N) && al16(a.K) && al16(a.out.macro) && al16(a.out.micro) && al16(a.out.lat)) {
+    const bool aligned =
+        al16(a.M) && al16(a.N) && al16(a.K) && al16(a.out.macro) && al16(a.out.micro) && al16(a.out.lat);
+    const DecOut& o = a.out;
+    const bool plain = !(o.wave || o.flags || o.comps || o.tail || o.g || o.l || o.topk_macro);
+    if (aligned && plain && a.htab && variant != 4)
+        return variant == 5 ? go_gather_h<4>(a, grid, st) : go_gather_h<0>(a, grid, st);
+    if (aligned) {
         if (variant == 1) return go_gather<4, true, 5>(im, a, grid, smem, st);
         if (variant == 2) return go_gather<4, false, 5>(im, a, grid, smem, st);
         if (variant == 3) return go_gather<4, false, 0>(im, a, grid, smem, st);

@@ -63,6 +63,27 @@ struct GroupedArgs {
     DecOut out;
 };
 
+// Run-compressed grid heads for k_gather_h.  Along M the 16-byte head
+// (latency, macro, micro) of a grid entry is piecewise constant -- G changes
+// only where ceil(M / t_m) does -- so each pair's row is cut into blocks of
+// 2^kRunBlkShift M values: bhead[p * nblk + b] is the block's head when the
+// block holds a single run, else {first run index, 0, INT32_MIN, 0} and the
+// runs (rkey[r] = flat entry index where run r starts, rkey[nruns] =
+// 0xffffffff, rval[r] = head) resolve it.  Built on the device after a full
+// sweep (or by wt_grid_finalize); hdr = {valid, nruns, any multi-run block,
+// a head used the INT32_MIN marker}.  The gather stages it in shared memory
+// when it fits `budget` bytes, else reads heads from L2.
+constexpr int kRunBlkShift = 6;
+struct RunIndex {
+    int32_t* hdr;
+    int4* bhead;
+    uint32_t* rkey;
+    int4* rval;
+    int32_t nblk;    // blocks per pair
+    int32_t nbtot;   // n_pairs * nblk
+    int32_t budget;  // shared-memory bytes reserved for the index (0 = none)
+};
+
 struct GatherArgs {
     const uint64_t* pair_keys;  // sorted (N << 32 | K)
     const int32_t* pair_ids;
@@ -82,7 +103,18 @@ struct GatherArgs {
     int32_t* off_M;  // compacted copies of the off-grid queries' dims
     int32_t* off_N;
     int32_t* off_K;
+    // open-addressing (N, K) -> pair table for k_gather_h: 2^hbits int4
+    // slots {N, K, pair id, 0}, empty = pair id -1; null when not built
+    const int4* htab;
+    int32_t hbits;
+    RunIndex runs;
 };
+
+// slot of (N, K) in a 2^bits table: multiplicative hash, high bits
+__host__ __device__ __forceinline__ uint32_t pair_slot(uint32_t N, uint32_t K, int bits) {
+    const uint32_t h = N * 0x9E3779B1u + K * 0x7FEB352Du;
+    return (h ^ (h >> 16)) * 0x85EBCA6Bu >> (32 - bits);
+}
 
 struct PredictArgs {
     const int32_t* config;
@@ -124,6 +156,10 @@ cudaError_t launch_sweep(const DevImage& im, const SweepArgs& a, bool wide, cuda
 cudaError_t launch_eval(const DevImage& im, const EvalArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_grouped(const DevImage& im, const GroupedArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_gather(const DevImage& im, const GatherArgs& a, int grid, cudaStream_t st);
+// run index of a filled grid (n < 2^32 - 1 entries); temp from runs_temp_bytes
+size_t runs_temp_bytes(int64_t n);
+cudaError_t launch_runs_build(const wt_grid_entry* entries, int64_t n, int64_t mcount, const RunIndex& ri,
+                              void* temp, cudaStream_t st);
 cudaError_t launch_predict(const DevImage& im, const PredictArgs& a, cudaStream_t st);
 // one query, one warp; result + sequence number written to (pinned) `out`
 struct OneOut {

@@ -53,4 +53,5 @@ def sharded_sweep(grid, group=None, stream=None):
         grid.sweep(lo, hi, stream=stream)
 
     gather_grid(ent, grid.n_entries, group=group, fill=fill)
+    grid.finalize(stream=stream)
     return ent

@@ -182,6 +182,93 @@ def test_gather_matches_tune_with_offgrid(capi, orc, synth256):
     assert_same({k: v[sub] for k, v in got.items()}, want)
 
 
+@pytest.mark.parametrize("n_extra,offset", [(0, 0), (700, 0), (700, 1), (2100, 0)])
+def test_hashed_gather_plain_outputs(capi, orc, synth256, n_extra, offset):
+    """The common call (macro / micro / latency only) goes through the hashed
+    pair table (k_gather_h): many pairs (probe chains), invalid dims, N = K = 0
+    (never matches an empty slot), M outside the grid, n % 4 != 0 and
+    misaligned arrays (scalar kernel); answers == evaluate mode == oracle.
+    2100 extra pairs exceed the hashed-table cap (binary-search kernel)."""
+    from paper_2604_10187_b200 import synthetic as S
+
+    cfg, t, reg = synth256
+    eng = capi.Engine(t, reg, n_sm=148)
+    rng = np.random.default_rng(11 + n_extra)
+    pairs = list(S.LLAMA3_8B) + [(int(a), int(b)) for a, b in rng.integers(1, 40000, (n_extra, 2))]
+    grid = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 3, 300)
+    grid.sweep()
+    n = 50001
+    P = np.array(pairs)[rng.integers(0, len(pairs), n)]
+    M = rng.integers(1, 320, n).astype(np.int32)
+    N, K = P[:, 0].astype(np.int32), P[:, 1].astype(np.int32)
+    off = rng.random(n) < 0.05
+    N[off] = rng.integers(1, 40000, off.sum())
+    K[off] = rng.integers(1, 40000, off.sum())
+    M[:7] = [0, -3, 1, 2, 300, 301, 5]
+    N[:7] = [4096, 4096, 0, 4096, 4096, 4096, -1]
+    K[:7] = [4096, 4096, 0, 4096, 4096, 4096, 4096]
+    direct = tune_gpu(capi, eng, M, N, K)
+    buf = [torch.empty(n + offset, dtype=d, device="cuda") for d in (torch.int32, torch.int32, torch.float64)]
+    out = [b[offset:] for b in buf]
+    ins = [dev(np.concatenate([np.zeros(offset, np.int32), x]))[offset:] for x in (M, N, K)]
+    grid.gather(*ins, capi.Engine.decisions(*out))
+    torch.cuda.synchronize()
+    mac, mic, lat = (o.cpu().numpy() for o in out)
+    ok = (direct["flags"].astype(np.uint32) >> 24) == 0
+    np.testing.assert_array_equal(mac, direct["macro"])
+    np.testing.assert_array_equal(mic, direct["micro"])
+    np.testing.assert_array_equal(U.bits(lat[ok]), U.bits(direct["lat"][ok]))
+    assert (~ok).sum() >= 3
+    tiles = {int(i): (int(a), int(b), int(c)) for i, a, b, c in zip(cfg["id"], cfg["t_m"], cfg["t_n"], cfg["t_k"])}
+    flat = po.FlatTables(U.pytables_from_arrays(t), tiles)
+    sub = np.random.default_rng(1).choice(n, 5000, replace=False)
+    want = orc.tune(flat, 148, 1, M[sub], N[sub], K[sub])
+    good = want["status"] == 0
+    np.testing.assert_array_equal(mac[sub][good], want["macro"][good])
+    np.testing.assert_array_equal(U.bits(lat[sub][good]), U.bits(want["lat"][good]))
+
+
+def test_run_index_follows_entries(capi, synth256):
+    """The run-compressed heads the gather serves from shared memory are
+    rebuilt by a full sweep, invalidated by a partial one and rebuilt by
+    finalize() after entries are written directly."""
+    from paper_2604_10187_b200 import synthetic as S
+
+    cfg, t, reg = synth256
+    eng = capi.Engine(t, reg, n_sm=148)
+    pairs = S.LLAMA3_8B
+    grid = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 4096)
+    M, N, K = S.query_stream(20003, pairs, seed=3, off_grid_frac=0.0, m_max=4096)
+    n = len(M)
+
+    def gather():
+        out = [torch.empty(n, dtype=d, device="cuda") for d in (torch.int32, torch.int32, torch.float64)]
+        grid.gather(dev(M), dev(N), dev(K), capi.Engine.decisions(*out))
+        torch.cuda.synchronize()
+        return [o.cpu().numpy() for o in out]
+
+    grid.sweep()
+    want = tune_gpu(capi, eng, M, N, K)
+    for step in ("full", "partial", "written", "finalized"):
+        if step == "partial":
+            grid.sweep(0, 1000)
+        elif step == "written":
+            ent = grid.entries_tensor()
+            saved = ent.clone()
+            ent.zero_()
+            grid.finalize()
+            mac, mic, lat = gather()
+            assert (mac == 0).all() and (mic == 0).all() and (lat == 0).all()
+            ent.copy_(saved)
+            continue
+        elif step == "finalized":
+            grid.finalize()
+        mac, mic, lat = gather()
+        np.testing.assert_array_equal(mac, want["macro"], err_msg=step)
+        np.testing.assert_array_equal(mic, want["micro"], err_msg=step)
+        np.testing.assert_array_equal(U.bits(lat), U.bits(want["lat"]), err_msg=step)
+
+
 def test_topk_matches_oracle(capi, orc, synth256):
     from paper_2604_10187_b200 import synthetic as S
 
@@ -367,6 +454,9 @@ def test_sharded_sweep_equals_full(capi, synth256):
     {"WT_GATHER_VARIANT": "1"},
     {"WT_EVAL_RPT": "2", "WT_GATHER_VARIANT": "2"},
     {"WT_GATHER_VARIANT": "3"},
+    {"WT_GATHER_VARIANT": "4"},
+    {"WT_GATHER_RUNS_KB": "0"},
+    {"WT_GATHER_VARIANT": "5"},
 ])
 def test_launch_variants(capi, env):
     """Every launch shape the tuning knobs can select stays bit-exact."""
