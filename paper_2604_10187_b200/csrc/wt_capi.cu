@@ -171,7 +171,8 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
            o_al = ar.take(h.anchor_l.size() * 8), o_am = ar.take(h.anchor_micro.size() * 4);
     const size_t NS = h.seg_pos.size();
     size_t o_st = ar.take(NS * 16), o_sm = ar.take(NS * 16), o_sp = ar.take(NS * 4), o_cc = ar.take(C * 4),
-           o_th2 = ar.take(C * R * 32), o_m2 = ar.take(C * R * 4);
+           o_th2 = ar.take(C * R * 32), o_m2 = ar.take(C * R * 4), o_th2t = ar.take(C * R * 32),
+           o_m2t = ar.take(C * R * 4);
     cudaError_t ce = cudaMalloc(&e->mem, ar.used);
     if (ce != cudaSuccess) {
         delete e;
@@ -193,6 +194,7 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
         {o_st, h.seg_tiles.data(), NS * 16},      {o_sm, h.seg_magic.data(), NS * 16},
         {o_sp, h.seg_pos.data(), NS * 4},         {o_cc, h.cls_cfg.data(), C * 4},
         {o_th2, h.theta2.data(), C * R * 32},     {o_m2, h.meta2.data(), C * R * 4},
+        {o_th2t, h.theta2t.data(), C * R * 32},   {o_m2t, h.meta2t.data(), C * R * 4},
     };
     for (const Piece& p : pieces) {
         ce = cudaMemcpy(base + p.off, p.src, p.n, cudaMemcpyHostToDevice);
@@ -231,6 +233,8 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
     d.cls_cfg = reinterpret_cast<const int32_t*>(base + o_cc);
     d.theta2 = reinterpret_cast<const double4*>(base + o_th2);
     d.meta2 = reinterpret_cast<const uint32_t*>(base + o_m2);
+    d.theta2t = reinterpret_cast<const double4*>(base + o_th2t);
+    d.meta2t = reinterpret_cast<const uint32_t*>(base + o_m2t);
     // list-mode chunk: keep the staged rows near 40 KB so several CTAs fit per SM
     e->eval_chunk = int(std::max<size_t>(1, std::min<size_t>(C, 40960 / (R * 36 + 32))));
     e->eval_grid = sm_count(device) * 4;
@@ -315,6 +319,27 @@ static wt_status check_out(const wt_decisions* o) {
     return WT_OK;
 }
 
+// List evaluation without top-k: the row-grouped pipeline (wt_eval3.cu) by
+// default, the shared-memory staged kernel with WT_EVAL_MODE=2 (A/B runs).
+static cudaError_t run_list_eval(const wt_engine* e, const EvalArgs& a, cudaStream_t s) {
+    static const int mode = [] {
+        const char* v = std::getenv("WT_EVAL_MODE");
+        return v ? std::atoi(v) : 3;
+    }();
+    if (mode == 2) {
+        const int64_t tiles = (a.n + eval2_tile() - 1) / eval2_tile();
+        g_launches++;
+        return launch_eval2(e->dev, a, int(std::min<int64_t>(tiles, e->eval_grid2)), s);
+    }
+    void* scratch = nullptr;
+    cudaError_t ce = cudaMallocFromPoolAsync(&scratch, eval3_scratch_bytes(a.n), lib_pool(e->device), s);
+    if (ce != cudaSuccess) return ce;
+    ce = launch_eval3(e->dev, a, scratch, s);
+    cudaFreeAsync(scratch, s);
+    g_launches += kEval3Launches;
+    return ce;
+}
+
 wt_status wt_tune_batch(const wt_engine* e, const int32_t* M, const int32_t* N, const int32_t* K,
                         int64_t n, const wt_decisions* out, void* stream) {
     if (!e) return set_err(WT_INVALID_ARGUMENT, "null engine");
@@ -336,11 +361,10 @@ wt_status wt_tune_batch(const wt_engine* e, const int32_t* M, const int32_t* N, 
     if (a.out.topk > 0) {  // per-config order kernel keeps the top-k list
         const int64_t tiles = (n + kEvalThreads - 1) / kEvalThreads;
         ce = launch_eval(e->dev, a, int(std::min<int64_t>(tiles, e->eval_grid)), static_cast<cudaStream_t>(stream));
+        g_launches++;
     } else {
-        const int64_t tiles = (n + eval2_tile() - 1) / eval2_tile();
-        ce = launch_eval2(e->dev, a, int(std::min<int64_t>(tiles, e->eval_grid2)), static_cast<cudaStream_t>(stream));
+        ce = run_list_eval(e, a, static_cast<cudaStream_t>(stream));
     }
-    g_launches++;
     if (ce != cudaSuccess) return cuda_err(ce, "wt_tune_batch");
     return WT_OK;
 }
@@ -933,8 +957,12 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
             ea.K = offK;
             ea.inputs_compact = 1;
         }
-        ce = ea.out.topk > 0 ? launch_eval(e->dev, ea, e->eval_grid, s) : launch_eval2(e->dev, ea, e->eval_grid2, s);
-        g_launches++;
+        if (ea.out.topk > 0) {
+            ce = launch_eval(e->dev, ea, e->eval_grid, s);
+            g_launches++;
+        } else {
+            ce = run_list_eval(e, ea, s);
+        }
     }
     cudaFreeAsync(scratch, s);
     if (ce != cudaSuccess) return cuda_err(ce, "wt_gather_batch");

@@ -218,6 +218,11 @@ cudaError_t launch_serve(const DevImage& im, int64_t n_anchor, Mailbox* mb, uint
 size_t sweep2_scratch_bytes(const DevImage& im, const SweepArgs& a);
 cudaError_t launch_sweep2(const DevImage& im, const SweepArgs& a, bool wide, void* scratch, cudaStream_t st);
 cudaError_t launch_eval2(const DevImage& im, const EvalArgs& a, int grid, cudaStream_t st);
+// row-grouped list evaluation (wt_eval3.cu): key + histogram, scan, scatter,
+// evaluation; scratch of eval3_scratch_bytes(a.n) (a.n = host upper bound)
+size_t eval3_scratch_bytes(int64_t n);
+cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, cudaStream_t st);
+constexpr int kEval3Launches = 5;  // key, scan (2), scatter, eval
 int eval2_tile();
 cudaError_t launch_explain(const DevImage& im, const ExplainArgs& a, cudaStream_t st);
 cudaError_t launch_nearest(const NearestArgs& a, cudaStream_t st);

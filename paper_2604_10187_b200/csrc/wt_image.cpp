@@ -260,6 +260,14 @@ wt_status build_image(const wt_tables_desc& T, const wt_registry_desc& reg, cons
             std::copy(im.rowmeta.begin() + size_t(c) * R, im.rowmeta.begin() + size_t(c + 1) * R,
                       im.meta2.begin() + size_t(pos) * R);
         }
+        im.theta2t.resize(im.theta.size());
+        im.meta2t.resize(im.rowmeta.size());
+        for (int32_t pos = 0; pos < C; ++pos)
+            for (int32_t r = 0; r < R; ++r) {
+                std::copy(im.theta2.begin() + (size_t(pos) * R + r) * 4, im.theta2.begin() + (size_t(pos) * R + r + 1) * 4,
+                          im.theta2t.begin() + (size_t(r) * C + pos) * 4);
+                im.meta2t[size_t(r) * C + pos] = im.meta2[size_t(pos) * R + r];
+            }
     }
     if (im.anchor_l.empty()) {  // keep the pool non-empty for the device
         im.anchor_l.push_back(0);

@@ -68,6 +68,8 @@ struct DevImage {
     const int32_t* cls_cfg;   // [C] class-ordered position -> config index
     const double4* theta2;    // [C*R] rows in class order
     const uint32_t* meta2;    // [C*R] rowmeta in class order
+    const double4* theta2t;   // [R][C] rows by wave, class order inside (k_eval3:
+    const uint32_t* meta2t;   //        a segment's configs are contiguous)
 };
 
 constexpr int kSegCfg = 32;
@@ -95,6 +97,8 @@ struct HostImage {
     std::vector<int32_t> cls_cfg;
     std::vector<double> theta2;
     std::vector<uint32_t> meta2;
+    std::vector<double> theta2t;  // [R][C] transposed theta2
+    std::vector<uint32_t> meta2t;
 };
 
 // Thread-local message returned by wt_last_error().

@@ -457,6 +457,9 @@ def test_sharded_sweep_equals_full(capi, synth256):
     {"WT_GATHER_VARIANT": "4"},
     {"WT_GATHER_RUNS_KB": "0"},
     {"WT_GATHER_VARIANT": "5"},
+    {"WT_EVAL_MODE": "2"},
+    {"WT_EVAL_KEY_BITS": "8"},
+    {"WT_EVAL_KEY_BITS": "24"},
 ])
 def test_launch_variants(capi, env):
     """Every launch shape the tuning knobs can select stays bit-exact."""

@@ -1,5 +1,6 @@
 """Drives one kernel family for an ncu capture (diagnostic; not a bench line).
-usage: python tools/prof_kernels.py {sweep3|eval|gather} [n]"""
+usage: python tools/prof_kernels.py {sweep3|eval|gather|step|fit} [n]
+(step = the bench step: gather of the config-2 stream with 1% off-grid)"""
 import os
 import sys
 
@@ -31,7 +32,7 @@ else:
     pairs = S.LLAMA3_8B
     grid = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 8192)
     grid.sweep()
-    frac = 1.0 if mode == "eval" else 0.0
+    frac = {"eval": 1.0, "step": 0.01}.get(mode, 0.0)
     M, N, K = (torch.from_numpy(x).cuda() for x in S.query_stream(n, pairs, seed=3, off_grid_frac=frac))
     o = [torch.empty(n, dtype=d, device="cuda") for d in (torch.int32, torch.int32, torch.float64)]
     d = capi.Engine.decisions(*o)
