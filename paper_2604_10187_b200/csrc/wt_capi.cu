@@ -321,22 +321,28 @@ static wt_status check_out(const wt_decisions* o) {
 
 // List evaluation without top-k: the row-grouped pipeline (wt_eval3.cu) by
 // default, the shared-memory staged kernel with WT_EVAL_MODE=2 (A/B runs).
-static cudaError_t run_list_eval(const wt_engine* e, const EvalArgs& a, cudaStream_t s) {
+static int eval_mode() {
     static const int mode = [] {
         const char* v = std::getenv("WT_EVAL_MODE");
         return v ? std::atoi(v) : 3;
     }();
-    if (mode == 2) {
+    return mode;
+}
+
+// scratch != null: allocated (and keyed) by the caller
+static cudaError_t run_list_eval(const wt_engine* e, const EvalArgs& a, cudaStream_t s, void* scratch = nullptr) {
+    if (eval_mode() == 2) {
         const int64_t tiles = (a.n + eval2_tile() - 1) / eval2_tile();
         g_launches++;
         return launch_eval2(e->dev, a, int(std::min<int64_t>(tiles, e->eval_grid2)), s);
     }
-    void* scratch = nullptr;
-    cudaError_t ce = cudaMallocFromPoolAsync(&scratch, eval3_scratch_bytes(a.n), lib_pool(e->device), s);
+    const bool own = scratch == nullptr;
+    cudaError_t ce = cudaSuccess;
+    if (own) ce = cudaMallocFromPoolAsync(&scratch, eval3_scratch_bytes(a.n), lib_pool(e->device), s);
     if (ce != cudaSuccess) return ce;
-    ce = launch_eval3(e->dev, a, scratch, s);
-    cudaFreeAsync(scratch, s);
-    g_launches += kEval3Launches;
+    ce = launch_eval3(e->dev, a, scratch, !own, s);
+    if (own) cudaFreeAsync(scratch, s);
+    g_launches += own ? kEval3Launches : kEval3Launches - 1;
     return ce;
 }
 
@@ -936,6 +942,20 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
     a.htab = g->dhash;
     a.hbits = g->hbits;
     a.runs = g->runs;
+    // row-grouped evaluation of the off-grid list: keys counted while compacting
+    void* escratch = nullptr;
+    if (g->topk == 0 && out->topk == 0 && eval_mode() == 3) {
+        ce = cudaMallocFromPoolAsync(&escratch, eval3_scratch_bytes(n), lib_pool(e->device), s);
+        if (ce != cudaSuccess) {
+            cudaFreeAsync(scratch, s);
+            return cuda_err(ce, "wt_gather_batch: eval scratch");
+        }
+        const Eval3Bufs b = eval3_bufs(escratch, n);
+        cudaMemsetAsync(b.hist, 0, b.hist_bytes, s);
+        a.off_key = b.keys;
+        a.key_hist = b.hist;
+        a.key_bits = b.key_bits;
+    }
     const int grid = int(std::min<int64_t>((n + kGatherThreads - 1) / kGatherThreads,
                                            int64_t(sm_count(e->device)) * 8));
     ce = launch_gather(e->dev, a, grid, s);
@@ -961,10 +981,11 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
             ce = launch_eval(e->dev, ea, e->eval_grid, s);
             g_launches++;
         } else {
-            ce = run_list_eval(e, ea, s);
+            ce = run_list_eval(e, ea, s, escratch);
         }
     }
     cudaFreeAsync(scratch, s);
+    if (escratch) cudaFreeAsync(escratch, s);
     if (ce != cudaSuccess) return cuda_err(ce, "wt_gather_batch");
     return WT_OK;
 }

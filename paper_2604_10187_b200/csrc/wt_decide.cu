@@ -426,7 +426,11 @@ struct WarpBuf {  // one warp's pending off-grid queries (index + dims)
     int32_t m[kWarpBuf], n[kWarpBuf], k[kWarpBuf];
 };
 
-__device__ __forceinline__ void wbuf_drain(WarpBuf& b, int& wcnt, const GatherArgs& a, int lane) {
+// With a.off_key set, the drain also computes each appended query's
+// grouping key for the list evaluation (wt_eval3.cu) and counts it -- work
+// the HBM-bound gather absorbs, instead of a separate pass over the list.
+__device__ __forceinline__ void wbuf_drain(WarpBuf& b, int& wcnt, const GatherArgs& a, int lane,
+                                           const DevImage* im = nullptr) {
     __syncwarp();
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(reinterpret_cast<unsigned long long*>(a.off_count), (unsigned long long)wcnt);
@@ -436,13 +440,18 @@ __device__ __forceinline__ void wbuf_drain(WarpBuf& b, int& wcnt, const GatherAr
         a.off_M[base + i] = b.m[i];
         a.off_N[base + i] = b.n[i];
         a.off_K[base + i] = b.k[i];
+        if (im && a.off_key) {
+            const uint32_t key = eval_key(*im, b.m[i], b.n[i], b.k[i], a.key_bits, int64_t(base + i));
+            a.off_key[base + i] = key;
+            atomicAdd(a.key_hist + key, 1u);
+        }
     }
     __syncwarp();
     wcnt = 0;
 }
 
 __device__ __forceinline__ void wbuf_push(bool off, int64_t q, int32_t M, int32_t N, int32_t K, WarpBuf& b,
-                                          int& wcnt, const GatherArgs& a, int lane) {
+                                          int& wcnt, const GatherArgs& a, int lane, const DevImage* im = nullptr) {
     const unsigned mask = __ballot_sync(0xffffffffu, off);
     if (off) {
         const int at = wcnt + __popc(mask & ((1u << lane) - 1u));
@@ -452,11 +461,12 @@ __device__ __forceinline__ void wbuf_push(bool off, int64_t q, int32_t M, int32_
         b.k[at] = K;
     }
     wcnt += __popc(mask);
-    if (wcnt > 32) wbuf_drain(b, wcnt, a, lane);
+    if (wcnt > 32) wbuf_drain(b, wcnt, a, lane, im);
 }
 
-__device__ __forceinline__ void wbuf_flush(WarpBuf& b, int& wcnt, const GatherArgs& a, int lane) {
-    if (wcnt > 0) wbuf_drain(b, wcnt, a, lane);
+__device__ __forceinline__ void wbuf_flush(WarpBuf& b, int& wcnt, const GatherArgs& a, int lane,
+                                           const DevImage* im = nullptr) {
+    if (wcnt > 0) wbuf_drain(b, wcnt, a, lane, im);
 }
 
 // One query: returns true when answered from the grid (writes optional
@@ -593,7 +603,8 @@ __global__ void __launch_bounds__(kGatherThreads, MINB) k_gather(DevImage im, Ga
             }
         }
 #pragma unroll
-        for (int j = 0; j < V; ++j) wbuf_push(live && !on[j], v * V + j, M[j], N[j], K[j], slice, wcnt, a, lane);
+        for (int j = 0; j < V; ++j)
+            wbuf_push(live && !on[j], v * V + j, M[j], N[j], K[j], slice, wcnt, a, lane, &im);
     }
     // scalar tail (n % V queries), handled by the first warp of block 0
     if (V > 1 && blockIdx.x == 0 && threadIdx.x < 32) {
@@ -613,9 +624,9 @@ __global__ void __launch_bounds__(kGatherThreads, MINB) k_gather(DevImage im, Ga
                 o.lat[q] = __hiloint2double(lo4.y, lo4.x);
             }
         }
-        wbuf_push(live && !on, q, tM, tN, tK, slice, wcnt, a, lane);
+        wbuf_push(live && !on, q, tM, tN, tK, slice, wcnt, a, lane, &im);
     }
-    wbuf_flush(slice, wcnt, a, lane);
+    wbuf_flush(slice, wcnt, a, lane, &im);
 }
 
 // Hashed gather: the common call (macro / micro / latency outputs only,
@@ -664,8 +675,8 @@ __device__ __forceinline__ bool hlookup(const int4* tab, uint32_t hmask, int bit
 }
 
 template <bool RUNS>
-__device__ __forceinline__ void gather_h_loop(const GatherArgs& a, const int4* tab, const RunSmem& rs,
-                                              WarpBuf& slice) {
+__device__ __forceinline__ void gather_h_loop(const DevImage& im, const GatherArgs& a, const int4* tab,
+                                              const RunSmem& rs, WarpBuf& slice) {
     const int bits = a.hbits;
     const uint32_t hmask = (1u << bits) - 1u;
     const uint32_t mlo = uint32_t(a.m_lo), mcnt = uint32_t(a.mcount);
@@ -751,7 +762,8 @@ __device__ __forceinline__ void gather_h_loop(const GatherArgs& a, const int4* t
         }
         if (__any_sync(0xffffffffu, offm != 0)) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) wbuf_push((offm >> j) & 1u, v * 4 + j, M[j], N[j], K[j], slice, wcnt, a, lane);
+            for (int j = 0; j < 4; ++j)
+                wbuf_push((offm >> j) & 1u, v * 4 + j, M[j], N[j], K[j], slice, wcnt, a, lane, &im);
         }
     }
     // scalar tail (n % 4 queries), first warp of block 0
@@ -772,13 +784,13 @@ __device__ __forceinline__ void gather_h_loop(const GatherArgs& a, const int4* t
                 a.out.lat[q] = __hiloint2double(lo4.y, lo4.x);
             }
         }
-        wbuf_push(live && !on, q, tM, tN, tK, slice, wcnt, a, lane);
+        wbuf_push(live && !on, q, tM, tN, tK, slice, wcnt, a, lane, &im);
     }
-    wbuf_flush(slice, wcnt, a, lane);
+    wbuf_flush(slice, wcnt, a, lane, &im);
 }
 
 template <int MINB>
-__global__ void __launch_bounds__(kGatherThreads, MINB) k_gather_h(GatherArgs a) {
+__global__ void __launch_bounds__(kGatherThreads, MINB) k_gather_h(DevImage im, GatherArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     int4* tab = reinterpret_cast<int4*>(smem);
     __shared__ WarpBuf wbuf[kGatherThreads / 32];
@@ -810,9 +822,9 @@ __global__ void __launch_bounds__(kGatherThreads, MINB) k_gather_h(GatherArgs a)
     __syncthreads();
     WarpBuf& slice = wbuf[threadIdx.x >> 5];
     if (runs)
-        gather_h_loop<true>(a, tab, rs, slice);
+        gather_h_loop<true>(im, a, tab, rs, slice);
     else
-        gather_h_loop<false>(a, tab, rs, slice);
+        gather_h_loop<false>(im, a, tab, rs, slice);
 }
 
 // ---- run index build (after a full sweep / wt_grid_finalize)
@@ -1159,7 +1171,7 @@ static cudaError_t go_gather(const DevImage& im, const GatherArgs& a, int grid, 
 // Hashed gather launch: persistent grid of co-resident CTAs; the hash table
 // and the run-index budget are dynamic shared memory.
 template <int MINB>
-static cudaError_t go_gather_h(const GatherArgs& a, int grid, cudaStream_t st) {
+static cudaError_t go_gather_h(const DevImage& im, const GatherArgs& a, int grid, cudaStream_t st) {
     static int occ = 0, sms = 0;
     static size_t occ_hs = 0, attr_hs = 0;
     const size_t hs = (size_t(1) << a.hbits) * sizeof(int4) + size_t(a.runs.budget);
@@ -1176,7 +1188,7 @@ static cudaError_t go_gather_h(const GatherArgs& a, int grid, cudaStream_t st) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather_h<MINB>, kGatherThreads, hs);
         if (occ < 1) occ = 1;
     }
-    k_gather_h<MINB><<<std::min(grid, sms * occ), kGatherThreads, hs, st>>>(a);
+    k_gather_h<MINB><<<std::min(grid, sms * occ), kGatherThreads, hs, st>>>(im, a);
     return cudaGetLastError();
 }
 
@@ -1192,7 +1204,7 @@ cudaError_t launch_gather(const DevImage& im, const GatherArgs& a, int grid, cud
     const DecOut& o = a.out;
     const bool plain = !(o.wave || o.flags || o.comps || o.tail || o.g || o.l || o.topk_macro);
     if (aligned && plain && a.htab && variant != 4)
-        return variant == 5 ? go_gather_h<4>(a, grid, st) : go_gather_h<0>(a, grid, st);
+        return variant == 5 ? go_gather_h<4>(im, a, grid, st) : go_gather_h<0>(im, a, grid, st);
     if (aligned) {
         if (variant == 1) return go_gather<4, true, 5>(im, a, grid, smem, st);
         if (variant == 2) return go_gather<4, false, 5>(im, a, grid, smem, st);

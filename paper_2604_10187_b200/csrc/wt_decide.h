@@ -108,6 +108,11 @@ struct GatherArgs {
     const int4* htab;
     int32_t hbits;
     RunIndex runs;
+    // optional: grouping key of every compacted off-grid query + its bucket
+    // histogram, computed while compacting (k_gather_h), for launch_eval3
+    uint32_t* off_key;
+    uint32_t* key_hist;
+    int32_t key_bits;
 };
 
 // slot of (N, K) in a 2^bits table: multiplicative hash, high bits
@@ -221,7 +226,15 @@ cudaError_t launch_eval2(const DevImage& im, const EvalArgs& a, int grid, cudaSt
 // row-grouped list evaluation (wt_eval3.cu): key + histogram, scan, scatter,
 // evaluation; scratch of eval3_scratch_bytes(a.n) (a.n = host upper bound)
 size_t eval3_scratch_bytes(int64_t n);
-cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, cudaStream_t st);
+struct Eval3Bufs {
+    uint32_t* hist;  // 2^(key_bits + spread) bucket counters
+    uint32_t* keys;  // per list slot
+    int32_t key_bits;
+    size_t hist_bytes;
+};
+Eval3Bufs eval3_bufs(void* scratch, int64_t n);
+// keys_ready: hist / keys were filled by the gather's compaction
+cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, bool keys_ready, cudaStream_t st);
 constexpr int kEval3Launches = 5;  // key, scan (2), scatter, eval
 int eval2_tile();
 cudaError_t launch_explain(const DevImage& im, const ExplainArgs& a, cudaStream_t st);

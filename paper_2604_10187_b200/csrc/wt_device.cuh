@@ -196,4 +196,72 @@ __device__ __forceinline__ void write_decision(const DecOut& o, int64_t q, const
     if (o.tail) o.tail[q] = ok ? double(f.tail) : 0.0;
 }
 
+// ---- list-mode grouping key (wt_eval3.cu)
+constexpr int kSpreadBits = 3;
+
+// Per-query validity exactly as k_eval2 (kernel_map.cpp:238-239 + the
+// 32-bit wave guard); invalid queries evaluate as (1, 1, 1) and are flagged.
+__device__ __forceinline__ uint32_t query_status(const DevImage& im, int32_t m, int32_t n, int32_t k, uint32_t* M,
+                                                 uint32_t* N, uint32_t* K) {
+    *M = *N = *K = 1u;
+    if (m < 1 || n < 1 || k < 1) return WT_INVALID_ARGUMENT;
+    const uint64_t gmax = uint64_t((uint32_t(m) + uint32_t(im.tm_min) - 1) / uint32_t(im.tm_min)) *
+                          uint64_t((uint32_t(n) + uint32_t(im.tn_min) - 1) / uint32_t(im.tn_min));
+    if ((gmax + uint64_t(im.S) - 1) / uint64_t(im.S) >= (uint64_t(1) << 31)) return WT_UNSUPPORTED;
+    *M = uint32_t(m);
+    *N = uint32_t(n);
+    *K = uint32_t(k);
+    return 0;
+}
+
+// wave row of shape (M, N) under a tile class's magic numbers (g = tiles)
+__device__ __forceinline__ uint32_t row_for(const DevImage& im, uint32_t y2M, uint32_t y2N, uint4 mg, uint64_t* g) {
+    const uint32_t mt = mdiv2(y2M, mg.x, mg.w & 0xffu) + 1u;
+    const uint32_t nt = mdiv2(y2N, mg.y, (mg.w >> 8) & 0xffu) + 1u;
+    *g = uint64_t(mt) * nt;
+    const uint32_t gc = *g > im.RS ? im.RS : uint32_t(*g);
+    return row_of(gc, im.mS, im.sS);
+}
+
+// Grouping key of a query: the wave rows of the first and the last tile
+// class (a prefix, so neighbouring groups are similar) + a hash of the rows
+// of every distinct (t_m, t_n); `bits` wide, then kSpreadBits sub-bucket bits
+// from the list slot (spreads the atomics of large groups; the sub-buckets
+// of one key stay adjacent after the scan).
+__device__ __forceinline__ uint32_t eval_key(const DevImage& im, int32_t m, int32_t n, int32_t k, int bits,
+                                             int64_t slot) {
+    uint32_t M, N, K;
+    uint32_t key = 0;
+    if (!query_status(im, m, n, k, &M, &N, &K)) {
+        int br = 1;
+        while ((1 << br) < im.R) ++br;
+        const int pre = (2 * br + 4 <= bits) ? 2 : (br + 4 <= bits ? 1 : 0);
+        const int hb = bits - pre * br;
+        const uint32_t y2M = 2u * (M - 1u), y2N = 2u * (N - 1u);
+        uint32_t h = 0x811c9dc5u, first = 0, last = 0, pm = 0, pn = 0, ps = 0xffffffffu;
+        for (int s = 0; s < im.nseg; ++s) {
+            const uint4 mg = __ldg(im.seg_magic + s);
+            if (mg.x == pm && mg.y == pn && (mg.w & 0xffffu) == ps) continue;  // same (t_m, t_n)
+            pm = mg.x;
+            pn = mg.y;
+            ps = mg.w & 0xffffu;
+            uint64_t g;
+            const uint32_t r = row_for(im, y2M, y2N, mg, &g);
+            if (s == 0) first = r;
+            last = r;
+            h = (h ^ r) * 0x01000193u;
+        }
+        h ^= h >> 15;
+        h *= 0x2c1b3c6du;
+        h ^= h >> 12;
+        if (pre == 2)
+            key = (first << (bits - br)) | (last << (bits - 2 * br)) | (h & ((1u << hb) - 1u));
+        else if (pre == 1)
+            key = (first << (bits - br)) | (h & ((1u << hb) - 1u));
+        else
+            key = h & ((1u << bits) - 1u);
+    }
+    return (key << kSpreadBits) | uint32_t(slot & ((1 << kSpreadBits) - 1));
+}
+
 }  // namespace wtb

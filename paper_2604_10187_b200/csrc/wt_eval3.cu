@@ -40,35 +40,11 @@ namespace wtb {
 namespace {
 
 constexpr int kT3 = 256;
-constexpr int kSpreadBits = 3;
 constexpr int kMaxSmemSeg = 256;  // segment headers staged in shared memory up to this count
 constexpr double kInf3 = __builtin_huge_val();
 
 __device__ __forceinline__ bool lex_less3(double a, int ia, double b, int ib) {
     return a < b || (a == b && ia < ib);
-}
-
-// Per-query validity exactly as k_eval2 (kernel_map.cpp:238-239 + the
-// 32-bit wave guard); invalid queries evaluate as (1, 1, 1) and are flagged.
-__device__ __forceinline__ uint32_t query_status(const DevImage& im, int32_t m, int32_t n, int32_t k, uint32_t* M,
-                                                 uint32_t* N, uint32_t* K) {
-    *M = *N = *K = 1u;
-    if (m < 1 || n < 1 || k < 1) return WT_INVALID_ARGUMENT;
-    const uint64_t gmax = uint64_t((uint32_t(m) + uint32_t(im.tm_min) - 1) / uint32_t(im.tm_min)) *
-                          uint64_t((uint32_t(n) + uint32_t(im.tn_min) - 1) / uint32_t(im.tn_min));
-    if ((gmax + uint64_t(im.S) - 1) / uint64_t(im.S) >= (uint64_t(1) << 31)) return WT_UNSUPPORTED;
-    *M = uint32_t(m);
-    *N = uint32_t(n);
-    *K = uint32_t(k);
-    return 0;
-}
-
-__device__ __forceinline__ uint32_t row_for(const DevImage& im, uint32_t y2M, uint32_t y2N, uint4 mg, uint64_t* g) {
-    const uint32_t mt = mdiv2(y2M, mg.x, mg.w & 0xffu) + 1u;
-    const uint32_t nt = mdiv2(y2N, mg.y, (mg.w >> 8) & 0xffu) + 1u;
-    *g = uint64_t(mt) * nt;
-    const uint32_t gc = *g > im.RS ? im.RS : uint32_t(*g);
-    return row_of(gc, im.mS, im.sS);
 }
 
 }  // namespace
@@ -77,65 +53,75 @@ __device__ __forceinline__ uint32_t row_for(const DevImage& im, uint32_t y2M, ui
 __global__ void k_ekey(DevImage im, EvalArgs a, int bits, uint32_t* keys, uint32_t* hist) {
     const int64_t n = a.count ? *a.count : a.n;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    int br = 1;
-    while ((1 << br) < im.R) ++br;
-    const int pre = (2 * br + 4 <= bits) ? 2 : (br + 4 <= bits ? 1 : 0);
-    const int hb = bits - pre * br;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
         const int64_t src = a.inputs_compact ? i : (a.idx ? a.idx[i] : i);
-        uint32_t M, N, K;
-        uint32_t key = 0;
-        if (!query_status(im, a.M[src], a.N[src], a.K[src], &M, &N, &K)) {
-            const uint32_t y2M = 2u * (M - 1u), y2N = 2u * (N - 1u);
-            uint32_t h = 0x811c9dc5u, first = 0, last = 0, pm = 0, pn = 0, ps = 0xffffffffu;
-            for (int s = 0; s < im.nseg; ++s) {
-                const uint4 mg = __ldg(im.seg_magic + s);
-                if (mg.x == pm && mg.y == pn && (mg.w & 0xffffu) == ps) continue;  // same (t_m, t_n)
-                pm = mg.x;
-                pn = mg.y;
-                ps = mg.w & 0xffffu;
-                uint64_t g;
-                const uint32_t r = row_for(im, y2M, y2N, mg, &g);
-                if (s == 0) first = r;
-                last = r;
-                h = (h ^ r) * 0x01000193u;
-            }
-            h ^= h >> 15;
-            h *= 0x2c1b3c6du;
-            h ^= h >> 12;
-            if (pre == 2)
-                key = (first << (bits - br)) | (last << (bits - 2 * br)) | (h & ((1u << hb) - 1u));
-            else if (pre == 1)
-                key = (first << (bits - br)) | (h & ((1u << hb) - 1u));
-            else
-                key = h & ((1u << bits) - 1u);
-        }
-        // 8 adjacent sub-buckets per key (by query slot) spread the atomics of
-        // large groups; sub-buckets of one key stay contiguous after the scan
-        key = (key << kSpreadBits) | uint32_t(i & ((1 << kSpreadBits) - 1));
+        const uint32_t key = eval_key(im, a.M[src], a.N[src], a.K[src], bits, i);
         keys[i] = key;
         atomicAdd(hist + key, 1u);
     }
 }
 
-__global__ void k_escatter(EvalArgs a, const uint32_t* keys, uint32_t* offs, int64_t* sq, int32_t* sM, int32_t* sN,
-                           int32_t* sK) {
+// Counting-sort scatter with CTA-level aggregation: a chunk of 2048 list
+// slots is ranked per key in a shared-memory hash table, then one global
+// atomicAdd per (chunk, key) reserves the chunk's positions -- large groups
+// cost one global atomic per chunk instead of one per query.
+constexpr int kScPer = 8;       // slots per thread
+constexpr int kScTab = 4096;    // table slots (load <= 1/2)
+constexpr uint32_t kEmpty = 0xffffffffu;  // keys are < 2^27
+
+// Records are packed {query index (low 32 bits), M, N, K}: one 16-byte store
+// per query (scattered 4-byte stores cost a partial sector each).  Batches of
+// 2^31 queries or more also store the index's high half in `qhi`.
+__global__ void __launch_bounds__(kT3) k_escatter(EvalArgs a, const uint32_t* keys, uint32_t* offs, int4* rec,
+                                                  int32_t* qhi) {
+    __shared__ uint32_t tkey[kScTab];
+    __shared__ uint32_t tcnt[kScTab];
     const int64_t n = a.count ? *a.count : a.n;
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const uint32_t p = atomicAdd(offs + keys[i], 1u);
-        const int64_t src = a.inputs_compact ? i : (a.idx ? a.idx[i] : i);
-        sq[p] = a.idx ? a.idx[i] : i;
-        sM[p] = a.M[src];
-        sN[p] = a.N[src];
-        sK[p] = a.K[src];
+    const int64_t chunk = int64_t(kT3) * kScPer;
+    for (int64_t c0 = int64_t(blockIdx.x) * chunk; c0 < n; c0 += int64_t(gridDim.x) * chunk) {
+        for (int i = threadIdx.x; i < kScTab; i += kT3) {
+            tkey[i] = kEmpty;
+            tcnt[i] = 0;
+        }
+        __syncthreads();
+        uint32_t slot[kScPer], rank[kScPer];
+#pragma unroll
+        for (int k = 0; k < kScPer; ++k) {
+            const int64_t i = c0 + int64_t(k) * kT3 + threadIdx.x;
+            slot[k] = kEmpty;
+            if (i < n) {
+                const uint32_t key = keys[i];
+                uint32_t h = (key * 0x9E3779B1u) >> 20;  // 12 bits = kScTab
+                for (;;) {
+                    const uint32_t old = atomicCAS(tkey + h, kEmpty, key);
+                    if (old == kEmpty || old == key) break;
+                    h = (h + 1u) & (kScTab - 1u);
+                }
+                slot[k] = h;
+                rank[k] = atomicAdd(tcnt + h, 1u);
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kScTab; i += kT3)
+            if (tcnt[i]) tcnt[i] = atomicAdd(offs + tkey[i], tcnt[i]);  // count -> chunk's base
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kScPer; ++k) {
+            if (slot[k] == kEmpty) continue;
+            const int64_t i = c0 + int64_t(k) * kT3 + threadIdx.x;
+            const uint32_t p = tcnt[slot[k]] + rank[k];
+            const int64_t src = a.inputs_compact ? i : (a.idx ? a.idx[i] : i);
+            const int64_t q = a.idx ? a.idx[i] : i;
+            rec[p] = make_int4(int32_t(uint32_t(q)), a.M[src], a.N[src], a.K[src]);
+            if (qhi) qhi[p] = int32_t(q >> 32);
+        }
+        __syncthreads();
     }
 }
 
 // ------------------------------------------------------------------ eval
 template <bool SPECIAL>
-__global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const int64_t* sq, const int32_t* sM,
-                                               const int32_t* sN, const int32_t* sK) {
+__global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const int4* rec, const int32_t* qhi) {
     // segment headers in shared memory (broadcast LDS instead of dependent
     // global loads at every segment start)
     __shared__ int4 h_tiles[kMaxSmemSeg];
@@ -157,6 +143,28 @@ __global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const
     const int64_t nt = (n + 3) / 4;  // thread tiles of 4 consecutive grouped queries
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     const int C = im.C;
+    // Per-warp two-stage row buffers: while segment s is evaluated from one
+    // stage, the lanes' loads of segment s+1's rows (at lane 0's row of that
+    // tile class) are in flight and land in the other stage.  A warp whose
+    // 128 queries share that row (the uniform case) then reads broadcasts
+    // from shared memory instead of waiting on L1/L2.
+    __shared__ __align__(16) double4 wrows[kT3 / 32][2][kSegCfg];
+    const int lane = threadIdx.x & 31;
+    double4* myrows = wrows[threadIdx.x >> 5][0];
+    auto issue = [&](int s2, uint32_t r, int4& R0, int4& R1) {
+        const int n2 = 2 * Ts[s2].w;  // 16-byte halves of the segment's rows
+        const int4* src = reinterpret_cast<const int4*>(im.theta2t + size_t(r) * C + Ps[s2]);
+        R0 = lane < n2 ? __ldg(src + lane) : make_int4(0, 0, 0, 0);
+        R1 = lane + 32 < n2 ? __ldg(src + lane + 32) : make_int4(0, 0, 0, 0);
+    };
+    auto commit = [&](int stage, int s2, const int4& R0, const int4& R1) {
+        const int n2 = 2 * Ts[s2].w;
+        int4* dst = reinterpret_cast<int4*>(myrows + stage * kSegCfg);
+        __syncwarp();
+        if (lane < n2) dst[lane] = R0;
+        if (lane + 32 < n2) dst[lane + 32] = R1;
+        __syncwarp();
+    };
     // warp-uniform trip count: every lane of a warp stays in the loop
     for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < nt; base += stride) {
         const int64_t t = base + threadIdx.x;
@@ -171,8 +179,9 @@ __global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const
             uint32_t M = 1, N = 1, K = 1, st = 0;
             q[j] = -1;
             if (live) {
-                q[j] = sq[i];
-                st = query_status(im, sM[i], sN[i], sK[i], &M, &N, &K);
+                const int4 r = rec[i];
+                q[j] = int64_t(uint32_t(r.x)) | (qhi ? int64_t(qhi[i]) << 32 : 0);
+                st = query_status(im, r.y, r.z, r.w, &M, &N, &K);
             }
             y2M[j] = 2u * (M - 1u);
             y2N[j] = 2u * (N - 1u);
@@ -186,6 +195,13 @@ __global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const
         uint32_t row[4] = {0, 0, 0, 0};
         double gd[4] = {0, 0, 0, 0}, ld[4] = {0, 0, 0, 0};
         bool uni = false;
+        {
+            uint64_t g;
+            const uint32_t r = __shfl_sync(0xffffffffu, row_for(im, y2M[0], y2N[0], Ms[0], &g), 0);
+            int4 R0, R1;
+            issue(0, r, R0, R1);
+            commit(0, 0, R0, R1);
+        }
         for (int s = 0; s < im.nseg; ++s) {
             const uint4 mg = Ms[s];
             const int pos = Ps[s];
@@ -210,12 +226,22 @@ __global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const
 #pragma unroll
                 for (int j = 0; j < 4; ++j) ld[j] = u32_to_f64(mdiv2(y2K[j], mg.z, sk) + 1u);
             }
+            const bool ahead = s + 1 < im.nseg;
+            int4 R0 = make_int4(0, 0, 0, 0), R1 = R0;
+            if (ahead) {
+                const uint4 mn = Ms[s + 1];
+                uint32_t rn = row[0];
+                if (mn.x != pm || mn.y != pn || (mn.w & 0xffffu) != ps) {
+                    uint64_t g;
+                    rn = row_for(im, y2M[0], y2N[0], mn, &g);
+                }
+                issue(s + 1, __shfl_sync(0xffffffffu, rn, 0), R0, R1);
+            }
             double sb[4] = {kInf3, kInf3, kInf3, kInf3};
             int sj[4] = {-1, -1, -1, -1};
             if (uni) {
                 // one broadcast row per config ([row][class position] layout:
                 // the segment's configs are contiguous), reused by 4 queries
-                const double4* p = im.theta2t + size_t(row[0]) * C + pos;
                 const uint32_t* pmeta = im.meta2t + size_t(row[0]) * C + pos;
                 auto eval1 = [&](const double4& th, int c) {
                     double tt[4], u[4], v[4];
@@ -245,20 +271,9 @@ __global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const
                         for (int j = 0; j < 4; ++j) acc[j] |= mm;
                     }
                 };
-                // ping-pong buffers: the next pair of rows is in flight while
-                // the current pair is evaluated
-                double4 a0 = ldg_row(p), a1 = ncfg > 1 ? ldg_row(p + 1) : a0;
-                int c = 0;
-                for (; c + 1 < ncfg; c += 2) {
-                    double4 b0 = a0, b1 = a1;
-                    if (c + 2 < ncfg) b0 = ldg_row(p + c + 2);
-                    if (c + 3 < ncfg) b1 = ldg_row(p + c + 3);
-                    eval1(a0, c);
-                    eval1(a1, c + 1);
-                    a0 = b0;
-                    a1 = b1;
-                }
-                if (c < ncfg) eval1(a0, c);
+                const double4* sp = myrows + (s & 1) * kSegCfg;
+#pragma unroll 2
+                for (int c = 0; c < ncfg; ++c) eval1(sp[c], c);
             } else {
                 for (int c = 0; c < ncfg; ++c) {
                     double4 th[4];
@@ -291,6 +306,7 @@ __global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const
                     bp[j] = cand;
                 }
             }
+            if (ahead) commit((s + 1) & 1, s + 1, R0, R1);
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -338,10 +354,23 @@ size_t eval3_scratch_bytes(int64_t n) {
     cub::DeviceScan::ExclusiveSum(nullptr, scan, static_cast<const uint32_t*>(nullptr),
                                   static_cast<uint32_t*>(nullptr), int(nb));
     const size_t un = size_t(std::max<int64_t>(n, 1));
-    return al256(nb * 4) * 2 + al256(un * 4) + al256(un * 8) + 3 * al256(un * 4) + al256(scan);
+    return al256(nb * 4) * 2 + al256(un * 4) + al256(un * 16) + al256(un * 4) + al256(scan);
 }
 
-cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, cudaStream_t st) {
+Eval3Bufs eval3_bufs(void* scratch, int64_t n) {
+    Eval3Bufs b;
+    const size_t nb = size_t(1) << (key_bits() + kSpreadBits);
+    const size_t un = size_t(std::max<int64_t>(n, 1));
+    char* p = static_cast<char*>(scratch);
+    b.hist = reinterpret_cast<uint32_t*>(p);
+    b.keys = reinterpret_cast<uint32_t*>(p + 2 * al256(nb * 4));
+    (void)un;
+    b.key_bits = key_bits();
+    b.hist_bytes = nb * 4;
+    return b;
+}
+
+cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, bool keys_ready, cudaStream_t st) {
     const int bits = key_bits();
     const size_t nb = size_t(1) << (bits + kSpreadBits);
     const size_t un = size_t(std::max<int64_t>(a.n, 1));
@@ -352,13 +381,9 @@ cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, c
     p += al256(nb * 4);
     uint32_t* keys = reinterpret_cast<uint32_t*>(p);
     p += al256(un * 4);
-    int64_t* sq = reinterpret_cast<int64_t*>(p);
-    p += al256(un * 8);
-    int32_t* sM = reinterpret_cast<int32_t*>(p);
-    p += al256(un * 4);
-    int32_t* sN = reinterpret_cast<int32_t*>(p);
-    p += al256(un * 4);
-    int32_t* sK = reinterpret_cast<int32_t*>(p);
+    int4* rec = reinterpret_cast<int4*>(p);
+    p += al256(un * 16);
+    int32_t* qhi = a.n >= (int64_t(1) << 31) ? reinterpret_cast<int32_t*>(p) : nullptr;
     p += al256(un * 4);
     void* tmp = p;
 
@@ -375,21 +400,26 @@ cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, c
     // grids: enough CTAs for n (host upper bound), capped at a few waves
     const int64_t want = (a.n + kT3 - 1) / kT3;
     const int gk = int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(sms) * 8)));
-    cudaError_t e = cudaMemsetAsync(hist, 0, nb * 4, st);
-    if (e != cudaSuccess) return e;
-    k_ekey<<<gk, kT3, 0, st>>>(im, a, bits, keys, hist);
+    cudaError_t e = cudaSuccess;
+    if (!keys_ready) {
+        e = cudaMemsetAsync(hist, 0, nb * 4, st);
+        if (e != cudaSuccess) return e;
+        k_ekey<<<gk, kT3, 0, st>>>(im, a, bits, keys, hist);
+    }
     size_t sb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, sb, hist, offs, int(nb), st);
     e = cub::DeviceScan::ExclusiveSum(tmp, sb, hist, offs, int(nb), st);
     if (e != cudaSuccess) return e;
-    k_escatter<<<gk, kT3, 0, st>>>(a, keys, offs, sq, sM, sN, sK);
+    const int gs = int(std::max<int64_t>(1, std::min<int64_t>((a.n + kT3 * kScPer - 1) / (kT3 * kScPer),
+                                                              int64_t(sms) * 4)));
+    k_escatter<<<gs, kT3, 0, st>>>(a, keys, offs, rec, qhi);
     const int64_t want3 = (a.n + 4 * kT3 - 1) / (4 * kT3);
     if (im.special) {
         const int g3 = int(std::max<int64_t>(1, std::min<int64_t>(want3, int64_t(sms) * occs)));
-        k_eval3<true><<<g3, kT3, 0, st>>>(im, a, sq, sM, sN, sK);
+        k_eval3<true><<<g3, kT3, 0, st>>>(im, a, rec, qhi);
     } else {
         const int g3 = int(std::max<int64_t>(1, std::min<int64_t>(want3, int64_t(sms) * occ)));
-        k_eval3<false><<<g3, kT3, 0, st>>>(im, a, sq, sM, sN, sK);
+        k_eval3<false><<<g3, kT3, 0, st>>>(im, a, rec, qhi);
     }
     return cudaGetLastError();
 }
