@@ -312,6 +312,13 @@ wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_
  * this library in this process. */
 int64_t wt_launch_count(void);
 
+/* Per-kernel timing for benchmarks.  While enabled, wt_gather_batch records
+ * CUDA events on its stream around (0) the gather kernel and (1) the
+ * off-grid evaluation that follows it; wt_kernel_time_ms returns the
+ * elapsed time of the most recent call (waits for its events). */
+wt_status wt_set_kernel_timing(int enable);
+wt_status wt_kernel_time_ms(int which, float* ms);
+
 /* ---- batched fit / dual-table build (K2) --------------------------------- */
 
 /* ProfileRecord SoA (profiler.hpp:56-63), host arrays. */

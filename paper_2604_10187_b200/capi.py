@@ -96,7 +96,7 @@ EXPORTS = (
     "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_destroy wt_grid_storage wt_sweep wt_grid_finalize "
     "wt_gather_batch wt_decide_host_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
     "wt_simulate_batch wt_profile_sim wt_tune_one wt_engine_set_resident wt_baseline_create "
-    "wt_baseline_destroy wt_baseline_tune_batch wt_baseline_predict_batch").split()
+    "wt_baseline_destroy wt_baseline_tune_batch wt_baseline_predict_batch wt_set_kernel_timing wt_kernel_time_ms").split()
 
 _lib = None
 
@@ -119,6 +119,19 @@ def lib():
 def check(st):
     if st != WT_OK:
         raise WtError(st, lib().wt_last_error().decode())
+
+
+def set_kernel_timing(on: bool):
+    """Record CUDA events around the gather kernel / off-grid evaluation of
+    every wt_gather_batch call (benchmarking)."""
+    check(lib().wt_set_kernel_timing(1 if on else 0))
+
+
+def kernel_time_ms(which: int) -> float:
+    """Elapsed ms of the last timed call: 0 = gather kernel, 1 = off-grid evaluation."""
+    ms = C.c_float()
+    check(lib().wt_kernel_time_ms(which, C.byref(ms)))
+    return ms.value
 
 
 def launch_count():

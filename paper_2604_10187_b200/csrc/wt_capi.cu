@@ -142,7 +142,34 @@ struct wt_grid {
     RunIndex runs{};        // run-compressed heads (k_gather_h); budget 0 = none
 };
 
+namespace {
+std::atomic<int> g_timing{0};
+cudaEvent_t g_tev[4] = {};
+bool g_tev_used = false;
+void timing_mark(int i, cudaStream_t s) {
+    if (!g_timing.load()) return;
+    if (!g_tev[i]) cudaEventCreate(&g_tev[i]);
+    cudaEventRecord(g_tev[i], s);
+    g_tev_used = true;
+}
+}  // namespace
+
 extern "C" {
+
+wt_status wt_set_kernel_timing(int enable) {
+    g_timing.store(enable ? 1 : 0);
+    return WT_OK;
+}
+
+wt_status wt_kernel_time_ms(int which, float* ms) {
+    if (!ms || which < 0 || which > 1) return set_err(WT_INVALID_ARGUMENT, "which must be 0 or 1");
+    if (!g_tev_used || !g_tev[2 * which] || !g_tev[2 * which + 1])
+        return set_err(WT_RUNTIME_ERROR, "no timed call recorded");
+    cudaError_t ce = cudaEventSynchronize(g_tev[2 * which + 1]);
+    if (ce == cudaSuccess) ce = cudaEventElapsedTime(ms, g_tev[2 * which], g_tev[2 * which + 1]);
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_kernel_time_ms");
+    return WT_OK;
+}
 
 const char* wt_last_error(void) { return g_err.c_str(); }
 const char* wt_version(void) { return "wavetune-b200 0.1 (sm_100a)"; }
@@ -958,7 +985,10 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
     }
     const int grid = int(std::min<int64_t>((n + kGatherThreads - 1) / kGatherThreads,
                                            int64_t(sm_count(e->device)) * 8));
+    timing_mark(0, s);
     ce = launch_gather(e->dev, a, grid, s);
+    timing_mark(1, s);
+    timing_mark(2, s);
     g_launches++;
     if (ce == cudaSuccess) {
         EvalArgs ea{};
@@ -984,6 +1014,7 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
             ce = run_list_eval(e, ea, s, escratch);
         }
     }
+    timing_mark(3, s);
     cudaFreeAsync(scratch, s);
     if (escratch) cudaFreeAsync(escratch, s);
     if (ce != cudaSuccess) return cuda_err(ce, "wt_gather_batch");

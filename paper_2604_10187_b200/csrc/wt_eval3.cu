@@ -120,14 +120,14 @@ __global__ void __launch_bounds__(kT3) k_escatter(EvalArgs a, const uint32_t* ke
 }
 
 // ------------------------------------------------------------------ eval
-template <bool SPECIAL>
+template <bool SPECIAL, bool HS>
 __global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const int4* rec, const int32_t* qhi) {
     // segment headers in shared memory (broadcast LDS instead of dependent
     // global loads at every segment start)
     __shared__ int4 h_tiles[kMaxSmemSeg];
     __shared__ uint4 h_magic[kMaxSmemSeg];
     __shared__ int32_t h_pos[kMaxSmemSeg];
-    const bool hs = im.nseg <= kMaxSmemSeg;
+    constexpr bool hs = HS;  // nseg <= kMaxSmemSeg: headers from shared memory
     if (hs) {
         for (int i = threadIdx.x; i < im.nseg; i += blockDim.x) {
             h_tiles[i] = im.seg_tiles[i];
@@ -392,8 +392,8 @@ cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, b
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval3<false>, kT3, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs, k_eval3<true>, kT3, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval3<false, true>, kT3, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs, k_eval3<true, true>, kT3, 0);
         occ = std::max(occ, 1);
         occs = std::max(occs, 1);
     }
@@ -414,13 +414,12 @@ cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, b
                                                               int64_t(sms) * 4)));
     k_escatter<<<gs, kT3, 0, st>>>(a, keys, offs, rec, qhi);
     const int64_t want3 = (a.n + 4 * kT3 - 1) / (4 * kT3);
-    if (im.special) {
-        const int g3 = int(std::max<int64_t>(1, std::min<int64_t>(want3, int64_t(sms) * occs)));
-        k_eval3<true><<<g3, kT3, 0, st>>>(im, a, rec, qhi);
-    } else {
-        const int g3 = int(std::max<int64_t>(1, std::min<int64_t>(want3, int64_t(sms) * occ)));
-        k_eval3<false><<<g3, kT3, 0, st>>>(im, a, rec, qhi);
-    }
+    const bool hs = im.nseg <= kMaxSmemSeg;
+    const int g3 = int(std::max<int64_t>(1, std::min<int64_t>(want3, int64_t(sms) * (im.special ? occs : occ))));
+    if (im.special)
+        hs ? k_eval3<true, true><<<g3, kT3, 0, st>>>(im, a, rec, qhi) : k_eval3<true, false><<<g3, kT3, 0, st>>>(im, a, rec, qhi);
+    else
+        hs ? k_eval3<false, true><<<g3, kT3, 0, st>>>(im, a, rec, qhi) : k_eval3<false, false><<<g3, kT3, 0, st>>>(im, a, rec, qhi);
     return cudaGetLastError();
 }
 

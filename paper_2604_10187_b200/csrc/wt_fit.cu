@@ -764,6 +764,12 @@ namespace {
 thread_local cudaStream_t t_alloc_stream = nullptr;
 thread_local cudaMemPool_t t_alloc_pool = nullptr;
 
+// cub temporaries: the library pool too (the default pool releases its
+// memory at every synchronisation and re-maps it on the next allocation)
+cudaError_t talloc(void** p, size_t bytes, cudaStream_t s) {
+    return t_alloc_pool ? cudaMallocFromPoolAsync(p, bytes, t_alloc_pool, s) : cudaMallocAsync(p, bytes, s);
+}
+
 template <typename T>
 T* dalloc(std::vector<void*>& owned, size_t n) {
     void* p = nullptr;
@@ -822,7 +828,7 @@ wt_status run_sort(const Rec& rc, const int32_t* mpos, int64_t* perm, int64_t* p
                                         std::max(1, ps.bits), s);
         if (need > tmp_bytes) {
             if (tmp) cudaFreeAsync(tmp, s);
-            CK(cudaMallocAsync(&tmp, need, s));
+            CK(talloc(&tmp, need, s));
             tmp_bytes = need;
         }
         CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_alt, perm, perm_alt, n, 0,
@@ -937,7 +943,7 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
         size_t need = 0;
         cub::DeviceSelect::Flagged(nullptr, need, it, valid, idx, nvalid_d, n_all, s);
         void* t = nullptr;
-        CK(cudaMallocAsync(&t, need, s));
+        CK(talloc(&t, need, s));
         CK(cub::DeviceSelect::Flagged(t, need, it, valid, idx, nvalid_d, n_all, s));
         cudaFreeAsync(t, s);
     }
@@ -993,7 +999,7 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
         size_t need = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, need, gflag, gid, n, s);
         void* t = nullptr;
-        CK(cudaMallocAsync(&t, need, s));
+        CK(talloc(&t, need, s));
         CK(cub::DeviceScan::ExclusiveSum(t, need, gflag, gid, n, s));
         cudaFreeAsync(t, s);
     }
@@ -1019,7 +1025,7 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
         size_t need = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, need, wid, soff, G, s);
         void* t = nullptr;
-        CK(cudaMallocAsync(&t, need, s));
+        CK(talloc(&t, need, s));
         CK(cub::DeviceScan::ExclusiveSum(t, need, wid, soff, G, s));
         cudaFreeAsync(t, s);
     }
@@ -1038,7 +1044,7 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
         size_t need = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, need, in, out, G, s);
         void* t = nullptr;
-        CK(cudaMallocAsync(&t, need, s));
+        CK(talloc(&t, need, s));
         CK(cub::DeviceScan::ExclusiveSum(t, need, in, out, G, s));
         cudaFreeAsync(t, s);
     }
