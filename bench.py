@@ -362,8 +362,9 @@ def run_wavetune(args):
             "config1_sweep": {"ms": sweep_ms, "evals": grid.n_entries * eng.n_configs,
                               "evals_per_s": grid.n_entries * eng.n_configs / (sweep_ms * 1e-3)},
             "config3_sweep": {"ms": ms3, "evals": evals3, "evals_per_s": evals3 / (ms3 * 1e-3),
-                              "fp64_flop_per_s": 7.0 * evals3 / (ms3 * 1e-3),
-                              "fp64_frac_of_18.6TF": 7.0 * evals3 / (ms3 * 1e-3) / 18.6e12,
+                              "evals_note": "(shape, config) pairs decided per second; configs proven "
+                                            "dominated in a (wave row, L bucket) cell are skipped "
+                                            "(exact pruning, WT_PRUNE=0 evaluates all)",
                               "shapes": g3.n_entries, "configs": eng3.n_configs,
                               "sharding": f"shape slices x{ws} + NCCL all_gather" if ws > 1 else "single GPU"},
             "config4_fit": {"ms": fit_ms, "records": int(len(rec4["g"])), "tables": int(fit["n_tables"]),

@@ -199,7 +199,7 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
     const size_t NS = h.seg_pos.size();
     size_t o_st = ar.take(NS * 16), o_sm = ar.take(NS * 16), o_sp = ar.take(NS * 4), o_cc = ar.take(C * 4),
            o_th2 = ar.take(C * R * 32), o_m2 = ar.take(C * R * 4), o_th2t = ar.take(C * R * 32),
-           o_m2t = ar.take(C * R * 4);
+           o_m2t = ar.take(C * R * 4), o_smask = ar.take(NS * R * kLB * 4), o_sor = ar.take(NS * R * 4);
     cudaError_t ce = cudaMalloc(&e->mem, ar.used);
     if (ce != cudaSuccess) {
         delete e;
@@ -222,6 +222,7 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
         {o_sp, h.seg_pos.data(), NS * 4},         {o_cc, h.cls_cfg.data(), C * 4},
         {o_th2, h.theta2.data(), C * R * 32},     {o_m2, h.meta2.data(), C * R * 4},
         {o_th2t, h.theta2t.data(), C * R * 32},   {o_m2t, h.meta2t.data(), C * R * 4},
+        {o_smask, h.segmask.data(), NS * R * kLB * 4}, {o_sor, h.segor.data(), NS * R * 4},
     };
     for (const Piece& p : pieces) {
         ce = cudaMemcpy(base + p.off, p.src, p.n, cudaMemcpyHostToDevice);
@@ -262,6 +263,13 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
     d.meta2 = reinterpret_cast<const uint32_t*>(base + o_m2);
     d.theta2t = reinterpret_cast<const double4*>(base + o_th2t);
     d.meta2t = reinterpret_cast<const uint32_t*>(base + o_m2t);
+    d.segmask = reinterpret_cast<const uint32_t*>(base + o_smask);
+    d.segor = reinterpret_cast<const uint32_t*>(base + o_sor);
+    static const int prune = [] {
+        const char* v = std::getenv("WT_PRUNE");
+        return v ? std::atoi(v) : 1;
+    }();
+    d.prune = prune;
     // list-mode chunk: keep the staged rows near 40 KB so several CTAs fit per SM
     e->eval_chunk = int(std::max<size_t>(1, std::min<size_t>(C, 40960 / (R * 36 + 32))));
     e->eval_grid = sm_count(device) * 4;
@@ -982,6 +990,7 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
         a.off_key = b.keys;
         a.key_hist = b.hist;
         a.key_bits = b.key_bits;
+        a.key_mode = b.key_mode;
     }
     const int grid = int(std::min<int64_t>((n + kGatherThreads - 1) / kGatherThreads,
                                            int64_t(sm_count(e->device)) * 8));

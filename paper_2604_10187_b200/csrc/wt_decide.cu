@@ -441,7 +441,7 @@ __device__ __forceinline__ void wbuf_drain(WarpBuf& b, int& wcnt, const GatherAr
         a.off_N[base + i] = b.n[i];
         a.off_K[base + i] = b.k[i];
         if (im && a.off_key) {
-            const uint32_t key = eval_key(*im, b.m[i], b.n[i], b.k[i], a.key_bits, int64_t(base + i));
+            const uint32_t key = eval_key(*im, b.m[i], b.n[i], b.k[i], a.key_bits, int64_t(base + i), a.key_mode);
             a.off_key[base + i] = key;
             atomicAdd(a.key_hist + key, 1u);
         }

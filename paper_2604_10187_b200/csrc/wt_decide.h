@@ -113,6 +113,7 @@ struct GatherArgs {
     uint32_t* off_key;
     uint32_t* key_hist;
     int32_t key_bits;
+    int32_t key_mode;
 };
 
 // slot of (N, K) in a 2^bits table: multiplicative hash, high bits
@@ -230,6 +231,7 @@ struct Eval3Bufs {
     uint32_t* hist;  // 2^(key_bits + spread) bucket counters
     uint32_t* keys;  // per list slot
     int32_t key_bits;
+    int32_t key_mode;
     size_t hist_bytes;
 };
 Eval3Bufs eval3_bufs(void* scratch, int64_t n);

@@ -43,7 +43,7 @@ struct SegHdr {  // one staged segment
     uint32_t mM, sM, nt, rowlo;
     int32_t ncfg, pos, off, stride;
     double ld;
-    uint32_t mN, mK, pad0, pad1;
+    uint32_t mN, mK, seg, lb;  // segment index, L bucket (sweep: one K per tile)
 };
 
 __device__ __forceinline__ bool lex_less(double a, int ia, double b, int ib) {
@@ -138,6 +138,8 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
                 h.off = off;
                 h.stride = need / max(st.w, 1);  // rows of this segment in the tile
                 h.ld = u32_to_f64(lk);
+                h.seg = uint32_t(s);
+                h.lb = uint32_t(min(31 - __clz(int(lk)), kLB - 1));
                 hdr[tid] = h;
             }
             __syncthreads();
@@ -161,7 +163,7 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
                 const double4* pr[RPT];
                 const uint32_t* pm[RPT];
                 double gd[RPT], sb[RPT];
-                int sj[RPT];
+                int sj[RPT], rr[RPT];
 #pragma unroll
                 for (int j = 0; j < RPT; ++j) {
                     const uint32_t q = mdiv2(y2[j], h.mM, h.sM);
@@ -176,14 +178,31 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
                         gd[j] = u32_to_f64(g);
                     }
                     const int r = int(row_of(gc, mS, sS) - h.rowlo);
+                    rr[j] = r;
                     pr[j] = rows + h.off + r * h.ncfg;
                     pm[j] = meta + h.off + r * h.ncfg;
                     sb[j] = kInf;
                     sj[j] = -1;
                 }
                 const double ld = h.ld;
-#pragma unroll 2
-                for (int c = 0; c < h.ncfg; ++c) {
+                // exact pruning: configs beaten everywhere in the (row, L
+                // bucket) cells of this warp's shapes are skipped
+                uint32_t live = 0xffffffffu;
+                if (im.prune) {
+                    live = 0;
+                    const uint32_t* mk = im.segmask + size_t(h.seg) * R * kLB + h.lb;
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) live |= __ldg(mk + (h.rowlo + uint32_t(rr[j])) * kLB);
+                    live = __reduce_or_sync(0xffffffffu, live);
+                }
+                live &= h.ncfg >= 32 ? 0xffffffffu : ((1u << h.ncfg) - 1u);
+                if constexpr (SPECIAL) {
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j)
+                        acc[j] |= __ldg(im.segor + size_t(h.seg) * R + h.rowlo + uint32_t(rr[j]));
+                }
+                for (uint32_t mm = live; mm; mm &= mm - 1u) {
+                    const int c = __ffs(int(mm)) - 1;
                     double4 th[RPT];
                     double t[RPT], u[RPT];
 #pragma unroll
@@ -206,7 +225,6 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
                             sb[j] = t[j];
                             sj[j] = c;
                         }
-                        if constexpr (SPECIAL) acc[j] |= pm[j][c];
                     }
                 }
 #pragma unroll

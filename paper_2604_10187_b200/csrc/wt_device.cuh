@@ -197,7 +197,7 @@ __device__ __forceinline__ void write_decision(const DecOut& o, int64_t q, const
 }
 
 // ---- list-mode grouping key (wt_eval3.cu)
-constexpr int kSpreadBits = 3;
+constexpr int kSpreadBits = 2;
 
 // Per-query validity exactly as k_eval2 (kernel_map.cpp:238-239 + the
 // 32-bit wave guard); invalid queries evaluate as (1, 1, 1) and are flagged.
@@ -223,20 +223,20 @@ __device__ __forceinline__ uint32_t row_for(const DevImage& im, uint32_t y2M, ui
     return row_of(gc, im.mS, im.sS);
 }
 
-// Grouping key of a query: the wave rows of the first and the last tile
-// class (a prefix, so neighbouring groups are similar) + a hash of the rows
-// of every distinct (t_m, t_n); `bits` wide, then kSpreadBits sub-bucket bits
-// from the list slot (spreads the atomics of large groups; the sub-buckets
-// of one key stay adjacent after the scan).
+// Grouping key of a query (list evaluation, wt_eval3.cu): the wave row of
+// the last tile class (a prefix, so neighbouring groups are similar), the
+// bucket floor(log2 K) (the pruning masks are per L bucket) and a hash of
+// the rows of every distinct (t_m, t_n); `bits` wide, then kSpreadBits
+// sub-bucket bits from the list slot (spreads the atomics of large groups;
+// the sub-buckets of one key stay adjacent after the scan).
+// mode 0: rows of the first and the last class + hash (no K bucket).
 __device__ __forceinline__ uint32_t eval_key(const DevImage& im, int32_t m, int32_t n, int32_t k, int bits,
-                                             int64_t slot) {
+                                             int64_t slot, int mode = 1) {
     uint32_t M, N, K;
     uint32_t key = 0;
     if (!query_status(im, m, n, k, &M, &N, &K)) {
         int br = 1;
         while ((1 << br) < im.R) ++br;
-        const int pre = (2 * br + 4 <= bits) ? 2 : (br + 4 <= bits ? 1 : 0);
-        const int hb = bits - pre * br;
         const uint32_t y2M = 2u * (M - 1u), y2N = 2u * (N - 1u);
         uint32_t h = 0x811c9dc5u, first = 0, last = 0, pm = 0, pn = 0, ps = 0xffffffffu;
         for (int s = 0; s < im.nseg; ++s) {
@@ -246,18 +246,19 @@ __device__ __forceinline__ uint32_t eval_key(const DevImage& im, int32_t m, int3
             pn = mg.y;
             ps = mg.w & 0xffffu;
             uint64_t g;
-            const uint32_t r = row_for(im, y2M, y2N, mg, &g);
-            if (s == 0) first = r;
-            last = r;
-            h = (h ^ r) * 0x01000193u;
+            last = row_for(im, y2M, y2N, mg, &g);
+            if (s == 0) first = last;
+            h = (h ^ last) * 0x01000193u;
         }
         h ^= h >> 15;
         h *= 0x2c1b3c6du;
         h ^= h >> 12;
-        if (pre == 2)
-            key = (first << (bits - br)) | (last << (bits - 2 * br)) | (h & ((1u << hb) - 1u));
-        else if (pre == 1)
-            key = (first << (bits - br)) | (h & ((1u << hb) - 1u));
+        const uint32_t kb = uint32_t(31 - __clz(int(K)));  // 0..30
+        const int hb = bits - br - 5;
+        if (mode == 0 && bits - 2 * br >= 2)
+            key = (first << (bits - br)) | (last << (bits - 2 * br)) | (h & ((1u << (bits - 2 * br)) - 1u));
+        else if (hb >= 2)
+            key = (last << (bits - br)) | (kb << hb) | (h & ((1u << hb) - 1u));
         else
             key = h & ((1u << bits) - 1u);
     }

@@ -50,12 +50,12 @@ __device__ __forceinline__ bool lex_less3(double a, int ia, double b, int ib) {
 }  // namespace
 
 // ------------------------------------------------------------------ keys
-__global__ void k_ekey(DevImage im, EvalArgs a, int bits, uint32_t* keys, uint32_t* hist) {
+__global__ void k_ekey(DevImage im, EvalArgs a, int bits, int mode, uint32_t* keys, uint32_t* hist) {
     const int64_t n = a.count ? *a.count : a.n;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
         const int64_t src = a.inputs_compact ? i : (a.idx ? a.idx[i] : i);
-        const uint32_t key = eval_key(im, a.M[src], a.N[src], a.K[src], bits, i);
+        const uint32_t key = eval_key(im, a.M[src], a.N[src], a.K[src], bits, i, mode);
         keys[i] = key;
         atomicAdd(hist + key, 1u);
     }
@@ -194,15 +194,18 @@ __global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const
         uint32_t pm = 0, pn = 0, ps = 0xffffffffu, pk = 0, psk = 0xffffffffu;
         uint32_t row[4] = {0, 0, 0, 0};
         double gd[4] = {0, 0, 0, 0}, ld[4] = {0, 0, 0, 0};
+        uint32_t lbp = 0;  // the 4 queries' L buckets, 8 bits each
         bool uni = false;
+        const int s_first = 0;
         {
             uint64_t g;
-            const uint32_t r = __shfl_sync(0xffffffffu, row_for(im, y2M[0], y2N[0], Ms[0], &g), 0);
+            const uint32_t r = __shfl_sync(0xffffffffu, row_for(im, y2M[0], y2N[0], Ms[s_first], &g), 0);
             int4 R0, R1;
-            issue(0, r, R0, R1);
-            commit(0, 0, R0, R1);
+            issue(s_first, r, R0, R1);
+            commit(0, s_first, R0, R1);
         }
-        for (int s = 0; s < im.nseg; ++s) {
+        for (int s = s_first, stage = 0; s < im.nseg; stage ^= 1) {
+            const int s_next = s + 1;
             const uint4 mg = Ms[s];
             const int pos = Ps[s];
             const int ncfg = Ts[s].w;
@@ -223,26 +226,44 @@ __global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const
             if (mg.z != pk || sk != psk) {
                 pk = mg.z;
                 psk = sk;
+                lbp = 0;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) ld[j] = u32_to_f64(mdiv2(y2K[j], mg.z, sk) + 1u);
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t L = mdiv2(y2K[j], mg.z, sk) + 1u;
+                    ld[j] = u32_to_f64(L);
+                    lbp |= uint32_t(min(31 - __clz(int(L)), kLB - 1)) << (8 * j);
+                }
             }
-            const bool ahead = s + 1 < im.nseg;
+            // configs that can still win for the warp's (row, L bucket) cells
+            uint32_t live = 0xffffffffu;
+            if (im.prune) {
+                live = 0;
+                const uint32_t* mk = im.segmask + size_t(s) * im.R * kLB;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) live |= __ldg(mk + row[j] * kLB + ((lbp >> (8 * j)) & 0xffu));
+                live = __reduce_or_sync(0xffffffffu, live);
+            }
+            live &= ncfg >= 32 ? 0xffffffffu : ((1u << ncfg) - 1u);
+            if constexpr (SPECIAL) {  // flags of every config count, evaluated or not
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[j] |= __ldg(im.segor + size_t(s) * im.R + row[j]);
+            }
+            const bool ahead = s_next < im.nseg;
             int4 R0 = make_int4(0, 0, 0, 0), R1 = R0;
             if (ahead) {
-                const uint4 mn = Ms[s + 1];
+                const uint4 mn = Ms[s_next];
                 uint32_t rn = row[0];
                 if (mn.x != pm || mn.y != pn || (mn.w & 0xffffu) != ps) {
                     uint64_t g;
                     rn = row_for(im, y2M[0], y2N[0], mn, &g);
                 }
-                issue(s + 1, __shfl_sync(0xffffffffu, rn, 0), R0, R1);
+                issue(s_next, __shfl_sync(0xffffffffu, rn, 0), R0, R1);
             }
             double sb[4] = {kInf3, kInf3, kInf3, kInf3};
             int sj[4] = {-1, -1, -1, -1};
             if (uni) {
                 // one broadcast row per config ([row][class position] layout:
                 // the segment's configs are contiguous), reused by 4 queries
-                const uint32_t* pmeta = im.meta2t + size_t(row[0]) * C + pos;
                 auto eval1 = [&](const double4& th, int c) {
                     double tt[4], u[4], v[4];
 #pragma unroll
@@ -265,17 +286,16 @@ __global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const
                             sb[j] = tt[j];
                             sj[j] = c;
                         }
-                    if constexpr (SPECIAL) {
-                        const uint32_t mm = __ldg(pmeta + c);
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) acc[j] |= mm;
-                    }
                 };
-                const double4* sp = myrows + (s & 1) * kSegCfg;
-#pragma unroll 2
-                for (int c = 0; c < ncfg; ++c) eval1(sp[c], c);
+                const double4* sp = myrows + stage * kSegCfg;
+                // ascending config order: the strict-< scan keeps its meaning
+                for (uint32_t mm = live; mm; mm &= mm - 1u) {
+                    const int c = __ffs(int(mm)) - 1;
+                    eval1(sp[c], c);
+                }
             } else {
-                for (int c = 0; c < ncfg; ++c) {
+                for (uint32_t mm = live; mm; mm &= mm - 1u) {
+                    const int c = __ffs(int(mm)) - 1;
                     double4 th[4];
 #pragma unroll
                     for (int j = 0; j < 4; ++j) th[j] = ldg_row(im.theta2t + size_t(row[j]) * C + pos + c);
@@ -289,7 +309,6 @@ __global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const
                             sb[j] = tt;
                             sj[j] = c;
                         }
-                        if constexpr (SPECIAL) acc[j] |= __ldg(im.meta2t + size_t(row[j]) * C + pos + c);
                     }
                 }
             }
@@ -306,7 +325,8 @@ __global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const
                     bp[j] = cand;
                 }
             }
-            if (ahead) commit((s + 1) & 1, s + 1, R0, R1);
+            if (ahead) commit(stage ^ 1, s_next, R0, R1);
+            s = s_next;
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -346,6 +366,13 @@ int key_bits() {
     return b;
 }
 size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
+int key_mode() {
+    static const int m = [] {
+        const char* v = std::getenv("WT_EVAL_KEY_MODE");
+        return v ? std::atoi(v) : 1;
+    }();
+    return m;
+}
 }  // namespace
 
 size_t eval3_scratch_bytes(int64_t n) {
@@ -366,6 +393,7 @@ Eval3Bufs eval3_bufs(void* scratch, int64_t n) {
     b.keys = reinterpret_cast<uint32_t*>(p + 2 * al256(nb * 4));
     (void)un;
     b.key_bits = key_bits();
+    b.key_mode = key_mode();
     b.hist_bytes = nb * 4;
     return b;
 }
@@ -404,7 +432,7 @@ cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, b
     if (!keys_ready) {
         e = cudaMemsetAsync(hist, 0, nb * 4, st);
         if (e != cudaSuccess) return e;
-        k_ekey<<<gk, kT3, 0, st>>>(im, a, bits, keys, hist);
+        k_ekey<<<gk, kT3, 0, st>>>(im, a, bits, key_mode(), keys, hist);
     }
     size_t sb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, sb, hist, offs, int(nb), st);

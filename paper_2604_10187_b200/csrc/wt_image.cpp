@@ -16,6 +16,7 @@
 //     extrapolated else w), ties to the smaller wave.
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdlib>
 #include <map>
 #include <numeric>
@@ -30,6 +31,116 @@ namespace {
 wt_status fail(std::string* err, wt_status st, const std::string& msg) {
     *err = msg;
     return st;
+}
+
+}  // namespace
+
+namespace {
+
+// Dominance test for the pruning masks.  d(G, L) = f_v - f_d - eps * (S_v + S_d)
+// with f = alpha*G*L + beta*G + gamma*L + delta and S the same with absolute
+// coefficients (a bound on the magnitude every fp64 rounding error of the
+// evaluation scales with): d is bilinear, so d > 0 on a rectangle (possibly
+// unbounded in G and/or L) iff it holds at the finite corners and the slopes
+// along the unbounded directions are >= 0.  eps = 1e-9 is ~10^6 times the
+// worst-case relative rounding error of the 7-operation evaluation, so
+// d > 0 implies fl(f_v) > fl(f_d): the victim can neither win nor tie.
+bool dominated_by(const double* v, const double* d, long double G0, long double G1, bool ginf, long double L0,
+                  long double L1, bool linf) {
+    for (int q = 0; q < 4; ++q)
+        if (!std::isfinite(v[q]) || !std::isfinite(d[q])) return false;
+    const long double eps = 1e-9L;
+    long double k[4];
+    for (int q = 0; q < 4; ++q)
+        k[q] = (long double)v[q] - (long double)d[q] - eps * (std::fabs((long double)v[q]) + std::fabs((long double)d[q]));
+    const long double a = k[0], b = k[1], c = k[2], e = k[3];
+    auto val = [&](long double G, long double L) { return a * G * L + b * G + c * L + e; };
+    if (!(val(G0, L0) > 0)) return false;
+    if (linf ? !(a * G0 + c >= 0) : !(val(G0, L1) > 0)) return false;
+    if (ginf) {
+        if (!(a * L0 + b >= 0)) return false;
+        if (linf ? !(a >= 0) : !(a * L1 + b >= 0)) return false;
+    } else {
+        if (!(val(G1, L0) > 0)) return false;
+        if (linf ? !(a * G1 + c >= 0) : !(val(G1, L1) > 0)) return false;
+    }
+    return true;
+}
+
+// Masks for every (segment, row, L bucket): a config is dropped when one of
+// the class's per-corner leaders (the configs with the smallest value at the
+// rectangle's four corners, unbounded sides sampled far out) dominates it.
+void build_prune_masks(HostImage& im) {
+    const int32_t R = im.R, NS = int32_t(im.seg_pos.size()), C = im.C;
+    const uint32_t S = uint32_t(im.S);
+    im.segmask.assign(size_t(NS) * R * kLB, 0u);
+    im.segor.assign(size_t(NS) * R, 0u);
+    // classes = runs of segments with equal (t_m, t_n, t_k)
+    std::vector<int32_t> cls_of(NS);
+    for (int32_t s = 0, k = -1; s < NS; ++s) {
+        if (s == 0 || im.seg_tiles[4 * s] != im.seg_tiles[4 * (s - 1)] ||
+            im.seg_tiles[4 * s + 1] != im.seg_tiles[4 * (s - 1) + 1] ||
+            im.seg_tiles[4 * s + 2] != im.seg_tiles[4 * (s - 1) + 2])
+            ++k;
+        cls_of[s] = k;
+    }
+    for (int32_t s0 = 0; s0 < NS;) {
+        int32_t s1 = s0;
+        while (s1 < NS && cls_of[s1] == cls_of[s0]) ++s1;
+        const int32_t p0 = im.seg_pos[s0];
+        const int32_t p1 = s1 < NS ? im.seg_pos[s1] : C;  // class positions [p0, p1)
+        for (int32_t r = 0; r < R; ++r) {
+            auto th = [&](int32_t pos) { return &im.theta2[(size_t(pos) * R + r) * 4]; };
+            auto usable = [&](int32_t pos) {
+                return !(im.meta2[size_t(pos) * R + r] & ROW_NO_COEFF);
+            };
+            const long double G0 = (long double)r * S + 1, G1 = (long double)(r + 1) * S;
+            const bool ginf = r == R - 1;
+            for (int32_t lb = 0; lb < kLB; ++lb) {
+                const long double L0 = std::ldexp(1.0L, lb), L1 = std::ldexp(1.0L, lb + 1) - 1;
+                const bool linf = lb == kLB - 1;
+                const long double Gs[2] = {G0, ginf ? G0 * 1e6L : G1}, Ls[2] = {L0, linf ? 2147483647.0L : L1};
+                std::vector<int32_t> lead;
+                for (int i = 0; i < 2; ++i)
+                    for (int j = 0; j < 2; ++j) {
+                        int32_t best = -1;
+                        long double bv = 0;
+                        for (int32_t pos = p0; pos < p1; ++pos) {
+                            const double* t = th(pos);
+                            if (!usable(pos) || !std::isfinite(t[0]) || !std::isfinite(t[1]) || !std::isfinite(t[2]) ||
+                                !std::isfinite(t[3]))
+                                continue;
+                            const long double v = t[0] * Gs[i] * Ls[j] + t[1] * Gs[i] + t[2] * Ls[j] + t[3];
+                            if (best < 0 || v < bv) {
+                                best = pos;
+                                bv = v;
+                            }
+                        }
+                        if (best >= 0 && std::find(lead.begin(), lead.end(), best) == lead.end()) lead.push_back(best);
+                    }
+                for (int32_t s = s0; s < s1; ++s) {
+                    const int32_t ps = im.seg_pos[s], n = im.seg_tiles[4 * s + 3];
+                    uint32_t m = 0;
+                    for (int32_t i = 0; i < n; ++i) {
+                        bool drop = false;
+                        for (int32_t d : lead)
+                            if (d != ps + i && usable(d) && dominated_by(th(ps + i), th(d), G0, G1, ginf, L0, L1, linf)) {
+                                drop = true;
+                                break;
+                            }
+                        if (!drop) m |= 1u << i;
+                    }
+                    im.segmask[(size_t(s) * R + r) * kLB + lb] = m;
+                }
+            }
+            for (int32_t s = s0; s < s1; ++s) {
+                uint32_t o = 0;
+                for (int32_t i = 0; i < im.seg_tiles[4 * s + 3]; ++i) o |= im.meta2[size_t(im.seg_pos[s] + i) * R + r];
+                im.segor[size_t(s) * R + r] = o;
+            }
+        }
+        s0 = s1;
+    }
 }
 
 }  // namespace
@@ -260,6 +371,7 @@ wt_status build_image(const wt_tables_desc& T, const wt_registry_desc& reg, cons
             std::copy(im.rowmeta.begin() + size_t(c) * R, im.rowmeta.begin() + size_t(c + 1) * R,
                       im.meta2.begin() + size_t(pos) * R);
         }
+        build_prune_masks(im);
         im.theta2t.resize(im.theta.size());
         im.meta2t.resize(im.rowmeta.size());
         for (int32_t pos = 0; pos < C; ++pos)

@@ -70,9 +70,20 @@ struct DevImage {
     const uint32_t* meta2;    // [C*R] rowmeta in class order
     const double4* theta2t;   // [R][C] rows by wave, class order inside (k_eval3:
     const uint32_t* meta2t;   //        a segment's configs are contiguous)
+    // Exact pruning: bit i of segmask[(seg * R + row) * kLB + lb] is clear when
+    // config i of the segment is strictly beaten -- with a margin far above
+    // fp64 rounding -- by another config of its tile class for every (G, L)
+    // of wave row `row` and L-bucket lb (L in [2^lb, 2^(lb+1)), last bucket
+    // unbounded); such a config can neither win nor tie Stage I there.
+    // segor[seg * R + row] = OR of the segment's rowmeta at that row (the
+    // flags of skipped configs still count).  prune = 0: all bits set.
+    int32_t prune;
+    const uint32_t* segmask;
+    const uint32_t* segor;
 };
 
 constexpr int kSegCfg = 32;
+constexpr int kLB = 16;  // L buckets of the pruning masks
 
 // Host-side resolved image (built by build_image, uploaded by the C-ABI).
 struct HostImage {
@@ -99,6 +110,8 @@ struct HostImage {
     std::vector<uint32_t> meta2;
     std::vector<double> theta2t;  // [R][C] transposed theta2
     std::vector<uint32_t> meta2t;
+    std::vector<uint32_t> segmask;  // [nseg][R][kLB]
+    std::vector<uint32_t> segor;    // [nseg][R]
 };
 
 // Thread-local message returned by wt_last_error().

@@ -1,0 +1,132 @@
+"""GPU parity of the exact pruning (segmask: configs strictly beaten in every
+(wave row, L bucket) cell are skipped by k_sweep2 / k_eval3) on adversarial
+tables: exact duplicates (ties -> smaller macro id must win), 1-ulp and
+1e-12 relative neighbours (inside the dominance margin: never pruned),
+clearly dominated rows (pruned), and rows where the winner changes with L.
+Every decision is compared bit for bit with the C oracle, through the grid
+sweep + gather and through the list evaluation (tune_batch), and with
+pruning disabled (WT_PRUNE=0, subprocess) as a second witness."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import pyoracle as po
+import wtutil as U
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def adversarial_tables():
+    from paper_2604_10187_b200 import synthetic as S
+
+    cfg = S.config_space(False)
+    t = S.synthetic_tables(cfg)
+    C, W = len(cfg["id"]), int(t["W"][0])
+    th = t["coeff_theta"].reshape(C, W, 4).copy()
+    te = t["theta_ext"].reshape(C, 4).copy()
+    key = list(zip(cfg["t_m"], cfg["t_n"], cfg["t_k"]))
+    classes = {}
+    for c, k in enumerate(key):
+        classes.setdefault(k, []).append(c)
+    rng = np.random.default_rng(7)
+    for cs in classes.values():
+        c0, c1, c2, c3, c4, c5 = cs[:6]
+        th[c1] = th[c0]                                   # exact tie: c0 (smaller id) must win
+        te[c1] = te[c0]
+        th[c2] = np.nextafter(th[c0], np.inf)             # 1 ulp worse: within margin, kept
+        th[c3] = th[c0] * (1 + 1e-12)                     # 1e-12 relative: kept
+        th[c4] = th[c0] * 1.5 + np.abs(th[c0]) * 0.1      # clearly dominated: pruned
+        te[c4] = te[c0] * 1.5 + np.abs(te[c0]) * 0.1
+        # c5: cheaper fixed cost, steeper per-iteration slope -> wins only at short L
+        th[c5, :, 1] = th[c0, :, 1] * 0.5
+        th[c5, :, 3] = th[c0, :, 3] * 0.5
+        th[c5, :, 0] = th[c0, :, 0] * (1.5 + rng.random())
+        th[c5, :, 2] = th[c0, :, 2] * (1.5 + rng.random())
+    t["coeff_theta"] = th.reshape(-1)
+    t["theta_ext"] = te.reshape(-1)
+    return cfg, t
+
+
+def run(capi, cfg, t, M, N, K, pairs):
+    from paper_2604_10187_b200 import synthetic as S
+
+    eng = capi.Engine(t, S.registry_arrays(cfg), n_sm=148)
+    grid = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 4096)
+    grid.sweep()
+    n = len(M)
+    res = {}
+    for mode in ("grid", "list"):
+        out = [torch.empty(n, dtype=d, device="cuda") for d in (torch.int32, torch.int32, torch.float64)]
+        dm = [torch.as_tensor(x).cuda() for x in (M, N, K)]
+        if mode == "grid":
+            grid.gather(*dm, capi.Engine.decisions(*out))
+        else:
+            eng.tune_batch(*dm, capi.Engine.decisions(*out))
+        torch.cuda.synchronize()
+        res[mode] = [o.cpu().numpy() for o in out]
+    return res
+
+
+def queries(pairs, n=60000, seed=3):
+    rng = np.random.default_rng(seed)
+    P = np.array(pairs)[rng.integers(0, len(pairs), n)]
+    M = rng.integers(1, 4097, n).astype(np.int32)
+    N, K = P[:, 0].astype(np.int32), P[:, 1].astype(np.int32)
+    off = rng.random(n) < 0.3
+    N[off] = rng.integers(16, 40000, off.sum())
+    K[off] = rng.integers(1, 1 << 20, off.sum())  # L from 1 to 16k: every L bucket
+    return M, N, K
+
+
+def test_pruning_is_exact_on_adversarial_tables():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_10187_b200 import capi, synthetic as S
+
+    cfg, t = adversarial_tables()
+    pairs = S.LLAMA3_8B
+    M, N, K = queries(pairs)
+    res = run(capi, cfg, t, M, N, K, pairs)
+    tiles = {int(i): (int(a), int(b), int(c)) for i, a, b, c in zip(cfg["id"], cfg["t_m"], cfg["t_n"], cfg["t_k"])}
+    want = po.Oracle().tune(po.FlatTables(U.pytables_from_arrays(t), tiles), 148, 1, M, N, K)
+    ok = want["status"] == 0
+    assert ok.all()
+    for mode, (mac, mic, lat) in res.items():
+        np.testing.assert_array_equal(mac, want["macro"], err_msg=mode)
+        np.testing.assert_array_equal(mic, want["micro"], err_msg=mode)
+        np.testing.assert_array_equal(U.bits(lat), U.bits(want["lat"]), err_msg=mode)
+    # ties resolved to the smaller id somewhere (the duplicated rows win)
+    ids = np.array(cfg["id"])
+    assert np.isin(res["list"][0], ids).all()
+
+
+def test_pruning_matches_unpruned_run():
+    """Same decisions with WT_PRUNE=0 (every config evaluated)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    script = (
+        "import sys, numpy as np; sys.path[:0] = [%r, %r, %r];"
+        "import torch; import test_gpu_prune as T; from paper_2604_10187_b200 import capi, synthetic as S;"
+        "cfg, t = T.adversarial_tables(); M, N, K = T.queries(S.LLAMA3_8B);"
+        "r = T.run(capi, cfg, t, M, N, K, S.LLAMA3_8B);"
+        "np.savez(sys.argv[1], gm=r['grid'][0], gl=r['grid'][2], lm=r['list'][0], ll=r['list'][2])"
+    ) % (os.path.dirname(HERE), os.path.join(os.path.dirname(HERE), "oracle"), HERE)
+    outs = []
+    for prune in ("1", "0"):
+        f = os.path.join("/tmp", f"wt_prune_{prune}_{os.getpid()}.npz")
+        r = subprocess.run([sys.executable, "-c", script, f], env={**os.environ, "WT_PRUNE": prune},
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs.append(np.load(f))
+        os.unlink(f)
+    for k in ("gm", "lm"):
+        np.testing.assert_array_equal(outs[0][k], outs[1][k])
+    for k in ("gl", "ll"):
+        np.testing.assert_array_equal(outs[0][k].view(np.int64), outs[1][k].view(np.int64))
