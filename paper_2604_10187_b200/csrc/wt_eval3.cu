@@ -355,6 +355,223 @@ __global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const
     }
 }
 
+// k_eval4: the pruned evaluation without per-segment staging or merges.
+// With the dominance masks only ~1 config per segment survives for a warp,
+// so what costs is the per-segment bookkeeping, not the fp64 work: rows are
+// recomputed only when (t_m, t_n) changes, L only when t_k leaves a 2-entry
+// cache, the surviving configs' rows are loaded directly (warp-uniform
+// addresses in the common case: one broadcast request), and every evaluation
+// updates the running (latency, config index) winner in place -- strict-<
+// plus the index tie-break, i.e. the lexicographic order tune()'s ascending
+// strict-< scan produces (tuner.cpp:135-149).
+template <bool SPECIAL, bool HS>
+__global__ void __launch_bounds__(kT3, 2) k_eval4(DevImage im, EvalArgs a, const int4* rec, const int32_t* qhi) {
+    __shared__ int4 h_tiles[kMaxSmemSeg];
+    __shared__ uint4 h_magic[kMaxSmemSeg];
+    __shared__ int32_t h_pos[kMaxSmemSeg];
+    if (HS) {
+        for (int i = threadIdx.x; i < im.nseg; i += blockDim.x) {
+            h_tiles[i] = im.seg_tiles[i];
+            h_magic[i] = im.seg_magic[i];
+            h_pos[i] = im.seg_pos[i];
+        }
+    }
+    __syncthreads();
+    const int4* Ts = HS ? h_tiles : im.seg_tiles;
+    const uint4* Ms = HS ? h_magic : im.seg_magic;
+    const int32_t* Ps = HS ? h_pos : im.seg_pos;
+    const int64_t n = a.count ? *a.count : a.n;
+    const int64_t nt = (n + 3) / 4;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    const int C = im.C, R = im.R;
+    // Per-warp plan of 32 segments, built lane-parallel (lane = segment) from
+    // lane 0's first query: its wave row and L bucket, the pruning mask of
+    // that cell and the rows of its first two surviving configs, all loaded
+    // at once.  A segment whose 128 queries all share that (row, L bucket)
+    // -- checked exactly per segment -- then reads mask and rows from shared
+    // memory instead of two dependent global round trips.
+    __shared__ __align__(16) double4 pth[kT3 / 32][32][2];
+    __shared__ uint32_t pmask[kT3 / 32][32], pcell[kT3 / 32][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < nt; base += stride) {
+        const int64_t t = base + threadIdx.x;
+        uint32_t y2M[4], y2N[4], y2K[4], status[4], acc[4];
+        int64_t q[4];
+        double best[4];
+        int bci[4];  // winner's config index (INT32_MAX: none yet)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t i = t * 4 + j;
+            const bool live = t < nt && i < n;
+            uint32_t M = 1, N = 1, K = 1, st = 0;
+            q[j] = -1;
+            if (live) {
+                const int4 r = rec[i];
+                q[j] = int64_t(uint32_t(r.x)) | (qhi ? int64_t(qhi[i]) << 32 : 0);
+                st = query_status(im, r.y, r.z, r.w, &M, &N, &K);
+            }
+            y2M[j] = 2u * (M - 1u);
+            y2N[j] = 2u * (N - 1u);
+            y2K[j] = 2u * (K - 1u);
+            status[j] = st;
+            best[j] = kInf3;
+            bci[j] = INT32_MAX;
+            acc[j] = 0;
+        }
+        uint32_t pm = 0, pn = 0, ps = 0xffffffffu;
+        uint32_t row[4] = {0, 0, 0, 0};
+        double gd[4] = {0, 0, 0, 0};
+        bool uni = false;
+        // two-entry cache of L per t_k (tags = magic, shift)
+        uint32_t tagA = 0xffffffffu, tagB = 0xffffffffu;
+        double ldA[4] = {0, 0, 0, 0}, ldB[4] = {0, 0, 0, 0};
+        uint32_t lbA = 0, lbB = 0;
+        bool nextA = true;
+        const uint32_t y2M0 = __shfl_sync(0xffffffffu, y2M[0], 0), y2N0 = __shfl_sync(0xffffffffu, y2N[0], 0),
+                       y2K0 = __shfl_sync(0xffffffffu, y2K[0], 0);
+        for (int s = 0; s < im.nseg; ++s) {
+            if ((s & 31) == 0) {  // plan segments [s, s + 32)
+                __syncwarp();     // the previous plan is no longer read
+                const int sg = s + lane;
+                uint32_t m = 0, cell = 0xffffffffu;
+                if (sg < im.nseg) {
+                    const uint4 mq = Ms[sg];
+                    uint64_t g;
+                    const uint32_t r = row_for(im, y2M0, y2N0, mq, &g);
+                    const uint32_t L = mdiv2(y2K0, mq.z, (mq.w >> 16) & 0xffu) + 1u;
+                    const uint32_t lb = uint32_t(min(31 - __clz(int(L)), kLB - 1));
+                    const int nq = Ts[sg].w;
+                    m = im.prune ? __ldg(im.segmask + (size_t(sg) * R + r) * kLB + lb) : 0xffffffffu;
+                    m &= nq >= 32 ? 0xffffffffu : ((1u << nq) - 1u);
+                    cell = r | (lb << 24);
+                    const double4* tp = im.theta2t + size_t(r) * C + Ps[sg];
+                    if (m) pth[wid][lane][0] = ldg_row(tp + (__ffs(int(m)) - 1));
+                    const uint32_t m2 = m & (m - 1u);
+                    if (m2) pth[wid][lane][1] = ldg_row(tp + (__ffs(int(m2)) - 1));
+                }
+                pmask[wid][lane] = m;
+                pcell[wid][lane] = cell;
+                __syncwarp();
+            }
+            const uint4 mg = Ms[s];
+            const int pos = Ps[s];
+            const int ncfg = Ts[s].w;
+            if (mg.x != pm || mg.y != pn || (mg.w & 0xffffu) != ps) {
+                pm = mg.x;
+                pn = mg.y;
+                ps = mg.w & 0xffffu;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint64_t g;
+                    row[j] = row_for(im, y2M[j], y2N[j], mg, &g);
+                    gd[j] = u64_to_f64(g);
+                }
+                const uint32_t r0 = __shfl_sync(0xffffffffu, row[0], 0);
+                uni = __all_sync(0xffffffffu, row[0] == r0 && row[1] == r0 && row[2] == r0 && row[3] == r0);
+            }
+            const uint32_t sk = (mg.w >> 16) & 0xffu;
+            const uint32_t tag = mg.z ^ (sk << 24);
+            if (tag != tagA && tag != tagB) {
+                double* ld = nextA ? ldA : ldB;
+                uint32_t lb = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t L = mdiv2(y2K[j], mg.z, sk) + 1u;
+                    ld[j] = u32_to_f64(L);
+                    lb |= uint32_t(min(31 - __clz(int(L)), kLB - 1)) << (8 * j);
+                }
+                if (nextA) {
+                    tagA = tag;
+                    lbA = lb;
+                } else {
+                    tagB = tag;
+                    lbB = lb;
+                }
+                nextA = !nextA;
+            }
+            const bool useA = tag == tagA;
+            double ld[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) ld[j] = useA ? ldA[j] : ldB[j];
+            const uint32_t lbp = useA ? lbA : lbB;
+            // does the whole warp sit in the planned (row, L bucket) cell?
+            const uint32_t cell = pcell[wid][s & 31];
+            const bool lbu = ((lbp ^ (lbp >> 8)) & 0x00ffffu) == 0 && ((lbp ^ (lbp >> 16)) & 0xffu) == 0;
+            const bool inplan = __all_sync(0xffffffffu, uni && row[0] == (cell & 0xffffffu) && lbu &&
+                                                            (lbp & 0xffu) == (cell >> 24));
+            uint32_t live;
+            if (inplan) {
+                live = pmask[wid][s & 31];
+            } else {
+                live = 0xffffffffu;
+                if (im.prune) {
+                    const uint32_t* mk = im.segmask + size_t(s) * R * kLB;
+                    live = 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) live |= __ldg(mk + row[j] * kLB + ((lbp >> (8 * j)) & 0xffu));
+                    live = __reduce_or_sync(0xffffffffu, live);
+                }
+                live &= ncfg >= 32 ? 0xffffffffu : ((1u << ncfg) - 1u);
+            }
+            int k_staged = 0;  // index of the next planned row in pth
+            if constexpr (SPECIAL) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[j] |= __ldg(im.segor + size_t(s) * R + row[j]);
+            }
+            for (uint32_t mm = live; mm; mm &= mm - 1u) {
+                const int c = __ffs(int(mm)) - 1;
+                const int ci = __ldg(im.cls_cfg + pos + c);
+                double4 th[4];
+                if (inplan && k_staged < 2) {
+                    th[0] = pth[wid][s & 31][k_staged++];
+                    th[1] = th[2] = th[3] = th[0];
+                } else if (uni) {
+                    th[0] = ldg_row(im.theta2t + size_t(row[0]) * C + pos + c);
+                    th[1] = th[2] = th[3] = th[0];
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) th[j] = ldg_row(im.theta2t + size_t(row[j]) * C + pos + c);
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    double tt = __dmul_rn(__dmul_rn(th[j].x, gd[j]), ld[j]);
+                    tt = __dadd_rn(tt, __dmul_rn(th[j].y, gd[j]));
+                    tt = __dadd_rn(tt, __dmul_rn(th[j].z, ld[j]));
+                    tt = __dadd_rn(tt, th[j].w);
+                    if (tt < best[j] || (tt == best[j] && ci < bci[j])) {
+                        best[j] = tt;
+                        bci[j] = ci;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (q[j] < 0) continue;
+            Final f;
+            uint64_t g = 0;
+            int64_t l = 0;
+            const int bc = bci[j] != INT32_MAX ? bci[j] : -1;
+            if (status[j]) {
+                f.flags = status[j] << 24;
+                f.macro = f.micro = f.wave = -1;
+                f.comps = 0;
+                f.tail = 0.f;
+            } else {
+                if (bc >= 0) {
+                    const int4 tl4 = __ldg(im.tiles + bc);
+                    const uint32_t M = y2M[j] / 2u + 1u, N = y2N[j] / 2u + 1u, K = y2K[j] / 2u + 1u;
+                    g = uint64_t((M + uint32_t(tl4.x) - 1) / uint32_t(tl4.x)) *
+                        uint64_t((N + uint32_t(tl4.y) - 1) / uint32_t(tl4.y));
+                    l = int64_t((K + uint32_t(tl4.z) - 1) / uint32_t(tl4.z));
+                }
+                f = finish(im, bc, 0.0, g, l, acc[j]);
+            }
+            write_decision(a.out, q[j], f, best[j], g, l);
+        }
+    }
+}
+
 // ---------------------------------------------------------------- launcher
 namespace {
 int key_bits() {
@@ -444,6 +661,17 @@ cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, b
     const int64_t want3 = (a.n + 4 * kT3 - 1) / (4 * kT3);
     const bool hs = im.nseg <= kMaxSmemSeg;
     const int g3 = int(std::max<int64_t>(1, std::min<int64_t>(want3, int64_t(sms) * (im.special ? occs : occ))));
+    static const int kern = [] {
+        const char* v = std::getenv("WT_EVAL_KERNEL");
+        return v ? std::atoi(v) : 4;
+    }();
+    if (kern == 4) {
+        if (im.special)
+            hs ? k_eval4<true, true><<<g3, kT3, 0, st>>>(im, a, rec, qhi) : k_eval4<true, false><<<g3, kT3, 0, st>>>(im, a, rec, qhi);
+        else
+            hs ? k_eval4<false, true><<<g3, kT3, 0, st>>>(im, a, rec, qhi) : k_eval4<false, false><<<g3, kT3, 0, st>>>(im, a, rec, qhi);
+        return cudaGetLastError();
+    }
     if (im.special)
         hs ? k_eval3<true, true><<<g3, kT3, 0, st>>>(im, a, rec, qhi) : k_eval3<true, false><<<g3, kT3, 0, st>>>(im, a, rec, qhi);
     else

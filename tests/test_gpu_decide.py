@@ -461,6 +461,7 @@ def test_sharded_sweep_equals_full(capi, synth256):
     {"WT_EVAL_KEY_BITS": "8"},
     {"WT_EVAL_KEY_BITS": "24"},
     {"WT_PRUNE": "0"},
+    {"WT_EVAL_KERNEL": "3"},
 ])
 def test_launch_variants(capi, env):
     """Every launch shape the tuning knobs can select stays bit-exact."""
