@@ -270,6 +270,8 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
         return v ? std::atoi(v) : 1;
     }();
     d.prune = prune;
+    d.seg_maxcfg = 1;
+    for (size_t k = 0; k < NS; ++k) d.seg_maxcfg = std::max(d.seg_maxcfg, h.seg_tiles[4 * k + 3]);
     // list-mode chunk: keep the staged rows near 40 KB so several CTAs fit per SM
     e->eval_chunk = int(std::max<size_t>(1, std::min<size_t>(C, 40960 / (R * 36 + 32))));
     e->eval_grid = sm_count(device) * 4;

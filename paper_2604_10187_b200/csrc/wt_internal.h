@@ -78,6 +78,7 @@ struct DevImage {
     // segor[seg * R + row] = OR of the segment's rowmeta at that row (the
     // flags of skipped configs still count).  prune = 0: all bits set.
     int32_t prune;
+    int32_t seg_maxcfg;       // largest segment (configs)
     const uint32_t* segmask;
     const uint32_t* segor;
 };
