@@ -400,8 +400,10 @@ def run_wavetune(args):
                          "share_of_step": gather_ms / t_ms},
             "offgrid_eval": {"queries": n_off, "ms": eval_ms, "share_of_step": eval_ms / t_ms,
                              "evals": n_off * eng.n_configs,
-                             "fp64_flop_per_s": 7.0 * n_off * eng.n_configs / (eval_ms * 1e-3),
-                             "pipeline": "scan + counting-sort scatter + k_eval3 (keys counted in k_gather_h)"},
+                             "evals_per_s": n_off * eng.n_configs / (eval_ms * 1e-3),
+                             "evals_note": "(query, config) pairs decided per second; dominated configs "
+                                           "skipped exactly (WT_PRUNE=0 evaluates all)",
+                             "pipeline": "scan + counting-sort scatter + k_eval4 (keys counted in k_gather_h)"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -12,8 +12,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/la
 # the bench step's kernels, captured on the bench's own 1e8-query stream
 ncu --set full --clock-control none --import-source on -k regex:k_gather_h -s 2 -c 1 -o $O/ncu_gather_$TAG -f \
     python tools/prof_kernels.py step 100000000 > /dev/null 2>&1; echo "gather $?"
-ncu --set full --clock-control none --import-source on -k regex:k_eval3 -s 2 -c 1 -o $O/ncu_eval3_$TAG -f \
-    python tools/prof_kernels.py step 100000000 > /dev/null 2>&1; echo "eval3 $?"
+ncu --set full --clock-control none --import-source on -k regex:k_eval4 -s 2 -c 1 -o $O/ncu_eval4_$TAG -f \
+    python tools/prof_kernels.py step 100000000 > /dev/null 2>&1; echo "eval4 $?"
 ncu --set full --clock-control none --import-source on -k regex:k_escatter -s 2 -c 1 -o $O/ncu_escatter_$TAG -f \
     python tools/prof_kernels.py step 100000000 > /dev/null 2>&1; echo "escatter $?"
 ncu --set full --clock-control none --import-source on -k regex:k_sweep2 -s 2 -c 1 -o $O/ncu_sweep2_$TAG -f \
