@@ -934,21 +934,27 @@ wt_status wt_grid_finalize(const wt_engine* e, wt_grid* g, void* stream) {
     return WT_OK;
 }
 
-wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M, const int32_t* N,
-                          const int32_t* K, int64_t n, const wt_decisions* out, void* stream) {
-    if (!e || !g) return set_err(WT_INVALID_ARGUMENT, "null argument");
-    if (g->eng != e) return set_err(WT_INVALID_ARGUMENT, "grid was created for another engine");
-    wt_status st = check_out(out);
-    if (st) return st;
-    if (out->topk && out->topk != g->topk)
-        return set_err(WT_INVALID_ARGUMENT, "topk must match the grid's topk");
-    if (n <= 0) return n == 0 ? WT_OK : set_err(WT_INVALID_ARGUMENT, "negative batch size");
-    DeviceGuard guard(e->device);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    void* scratch = nullptr;
-    // [count | idx (n) | M (n) | N (n) | K (n)] -- the off-grid compaction list
-    const size_t bytes = size_t(n + 2) * sizeof(int64_t) + 3 * size_t(n + 4) * sizeof(int32_t);
-    cudaError_t ce = cudaMallocFromPoolAsync(&scratch, bytes, lib_pool(e->device), s);
+}  // extern "C"
+
+// [count | idx (n) | M (n) | N (n) | K (n)] -- the off-grid compaction list
+static size_t gather_scratch_bytes(int64_t n) {
+    return size_t(n + 2) * sizeof(int64_t) + 3 * size_t(n + 4) * sizeof(int32_t);
+}
+
+static bool gather_needs_eval3(const wt_grid* g, const wt_decisions* out) {
+    return g->topk == 0 && out->topk == 0 && eval_mode() == 3;
+}
+
+// The gather + off-grid evaluation of one batch.  Scratch buffers are taken
+// from the library pool unless the caller supplies them (the host pipeline
+// keeps one set per slot: pool reuse across its streams would otherwise add
+// cross-stream waits).
+static wt_status gather_impl(const wt_engine* e, const wt_grid* g, const int32_t* M, const int32_t* N,
+                             const int32_t* K, int64_t n, const wt_decisions* out, cudaStream_t s,
+                             void* scratch_in, void* escratch_in) {
+    void* scratch = scratch_in;
+    cudaError_t ce = cudaSuccess;
+    if (!scratch) ce = cudaMallocFromPoolAsync(&scratch, gather_scratch_bytes(n), lib_pool(e->device), s);
     if (ce != cudaSuccess) return cuda_err(ce, "wt_gather_batch: scratch");
     int64_t* count = static_cast<int64_t*>(scratch);
     int64_t* idx = count + 2;
@@ -980,11 +986,11 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
     a.hbits = g->hbits;
     a.runs = g->runs;
     // row-grouped evaluation of the off-grid list: keys counted while compacting
-    void* escratch = nullptr;
-    if (g->topk == 0 && out->topk == 0 && eval_mode() == 3) {
-        ce = cudaMallocFromPoolAsync(&escratch, eval3_scratch_bytes(n), lib_pool(e->device), s);
+    void* escratch = escratch_in;
+    if (gather_needs_eval3(g, out)) {
+        if (!escratch) ce = cudaMallocFromPoolAsync(&escratch, eval3_scratch_bytes(n), lib_pool(e->device), s);
         if (ce != cudaSuccess) {
-            cudaFreeAsync(scratch, s);
+            if (!scratch_in) cudaFreeAsync(scratch, s);
             return cuda_err(ce, "wt_gather_batch: eval scratch");
         }
         const Eval3Bufs b = eval3_bufs(escratch, n);
@@ -1026,10 +1032,25 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
         }
     }
     timing_mark(3, s);
-    cudaFreeAsync(scratch, s);
-    if (escratch) cudaFreeAsync(escratch, s);
+    if (!scratch_in) cudaFreeAsync(scratch, s);
+    if (escratch && !escratch_in) cudaFreeAsync(escratch, s);
     if (ce != cudaSuccess) return cuda_err(ce, "wt_gather_batch");
     return WT_OK;
+}
+
+extern "C" {
+
+wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M, const int32_t* N,
+                          const int32_t* K, int64_t n, const wt_decisions* out, void* stream) {
+    if (!e || !g) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    if (g->eng != e) return set_err(WT_INVALID_ARGUMENT, "grid was created for another engine");
+    wt_status st = check_out(out);
+    if (st) return st;
+    if (out->topk && out->topk != g->topk)
+        return set_err(WT_INVALID_ARGUMENT, "topk must match the grid's topk");
+    if (n <= 0) return n == 0 ? WT_OK : set_err(WT_INVALID_ARGUMENT, "negative batch size");
+    DeviceGuard guard(e->device);
+    return gather_impl(e, g, M, N, K, n, out, static_cast<cudaStream_t>(stream), nullptr, nullptr);
 }
 
 wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_t* M,
@@ -1047,7 +1068,14 @@ wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_
     const int kSlots = int(std::min<int64_t>(kMaxSlots, (n + chunk - 1) / chunk));
     cudaStream_t st[kMaxSlots] = {};
     void* buf[kMaxSlots] = {};
-    const size_t per = size_t(chunk) * (8 + 3 * 4 + 4 + 4);
+    // per slot: I/O buffers, then the gather's and the evaluation's scratch
+    // (owned by the slot for the whole call: no pool traffic between streams)
+    wt_decisions probe{};
+    const bool ev3 = g && gather_needs_eval3(g, &probe);
+    const size_t io = (size_t(chunk) * (8 + 3 * 4 + 4 + 4) + 255) & ~size_t(255);
+    const size_t gs = g ? (gather_scratch_bytes(chunk) + 255) & ~size_t(255) : 0;
+    const size_t es = ev3 ? eval3_scratch_bytes(chunk) : 0;
+    const size_t per = io + gs + es;
     cudaError_t ce = cudaSuccess;
     for (int s = 0; s < kSlots && ce == cudaSuccess; ++s) {
         ce = cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking);
@@ -1071,7 +1099,12 @@ wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_
         d.macro_id = dmac;
         d.micro_id = dmic;
         d.latency_us = dlat;
-        rs = g ? wt_gather_batch(e, g, dM, dN, dK, m, &d, st[s]) : wt_tune_batch(e, dM, dN, dK, m, &d, st[s]);
+        if (g) {
+            char* sb = static_cast<char*>(buf[s]) + io;
+            rs = gather_impl(e, g, dM, dN, dK, m, &d, st[s], sb, ev3 ? sb + gs : nullptr);
+        } else {
+            rs = wt_tune_batch(e, dM, dN, dK, m, &d, st[s]);
+        }
         cudaMemcpyAsync(macro_id + i, dmac, size_t(m) * 4, cudaMemcpyDeviceToHost, st[s]);
         cudaMemcpyAsync(micro_id + i, dmic, size_t(m) * 4, cudaMemcpyDeviceToHost, st[s]);
         ce = cudaMemcpyAsync(latency_us + i, dlat, size_t(m) * 8, cudaMemcpyDeviceToHost, st[s]);

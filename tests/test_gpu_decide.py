@@ -525,3 +525,29 @@ def test_resident_server_matches_batch(capi, landscape, synth256):
         t0 = time.perf_counter()
         torch.cuda.synchronize()
         assert time.perf_counter() - t0 < 0.5
+
+
+@pytest.mark.parametrize("chunk", [1000, 4096, 1 << 22])
+def test_decide_host_pipeline_matches_device(capi, synth256, chunk):
+    """wt_decide_host_sync (pinned host buffers, chunked H2D / gather / D2H
+    over several streams with per-slot scratch) == the device-resident call,
+    including a ragged last chunk and off-grid queries."""
+    from paper_2604_10187_b200 import synthetic as S
+
+    cfg, t, reg = synth256
+    eng = capi.Engine(t, reg, n_sm=148)
+    pairs = S.LLAMA3_8B
+    grid = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 8192)
+    grid.sweep()
+    M, N, K = S.query_stream(30011, pairs, seed=9, off_grid_frac=0.05)
+    n = len(M)
+    out = [torch.empty(n, dtype=d, device="cuda") for d in (torch.int32, torch.int32, torch.float64)]
+    grid.gather(dev(M), dev(N), dev(K), capi.Engine.decisions(*out))
+    torch.cuda.synchronize()
+    Mp, Np, Kp = (torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in (M, N, K))
+    mac = torch.empty(n, dtype=torch.int32).pin_memory()
+    mic = torch.empty(n, dtype=torch.int32).pin_memory()
+    lat = torch.empty(n, dtype=torch.float64).pin_memory()
+    grid.decide_host(Mp, Np, Kp, mac, mic, lat, chunk=chunk)
+    assert torch.equal(mac, out[0].cpu()) and torch.equal(mic, out[1].cpu())
+    assert torch.equal(lat.view(torch.int64), out[2].cpu().view(torch.int64))
