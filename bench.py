@@ -324,8 +324,19 @@ def run_wavetune(args):
         # wave-structured samples (K2; device time from records in HBM)
         cfg3 = S.config_space(full=True)
         rec4 = S.synthetic_records(cfg3, micros_per_macro=1)
-        fit = capi.fit_build(rec4, cfg3["id"], 40, 10, device=local)  # warm-up
-        fit = capi.fit_build(rec4, cfg3["id"], 40, 10, device=local)
+        fit_wall_ms = None
+        if ws > 1:  # sharded by macro, tables all-gathered (dist.sharded_fit)
+            from paper_2604_10187_b200.dist import sharded_fit
+
+            sharded_fit(rec4, cfg3["id"], 40, 10, device=local)  # warm-up
+            dist.barrier()
+            tw = time.perf_counter()
+            fit = sharded_fit(rec4, cfg3["id"], 40, 10, device=local)
+            dist.barrier()
+            fit_wall_ms = (time.perf_counter() - tw) * 1e3
+        else:
+            fit = capi.fit_build(rec4, cfg3["id"], 40, 10, device=local)  # warm-up
+            fit = capi.fit_build(rec4, cfg3["id"], 40, 10, device=local)
         t3 = {k: fit[k] for k in ("macro_id", "theta_ext", "coeff_off", "coeff_w", "coeff_theta", "awave_off",
                                    "awave_w", "awave_aoff", "anchor_l", "anchor_micro", "ext_aoff", "ext_l",
                                    "ext_micro")}
@@ -367,7 +378,9 @@ def run_wavetune(args):
                                             "(exact pruning, WT_PRUNE=0 evaluates all)",
                               "shapes": g3.n_entries, "configs": eng3.n_configs,
                               "sharding": f"shape slices x{ws} + NCCL all_gather" if ws > 1 else "single GPU"},
-            "config4_fit": {"ms": fit_ms, "records": int(len(rec4["g"])), "tables": int(fit["n_tables"]),
+            "config4_fit": {"ms": fit_ms, "wall_ms_with_exchange": fit_wall_ms,
+                            "sharding": f"macros x{ws} + all_gather_object" if ws > 1 else "single GPU",
+                            "records": int(len(rec4["g"])), "tables": int(fit["n_tables"]),
                             "buckets": int(len(fit["coeff_w"])),
                             "median_bucket_mape": float(np.median(fit["diag_mape"])),
                             "median_bucket_r2": float(np.median(fit["diag_r2"]))},

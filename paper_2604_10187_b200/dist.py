@@ -1,4 +1,4 @@
-"""Multi-GPU decision grids: the flattened shape index (pair-major, M-minor)
+"""Multi-GPU decision grids and fits.  Grids: the flattened shape index (pair-major, M-minor)
 is cut into equal contiguous slices, one per rank; every rank sweeps its
 slice into its own grid (wt_sweep over [begin, end)), then one NCCL
 all-gather over NVLink assembles the full grid on every rank.  The sweep is
@@ -55,3 +55,101 @@ def sharded_sweep(grid, group=None, stream=None):
     gather_grid(ent, grid.n_entries, group=group, fill=fill)
     grid.finalize(stream=stream)
     return ent
+
+
+# ---------------------------------------------------------------- sharded fit
+# build_dual_table fits every macro from its own records only (model.cpp:194-
+# 253: records grouped by macro, macros visited in registry order), so the
+# fit shards by macro: each rank fits a contiguous slice of the registry and
+# the per-rank table sets are concatenated in rank order, which is registry
+# order.  W must be global: the reference takes params.W, or the largest
+# record wave when W <= 0 -- an all-reduce(max) here.
+
+_PER_TABLE = {"macro_id": 1, "theta_ext": 4, "ext_flags": 1, "W_arr": 1, "lin_theta": 4, "lin_r2": 1,
+              "lin_mape": 1, "lin_degenerate": 1}
+# CSR groups: offsets key -> (per-entry arrays with their widths)
+_CSR = {
+    "coeff_off": {"coeff_w": 1, "coeff_theta": 4, "diag_r2": 1, "diag_mape": 1, "diag_samples": 1, "diag_flags": 1},
+    "ext_aoff": {"ext_l": 1, "ext_micro": 1},
+    "step_off": {"step_l": 1, "step_t": 1},
+}
+
+
+def macro_shards(registry_ids, world: int):
+    """Contiguous slices of the registry (registry order), one per rank."""
+    import numpy as np
+
+    ids = np.asarray(registry_ids)
+    per = -(-len(ids) // world)
+    return [ids[r * per: (r + 1) * per] for r in range(world)]
+
+
+def records_of(records: dict, ids):
+    """The records whose macro is in `ids` (order preserved)."""
+    import numpy as np
+
+    m = np.isin(records["macro"], ids)
+    return {k: v[m] for k, v in records.items()}
+
+
+def merge_tables(parts):
+    """Concatenate table sets (fit_build outputs, in registry order) into one.
+    Empty parts (n_tables == 0) are skipped."""
+    import numpy as np
+
+    parts = [p for p in parts if p and p["n_tables"] > 0]
+    if not parts:
+        raise RuntimeError("no tables built")
+    out = {"n_tables": sum(p["n_tables"] for p in parts), "W": parts[0]["W"], "p": parts[0]["p"],
+           "device_ms": max(p.get("device_ms", 0.0) for p in parts)}
+    for k in _PER_TABLE:
+        out[k] = np.concatenate([p[k] for p in parts])
+    for off, members in _CSR.items():
+        offs, base = [np.zeros(1, np.int32)], 0
+        for p in parts:
+            offs.append(p[off][1:] + base)
+            base += int(p[off][-1])
+        out[off] = np.concatenate(offs).astype(np.int32)
+        for k in members:
+            out[k] = np.concatenate([p[k] for p in parts])
+    # anchors: awave_off over waves, awave_aoff over anchors
+    aw, an = [np.zeros(1, np.int32)], [np.zeros(1, np.int32)]
+    bw = ba = 0
+    for p in parts:
+        aw.append(p["awave_off"][1:] + bw)
+        an.append(p["awave_aoff"][1:] + ba)
+        bw += int(p["awave_off"][-1])
+        ba += int(p["awave_aoff"][-1])
+    out["awave_off"] = np.concatenate(aw).astype(np.int32)
+    out["awave_aoff"] = np.concatenate(an).astype(np.int32)
+    for k in ("awave_w", "anchor_l", "anchor_micro", "anchor_partial"):
+        out[k] = np.concatenate([p[k] for p in parts])
+    return out
+
+
+def sharded_fit(records: dict, registry_ids, W: int = 0, p: int = 10, group=None, fit=None, device: int = 0):
+    """build_dual_table sharded by macro over the ranks of `group`; every
+    rank returns the full table set.  `fit(records, ids, W, p, device)`
+    defaults to the GPU fit (capi.fit_build); the CPU tests pass a stand-in.
+    The exchange is one all_gather_object of the per-rank tables (a few MB,
+    NCCL over NVLink on B200)."""
+    import numpy as np
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if fit is None:
+        from . import capi
+
+        fit = capi.fit_build
+    if W <= 0:  # the reference's "max r.w over all records", made global
+        wmax = torch.tensor([int(np.max(records["w"])) if len(records["w"]) else 0], dtype=torch.int64)
+        if dist.get_backend(group) == "nccl":
+            wmax = wmax.cuda()
+        dist.all_reduce(wmax, op=dist.ReduceOp.MAX, group=group)
+        W = int(wmax.item())
+    ids = macro_shards(registry_ids, world)[rank]
+    mine = records_of(records, ids)
+    part = fit(mine, ids, W, p, device) if len(ids) and len(mine["g"]) else None
+    parts = [None] * world
+    dist.all_gather_object(parts, part, group=group)
+    return merge_tables(parts)

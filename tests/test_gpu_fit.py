@@ -160,3 +160,25 @@ def test_build_config4_scale_subset_parity(capi, orc):
         np.testing.assert_array_equal(U.bits(gpu["theta_ext"][4 * i:4 * i + 4]), U.bits(want["theta_ext"][4 * j:4 * j + 4]))
     # predicted-vs-sampled error on the synthetic profile is reported, and sane
     assert np.median(gpu["diag_mape"]) < 0.05
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_macro_sharded_fit_equals_full_build(capi, world):
+    """dist.sharded_fit's decomposition on one GPU: fit_build over each
+    rank's contiguous registry slice, merged in rank order, is bit-identical
+    to the single build (every array, every offset)."""
+    from paper_2604_10187_b200 import synthetic as S
+    from paper_2604_10187_b200.dist import macro_shards, merge_tables, records_of
+
+    cfg = S.config_space(False)
+    rec = S.synthetic_records(cfg, micros_per_macro=2)
+    full = capi.fit_build(rec, cfg["id"], 40, 10)
+    parts = [capi.fit_build(records_of(rec, ids), ids, 40, 10) for ids in macro_shards(cfg["id"], world)]
+    got = merge_tables(parts)
+    assert got["n_tables"] == full["n_tables"]
+    for k, v in got.items():
+        if isinstance(v, np.ndarray):
+            if v.dtype == np.float64:
+                np.testing.assert_array_equal(v.view(np.int64), full[k].view(np.int64), err_msg=k)
+            else:
+                np.testing.assert_array_equal(v, full[k], err_msg=k)
