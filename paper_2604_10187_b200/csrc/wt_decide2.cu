@@ -44,6 +44,7 @@ struct SegHdr {  // one staged segment
     int32_t ncfg, pos, off, stride;
     double ld;
     uint32_t mN, mK, seg, lb;  // segment index, L bucket (sweep: one K per tile)
+    uint32_t live, nl, pad2, pad3;  // sweep: configs staged (union over the tile's cells), count
 };
 
 __device__ __forceinline__ bool lex_less(double a, int ia, double b, int ib) {
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
             // -- plan this staging round: segments s0.. whose row ranges fit
             const int s = s0 + tid;
             int need = 0;
-            uint32_t rlo = 0, nt = 0, mM = 0, sM = 0, lk = 1;
+            uint32_t rlo = 0, nt = 0, mM = 0, sM = 0, lk = 1, live = 0;
             int4 st = make_int4(0, 0, 0, 0);
             if (s < seg_hi) {
                 st = __ldg(im.seg_tiles + s);
@@ -121,7 +122,16 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
                 const uint64_t ghi = uint64_t(cdiv_m(Mhi, mM, sM)) * nt;
                 rlo = row_of(uint32_t(glo > RS ? RS : glo), mS, sS);
                 const uint32_t rhi = row_of(uint32_t(ghi > RS ? RS : ghi), mS, sS);
-                need = int(rhi - rlo + 1) * st.w;
+                // only configs that survive pruning in some cell of the tile
+                // are staged (compact [row][live index] layout)
+                live = st.w >= 32 ? 0xffffffffu : ((1u << st.w) - 1u);
+                if (im.prune) {
+                    const uint32_t lb = uint32_t(min(31 - __clz(int(lk)), kLB - 1));
+                    uint32_t u = 0;
+                    for (uint32_t r = rlo; r <= rhi; ++r) u |= __ldg(im.segmask + (size_t(s) * R + r) * kLB + lb);
+                    live &= u;
+                }
+                need = int(rhi - rlo + 1) * __popc(live);
             }
             int off;
             Scan(scan_tmp).ExclusiveSum(need, off);
@@ -136,7 +146,9 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
                 h.ncfg = st.w;
                 h.pos = __ldg(im.seg_pos + s);
                 h.off = off;
-                h.stride = need / max(st.w, 1);  // rows of this segment in the tile
+                h.live = live;
+                h.nl = uint32_t(__popc(live));
+                h.stride = need / max(int(h.nl), 1);  // rows of this segment in the tile
                 h.ld = u32_to_f64(lk);
                 h.seg = uint32_t(s);
                 h.lb = uint32_t(min(31 - __clz(int(lk)), kLB - 1));
@@ -146,14 +158,15 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
             // -- stage rows [rowlo, rowlo + nrows) as [row][config], gamma*l folded
             for (int k = 0; k < count; ++k) {
                 const SegHdr h = hdr[k];
-                const int n = h.stride * h.ncfg;
+                const int nl = int(h.nl);
+                const int n = h.stride * nl;
                 for (int i = tid; i < n; i += kT2) {
-                    const int r = i / h.ncfg, c = i - r * h.ncfg;
+                    const int r = i / nl, q = i - r * nl;
+                    const int c = int(__fns(h.live, 0, q + 1));  // q-th staged config
                     const size_t src = size_t(h.pos + c) * R + h.rowlo + r;
                     double4 th = ldg_row(im.theta2 + src);
                     th.z = __dmul_rn(th.z, h.ld);
                     rows[h.off + i] = th;
-                    if constexpr (SPECIAL) meta[h.off + i] = __ldg(im.meta2 + src);
                 }
             }
             __syncthreads();
@@ -161,7 +174,6 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
             for (int k = 0; k < count; ++k) {
                 const SegHdr h = hdr[k];
                 const double4* pr[RPT];
-                const uint32_t* pm[RPT];
                 double gd[RPT], sb[RPT];
                 int sj[RPT], rr[RPT];
 #pragma unroll
@@ -179,8 +191,7 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
                     }
                     const int r = int(row_of(gc, mS, sS) - h.rowlo);
                     rr[j] = r;
-                    pr[j] = rows + h.off + r * h.ncfg;
-                    pm[j] = meta + h.off + r * h.ncfg;
+                    pr[j] = rows + h.off + r * int(h.nl);
                     sb[j] = kInf;
                     sj[j] = -1;
                 }
@@ -195,7 +206,7 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
                     for (int j = 0; j < RPT; ++j) live |= __ldg(mk + (h.rowlo + uint32_t(rr[j])) * kLB);
                     live = __reduce_or_sync(0xffffffffu, live);
                 }
-                live &= h.ncfg >= 32 ? 0xffffffffu : ((1u << h.ncfg) - 1u);
+                live &= h.live;  // subset of the staged configs
                 if constexpr (SPECIAL) {
 #pragma unroll
                     for (int j = 0; j < RPT; ++j)
@@ -203,10 +214,11 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
                 }
                 for (uint32_t mm = live; mm; mm &= mm - 1u) {
                     const int c = __ffs(int(mm)) - 1;
+                    const int qi = __popc(h.live & ((1u << c) - 1u));  // staged index
                     double4 th[RPT];
                     double t[RPT], u[RPT];
 #pragma unroll
-                    for (int j = 0; j < RPT; ++j) th[j] = pr[j][c];
+                    for (int j = 0; j < RPT; ++j) th[j] = pr[j][qi];
 #pragma unroll
                     for (int j = 0; j < RPT; ++j) t[j] = __dmul_rn(th[j].x, gd[j]);
 #pragma unroll
