@@ -1,5 +1,5 @@
 """GPU parity of the exact pruning (segmask: configs strictly beaten in every
-(wave row, L bucket) cell are skipped by k_sweep2 / k_eval3) on adversarial
+(wave row, L bucket) cell are skipped by k_sweep2 / k_eval4) on adversarial
 tables: exact duplicates (ties -> smaller macro id must win), 1-ulp and
 1e-12 relative neighbours (inside the dominance margin: never pruned),
 clearly dominated rows (pruned), and rows where the winner changes with L.
@@ -130,3 +130,29 @@ def test_pruning_matches_unpruned_run():
         np.testing.assert_array_equal(outs[0][k], outs[1][k])
     for k in ("gl", "ll"):
         np.testing.assert_array_equal(outs[0][k].view(np.int64), outs[1][k].view(np.int64))
+
+
+def test_many_tile_classes_list_and_grid():
+    """More segments than the kernels stage headers for in shared memory
+    (320 distinct tile classes): the global-header variants of k_eval4 /
+    k_sweep2 against the oracle."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_10187_b200 import capi, synthetic as S
+
+    base = S.config_space(False)
+    n = 320
+    cfg = {k: np.resize(np.asarray(v), n) for k, v in base.items()}
+    cfg["id"] = np.arange(n, dtype=np.int32)
+    cfg["t_m"] = np.where(np.arange(n) % 2 == 0, 64, 128).astype(np.int64)
+    cfg["t_n"] = (16 + 8 * (np.arange(n) // 2)).astype(np.int64)   # 160 widths x 2 heights = 320 classes
+    cfg["t_k"] = np.full(n, 64, np.int64)
+    t = S.synthetic_tables(cfg)
+    pairs = S.LLAMA3_8B
+    M, N, K = queries(pairs, n=20000, seed=4)
+    res = run(capi, cfg, t, M, N, K, pairs)
+    tiles = {int(i): (int(a), int(b), int(c)) for i, a, b, c in zip(cfg["id"], cfg["t_m"], cfg["t_n"], cfg["t_k"])}
+    want = po.Oracle().tune(po.FlatTables(U.pytables_from_arrays(t), tiles), 148, 1, M, N, K)
+    for mode, (mac, mic, lat) in res.items():
+        np.testing.assert_array_equal(mac, want["macro"], err_msg=mode)
+        np.testing.assert_array_equal(U.bits(lat), U.bits(want["lat"]), err_msg=mode)
