@@ -139,6 +139,19 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
                            const wt_hw* hw, int device, wt_engine** out);
 wt_status wt_engine_destroy(wt_engine* e);
 wt_status wt_engine_info_get(const wt_engine* e, wt_engine_info* out);
+/* Host-only (no device needed): the exact pruning plan an engine built from
+ * (tables, registry, hw) would use -- for tests and inspection.  Segments
+ * are runs of <= 32 configs of one tile class; cls_cfg[pos] = config index
+ * (ascending macro_id order) at class position pos, segment s covers
+ * positions [seg_pos[s], seg_pos[s] + seg_n[s]); bit i of
+ * masks[(s * R + row) * 16 + lb] set = config seg_pos[s] + i may win in wave
+ * row `row`, L bucket lb (L in [2^lb, 2^(lb+1)), last bucket unbounded).
+ * Call with masks == NULL to get *n_seg, *R and *C; buffers are caller-owned
+ * (cls_cfg [C], seg_pos / seg_n [n_seg], masks [n_seg * R * 16]). */
+wt_status wt_prune_plan(const wt_tables_desc* tables, const wt_registry_desc* registry, const wt_hw* hw,
+                        int32_t* n_seg, int32_t* R, int32_t* C, int32_t* cls_cfg, int32_t* seg_pos,
+                        int32_t* seg_n, uint32_t* masks);
+
 /* Position of macro_id in the engine's ascending config order, or -1. */
 int32_t wt_engine_config_index(const wt_engine* e, int32_t macro_id);
 

@@ -96,7 +96,8 @@ EXPORTS = (
     "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_destroy wt_grid_storage wt_sweep wt_grid_finalize "
     "wt_gather_batch wt_decide_host_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
     "wt_simulate_batch wt_profile_sim wt_tune_one wt_engine_set_resident wt_baseline_create "
-    "wt_baseline_destroy wt_baseline_tune_batch wt_baseline_predict_batch wt_set_kernel_timing wt_kernel_time_ms").split()
+    "wt_baseline_destroy wt_baseline_tune_batch wt_baseline_predict_batch wt_set_kernel_timing wt_kernel_time_ms "
+    "wt_prune_plan").split()
 
 _lib = None
 
@@ -155,35 +156,60 @@ def _stream_ptr(stream):
     return getattr(stream, "cuda_stream", stream)
 
 
+def _descs(tables: dict, registry: dict, keep: list):
+    """ctypes descriptors of a table set + registry (arrays kept alive in `keep`)."""
+
+    def arr(x, dt):
+        a = np.ascontiguousarray(x, dtype=dt)
+        if a.size == 0:
+            a = np.zeros(1, dt)
+        keep.append(a)
+        return a.ctypes.data
+
+    td = wt_tables_desc()
+    td.n_tables = len(tables["macro_id"])
+    dts = dict(macro_id=np.int32, W=np.int32, theta_ext=np.float64, coeff_off=np.int32, coeff_w=np.int32,
+               coeff_theta=np.float64, awave_off=np.int32, awave_w=np.int32, awave_aoff=np.int32,
+               anchor_l=np.int64, anchor_micro=np.int32, ext_aoff=np.int32, ext_l=np.int64,
+               ext_micro=np.int32)
+    for k in _TABLE_FIELDS:
+        setattr(td, k, arr(tables[k], dts[k]))
+    rd = wt_registry_desc()
+    rd.family = registry.get("family", WT_FAMILY_DENSE_GEMM)
+    rd.n_macros = len(registry["id"])
+    rd.id = arr(registry["id"], np.int32)
+    rd.t_m = arr(registry["t_m"], np.int64)
+    rd.t_n = arr(registry["t_n"], np.int64)
+    rd.t_k = arr(registry["t_k"], np.int64)
+    return td, rd
+
+
+def prune_plan(tables: dict, registry: dict, n_sm: int, blocks_per_sm: int = 1):
+    """Host-only: the engine's exact pruning plan (wt_prune_plan) as numpy
+    arrays: cls_cfg [C], seg_pos / seg_n [n_seg], masks [n_seg, R, 16]."""
+    keep = []
+    td, rd = _descs(tables, registry, keep)
+    hw = wt_hw(n_sm, blocks_per_sm)
+    ns, R, Cn = C.c_int32(), C.c_int32(), C.c_int32()
+    check(lib().wt_prune_plan(C.byref(td), C.byref(rd), C.byref(hw), C.byref(ns), C.byref(R), C.byref(Cn),
+                              None, None, None, None))
+    cc = np.zeros(Cn.value, np.int32)
+    sp = np.zeros(ns.value, np.int32)
+    sn = np.zeros(ns.value, np.int32)
+    mk = np.zeros(ns.value * R.value * 16, np.uint32)
+    check(lib().wt_prune_plan(C.byref(td), C.byref(rd), C.byref(hw), C.byref(ns), C.byref(R), C.byref(Cn),
+                              C.c_void_p(cc.ctypes.data), C.c_void_p(sp.ctypes.data), C.c_void_p(sn.ctypes.data),
+                              C.c_void_p(mk.ctypes.data)))
+    return dict(cls_cfg=cc, seg_pos=sp, seg_n=sn, masks=mk.reshape(ns.value, R.value, 16), R=R.value)
+
+
 class Engine:
     """Owns a wt_engine (device image of tables + registry + hardware)."""
 
     def __init__(self, tables: dict, registry: dict, n_sm: int, blocks_per_sm: int = 1, device: int = 0):
         L = lib()
         self._keep = []
-
-        def arr(x, dt):
-            a = np.ascontiguousarray(x, dtype=dt)
-            if a.size == 0:
-                a = np.zeros(1, dt)
-            self._keep.append(a)
-            return a.ctypes.data
-
-        td = wt_tables_desc()
-        td.n_tables = len(tables["macro_id"])
-        dts = dict(macro_id=np.int32, W=np.int32, theta_ext=np.float64, coeff_off=np.int32, coeff_w=np.int32,
-                   coeff_theta=np.float64, awave_off=np.int32, awave_w=np.int32, awave_aoff=np.int32,
-                   anchor_l=np.int64, anchor_micro=np.int32, ext_aoff=np.int32, ext_l=np.int64,
-                   ext_micro=np.int32)
-        for k in _TABLE_FIELDS:
-            setattr(td, k, arr(tables[k], dts[k]))
-        rd = wt_registry_desc()
-        rd.family = registry.get("family", WT_FAMILY_DENSE_GEMM)
-        rd.n_macros = len(registry["id"])
-        rd.id = arr(registry["id"], np.int32)
-        rd.t_m = arr(registry["t_m"], np.int64)
-        rd.t_n = arr(registry["t_n"], np.int64)
-        rd.t_k = arr(registry["t_k"], np.int64)
+        td, rd = _descs(tables, registry, self._keep)
         hw = wt_hw(n_sm, blocks_per_sm)
         h = C.c_void_p()
         check(L.wt_engine_create(C.byref(td), C.byref(rd), C.byref(hw), C.c_int(device), C.byref(h)))

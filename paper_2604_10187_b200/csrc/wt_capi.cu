@@ -176,6 +176,29 @@ const char* wt_version(void) { return "wavetune-b200 0.1 (sm_100a)"; }
 int wt_abi_version(void) { return WT_ABI_VERSION; }
 int64_t wt_launch_count(void) { return g_launches.load(); }
 
+wt_status wt_prune_plan(const wt_tables_desc* tables, const wt_registry_desc* registry, const wt_hw* hw,
+                        int32_t* n_seg, int32_t* R, int32_t* C, int32_t* cls_cfg, int32_t* seg_pos,
+                        int32_t* seg_n, uint32_t* masks) {
+    if (!tables || !registry || !hw || !n_seg || !R || !C) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    HostImage h;
+    std::string err;
+    const wt_status st = build_image(*tables, *registry, *hw, &h, &err);
+    if (st != WT_OK) return set_err(st, err);
+    const int32_t ns = int32_t(h.seg_pos.size());
+    *n_seg = ns;
+    *R = h.R;
+    *C = h.C;
+    if (!masks) return WT_OK;
+    if (!cls_cfg || !seg_pos || !seg_n) return set_err(WT_INVALID_ARGUMENT, "null output buffer");
+    std::copy(h.cls_cfg.begin(), h.cls_cfg.end(), cls_cfg);
+    for (int32_t k = 0; k < ns; ++k) {
+        seg_pos[k] = h.seg_pos[k];
+        seg_n[k] = h.seg_tiles[4 * k + 3];
+    }
+    std::copy(h.segmask.begin(), h.segmask.end(), masks);
+    return WT_OK;
+}
+
 wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc* registry,
                            const wt_hw* hw, int device, wt_engine** out) {
     if (!tables || !registry || !hw || !out) return set_err(WT_INVALID_ARGUMENT, "null argument");

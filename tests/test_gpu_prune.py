@@ -24,34 +24,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def adversarial_tables():
-    from paper_2604_10187_b200 import synthetic as S
-
-    cfg = S.config_space(False)
-    t = S.synthetic_tables(cfg)
-    C, W = len(cfg["id"]), int(t["W"][0])
-    th = t["coeff_theta"].reshape(C, W, 4).copy()
-    te = t["theta_ext"].reshape(C, 4).copy()
-    key = list(zip(cfg["t_m"], cfg["t_n"], cfg["t_k"]))
-    classes = {}
-    for c, k in enumerate(key):
-        classes.setdefault(k, []).append(c)
-    rng = np.random.default_rng(7)
-    for cs in classes.values():
-        c0, c1, c2, c3, c4, c5 = cs[:6]
-        th[c1] = th[c0]                                   # exact tie: c0 (smaller id) must win
-        te[c1] = te[c0]
-        th[c2] = np.nextafter(th[c0], np.inf)             # 1 ulp worse: within margin, kept
-        th[c3] = th[c0] * (1 + 1e-12)                     # 1e-12 relative: kept
-        th[c4] = th[c0] * 1.5 + np.abs(th[c0]) * 0.1      # clearly dominated: pruned
-        te[c4] = te[c0] * 1.5 + np.abs(te[c0]) * 0.1
-        # c5: cheaper fixed cost, steeper per-iteration slope -> wins only at short L
-        th[c5, :, 1] = th[c0, :, 1] * 0.5
-        th[c5, :, 3] = th[c0, :, 3] * 0.5
-        th[c5, :, 0] = th[c0, :, 0] * (1.5 + rng.random())
-        th[c5, :, 2] = th[c0, :, 2] * (1.5 + rng.random())
-    t["coeff_theta"] = th.reshape(-1)
-    t["theta_ext"] = te.reshape(-1)
-    return cfg, t
+    return U.adversarial_tables()
 
 
 def run(capi, cfg, t, M, N, K, pairs):
