@@ -182,3 +182,37 @@ def test_macro_sharded_fit_equals_full_build(capi, world):
                 np.testing.assert_array_equal(v.view(np.int64), full[k].view(np.int64), err_msg=k)
             else:
                 np.testing.assert_array_equal(v, full[k], err_msg=k)
+
+
+def test_memmap_artifacts_feed_fit_and_engine(capi, tmp_path):
+    """Binary SoA images (artifact.py) loaded as memmap views go straight
+    into wt_fit_build / wt_engine_create: same tables, same decisions."""
+    import torch
+
+    from paper_2604_10187_b200 import artifact as A, synthetic as S
+
+    cfg = S.config_space(False)
+    rec = {k: np.asarray(v, A.RECORD_FIELDS[k]) for k, v in S.synthetic_records(cfg).items()}
+    A.save_records_bin(str(tmp_path / "r.wtr"), rec)
+    rm = A.load_records_bin(str(tmp_path / "r.wtr"))
+    f1 = capi.fit_build(rec, cfg["id"], 40, 10)
+    f2 = capi.fit_build(rm, cfg["id"], 40, 10)
+    for k in A.TABLE_FIELDS:
+        if k in f1:
+            np.testing.assert_array_equal(np.asarray(f1[k]), np.asarray(f2[k]), err_msg=k)
+    t = {k: f1[k] for k in A.TABLE_FIELDS if k in f1}
+    t["W"] = f1["W_arr"]
+    A.save_tables_bin(str(tmp_path / "t.wtt"), t)
+    tm = A.load_tables_bin(str(tmp_path / "t.wtt"))
+    reg = S.registry_arrays(cfg)
+    M, N, K = S.query_stream(5000, S.LLAMA3_8B, seed=2, off_grid_frac=0.5)
+    outs = []
+    for tab in (t, tm):
+        eng = capi.Engine(tab, reg, n_sm=148)
+        o = [torch.empty(len(M), dtype=d, device="cuda") for d in (torch.int32, torch.int32, torch.float64)]
+        eng.tune_batch(*(torch.from_numpy(x).cuda() for x in (M, N, K)), capi.Engine.decisions(*o))
+        torch.cuda.synchronize()
+        outs.append([x.cpu().numpy() for x in o])
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a.view(np.int64) if a.dtype == np.float64 else a,
+                                      b.view(np.int64) if b.dtype == np.float64 else b)
