@@ -389,6 +389,16 @@ def run_wavetune(args):
         g3.close()
         eng3.close()
 
+    if rank == 0 and ws == 1 and not args.skip_cpu and sec:
+        # config 1 beside its CPU baseline: the reference's tune() over the
+        # same 32,768 grid shapes on all host threads (one pass)
+        Mg = np.tile(np.arange(1, 8193, dtype=np.int32), len(pairs))
+        Ng = np.repeat(np.array([q[0] for q in pairs], np.int32), 8192)
+        Kg = np.repeat(np.array([q[1] for q in pairs], np.int32), 8192)
+        thr = host_threads()
+        r1, n1, t1 = reference_rate(Mg, Ng, Kg, cfg, tables, 1e9, thr)
+        sec["config1_sweep"]["cpu_reference"] = {"ms": 1e3 * max(t1), "shapes": int(n1), "threads": thr,
+                                                 "evals_per_s": n1 * eng.n_configs / max(t1)}
     if rank == 0:
         cpu = None
         if ws == 1 and not args.skip_cpu:
