@@ -364,8 +364,8 @@ __global__ void __launch_bounds__(kT3, 2) k_eval3(DevImage im, EvalArgs a, const
 // updates the running (latency, config index) winner in place -- strict-<
 // plus the index tie-break, i.e. the lexicographic order tune()'s ascending
 // strict-< scan produces (tuner.cpp:135-149).
-template <bool SPECIAL, bool HS>
-__global__ void __launch_bounds__(kT3, 2) k_eval4(DevImage im, EvalArgs a, const int4* rec, const int32_t* qhi) {
+template <bool SPECIAL, bool HS, int RPT>
+__global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval4(DevImage im, EvalArgs a, const int4* rec, const int32_t* qhi) {
     __shared__ int4 h_tiles[kMaxSmemSeg];
     __shared__ uint4 h_magic[kMaxSmemSeg];
     __shared__ int32_t h_pos[kMaxSmemSeg];
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kT3, 2) k_eval4(DevImage im, EvalArgs a, const
     const uint4* Ms = HS ? h_magic : im.seg_magic;
     const int32_t* Ps = HS ? h_pos : im.seg_pos;
     const int64_t n = a.count ? *a.count : a.n;
-    const int64_t nt = (n + 3) / 4;
+    const int64_t nt = (n + RPT - 1) / RPT;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     const int C = im.C, R = im.R;
     // Per-warp plan of 32 segments, built lane-parallel (lane = segment) from
@@ -395,13 +395,13 @@ __global__ void __launch_bounds__(kT3, 2) k_eval4(DevImage im, EvalArgs a, const
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < nt; base += stride) {
         const int64_t t = base + threadIdx.x;
-        uint32_t y2M[4], y2N[4], y2K[4], status[4], acc[4];
-        int64_t q[4];
-        double best[4];
-        int bci[4];  // winner's config index (INT32_MAX: none yet)
+        uint32_t y2M[RPT], y2N[RPT], y2K[RPT], status[RPT], acc[RPT];
+        int64_t q[RPT];
+        double best[RPT];
+        int bci[RPT];  // winner's config index (INT32_MAX: none yet)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int64_t i = t * 4 + j;
+        for (int j = 0; j < RPT; ++j) {
+            const int64_t i = t * RPT + j;
             const bool live = t < nt && i < n;
             uint32_t M = 1, N = 1, K = 1, st = 0;
             q[j] = -1;
@@ -419,12 +419,12 @@ __global__ void __launch_bounds__(kT3, 2) k_eval4(DevImage im, EvalArgs a, const
             acc[j] = 0;
         }
         uint32_t pm = 0, pn = 0, ps = 0xffffffffu;
-        uint32_t row[4] = {0, 0, 0, 0};
-        double gd[4] = {0, 0, 0, 0};
+        uint32_t row[RPT] = {};
+        double gd[RPT] = {};
         bool uni = false;
         // two-entry cache of L per t_k (tags = magic, shift)
         uint32_t tagA = 0xffffffffu, tagB = 0xffffffffu;
-        double ldA[4] = {0, 0, 0, 0}, ldB[4] = {0, 0, 0, 0};
+        double ldA[RPT] = {}, ldB[RPT] = {};
         uint32_t lbA = 0, lbB = 0;
         bool nextA = true;
         const uint32_t y2M0 = __shfl_sync(0xffffffffu, y2M[0], 0), y2N0 = __shfl_sync(0xffffffffu, y2N[0], 0),
@@ -461,13 +461,16 @@ __global__ void __launch_bounds__(kT3, 2) k_eval4(DevImage im, EvalArgs a, const
                 pn = mg.y;
                 ps = mg.w & 0xffffu;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < RPT; ++j) {
                     uint64_t g;
                     row[j] = row_for(im, y2M[j], y2N[j], mg, &g);
                     gd[j] = u64_to_f64(g);
                 }
                 const uint32_t r0 = __shfl_sync(0xffffffffu, row[0], 0);
-                uni = __all_sync(0xffffffffu, row[0] == r0 && row[1] == r0 && row[2] == r0 && row[3] == r0);
+                bool same = true;
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) same = same && row[j] == r0;
+                uni = __all_sync(0xffffffffu, same);
             }
             const uint32_t sk = (mg.w >> 16) & 0xffu;
             const uint32_t tag = mg.z ^ (sk << 24);
@@ -475,7 +478,7 @@ __global__ void __launch_bounds__(kT3, 2) k_eval4(DevImage im, EvalArgs a, const
                 double* ld = nextA ? ldA : ldB;
                 uint32_t lb = 0;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < RPT; ++j) {
                     const uint32_t L = mdiv2(y2K[j], mg.z, sk) + 1u;
                     ld[j] = u32_to_f64(L);
                     lb |= uint32_t(min(31 - __clz(int(L)), kLB - 1)) << (8 * j);
@@ -490,13 +493,15 @@ __global__ void __launch_bounds__(kT3, 2) k_eval4(DevImage im, EvalArgs a, const
                 nextA = !nextA;
             }
             const bool useA = tag == tagA;
-            double ld[4];
+            double ld[RPT];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) ld[j] = useA ? ldA[j] : ldB[j];
+            for (int j = 0; j < RPT; ++j) ld[j] = useA ? ldA[j] : ldB[j];
             const uint32_t lbp = useA ? lbA : lbB;
             // does the whole warp sit in the planned (row, L bucket) cell?
             const uint32_t cell = pcell[wid][s & 31];
-            const bool lbu = ((lbp ^ (lbp >> 8)) & 0x00ffffu) == 0 && ((lbp ^ (lbp >> 16)) & 0xffu) == 0;
+            bool lbu = true;
+#pragma unroll
+            for (int j = 1; j < RPT; ++j) lbu = lbu && ((lbp >> (8 * j)) & 0xffu) == (lbp & 0xffu);
             const bool inplan = __all_sync(0xffffffffu, uni && row[0] == (cell & 0xffffffu) && lbu &&
                                                             (lbp & 0xffu) == (cell >> 24));
             uint32_t live;
@@ -508,7 +513,7 @@ __global__ void __launch_bounds__(kT3, 2) k_eval4(DevImage im, EvalArgs a, const
                     const uint32_t* mk = im.segmask + size_t(s) * R * kLB;
                     live = 0;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) live |= __ldg(mk + row[j] * kLB + ((lbp >> (8 * j)) & 0xffu));
+                    for (int j = 0; j < RPT; ++j) live |= __ldg(mk + row[j] * kLB + ((lbp >> (8 * j)) & 0xffu));
                     live = __reduce_or_sync(0xffffffffu, live);
                 }
                 live &= ncfg >= 32 ? 0xffffffffu : ((1u << ncfg) - 1u);
@@ -516,24 +521,26 @@ __global__ void __launch_bounds__(kT3, 2) k_eval4(DevImage im, EvalArgs a, const
             int k_staged = 0;  // index of the next planned row in pth
             if constexpr (SPECIAL) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[j] |= __ldg(im.segor + size_t(s) * R + row[j]);
+                for (int j = 0; j < RPT; ++j) acc[j] |= __ldg(im.segor + size_t(s) * R + row[j]);
             }
             for (uint32_t mm = live; mm; mm &= mm - 1u) {
                 const int c = __ffs(int(mm)) - 1;
                 const int ci = __ldg(im.cls_cfg + pos + c);
-                double4 th[4];
+                double4 th[RPT];
                 if (inplan && k_staged < 2) {
                     th[0] = pth[wid][s & 31][k_staged++];
-                    th[1] = th[2] = th[3] = th[0];
+#pragma unroll
+                    for (int j = 1; j < RPT; ++j) th[j] = th[0];
                 } else if (uni) {
                     th[0] = ldg_row(im.theta2t + size_t(row[0]) * C + pos + c);
-                    th[1] = th[2] = th[3] = th[0];
+#pragma unroll
+                    for (int j = 1; j < RPT; ++j) th[j] = th[0];
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) th[j] = ldg_row(im.theta2t + size_t(row[j]) * C + pos + c);
+                    for (int j = 0; j < RPT; ++j) th[j] = ldg_row(im.theta2t + size_t(row[j]) * C + pos + c);
                 }
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < RPT; ++j) {
                     double tt = __dmul_rn(__dmul_rn(th[j].x, gd[j]), ld[j]);
                     tt = __dadd_rn(tt, __dmul_rn(th[j].y, gd[j]));
                     tt = __dadd_rn(tt, __dmul_rn(th[j].z, ld[j]));
@@ -546,7 +553,7 @@ __global__ void __launch_bounds__(kT3, 2) k_eval4(DevImage im, EvalArgs a, const
             }
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < RPT; ++j) {
             if (q[j] < 0) continue;
             Final f;
             uint64_t g = 0;
@@ -666,10 +673,28 @@ cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, b
         return v ? std::atoi(v) : 4;
     }();
     if (kern == 4) {
-        if (im.special)
-            hs ? k_eval4<true, true><<<g3, kT3, 0, st>>>(im, a, rec, qhi) : k_eval4<true, false><<<g3, kT3, 0, st>>>(im, a, rec, qhi);
-        else
-            hs ? k_eval4<false, true><<<g3, kT3, 0, st>>>(im, a, rec, qhi) : k_eval4<false, false><<<g3, kT3, 0, st>>>(im, a, rec, qhi);
+        static const int rpt = [] {
+            const char* v = std::getenv("WT_EVAL4_RPT");
+            const int x = v ? std::atoi(v) : 2;  // measured best on B200 (r01e: 2 > 1 > 4)
+            return x == 1 || x == 4 ? x : 2;
+        }();
+        auto go = [&](auto fn, int r) {
+            int o = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kT3, 0);
+            const int64_t w = (a.n + int64_t(r) * kT3 - 1) / (int64_t(r) * kT3);
+            const int g = int(std::max<int64_t>(1, std::min<int64_t>(w, int64_t(sms) * std::max(o, 1))));
+            fn<<<g, kT3, 0, st>>>(im, a, rec, qhi);
+        };
+#define WT_GO4(SP, H)                                         \
+    (rpt == 1   ? go(k_eval4<SP, H, 1>, 1)                    \
+     : rpt == 2 ? go(k_eval4<SP, H, 2>, 2)                    \
+                : go(k_eval4<SP, H, 4>, 4))
+        if (im.special) {
+            if (hs) WT_GO4(true, true); else WT_GO4(true, false);
+        } else {
+            if (hs) WT_GO4(false, true); else WT_GO4(false, false);
+        }
+#undef WT_GO4
         return cudaGetLastError();
     }
     if (im.special)
