@@ -1,3 +1,5 @@
+"""Minimal GPU smoke of the list evaluation (tune_batch on 1e2 / 5e3 / 1e5 off-grid
+queries) -- run under `timeout` before larger suites after touching wt_eval3.cu."""
 import sys, time
 sys.path[:0]=['/root/repo','/root/repo/oracle','/root/repo/tests']
 import numpy as np, torch
