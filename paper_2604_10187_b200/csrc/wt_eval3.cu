@@ -369,17 +369,22 @@ __global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval
     __shared__ int4 h_tiles[kMaxSmemSeg];
     __shared__ uint4 h_magic[kMaxSmemSeg];
     __shared__ int32_t h_pos[kMaxSmemSeg];
+    // HS: segment headers and the class-position -> config map (dynamic,
+    // C ints) in shared memory
+    extern __shared__ int32_t h_cls[];
     if (HS) {
         for (int i = threadIdx.x; i < im.nseg; i += blockDim.x) {
             h_tiles[i] = im.seg_tiles[i];
             h_magic[i] = im.seg_magic[i];
             h_pos[i] = im.seg_pos[i];
         }
+        for (int i = threadIdx.x; i < im.C; i += blockDim.x) h_cls[i] = im.cls_cfg[i];
     }
     __syncthreads();
     const int4* Ts = HS ? h_tiles : im.seg_tiles;
     const uint4* Ms = HS ? h_magic : im.seg_magic;
     const int32_t* Ps = HS ? h_pos : im.seg_pos;
+    auto cfg_at = [&](int pos) { return HS ? h_cls[pos] : __ldg(im.cls_cfg + pos); };
     const int64_t n = a.count ? *a.count : a.n;
     const int64_t nt = (n + RPT - 1) / RPT;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -525,7 +530,7 @@ __global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval
             }
             for (uint32_t mm = live; mm; mm &= mm - 1u) {
                 const int c = __ffs(int(mm)) - 1;
-                const int ci = __ldg(im.cls_cfg + pos + c);
+                const int ci = cfg_at(pos + c);
                 double4 th[RPT];
                 if (inplan && k_staged < 2) {
                     th[0] = pth[wid][s & 31][k_staged++];
@@ -678,21 +683,24 @@ cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, b
             const int x = v ? std::atoi(v) : 2;  // measured best on B200 (r01e: 2 > 1 > 4)
             return x == 1 || x == 4 ? x : 2;
         }();
+        const bool hs4 = hs && im.C <= 8192;
+        const size_t dyn = hs4 ? size_t(im.C) * sizeof(int32_t) : 0;
         auto go = [&](auto fn, int r) {
+            if (dyn > 16 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
             int o = 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kT3, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kT3, dyn);
             const int64_t w = (a.n + int64_t(r) * kT3 - 1) / (int64_t(r) * kT3);
             const int g = int(std::max<int64_t>(1, std::min<int64_t>(w, int64_t(sms) * std::max(o, 1))));
-            fn<<<g, kT3, 0, st>>>(im, a, rec, qhi);
+            fn<<<g, kT3, dyn, st>>>(im, a, rec, qhi);
         };
 #define WT_GO4(SP, H)                                         \
     (rpt == 1   ? go(k_eval4<SP, H, 1>, 1)                    \
      : rpt == 2 ? go(k_eval4<SP, H, 2>, 2)                    \
                 : go(k_eval4<SP, H, 4>, 4))
         if (im.special) {
-            if (hs) WT_GO4(true, true); else WT_GO4(true, false);
+            if (hs4) WT_GO4(true, true); else WT_GO4(true, false);
         } else {
-            if (hs) WT_GO4(false, true); else WT_GO4(false, false);
+            if (hs4) WT_GO4(false, true); else WT_GO4(false, false);
         }
 #undef WT_GO4
         return cudaGetLastError();
