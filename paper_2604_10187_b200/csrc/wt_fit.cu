@@ -285,9 +285,14 @@ __device__ FitOut warp_fit(const double* g, const double* l, const double* t, in
     __syncwarp();
     const double ss_tot = wdot(Wk, nullptr, 0, n, lane);
     o.r2 = ss_tot > 0 ? __dadd_rn(1.0, -__ddiv_rn(ss_res, ss_tot)) : (ss_res < 1e-18 ? 1.0 : 0.0);
+    // MAPE: the divisions in parallel, the sum sequential in sample order
+    // (the reference's loop order; same bits)
+    __syncwarp();
+    for (int r = lane; r < n; r += 32) Wk[r] = __ddiv_rn(fabs(__dadd_rn(t[r], -F[r])), fabs(t[r]));
+    __syncwarp();
     double mp = 0.0;
     if (lane == 0)
-        for (int r = 0; r < n; ++r) mp = __dadd_rn(mp, __ddiv_rn(fabs(__dadd_rn(t[r], -F[r])), fabs(t[r])));
+        for (int r = 0; r < n; ++r) mp = __dadd_rn(mp, Wk[r]);
     mp = __shfl_sync(FULL, mp, 0);
     o.mape = __ddiv_rn(mp, double(n));
     __syncwarp();
