@@ -116,6 +116,8 @@ __device__ void wbacksolve(const double* A, int n, int m, double* c, int lane) {
     __syncwarp();
 }
 
+constexpr int kFitScr = 19;  // scratch doubles per sample (warp_fit)
+
 struct FitOut {
     double c[4];
     double r2, mape;
@@ -130,7 +132,9 @@ __device__ FitOut warp_fit(const double* g, const double* l, const double* t, in
     double* Sub = A + 4 * size_t(n);  // reduced-fit columns
     double* Wk = Sub + 4 * size_t(n);
     double* F = Wk + size_t(n);
+    double* T = F + size_t(n);  // the latencies, read once from global memory
     for (int r = lane; r < n; r += 32) {
+        T[r] = t[r];
         D[r] = __dmul_rn(g[r], l[r]);
         D[n + r] = g[r];
         D[2 * size_t(n) + r] = l[r];
@@ -231,7 +235,7 @@ __device__ FitOut warp_fit(const double* g, const double* l, const double* t, in
     double x[4] = {0.0, 0.0, 0.0, 0.0};
     o.degenerate = 0;
     if (rank >= 4 && n >= 4) {
-        for (int r = lane; r < n; r += 32) Wk[r] = t[r];
+        for (int r = lane; r < n; r += 32) Wk[r] = T[r];
         __syncwarp();
         for (int k = 0; k < nz; ++k) wapply(A + size_t(k) * n, tau[k], Wk, k, n, lane);
         wbacksolve(A, n, nz, Wk, lane);
@@ -253,7 +257,7 @@ __device__ FitOut warp_fit(const double* g, const double* l, const double* t, in
             __syncwarp();
             for (int j = k + 1; j < keep; ++j) wapply(colk, ht[k], Sub + size_t(j) * n, k, n, lane);
         }
-        for (int r = lane; r < n; r += 32) Wk[r] = t[r];
+        for (int r = lane; r < n; r += 32) Wk[r] = T[r];
         __syncwarp();
         for (int k = 0; k < hs; ++k) wapply(Sub + size_t(k) * n, ht[k], Wk, k, n, lane);
         wbacksolve(Sub, n, hs, Wk, lane);
@@ -271,15 +275,15 @@ __device__ FitOut warp_fit(const double* g, const double* l, const double* t, in
         acc = __dadd_rn(acc, __dmul_rn(D[2 * size_t(n) + r], x[2]));
         acc = __dadd_rn(acc, __dmul_rn(D[3 * size_t(n) + r], x[3]));
         F[r] = acc;
-        const double d = __dadd_rn(t[r], -acc);
+        const double d = __dadd_rn(T[r], -acc);
         Wk[r] = __dmul_rn(d, d);
     }
     __syncwarp();
     const double ss_res = wdot(Wk, nullptr, 0, n, lane);
-    const double mean = __ddiv_rn(wdot(t, nullptr, 0, n, lane), double(n));
+    const double mean = __ddiv_rn(wdot(T, nullptr, 0, n, lane), double(n));
     __syncwarp();
     for (int r = lane; r < n; r += 32) {
-        const double d = __dadd_rn(t[r], -mean);
+        const double d = __dadd_rn(T[r], -mean);
         Wk[r] = __dmul_rn(d, d);
     }
     __syncwarp();
@@ -288,7 +292,7 @@ __device__ FitOut warp_fit(const double* g, const double* l, const double* t, in
     // MAPE: the divisions in parallel, the sum sequential in sample order
     // (the reference's loop order; same bits)
     __syncwarp();
-    for (int r = lane; r < n; r += 32) Wk[r] = __ddiv_rn(fabs(__dadd_rn(t[r], -F[r])), fabs(t[r]));
+    for (int r = lane; r < n; r += 32) Wk[r] = __ddiv_rn(fabs(__dadd_rn(T[r], -F[r])), fabs(T[r]));
     __syncwarp();
     double mp = 0.0;
     if (lane == 0)
@@ -554,14 +558,14 @@ constexpr int kFitSmemRows = 32;  // buckets up to 32 samples run entirely in sh
 
 __global__ void __launch_bounds__(32 * kFitWarps) k_fit(const double* sg, const double* sl, const double* st,
                                                         Buckets b, double* scratch) {
-    __shared__ double wscr[kFitWarps][18 * kFitSmemRows];
+    __shared__ double wscr[kFitWarps][kFitScr * kFitSmemRows];
     const int lane = threadIdx.x & 31;
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
     for (int64_t q = warp; q < b.nb; q += nw) {
         const int64_t lo = b.slo[q], n = b.shi[q] - lo;
         if (n <= 0) continue;
-        double* scr = n <= kFitSmemRows ? wscr[threadIdx.x >> 5] : scratch + 18 * lo;
+        double* scr = n <= kFitSmemRows ? wscr[threadIdx.x >> 5] : scratch + kFitScr * lo;
         FitOut o = warp_fit(sg + lo, sl + lo, st + lo, int(n), scr, lane);
         if (lane == 0) {
             for (int c = 0; c < 4; ++c) b.coeff[4 * q + c] = o.c[c];
@@ -661,7 +665,7 @@ __global__ void k_extrap(Rec rc, const double* sg, const double* sl, const doubl
         const int64_t gslice = m.gstart_of_bucket[b0];  // ext anchors slice for this macro
         if (used >= 2) {
             const int64_t lo = b.slo[wb0], n = b.shi[wb1 - 1] - lo;
-            FitOut o = warp_fit(sg + lo, sl + lo, st + lo, int(n), scratch + 18 * lo, lane);
+            FitOut o = warp_fit(sg + lo, sl + lo, st + lo, int(n), scratch + kFitScr * lo, lane);
             if (lane == 0) {
                 for (int c = 0; c < 4; ++c) m.theta[4 * q + c] = o.c[c];
                 m.flags[q] = o.degenerate ? 1 : 0;
@@ -1068,7 +1072,7 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
     double* sg = dalloc<double>(owned, S_total);
     double* sl = dalloc<double>(owned, S_total);
     double* stt = dalloc<double>(owned, S_total);
-    double* scratch = dalloc<double>(owned, 18 * S_total);
+    double* scratch = dalloc<double>(owned, kFitScr * S_total);
     if (!scratch) {
         g_fit_err = "cudaMalloc failed (fit scratch)";
         return WT_CUDA_ERROR;
@@ -1263,7 +1267,7 @@ wt_status wt_fit_bucket_batch(const double* g, const double* l, const double* t,
     double* dg = dalloc<double>(owned, S);
     double* dl = dalloc<double>(owned, S);
     double* dt = dalloc<double>(owned, S);
-    double* scr = dalloc<double>(owned, 18 * S);
+    double* scr = dalloc<double>(owned, kFitScr * S);
     int64_t* lo = dalloc<int64_t>(owned, nb);
     int64_t* hi = dalloc<int64_t>(owned, nb);
     std::vector<int64_t> hlo(nb), hhi(nb);
