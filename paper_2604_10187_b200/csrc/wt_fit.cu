@@ -633,6 +633,60 @@ __global__ void k_step(int64_t NM, const int64_t* mbs, const int64_t* bgs, const
     nslot[q] = n;
 }
 
+// The same step baseline, parallel over (macro, loop count): k_step_slots
+// lists each macro's distinct l ascending (the order the final insertion sort
+// of k_step produces), then one thread per (macro, slot) accumulates its
+// slot over the macro's groups in group order -- the identical sequence of
+// additions -- and divides.
+constexpr int kStepMaxSlots = 16;
+
+__global__ void k_step_slots(int64_t NM, const int64_t* mbs, const int64_t* bgs, const int64_t* gl, int64_t* slot_l,
+                             int32_t* nslot) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= NM) return;
+    const int64_t g0 = bgs[mbs[q]], g1 = bgs[mbs[q + 1]];
+    int n = 0;
+    for (int64_t grp = g0; grp < g1; ++grp) {
+        const int64_t l = gl[grp];
+        int s = 0;
+        while (s < n && slot_l[g0 + s] != l) ++s;
+        if (s == n) {
+            slot_l[g0 + n] = l;
+            ++n;
+        }
+    }
+    for (int a = 1; a < n; ++a)
+        for (int b = a; b > 0 && slot_l[g0 + b - 1] > slot_l[g0 + b]; --b) {
+            const int64_t tl = slot_l[g0 + b];
+            slot_l[g0 + b] = slot_l[g0 + b - 1];
+            slot_l[g0 + b - 1] = tl;
+        }
+    nslot[q] = n;
+}
+
+__global__ void k_step_sum(int64_t NM, const int64_t* mbs, const int64_t* bgs, const int64_t* gw, const int64_t* gl,
+                           const int64_t* soff, const int32_t* nsamp, const double* st, const int64_t* slot_l,
+                           const int32_t* nslot, double* slot_num, double* slot_den) {
+    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t q = idx / kStepMaxSlots;
+    if (q >= NM) return;
+    const int64_t g0 = bgs[mbs[q]], g1 = bgs[mbs[q + 1]];
+    for (int s = int(idx % kStepMaxSlots); s < nslot[q]; s += kStepMaxSlots) {  // > 16 slots: strided
+        const int64_t l = slot_l[g0 + s];
+        double num = 0.0, den = 0.0;
+        for (int64_t grp = g0; grp < g1; ++grp) {
+            if (gl[grp] != l) continue;
+            const double w = __ll2double_rn(gw[grp]);
+            for (int64_t i = soff[grp], e = soff[grp] + nsamp[grp]; i < e; ++i) {
+                num = __dadd_rn(num, __dmul_rn(w, st[i]));
+                den = __dadd_rn(den, __dmul_rn(w, w));
+            }
+        }
+        slot_num[g0 + s] = __ddiv_rn(num, den);
+        slot_den[g0 + s] = den;
+    }
+}
+
 struct Macros {
     int64_t nmac;
     const int64_t* bstart;  // [nmac+1] bucket range per macro
@@ -1110,8 +1164,19 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
     double* d_snum = dalloc<double>(owned, G);
     double* d_sden = dalloc<double>(owned, G);
     int32_t* d_nslot = dalloc<int32_t>(owned, NM);
-    k_step<<<int((NM + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, gw, gl, soff, gr.nsamp, stt, d_sll, d_snum,
-                                                  d_sden, d_nslot);
+    {
+        // slot counts per macro bound the parallel variant (distinct l per macro)
+        static const bool serial = std::getenv("WT_STEP_SERIAL") != nullptr;
+        if (serial) {
+            k_step<<<int((NM + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, gw, gl, soff, gr.nsamp, stt, d_sll, d_snum,
+                                                          d_sden, d_nslot);
+        } else {
+            k_step_slots<<<int((NM + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, gl, d_sll, d_nslot);
+            const int64_t nt = NM * kStepMaxSlots;
+            k_step_sum<<<int((nt + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, gw, gl, soff, gr.nsamp, stt, d_sll,
+                                                              d_nslot, d_snum, d_sden);
+        }
+    }
     CK(cudaEventRecord(ev1, s));
     trace("baselines");
 
