@@ -347,13 +347,16 @@ def run_wavetune(args):
         p3 = S.unique_pairs(S.LLAMA3_70B, S.QWEN2_72B)
         g3 = capi.Grid(eng3, [p[0] for p in p3], [p[1] for p in p3], 1, 65536)
         if ws > 1:
-            from paper_2604_10187_b200.dist import sharded_sweep
+            # NCCL all-gather by default; WT_FUSED_SWEEP=1: the sweep epilogue
+            # stores straight into the peers' grids (CUDA IPC over NVLink)
+            from paper_2604_10187_b200.dist import fused_sharded_sweep, sharded_sweep
 
-            sharded_sweep(g3, stream=stream)
+            sweep_n = fused_sharded_sweep if os.environ.get("WT_FUSED_SWEEP") == "1" else sharded_sweep
+            sweep_n(g3, stream=stream)
             torch.cuda.synchronize(dev)
             dist.barrier()
             e0.record(stream)
-            sharded_sweep(g3, stream=stream)
+            sweep_n(g3, stream=stream)
             e1.record(stream)
         else:
             g3.sweep(stream=stream)
@@ -377,7 +380,9 @@ def run_wavetune(args):
                                             "dominated in a (wave row, L bucket) cell are skipped "
                                             "(exact pruning, WT_PRUNE=0 evaluates all)",
                               "shapes": g3.n_entries, "configs": eng3.n_configs,
-                              "sharding": f"shape slices x{ws} + NCCL all_gather" if ws > 1 else "single GPU"},
+                              "sharding": (f"shape slices x{ws} + " + ("fused peer stores" if os.environ.get("WT_FUSED_SWEEP") == "1"
+                                                                      else "NCCL all_gather")) if ws > 1
+                                          else "single GPU"},
             "config4_fit": {"ms": fit_ms, "wall_ms_with_exchange": fit_wall_ms,
                             "sharding": f"macros x{ws} + all_gather_object" if ws > 1 else "single GPU",
                             "records": int(len(rec4["g"])), "tables": int(fit["n_tables"]),

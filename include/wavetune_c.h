@@ -303,6 +303,20 @@ wt_status wt_grid_storage(const wt_grid* g, wt_grid_entry** entries, int64_t* n_
  * A full-range sweep also rebuilds the grid's run index (below); a partial
  * one invalidates it until wt_grid_finalize. */
 wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, void* stream);
+/* Fused multi-GPU sweep: fills entries [begin, end) and stores each entry
+ * into every grid storage in dests[0..n_dests) (n_dests <= 8; this rank's
+ * own wt_grid_storage and its peers' storages opened with wt_ipc_open:
+ * stores travel over NVLink from the sweep's epilogue, no all-gather).  All
+ * destinations must have this grid's shape.  Afterwards (all ranks done:
+ * device sync + barrier) each rank calls wt_grid_finalize on its grid.
+ * Grids with top-k are not supported. */
+wt_status wt_sweep_to(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, wt_grid_entry* const* dests,
+                      int n_dests, void* stream);
+/* CUDA IPC handle (64 bytes) of the grid's storage and the entries' byte
+ * offset in it, for peers to open with wt_ipc_open. */
+wt_status wt_grid_ipc_handle(const wt_grid* g, void* handle, int64_t* offset);
+wt_status wt_ipc_open(const void* handle, int64_t offset, int device, wt_grid_entry** entries, void** base);
+wt_status wt_ipc_close(void* base);
 /* Rebuilds the run-compressed copy of the entries' heads (latency, macro,
  * micro are piecewise constant along M) that wt_gather_batch serves from
  * shared memory when it fits.  Stream-ordered, no host sync. */

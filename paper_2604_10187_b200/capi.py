@@ -97,7 +97,7 @@ EXPORTS = (
     "wt_gather_batch wt_decide_host_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
     "wt_simulate_batch wt_profile_sim wt_tune_one wt_engine_set_resident wt_baseline_create "
     "wt_baseline_destroy wt_baseline_tune_batch wt_baseline_predict_batch wt_set_kernel_timing wt_kernel_time_ms "
-    "wt_prune_plan").split()
+    "wt_prune_plan wt_sweep_to wt_grid_ipc_handle wt_ipc_open wt_ipc_close").split()
 
 _lib = None
 
@@ -360,6 +360,21 @@ class Grid:
         check(lib().wt_sweep(self.engine.handle, self.handle, C.c_int64(begin), C.c_int64(end),
                              vp(_stream_ptr(stream))))
 
+    def sweep_to(self, dest_ptrs, begin=0, end=None, stream=None):
+        """Fused sweep: entries [begin, end) stored into every grid storage in
+        `dest_ptrs` (device addresses: this grid's, peers' via ipc_open)."""
+        end = self.n_entries if end is None else end
+        arr = (C.c_void_p * len(dest_ptrs))(*[C.c_void_p(int(p)) for p in dest_ptrs])
+        check(lib().wt_sweep_to(self.engine.handle, self.handle, C.c_int64(begin), C.c_int64(end), arr,
+                                C.c_int(len(dest_ptrs)), vp(_stream_ptr(stream))))
+
+    def ipc_handle(self):
+        """(64-byte CUDA IPC handle of the storage, byte offset of the entries)."""
+        h = (C.c_char * 64)()
+        off = C.c_int64()
+        check(lib().wt_grid_ipc_handle(self.handle, h, C.byref(off)))
+        return bytes(h), off.value
+
     def finalize(self, stream=None):
         """Rebuild the run index after entries were written directly (e.g. the
         all-gather of a sharded sweep); a full sweep() does it itself."""
@@ -395,6 +410,18 @@ def _np_from(ptr, n, dt):
         return np.zeros(0, dt)
     ct = {np.int32: C.c_int32, np.int64: C.c_int64, np.float64: C.c_double}[dt]
     return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ct)), shape=(n,)).copy()
+
+
+def ipc_open(handle: bytes, offset: int, device: int = 0):
+    """Map a peer's grid storage (wt_ipc_open): returns (entries address, base)."""
+    h = (C.c_char * 64).from_buffer_copy(handle)
+    ent, base = C.c_void_p(), C.c_void_p()
+    check(lib().wt_ipc_open(h, C.c_int64(offset), C.c_int(device), C.byref(ent), C.byref(base)))
+    return ent.value, base.value
+
+
+def ipc_close(base):
+    check(lib().wt_ipc_close(C.c_void_p(base)))
 
 
 def fit_build(records: dict, registry_ids, W: int = 0, p: int = 10, device: int = 0):

@@ -941,6 +941,75 @@ wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, v
     return WT_OK;
 }
 
+wt_status wt_sweep_to(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, wt_grid_entry* const* dests,
+                      int n_dests, void* stream) {
+    if (!e || !g || !dests) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    if (g->eng != e) return set_err(WT_INVALID_ARGUMENT, "grid was created for another engine");
+    if (n_dests < 1 || n_dests > 8) return set_err(WT_INVALID_ARGUMENT, "n_dests must be in [1, 8]");
+    if (g->topk > 0) return set_err(WT_UNSUPPORTED, "fused sweeps cover grids without top-k");
+    if (begin < 0 || end > g->n_entries || begin > end)
+        return set_err(WT_OUT_OF_RANGE, "sweep range outside the grid");
+    for (int d = 0; d < n_dests; ++d)
+        if (!dests[d]) return set_err(WT_INVALID_ARGUMENT, "null destination grid");
+    if (begin == end) return WT_OK;
+    DeviceGuard guard(e->device);
+    SweepArgs a{};
+    a.N = g->dN;
+    a.K = g->dK;
+    a.m_lo = g->m_lo;
+    a.mcount = g->mcount;
+    a.begin = begin;
+    a.end = end;
+    a.chunk = g->sweep_chunk;
+    a.entries = g->entries;
+    for (int d = 0; d < n_dests; ++d) a.dst[d] = dests[d];
+    a.ndst = n_dests;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    void* scratch = nullptr;
+    const size_t sb = sweep2_scratch_bytes(e->dev, a);
+    cudaError_t ce = cudaSuccess;
+    if (sb) ce = cudaMallocFromPoolAsync(&scratch, sb, lib_pool(e->device), s);
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep_to: scratch");
+    ce = launch_sweep2(e->dev, a, g->wide, scratch, s);
+    if (scratch) cudaFreeAsync(scratch, s);
+    g_launches += sb ? 2 : 1;
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep_to");
+    // this grid's own run index is stale until the caller finalizes it
+    if (g->runs.budget > 0) cudaMemsetAsync(g->runs.hdr, 0, 4, s);
+    return WT_OK;
+}
+
+wt_status wt_grid_ipc_handle(const wt_grid* g, void* handle, int64_t* offset) {
+    if (!g || !handle || !offset) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    DeviceGuard guard(g->eng->device);
+    cudaIpcMemHandle_t h;
+    const cudaError_t ce = cudaIpcGetMemHandle(&h, g->mem);
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_grid_ipc_handle");
+    std::memcpy(handle, &h, sizeof(h));
+    *offset = reinterpret_cast<char*>(g->entries) - static_cast<char*>(g->mem);
+    return WT_OK;
+}
+
+wt_status wt_ipc_open(const void* handle, int64_t offset, int device, wt_grid_entry** entries, void** base) {
+    if (!handle || !entries || !base) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    DeviceGuard guard(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* p = nullptr;
+    const cudaError_t ce = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_ipc_open");
+    *base = p;
+    *entries = reinterpret_cast<wt_grid_entry*>(static_cast<char*>(p) + offset);
+    return WT_OK;
+}
+
+wt_status wt_ipc_close(void* base) {
+    if (!base) return WT_OK;
+    const cudaError_t ce = cudaIpcCloseMemHandle(base);
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_ipc_close");
+    return WT_OK;
+}
+
 wt_status wt_grid_finalize(const wt_engine* e, wt_grid* g, void* stream) {
     if (!e || !g) return set_err(WT_INVALID_ARGUMENT, "null argument");
     if (g->eng != e) return set_err(WT_INVALID_ARGUMENT, "grid was created for another engine");

@@ -40,7 +40,29 @@ struct SweepArgs {
     int32_t topk;
     int32_t* topk_macro;
     double* topk_lat;
+    // fused multi-GPU sweep (wt_sweep_to): the epilogue stores every entry
+    // into each of these grids (local or peer-mapped over NVLink) instead of
+    // `entries`; ndst == 0 -> `entries` only
+    wt_grid_entry* dst[8];
+    int32_t ndst;
 };
+
+#ifdef __CUDACC__
+// one grid entry into `entries` or into every destination of a fused sweep
+__device__ __forceinline__ void store_entry(const SweepArgs& a, int64_t idx, int4 lo, int4 hi) {
+    if (a.ndst == 0) {
+        int4* e = reinterpret_cast<int4*>(a.entries + idx);
+        e[0] = lo;
+        e[1] = hi;
+        return;
+    }
+    for (int d = 0; d < a.ndst; ++d) {
+        int4* e = reinterpret_cast<int4*>(a.dst[d] + idx);
+        e[0] = lo;
+        e[1] = hi;
+    }
+}
+#endif
 
 struct EvalArgs {
     const int32_t* M;

@@ -287,9 +287,7 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
             hi.y = int(f.flags);
             hi.z = f.comps;
             hi.w = __float_as_int(f.tail);
-            int4* e = reinterpret_cast<int4*>(a.entries + idx);
-            e[0] = lo;
-            e[1] = hi;
+            store_entry(a, idx, lo, hi);
         }
         seg0 = seg_end;
     }
@@ -337,9 +335,7 @@ __global__ void k_sweep_merge(DevImage im, SweepArgs a, Part part) {
     hi.y = int(f.flags);
     hi.z = f.comps;
     hi.w = __float_as_int(f.tail);
-    int4* e = reinterpret_cast<int4*>(a.entries + idx);
-    e[0] = lo;
-    e[1] = hi;
+    store_entry(a, idx, lo, hi);
 }
 
 // One staged segment against the RPT shapes of a thread: class-level integer

@@ -44,6 +44,43 @@ def gather_grid(local_full: torch.Tensor, n_entries: int, group=None, fill=None)
     return staging
 
 
+def fused_sharded_sweep(grid, group=None, stream=None):
+    """The sweep with the exchange fused into its epilogue: every rank maps
+    its peers' grid storages (CUDA IPC over NVLink) and its sweep kernel
+    stores each entry of its slice into all of them -- the transfer overlaps
+    the computation tile by tile and no all-gather follows.  Two barriers:
+    mappings ready, all stores landed; then each rank rebuilds its run index.
+    (Single-process tests drive the same multi-destination epilogue with
+    several local grids: tests/test_gpu_decide.py::test_sweep_to_*.)"""
+    from . import capi
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = grid.engine.device
+    lo, hi, _ = shard_bounds(grid.n_entries, world, rank)
+    mine = grid.ipc_handle()
+    handles = [None] * world
+    dist.all_gather_object(handles, mine, group=group)
+    dests, opened = [grid.entries_ptr], []
+    try:
+        for r in range(world):
+            if r != rank:
+                ent, base = capi.ipc_open(handles[r][0], handles[r][1], dev)
+                dests.append(ent)
+                opened.append(base)
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)
+        if hi > lo:
+            grid.sweep_to(dests, lo, hi, stream=stream)
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)
+        grid.finalize(stream=stream)
+    finally:
+        for b in opened:
+            capi.ipc_close(b)
+    return grid
+
+
 def sharded_sweep(grid, group=None, stream=None):
     """Fill `grid` (a capi.Grid, identical on every rank) cooperatively:
     each rank sweeps its slice, then the NCCL all-gather replicates it."""

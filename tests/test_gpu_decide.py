@@ -553,3 +553,41 @@ def test_decide_host_pipeline_matches_device(capi, synth256, chunk):
     grid.decide_host(Mp, Np, Kp, mac, mic, lat, chunk=chunk)
     assert torch.equal(mac, out[0].cpu()) and torch.equal(mic, out[1].cpu())
     assert torch.equal(lat.view(torch.int64), out[2].cpu().view(torch.int64))
+
+
+def test_sweep_to_fills_every_destination(capi, synth256):
+    """The fused sweep's multi-destination epilogue (wt_sweep_to), driven in
+    one process: rank slices swept into two local grids (standing in for
+    peer-mapped storages) give, in both, exactly the single full sweep --
+    with and without config splits (k_sweep_merge)."""
+    from paper_2604_10187_b200 import synthetic as S
+    from paper_2604_10187_b200.dist import shard_bounds
+
+    cfg, t, reg = synth256
+    eng = capi.Engine(t, reg, n_sm=148)
+    pairs = S.LLAMA3_8B
+    full = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 3001)
+    full.sweep()
+    for world in (2, 3):
+        grids = [capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 3001) for _ in range(world)]
+        for g in grids:
+            g.entries_tensor().fill_(-7)
+        ptrs = [g.entries_ptr for g in grids]
+        for r, g in enumerate(grids):
+            lo, hi, _ = shard_bounds(g.n_entries, world, r)
+            g.sweep_to(ptrs[r:] + ptrs[:r], lo, hi)
+        torch.cuda.synchronize()
+        for g in grids:
+            g.finalize()
+            assert torch.equal(g.entries_tensor(), full.entries_tensor())
+        # the finalized run index serves gathers
+        M, N, K = S.query_stream(5000, pairs, seed=4, off_grid_frac=0.0, m_max=3001)
+        outs = []
+        for g in (grids[0], full):
+            o = [torch.empty(len(M), dtype=d, device="cuda") for d in (torch.int32, torch.int32, torch.float64)]
+            g.gather(dev(M), dev(N), dev(K), capi.Engine.decisions(*o))
+            torch.cuda.synchronize()
+            outs.append([x.cpu() for x in o])
+        for a, b in zip(*outs):
+            assert torch.equal(a.view(torch.int64) if a.dtype == torch.float64 else a,
+                               b.view(torch.int64) if b.dtype == torch.float64 else b)
