@@ -1142,7 +1142,28 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
         return set_err(WT_INVALID_ARGUMENT, "topk must match the grid's topk");
     if (n <= 0) return n == 0 ? WT_OK : set_err(WT_INVALID_ARGUMENT, "negative batch size");
     DeviceGuard guard(e->device);
-    return gather_impl(e, g, M, N, K, n, out, static_cast<cudaStream_t>(stream), nullptr, nullptr);
+    // batches beyond 2^28 queries run in stream-ordered slices, bounding the
+    // compaction / evaluation scratch (~44 B per query of a slice)
+    constexpr int64_t kSlice = int64_t(1) << 28;
+    for (int64_t i = 0; i < n; i += kSlice) {
+        const int64_t m = std::min(kSlice, n - i);
+        wt_decisions d = *out;
+        d.macro_id += i;
+        d.micro_id += i;
+        d.latency_us += i;
+        if (d.g) d.g += i;
+        if (d.l) d.l += i;
+        if (d.wave) d.wave += i;
+        if (d.flags) d.flags += i;
+        if (d.comparisons) d.comparisons += i;
+        if (d.tail_frac) d.tail_frac += i;
+        if (d.topk_macro) d.topk_macro += i * d.topk;
+        if (d.topk_latency) d.topk_latency += i * d.topk;
+        const wt_status st2 =
+            gather_impl(e, g, M + i, N + i, K + i, m, &d, static_cast<cudaStream_t>(stream), nullptr, nullptr);
+        if (st2 != WT_OK) return st2;
+    }
+    return WT_OK;
 }
 
 wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_t* M,
