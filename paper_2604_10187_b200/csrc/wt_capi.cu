@@ -406,6 +406,35 @@ static cudaError_t run_list_eval(const wt_engine* e, const EvalArgs& a, cudaStre
     return ce;
 }
 
+// the decisions of queries [i, ...) of a batch (pointer offsets)
+static wt_decisions offset_decisions(const wt_decisions& o, int64_t i) {
+    wt_decisions d = o;
+    d.macro_id += i;
+    d.micro_id += i;
+    d.latency_us += i;
+    if (d.g) d.g += i;
+    if (d.l) d.l += i;
+    if (d.wave) d.wave += i;
+    if (d.flags) d.flags += i;
+    if (d.comparisons) d.comparisons += i;
+    if (d.tail_frac) d.tail_frac += i;
+    if (d.topk_macro) d.topk_macro += i * d.topk;
+    if (d.topk_latency) d.topk_latency += i * d.topk;
+    return d;
+}
+
+// scratch-bounding slice of huge batches (WT_BATCH_SLICE overrides, for tests;
+// multiples of 4 keep the 16-byte alignment of the sliced arrays)
+static int64_t batch_slice() {
+    static const int64_t v = [] {
+        const char* x = std::getenv("WT_BATCH_SLICE");
+        const int64_t d = int64_t(1) << 28;
+        const int64_t s = x ? std::atoll(x) : d;
+        return s >= 4 ? s & ~int64_t(3) : d;
+    }();
+    return v;
+}
+
 wt_status wt_tune_batch(const wt_engine* e, const int32_t* M, const int32_t* N, const int32_t* K,
                         int64_t n, const wt_decisions* out, void* stream) {
     if (!e) return set_err(WT_INVALID_ARGUMENT, "null engine");
@@ -429,7 +458,18 @@ wt_status wt_tune_batch(const wt_engine* e, const int32_t* M, const int32_t* N, 
         ce = launch_eval(e->dev, a, int(std::min<int64_t>(tiles, e->eval_grid)), static_cast<cudaStream_t>(stream));
         g_launches++;
     } else {
-        ce = run_list_eval(e, a, static_cast<cudaStream_t>(stream));
+        ce = cudaSuccess;
+        const int64_t kBatchSlice = batch_slice();
+        for (int64_t i = 0; i < n && ce == cudaSuccess; i += kBatchSlice) {
+            const wt_decisions d = offset_decisions(*out, i);
+            EvalArgs b = a;
+            b.M = M + i;
+            b.N = N + i;
+            b.K = K + i;
+            b.n = std::min(kBatchSlice, n - i);
+            b.out = to_out(&d);
+            ce = run_list_eval(e, b, static_cast<cudaStream_t>(stream));
+        }
     }
     if (ce != cudaSuccess) return cuda_err(ce, "wt_tune_batch");
     return WT_OK;
@@ -1144,21 +1184,10 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
     DeviceGuard guard(e->device);
     // batches beyond 2^28 queries run in stream-ordered slices, bounding the
     // compaction / evaluation scratch (~44 B per query of a slice)
-    constexpr int64_t kSlice = int64_t(1) << 28;
-    for (int64_t i = 0; i < n; i += kSlice) {
-        const int64_t m = std::min(kSlice, n - i);
-        wt_decisions d = *out;
-        d.macro_id += i;
-        d.micro_id += i;
-        d.latency_us += i;
-        if (d.g) d.g += i;
-        if (d.l) d.l += i;
-        if (d.wave) d.wave += i;
-        if (d.flags) d.flags += i;
-        if (d.comparisons) d.comparisons += i;
-        if (d.tail_frac) d.tail_frac += i;
-        if (d.topk_macro) d.topk_macro += i * d.topk;
-        if (d.topk_latency) d.topk_latency += i * d.topk;
+    const int64_t kBatchSlice = batch_slice();
+    for (int64_t i = 0; i < n; i += kBatchSlice) {
+        const int64_t m = std::min(kBatchSlice, n - i);
+        const wt_decisions d = offset_decisions(*out, i);
         const wt_status st2 =
             gather_impl(e, g, M + i, N + i, K + i, m, &d, static_cast<cudaStream_t>(stream), nullptr, nullptr);
         if (st2 != WT_OK) return st2;

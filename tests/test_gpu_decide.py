@@ -464,6 +464,7 @@ def test_sharded_sweep_equals_full(capi, synth256):
     {"WT_EVAL_KERNEL": "3"},
     {"WT_EVAL4_RPT": "4"},
     {"WT_EVAL4_RPT": "1"},
+    {"WT_BATCH_SLICE": "4100"},
 ])
 def test_launch_variants(capi, env):
     """Every launch shape the tuning knobs can select stays bit-exact."""
