@@ -268,6 +268,7 @@ __device__ FitOut warp_fit(const double* g, const double* l, const double* t, in
         x[c] = __ddiv_rn(x[c], scale[c]);
         o.c[c] = x[c];
     }
+    __syncwarp();  // every lane has read the solution out of Wk before it is reused below
     // residuals (model.cpp:64-75)
     for (int r = lane; r < n; r += 32) {
         double acc = __dmul_rn(D[r], x[0]);
