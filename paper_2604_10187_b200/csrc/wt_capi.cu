@@ -2,6 +2,7 @@
 // Owns device images (engines) and decision grids, validates inputs the way
 // the reference does, and launches the sm_100a kernels of wt_decide.cu.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -15,6 +16,16 @@
 #include "wavetune_c.h"
 #include "wt_decide.h"
 #include "wt_internal.h"
+
+namespace {
+// NVTX range around each C-ABI entry point (a no-op unless a tool -- nsys,
+// ncu --nvtx -- is attached): the library's calls show up by name on timelines.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 
 using namespace wtb;
 
@@ -201,6 +212,7 @@ wt_status wt_prune_plan(const wt_tables_desc* tables, const wt_registry_desc* re
 
 wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc* registry,
                            const wt_hw* hw, int device, wt_engine** out) {
+    NvtxRange nvtx_("wt_engine_create");
     if (!tables || !registry || !hw || !out) return set_err(WT_INVALID_ARGUMENT, "null argument");
     *out = nullptr;
     auto* e = new wt_engine;
@@ -437,6 +449,7 @@ static int64_t batch_slice() {
 
 wt_status wt_tune_batch(const wt_engine* e, const int32_t* M, const int32_t* N, const int32_t* K,
                         int64_t n, const wt_decisions* out, void* stream) {
+    NvtxRange nvtx_("wt_tune_batch");
     if (!e) return set_err(WT_INVALID_ARGUMENT, "null engine");
     if (n < 0) return set_err(WT_INVALID_ARGUMENT, "negative batch size");
     wt_status st = check_out(out);
@@ -800,6 +813,7 @@ wt_status wt_nearest_anchor_batch(const int64_t* anchors, int32_t n_anchors, con
 
 // ------------------------------------------------------------------ grid
 wt_status wt_grid_create(const wt_engine* e, const wt_grid_desc* desc, wt_grid** out) {
+    NvtxRange nvtx_("wt_grid_create");
     if (!e || !desc || !out) return set_err(WT_INVALID_ARGUMENT, "null argument");
     *out = nullptr;
     if (desc->n_pairs <= 0) return set_err(WT_INVALID_ARGUMENT, "grid needs at least one (N, K) pair");
@@ -936,6 +950,7 @@ wt_status wt_grid_storage(const wt_grid* g, wt_grid_entry** entries, int64_t* n_
 }
 
 wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, void* stream) {
+    NvtxRange nvtx_("wt_sweep");
     if (!e || !g) return set_err(WT_INVALID_ARGUMENT, "null argument");
     if (g->eng != e) return set_err(WT_INVALID_ARGUMENT, "grid was created for another engine");
     if (begin < 0 || end > g->n_entries || begin > end)
@@ -983,6 +998,7 @@ wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, v
 
 wt_status wt_sweep_to(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, wt_grid_entry* const* dests,
                       int n_dests, void* stream) {
+    NvtxRange nvtx_("wt_sweep_to");
     if (!e || !g || !dests) return set_err(WT_INVALID_ARGUMENT, "null argument");
     if (g->eng != e) return set_err(WT_INVALID_ARGUMENT, "grid was created for another engine");
     if (n_dests < 1 || n_dests > 8) return set_err(WT_INVALID_ARGUMENT, "n_dests must be in [1, 8]");
@@ -1051,6 +1067,7 @@ wt_status wt_ipc_close(void* base) {
 }
 
 wt_status wt_grid_finalize(const wt_engine* e, wt_grid* g, void* stream) {
+    NvtxRange nvtx_("wt_grid_finalize");
     if (!e || !g) return set_err(WT_INVALID_ARGUMENT, "null argument");
     if (g->eng != e) return set_err(WT_INVALID_ARGUMENT, "grid was created for another engine");
     if (g->runs.budget <= 0) return WT_OK;
@@ -1174,6 +1191,7 @@ extern "C" {
 
 wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M, const int32_t* N,
                           const int32_t* K, int64_t n, const wt_decisions* out, void* stream) {
+    NvtxRange nvtx_("wt_gather_batch");
     if (!e || !g) return set_err(WT_INVALID_ARGUMENT, "null argument");
     if (g->eng != e) return set_err(WT_INVALID_ARGUMENT, "grid was created for another engine");
     wt_status st = check_out(out);
@@ -1198,6 +1216,7 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
 wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_t* M,
                               const int32_t* N, const int32_t* K, int64_t n, int32_t* macro_id,
                               int32_t* micro_id, double* latency_us, int64_t chunk) {
+    NvtxRange nvtx_("wt_decide_host_sync");
     if (!e || !M || !N || !K || !macro_id || !micro_id || !latency_us)
         return set_err(WT_INVALID_ARGUMENT, "null argument");
     if (n <= 0) return n == 0 ? WT_OK : set_err(WT_INVALID_ARGUMENT, "negative batch size");
