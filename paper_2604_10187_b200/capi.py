@@ -391,7 +391,9 @@ class Grid:
                                         C.c_int64(chunk)))
 
     def entries_tensor(self):
-        """The grid's device storage viewed as an int32 [n_entries, 8] torch tensor (no copy)."""
+        """The grid's device storage viewed as an int32 [n_entries, 8] torch tensor (no copy).
+        After writing through it, call finalize(): the gather serves answers
+        from the run index built from the entries, not from the entries."""
         import torch
 
         class _Cuda:
