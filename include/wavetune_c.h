@@ -295,8 +295,10 @@ typedef struct {
 
 wt_status wt_grid_create(const wt_engine* e, const wt_grid_desc* desc, wt_grid** out);
 wt_status wt_grid_destroy(wt_grid* g);
-/* Raw device storage (for collectives / inspection).  After writing entries
- * through it (e.g. an all-gather of sweep shards) call wt_grid_finalize. */
+/* Raw device storage (for collectives / inspection).  Taking it invalidates
+ * the grid's run index (gathers then read the entries from L2) until the next
+ * full wt_sweep or wt_grid_finalize -- call finalize after writing entries
+ * (e.g. an all-gather of sweep shards). */
 wt_status wt_grid_storage(const wt_grid* g, wt_grid_entry** entries, int64_t* n_entries,
                           int32_t** topk_macro, double** topk_latency);
 /* Fills entries [begin, end) (flattened index) -- one shard of the sweep.

@@ -392,8 +392,10 @@ class Grid:
 
     def entries_tensor(self):
         """The grid's device storage viewed as an int32 [n_entries, 8] torch tensor (no copy).
-        After writing through it, call finalize(): the gather serves answers
-        from the run index built from the entries, not from the entries."""
+        Taking it invalidates the run index (gathers fall back to reading the
+        entries) until finalize() or a full sweep() rebuilds it."""
+        ent, n = C.c_void_p(), C.c_int64()
+        check(lib().wt_grid_storage(self.handle, C.byref(ent), C.byref(n), None, None))
         import torch
 
         class _Cuda:

@@ -942,6 +942,12 @@ wt_status wt_grid_destroy(wt_grid* g) {
 wt_status wt_grid_storage(const wt_grid* g, wt_grid_entry** entries, int64_t* n_entries,
                           int32_t** topk_macro, double** topk_latency) {
     if (!g) return set_err(WT_INVALID_ARGUMENT, "null grid");
+    // whoever takes the raw storage may write it: the run index is stale
+    // until the next full sweep / wt_grid_finalize (gathers read L2 meanwhile)
+    if (g->runs.budget > 0) {
+        DeviceGuard guard(g->eng->device);
+        cudaMemset(g->runs.hdr, 0, 4);
+    }
     if (entries) *entries = g->entries;
     if (n_entries) *n_entries = g->n_entries;
     if (topk_macro) *topk_macro = g->tk_macro;
