@@ -43,9 +43,6 @@ constexpr int kT3 = 256;
 constexpr int kMaxSmemSeg = 256;  // segment headers staged in shared memory up to this count
 constexpr double kInf3 = __builtin_huge_val();
 
-__device__ __forceinline__ bool lex_less3(double a, int ia, double b, int ib) {
-    return a < b || (a == b && ia < ib);
-}
 
 }  // namespace
 
