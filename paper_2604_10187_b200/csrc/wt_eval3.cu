@@ -395,6 +395,10 @@ __global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval
     __shared__ __align__(16) double4 pth[kT3 / 32][32][2];
     __shared__ uint32_t pmask[kT3 / 32][32], pcell[kT3 / 32][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // this warp's plan slices, addressed once (not re-derived per segment)
+    double4 (*const my_pth)[2] = pth[wid];
+    uint32_t* const my_pmask = pmask[wid];
+    uint32_t* const my_pcell = pcell[wid];
     for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < nt; base += stride) {
         const int64_t t = base + threadIdx.x;
         uint32_t y2M[RPT], y2N[RPT], y2K[RPT], status[RPT], acc[RPT];
@@ -447,12 +451,12 @@ __global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval
                     m &= nq >= 32 ? 0xffffffffu : ((1u << nq) - 1u);
                     cell = r | (lb << 24);
                     const double4* tp = im.theta2t + size_t(r) * C + Ps[sg];
-                    if (m) pth[wid][lane][0] = ldg_row(tp + (__ffs(int(m)) - 1));
+                    if (m) my_pth[lane][0] = ldg_row(tp + (__ffs(int(m)) - 1));
                     const uint32_t m2 = m & (m - 1u);
-                    if (m2) pth[wid][lane][1] = ldg_row(tp + (__ffs(int(m2)) - 1));
+                    if (m2) my_pth[lane][1] = ldg_row(tp + (__ffs(int(m2)) - 1));
                 }
-                pmask[wid][lane] = m;
-                pcell[wid][lane] = cell;
+                my_pmask[lane] = m;
+                my_pcell[lane] = cell;
                 __syncwarp();
             }
             const uint4 mg = Ms[s];
@@ -500,7 +504,7 @@ __global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval
             for (int j = 0; j < RPT; ++j) ld[j] = useA ? ldA[j] : ldB[j];
             const uint32_t lbp = useA ? lbA : lbB;
             // does the whole warp sit in the planned (row, L bucket) cell?
-            const uint32_t cell = pcell[wid][s & 31];
+            const uint32_t cell = my_pcell[s & 31];
             bool lbu = true;
 #pragma unroll
             for (int j = 1; j < RPT; ++j) lbu = lbu && ((lbp >> (8 * j)) & 0xffu) == (lbp & 0xffu);
@@ -508,7 +512,7 @@ __global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval
                                                             (lbp & 0xffu) == (cell >> 24));
             uint32_t live;
             if (inplan) {
-                live = pmask[wid][s & 31];
+                live = my_pmask[s & 31];
             } else {
                 live = 0xffffffffu;
                 if (im.prune) {
@@ -530,7 +534,7 @@ __global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval
                 const int ci = cfg_at(pos + c);
                 double4 th[RPT];
                 if (inplan && k_staged < 2) {
-                    th[0] = pth[wid][s & 31][k_staged++];
+                    th[0] = my_pth[s & 31][k_staged++];
 #pragma unroll
                     for (int j = 1; j < RPT; ++j) th[j] = th[0];
                 } else if (uni) {
