@@ -129,3 +129,47 @@ def test_many_tile_classes_list_and_grid():
     for mode, (mac, mic, lat) in res.items():
         np.testing.assert_array_equal(mac, want["macro"], err_msg=mode)
         np.testing.assert_array_equal(U.bits(lat), U.bits(want["lat"]), err_msg=mode)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_odd_tiles_random_registry(seed):
+    """Non-power-of-two tiles (t_m 48/80/112, t_n 24/40/72/200, t_k 32/96):
+    runs of the grid heads break inside 64-wide blocks (multi-run blocks),
+    G and L cross wave / bucket boundaries at odd places; grid gather and
+    list evaluation against the oracle, bit for bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_10187_b200 import capi, synthetic as S
+
+    rows = [(tm, tn, tk, st, 4, 1, 1) for tm in (48, 80, 112) for tn in (24, 40, 72, 200) for tk in (32, 96)
+            for st in (2, 3)]
+    a = np.array(rows, np.int64)
+    cfg = dict(id=(np.arange(len(a)) * 3 + 5).astype(np.int32), t_m=a[:, 0], t_n=a[:, 1], t_k=a[:, 2],
+               stages=a[:, 3], warps=a[:, 4], cluster=a[:, 5], swizzle=a[:, 6])
+    t = S.synthetic_tables(cfg, seed=seed)
+    rng = np.random.default_rng(seed)
+    pairs = [(int(x), int(y)) for x, y in rng.integers(100, 20000, (5, 2))]
+    eng = capi.Engine(t, S.registry_arrays(cfg), n_sm=148)
+    grid = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 3000)
+    grid.sweep()
+    n = 30001
+    P = np.array(pairs)[rng.integers(0, len(pairs), n)]
+    M = rng.integers(1, 3400, n).astype(np.int32)
+    N, K = P[:, 0].astype(np.int32), P[:, 1].astype(np.int32)
+    off = rng.random(n) < 0.5
+    N[off] = rng.integers(1, 50000, off.sum())
+    K[off] = rng.integers(1, 1 << 18, off.sum())
+    res = {}
+    for mode in ("grid", "list"):
+        o = [torch.empty(n, dtype=d, device="cuda") for d in (torch.int32, torch.int32, torch.float64)]
+        dm = [torch.as_tensor(x).cuda() for x in (M, N, K)]
+        (grid.gather if mode == "grid" else eng.tune_batch)(*dm, capi.Engine.decisions(*o))
+        torch.cuda.synchronize()
+        res[mode] = [x.cpu().numpy() for x in o]
+    tiles = {int(i): (int(x), int(y), int(z)) for i, x, y, z in zip(cfg["id"], cfg["t_m"], cfg["t_n"], cfg["t_k"])}
+    want = po.Oracle().tune(po.FlatTables(U.pytables_from_arrays(t), tiles), 148, 1, M, N, K)
+    assert (want["status"] == 0).all()
+    for mode, (mac, mic, lat) in res.items():
+        np.testing.assert_array_equal(mac, want["macro"], err_msg=mode)
+        np.testing.assert_array_equal(mic, want["micro"], err_msg=mode)
+        np.testing.assert_array_equal(U.bits(lat), U.bits(want["lat"]), err_msg=mode)

@@ -76,3 +76,13 @@ def test_prune_plan_is_exact_on_synthetic_tables():
 def test_prune_plan_is_exact_on_adversarial_tables():
     cfg, t = U.adversarial_tables()
     check_plan(t, cfg, seed=1)
+
+
+def test_prune_plan_is_exact_on_odd_tiles():
+    from paper_2604_10187_b200 import synthetic as S
+
+    rows = [(tm, tn, tk, st, 4, 1, 1) for tm in (48, 112) for tn in (24, 200) for tk in (32, 96) for st in (2, 3, 4)]
+    a = np.array(rows, np.int64)
+    cfg = dict(id=(np.arange(len(a)) * 3 + 5).astype(np.int32), t_m=a[:, 0], t_n=a[:, 1], t_k=a[:, 2],
+               stages=a[:, 3], warps=a[:, 4], cluster=a[:, 5], swizzle=a[:, 6])
+    check_plan(S.synthetic_tables(cfg, seed=3), cfg, seed=2)
