@@ -127,6 +127,36 @@ def test_tune_matches_reference_on_its_landscape(capi, ref, orc, landscape):
     ref.close(h)
 
 
+def test_grid_gather_matches_reference_on_its_landscape(capi, ref, landscape):
+    """The reference's own landscape through the serving path: grid sweep,
+    run index, hashed gather and the pruned off-grid evaluation (plain
+    outputs) against the reference's tune() itself."""
+    L = landscape
+    eng = capi.Engine(L["arrays"], L["registry"], n_sm=132)
+    rng = np.random.default_rng(44)
+    pairs = [(int(x), int(y)) for x, y in rng.integers(1, 9000, (6, 2))]
+    grid = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 6000)
+    grid.sweep()
+    n = 40003
+    P = np.array(pairs)[rng.integers(0, len(pairs), n)]
+    M = rng.integers(1, 6500, n).astype(np.int32)
+    N, K = P[:, 0].astype(np.int32), P[:, 1].astype(np.int32)
+    off = rng.random(n) < 0.2
+    N[off] = rng.integers(1, 9000, off.sum())
+    K[off] = rng.integers(1, 9000, off.sum())
+    out = [torch.empty(n, dtype=d, device="cuda") for d in (torch.int32, torch.int32, torch.float64)]
+    grid.gather(dev(M), dev(N), dev(K), capi.Engine.decisions(*out))
+    torch.cuda.synchronize()
+    mac, mic, lat = (o.cpu().numpy() for o in out)
+    h = ref.open(L["tab"], L["reg"], 132)
+    want = ref.tune(h, M, N, K, nthreads=8)
+    ref.close(h)
+    assert (want["status"] == 0).all()
+    np.testing.assert_array_equal(mac, want["macro"])
+    np.testing.assert_array_equal(mic, want["micro"])
+    np.testing.assert_array_equal(U.bits(lat), U.bits(want["lat"]))
+
+
 def test_sweep_grid_config1_bitexact(capi, orc, synth256):
     """Config 1: 4 Llama-3-8B pairs x M=1..8192 x 256 configs, every entry vs
     the oracle tune()."""
