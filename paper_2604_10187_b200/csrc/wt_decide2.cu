@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(kT2) k_eval2(DevImage im, EvalArgs a, int cap_
 namespace {
 struct Tuning {
     int sweep_rpt = 4, eval_rpt = 4;
-    int sweep_kb = 96, eval_kb = 96;
+    int sweep_kb = 48, eval_kb = 96;  // sweep: 48 KB measured best with pruning (r01j A/B)
 };
 const Tuning& tuning() {
     static const Tuning t = [] {
