@@ -495,6 +495,7 @@ def test_sharded_sweep_equals_full(capi, synth256):
     {"WT_EVAL4_RPT": "4"},
     {"WT_EVAL4_RPT": "1"},
     {"WT_BATCH_SLICE": "4100"},
+    {"WT_SWEEP_SMEM_KB": "96"},
 ])
 def test_launch_variants(capi, env):
     """Every launch shape the tuning knobs can select stays bit-exact."""
