@@ -152,6 +152,12 @@ wt_status wt_prune_plan(const wt_tables_desc* tables, const wt_registry_desc* re
                         int32_t* n_seg, int32_t* R, int32_t* C, int32_t* cls_cfg, int32_t* seg_pos,
                         int32_t* seg_n, uint32_t* masks);
 
+/* Extension (A/B and second-witness runs): enable = 0 makes every kernel
+ * evaluate all configs (the pruning masks are ignored); 1 (default, unless
+ * the WT_PRUNE=0 environment variable was set) uses them.  Not thread-safe
+ * against calls in flight on the same engine. */
+wt_status wt_engine_set_prune(wt_engine* e, int32_t enable);
+
 /* Position of macro_id in the engine's ascending config order, or -1. */
 int32_t wt_engine_config_index(const wt_engine* e, int32_t macro_id);
 
@@ -298,7 +304,9 @@ wt_status wt_grid_destroy(wt_grid* g);
 /* Raw device storage (for collectives / inspection).  Taking it invalidates
  * the grid's run index (gathers then read the entries from L2) until the next
  * full wt_sweep or wt_grid_finalize -- call finalize after writing entries
- * (e.g. an all-gather of sweep shards). */
+ * (e.g. an all-gather of sweep shards).  The invalidation is a host-side
+ * generation bump (no device work): gathers launched after this call never
+ * use an index built for earlier entries, whatever stream built it. */
 wt_status wt_grid_storage(const wt_grid* g, wt_grid_entry** entries, int64_t* n_entries,
                           int32_t** topk_macro, double** topk_latency);
 /* Fills entries [begin, end) (flattened index) -- one shard of the sweep.
@@ -336,6 +344,13 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
 wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_t* M,
                               const int32_t* N, const int32_t* K, int64_t n, int32_t* macro_id,
                               int32_t* micro_id, double* latency_us, int64_t chunk);
+/* The same, ordered after all work already queued on `stream` (NULL = the
+ * legacy default stream, which is what wt_decide_host_sync uses): a grid
+ * still being swept / finalized on that stream is complete before the first
+ * gather reads it.  Work on other non-blocking streams is not waited for. */
+wt_status wt_decide_host_stream_sync(const wt_engine* e, const wt_grid* g, const int32_t* M, const int32_t* N,
+                                     const int32_t* K, int64_t n, int32_t* macro_id, int32_t* micro_id,
+                                     double* latency_us, int64_t chunk, void* stream);
 
 /* Kernel launch counter (for bench accounting): total launches issued by
  * this library in this process. */

@@ -92,9 +92,9 @@ class wt_build_result(C.Structure):
 # entry points declared in include/wavetune_c.h (tests check they all exist)
 EXPORTS = (
     "wt_last_error wt_version wt_abi_version wt_engine_create wt_engine_destroy wt_engine_info_get "
-    "wt_engine_config_index wt_tune_batch wt_tune_grouped_batch wt_predict_batch wt_explain "
+    "wt_engine_config_index wt_engine_set_prune wt_tune_batch wt_tune_grouped_batch wt_predict_batch wt_explain "
     "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_destroy wt_grid_storage wt_sweep wt_grid_finalize "
-    "wt_gather_batch wt_decide_host_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
+    "wt_gather_batch wt_decide_host_sync wt_decide_host_stream_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
     "wt_simulate_batch wt_profile_sim wt_tune_one wt_engine_set_resident wt_baseline_create "
     "wt_baseline_destroy wt_baseline_tune_batch wt_baseline_predict_batch wt_set_kernel_timing wt_kernel_time_ms "
     "wt_prune_plan wt_sweep_to wt_grid_ipc_handle wt_ipc_open wt_ipc_close").split()
@@ -234,6 +234,10 @@ class Engine:
     @property
     def n_configs(self):
         return self.info.n_configs
+
+    def set_prune(self, enable: bool):
+        """Extension: False evaluates every config (pruning masks ignored)."""
+        check(lib().wt_engine_set_prune(self.handle, C.c_int32(1 if enable else 0)))
 
     def config_index(self, macro_id):
         return int(lib().wt_engine_config_index(self.handle, C.c_int32(macro_id)))
@@ -384,11 +388,20 @@ class Grid:
         check(lib().wt_gather_batch(self.engine.handle, self.handle, vp(_ptr(M)), vp(_ptr(N)), vp(_ptr(K)),
                                     C.c_int64(M.numel()), C.byref(out), vp(_stream_ptr(stream))))
 
-    def decide_host(self, M, N, K, macro, micro, lat, chunk=1 << 22):
-        """End-to-end over host (pinned) buffers: H2D, gather, D2H, pipelined."""
-        check(lib().wt_decide_host_sync(self.engine.handle, self.handle, vp(_ptr(M)), vp(_ptr(N)), vp(_ptr(K)),
-                                        C.c_int64(M.numel()), vp(_ptr(macro)), vp(_ptr(micro)), vp(_ptr(lat)),
-                                        C.c_int64(chunk)))
+    def decide_host(self, M, N, K, macro, micro, lat, chunk=1 << 22, stream=None):
+        """End-to-end over host (pinned) buffers: H2D, gather, D2H, pipelined;
+        ordered after the work queued on `stream` (default: torch's current
+        stream of the engine's device)."""
+        if stream is None:
+            try:
+                import torch
+
+                stream = torch.cuda.current_stream(self.engine.device)
+            except Exception:
+                stream = None
+        check(lib().wt_decide_host_stream_sync(self.engine.handle, self.handle, vp(_ptr(M)), vp(_ptr(N)),
+                                               vp(_ptr(K)), C.c_int64(M.numel()), vp(_ptr(macro)), vp(_ptr(micro)),
+                                               vp(_ptr(lat)), C.c_int64(chunk), vp(_stream_ptr(stream))))
 
     def entries_tensor(self):
         """The grid's device storage viewed as an int32 [n_entries, 8] torch tensor (no copy).

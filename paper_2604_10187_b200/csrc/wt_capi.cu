@@ -6,10 +6,12 @@
 
 #include <algorithm>
 #include <atomic>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <string>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <vector>
 
@@ -98,6 +100,52 @@ int sm_count(int device) {
 }  // namespace
 
 void wtb::set_last_error(const std::string& msg) { g_err = msg; }
+
+namespace {
+std::mutex g_launch_mu;
+std::map<std::pair<int, const void*>, size_t> g_smem_attr;                  // (device, kernel) -> limit set
+std::map<std::tuple<int, const void*, int, size_t>, int> g_occ;              // -> CTAs per SM
+std::map<int, int> g_sms;
+}  // namespace
+
+cudaError_t wtb::prepare_smem(const void* kernel, size_t dyn_smem) {
+    if (dyn_smem == 0) return cudaSuccess;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_launch_mu);
+    size_t& cur = g_smem_attr[{dev, kernel}];
+    if (dyn_smem <= cur) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn_smem));
+    if (e == cudaSuccess) cur = dyn_smem;
+    return e;
+}
+
+int wtb::occupancy(const void* kernel, int threads, size_t dyn_smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (prepare_smem(kernel, dyn_smem) != cudaSuccess) return 1;
+    std::lock_guard<std::mutex> lock(g_launch_mu);
+    auto key = std::make_tuple(dev, kernel, threads, dyn_smem);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) return it->second;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, dyn_smem);
+    occ = std::max(occ, 1);
+    g_occ[key] = occ;
+    return occ;
+}
+
+int wtb::device_sms() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_launch_mu);
+    auto it = g_sms.find(dev);
+    if (it != g_sms.end()) return it->second;
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_sms[dev] = n;
+    return n;
+}
 cudaMemPool_t wtb::device_pool(int device) { return lib_pool(device); }
 
 struct wt_engine {
@@ -151,6 +199,17 @@ struct wt_grid {
     int4* dhash = nullptr;  // (N, K) -> pair open-addressing table (k_gather_h)
     int32_t hbits = 0;
     RunIndex runs{};        // run-compressed heads (k_gather_h); budget 0 = none
+    mutable std::atomic<int32_t> gen{1};  // run-index generation (wt_decide.h, RunIndex)
+    RunIndex runs_now() const {  // the index as a launch sees it
+        RunIndex r = runs;
+        r.gen = gen.load();
+        return r;
+    }
+    void invalidate_runs() const {  // entries may change: stale index never matches again
+        int32_t v = gen.load();
+        while (!gen.compare_exchange_weak(v, v == INT32_MAX ? 1 : v + 1)) {
+        }
+    }
 };
 
 namespace {
@@ -336,6 +395,12 @@ wt_status wt_engine_info_get(const wt_engine* e, wt_engine_info* out) {
     out->has_fallback_rows = e->host.special ? 1 : 0;
     out->device = e->device;
     out->device_bytes = e->bytes;
+    return WT_OK;
+}
+
+wt_status wt_engine_set_prune(wt_engine* e, int32_t enable) {
+    if (!e) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    e->dev.prune = enable ? 1 : 0;
     return WT_OK;
 }
 
@@ -943,11 +1008,9 @@ wt_status wt_grid_storage(const wt_grid* g, wt_grid_entry** entries, int64_t* n_
                           int32_t** topk_macro, double** topk_latency) {
     if (!g) return set_err(WT_INVALID_ARGUMENT, "null grid");
     // whoever takes the raw storage may write it: the run index is stale
-    // until the next full sweep / wt_grid_finalize (gathers read L2 meanwhile)
-    if (g->runs.budget > 0) {
-        DeviceGuard guard(g->eng->device);
-        cudaMemset(g->runs.hdr, 0, 4);
-    }
+    // until the next full sweep / wt_grid_finalize (gathers read L2 meanwhile);
+    // host-side generation bump, no device write that could race a build
+    g->invalidate_runs();
     if (entries) *entries = g->entries;
     if (n_entries) *n_entries = g->n_entries;
     if (topk_macro) *topk_macro = g->tk_macro;
@@ -996,8 +1059,7 @@ wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, v
     // invalidated by a partial one (wt_grid_finalize rebuilds it)
     if (g->runs.budget > 0) {
         if (begin == 0 && end == g->n_entries) return wt_grid_finalize(e, g, stream);
-        ce = cudaMemsetAsync(g->runs.hdr, 0, 4, s);
-        if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep: run index");
+        g->invalidate_runs();
     }
     return WT_OK;
 }
@@ -1037,7 +1099,7 @@ wt_status wt_sweep_to(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end
     g_launches += sb ? 2 : 1;
     if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep_to");
     // this grid's own run index is stale until the caller finalizes it
-    if (g->runs.budget > 0) cudaMemsetAsync(g->runs.hdr, 0, 4, s);
+    g->invalidate_runs();
     return WT_OK;
 }
 
@@ -1082,7 +1144,7 @@ wt_status wt_grid_finalize(const wt_engine* e, wt_grid* g, void* stream) {
     void* temp = nullptr;
     cudaError_t ce = cudaMallocFromPoolAsync(&temp, runs_temp_bytes(g->n_entries), lib_pool(e->device), s);
     if (ce != cudaSuccess) return cuda_err(ce, "wt_grid_finalize: scratch");
-    ce = launch_runs_build(g->entries, g->n_entries, g->mcount, g->runs, temp, s);
+    ce = launch_runs_build(g->entries, g->n_entries, g->mcount, g->runs_now(), temp, s);
     cudaFreeAsync(temp, s);
     g_launches += 5;
     if (ce != cudaSuccess) return cuda_err(ce, "wt_grid_finalize");
@@ -1139,7 +1201,7 @@ static wt_status gather_impl(const wt_engine* e, const wt_grid* g, const int32_t
     a.off_K = offK;
     a.htab = g->dhash;
     a.hbits = g->hbits;
-    a.runs = g->runs;
+    a.runs = g->runs_now();
     // row-grouped evaluation of the off-grid list: keys counted while compacting
     void* escratch = escratch_in;
     if (gather_needs_eval3(g, out)) {
@@ -1222,6 +1284,12 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
 wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_t* M,
                               const int32_t* N, const int32_t* K, int64_t n, int32_t* macro_id,
                               int32_t* micro_id, double* latency_us, int64_t chunk) {
+    return wt_decide_host_stream_sync(e, g, M, N, K, n, macro_id, micro_id, latency_us, chunk, nullptr);
+}
+
+wt_status wt_decide_host_stream_sync(const wt_engine* e, const wt_grid* g, const int32_t* M, const int32_t* N,
+                                     const int32_t* K, int64_t n, int32_t* macro_id, int32_t* micro_id,
+                                     double* latency_us, int64_t chunk, void* stream) {
     NvtxRange nvtx_("wt_decide_host_sync");
     if (!e || !M || !N || !K || !macro_id || !micro_id || !latency_us)
         return set_err(WT_INVALID_ARGUMENT, "null argument");
@@ -1243,9 +1311,14 @@ wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_
     const size_t gs = g ? (gather_scratch_bytes(chunk) + 255) & ~size_t(255) : 0;
     const size_t es = ev3 ? eval3_scratch_bytes(chunk) : 0;
     const size_t per = io + gs + es;
-    cudaError_t ce = cudaSuccess;
+    // the internal streams start after everything already queued on the
+    // caller's stream (e.g. a sweep / finalize still filling the grid)
+    cudaEvent_t after = nullptr;
+    cudaError_t ce = cudaEventCreateWithFlags(&after, cudaEventDisableTiming);
+    if (ce == cudaSuccess) ce = cudaEventRecord(after, static_cast<cudaStream_t>(stream));
     for (int s = 0; s < kSlots && ce == cudaSuccess; ++s) {
         ce = cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking);
+        if (ce == cudaSuccess) ce = cudaStreamWaitEvent(st[s], after, 0);
         if (ce == cudaSuccess) ce = cudaMallocFromPoolAsync(&buf[s], per, lib_pool(e->device), st[s]);
     }
     wt_status rs = WT_OK;
@@ -1287,6 +1360,7 @@ wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_
         }
         if (st[s]) cudaStreamDestroy(st[s]);
     }
+    if (after) cudaEventDestroy(after);
     if (rs != WT_OK) return rs;
     if (ce != cudaSuccess) return cuda_err(ce, "wt_decide_host_sync");
     return WT_OK;

@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(kGatherThreads, MINB) k_gather_h(DevImage im, 
         nr = hd.y;
         multi = hd.z != 0;
         const int64_t need = int64_t(ri.nbtot) * 16 + (multi ? int64_t(nr) * 20 + 4 : 0);
-        runs = hd.x != 0 && need <= ri.budget;
+        runs = hd.x != 0 && hd.x == ri.gen && need <= ri.budget;
     }
     RunSmem rs{};
     if (runs) {
@@ -864,7 +864,7 @@ __global__ void k_runscatter(const wt_grid_entry* ent, int64_t n, const uint32_t
 // one thread per block of M values: its head, or the multi-run marker
 __global__ void k_runheads(int64_t mcount, const uint32_t* flags, const uint32_t* ids, RunIndex ri) {
     const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (b == 0) ri.hdr[0] = ri.hdr[3] ? 0 : 1;
+    if (b == 0) ri.hdr[0] = ri.hdr[3] ? 0 : ri.gen;
     if (b >= ri.nbtot) return;
     const int64_t p = b / ri.nblk, blk = b - p * ri.nblk;
     const int64_t i0 = p * mcount + (blk << kRunBlkShift);
@@ -993,7 +993,7 @@ template <int RPT, bool SPECIAL, bool WIDE, int KM>
 static cudaError_t launch_sweep_t(const DevImage& im, const SweepArgs& a, int grid, size_t smem,
                                   cudaStream_t st) {
     auto fn = k_sweep<RPT, SPECIAL, WIDE, KM>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = prepare_smem(reinterpret_cast<const void*>(fn), smem);
     if (e != cudaSuccess) return e;
     fn<<<grid, kSweepThreads, smem, st>>>(im, a);
     return cudaGetLastError();
@@ -1128,7 +1128,7 @@ template <bool SPECIAL, int KM>
 static cudaError_t launch_eval_t(const DevImage& im, const EvalArgs& a, int grid, size_t smem,
                                  cudaStream_t st) {
     auto fn = k_eval<SPECIAL, KM>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = prepare_smem(reinterpret_cast<const void*>(fn), smem);
     if (e != cudaSuccess) return e;
     fn<<<grid, kEvalThreads, smem, st>>>(im, a);
     return cudaGetLastError();
@@ -1155,15 +1155,8 @@ cudaError_t launch_grouped(const DevImage& im, const GroupedArgs& a, int grid, c
 // no cap; 4 = never hashed; 5 = hashed, 4 CTAs/SM (register cap).
 template <int V, bool PF, int MINB>
 static cudaError_t go_gather(const DevImage& im, const GatherArgs& a, int grid, size_t smem, cudaStream_t st) {
-    static int occ = 0, sms = 0;
-    if (!occ) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather<V, PF, MINB>, kGatherThreads, 4096);
-        if (occ < 1) occ = 1;
-    }
-    grid = std::min(grid, sms * occ);
+    const void* fn = reinterpret_cast<const void*>(k_gather<V, PF, MINB>);
+    grid = std::min(grid, device_sms() * occupancy(fn, kGatherThreads, 4096));
     k_gather<V, PF, MINB><<<grid, kGatherThreads, smem, st>>>(im, a);
     return cudaGetLastError();
 }
@@ -1172,23 +1165,12 @@ static cudaError_t go_gather(const DevImage& im, const GatherArgs& a, int grid, 
 // and the run-index budget are dynamic shared memory.
 template <int MINB>
 static cudaError_t go_gather_h(const DevImage& im, const GatherArgs& a, int grid, cudaStream_t st) {
-    static int occ = 0, sms = 0;
-    static size_t occ_hs = 0, attr_hs = 0;
     const size_t hs = (size_t(1) << a.hbits) * sizeof(int4) + size_t(a.runs.budget);
-    if (hs > attr_hs) {  // static + dynamic may exceed the 48 KB default
-        cudaError_t e = cudaFuncSetAttribute(k_gather_h<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hs));
-        if (e != cudaSuccess) return e;
-        attr_hs = hs;
-    }
-    if (!occ || occ_hs != hs) {
-        occ_hs = hs;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather_h<MINB>, kGatherThreads, hs);
-        if (occ < 1) occ = 1;
-    }
-    k_gather_h<MINB><<<std::min(grid, sms * occ), kGatherThreads, hs, st>>>(im, a);
+    const void* fn = reinterpret_cast<const void*>(k_gather_h<MINB>);
+    const int occ = occupancy(fn, kGatherThreads, hs);  // also raises the smem limit (static + dynamic > 48 KB)
+    cudaError_t e = prepare_smem(fn, hs);
+    if (e != cudaSuccess) return e;
+    k_gather_h<MINB><<<std::min(grid, device_sms() * occ), kGatherThreads, hs, st>>>(im, a);
     return cudaGetLastError();
 }
 

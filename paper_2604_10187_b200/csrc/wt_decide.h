@@ -92,8 +92,12 @@ struct GroupedArgs {
 // block holds a single run, else {first run index, 0, INT32_MIN, 0} and the
 // runs (rkey[r] = flat entry index where run r starts, rkey[nruns] =
 // 0xffffffff, rval[r] = head) resolve it.  Built on the device after a full
-// sweep (or by wt_grid_finalize); hdr = {valid, nruns, any multi-run block,
-// a head used the INT32_MIN marker}.  The gather stages it in shared memory
+// sweep (or by wt_grid_finalize); hdr = {generation the index was built for
+// (0 = none), nruns, any multi-run block, a head used the INT32_MIN marker}.
+// The host bumps the grid's generation whenever entries may change outside a
+// full sweep (raw storage handed out, partial / fused sweeps); a gather uses
+// the index only when hdr[0] equals the generation it was launched with, so
+// no device write is needed to invalidate it (and none can race).  The gather stages it in shared memory
 // when it fits `budget` bytes, else reads heads from L2.
 constexpr int kRunBlkShift = 6;
 struct RunIndex {
@@ -104,6 +108,7 @@ struct RunIndex {
     int32_t nblk;    // blocks per pair
     int32_t nbtot;   // n_pairs * nblk
     int32_t budget;  // shared-memory bytes reserved for the index (0 = none)
+    int32_t gen;     // generation at enqueue time (build: written to hdr[0]; gather: expected)
 };
 
 struct GatherArgs {
@@ -177,6 +182,14 @@ struct NearestArgs {
 
 // Library-owned stream-ordered memory pool of a device (wt_capi.cu).
 cudaMemPool_t device_pool(int device);
+// Launch helpers for the current device, safe for concurrent host threads
+// and several devices per process: the dynamic shared-memory limit of a
+// kernel is raised monotonically per (device, kernel) -- never lowered under
+// a launch in flight -- and occupancy is cached per (device, kernel,
+// threads, dynamic smem).
+cudaError_t prepare_smem(const void* kernel, size_t dyn_smem);
+int occupancy(const void* kernel, int threads, size_t dyn_smem);  // >= 1
+int device_sms();
 
 size_t sweep_smem_bytes(const DevImage& im, int chunk, bool special);
 size_t eval_smem_bytes(const DevImage& im, int chunk, bool special);

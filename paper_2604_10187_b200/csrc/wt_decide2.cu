@@ -622,21 +622,19 @@ const Tuning& tuning() {
     }();
     return t;
 }
-int n_sms() {
-    int dev = 0, n = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n;
-}
+int n_sms() { return device_sms(); }
 // bytes of one staged segment in the worst case (all R rows)
 size_t seg_worst(const DevImage& im, bool list) {
     return list ? size_t(im.R) * (2 * im.seg_cfg + 1) * 16 + size_t(im.R) * im.seg_cfg * 4
                 : size_t(im.R) * im.seg_cfg * (sizeof(double4) + 4);
 }
+// Dynamic shared memory of a sweep / list CTA: the segment-header region
+// plus a row-staging budget of `kb` KB (raised to one worst-case segment when
+// that is larger), capped at 200 KB.  `kb` is the staging budget alone, so
+// WT_SWEEP_SMEM_KB=48 means 48 KB of staged rows on top of the headers.
 size_t smem_for(int kb, const DevImage& im, bool list) {
-    size_t b = size_t(kb) * 1024;
-    const size_t need = kT2 * sizeof(SegHdr) + seg_worst(im, list) + 1024;
-    return std::min<size_t>(std::max(b, need), 200 * 1024);
+    const size_t stage = std::max(size_t(kb) * 1024, seg_worst(im, list));
+    return std::min<size_t>(kT2 * sizeof(SegHdr) + stage + 1024, 200 * 1024);
 }
 }  // namespace
 
@@ -666,7 +664,7 @@ static cudaError_t go_sweep2(const DevImage& im, const SweepArgs& a, int64_t uni
     const size_t smem = smem_for(tuning().sweep_kb, im, false);
     const int cap = int((smem - kT2 * sizeof(SegHdr)) / (sizeof(double4) + (SP ? 4 : 0)));
     auto fn = k_sweep2<RPT, SP, WIDE>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = prepare_smem(reinterpret_cast<const void*>(fn), smem);
     if (e != cudaSuccess) return e;
     fn<<<unsigned(units), kT2, smem, st>>>(im, a, cap, part, ntiles);
     return cudaGetLastError();
@@ -708,7 +706,7 @@ static cudaError_t go_eval2(const DevImage& im, const EvalArgs& a, int grid, cud
     const size_t smem = smem_for(tuning().eval_kb, im, true);
     const int cap = int((smem - kT2 * sizeof(SegHdr)) / (sizeof(double4) + (SP ? 8 : 0)));  // 32-byte units
     auto fn = k_eval2<RPT, SP>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = prepare_smem(reinterpret_cast<const void*>(fn), smem);
     if (e != cudaSuccess) return e;
     fn<<<grid, kT2, smem, st>>>(im, a, cap);
     return cudaGetLastError();

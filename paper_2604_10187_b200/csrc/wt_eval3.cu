@@ -645,16 +645,9 @@ cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, b
     p += al256(un * 4);
     void* tmp = p;
 
-    static int sms = 0, occ = 0, occs = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval3<false, true>, kT3, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs, k_eval3<true, true>, kT3, 0);
-        occ = std::max(occ, 1);
-        occs = std::max(occs, 1);
-    }
+    const int sms = device_sms();
+    const int occ = occupancy(reinterpret_cast<const void*>(k_eval3<false, true>), kT3, 0);
+    const int occs = occupancy(reinterpret_cast<const void*>(k_eval3<true, true>), kT3, 0);
     // grids: enough CTAs for n (host upper bound), capped at a few waves
     const int64_t want = (a.n + kT3 - 1) / kT3;
     const int gk = int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(sms) * 8)));
@@ -687,9 +680,7 @@ cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, b
         const bool hs4 = hs && im.C <= 8192;
         const size_t dyn = hs4 ? size_t(im.C) * sizeof(int32_t) : 0;
         auto go = [&](auto fn, int r) {
-            if (dyn > 16 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
-            int o = 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kT3, dyn);
+            const int o = occupancy(reinterpret_cast<const void*>(fn), kT3, dyn);  // raises the smem limit too
             const int64_t w = (a.n + int64_t(r) * kT3 - 1) / (int64_t(r) * kT3);
             const int g = int(std::max<int64_t>(1, std::min<int64_t>(w, int64_t(sms) * std::max(o, 1))));
             fn<<<g, kT3, dyn, st>>>(im, a, rec, qhi);

@@ -209,7 +209,7 @@ cudaError_t launch_serve(const DevImage& im, int64_t n_anchor, Mailbox* mb, uint
                          cudaStream_t st) {
     const size_t smem = staged_bytes(im, n_anchor);
     if (smem <= kServeSmemMax) {
-        cudaError_t e = cudaFuncSetAttribute(k_serve<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaError_t e = prepare_smem(reinterpret_cast<const void*>(k_serve<false>), smem);
         if (e != cudaSuccess) return e;
         k_serve<false><<<1, kServeThreads, smem, st>>>(im, n_anchor, mb, last, idle_ns);
     } else {

@@ -479,7 +479,7 @@ def test_sharded_sweep_equals_full(capi, synth256):
 
 @pytest.mark.parametrize("env", [
     {"WT_SWEEP_RPT": "2", "WT_EVAL_RPT": "2"},
-    {"WT_SWEEP_SMEM_KB": "48", "WT_EVAL_SMEM_KB": "64"},
+    {"WT_SWEEP_SMEM_KB": "24", "WT_EVAL_SMEM_KB": "64"},
     {"WT_SWEEP_RPT": "2", "WT_SWEEP_SMEM_KB": "160", "WT_EVAL_RPT": "4", "WT_EVAL_SMEM_KB": "160"},
     {"WT_GATHER_VARIANT": "1"},
     {"WT_EVAL_RPT": "2", "WT_GATHER_VARIANT": "2"},

@@ -163,3 +163,20 @@ def registry_arrays_of(cfg):
     from paper_2604_10187_b200 import synthetic as S
 
     return S.registry_arrays(cfg)
+
+
+def oracle_tune_mt(orc, flat, n_sm, bps, M, N, K, threads=None, chunk=4096):
+    """Oracle.tune over host threads (the ctypes call releases the GIL);
+    results concatenated in query order."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    n = len(M)
+    threads = threads or max(1, min(32, len(os.sched_getaffinity(0))))
+    parts = [(i, min(n, i + chunk)) for i in range(0, n, chunk)]
+    with ThreadPoolExecutor(threads) as ex:
+        outs = list(ex.map(lambda p: orc.tune(flat, n_sm, bps, M[p[0]:p[1]], N[p[0]:p[1]], K[p[0]:p[1]]), parts))
+    return {k: np.concatenate([o[k] for o in outs]) for k in outs[0]}
+
+
+def tiles_of(cfg):
+    return {int(i): (int(a), int(b), int(c)) for i, a, b, c in zip(cfg["id"], cfg["t_m"], cfg["t_n"], cfg["t_k"])}
