@@ -110,13 +110,16 @@ std::map<int, int> g_sms;
 
 cudaError_t wtb::prepare_smem(const void* kernel, size_t dyn_smem) {
     if (dyn_smem == 0) return cudaSuccess;
+    // never below the 48 KB default (a lower limit would reject launches
+    // that need no opt-in); opted in once per (device, kernel, high-water)
+    const size_t want = std::max<size_t>(dyn_smem, 48 * 1024);
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(g_launch_mu);
     size_t& cur = g_smem_attr[{dev, kernel}];
-    if (dyn_smem <= cur) return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn_smem));
-    if (e == cudaSuccess) cur = dyn_smem;
+    if (want <= cur) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(want));
+    if (e == cudaSuccess) cur = want;
     return e;
 }
 
