@@ -152,6 +152,11 @@ wt_status wt_prune_plan(const wt_tables_desc* tables, const wt_registry_desc* re
                         int32_t* n_seg, int32_t* R, int32_t* C, int32_t* cls_cfg, int32_t* seg_pos,
                         int32_t* seg_n, uint32_t* masks);
 
+/* Inspection: copies the engine's pruning masks (built on the device) to
+ * host memory, laid out as wt_prune_plan's masks; n = n_seg * R * 16 words.
+ * Synchronous. */
+wt_status wt_engine_prune_masks(const wt_engine* e, uint32_t* masks, int64_t n);
+
 /* Extension (A/B and second-witness runs): enable = 0 makes every kernel
  * evaluate all configs (the pruning masks are ignored); 1 (default, unless
  * the WT_PRUNE=0 environment variable was set) uses them.  Not thread-safe

@@ -17,6 +17,7 @@
 
 #include "wavetune_c.h"
 #include "wt_decide.h"
+#include "wt_image_dev.h"
 #include "wt_internal.h"
 
 namespace {
@@ -151,9 +152,18 @@ int wtb::device_sms() {
 }
 cudaMemPool_t wtb::device_pool(int device) { return lib_pool(device); }
 
+// Host-side facts about an engine (the image itself lives on the device).
+struct EngineMeta {
+    int32_t C = 0, R = 0, S = 0, family = 0;
+    bool special = false;
+    std::vector<int32_t> macro_id;  // ascending (config order)
+    int32_t tm_min = 0, tn_min = 0;
+    int64_t n_pool = 0;             // anchor pool entries
+};
+
 struct wt_engine {
     int device = 0;
-    HostImage host;
+    EngineMeta host;
     DevImage dev{};
     void* mem = nullptr;
     size_t bytes = 0;
@@ -253,126 +263,268 @@ wt_status wt_prune_plan(const wt_tables_desc* tables, const wt_registry_desc* re
                         int32_t* n_seg, int32_t* R, int32_t* C, int32_t* cls_cfg, int32_t* seg_pos,
                         int32_t* seg_n, uint32_t* masks) {
     if (!tables || !registry || !hw || !n_seg || !R || !C) return set_err(WT_INVALID_ARGUMENT, "null argument");
-    HostImage h;
+    ImagePlan P;
+    std::vector<uint32_t> segmask;
     std::string err;
-    const wt_status st = build_image(*tables, *registry, *hw, &h, &err);
+    const wt_status st = masks ? prune_plan_host(*tables, *registry, *hw, &P, &segmask, &err)
+                               : plan_image(tables->macro_id, tables->W, tables->n_tables, *registry, *hw, &P, &err);
     if (st != WT_OK) return set_err(st, err);
-    const int32_t ns = int32_t(h.seg_pos.size());
+    const int32_t ns = int32_t(P.seg_pos.size());
     *n_seg = ns;
-    *R = h.R;
-    *C = h.C;
+    *R = P.R;
+    *C = P.C;
     if (!masks) return WT_OK;
     if (!cls_cfg || !seg_pos || !seg_n) return set_err(WT_INVALID_ARGUMENT, "null output buffer");
-    std::copy(h.cls_cfg.begin(), h.cls_cfg.end(), cls_cfg);
+    std::copy(P.cls_cfg.begin(), P.cls_cfg.end(), cls_cfg);
     for (int32_t k = 0; k < ns; ++k) {
-        seg_pos[k] = h.seg_pos[k];
-        seg_n[k] = h.seg_tiles[4 * k + 3];
+        seg_pos[k] = P.seg_pos[k];
+        seg_n[k] = P.seg_tiles[4 * k + 3];
     }
-    std::copy(h.segmask.begin(), h.segmask.end(), masks);
+    std::copy(segmask.begin(), segmask.end(), masks);
     return WT_OK;
 }
+
+}  // extern "C"
+
+namespace {
+
+// Device copy of the tables' CSR (wt_tables_desc with device pointers) and
+// the pool arrays, as the image builder reads them.
+struct DevTables {
+    TabView tv{};
+    const int64_t* anchor_l = nullptr;
+    const int32_t* anchor_micro = nullptr;
+    int64_t n_anchor = 0;
+    const int64_t* ext_l = nullptr;
+    const int32_t* ext_micro = nullptr;
+    int64_t n_ext = 0;
+};
+
+// Allocates the engine's arena, uploads the plan (one H2D copy), builds the
+// rows, class views and pruning masks on the device from `T`, copies the
+// anchor pool, and reads back the special-row flag (the only host sync).
+wt_status engine_build(wt_engine* e, const ImagePlan& P, const DevTables& T, cudaStream_t s) {
+    const size_t C = P.C, R = P.R, NS = P.seg_pos.size(), NCLS = P.cls_seg.size() - 1;
+    const int64_t n_pool = std::max<int64_t>(1, T.n_anchor + T.n_ext);
+    if (T.n_anchor + T.n_ext >= (int64_t(1) << 31))
+        return set_err(WT_UNSUPPORTED, "anchor pool above 2^31 entries is outside the device path's range");
+    Arena ar;
+    // plan region first (uploaded in one copy), then the device-built arrays
+    const size_t o_mid = ar.take(C * 4), o_til = ar.take(C * 16), o_mag = ar.take(C * 16), o_st = ar.take(NS * 16),
+                 o_sm = ar.take(NS * 16), o_sp = ar.take(NS * 4), o_cc = ar.take(C * 4), o_ord = ar.take(C * 4),
+                 o_cp = ar.take(C * 4), o_cs = ar.take((NCLS + 1) * 4);
+    const size_t plan_bytes = ar.used;
+    const size_t o_th = ar.take(C * R * 32), o_meta = ar.take(C * R * 4), o_used = ar.take(C * R * 4),
+                 o_amap = ar.take(C * R * 8), o_afb = ar.take(C * R * 4), o_al = ar.take(size_t(n_pool) * 8),
+                 o_am = ar.take(size_t(n_pool) * 4), o_th2 = ar.take(C * R * 32), o_m2 = ar.take(C * R * 4),
+                 o_th2t = ar.take(C * R * 32), o_m2t = ar.take(C * R * 4), o_smask = ar.take(NS * R * kLB * 4),
+                 o_sor = ar.take(NS * R * 4), o_spec = ar.take(4);
+    cudaError_t ce = cudaMalloc(&e->mem, ar.used);
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_engine_create: cudaMalloc");
+    e->bytes = ar.used;
+    char* base = static_cast<char*>(e->mem);
+    std::vector<char> stage(plan_bytes, 0);
+    auto put = [&](size_t off, const void* src, size_t n) {
+        if (n) std::memcpy(stage.data() + off, src, n);
+    };
+    put(o_mid, P.macro_id.data(), C * 4);
+    put(o_til, P.tiles.data(), C * 16);
+    put(o_mag, P.magic.data(), C * 16);
+    put(o_st, P.seg_tiles.data(), NS * 16);
+    put(o_sm, P.seg_magic.data(), NS * 16);
+    put(o_sp, P.seg_pos.data(), NS * 4);
+    put(o_cc, P.cls_cfg.data(), C * 4);
+    put(o_ord, P.order.data(), C * 4);
+    put(o_cp, P.cfg_pos.data(), C * 4);
+    put(o_cs, P.cls_seg.data(), (NCLS + 1) * 4);
+    ce = cudaMemcpyAsync(base, stage.data(), plan_bytes, cudaMemcpyHostToDevice, s);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(base + o_spec, 0, 4, s);
+    auto at = [&](size_t off) { return static_cast<void*>(base + off); };
+    if (ce == cudaSuccess && T.n_anchor > 0) {
+        ce = cudaMemcpyAsync(at(o_al), T.anchor_l, size_t(T.n_anchor) * 8, cudaMemcpyDeviceToDevice, s);
+        if (ce == cudaSuccess)
+            ce = cudaMemcpyAsync(at(o_am), T.anchor_micro, size_t(T.n_anchor) * 4, cudaMemcpyDeviceToDevice, s);
+    }
+    if (ce == cudaSuccess && T.n_ext > 0) {
+        ce = cudaMemcpyAsync(base + o_al + size_t(T.n_anchor) * 8, T.ext_l, size_t(T.n_ext) * 8,
+                             cudaMemcpyDeviceToDevice, s);
+        if (ce == cudaSuccess)
+            ce = cudaMemcpyAsync(base + o_am + size_t(T.n_anchor) * 4, T.ext_micro, size_t(T.n_ext) * 4,
+                                 cudaMemcpyDeviceToDevice, s);
+    }
+    if (ce == cudaSuccess && T.n_anchor + T.n_ext == 0) {  // keep the pool non-empty for the device
+        const int64_t z = 0;
+        const int32_t m1 = -1;
+        ce = cudaMemcpyAsync(at(o_al), &z, 8, cudaMemcpyHostToDevice, s);
+        if (ce == cudaSuccess) ce = cudaMemcpyAsync(at(o_am), &m1, 4, cudaMemcpyHostToDevice, s);
+    }
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_engine_create: upload");
+    ImgRowsArgs ra{};
+    ra.C = P.C;
+    ra.R = P.R;
+    ra.order = static_cast<const int32_t*>(at(o_ord));
+    ra.cfg_pos = static_cast<const int32_t*>(at(o_cp));
+    ra.theta = static_cast<double4*>(at(o_th));
+    ra.rowmeta = static_cast<uint32_t*>(at(o_meta));
+    ra.used_w = static_cast<int32_t*>(at(o_used));
+    ra.amap = static_cast<int2*>(at(o_amap));
+    ra.afb = static_cast<int32_t*>(at(o_afb));
+    ra.theta2 = static_cast<double4*>(at(o_th2));
+    ra.meta2 = static_cast<uint32_t*>(at(o_m2));
+    ra.theta2t = static_cast<double4*>(at(o_th2t));
+    ra.meta2t = static_cast<uint32_t*>(at(o_m2t));
+    ra.special = static_cast<uint32_t*>(at(o_spec));
+    ImgPruneArgs pa{};
+    pa.C = P.C;
+    pa.R = P.R;
+    pa.S = P.S;
+    pa.nseg = int32_t(NS);
+    pa.ncells = int64_t(NCLS) * P.R * kLB;
+    pa.cls_seg = static_cast<const int32_t*>(at(o_cs));
+    pa.seg_pos = static_cast<const int32_t*>(at(o_sp));
+    pa.seg_tiles = static_cast<const int4*>(at(o_st));
+    pa.theta2 = ra.theta2;
+    pa.meta2 = ra.meta2;
+    pa.segmask = static_cast<uint32_t*>(at(o_smask));
+    pa.segor = static_cast<uint32_t*>(at(o_sor));
+    ce = launch_image_build(T.tv, ra, pa, s);
+    g_launches += 2;
+    uint32_t special = 0;
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(&special, at(o_spec), 4, cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_engine_create: image build");
+
+    EngineMeta& h = e->host;
+    h.C = P.C;
+    h.R = P.R;
+    h.S = P.S;
+    h.family = P.family;
+    h.special = special != 0;
+    h.macro_id = P.macro_id;
+    h.tm_min = P.tm_min;
+    h.tn_min = P.tn_min;
+    h.n_pool = n_pool;
+    DevImage& d = e->dev;
+    d.C = P.C;
+    d.R = P.R;
+    d.S = P.S;
+    d.RS = uint32_t(P.R) * uint32_t(P.S);
+    const Magic ms = make_magic(uint32_t(P.S));
+    d.mS = ms.m;
+    d.sS = ms.s;
+    d.special = h.special ? 1 : 0;
+    d.macro_id = static_cast<const int32_t*>(at(o_mid));
+    d.tiles = static_cast<const int4*>(at(o_til));
+    d.magic = static_cast<const uint4*>(at(o_mag));
+    d.theta = ra.theta;
+    d.rowmeta = ra.rowmeta;
+    d.used_w = ra.used_w;
+    d.amap = ra.amap;
+    d.afb = ra.afb;
+    d.anchor_l = static_cast<const int64_t*>(at(o_al));
+    d.anchor_micro = static_cast<const int32_t*>(at(o_am));
+    d.tm_min = P.tm_min;
+    d.tn_min = P.tn_min;
+    d.nseg = int32_t(NS);
+    d.seg_cfg = P.seg_cfg;
+    d.seg_tiles = pa.seg_tiles;
+    d.seg_magic = static_cast<const uint4*>(at(o_sm));
+    d.seg_pos = pa.seg_pos;
+    d.cls_cfg = static_cast<const int32_t*>(at(o_cc));
+    d.theta2 = ra.theta2;
+    d.meta2 = ra.meta2;
+    d.theta2t = ra.theta2t;
+    d.meta2t = ra.meta2t;
+    d.segmask = pa.segmask;
+    d.segor = pa.segor;
+    static const int prune = [] {
+        const char* v = std::getenv("WT_PRUNE");
+        return v ? std::atoi(v) : 1;
+    }();
+    d.prune = prune;
+    d.seg_maxcfg = P.seg_maxcfg;
+    // list-mode chunk: keep the staged rows near 40 KB so several CTAs fit per SM
+    e->eval_chunk = int(std::max<size_t>(1, std::min<size_t>(C, 40960 / (R * 36 + 32))));
+    e->eval_grid = sm_count(e->device) * 4;
+    e->eval_grid2 = sm_count(e->device) * 4;  // upper bound; launch_eval2 clamps to residency
+    return WT_OK;
+}
+
+}  // namespace
+
+extern "C" {
 
 wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc* registry,
                            const wt_hw* hw, int device, wt_engine** out) {
     NvtxRange nvtx_("wt_engine_create");
     if (!tables || !registry || !hw || !out) return set_err(WT_INVALID_ARGUMENT, "null argument");
     *out = nullptr;
+    ImagePlan P;
+    std::string err;
+    const wt_status st = plan_image(tables->macro_id, tables->W, tables->n_tables, *registry, *hw, &P, &err);
+    if (st != WT_OK) return set_err(st, err);
+    const wt_tables_desc& t = *tables;
+    const int64_t n = t.n_tables, n_coeff = t.coeff_off[n], n_awave = t.awave_off[n];
+    const int64_t n_anchor = t.awave_aoff[n_awave], n_ext = t.ext_aoff[n];
+    DeviceGuard guard(device);
+    // the tables' CSR travels once (one packed H2D copy); everything else is
+    // resolved on the device
+    Arena ar;
+    const size_t o_W = ar.take(n * 4), o_te = ar.take(n * 32), o_co = ar.take((n + 1) * 4),
+                 o_cw = ar.take(n_coeff * 4), o_ct = ar.take(n_coeff * 32), o_ao = ar.take((n + 1) * 4),
+                 o_aw = ar.take(n_awave * 4), o_aa = ar.take((n_awave + 1) * 4), o_eo = ar.take((n + 1) * 4),
+                 o_al = ar.take(n_anchor * 8), o_am = ar.take(n_anchor * 4), o_el = ar.take(n_ext * 8),
+                 o_em = ar.take(n_ext * 4);
+    std::vector<char> stage(ar.used, 0);
+    auto put = [&](size_t off, const void* src, size_t bytes) {
+        if (bytes) std::memcpy(stage.data() + off, src, bytes);
+    };
+    put(o_W, t.W, n * 4);
+    put(o_te, t.theta_ext, n * 32);
+    put(o_co, t.coeff_off, (n + 1) * 4);
+    put(o_cw, t.coeff_w, n_coeff * 4);
+    put(o_ct, t.coeff_theta, n_coeff * 32);
+    put(o_ao, t.awave_off, (n + 1) * 4);
+    put(o_aw, t.awave_w, n_awave * 4);
+    put(o_aa, t.awave_aoff, (n_awave + 1) * 4);
+    put(o_eo, t.ext_aoff, (n + 1) * 4);
+    put(o_al, t.anchor_l, n_anchor * 8);
+    put(o_am, t.anchor_micro, n_anchor * 4);
+    put(o_el, t.ext_l, n_ext * 8);
+    put(o_em, t.ext_micro, n_ext * 4);
+    cudaStream_t s = nullptr;
+    cudaError_t ce = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_engine_create: stream");
+    struct SD {
+        cudaStream_t s;
+        ~SD() { cudaStreamDestroy(s); }
+    } sd{s};
+    void* tmp = nullptr;
+    ce = cudaMallocFromPoolAsync(&tmp, ar.used, lib_pool(device), s);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(tmp, stage.data(), ar.used, cudaMemcpyHostToDevice, s);
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_engine_create: table upload");
+    char* b = static_cast<char*>(tmp);
+    DevTables T;
+    T.tv = TabView{reinterpret_cast<const int32_t*>(b + o_W), reinterpret_cast<const double*>(b + o_te),
+                   reinterpret_cast<const int32_t*>(b + o_co), reinterpret_cast<const int32_t*>(b + o_cw),
+                   reinterpret_cast<const double*>(b + o_ct), reinterpret_cast<const int32_t*>(b + o_ao),
+                   reinterpret_cast<const int32_t*>(b + o_aw), reinterpret_cast<const int32_t*>(b + o_aa),
+                   reinterpret_cast<const int32_t*>(b + o_eo), n_anchor};
+    T.anchor_l = reinterpret_cast<const int64_t*>(b + o_al);
+    T.anchor_micro = reinterpret_cast<const int32_t*>(b + o_am);
+    T.n_anchor = n_anchor;
+    T.ext_l = reinterpret_cast<const int64_t*>(b + o_el);
+    T.ext_micro = reinterpret_cast<const int32_t*>(b + o_em);
+    T.n_ext = n_ext;
     auto* e = new wt_engine;
     e->device = device;
-    std::string err;
-    wt_status st = build_image(*tables, *registry, *hw, &e->host, &err);
-    if (st != WT_OK) {
+    const wt_status bs = engine_build(e, P, T, s);
+    cudaFreeAsync(tmp, s);
+    if (bs != WT_OK) {
+        if (e->mem) cudaFree(e->mem);
         delete e;
-        return set_err(st, err);
+        return bs;
     }
-    DeviceGuard guard(device);
-    const HostImage& h = e->host;
-    const size_t C = h.C, R = h.R;
-    Arena ar;
-    size_t o_mid = ar.take(C * 4), o_til = ar.take(C * 16), o_mag = ar.take(C * 16),
-           o_th = ar.take(C * R * 32), o_meta = ar.take(C * R * 4), o_used = ar.take(C * R * 4),
-           o_amap = ar.take(C * R * 8), o_afb = ar.take(C * R * 4),
-           o_al = ar.take(h.anchor_l.size() * 8), o_am = ar.take(h.anchor_micro.size() * 4);
-    const size_t NS = h.seg_pos.size();
-    size_t o_st = ar.take(NS * 16), o_sm = ar.take(NS * 16), o_sp = ar.take(NS * 4), o_cc = ar.take(C * 4),
-           o_th2 = ar.take(C * R * 32), o_m2 = ar.take(C * R * 4), o_th2t = ar.take(C * R * 32),
-           o_m2t = ar.take(C * R * 4), o_smask = ar.take(NS * R * kLB * 4), o_sor = ar.take(NS * R * 4);
-    cudaError_t ce = cudaMalloc(&e->mem, ar.used);
-    if (ce != cudaSuccess) {
-        delete e;
-        return cuda_err(ce, "wt_engine_create: cudaMalloc");
-    }
-    e->bytes = ar.used;
-    char* base = static_cast<char*>(e->mem);
-    struct Piece {
-        size_t off;
-        const void* src;
-        size_t n;
-    } pieces[] = {
-        {o_mid, h.macro_id.data(), C * 4},        {o_til, h.tiles.data(), C * 16},
-        {o_mag, h.magic.data(), C * 16},          {o_th, h.theta.data(), C * R * 32},
-        {o_meta, h.rowmeta.data(), C * R * 4},    {o_used, h.used_w.data(), C * R * 4},
-        {o_amap, h.amap.data(), C * R * 8},       {o_afb, h.afb.data(), C * R * 4},
-        {o_al, h.anchor_l.data(), h.anchor_l.size() * 8},
-        {o_am, h.anchor_micro.data(), h.anchor_micro.size() * 4},
-        {o_st, h.seg_tiles.data(), NS * 16},      {o_sm, h.seg_magic.data(), NS * 16},
-        {o_sp, h.seg_pos.data(), NS * 4},         {o_cc, h.cls_cfg.data(), C * 4},
-        {o_th2, h.theta2.data(), C * R * 32},     {o_m2, h.meta2.data(), C * R * 4},
-        {o_th2t, h.theta2t.data(), C * R * 32},   {o_m2t, h.meta2t.data(), C * R * 4},
-        {o_smask, h.segmask.data(), NS * R * kLB * 4}, {o_sor, h.segor.data(), NS * R * 4},
-    };
-    for (const Piece& p : pieces) {
-        ce = cudaMemcpy(base + p.off, p.src, p.n, cudaMemcpyHostToDevice);
-        if (ce != cudaSuccess) {
-            cudaFree(e->mem);
-            delete e;
-            return cuda_err(ce, "wt_engine_create: upload");
-        }
-    }
-    DevImage& d = e->dev;
-    d.C = h.C;
-    d.R = h.R;
-    d.S = h.S;
-    d.RS = uint32_t(h.R) * uint32_t(h.S);
-    Magic ms = make_magic(uint32_t(h.S));
-    d.mS = ms.m;
-    d.sS = ms.s;
-    d.special = h.special ? 1 : 0;
-    d.macro_id = reinterpret_cast<const int32_t*>(base + o_mid);
-    d.tiles = reinterpret_cast<const int4*>(base + o_til);
-    d.magic = reinterpret_cast<const uint4*>(base + o_mag);
-    d.theta = reinterpret_cast<const double4*>(base + o_th);
-    d.rowmeta = reinterpret_cast<const uint32_t*>(base + o_meta);
-    d.used_w = reinterpret_cast<const int32_t*>(base + o_used);
-    d.amap = reinterpret_cast<const int2*>(base + o_amap);
-    d.afb = reinterpret_cast<const int32_t*>(base + o_afb);
-    d.anchor_l = reinterpret_cast<const int64_t*>(base + o_al);
-    d.anchor_micro = reinterpret_cast<const int32_t*>(base + o_am);
-    d.tm_min = h.tm_min;
-    d.tn_min = h.tn_min;
-    d.nseg = int32_t(NS);
-    d.seg_cfg = h.seg_cfg;
-    d.seg_tiles = reinterpret_cast<const int4*>(base + o_st);
-    d.seg_magic = reinterpret_cast<const uint4*>(base + o_sm);
-    d.seg_pos = reinterpret_cast<const int32_t*>(base + o_sp);
-    d.cls_cfg = reinterpret_cast<const int32_t*>(base + o_cc);
-    d.theta2 = reinterpret_cast<const double4*>(base + o_th2);
-    d.meta2 = reinterpret_cast<const uint32_t*>(base + o_m2);
-    d.theta2t = reinterpret_cast<const double4*>(base + o_th2t);
-    d.meta2t = reinterpret_cast<const uint32_t*>(base + o_m2t);
-    d.segmask = reinterpret_cast<const uint32_t*>(base + o_smask);
-    d.segor = reinterpret_cast<const uint32_t*>(base + o_sor);
-    static const int prune = [] {
-        const char* v = std::getenv("WT_PRUNE");
-        return v ? std::atoi(v) : 1;
-    }();
-    d.prune = prune;
-    d.seg_maxcfg = 1;
-    for (size_t k = 0; k < NS; ++k) d.seg_maxcfg = std::max(d.seg_maxcfg, h.seg_tiles[4 * k + 3]);
-    // list-mode chunk: keep the staged rows near 40 KB so several CTAs fit per SM
-    e->eval_chunk = int(std::max<size_t>(1, std::min<size_t>(C, 40960 / (R * 36 + 32))));
-    e->eval_grid = sm_count(device) * 4;
-    e->eval_grid2 = sm_count(device) * 4;  // upper bound; launch_eval2 clamps to residency
     *out = e;
     return WT_OK;
 }
@@ -401,6 +553,16 @@ wt_status wt_engine_info_get(const wt_engine* e, wt_engine_info* out) {
     return WT_OK;
 }
 
+wt_status wt_engine_prune_masks(const wt_engine* e, uint32_t* masks, int64_t n) {
+    if (!e || !masks) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    const int64_t want = int64_t(e->dev.nseg) * e->dev.R * kLB;
+    if (n != want) return set_err(WT_INVALID_ARGUMENT, "masks must hold n_seg * R * 16 words");
+    DeviceGuard guard(e->device);
+    const cudaError_t ce = cudaMemcpy(masks, e->dev.segmask, size_t(n) * 4, cudaMemcpyDeviceToHost);
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_engine_prune_masks");
+    return WT_OK;
+}
+
 wt_status wt_engine_set_prune(wt_engine* e, int32_t enable) {
     if (!e) return set_err(WT_INVALID_ARGUMENT, "null argument");
     e->dev.prune = enable ? 1 : 0;
@@ -417,20 +579,31 @@ int32_t wt_engine_config_index(const wt_engine* e, int32_t macro_id) {
 int32_t wt_engine_anchor_map(const wt_engine* e, int32_t config, int32_t wave, int32_t extrapolated,
                              int64_t* anchors, int32_t* micros, int32_t cap, int32_t* fallback_wave) {
     if (!e || config < 0 || config >= e->host.C) return -1;
-    const HostImage& h = e->host;
+    const EngineMeta& h = e->host;
     int32_t row;
     if (extrapolated) row = h.R - 1;
     else if (wave >= 1 && wave < h.R) row = wave - 1;
     else return -1;
+    // inspection call: small synchronous reads of the device image
+    DeviceGuard guard(e->device);
     const size_t rr = size_t(config) * h.R + row;
-    if (h.rowmeta[rr] & ROW_NO_ANCHOR) return -1;
-    const int32_t off = h.amap[2 * rr], cnt = h.amap[2 * rr + 1];
-    for (int32_t i = 0; i < cnt && i < cap; ++i) {
-        if (anchors) anchors[i] = h.anchor_l[off + i];
-        if (micros) micros[i] = h.anchor_micro[off + i];
-    }
-    if (fallback_wave) fallback_wave[0] = h.afb[rr];
-    return cnt;
+    uint32_t meta = 0;
+    int2 am{0, 0};
+    int32_t fb = -1;
+    if (cudaMemcpy(&meta, e->dev.rowmeta + rr, 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(&am, e->dev.amap + rr, 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(&fb, e->dev.afb + rr, 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -1;
+    if (meta & ROW_NO_ANCHOR) return -1;
+    const int32_t n = std::min(am.y, std::max(cap, 0));
+    if (n > 0 && anchors &&
+        cudaMemcpy(anchors, e->dev.anchor_l + am.x, size_t(n) * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -1;
+    if (n > 0 && micros &&
+        cudaMemcpy(micros, e->dev.anchor_micro + am.x, size_t(n) * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -1;
+    if (fallback_wave) fallback_wave[0] = fb;
+    return am.y;
 }
 
 static DecOut to_out(const wt_decisions* o) {
@@ -585,7 +758,7 @@ wt_status wt_tune_one(const wt_engine* e, int32_t M, int32_t N, int32_t K, wt_de
             mb = e->mb_h;
             std::memset(static_cast<void*>(mb), 0, sizeof(Mailbox));
         }
-        const int64_t n_anchor = int64_t(e->host.anchor_l.size());
+        const int64_t n_anchor = e->host.n_pool;
         mb->M = M;
         mb->N = N;
         mb->K = K;

@@ -86,41 +86,39 @@ struct DevImage {
 constexpr int kSegCfg = 32;
 constexpr int kLB = 16;  // L buckets of the pruning masks
 
-// Host-side resolved image (built by build_image, uploaded by the C-ABI).
-struct HostImage {
+// Host-side structure of an image (plan_image): everything that depends only
+// on the table ids, their W, the registry and the hardware -- O(C log C) --
+// so the O(C * R) row resolution and the pruning masks can be built on the
+// device from tables that already live there (wt_image_dev.cu).
+struct ImagePlan {
     int32_t C = 0, R = 0, S = 0, family = 0;
-    bool special = false;
-    std::vector<int32_t> macro_id;
-    std::vector<int32_t> W;  // per config
-    std::vector<int32_t> tiles;   // 4 per config
-    std::vector<uint32_t> magic;  // 4 per config
-    std::vector<double> theta;    // 4 per row
-    std::vector<uint32_t> rowmeta;
-    std::vector<int32_t> used_w;
-    std::vector<int32_t> amap;    // 2 per row
-    std::vector<int32_t> afb;
-    std::vector<int64_t> anchor_l;
-    std::vector<int32_t> anchor_micro;
     int32_t tm_min = 0, tn_min = 0;
     int32_t seg_cfg = 32;
-    std::vector<int32_t> seg_tiles;  // 4 per segment
+    std::vector<int32_t> order;      // [C] config (ascending macro_id) -> table index
+    std::vector<int32_t> macro_id;   // [C]
+    std::vector<int32_t> tiles;      // 4 per config {t_m, t_n, t_k, 0}
+    std::vector<uint32_t> magic;     // 4 per config
+    std::vector<int32_t> seg_tiles;  // 4 per segment {t_m, t_n, t_k, ncfg}
     std::vector<uint32_t> seg_magic; // 4 per segment
-    std::vector<int32_t> seg_pos;
-    std::vector<int32_t> cls_cfg;
-    std::vector<double> theta2;
-    std::vector<uint32_t> meta2;
-    std::vector<double> theta2t;  // [R][C] transposed theta2
-    std::vector<uint32_t> meta2t;
-    std::vector<uint32_t> segmask;  // [nseg][R][kLB]
-    std::vector<uint32_t> segor;    // [nseg][R]
+    std::vector<int32_t> seg_pos;    // [nseg] first class-ordered position
+    std::vector<int32_t> cls_cfg;    // [C] class-ordered position -> config
+    std::vector<int32_t> cfg_pos;    // [C] config -> class-ordered position
+    std::vector<int32_t> cls_seg;    // [ncls + 1] first segment of each tile class
+    int32_t seg_maxcfg = 1;
 };
+
+// Validates and plans (the reference's error texts for duplicate ids,
+// unknown ids, empty table sets).  macro_id / W: host arrays of n tables.
+wt_status plan_image(const int32_t* macro_id, const int32_t* W, int32_t n, const wt_registry_desc& reg,
+                     const wt_hw& hw, ImagePlan* out, std::string* err);
+
+// Host-only pruning plan (wt_prune_plan): the same rows and masks the device
+// builder produces, computed on the host from host tables.
+wt_status prune_plan_host(const wt_tables_desc& t, const wt_registry_desc& r, const wt_hw& hw, ImagePlan* plan,
+                          std::vector<uint32_t>* segmask, std::string* err);
 
 // Thread-local message returned by wt_last_error().
 void set_last_error(const std::string& msg);
 
-// Resolves every reference fallback rule into dense rows; returns WT_OK or
-// an error status with *err set to the reference's message.
-wt_status build_image(const wt_tables_desc& t, const wt_registry_desc& r, const wt_hw& hw,
-                      HostImage* out, std::string* err);
 
 }  // namespace wtb
