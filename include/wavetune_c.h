@@ -426,6 +426,26 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
                        wt_build_result* result);
 wt_status wt_build_free(wt_build* b);
 
+/* build_dual_table over records ALREADY IN DEVICE MEMORY (wt_records_desc
+ * with device pointers), stream-ordered on `stream`; the built tables stay on
+ * the device (no host CSR).  Three scalar read-backs size the allocations
+ * (host syncs of the stream); the fit itself, the extrapolation and the CSR
+ * assembly are queued without further syncs.  flags: WT_FIT_BASELINES also
+ * fits the ablation baselines (not part of build_dual_table).  The tables
+ * feed wt_engine_create_from_build directly; wt_build_result_get copies them
+ * to the host on demand. */
+#define WT_FIT_BASELINES 1
+wt_status wt_fit_build_device(const wt_records_desc* records, const int32_t* registry_ids, int32_t n_macros,
+                              int32_t W, int32_t p, int32_t flags, int device, void* stream, wt_build** out);
+/* Host copies of a build's tables (synchronous; valid until wt_build_free). */
+wt_status wt_build_result_get(wt_build* b, wt_build_result* result);
+/* Engine from a build's device-resident tables (registry = the one the build
+ * was fitted against): the image -- rows, tile classes, pruning masks -- is
+ * resolved on the device, the tables never cross PCIe.  Work is queued on
+ * `stream` (ordered after the build); returns once the engine is ready. */
+wt_status wt_engine_create_from_build(const wt_build* b, const wt_registry_desc* registry, const wt_hw* hw,
+                                      void* stream, wt_engine** out);
+
 /* fit_bucket over nb independent buckets in one launch: samples of bucket b
  * are [off[b], off[b+1]) of g/l/t (host arrays).  coeffs [nb*4]. */
 wt_status wt_fit_bucket_batch(const double* g, const double* l, const double* t,

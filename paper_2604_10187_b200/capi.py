@@ -94,7 +94,7 @@ EXPORTS = (
     "wt_last_error wt_version wt_abi_version wt_engine_create wt_engine_destroy wt_engine_info_get "
     "wt_engine_config_index wt_engine_set_prune wt_engine_prune_masks wt_tune_batch wt_tune_grouped_batch wt_predict_batch wt_explain "
     "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_destroy wt_grid_storage wt_sweep wt_grid_finalize "
-    "wt_gather_batch wt_decide_host_sync wt_decide_host_stream_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
+    "wt_fit_build_device wt_build_result_get wt_engine_create_from_build wt_gather_batch wt_decide_host_sync wt_decide_host_stream_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
     "wt_simulate_batch wt_profile_sim wt_tune_one wt_engine_set_resident wt_baseline_create "
     "wt_baseline_destroy wt_baseline_tune_batch wt_baseline_predict_batch wt_set_kernel_timing wt_kernel_time_ms "
     "wt_prune_plan wt_sweep_to wt_grid_ipc_handle wt_ipc_open wt_ipc_close").split()
@@ -166,13 +166,15 @@ def _descs(tables: dict, registry: dict, keep: list):
         keep.append(a)
         return a.ctypes.data
 
-    td = wt_tables_desc()
-    td.n_tables = len(tables["macro_id"])
+    td = None
+    if tables is not None:
+        td = wt_tables_desc()
+        td.n_tables = len(tables["macro_id"])
     dts = dict(macro_id=np.int32, W=np.int32, theta_ext=np.float64, coeff_off=np.int32, coeff_w=np.int32,
                coeff_theta=np.float64, awave_off=np.int32, awave_w=np.int32, awave_aoff=np.int32,
                anchor_l=np.int64, anchor_micro=np.int32, ext_aoff=np.int32, ext_l=np.int64,
                ext_micro=np.int32)
-    for k in _TABLE_FIELDS:
+    for k in _TABLE_FIELDS if tables is not None else ():
         setattr(td, k, arr(tables[k], dts[k]))
     rd = wt_registry_desc()
     rd.family = registry.get("family", WT_FAMILY_DENSE_GEMM)
@@ -219,6 +221,24 @@ class Engine:
         info = wt_engine_info()
         check(L.wt_engine_info_get(h, C.byref(info)))
         self.info = info
+
+    @classmethod
+    def from_build(cls, build: "Build", registry: dict, n_sm: int, blocks_per_sm: int = 1, stream=None):
+        """Engine from a device-resident build (wt_engine_create_from_build)."""
+        self = cls.__new__(cls)
+        keep = []
+        _, rd = _descs(None, registry, keep)
+        hw = wt_hw(n_sm, blocks_per_sm)
+        h = C.c_void_p()
+        check(lib().wt_engine_create_from_build(build.handle, C.byref(rd), C.byref(hw), vp(_stream_ptr(stream)),
+                                                C.byref(h)))
+        self.handle = h
+        self.device = build.device
+        self._keep = []
+        info = wt_engine_info()
+        check(lib().wt_engine_info_get(h, C.byref(info)))
+        self.info = info
+        return self
 
     def close(self):
         if getattr(self, "handle", None):
@@ -472,6 +492,12 @@ def fit_build(records: dict, registry_ids, W: int = 0, p: int = 10, device: int 
     res = wt_build_result()
     check(lib().wt_fit_build(C.byref(rd), C.c_void_p(ids.ctypes.data), C.c_int32(len(ids)), C.c_int32(W),
                              C.c_int32(p), C.c_int(device), C.byref(h), C.byref(res)))
+    out = _result_dict(res)
+    lib().wt_build_free(h)
+    return out
+
+
+def _result_dict(res):
     nt = res.n_tables
     co_off = _np_from(res.coeff_off, nt + 1, np.int32)
     aw_off = _np_from(res.awave_off, nt + 1, np.int32)
@@ -492,15 +518,65 @@ def fit_build(records: dict, registry_ids, W: int = 0, p: int = 10, device: int 
         anchor_partial=_np_from(res.anchor_partial, nan, np.int32), ext_aoff=ex_off,
         ext_l=_np_from(res.ext_l, next_, np.int64), ext_micro=_np_from(res.ext_micro, next_, np.int32))
     out["W_arr"] = np.full(nt, res.W, np.int32)
-    # ablation baselines from the same selected samples (tuner.cpp:191-220)
-    s_off = _np_from(res.step_off, nt + 1, np.int32)
-    out.update(step_off=s_off, step_l=_np_from(res.step_l, int(s_off[-1]), np.int64),
-               step_t=_np_from(res.step_t, int(s_off[-1]), np.float64),
-               lin_theta=_np_from(res.lin_theta, 4 * nt, np.float64), lin_r2=_np_from(res.lin_r2, nt, np.float64),
-               lin_mape=_np_from(res.lin_mape, nt, np.float64),
-               lin_degenerate=_np_from(res.lin_degenerate, nt, np.int32))
-    lib().wt_build_free(h)
+    if res.step_off:  # ablation baselines from the same selected samples (tuner.cpp:191-220)
+        s_off = _np_from(res.step_off, nt + 1, np.int32)
+        out.update(step_off=s_off, step_l=_np_from(res.step_l, int(s_off[-1]), np.int64),
+                   step_t=_np_from(res.step_t, int(s_off[-1]), np.float64),
+                   lin_theta=_np_from(res.lin_theta, 4 * nt, np.float64),
+                   lin_r2=_np_from(res.lin_r2, nt, np.float64), lin_mape=_np_from(res.lin_mape, nt, np.float64),
+                   lin_degenerate=_np_from(res.lin_degenerate, nt, np.int32))
     return out
+
+
+TABLE_KEYS = ("macro_id", "theta_ext", "coeff_off", "coeff_w", "coeff_theta", "awave_off", "awave_w", "awave_aoff",
+              "anchor_l", "anchor_micro", "ext_aoff", "ext_l", "ext_micro")
+
+
+def engine_tables(fit: dict) -> dict:
+    """The tables of a fit result in wt_engine_create's input layout."""
+    t = {k: fit[k] for k in TABLE_KEYS}
+    t["W"] = fit["W_arr"]
+    return t
+
+
+class Build:
+    """A K2 build whose tables stay on the device (wt_fit_build_device):
+    records are device tensors, work is stream-ordered, and the engine is
+    made from the device tables (Engine.from_build) without a host copy."""
+
+    FIT_BASELINES = 1
+
+    def __init__(self, records: dict, registry_ids, W: int = 0, p: int = 10, flags: int = 0, device: int = 0,
+                 stream=None):
+        rd = wt_records_desc()
+        rd.n = int(records["g"].numel())
+        rd.g, rd.l, rd.w = _ptr(records["g"]), _ptr(records["l"]), _ptr(records["w"])
+        rd.macro_id, rd.micro_id = _ptr(records["macro"]), _ptr(records["micro"])
+        rd.latency_us = _ptr(records["lat"])
+        self._ids = np.ascontiguousarray(registry_ids, np.int32)
+        h = C.c_void_p()
+        check(lib().wt_fit_build_device(C.byref(rd), C.c_void_p(self._ids.ctypes.data), C.c_int32(len(self._ids)),
+                                        C.c_int32(W), C.c_int32(p), C.c_int32(flags), C.c_int(device),
+                                        vp(_stream_ptr(stream)), C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def result(self) -> dict:
+        """Host copies of the tables + diagnostics (wt_build_result_get)."""
+        res = wt_build_result()
+        check(lib().wt_build_result_get(self.handle, C.byref(res)))
+        return _result_dict(res)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().wt_build_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def fit_bucket_batch(g, l, t, off, device: int = 0):

@@ -59,15 +59,6 @@ struct DeviceGuard {
     }
 };
 
-// One device allocation carved into 256-byte aligned pieces.
-struct Arena {
-    size_t used = 0;
-    size_t take(size_t bytes) {
-        size_t off = used;
-        used += (bytes + 255) & ~size_t(255);
-        return off;
-    }
-};
 
 // Library-owned stream-ordered pool: scratch stays mapped between calls
 // (release threshold = max), so per-call compaction buffers cost nothing
@@ -509,7 +500,7 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
                    reinterpret_cast<const int32_t*>(b + o_co), reinterpret_cast<const int32_t*>(b + o_cw),
                    reinterpret_cast<const double*>(b + o_ct), reinterpret_cast<const int32_t*>(b + o_ao),
                    reinterpret_cast<const int32_t*>(b + o_aw), reinterpret_cast<const int32_t*>(b + o_aa),
-                   reinterpret_cast<const int32_t*>(b + o_eo), n_anchor};
+                   reinterpret_cast<const int32_t*>(b + o_eo), n_anchor, nullptr};
     T.anchor_l = reinterpret_cast<const int64_t*>(b + o_al);
     T.anchor_micro = reinterpret_cast<const int32_t*>(b + o_am);
     T.n_anchor = n_anchor;
@@ -520,6 +511,39 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
     e->device = device;
     const wt_status bs = engine_build(e, P, T, s);
     cudaFreeAsync(tmp, s);
+    if (bs != WT_OK) {
+        if (e->mem) cudaFree(e->mem);
+        delete e;
+        return bs;
+    }
+    *out = e;
+    return WT_OK;
+}
+
+wt_status wt_engine_create_from_build(const wt_build* b, const wt_registry_desc* registry, const wt_hw* hw,
+                                      void* stream, wt_engine** out) {
+    NvtxRange nvtx_("wt_engine_create_from_build");
+    if (!b || !registry || !hw || !out) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    BuildTables bt{};
+    if (build_device_tables(b, &bt) != WT_OK) return set_err(WT_INVALID_ARGUMENT, "invalid build");
+    std::vector<int32_t> W(bt.n_tables, bt.W);
+    ImagePlan P;
+    std::string err;
+    const wt_status st = plan_image(bt.macro_id_host, W.data(), bt.n_tables, *registry, *hw, &P, &err);
+    if (st != WT_OK) return set_err(st, err);
+    DeviceGuard guard(bt.device);
+    DevTables T;
+    T.tv = bt.tv;
+    T.anchor_l = bt.anchor_l;
+    T.anchor_micro = bt.anchor_micro;
+    T.n_anchor = bt.n_anchor;
+    T.ext_l = bt.ext_l;
+    T.ext_micro = bt.ext_micro;
+    T.n_ext = bt.n_ext;
+    auto* e = new wt_engine;
+    e->device = bt.device;
+    const wt_status bs = engine_build(e, P, T, static_cast<cudaStream_t>(stream));
     if (bs != WT_OK) {
         if (e->mem) cudaFree(e->mem);
         delete e;

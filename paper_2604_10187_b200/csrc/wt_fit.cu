@@ -36,6 +36,7 @@
 
 #include "wavetune_c.h"
 #include "wt_decide.h"
+#include "wt_image_dev.h"
 #include "wt_internal.h"
 
 namespace wtb {
@@ -315,7 +316,7 @@ struct Rec {
 };
 
 __global__ void k_mpos(Rec rc, int64_t n, const int32_t* ids_sorted, const int32_t* pos_sorted, int nm,
-                       int32_t* mpos, int32_t* valid) {
+                       int32_t* mpos, int32_t* valid, int32_t* has_rec) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int32_t id = rc.macro[i];
@@ -330,6 +331,7 @@ __global__ void k_mpos(Rec rc, int64_t n, const int32_t* ids_sorted, const int32
     const bool ok = lo < nm && ids_sorted[lo] == id;
     mpos[i] = ok ? pos_sorted[lo] : INT_MAX;
     valid[i] = ok ? 1 : 0;
+    if (ok) has_rec[pos_sorted[lo]] = 1;  // group_records finds this macro
 }
 
 struct Ranges {
@@ -343,7 +345,7 @@ __global__ void k_ranges(Rec rc, const int64_t* idx, int64_t n, Ranges* out) {
     unsigned long long gmin = ~0ULL, gmax = 0, lmin = ~0ULL, lmax = 0;
     int wmin = INT_MAX, wmax = INT_MIN, umin = INT_MAX, umax = INT_MIN;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t r = idx[i];
+        const int64_t r = idx ? idx[i] : i;  // idx == null: every record
         // offset by 2^63 so signed order becomes unsigned order
         const unsigned long long g = (unsigned long long)rc.g[r] ^ 0x8000000000000000ULL;
         const unsigned long long l = (unsigned long long)rc.l[r] ^ 0x8000000000000000ULL;
@@ -784,11 +786,46 @@ __global__ void k_extrap(Rec rc, const double* sg, const double* sl, const doubl
     (void)slo_group;
 }
 
+// Device-resident table CSR (wt_tables_desc layout, int32) from the fit's
+// bucket / group / macro boundaries -- the tables never leave HBM on their
+// way to the engine (wt_engine_create_from_build).  One thread per index of
+// the longest array (NB + 1).
+struct Csr32 {
+    int32_t* macro_id;    // [NM] registry id
+    int32_t* W;           // [NM]
+    int32_t* coeff_off;   // [NM+1] = awave_off (one wave map per bucket)
+    int32_t* coeff_w;     // [NB]   = awave_w
+    int32_t* awave_aoff;  // [NB+1] group range of each bucket (anchors = groups)
+    int32_t* ext_off;     // [NM]   first group of the macro: its ext-anchor slice
+    int32_t* nsamp;       // [NB]   diagnostics: samples per bucket
+    int32_t* dflags;      // [NB]   bit0 degenerate_fit, bit1 sparse_bucket
+};
+__global__ void k_csr32(int64_t NM, int64_t NB, const int64_t* mbs, const int64_t* bw, const int64_t* bgs,
+                        const int64_t* slo, const int64_t* shi, const int32_t* degen, const int64_t* mpos,
+                        const int32_t* reg_ids, int32_t W, Csr32 o) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i <= NM) o.coeff_off[i] = int32_t(mbs[i]);
+    if (i < NM) {
+        o.macro_id[i] = reg_ids[mpos[i]];
+        o.W[i] = W;
+        o.ext_off[i] = int32_t(bgs[mbs[i]]);
+    }
+    if (i < NB) {
+        o.coeff_w[i] = int32_t(bw[i]);
+        const int32_t ns = int32_t(shi[i] - slo[i]);
+        o.nsamp[i] = ns;
+        o.dflags[i] = (degen[i] ? 1 : 0) | (ns < 4 ? 2 : 0);
+    }
+    if (i <= NB) o.awave_aoff[i] = int32_t(bgs[i]);
+}
+
 }  // namespace fit
 }  // namespace wtb
 
 // ------------------------------------------------------------------ C-ABI
 using namespace wtb::fit;
+using wtb::Arena;
+using wtb::TabView;
 
 namespace {
 // errors surface through wt_last_error() (wt_capi.cu)
@@ -804,7 +841,33 @@ struct FitErr {
 } g_fit_err;
 }
 
+// The build: tables (and diagnostics) resident on the device, in the
+// wt_tables_desc CSR layout, until wt_build_free.  Host copies are made on
+// demand (wt_build_result_get) -- the engine is built from the device arrays
+// directly (wt_engine_create_from_build).
 struct wt_build {
+    int device = 0;
+    int32_t NM = 0, W = 0, p = 0;
+    int64_t NB = 0, G = 0;
+    bool baselines = false;
+    double device_ms = 0.0;
+    std::vector<void*> mem;  // device blocks owned by the build
+    // device outputs
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, done = nullptr;  // fit start / end (device_ms), all work queued
+    int32_t* d_degen = nullptr;
+    int32_t *t_macro = nullptr, *t_W = nullptr, *t_coeff_off = nullptr, *t_coeff_w = nullptr,
+            *t_awave_aoff = nullptr, *t_ext_off = nullptr, *t_ext_cnt = nullptr, *t_anchor_micro = nullptr,
+            *t_ext_micro = nullptr, *d_nsamp = nullptr, *d_dflags = nullptr, *d_partial = nullptr,
+            *d_ext_flags = nullptr;
+    double *t_theta_ext = nullptr, *t_coeff_theta = nullptr, *d_r2 = nullptr, *d_mape = nullptr;
+    int64_t *t_anchor_l = nullptr, *t_ext_l = nullptr;
+    // ablation baselines (when requested)
+    double *b_lin = nullptr, *b_lin_r2 = nullptr, *b_lin_mape = nullptr, *b_step_t = nullptr;
+    int32_t *b_lin_deg = nullptr, *b_nslot = nullptr;
+    int64_t* b_step_l = nullptr;
+    std::vector<int32_t> h_macro_id;  // registry order, known on the host at build time
+    // host copies (wt_build_result_get)
+    bool host_ready = false;
     std::vector<int32_t> macro_id, ext_flags, coeff_off, coeff_w, diag_samples, diag_flags, awave_off, awave_w,
         awave_aoff, anchor_micro, anchor_partial, ext_aoff, ext_micro, step_off, lin_degen;
     std::vector<double> theta_ext, coeff_theta, diag_r2, diag_mape, step_t, lin_theta, lin_r2, lin_mape;
@@ -845,11 +908,12 @@ T* dalloc(std::vector<void*>& owned, size_t n) {
     return static_cast<T*>(p);
 }
 
+// stream-ordered release of the temporaries at scope exit (no host sync)
 struct OwnedFree {
     std::vector<void*>* v;
+    cudaStream_t s;
     ~OwnedFree() {
-        for (void* q : *v) t_alloc_pool ? cudaFreeAsync(q, t_alloc_stream) : cudaFree(q);
-        if (t_alloc_pool) cudaStreamSynchronize(t_alloc_stream);
+        for (void* q : *v) cudaFreeAsync(q, s);
         t_alloc_pool = nullptr;
         t_alloc_stream = nullptr;
     }
@@ -902,73 +966,16 @@ wt_status run_sort(const Rec& rc, const int32_t* mpos, int64_t* perm, int64_t* p
     return WT_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_ids, int32_t n_macros,
-                       int32_t W, int32_t p, int device, wt_build** out, wt_build_result* result) {
-    if (!records || !out || !result || (n_macros > 0 && !registry_ids)) {
-        g_fit_err = "null argument";
-        return WT_INVALID_ARGUMENT;
-    }
-    *out = nullptr;
-    const int64_t n_all = records->n;
-    if (n_all <= 0) {
-        g_fit_err = "build_dual_table: empty record set";
-        return WT_INVALID_ARGUMENT;
-    }
-    int prev_dev = 0;
-    cudaGetDevice(&prev_dev);
-    cudaSetDevice(device);
-    struct Restore {
-        int d;
-        ~Restore() { cudaSetDevice(d); }
-    } restore{prev_dev};
-    cudaStream_t s;
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    struct SD {
-        cudaStream_t s;
-        ~SD() { cudaStreamDestroy(s); }
-    } sd{s};
+// build_dual_table (model.cpp:194-253) over records resident on the device,
+// stream-ordered on s.  Host synchronisations: three scalar read-backs that
+// size the next allocations (valid-record count + key ranges + per-macro
+// presence; group count; bucket / sample counts).  Outputs land in B.
+wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, int32_t n_macros, int32_t W,
+                   int32_t p, bool baselines, int device, cudaStream_t s, wt_build* B) {
     t_alloc_stream = s;
     t_alloc_pool = wtb::device_pool(device);
     std::vector<void*> owned;
-    OwnedFree freer{&owned};  // released (stream-ordered) before the stream dies
-
-    // W = params.W or the highest wave in the data (model.cpp:201-203)
-    if (W <= 0)
-        for (int64_t i = 0; i < n_all; ++i) W = std::max(W, records->w[i]);
-
-    // upload records
-    Rec rc{};
-    int64_t* dg = dalloc<int64_t>(owned, n_all);
-    int64_t* dl = dalloc<int64_t>(owned, n_all);
-    int32_t* dw = dalloc<int32_t>(owned, n_all);
-    int32_t* dma = dalloc<int32_t>(owned, n_all);
-    int32_t* dmi = dalloc<int32_t>(owned, n_all);
-    double* dt = dalloc<double>(owned, n_all);
-    if (!dg || !dl || !dw || !dma || !dmi || !dt) {
-        g_fit_err = "cudaMalloc failed";
-        return WT_CUDA_ERROR;
-    }
-    CK(cudaMemcpyAsync(dg, records->g, n_all * 8, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(dl, records->l, n_all * 8, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(dw, records->w, n_all * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(dma, records->macro_id, n_all * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(dmi, records->micro_id, n_all * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(dt, records->latency_us, n_all * 8, cudaMemcpyHostToDevice, s));
-    rc.g = dg;
-    rc.l = dl;
-    rc.w = dw;
-    rc.macro = dma;
-    rc.micro = dmi;
-    rc.lat = dt;
-
-    cudaEvent_t ev0, ev1;
-    cudaEventCreate(&ev0);
-    cudaEventCreate(&ev1);
-    CK(cudaEventRecord(ev0, s));
+    OwnedFree freer{&owned, s};  // temporaries released stream-ordered after the last kernel
     // WT_FIT_TRACE=1 prints a synchronised wall-clock breakdown of the stages
     const bool tr = std::getenv("WT_FIT_TRACE") != nullptr;
     auto t_start = std::chrono::steady_clock::now();
@@ -985,47 +992,69 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
     for (int32_t i = 0; i < n_macros; ++i) ids.push_back({registry_ids[i], i});
     std::stable_sort(ids.begin(), ids.end(), [](auto& a, auto& b) { return a.first < b.first; });
     ids.erase(std::unique(ids.begin(), ids.end(), [](auto& a, auto& b) { return a.first == b.first; }), ids.end());
-    std::vector<int32_t> hid, hpos;
-    for (auto& x : ids) {
-        hid.push_back(x.first);
-        hpos.push_back(x.second);
+    const int nid = int(ids.size());
+    // one upload: sorted ids | their registry positions | registry ids (order)
+    std::vector<int32_t> hup(2 * size_t(nid) + size_t(n_macros));
+    for (int i = 0; i < nid; ++i) {
+        hup[i] = ids[i].first;
+        hup[nid + i] = ids[i].second;
     }
-    int32_t* did = dalloc<int32_t>(owned, hid.size());
-    int32_t* dpos = dalloc<int32_t>(owned, hid.size());
-    CK(cudaMemcpyAsync(did, hid.data(), hid.size() * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(dpos, hpos.data(), hpos.size() * 4, cudaMemcpyHostToDevice, s));
+    std::copy(registry_ids, registry_ids + n_macros, hup.begin() + 2 * nid);
+    int32_t* dup = dalloc<int32_t>(owned, hup.size());
+    // read-back block: nvalid (i64) | ranges | has_rec[n_macros]
+    struct Head {
+        int64_t nvalid;
+        Ranges r;
+    };
+    const size_t rb_bytes = sizeof(Head) + size_t(n_macros) * 4;
+    char* drb = dalloc<char>(owned, rb_bytes);
     int32_t* mpos = dalloc<int32_t>(owned, n_all);
     int32_t* valid = dalloc<int32_t>(owned, n_all);
-    const int blocks_all = int((n_all + 255) / 256);
-    k_mpos<<<blocks_all, 256, 0, s>>>(rc, n_all, did, dpos, int(hid.size()), mpos, valid);
-    // compact valid record indices, order preserved
     int64_t* idx = dalloc<int64_t>(owned, n_all);
-    int64_t* idx2 = dalloc<int64_t>(owned, n_all);
-    int64_t* nvalid_d = dalloc<int64_t>(owned, 1);
-    {
+    if (!dup || !drb || !mpos || !valid || !idx) {
+        g_fit_err = "cudaMalloc failed";
+        return WT_CUDA_ERROR;
+    }
+    CK(cudaMemcpyAsync(dup, hup.data(), hup.size() * 4, cudaMemcpyHostToDevice, s));
+    Head h0{};
+    h0.r = Ranges{~0ULL, 0ULL, ~0ULL, 0ULL, INT_MAX, INT_MIN, INT_MAX, INT_MIN};
+    CK(cudaMemcpyAsync(drb, &h0, sizeof(Head), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(drb + sizeof(Head), 0, size_t(n_macros) * 4, s));
+    Head* dh = reinterpret_cast<Head*>(drb);
+    int32_t* has_rec = reinterpret_cast<int32_t*>(drb + sizeof(Head));
+    const int blocks_all = int((n_all + 255) / 256);
+    k_mpos<<<blocks_all, 256, 0, s>>>(rc, n_all, dup, dup + nid, nid, mpos, valid, has_rec);
+    // key ranges over every record (a superset of the valid ones: packing
+    // stays exact) and max w over ALL records (model.cpp:201-203)
+    k_ranges<<<int(std::min<int64_t>((n_all + 255) / 256, 148 * 4)), 256, 0, s>>>(rc, nullptr, n_all, &dh->r);
+    {  // compact valid record indices, order preserved
         cub::CountingInputIterator<int64_t> it(0);
         size_t need = 0;
-        cub::DeviceSelect::Flagged(nullptr, need, it, valid, idx, nvalid_d, n_all, s);
+        cub::DeviceSelect::Flagged(nullptr, need, it, valid, idx, &dh->nvalid, n_all, s);
         void* t = nullptr;
         CK(talloc(&t, need, s));
-        CK(cub::DeviceSelect::Flagged(t, need, it, valid, idx, nvalid_d, n_all, s));
+        CK(cub::DeviceSelect::Flagged(t, need, it, valid, idx, &dh->nvalid, n_all, s));
         cudaFreeAsync(t, s);
     }
-    int64_t n = 0;
-    CK(cudaMemcpyAsync(&n, nvalid_d, 8, cudaMemcpyDeviceToHost, s));
-    Ranges* dr = dalloc<Ranges>(owned, 1);
-    Ranges init{~0ULL, 0ULL, ~0ULL, 0ULL, INT_MAX, INT_MIN, INT_MAX, INT_MIN};
+    std::vector<char> hrb(rb_bytes);
+    CK(cudaMemcpyAsync(hrb.data(), drb, rb_bytes, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    Head hh;
+    std::memcpy(&hh, hrb.data(), sizeof(Head));
+    const int64_t n = hh.nvalid;
+    const Ranges hr = hh.r;
+    if (W <= 0) W = std::max(0, hr.wmax);
     if (n == 0) {
         g_fit_err = "build_dual_table: no macro produced a table";
         return WT_RUNTIME_ERROR;
     }
-    CK(cudaMemcpyAsync(dr, &init, sizeof(Ranges), cudaMemcpyHostToDevice, s));
-    k_ranges<<<int(std::min<int64_t>((n + 255) / 256, 148 * 4)), 256, 0, s>>>(rc, idx, n, dr);
-    Ranges hr;
-    CK(cudaMemcpyAsync(&hr, dr, sizeof(Ranges), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-
+    B->h_macro_id.clear();
+    {
+        const int32_t* hr_has = reinterpret_cast<const int32_t*>(hrb.data() + sizeof(Head));
+        for (int32_t i = 0; i < n_macros; ++i)
+            if (hr_has[i]) B->h_macro_id.push_back(registry_ids[i]);
+    }
+    // (the ranges' g / l / w / micro bounds cover every record)
     const int bits_g = bits_for(hr.gmax - hr.gmin), bits_l = bits_for(hr.lmax - hr.lmin);
     const int bits_w = bits_for((unsigned long long)((long long)hr.wmax - hr.wmin));
     const int bits_u = bits_for((unsigned long long)((long long)hr.umax - hr.umin));
@@ -1036,6 +1065,10 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
     auto passA = plan_passes({fg, fu, fl, fw, fm});
     auto passB = plan_passes({fg, fl, fw, fm});
 
+    CK(cudaEventCreate(&B->ev0));
+    CK(cudaEventCreate(&B->ev1));
+    CK(cudaEventCreateWithFlags(&B->done, cudaEventDisableTiming));
+    CK(cudaEventRecord(B->ev0, s));
     trace("registry + ranges");
     // 2. stable sorts
     int64_t* ordA = dalloc<int64_t>(owned, n);
@@ -1067,21 +1100,37 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
         CK(cub::DeviceScan::ExclusiveSum(t, need, gflag, gid, n, s));
         cudaFreeAsync(t, s);
     }
-    int32_t last_gid = 0, last_flag = 0;
-    CK(cudaMemcpyAsync(&last_gid, gid + n - 1, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&last_flag, gflag + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    int32_t last2[2] = {0, 0};
+    CK(cudaMemcpyAsync(&last2[0], gid + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&last2[1], gflag + n - 1, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    const int64_t G = int64_t(last_gid) + last_flag;
+    const int64_t G = int64_t(last2[0]) + last2[1];
+    // G-sized outputs (anchors = groups; ext-anchor slices live at each
+    // macro's first group) in one block owned by the build
+    {
+        Arena ar;
+        const size_t o_gl = ar.take(G * 8), o_gm = ar.take(G * 4), o_gp = ar.take(G * 4), o_el = ar.take(G * 8),
+                     o_em = ar.take(G * 4);
+        char* blk = dalloc<char>(B->mem, ar.used);
+        if (!blk) {
+            g_fit_err = "cudaMalloc failed (build outputs)";
+            return WT_CUDA_ERROR;
+        }
+        B->t_anchor_l = reinterpret_cast<int64_t*>(blk + o_gl);
+        B->t_anchor_micro = reinterpret_cast<int32_t*>(blk + o_gm);
+        B->d_partial = reinterpret_cast<int32_t*>(blk + o_gp);
+        B->t_ext_l = reinterpret_cast<int64_t*>(blk + o_el);
+        B->t_ext_micro = reinterpret_cast<int32_t*>(blk + o_em);
+    }
     int64_t* gstart = dalloc<int64_t>(owned, G + 1);
     k_group_starts<<<blocks, 256, 0, s>>>(gflag, gid, n, gstart);
     CK(cudaMemcpyAsync(gstart + G, &n, 8, cudaMemcpyHostToDevice, s));
-    Groups gr{gstart, dalloc<int32_t>(owned, G), dalloc<int32_t>(owned, G), dalloc<int64_t>(owned, G),
-              dalloc<int64_t>(owned, G), dalloc<int32_t>(owned, G)};
+    Groups gr{gstart, B->t_anchor_micro, B->d_partial, dalloc<int64_t>(owned, G), dalloc<int64_t>(owned, G),
+              dalloc<int32_t>(owned, G)};
     const int gblocks = int((G + 127) / 128);
     k_select<<<gblocks, 128, 0, s>>>(rc, ordA, ordB, G, gr);
     // sample offsets
     int64_t* soff = dalloc<int64_t>(owned, G + 1);
-    int64_t* ns64 = dalloc<int64_t>(owned, G);
     {
         // widen nsamp to int64 via a transform iterator
         auto wid = cub::TransformInputIterator<int64_t, cub::CastOp<int64_t>, const int32_t*>(gr.nsamp,
@@ -1093,12 +1142,11 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
         CK(cub::DeviceScan::ExclusiveSum(t, need, wid, soff, G, s));
         cudaFreeAsync(t, s);
     }
-    (void)ns64;
     trace("groups + select");
     // group keys and bucket / macro boundaries, all on the device
     int64_t* gm = dalloc<int64_t>(owned, G);
     int64_t* gw = dalloc<int64_t>(owned, G);
-    int64_t* gl = dalloc<int64_t>(owned, G);
+    int64_t* gl = B->t_anchor_l;
     int32_t* bflag = dalloc<int32_t>(owned, G);
     int32_t* mflag = dalloc<int32_t>(owned, G);
     int32_t* bid = dalloc<int32_t>(owned, G);
@@ -1113,17 +1161,51 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
         cudaFreeAsync(t, s);
     }
     int32_t tail4[4];
-    int64_t tail2[2];
+    int64_t tail_soff = 0;
+    int32_t last_ns = 0;
     CK(cudaMemcpyAsync(&tail4[0], bid + G - 1, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&tail4[1], bflag + G - 1, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&tail4[2], mid + G - 1, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&tail4[3], mflag + G - 1, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&tail2[0], soff + G - 1, 8, cudaMemcpyDeviceToHost, s));
-    int32_t last_ns = 0;
+    CK(cudaMemcpyAsync(&tail_soff, soff + G - 1, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&last_ns, gr.nsamp + G - 1, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const int64_t NB = int64_t(tail4[0]) + tail4[1], NM = int64_t(tail4[2]) + tail4[3];
-    const int64_t S_total = tail2[0] + last_ns;
+    const int64_t S_total = tail_soff + last_ns;
+    if (NM != int64_t(B->h_macro_id.size())) {
+        g_fit_err = "build_dual_table: macro count mismatch";
+        return WT_RUNTIME_ERROR;
+    }
+    // NM / NB-sized outputs in one block owned by the build
+    {
+        Arena ar;
+        const size_t o_mac = ar.take(NM * 4), o_W = ar.take(NM * 4), o_te = ar.take(NM * 32),
+                     o_co = ar.take((NM + 1) * 4), o_cw = ar.take(NB * 4), o_ct = ar.take(NB * 32),
+                     o_aa = ar.take((NB + 1) * 4), o_eo = ar.take(NM * 4), o_ec = ar.take(NM * 4),
+                     o_ns = ar.take(NB * 4), o_df = ar.take(NB * 4), o_ef = ar.take(NM * 4), o_r2 = ar.take(NB * 8),
+                     o_mp = ar.take(NB * 8), o_dg = ar.take(NB * 4);
+        char* blk = dalloc<char>(B->mem, ar.used);
+        if (!blk) {
+            g_fit_err = "cudaMalloc failed (build outputs)";
+            return WT_CUDA_ERROR;
+        }
+        B->t_macro = reinterpret_cast<int32_t*>(blk + o_mac);
+        B->t_W = reinterpret_cast<int32_t*>(blk + o_W);
+        B->t_theta_ext = reinterpret_cast<double*>(blk + o_te);
+        B->t_coeff_off = reinterpret_cast<int32_t*>(blk + o_co);
+        B->t_coeff_w = reinterpret_cast<int32_t*>(blk + o_cw);
+        B->t_coeff_theta = reinterpret_cast<double*>(blk + o_ct);
+        B->t_awave_aoff = reinterpret_cast<int32_t*>(blk + o_aa);
+        B->t_ext_off = reinterpret_cast<int32_t*>(blk + o_eo);
+        B->t_ext_cnt = reinterpret_cast<int32_t*>(blk + o_ec);
+        B->d_nsamp = reinterpret_cast<int32_t*>(blk + o_ns);
+        B->d_dflags = reinterpret_cast<int32_t*>(blk + o_df);
+        B->d_ext_flags = reinterpret_cast<int32_t*>(blk + o_ef);
+        B->d_r2 = reinterpret_cast<double*>(blk + o_r2);
+        B->d_mape = reinterpret_cast<double*>(blk + o_mp);
+        B->d_degen = reinterpret_cast<int32_t*>(blk + o_dg);
+    }
+    int32_t* bdegen = B->d_degen;
     double* sg = dalloc<double>(owned, S_total);
     double* sl = dalloc<double>(owned, S_total);
     double* stt = dalloc<double>(owned, S_total);
@@ -1142,134 +1224,179 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
     k_bucket_meta<<<gblocks, 128, 0, s>>>(G, gm, gw, soff, bflag, bid, mflag, mid, d_bgs, d_bw, d_bslo, d_mbs,
                                           d_mpos);
     k_bucket_tail<<<int((NB + 127) / 128), 128, 0, s>>>(NB, NM, G, S_total, soff, d_bgs, d_bshi, d_mbs);
-    Buckets bk{NB, d_bslo, d_bshi, dalloc<double>(owned, NB * 4), dalloc<double>(owned, NB),
-               dalloc<double>(owned, NB), dalloc<int32_t>(owned, NB)};
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    Buckets bk{NB, d_bslo, d_bshi, B->t_coeff_theta, B->d_r2, B->d_mape, bdegen};
+    const int nsm = wtb::device_sms();
     trace("samples + meta");
     k_fit<<<nsm * 8, 128, 0, s>>>(sg, sl, stt, bk, scratch);
     trace("k_fit");
-    Macros mc{NM, d_mbs, d_bw, d_bgs, W, p, dalloc<double>(owned, NM * 4), dalloc<int32_t>(owned, NM),
-              dalloc<int32_t>(owned, NM), dalloc<int64_t>(owned, G), dalloc<int32_t>(owned, G)};
+    Macros mc{NM, d_mbs, d_bw, d_bgs, W, p, B->t_theta_ext, B->d_ext_flags, B->t_ext_cnt, B->t_ext_l, B->t_ext_micro};
     // extrapolation pools reuse the bucket scratch layout (slice of the pooled samples)
     k_extrap<<<nsm * 4, 128, 0, s>>>(rc, sg, sl, stt, bk, soff, gr, ordA, mc, scratch);
     trace("k_extrap");
-    // ablation baselines from the same selected samples
-    int64_t* d_mslo = dalloc<int64_t>(owned, NM);
-    int64_t* d_mshi = dalloc<int64_t>(owned, NM);
-    k_macro_samples<<<int((NM + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, soff, G, S_total, d_mslo, d_mshi);
-    Buckets lin{NM, d_mslo, d_mshi, dalloc<double>(owned, NM * 4), dalloc<double>(owned, NM),
-                dalloc<double>(owned, NM), dalloc<int32_t>(owned, NM)};
-    k_fit<<<nsm * 8, 128, 0, s>>>(sg, sl, stt, lin, scratch);
-    int64_t* d_sll = dalloc<int64_t>(owned, G);
-    double* d_snum = dalloc<double>(owned, G);
-    double* d_sden = dalloc<double>(owned, G);
-    int32_t* d_nslot = dalloc<int32_t>(owned, NM);
     {
-        // slot counts per macro bound the parallel variant (distinct l per macro)
+        Csr32 o{B->t_macro, B->t_W, B->t_coeff_off, B->t_coeff_w, B->t_awave_aoff, B->t_ext_off, B->d_nsamp,
+                B->d_dflags};
+        k_csr32<<<int((NB + 1 + 255) / 256), 256, 0, s>>>(NM, NB, d_mbs, d_bw, d_bgs, d_bslo, d_bshi, bdegen, d_mpos,
+                                                          dup + 2 * nid, W, o);
+    }
+    CK(cudaEventRecord(B->ev1, s));
+    if (baselines) {
+        // ablation baselines from the same selected samples (not part of
+        // build_dual_table; outside the build's device time)
+        int64_t* d_mslo = dalloc<int64_t>(owned, NM);
+        int64_t* d_mshi = dalloc<int64_t>(owned, NM);
+        k_macro_samples<<<int((NM + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, soff, G, S_total, d_mslo, d_mshi);
+        B->b_lin = dalloc<double>(B->mem, NM * 4);
+        B->b_lin_r2 = dalloc<double>(B->mem, NM);
+        B->b_lin_mape = dalloc<double>(B->mem, NM);
+        B->b_lin_deg = dalloc<int32_t>(B->mem, NM);
+        B->b_step_l = dalloc<int64_t>(B->mem, G);
+        B->b_step_t = dalloc<double>(B->mem, G);
+        B->b_nslot = dalloc<int32_t>(B->mem, NM);
+        double* d_sden = dalloc<double>(owned, G);
+        if (!B->b_lin || !B->b_step_t || !B->b_nslot || !d_sden) {
+            g_fit_err = "cudaMalloc failed (baselines)";
+            return WT_CUDA_ERROR;
+        }
+        Buckets lin{NM, d_mslo, d_mshi, B->b_lin, B->b_lin_r2, B->b_lin_mape, B->b_lin_deg};
+        k_fit<<<nsm * 8, 128, 0, s>>>(sg, sl, stt, lin, scratch);
         static const bool serial = std::getenv("WT_STEP_SERIAL") != nullptr;
         if (serial) {
-            k_step<<<int((NM + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, gw, gl, soff, gr.nsamp, stt, d_sll, d_snum,
-                                                          d_sden, d_nslot);
+            k_step<<<int((NM + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, gw, gl, soff, gr.nsamp, stt, B->b_step_l,
+                                                          B->b_step_t, d_sden, B->b_nslot);
         } else {
-            k_step_slots<<<int((NM + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, gl, d_sll, d_nslot);
+            k_step_slots<<<int((NM + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, gl, B->b_step_l, B->b_nslot);
             const int64_t nt = NM * kStepMaxSlots;
-            k_step_sum<<<int((nt + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, gw, gl, soff, gr.nsamp, stt, d_sll,
-                                                              d_nslot, d_snum, d_sden);
+            k_step_sum<<<int((nt + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, gw, gl, soff, gr.nsamp, stt,
+                                                              B->b_step_l, B->b_nslot, B->b_step_t, d_sden);
         }
+        trace("baselines");
     }
-    CK(cudaEventRecord(ev1, s));
-    trace("baselines");
-
-    // 7. results to host and CSR assembly (registry order = mpos order)
-    std::vector<int64_t> b_gstart(NB + 1), b_slo(NB), b_shi(NB), b_w(NB), m_bstart(NM + 1), m_pos(NM), h_l_g(G);
-    std::vector<int32_t> h_gmicro(G), h_gpart(G);
-    CK(cudaMemcpyAsync(b_gstart.data(), d_bgs, (NB + 1) * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(b_slo.data(), d_bslo, NB * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(b_shi.data(), d_bshi, NB * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(b_w.data(), d_bw, NB * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(m_bstart.data(), d_mbs, (NM + 1) * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(m_pos.data(), d_mpos, NM * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_l_g.data(), gl, G * 8, cudaMemcpyDeviceToHost, s));
-    std::vector<double> h_coeff(NB * 4), h_r2(NB), h_mape(NB), h_theta(NM * 4);
-    std::vector<int32_t> h_degen(NB), h_mflags(NM), h_next(NM), h_em(G);
-    std::vector<int64_t> h_el(G);
-    CK(cudaMemcpyAsync(h_coeff.data(), bk.coeff, NB * 32, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_r2.data(), bk.r2, NB * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_mape.data(), bk.mape, NB * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_degen.data(), bk.degen, NB * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_theta.data(), mc.theta, NM * 32, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_mflags.data(), mc.flags, NM * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_next.data(), mc.next, NM * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_el.data(), mc.el, G * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_em.data(), mc.em, G * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_gmicro.data(), gr.micro, G * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_gpart.data(), gr.partial, G * 4, cudaMemcpyDeviceToHost, s));
-    std::vector<double> h_lth(NM * 4), h_lr2(NM), h_lmape(NM), h_snum(G);
-    std::vector<int32_t> h_ldeg(NM), h_nslot(NM);
-    std::vector<int64_t> h_sll(G);
-    CK(cudaMemcpyAsync(h_lth.data(), lin.coeff, NM * 32, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_lr2.data(), lin.r2, NM * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_lmape.data(), lin.mape, NM * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_ldeg.data(), lin.degen, NM * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_nslot.data(), d_nslot, NM * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_sll.data(), d_sll, G * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_snum.data(), d_snum, G * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, ev0, ev1);
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
     CK(cudaGetLastError());
+    B->NM = int32_t(NM);
+    B->NB = NB;
+    B->G = G;
+    B->W = W;
+    B->p = p;
+    B->baselines = baselines;
+    CK(cudaEventRecord(B->done, s));
+    return WT_OK;
+}
 
-    auto* B = new wt_build;
-    B->coeff_off.push_back(0);
-    B->awave_off.push_back(0);
-    B->awave_aoff.push_back(0);
-    B->ext_aoff.push_back(0);
+void build_release(wt_build* b) {
+    if (b->done) cudaEventSynchronize(b->done);
+    for (void* q : b->mem) cudaFreeAsync(q, nullptr);
+    if (!b->mem.empty()) cudaStreamSynchronize(nullptr);
+    b->mem.clear();
+    for (cudaEvent_t* e : {&b->ev0, &b->ev1, &b->done})
+        if (*e) {
+            cudaEventDestroy(*e);
+            *e = nullptr;
+        }
+}
+
+// Host copies of the device tables, assembled into the CSR layout of
+// wt_build_result (registry order).
+wt_status build_download(wt_build* B) {
+    if (B->host_ready) return WT_OK;
+    CK(cudaEventSynchronize(B->done));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, B->ev0, B->ev1));
+    B->device_ms = ms;
+    const int64_t NM = B->NM, NB = B->NB, G = B->G;
+    std::vector<int32_t> coeff_off(NM + 1), coeff_w(NB), aoff(NB + 1), ext_off(NM), ext_cnt(NM), gmicro(G), gpart(G),
+        nsamp(NB), dflags(NB), eflags(NM), ldeg, nslot;
+    std::vector<double> theta_ext(NM * 4), coeff(NB * 4), r2(NB), mape(NB), lth, lr2, lmape, stept;
+    std::vector<int64_t> gl(G), el(G), stepl;
+    auto get = [](void* dst, const void* src, size_t n) { return cudaMemcpy(dst, src, n, cudaMemcpyDeviceToHost); };
+    CK(get(coeff_off.data(), B->t_coeff_off, (NM + 1) * 4));
+    CK(get(coeff_w.data(), B->t_coeff_w, NB * 4));
+    CK(get(aoff.data(), B->t_awave_aoff, (NB + 1) * 4));
+    CK(get(ext_off.data(), B->t_ext_off, NM * 4));
+    CK(get(ext_cnt.data(), B->t_ext_cnt, NM * 4));
+    CK(get(gmicro.data(), B->t_anchor_micro, G * 4));
+    CK(get(gpart.data(), B->d_partial, G * 4));
+    CK(get(nsamp.data(), B->d_nsamp, NB * 4));
+    CK(get(dflags.data(), B->d_dflags, NB * 4));
+    CK(get(eflags.data(), B->d_ext_flags, NM * 4));
+    CK(get(theta_ext.data(), B->t_theta_ext, NM * 32));
+    CK(get(coeff.data(), B->t_coeff_theta, NB * 32));
+    CK(get(r2.data(), B->d_r2, NB * 8));
+    CK(get(mape.data(), B->d_mape, NB * 8));
+    CK(get(gl.data(), B->t_anchor_l, G * 8));
+    std::vector<int32_t> em(G);
+    CK(get(el.data(), B->t_ext_l, G * 8));
+    CK(get(em.data(), B->t_ext_micro, G * 4));
+    if (B->baselines) {
+        ldeg.resize(NM);
+        nslot.resize(NM);
+        lth.resize(NM * 4);
+        lr2.resize(NM);
+        lmape.resize(NM);
+        stept.resize(G);
+        stepl.resize(G);
+        CK(get(ldeg.data(), B->b_lin_deg, NM * 4));
+        CK(get(nslot.data(), B->b_nslot, NM * 4));
+        CK(get(lth.data(), B->b_lin, NM * 32));
+        CK(get(lr2.data(), B->b_lin_r2, NM * 8));
+        CK(get(lmape.data(), B->b_lin_mape, NM * 8));
+        CK(get(stept.data(), B->b_step_t, G * 8));
+        CK(get(stepl.data(), B->b_step_l, G * 8));
+    }
+    B->coeff_off.assign(1, 0);
+    B->awave_off.assign(1, 0);
+    B->awave_aoff.assign(1, 0);
+    B->ext_aoff.assign(1, 0);
+    B->step_off.assign(1, 0);
     for (int64_t mq = 0; mq < NM; ++mq) {
-        B->macro_id.push_back(registry_ids[m_pos[mq]]);
-        for (int c = 0; c < 4; ++c) B->theta_ext.push_back(h_theta[4 * mq + c]);
-        B->ext_flags.push_back(h_mflags[mq]);
-        for (int64_t k = m_bstart[mq]; k < m_bstart[mq + 1]; ++k) {
-            B->coeff_w.push_back(int32_t(b_w[k]));
-            for (int c = 0; c < 4; ++c) B->coeff_theta.push_back(h_coeff[4 * k + c]);
-            B->diag_r2.push_back(h_r2[k]);
-            B->diag_mape.push_back(h_mape[k]);
-            const int32_t ns = int32_t(b_shi[k] - b_slo[k]);
-            B->diag_samples.push_back(ns);
-            B->diag_flags.push_back((h_degen[k] ? 1 : 0) | (ns < 4 ? 2 : 0));
-            B->awave_w.push_back(int32_t(b_w[k]));
-            for (int64_t q = b_gstart[k]; q < b_gstart[k + 1]; ++q) {
-                B->anchor_l.push_back(h_l_g[q]);
-                B->anchor_micro.push_back(h_gmicro[q]);
-                B->anchor_partial.push_back(h_gpart[q]);
+        B->macro_id.push_back(B->h_macro_id[mq]);
+        for (int c = 0; c < 4; ++c) B->theta_ext.push_back(theta_ext[4 * mq + c]);
+        B->ext_flags.push_back(eflags[mq]);
+        for (int64_t k = coeff_off[mq]; k < coeff_off[mq + 1]; ++k) {
+            B->coeff_w.push_back(coeff_w[k]);
+            for (int c = 0; c < 4; ++c) B->coeff_theta.push_back(coeff[4 * k + c]);
+            B->diag_r2.push_back(r2[k]);
+            B->diag_mape.push_back(mape[k]);
+            B->diag_samples.push_back(nsamp[k]);
+            B->diag_flags.push_back(dflags[k]);
+            B->awave_w.push_back(coeff_w[k]);
+            for (int64_t q = aoff[k]; q < aoff[k + 1]; ++q) {
+                B->anchor_l.push_back(gl[q]);
+                B->anchor_micro.push_back(gmicro[q]);
+                B->anchor_partial.push_back(gpart[q]);
             }
             B->awave_aoff.push_back(int32_t(B->anchor_l.size()));
         }
         B->coeff_off.push_back(int32_t(B->coeff_w.size()));
         B->awave_off.push_back(int32_t(B->awave_w.size()));
-        const int64_t gs = b_gstart[m_bstart[mq]];
-        for (int q = 0; q < h_next[mq]; ++q) {
-            B->ext_l.push_back(h_el[gs + q]);
-            B->ext_micro.push_back(h_em[gs + q]);
+        for (int q = 0; q < ext_cnt[mq]; ++q) {
+            B->ext_l.push_back(el[ext_off[mq] + q]);
+            B->ext_micro.push_back(em[ext_off[mq] + q]);
         }
         B->ext_aoff.push_back(int32_t(B->ext_l.size()));
-        B->step_off.push_back(int32_t(B->step_l.size()));
-        for (int q = 0; q < h_nslot[mq]; ++q) {
-            B->step_l.push_back(h_sll[gs + q]);
-            B->step_t.push_back(h_snum[gs + q]);
+        if (B->baselines) {
+            const int64_t gs = ext_off[mq];  // step slots live at the macro's first group too
+            for (int q = 0; q < nslot[mq]; ++q) {
+                B->step_l.push_back(stepl[gs + q]);
+                B->step_t.push_back(stept[gs + q]);
+            }
+            B->step_off.push_back(int32_t(B->step_l.size()));
+            for (int c = 0; c < 4; ++c) B->lin_theta.push_back(lth[4 * mq + c]);
+            B->lin_r2.push_back(lr2[mq]);
+            B->lin_mape.push_back(lmape[mq]);
+            B->lin_degen.push_back(ldeg[mq]);
         }
-        for (int c = 0; c < 4; ++c) B->lin_theta.push_back(h_lth[4 * mq + c]);
-        B->lin_r2.push_back(h_lr2[mq]);
-        B->lin_mape.push_back(h_lmape[mq]);
-        B->lin_degen.push_back(h_ldeg[mq]);
     }
-    B->step_off.push_back(int32_t(B->step_l.size()));
+    B->host_ready = true;
+    return WT_OK;
+}
+
+void fill_result(const wt_build* B, wt_build_result* result) {
     wt_build_result& R = *result;
-    R.n_tables = int32_t(NM);
-    R.W = W;
-    R.p = p;
+    R = wt_build_result{};
+    R.n_tables = B->NM;
+    R.W = B->W;
+    R.p = B->p;
     R.macro_id = B->macro_id.data();
     R.theta_ext = B->theta_ext.data();
     R.ext_flags = B->ext_flags.data();
@@ -1289,19 +1416,159 @@ wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_i
     R.ext_aoff = B->ext_aoff.data();
     R.ext_l = B->ext_l.data();
     R.ext_micro = B->ext_micro.data();
-    R.device_ms = ms;
-    R.step_off = B->step_off.data();
-    R.step_l = B->step_l.data();
-    R.step_t = B->step_t.data();
-    R.lin_theta = B->lin_theta.data();
-    R.lin_r2 = B->lin_r2.data();
-    R.lin_mape = B->lin_mape.data();
-    R.lin_degenerate = B->lin_degen.data();
+    R.device_ms = B->device_ms;
+    if (B->baselines) {
+        R.step_off = B->step_off.data();
+        R.step_l = B->step_l.data();
+        R.step_t = B->step_t.data();
+        R.lin_theta = B->lin_theta.data();
+        R.lin_r2 = B->lin_r2.data();
+        R.lin_mape = B->lin_mape.data();
+        R.lin_degenerate = B->lin_degen.data();
+    }
+}
+
+struct DevRestore {
+    int d;
+    ~DevRestore() { cudaSetDevice(d); }
+};
+
+}  // namespace
+
+// For wt_capi.cu: the device CSR of a build (engine creation without a
+// host round trip).
+namespace wtb {
+wt_status build_device_tables(const wt_build* b, BuildTables* out) {
+    if (!b || !out) return WT_INVALID_ARGUMENT;
+    out->device = b->device;
+    out->n_tables = b->NM;
+    out->macro_id_host = b->h_macro_id.data();
+    out->W = b->W;
+    out->tv = TabView{b->t_W, b->t_theta_ext, b->t_coeff_off, b->t_coeff_w, b->t_coeff_theta, b->t_coeff_off,
+                      b->t_coeff_w, b->t_awave_aoff, b->t_ext_off, b->G, b->t_ext_cnt};
+    out->anchor_l = b->t_anchor_l;
+    out->anchor_micro = b->t_anchor_micro;
+    out->n_anchor = b->G;
+    out->ext_l = b->t_ext_l;
+    out->ext_micro = b->t_ext_micro;
+    out->n_ext = b->G;
+    return WT_OK;
+}
+}  // namespace wtb
+
+extern "C" {
+
+wt_status wt_fit_build(const wt_records_desc* records, const int32_t* registry_ids, int32_t n_macros,
+                       int32_t W, int32_t p, int device, wt_build** out, wt_build_result* result) {
+    if (!records || !out || !result || (n_macros > 0 && !registry_ids)) {
+        g_fit_err = "null argument";
+        return WT_INVALID_ARGUMENT;
+    }
+    *out = nullptr;
+    const int64_t n_all = records->n;
+    if (n_all <= 0) {
+        g_fit_err = "build_dual_table: empty record set";
+        return WT_INVALID_ARGUMENT;
+    }
+    int prev_dev = 0;
+    cudaGetDevice(&prev_dev);
+    cudaSetDevice(device);
+    DevRestore restore{prev_dev};
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct SD {
+        cudaStream_t s;
+        ~SD() { cudaStreamDestroy(s); }
+    } sd{s};
+    // upload the host records (one block from the pool; released stream-ordered)
+    Arena ar;
+    const size_t o_g = ar.take(n_all * 8), o_l = ar.take(n_all * 8), o_w = ar.take(n_all * 4),
+                 o_ma = ar.take(n_all * 4), o_mi = ar.take(n_all * 4), o_t = ar.take(n_all * 8);
+    void* blk = nullptr;
+    CK(cudaMallocFromPoolAsync(&blk, ar.used, wtb::device_pool(device), s));
+    char* b = static_cast<char*>(blk);
+    CK(cudaMemcpyAsync(b + o_g, records->g, n_all * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b + o_l, records->l, n_all * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b + o_w, records->w, n_all * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b + o_ma, records->macro_id, n_all * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b + o_mi, records->micro_id, n_all * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b + o_t, records->latency_us, n_all * 8, cudaMemcpyHostToDevice, s));
+    Rec rc{reinterpret_cast<const int64_t*>(b + o_g), reinterpret_cast<const int64_t*>(b + o_l),
+           reinterpret_cast<const int32_t*>(b + o_w), reinterpret_cast<const int32_t*>(b + o_ma),
+           reinterpret_cast<const int32_t*>(b + o_mi), reinterpret_cast<const double*>(b + o_t)};
+    auto* B = new wt_build;
+    B->device = device;
+    const wt_status st = fit_core(rc, n_all, registry_ids, n_macros, W, p, true, device, s, B);
+    cudaFreeAsync(blk, s);
+    cudaStreamSynchronize(s);
+    if (st != WT_OK) {
+        build_release(B);
+        delete B;
+        return st;
+    }
+    const wt_status st2 = build_download(B);
+    if (st2 != WT_OK) {
+        build_release(B);
+        delete B;
+        return st2;
+    }
+    fill_result(B, result);
     *out = B;
     return WT_OK;
 }
 
+wt_status wt_fit_build_device(const wt_records_desc* records, const int32_t* registry_ids, int32_t n_macros,
+                              int32_t W, int32_t p, int32_t flags, int device, void* stream, wt_build** out) {
+    if (!records || !out || (n_macros > 0 && !registry_ids)) {
+        g_fit_err = "null argument";
+        return WT_INVALID_ARGUMENT;
+    }
+    *out = nullptr;
+    if (records->n <= 0) {
+        g_fit_err = "build_dual_table: empty record set";
+        return WT_INVALID_ARGUMENT;
+    }
+    int prev_dev = 0;
+    cudaGetDevice(&prev_dev);
+    cudaSetDevice(device);
+    DevRestore restore{prev_dev};
+    Rec rc{records->g, records->l, records->w, records->macro_id, records->micro_id, records->latency_us};
+    auto* B = new wt_build;
+    B->device = device;
+    const wt_status st = fit_core(rc, records->n, registry_ids, n_macros, W, p, (flags & WT_FIT_BASELINES) != 0,
+                                  device, static_cast<cudaStream_t>(stream), B);
+    if (st != WT_OK) {
+        cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+        build_release(B);
+        delete B;
+        return st;
+    }
+    *out = B;
+    return WT_OK;
+}
+
+wt_status wt_build_result_get(wt_build* b, wt_build_result* result) {
+    if (!b || !result) {
+        g_fit_err = "null argument";
+        return WT_INVALID_ARGUMENT;
+    }
+    int prev_dev = 0;
+    cudaGetDevice(&prev_dev);
+    cudaSetDevice(b->device);
+    DevRestore restore{prev_dev};
+    const wt_status st = build_download(b);
+    if (st != WT_OK) return st;
+    fill_result(b, result);
+    return WT_OK;
+}
+
 wt_status wt_build_free(wt_build* b) {
+    if (!b) return WT_OK;
+    int prev_dev = 0;
+    cudaGetDevice(&prev_dev);
+    cudaSetDevice(b->device);
+    DevRestore restore{prev_dev};
+    build_release(b);
     delete b;
     return WT_OK;
 }

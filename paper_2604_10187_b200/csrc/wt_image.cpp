@@ -149,7 +149,7 @@ wt_status prune_plan_host(const wt_tables_desc& T, const wt_registry_desc& reg, 
     const ImagePlan& P = *plan;
     const int32_t C = P.C, R = P.R;
     const TabView tv{T.W, T.theta_ext, T.coeff_off, T.coeff_w, T.coeff_theta, T.awave_off, T.awave_w, T.awave_aoff,
-                     T.ext_aoff, 0};
+                     T.ext_aoff, 0, nullptr};
     // rows in class order
     std::vector<double> th2(size_t(C) * R * 4, 0.0);
     std::vector<uint32_t> m2(size_t(C) * R, 0);

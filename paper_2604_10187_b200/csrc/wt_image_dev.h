@@ -38,6 +38,23 @@ struct ImgPruneArgs {
     uint32_t* segor;
 };
 
+// Device-resident tables of a K2 build (wt_fit.cu), for engine creation
+// without a host round trip.
+struct BuildTables {
+    int device;
+    int32_t n_tables;
+    const int32_t* macro_id_host;  // [n_tables] registry order
+    int32_t W;                     // every table's W
+    TabView tv;                    // device pointers
+    const int64_t* anchor_l;
+    const int32_t* anchor_micro;
+    int64_t n_anchor;
+    const int64_t* ext_l;
+    const int32_t* ext_micro;
+    int64_t n_ext;
+};
+wt_status build_device_tables(const wt_build* b, BuildTables* out);
+
 cudaError_t launch_image_build(const TabView& T, const ImgRowsArgs& rows, const ImgPruneArgs& prune,
                                cudaStream_t st);
 

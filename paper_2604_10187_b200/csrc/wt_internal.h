@@ -117,6 +117,16 @@ wt_status plan_image(const int32_t* macro_id, const int32_t* W, int32_t n, const
 wt_status prune_plan_host(const wt_tables_desc& t, const wt_registry_desc& r, const wt_hw& hw, ImagePlan* plan,
                           std::vector<uint32_t>* segmask, std::string* err);
 
+// One device allocation carved into 256-byte aligned pieces.
+struct Arena {
+    size_t used = 0;
+    size_t take(size_t bytes) {
+        size_t off = used;
+        used += (bytes + 255) & ~size_t(255);
+        return off;
+    }
+};
+
 // Thread-local message returned by wt_last_error().
 void set_last_error(const std::string& msg);
 

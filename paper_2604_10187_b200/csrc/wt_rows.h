@@ -22,7 +22,9 @@ namespace wtb {
 // std::vector<DualTable> as key-ascending CSR (wt_tables_desc), host or
 // device pointers.  Anchor pool = anchor_l[0 .. n_anchor) followed by
 // ext_l[0 .. n_ext): a wave map i sits at awave_aoff[i], table t's
-// extrapolation anchors at ext_base + ext_aoff[t].
+// extrapolation anchors at ext_base + ext_aoff[t].  ext_cnt == null: CSR
+// (count = ext_aoff[t+1] - ext_aoff[t]); else count = ext_cnt[t] (the fit's
+// uncompacted per-macro slices).
 struct TabView {
     const int32_t* W;
     const double* theta_ext;
@@ -34,6 +36,7 @@ struct TabView {
     const int32_t* awave_aoff;
     const int32_t* ext_aoff;
     int64_t ext_base;
+    const int32_t* ext_cnt;
 };
 
 struct RowOut {
@@ -89,7 +92,7 @@ WT_HD void resolve_row(const TabView& T, int32_t t, int32_t r, int32_t R, RowOut
     bool have = false;
     const int32_t aw0 = T.awave_off[t], aw1 = T.awave_off[t + 1];
     if (extrap) {
-        const int32_t e0 = T.ext_aoff[t], e1 = T.ext_aoff[t + 1];
+        const int32_t e0 = T.ext_aoff[t], e1 = T.ext_cnt ? e0 + T.ext_cnt[t] : T.ext_aoff[t + 1];
         if (e1 > e0) {
             off = int32_t(T.ext_base + e0);
             cnt = e1 - e0;
