@@ -20,11 +20,11 @@
  * association order, so bitwise parity with a real Eigen build is UNPINNED
  * (pinned only to 1e-9 by the reference's golden fits, test_model.cpp:23-61,
  * acceptance.cpp:313-323).  This restatement fixes ONE order that the GPU fit
- * kernel reproduces exactly: a sum over rows r in [r0, n) accumulates 32
- * partials p[r mod 32] in ascending r (each starting from +0.0), then folds
- * them with a xor-butterfly (16, 8, 4, 2, 1): p[j] <- p[j] + p[j^off].
- * That is precisely what a warp computes with lane-strided accumulation and
- * __shfl_xor_sync, so CPU and GPU agree bit for bit.
+ * kernel reproduces exactly: every sum over rows r in [r0, n) is a plain
+ * ascending accumulation starting from +0.0 (products rounded first).  That
+ * is what one lane computes when it owns a column of the least-squares
+ * problem (the GPU fit gives each problem 4 lanes, one per design column),
+ * so CPU and GPU agree bit for bit.
  * All arithmetic is IEEE binary64 with no contraction (-ffp-contract=off).
  */
 #ifndef WT_FIT_CORE_H
@@ -35,19 +35,11 @@
 #include <stdlib.h>
 #include <string.h>
 
-#define WTF_LANES 32
-
-/* Sum of v[r] for r in [r0, n) in the lane-strided + butterfly order. */
+/* Sum of v[r] for r in [r0, n), ascending. */
 static inline double wtf_sum(const double* v, int r0, int n) {
-    double p[WTF_LANES];
-    for (int j = 0; j < WTF_LANES; ++j) p[j] = 0.0;
-    for (int r = r0; r < n; ++r) p[r & (WTF_LANES - 1)] = p[r & (WTF_LANES - 1)] + v[r];
-    for (int off = WTF_LANES / 2; off >= 1; off >>= 1) {
-        double q[WTF_LANES];
-        for (int j = 0; j < WTF_LANES; ++j) q[j] = p[j] + p[j ^ off];
-        memcpy(p, q, sizeof p);
-    }
-    return p[0];
+    double p = 0.0;
+    for (int r = r0; r < n; ++r) p = p + v[r];
+    return p;
 }
 
 /* dot(a[r0..n), b[r0..n)) with products rounded first. */

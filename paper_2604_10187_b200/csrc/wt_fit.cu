@@ -14,12 +14,15 @@
 //   4. k_samples    selected (g, l, t) samples laid out group after group, so
 //                   every (macro, w) bucket and every extrapolation window is
 //                   one contiguous slice in (w asc, l asc, g asc) order
-//   5. k_fit        warp / bucket: column-scaled ColPivHouseholderQR +
-//                   reduced HouseholderQR, R^2, MAPE (model.cpp:20-77)
-//   6. k_extrap     warp / macro: fit_extrapolation (model.cpp:140-192)
+//   5. k_qfit       4 lanes / bucket (8 buckets per warp): column-scaled
+//                   ColPivHouseholderQR + reduced HouseholderQR, R^2, MAPE
+//                   (model.cpp:20-77), each design column owned by one lane
+//   6. k_ext_prep / k_qfit / k_ext_vote: fit_extrapolation
+//                   (model.cpp:140-192), the pooled window fit on the same
+//                   quad-lane solver
 // The QR reproduces oracle/wt_fit_core.h's operation order exactly: every
-// reduction is lane-strided accumulation (lane j owns rows j, j+32, ...) then
-// a xor-butterfly, all binary64 _rn arithmetic, correctly rounded sqrt/div.
+// reduction is one lane's ascending accumulation, all binary64 _rn
+// arithmetic, correctly rounded sqrt/div.
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
@@ -44,80 +47,74 @@ namespace fit {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-// ------------------------------------------------------------ warp algebra
-__device__ __forceinline__ double butterfly(double p) {
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) p = __dadd_rn(p, __shfl_xor_sync(FULL, p, off));
-    return p;
+// --------------------------------------------------- quad-lane least squares
+// fit_bucket (model.cpp:20-77) with 4 lanes per problem, 8 problems per warp.
+// Lane q of a quad owns one design column at a time (column pivoting only
+// re-maps logical columns to owning lanes, no data moves), so every dot
+// product / norm is ONE lane's plain ascending accumulation -- the order of
+// oracle/wt_fit_core.h, hence bit-identical results.  The owner of the
+// pivot column builds the Householder reflector, then -- while the other
+// owners apply it to their columns -- applies it to the right-hand side.
+// Storage: element (row r, slot s) of the problem's 4 column slots at
+// A[r * la + s], its right-hand side at rhs[r * lr]; shared memory (la = 32
+// across the warp's 8 problems) when n <= rows, else the problem's own
+// global scratch (5 doubles per sample, la = 4).
+constexpr double kEps = DBL_EPSILON;
+
+__device__ __forceinline__ double qb(double v, int src, unsigned m) { return __shfl_sync(m, v, src, 4); }
+__device__ __forceinline__ int qbi(int v, int src, unsigned m) { return __shfl_sync(m, v, src, 4); }
+
+// design column c of sample r (model.cpp:24-32): g*l, g, l, 1
+__device__ __forceinline__ double dcol(const double* g, const double* l, int c, int r) {
+    return c == 0 ? __dmul_rn(g[r], l[r]) : c == 1 ? g[r] : c == 2 ? l[r] : 1.0;
 }
 
-// sum over rows [r0, n) of a[r]*b[r] (b == nullptr: of a[r])
-__device__ __forceinline__ double wdot(const double* a, const double* b, int r0, int n, int lane) {
-    double p = 0.0;
-    for (int r = r0 + ((lane - r0) & 31); r < n; r += 32) p = __dadd_rn(p, b ? __dmul_rn(a[r], b[r]) : a[r]);
-    return butterfly(p);
-}
-
-__device__ __forceinline__ double wmaxabs(const double* a, int n, int lane) {
-    double m = -1.0;
-    for (int r = lane; r < n; r += 32) m = fmax(m, fabs(a[r]));
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, off));
-    return m;
-}
-
-// Householder reflector on col[k..n) (makeHouseholderInPlace).
-__device__ double whouse(double* col, int k, int n, double* beta, int lane) {
-    const double c0 = col[k];
-    const double tailsq = (n - k == 1) ? 0.0 : wdot(col, col, k + 1, n, lane);
-    __syncwarp();
+// Householder reflector on rows [k, n) of column `col` (stride la):
+// makeHouseholderInPlace (wtf_house).  Returns tau; *beta = new diagonal.
+__device__ double q_house(double* col, int la, int k, int n, double* beta) {
+    const double c0 = col[k * la];
+    double tailsq = 0.0;
+    if (n - k != 1)
+        for (int r = k + 1; r < n; ++r) tailsq = __dadd_rn(tailsq, __dmul_rn(col[r * la], col[r * la]));
     if (tailsq <= DBL_MIN) {
         *beta = c0;
-        for (int r = k + 1 + lane; r < n; r += 32) col[r] = 0.0;
-        __syncwarp();
+        for (int r = k + 1; r < n; ++r) col[r * la] = 0.0;
         return 0.0;
     }
     double b = __dsqrt_rn(__dadd_rn(__dmul_rn(c0, c0), tailsq));
     if (c0 >= 0.0) b = -b;
     const double d = __dadd_rn(c0, -b);
-    for (int r = k + 1 + lane; r < n; r += 32) col[r] = __ddiv_rn(col[r], d);
-    __syncwarp();
+    for (int r = k + 1; r < n; ++r) col[r * la] = __ddiv_rn(col[r * la], d);
     *beta = b;
     return __ddiv_rn(__dadd_rn(b, -c0), b);
 }
 
-// y[k..n) -= tau * v * (v . y[k..n)), v = [1; ess[k+1..n)] (applyHouseholderOnTheLeft)
-__device__ void wapply(const double* ess, double tau, double* y, int k, int n, int lane) {
+// y[k..n) -= tau v (v . y), v = [1; ess[k+1..n)] (wtf_apply)
+__device__ void q_apply(const double* ess, int le, double tau, double* y, int ly, int k, int n) {
     if (n - k == 1) {
-        __syncwarp();
-        if (lane == 0) y[k] = __dmul_rn(y[k], __dadd_rn(1.0, -tau));
-        __syncwarp();
+        y[k * ly] = __dmul_rn(y[k * ly], __dadd_rn(1.0, -tau));
         return;
     }
     if (tau == 0.0) return;
-    double tmp = wdot(ess, y, k + 1, n, lane);
-    tmp = __dadd_rn(tmp, y[k]);
-    __syncwarp();
-    if (lane == 0) y[k] = __dadd_rn(y[k], -__dmul_rn(tau, tmp));
-    for (int r = k + 1 + lane; r < n; r += 32) y[r] = __dadd_rn(y[r], -__dmul_rn(__dmul_rn(tau, ess[r]), tmp));
-    __syncwarp();
+    double tmp = 0.0;
+    for (int r = k + 1; r < n; ++r) tmp = __dadd_rn(tmp, __dmul_rn(ess[r * le], y[r * ly]));
+    tmp = __dadd_rn(tmp, y[k * ly]);
+    y[k * ly] = __dadd_rn(y[k * ly], -__dmul_rn(tau, tmp));
+    for (int r = k + 1; r < n; ++r) y[r * ly] = __dadd_rn(y[r * ly], -__dmul_rn(__dmul_rn(tau, ess[r * le]), tmp));
 }
 
-// upper back-substitution on c[0..m) (single-panel triangular_solve_vector)
-__device__ void wbacksolve(const double* A, int n, int m, double* c, int lane) {
-    __syncwarp();
-    if (lane == 0) {
-        for (int i = m - 1; i >= 0; --i) {
-            if (c[i] != 0.0) {
-                c[i] = __ddiv_rn(c[i], A[size_t(i) * n + i]);
-                for (int j = 0; j < i; ++j) c[j] = __dadd_rn(c[j], -__dmul_rn(c[i], A[size_t(i) * n + j]));
-            }
+// upper back-substitution on rhs[0..m) with R column i at A + slot[i]
+// (wtf_backsolve); one lane
+__device__ void q_backsolve(const double* A, int la, const int* slot, int m, double* rhs, int lr) {
+    for (int i = m - 1; i >= 0; --i) {
+        double ci = rhs[i * lr];
+        if (ci != 0.0) {
+            ci = __ddiv_rn(ci, A[i * la + slot[i]]);
+            rhs[i * lr] = ci;
+            for (int j = 0; j < i; ++j) rhs[j * lr] = __dadd_rn(rhs[j * lr], -__dmul_rn(ci, A[j * la + slot[i]]));
         }
     }
-    __syncwarp();
 }
-
-constexpr int kFitScr = 19;  // scratch doubles per sample (warp_fit)
 
 struct FitOut {
     double c[4];
@@ -125,51 +122,42 @@ struct FitOut {
     int degenerate;
 };
 
-// fit_bucket on samples (g, l, t)[0..n) with scratch of 18*n doubles.
-__device__ FitOut warp_fit(const double* g, const double* l, const double* t, int n, double* scr, int lane) {
-    double* D = scr;            // design, 4 columns
-    double* Sc = D + 4 * size_t(n);   // scaled design (kept for the reduced fit)
-    double* A = Sc + 4 * size_t(n);   // QR workspace
-    double* Sub = A + 4 * size_t(n);  // reduced-fit columns
-    double* Wk = Sub + 4 * size_t(n);
-    double* F = Wk + size_t(n);
-    double* T = F + size_t(n);  // the latencies, read once from global memory
-    for (int r = lane; r < n; r += 32) {
-        T[r] = t[r];
-        D[r] = __dmul_rn(g[r], l[r]);
-        D[n + r] = g[r];
-        D[2 * size_t(n) + r] = l[r];
-        D[3 * size_t(n) + r] = 1.0;
+// One problem per quad: q = lane within the quad, m = the quad's mask.
+__device__ FitOut quad_fit(const double* g, const double* l, const double* t, int n, double* A, int la, double* rhs,
+                           int lr, int q, unsigned m) {
+    // 1. scaled design (model.cpp:36-41), right-hand side = t
+    double mxa = fabs(dcol(g, l, q, 0));
+    for (int r = 1; r < n; ++r) {
+        const double v = fabs(dcol(g, l, q, r));
+        if (v > mxa) mxa = v;
     }
-    __syncwarp();
-    double scale[4];
+    const double sc = mxa > 0 ? mxa : 1.0;
+    double nrm = 0.0;
+    for (int r = 0; r < n; ++r) {
+        const double v = __ddiv_rn(dcol(g, l, q, r), sc);
+        A[r * la + q] = v;
+        nrm = __dadd_rn(nrm, __dmul_rn(v, v));
+    }
+    if (q == 0)
+        for (int r = 0; r < n; ++r) rhs[r * lr] = t[r];
+    double scale[4], upd[4], direct[4];
+    const double dn = __dsqrt_rn(nrm);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-        const double m = wmaxabs(D + size_t(c) * n, n, lane);
-        scale[c] = (m > 0) ? m : 1.0;
-        for (int r = lane; r < n; r += 32) {
-            const double v = __ddiv_rn(D[size_t(c) * n + r], scale[c]);
-            Sc[size_t(c) * n + r] = v;
-            A[size_t(c) * n + r] = v;
-        }
+        scale[c] = qb(sc, c, m);
+        direct[c] = upd[c] = qb(dn, c, m);
     }
-    __syncwarp();
-    // ---- ColPivHouseholderQR
-    const int size = n < 4 ? n : 4;
-    double upd[4], direct[4], tau[4];
-    int trans[4], perm[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        direct[c] = __dsqrt_rn(wdot(A + size_t(c) * n, A + size_t(c) * n, 0, n, lane));
-        upd[c] = direct[c];
-    }
+    __syncwarp(m);
+    // 2. ColPivHouseholderQR (model.cpp:43-45): own[c] = slot of logical column c
+    int own[4] = {0, 1, 2, 3};
     double mx = upd[0];
 #pragma unroll
     for (int c = 1; c < 4; ++c)
         if (upd[c] > mx) mx = upd[c];
-    const double th_help = __ddiv_rn(__dmul_rn(__dmul_rn(mx, DBL_EPSILON), __dmul_rn(mx, DBL_EPSILON)), double(n));
-    const double downdate_th = __dsqrt_rn(DBL_EPSILON);
-    int nz = size;
+    const double th_help = __ddiv_rn(__dmul_rn(__dmul_rn(mx, kEps), __dmul_rn(mx, kEps)), double(n));
+    const double downdate_th = __dsqrt_rn(kEps);
+    const int size = n < 4 ? n : 4;
+    int nz = size, trans[4] = {0, 1, 2, 3};
     double maxpiv = 0.0;
     for (int k = 0; k < size; ++k) {
         int big = k;
@@ -179,18 +167,12 @@ __device__ FitOut warp_fit(const double* g, const double* l, const double* t, in
                 bigv = upd[c];
                 big = c;
             }
-        const double big_sq = __dmul_rn(bigv, bigv);
-        if (nz == size && big_sq < __dmul_rn(th_help, double(n - k))) nz = k;
+        if (nz == size && __dmul_rn(bigv, bigv) < __dmul_rn(th_help, double(n - k))) nz = k;
         trans[k] = big;
         if (big != k) {
-            double* ck = A + size_t(k) * n;
-            double* cb = A + size_t(big) * n;
-            for (int r = lane; r < n; r += 32) {
-                const double tv = ck[r];
-                ck[r] = cb[r];
-                cb[r] = tv;
-            }
-            __syncwarp();
+            int ti = own[k];
+            own[k] = own[big];
+            own[big] = ti;
             double tv = upd[k];
             upd[k] = upd[big];
             upd[big] = tv;
@@ -198,31 +180,46 @@ __device__ FitOut warp_fit(const double* g, const double* l, const double* t, in
             direct[k] = direct[big];
             direct[big] = tv;
         }
-        double* colk = A + size_t(k) * n;
-        double beta;
-        tau[k] = whouse(colk, k, n, &beta, lane);
-        if (lane == 0) colk[k] = beta;
-        __syncwarp();
-        if (fabs(beta) > maxpiv) maxpiv = fabs(beta);
-        for (int j = k + 1; j < 4; ++j) wapply(colk, tau[k], A + size_t(j) * n, k, n, lane);
-        for (int j = k + 1; j < 4; ++j) {
-            if (upd[j] != 0.0) {
-                double tq = __ddiv_rn(fabs(A[size_t(j) * n + k]), upd[j]);
-                tq = __dmul_rn(__dadd_rn(1.0, tq), __dadd_rn(1.0, -tq));
-                if (tq < 0.0) tq = 0.0;
-                const double ratio = __ddiv_rn(upd[j], direct[j]);
-                const double t2 = __dmul_rn(tq, __dmul_rn(ratio, ratio));
-                if (t2 <= downdate_th) {
-                    direct[j] = __dsqrt_rn(wdot(A + size_t(j) * n, A + size_t(j) * n, k + 1, n, lane));
-                    upd[j] = direct[j];
-                } else {
-                    upd[j] = __dmul_rn(upd[j], __dsqrt_rn(tq));
-                }
+        int lj = 0;  // logical column this lane owns
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (own[c] == q) lj = c;
+        double tk = 0.0, bk = 0.0;
+        if (lj == k) {
+            tk = q_house(A + q, la, k, n, &bk);
+            A[k * la + q] = bk;
+        }
+        tk = qb(tk, own[k], m);
+        bk = qb(bk, own[k], m);
+        if (fabs(bk) > maxpiv) maxpiv = fabs(bk);
+        __syncwarp(m);
+        if (lj > k)
+            q_apply(A + own[k], la, tk, A + q, la, k, n);
+        else if (lj == k)
+            q_apply(A + q, la, tk, rhs, lr, k, n);  // H_k on the right-hand side, in step
+        __syncwarp(m);
+        double nu = upd[lj], nd = direct[lj];
+        if (lj > k && nu != 0.0) {
+            double tq = __ddiv_rn(fabs(A[k * la + q]), nu);
+            tq = __dmul_rn(__dadd_rn(1.0, tq), __dadd_rn(1.0, -tq));
+            if (tq < 0.0) tq = 0.0;
+            const double ratio = __ddiv_rn(nu, nd);
+            const double t2 = __dmul_rn(tq, __dmul_rn(ratio, ratio));
+            if (t2 <= downdate_th) {
+                double s = 0.0;
+                for (int r = k + 1; r < n; ++r) s = __dadd_rn(s, __dmul_rn(A[r * la + q], A[r * la + q]));
+                nd = __dsqrt_rn(s);
+                nu = nd;
+            } else {
+                nu = __dmul_rn(nu, __dsqrt_rn(tq));
             }
         }
+        for (int j = k + 1; j < 4; ++j) {
+            upd[j] = qb(nu, own[j], m);
+            direct[j] = qb(nd, own[j], m);
+        }
     }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) perm[c] = c;
+    int perm[4] = {0, 1, 2, 3};
     for (int k = 0; k < size; ++k) {
         const int tv = perm[k];
         perm[k] = perm[trans[k]];
@@ -230,78 +227,76 @@ __device__ FitOut warp_fit(const double* g, const double* l, const double* t, in
     }
     const double pre = __dmul_rn(fabs(maxpiv), 1e-10);
     int rank = 0;
-    for (int i = 0; i < nz; ++i) rank += fabs(A[size_t(i) * n + i]) > pre;
+    for (int i = 0; i < nz; ++i) rank += fabs(A[i * la + own[i]]) > pre;
 
     FitOut o;
     double x[4] = {0.0, 0.0, 0.0, 0.0};
     o.degenerate = 0;
     if (rank >= 4 && n >= 4) {
-        for (int r = lane; r < n; r += 32) Wk[r] = T[r];
-        __syncwarp();
-        for (int k = 0; k < nz; ++k) wapply(A + size_t(k) * n, tau[k], Wk, k, n, lane);
-        wbacksolve(A, n, nz, Wk, lane);
-        for (int i = 0; i < nz; ++i) x[perm[i]] = Wk[i];
+        // the right-hand side already carries H_0..H_3 (nz = 4 here)
+        if (q == 0) {
+            q_backsolve(A, la, own, nz, rhs, lr);
+            for (int i = 0; i < nz; ++i) x[perm[i]] = rhs[i * lr];
+        }
     } else {
+        // reduced fit (model.cpp:51-59): unpivoted HouseholderQR of the first
+        // `keep` pivot columns of the scaled design
         o.degenerate = 1;
         int keep = rank < n ? rank : n;
         if (keep < 1) keep = 1;
-        for (int c = 0; c < keep; ++c)
-            for (int r = lane; r < n; r += 32) Sub[size_t(c) * n + r] = Sc[size_t(perm[c]) * n + r];
-        __syncwarp();
         const int hs = n < keep ? n : keep;
-        double ht[4];
+        __syncwarp(m);  // every lane is done reading the pivoted QR
+        if (q < keep)
+            for (int r = 0; r < n; ++r) A[r * la + q] = __ddiv_rn(dcol(g, l, perm[q], r), scale[perm[q]]);
+        if (q == 0)
+            for (int r = 0; r < n; ++r) rhs[r * lr] = t[r];
+        __syncwarp(m);
         for (int k = 0; k < hs; ++k) {
-            double* colk = Sub + size_t(k) * n;
-            double beta;
-            ht[k] = whouse(colk, k, n, &beta, lane);
-            if (lane == 0) colk[k] = beta;
-            __syncwarp();
-            for (int j = k + 1; j < keep; ++j) wapply(colk, ht[k], Sub + size_t(j) * n, k, n, lane);
+            double tk = 0.0, bk = 0.0;
+            if (q == k) {
+                tk = q_house(A + q, la, k, n, &bk);
+                A[k * la + q] = bk;
+            }
+            tk = qb(tk, k, m);
+            __syncwarp(m);
+            if (q > k && q < keep)
+                q_apply(A + k, la, tk, A + q, la, k, n);
+            else if (q == k)
+                q_apply(A + q, la, tk, rhs, lr, k, n);
+            __syncwarp(m);
         }
-        for (int r = lane; r < n; r += 32) Wk[r] = T[r];
-        __syncwarp();
-        for (int k = 0; k < hs; ++k) wapply(Sub + size_t(k) * n, ht[k], Wk, k, n, lane);
-        wbacksolve(Sub, n, hs, Wk, lane);
-        for (int c = 0; c < hs; ++c) x[perm[c]] = Wk[c];
+        if (q == 0) {
+            const int id[4] = {0, 1, 2, 3};
+            q_backsolve(A, la, id, hs, rhs, lr);
+            for (int c = 0; c < hs; ++c) x[perm[c]] = rhs[c * lr];
+        }
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        x[c] = __ddiv_rn(x[c], scale[c]);
-        o.c[c] = x[c];
+    for (int c = 0; c < 4; ++c) o.c[c] = __ddiv_rn(qb(x[c], 0, m), scale[c]);
+    // 3. diagnostics (model.cpp:64-75): lane 0 SS_res, lane 1 mean + SS_tot,
+    //    lane 2 MAPE -- each a sequential pass in sample order
+    double acc = 0.0;
+    if (q == 1) {
+        for (int r = 0; r < n; ++r) acc = __dadd_rn(acc, t[r]);
+        const double mean = __ddiv_rn(acc, double(n));
+        acc = 0.0;
+        for (int r = 0; r < n; ++r) {
+            const double d = __dadd_rn(t[r], -mean);
+            acc = __dadd_rn(acc, __dmul_rn(d, d));
+        }
+    } else if (q != 3) {
+        for (int r = 0; r < n; ++r) {
+            double f = __dmul_rn(__dmul_rn(g[r], l[r]), o.c[0]);
+            f = __dadd_rn(f, __dmul_rn(g[r], o.c[1]));
+            f = __dadd_rn(f, __dmul_rn(l[r], o.c[2]));
+            f = __dadd_rn(f, __dmul_rn(1.0, o.c[3]));
+            const double d = __dadd_rn(t[r], -f);
+            acc = q == 0 ? __dadd_rn(acc, __dmul_rn(d, d)) : __dadd_rn(acc, __ddiv_rn(fabs(d), fabs(t[r])));
+        }
     }
-    __syncwarp();  // every lane has read the solution out of Wk before it is reused below
-    // residuals (model.cpp:64-75)
-    for (int r = lane; r < n; r += 32) {
-        double acc = __dmul_rn(D[r], x[0]);
-        acc = __dadd_rn(acc, __dmul_rn(D[n + r], x[1]));
-        acc = __dadd_rn(acc, __dmul_rn(D[2 * size_t(n) + r], x[2]));
-        acc = __dadd_rn(acc, __dmul_rn(D[3 * size_t(n) + r], x[3]));
-        F[r] = acc;
-        const double d = __dadd_rn(T[r], -acc);
-        Wk[r] = __dmul_rn(d, d);
-    }
-    __syncwarp();
-    const double ss_res = wdot(Wk, nullptr, 0, n, lane);
-    const double mean = __ddiv_rn(wdot(T, nullptr, 0, n, lane), double(n));
-    __syncwarp();
-    for (int r = lane; r < n; r += 32) {
-        const double d = __dadd_rn(T[r], -mean);
-        Wk[r] = __dmul_rn(d, d);
-    }
-    __syncwarp();
-    const double ss_tot = wdot(Wk, nullptr, 0, n, lane);
+    const double ss_res = qb(acc, 0, m), ss_tot = qb(acc, 1, m), mp = qb(acc, 2, m);
     o.r2 = ss_tot > 0 ? __dadd_rn(1.0, -__ddiv_rn(ss_res, ss_tot)) : (ss_res < 1e-18 ? 1.0 : 0.0);
-    // MAPE: the divisions in parallel, the sum sequential in sample order
-    // (the reference's loop order; same bits)
-    __syncwarp();
-    for (int r = lane; r < n; r += 32) Wk[r] = __ddiv_rn(fabs(__dadd_rn(T[r], -F[r])), fabs(T[r]));
-    __syncwarp();
-    double mp = 0.0;
-    if (lane == 0)
-        for (int r = 0; r < n; ++r) mp = __dadd_rn(mp, Wk[r]);
-    mp = __shfl_sync(FULL, mp, 0);
     o.mape = __ddiv_rn(mp, double(n));
-    __syncwarp();
     return o;
 }
 
@@ -556,26 +551,48 @@ struct Buckets {
     int32_t* degen;
 };
 
-constexpr int kFitWarps = 4;     // 128-thread CTAs
-constexpr int kFitSmemRows = 32;  // buckets up to 32 samples run entirely in shared memory
+constexpr int kQWarps = 4;   // warps per CTA (128 threads)
+constexpr int kQRows = 32;   // problems of <= 32 samples run in shared memory
+constexpr int kQScr = 5;     // global scratch doubles per sample (larger problems)
 
-__global__ void __launch_bounds__(32 * kFitWarps) k_fit(const double* sg, const double* sl, const double* st,
-                                                        Buckets b, double* scratch) {
-    __shared__ double wscr[kFitWarps][kFitScr * kFitSmemRows];
-    const int lane = threadIdx.x & 31;
+// fit_bucket over b.nb independent problems; quad p of warp w takes problem
+// 8w + p (grid-stride).  Shared slab per warp: [kQRows][32] column slots +
+// [kQRows][8] right-hand sides (40 KB per CTA).
+__global__ void __launch_bounds__(32 * kQWarps) k_qfit(const double* sg, const double* sl, const double* st,
+                                                       Buckets b, double* gscr) {
+    __shared__ double slab[kQWarps][kQRows * 40];
+    const int lane = threadIdx.x & 31, q = lane & 3, pq = lane >> 2;
+    const unsigned m = 0xFu << (lane & ~3);
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t q = warp; q < b.nb; q += nw) {
-        const int64_t lo = b.slo[q], n = b.shi[q] - lo;
+    double* sA = slab[threadIdx.x >> 5];
+    double* sR = sA + kQRows * 32;
+    for (int64_t base = warp * 8; base < b.nb; base += nw * 8) {
+        const int64_t pi = base + pq;
+        if (pi >= b.nb) continue;
+        const int64_t lo = b.slo[pi], n = b.shi[pi] - lo;
         if (n <= 0) continue;
-        double* scr = n <= kFitSmemRows ? wscr[threadIdx.x >> 5] : scratch + kFitScr * lo;
-        FitOut o = warp_fit(sg + lo, sl + lo, st + lo, int(n), scr, lane);
-        if (lane == 0) {
-            for (int c = 0; c < 4; ++c) b.coeff[4 * q + c] = o.c[c];
-            b.r2[q] = o.r2;
-            b.mape[q] = o.mape;
-            b.degen[q] = o.degenerate;
+        double *A, *R;
+        int la, lr;
+        if (n <= kQRows) {
+            A = sA + pq * 4;
+            la = 32;
+            R = sR + pq;
+            lr = 8;
+        } else {
+            A = gscr + kQScr * lo;
+            la = 4;
+            R = A + 4 * n;
+            lr = 1;
         }
+        const FitOut o = quad_fit(sg + lo, sl + lo, st + lo, int(n), A, la, R, lr, q, m);
+        if (q == 0) {
+            for (int c = 0; c < 4; ++c) b.coeff[4 * pi + c] = o.c[c];
+            if (b.r2) b.r2[pi] = o.r2;
+            if (b.mape) b.mape[pi] = o.mape;
+            b.degen[pi] = o.degenerate;
+        }
+        __syncwarp(m);  // the slab is reused by the quad's next problem
     }
 }
 
@@ -703,87 +720,98 @@ struct Macros {
     int32_t* em;
 };
 
-__global__ void k_extrap(Rec rc, const double* sg, const double* sl, const double* st, Buckets b,
-                         const int64_t* slo_group, Groups gr, const int64_t* ordA, Macros m, double* scratch) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t q = warp; q < m.nmac; q += nw) {
-        const int64_t b0 = m.bstart[q], b1 = m.bstart[q + 1];
-        const int w_lo = max(1, m.W - m.p + 1);
-        int64_t wb0 = -1, wb1 = -1;
-        int used = 0;
-        for (int64_t k = b0; k < b1; ++k)
-            if (m.bw[k] >= w_lo && m.bw[k] <= m.W) {
-                if (wb0 < 0) wb0 = k;
-                wb1 = k + 1;
-                ++used;
-            }
-        const int64_t gslice = m.gstart_of_bucket[b0];  // ext anchors slice for this macro
-        if (used >= 2) {
-            const int64_t lo = b.slo[wb0], n = b.shi[wb1 - 1] - lo;
-            FitOut o = warp_fit(sg + lo, sl + lo, st + lo, int(n), scratch + kFitScr * lo, lane);
-            if (lane == 0) {
-                for (int c = 0; c < 4; ++c) m.theta[4 * q + c] = o.c[c];
-                m.flags[q] = o.degenerate ? 1 : 0;
-                // majority vote per l over window groups, ties -> smaller micro
-                const int64_t g0 = m.gstart_of_bucket[wb0], g1 = m.gstart_of_bucket[wb1];
-                int cnt = 0;
-                int64_t prev_l = 0;
-                bool have_prev = false;
-                for (;;) {  // distinct l ascending
-                    bool found = false;
-                    int64_t lv = 0;
-                    for (int64_t k = g0; k < g1; ++k) {
-                        const int64_t gl = rc.l[ordA[gr.start[k]]];
-                        if ((!have_prev || gl > prev_l) && (!found || gl < lv)) {
-                            lv = gl;
-                            found = true;
-                        }
-                    }
-                    if (!found) break;
-                    int32_t best_micro = -1, best_count = -1, cur = INT_MIN;
-                    for (;;) {
-                        int32_t nxt = INT_MAX;
-                        for (int64_t k = g0; k < g1; ++k) {
-                            const int64_t gl = rc.l[ordA[gr.start[k]]];
-                            if (gl == lv && gr.micro[k] > cur && gr.micro[k] < nxt) nxt = gr.micro[k];
-                        }
-                        if (nxt == INT_MAX) break;
-                        int32_t c = 0;
-                        for (int64_t k = g0; k < g1; ++k)
-                            if (rc.l[ordA[gr.start[k]]] == lv && gr.micro[k] == nxt) ++c;
-                        if (c > best_count) {
-                            best_count = c;
-                            best_micro = nxt;
-                        }
-                        cur = nxt;
-                    }
-                    m.el[gslice + cnt] = lv;
-                    m.em[gslice + cnt] = best_micro;
-                    ++cnt;
-                    prev_l = lv;
-                    have_prev = true;
-                }
-                m.next[q] = cnt;
-            }
-        } else if (lane == 0) {
-            // fewer than two window waves: the highest wave's fit and anchors
-            const int64_t top = b1 - 1;
-            for (int c = 0; c < 4; ++c) m.theta[4 * q + c] = b.coeff[4 * top + c];
-            m.flags[q] = 2;
-            const int64_t g0 = m.gstart_of_bucket[top], g1 = m.gstart_of_bucket[top + 1];
-            int cnt = 0;
-            for (int64_t k = g0; k < g1; ++k) {
-                m.el[gslice + cnt] = rc.l[ordA[gr.start[k]]];
-                m.em[gslice + cnt] = gr.micro[k];
-                ++cnt;
-            }
-            m.next[q] = cnt;
+// fit_extrapolation (model.cpp:140-192), split around the pooled fit:
+// k_ext_prep (thread / macro) finds the window [max(1, W-p+1), W]; with >= 2
+// waves of data it queues the pooled slice for k_qfit, else it copies the
+// highest wave's fit and anchors (ext_insufficient_waves).  k_ext_vote
+// (thread / macro) then takes the fit's degenerate flag and the per-l
+// majority micro (ties -> smaller micro id).
+__global__ void k_ext_prep(Rec rc, Buckets b, Groups gr, const int64_t* ordA, Macros m, int64_t* elo, int64_t* ehi) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= m.nmac) return;
+    const int64_t b0 = m.bstart[q], b1 = m.bstart[q + 1];
+    const int w_lo = max(1, m.W - m.p + 1);
+    int64_t wb0 = -1, wb1 = -1;
+    int used = 0;
+    for (int64_t k = b0; k < b1; ++k)
+        if (m.bw[k] >= w_lo && m.bw[k] <= m.W) {
+            if (wb0 < 0) wb0 = k;
+            wb1 = k + 1;
+            ++used;
         }
-        __syncwarp();
+    if (used >= 2) {
+        elo[q] = b.slo[wb0];
+        ehi[q] = b.shi[wb1 - 1];
+        return;
     }
-    (void)slo_group;
+    elo[q] = ehi[q] = 0;
+    // fewer than two window waves: the highest wave's fit and anchors
+    const int64_t top = b1 - 1, gslice = m.gstart_of_bucket[b0];
+    for (int c = 0; c < 4; ++c) m.theta[4 * q + c] = b.coeff[4 * top + c];
+    m.flags[q] = 2;
+    const int64_t g0 = m.gstart_of_bucket[top], g1 = m.gstart_of_bucket[top + 1];
+    int cnt = 0;
+    for (int64_t k = g0; k < g1; ++k) {
+        m.el[gslice + cnt] = rc.l[ordA[gr.start[k]]];
+        m.em[gslice + cnt] = gr.micro[k];
+        ++cnt;
+    }
+    m.next[q] = cnt;
+}
+
+__global__ void k_ext_vote(Rec rc, Groups gr, const int64_t* ordA, Macros m, const int64_t* elo, const int64_t* ehi,
+                           const int32_t* edeg) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= m.nmac || ehi[q] <= elo[q]) return;
+    m.flags[q] = edeg[q] ? 1 : 0;
+    const int64_t b0 = m.bstart[q], b1 = m.bstart[q + 1];
+    const int w_lo = max(1, m.W - m.p + 1);
+    int64_t wb0 = -1, wb1 = -1;
+    for (int64_t k = b0; k < b1; ++k)
+        if (m.bw[k] >= w_lo && m.bw[k] <= m.W) {
+            if (wb0 < 0) wb0 = k;
+            wb1 = k + 1;
+        }
+    const int64_t gslice = m.gstart_of_bucket[b0];
+    const int64_t g0 = m.gstart_of_bucket[wb0], g1 = m.gstart_of_bucket[wb1];
+    int cnt = 0;
+    int64_t prev_l = 0;
+    bool have_prev = false;
+    for (;;) {  // distinct l ascending
+        bool found = false;
+        int64_t lv = 0;
+        for (int64_t k = g0; k < g1; ++k) {
+            const int64_t gl = rc.l[ordA[gr.start[k]]];
+            if ((!have_prev || gl > prev_l) && (!found || gl < lv)) {
+                lv = gl;
+                found = true;
+            }
+        }
+        if (!found) break;
+        int32_t best_micro = -1, best_count = -1, cur = INT_MIN;
+        for (;;) {
+            int32_t nxt = INT_MAX;
+            for (int64_t k = g0; k < g1; ++k) {
+                const int64_t gl = rc.l[ordA[gr.start[k]]];
+                if (gl == lv && gr.micro[k] > cur && gr.micro[k] < nxt) nxt = gr.micro[k];
+            }
+            if (nxt == INT_MAX) break;
+            int32_t c = 0;
+            for (int64_t k = g0; k < g1; ++k)
+                if (rc.l[ordA[gr.start[k]]] == lv && gr.micro[k] == nxt) ++c;
+            if (c > best_count) {
+                best_count = c;
+                best_micro = nxt;
+            }
+            cur = nxt;
+        }
+        m.el[gslice + cnt] = lv;
+        m.em[gslice + cnt] = best_micro;
+        ++cnt;
+        prev_l = lv;
+        have_prev = true;
+    }
+    m.next[q] = cnt;
 }
 
 // Device-resident table CSR (wt_tables_desc layout, int32) from the fit's
@@ -1209,7 +1237,9 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     double* sg = dalloc<double>(owned, S_total);
     double* sl = dalloc<double>(owned, S_total);
     double* stt = dalloc<double>(owned, S_total);
-    double* scratch = dalloc<double>(owned, kFitScr * S_total);
+    // global scratch of problems above kQRows samples (extrapolation pools,
+    // linear baseline); virtual until touched
+    double* scratch = dalloc<double>(owned, kQScr * S_total);
     if (!scratch) {
         g_fit_err = "cudaMalloc failed (fit scratch)";
         return WT_CUDA_ERROR;
@@ -1227,12 +1257,23 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     Buckets bk{NB, d_bslo, d_bshi, B->t_coeff_theta, B->d_r2, B->d_mape, bdegen};
     const int nsm = wtb::device_sms();
     trace("samples + meta");
-    k_fit<<<nsm * 8, 128, 0, s>>>(sg, sl, stt, bk, scratch);
-    trace("k_fit");
+    const int qgrid = int(std::max<int64_t>(1, std::min<int64_t>((NB + 8 * kQWarps - 1) / (8 * kQWarps), nsm * 16)));
+    k_qfit<<<qgrid, 32 * kQWarps, 0, s>>>(sg, sl, stt, bk, scratch);
+    trace("k_qfit buckets");
     Macros mc{NM, d_mbs, d_bw, d_bgs, W, p, B->t_theta_ext, B->d_ext_flags, B->t_ext_cnt, B->t_ext_l, B->t_ext_micro};
-    // extrapolation pools reuse the bucket scratch layout (slice of the pooled samples)
-    k_extrap<<<nsm * 4, 128, 0, s>>>(rc, sg, sl, stt, bk, soff, gr, ordA, mc, scratch);
-    trace("k_extrap");
+    {
+        int64_t* elo = dalloc<int64_t>(owned, NM);
+        int64_t* ehi = dalloc<int64_t>(owned, NM);
+        int32_t* edeg = dalloc<int32_t>(owned, NM);
+        const int mblocks = int((NM + 127) / 128);
+        k_ext_prep<<<mblocks, 128, 0, s>>>(rc, bk, gr, ordA, mc, elo, ehi);
+        // pooled window fits (model.cpp:171-176): theta_ext straight into the table
+        Buckets ext{NM, elo, ehi, B->t_theta_ext, nullptr, nullptr, edeg};
+        const int egrid = int(std::max<int64_t>(1, std::min<int64_t>((NM + 8 * kQWarps - 1) / (8 * kQWarps), nsm * 16)));
+        k_qfit<<<egrid, 32 * kQWarps, 0, s>>>(sg, sl, stt, ext, scratch);
+        k_ext_vote<<<mblocks, 128, 0, s>>>(rc, gr, ordA, mc, elo, ehi, edeg);
+    }
+    trace("extrapolation");
     {
         Csr32 o{B->t_macro, B->t_W, B->t_coeff_off, B->t_coeff_w, B->t_awave_aoff, B->t_ext_off, B->d_nsamp,
                 B->d_dflags};
@@ -1259,7 +1300,8 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
             return WT_CUDA_ERROR;
         }
         Buckets lin{NM, d_mslo, d_mshi, B->b_lin, B->b_lin_r2, B->b_lin_mape, B->b_lin_deg};
-        k_fit<<<nsm * 8, 128, 0, s>>>(sg, sl, stt, lin, scratch);
+        k_qfit<<<int(std::max<int64_t>(1, std::min<int64_t>((NM + 31) / 32, nsm * 16))), 32 * kQWarps, 0, s>>>(
+            sg, sl, stt, lin, scratch);
         static const bool serial = std::getenv("WT_STEP_SERIAL") != nullptr;
         if (serial) {
             k_step<<<int((NM + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, gw, gl, soff, gr.nsamp, stt, B->b_step_l,
@@ -1600,7 +1642,7 @@ wt_status wt_fit_bucket_batch(const double* g, const double* l, const double* t,
     double* dg = dalloc<double>(owned, S);
     double* dl = dalloc<double>(owned, S);
     double* dt = dalloc<double>(owned, S);
-    double* scr = dalloc<double>(owned, kFitScr * S);
+    double* scr = dalloc<double>(owned, kQScr * S);
     int64_t* lo = dalloc<int64_t>(owned, nb);
     int64_t* hi = dalloc<int64_t>(owned, nb);
     std::vector<int64_t> hlo(nb), hhi(nb);
@@ -1615,7 +1657,7 @@ wt_status wt_fit_bucket_batch(const double* g, const double* l, const double* t,
     CK(cudaMemcpy(hi, hhi.data(), nb * 8, cudaMemcpyHostToDevice));
     Buckets bk{nb, lo, hi, dalloc<double>(owned, nb * 4), dalloc<double>(owned, nb), dalloc<double>(owned, nb),
                dalloc<int32_t>(owned, nb)};
-    k_fit<<<int(std::min<int64_t>((nb + 3) / 4, 148 * 16)), 128>>>(dg, dl, dt, bk, scr);
+    k_qfit<<<int(std::min<int64_t>((nb + 31) / 32, 148 * 16)), 32 * kQWarps>>>(dg, dl, dt, bk, scr);
     CK(cudaGetLastError());
     CK(cudaMemcpy(coeffs, bk.coeff, nb * 32, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(r2, bk.r2, nb * 8, cudaMemcpyDeviceToHost));

@@ -1,5 +1,6 @@
 """Drives one kernel family for an ncu capture (diagnostic; not a bench line).
-usage: python tools/prof_kernels.py {sweep3|eval|gather|step|fit} [n]
+usage: python tools/prof_kernels.py {sweep3|eval|gather|step|fit|build} [n]
+(build = the bench's records-in-HBM -> grid chain at config 3/4, 3 times)
 (step = the bench step: gather of the config-2 stream with 1% off-grid)"""
 import os
 import sys
@@ -18,6 +19,22 @@ if mode == "fit":
     for _ in range(2):
         r = capi.fit_build(rec, cfg["id"], 40, 10)
     print("fit device ms", r["device_ms"])
+elif mode == "build":
+    cfg = S.config_space(True)
+    rec = S.synthetic_records(cfg, micros_per_macro=1)
+    cv = {"g": torch.int64, "l": torch.int64, "w": torch.int32, "macro": torch.int32, "micro": torch.int32,
+          "lat": torch.float64}
+    recd = {k: torch.as_tensor(np.ascontiguousarray(rec[k])).to(dtype=cv[k], device="cuda") for k in cv}
+    reg = S.registry_arrays(cfg)
+    p3 = S.unique_pairs(S.LLAMA3_70B, S.QWEN2_72B)
+    for _ in range(3):
+        b = capi.Build(recd, cfg["id"], 40, 10)
+        e = capi.Engine.from_build(b, reg, n_sm=148)
+        g = capi.Grid(e, [p[0] for p in p3], [p[1] for p in p3], 1, 65536)
+        g.sweep()
+        torch.cuda.synchronize()
+        for x in (g, e, b):
+            x.close()
 elif mode == "sweep3":
     cfg = S.config_space(True)
     eng = capi.Engine(S.synthetic_tables(cfg), S.registry_arrays(cfg), n_sm=148)
