@@ -157,6 +157,13 @@ wt_status wt_prune_plan(const wt_tables_desc* tables, const wt_registry_desc* re
  * Synchronous. */
 wt_status wt_engine_prune_masks(const wt_engine* e, uint32_t* masks, int64_t n);
 
+/* Instrumentation: while `counter` (a device uint64, caller-owned) is set,
+ * the grid sweep (k_sweep2) and the list evaluation (k_eval4) add the number
+ * of (shape | query, config) evaluations they physically execute -- per warp
+ * and segment, surviving configs x 32 lanes x shapes per lane, idle lanes
+ * included.  NULL turns it off.  Costs one atomic per warp and segment. */
+wt_status wt_engine_count_evals(wt_engine* e, unsigned long long* counter);
+
 /* Extension (A/B and second-witness runs): enable = 0 makes every kernel
  * evaluate all configs (the pruning masks are ignored); 1 (default, unless
  * the WT_PRUNE=0 environment variable was set) uses them.  Not thread-safe

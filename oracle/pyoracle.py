@@ -323,6 +323,23 @@ class Reference:
         if st:
             raise RuntimeError(self.err())
 
+    def build_timed(self, rec, sample_ids, t_m, t_n, t_k, W, p, n_sm, nthreads):
+        """Wall seconds of the reference's build_dual_table over ALL records
+        for the sample macros, parallel across macros."""
+        self.lib.wtref_build_timed.restype = C.c_double
+        cols = [np.ascontiguousarray(rec[k], dt) for k, dt in
+                (("g", I64), ("l", I64), ("w", I32), ("macro", I32), ("micro", I32), ("lat", F64))]
+        ids = np.ascontiguousarray(sample_ids, I32)
+        tm, tn, tk = (np.ascontiguousarray(x, I64) for x in (t_m, t_n, t_k))
+        nt = C.c_int32()
+        sec = self.lib.wtref_build_timed(*[C.c_void_p(c.ctypes.data) for c in cols], C.c_int64(len(cols[0])),
+                                         C.c_void_p(ids.ctypes.data), C.c_void_p(tm.ctypes.data),
+                                         C.c_void_p(tn.ctypes.data), C.c_void_p(tk.ctypes.data), C.c_int(len(ids)),
+                                         C.c_int(W), C.c_int(p), C.c_int(n_sm), C.c_int(nthreads), C.byref(nt))
+        if sec < 0:
+            raise RuntimeError(self.err())
+        return sec, nt.value
+
     def build_plan(self, n_sm, bps, W, I, tau, anchors, out_json):
         a = np.ascontiguousarray(anchors, I64)
         return self.lib.wtref_build_plan(C.c_int(n_sm), C.c_int(bps), C.c_int(W), C.c_int(I), C.c_double(tau),

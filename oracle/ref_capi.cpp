@@ -17,6 +17,7 @@
 // own artefacts.  Queries are split across std::thread workers (static
 // interleave): tune() is pure and reentrant.
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -217,6 +218,45 @@ WTREF_API int wtref_build(const char* records_csv, const char* registry_json, co
         return 0;
     } catch (const std::exception& e) {
         return fail(e);
+    }
+}
+
+// CPU baseline of the build: the reference's own
+// build_dual_table (model.cpp:194-253) over the FULL record set, timed on a
+// sample of macros and parallelised only across macros -- thread t runs one
+// build_dual_table call over a registry holding sample macros t, t + T, ...
+// Records are converted to ProfileRecord once, outside the timed region.
+// Returns the wall seconds of the parallel region (or -1 on error);
+// *n_tables = tables built.
+WTREF_API double wtref_build_timed(const int64_t* g, const int64_t* l, const int32_t* w, const int32_t* macro,
+                                   const int32_t* micro, const double* lat, int64_t n, const int32_t* sample_ids,
+                                   const int64_t* t_m, const int64_t* t_n, const int64_t* t_k, int n_sample, int W,
+                                   int p, int n_sm, int nthreads, int32_t* n_tables) {
+    try {
+        std::vector<ProfileRecord> records(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) records[i] = ProfileRecord{g[i], l[i], w[i], macro[i], micro[i], lat[i]};
+        if (nthreads < 1) nthreads = 1;
+        std::vector<ConfigRegistry> regs(nthreads);
+        for (int i = 0; i < n_sample; ++i)
+            regs[i % nthreads].macros.push_back(MacroConfig{sample_ids[i], GemmTiles{t_m[i], t_n[i], t_k[i]}});
+        std::vector<int> built(nthreads, 0);
+        auto work = [&](int t) {
+            if (regs[t].macros.empty()) return;
+            built[t] = static_cast<int>(
+                build_dual_table(records, regs[t], HardwareSpec{n_sm, 1, "b200"}, {W, p}).size());
+        };
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        for (int t = 0; t < nthreads; ++t) pool.emplace_back(work, t);
+        for (auto& th : pool) th.join();
+        const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        int tot = 0;
+        for (int b : built) tot += b;
+        if (n_tables) *n_tables = tot;
+        return sec;
+    } catch (const std::exception& e) {
+        fail(e);
+        return -1.0;
     }
 }
 

@@ -92,7 +92,7 @@ class wt_build_result(C.Structure):
 # entry points declared in include/wavetune_c.h (tests check they all exist)
 EXPORTS = (
     "wt_last_error wt_version wt_abi_version wt_engine_create wt_engine_destroy wt_engine_info_get "
-    "wt_engine_config_index wt_engine_set_prune wt_engine_prune_masks wt_tune_batch wt_tune_grouped_batch wt_predict_batch wt_explain "
+    "wt_engine_config_index wt_engine_set_prune wt_engine_count_evals wt_engine_prune_masks wt_tune_batch wt_tune_grouped_batch wt_predict_batch wt_explain "
     "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_destroy wt_grid_storage wt_sweep wt_grid_finalize "
     "wt_fit_build_device wt_build_result_get wt_engine_create_from_build wt_gather_batch wt_decide_host_sync wt_decide_host_stream_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
     "wt_simulate_batch wt_profile_sim wt_tune_one wt_engine_set_resident wt_baseline_create "
@@ -262,6 +262,12 @@ class Engine:
         m = np.zeros(n_seg * R * 16, np.uint32)
         check(lib().wt_engine_prune_masks(self.handle, C.c_void_p(m.ctypes.data), C.c_int64(m.size)))
         return m.reshape(n_seg, R, 16)
+
+    def count_evals(self, counter):
+        """Instrumentation: `counter` = a 1-element int64 CUDA tensor that the
+        sweep / list evaluation add their physically executed evaluations to
+        (None turns it off)."""
+        check(lib().wt_engine_count_evals(self.handle, vp(_ptr(counter) if counter is not None else None)))
 
     def set_prune(self, enable: bool):
         """Extension: False evaluates every config (pruning masks ignored)."""

@@ -587,6 +587,12 @@ wt_status wt_engine_prune_masks(const wt_engine* e, uint32_t* masks, int64_t n) 
     return WT_OK;
 }
 
+wt_status wt_engine_count_evals(wt_engine* e, unsigned long long* counter) {
+    if (!e) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    e->dev.eval_count = counter;
+    return WT_OK;
+}
+
 wt_status wt_engine_set_prune(wt_engine* e, int32_t enable) {
     if (!e) return set_err(WT_INVALID_ARGUMENT, "null argument");
     e->dev.prune = enable ? 1 : 0;

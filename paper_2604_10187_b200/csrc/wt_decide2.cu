@@ -207,6 +207,8 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
                     live = __reduce_or_sync(0xffffffffu, live);
                 }
                 live &= h.live;  // subset of the staged configs
+                if (im.eval_count && (tid & 31) == 0)
+                    atomicAdd(im.eval_count, (unsigned long long)__popc(live) * 32ull * RPT);
                 if constexpr (SPECIAL) {
 #pragma unroll
                     for (int j = 0; j < RPT; ++j)

@@ -524,6 +524,8 @@ __global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval
                 }
                 live &= ncfg >= 32 ? 0xffffffffu : ((1u << ncfg) - 1u);
             }
+            if (im.eval_count && lane == 0)
+                atomicAdd(im.eval_count, (unsigned long long)__popc(live) * 32ull * RPT);
             int k_staged = 0;  // index of the next planned row in pth
             if constexpr (SPECIAL) {
 #pragma unroll

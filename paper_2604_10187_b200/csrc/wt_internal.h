@@ -79,6 +79,9 @@ struct DevImage {
     // flags of skipped configs still count).  prune = 0: all bits set.
     int32_t prune;
     int32_t seg_maxcfg;       // largest segment (configs)
+    // instrumentation (null = off): physically executed (shape|query, config)
+    // evaluations of k_sweep2 / k_eval4, lane-evaluations incl. idle lanes
+    unsigned long long* eval_count;
     const uint32_t* segmask;
     const uint32_t* segor;
 };
