@@ -57,6 +57,44 @@ def gather_traffic(n_decisions):
     return d["dram_bytes_per_decision"] * n_decisions, os.path.relpath(caps[-1], ROOT)
 
 
+def fp64_peak():
+    """Measured FP64 rates of this B200 pool (tools/micro/fp64_peak.cu: DMUL
+    and DADD chains, no FMA, and the 4 DMUL : 3 DADD mix of one bilinear
+    evaluation), committed under profiles/."""
+    import glob
+
+    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_fp64_peak.json")))
+    if not caps:
+        return None, None
+    with open(caps[-1]) as f:
+        return json.load(f), os.path.relpath(caps[-1], ROOT)
+
+
+def fp64_roofline(phys_evals, logical_evals, ms, flops_per_eval):
+    """ALU roofline on PHYSICALLY executed (shape|query, config) evaluations
+    (the kernels' wt_engine_count_evals counter) against the measured
+    bilinear-evaluation rate."""
+    pk, src = fp64_peak()
+    if pk is None or not ms:
+        return None
+    achieved = phys_evals / (ms * 1e-3)
+    peak = pk["bilinear_evals_per_s"] * 7.0 / flops_per_eval
+    return {"bound": "fp64", "unit": "evals/s", "achieved": achieved, "peak": peak, "frac": achieved / peak,
+            "physical_evals": int(phys_evals), "logical_evals": int(logical_evals),
+            "survival": phys_evals / max(1, logical_evals), "flops_per_eval": flops_per_eval,
+            "peak_source": f"{src} (measured DMUL/DADD mix, no FMA; {pk['dmul_per_s']:.3e} DMUL/s)"}
+
+
+def count_evals(torch, eng, dev, fn):
+    ctr = torch.zeros(1, dtype=torch.int64, device=dev)
+    torch.cuda.synchronize(dev)
+    eng.count_evals(ctr)
+    fn()
+    torch.cuda.synchronize(dev)
+    eng.count_evals(None)
+    return int(ctr.item())
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -268,6 +306,7 @@ def build_secondary(args, capi, S, torch, dist, ws, rank, local, dev, stream, gr
         torch.cuda.synchronize(dev)
         ms3 = e0.elapsed_time(e1)
         evals3 = g.n_entries * e.n_configs
+        phys3 = count_evals(torch, e, dev, lambda: g.sweep(stream=stream))
         out["full_build"] = {
             "ms_wall": min(walls), "ms_wall_runs": walls, "ms_device_events": min(devs),
             "stages_ms_wall_synced": stages,
@@ -280,7 +319,8 @@ def build_secondary(args, capi, S, torch, dist, ws, rank, local, dev, stream, gr
         out["config3_sweep"] = {"ms": ms3, "evals": evals3, "evals_per_s": evals3 / (ms3 * 1e-3),
                                 "evals_note": "(shape, config) pairs decided per second; configs proven dominated "
                                               "in a (wave row, L bucket) cell are skipped (exact pruning)",
-                                "shapes": g.n_entries, "configs": e.n_configs, "sharding": "single GPU"}
+                                "shapes": g.n_entries, "configs": e.n_configs, "sharding": "single GPU",
+                                "roofline": fp64_roofline(phys3, evals3, ms3, 6)}
         out["config4_fit"] = {"ms_device": res4["device_ms"], "records": int(len(rec4["g"])),
                               "tables": int(res4["n_tables"]), "buckets": int(len(res4["coeff_w"])),
                               "median_bucket_mape": float(np.median(res4["diag_mape"])),
@@ -322,8 +362,10 @@ def build_secondary(args, capi, S, torch, dist, ws, rank, local, dev, stream, gr
                               "tables": int(fit["n_tables"])}
         g3.close()
         eng3.close()
-    out["config1_sweep"] = {"ms": sweep_ms, "evals": grid.n_entries * eng.n_configs,
-                            "evals_per_s": grid.n_entries * eng.n_configs / (sweep_ms * 1e-3)}
+    ev1 = grid.n_entries * eng.n_configs
+    phys1 = count_evals(torch, eng, dev, lambda: grid.sweep(stream=stream))
+    out["config1_sweep"] = {"ms": sweep_ms, "evals": ev1, "evals_per_s": ev1 / (sweep_ms * 1e-3),
+                            "roofline": fp64_roofline(phys1, ev1, sweep_ms, 6)}
     return out
 
 
@@ -492,6 +534,7 @@ def run_wavetune(args):
     alg_bytes = 28.0 * n + 24.0 * n_off
     achieved = alg_bytes / (gather_ms * 1e-3) / 1e9
     traffic, traffic_src = gather_traffic(n)
+    phys_off = count_evals(torch, eng, dev, step)
 
     # e2e through the public API with host buffers (pinned), copies inside
     Mp, Np, Kp = (torch.from_numpy(x).pin_memory() for x in (Mh, Nh, Kh))
@@ -548,7 +591,8 @@ def run_wavetune(args):
                              "evals_per_s": n_off * eng.n_configs / (eval_ms * 1e-3),
                              "evals_note": "(query, config) pairs decided per second; dominated configs "
                                            "skipped exactly (WT_PRUNE=0 evaluates all)",
-                             "pipeline": "scan + counting-sort scatter + k_eval4 (keys counted in k_gather_h)"},
+                             "pipeline": "scan + counting-sort scatter + k_eval4 (keys counted in k_gather_h)",
+                             "roofline": fp64_roofline(phys_off, n_off * eng.n_configs, eval_ms, 7)},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -348,6 +348,18 @@ wt_status wt_grid_finalize(const wt_engine* e, wt_grid* g, void* stream);
 wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M, const int32_t* N,
                           const int32_t* K, int64_t n, const wt_decisions* out, void* stream);
 
+/* 64-bit dimensions (the reference's DenseGemm{i64 m, n, k},
+ * kernel_map.hpp:25-27; attention (s_q, n_heads, s_kv) the same way): i64
+ * device arrays, otherwise the contract of wt_tune_batch / wt_gather_batch.
+ * Queries whose dims all fit int32 take the int32 kernels; the others are
+ * evaluated in 64-bit integer arithmetic by a warp-per-query kernel.  A tile
+ * product above 2^63 or >= 2^31 waves for the smallest tile ->
+ * WT_UNSUPPORTED in that query's flags.  No top-k (topk must be 0). */
+wt_status wt_tune_batch_i64(const wt_engine* e, const int64_t* M, const int64_t* N, const int64_t* K, int64_t n,
+                            const wt_decisions* out, void* stream);
+wt_status wt_gather_batch_i64(const wt_engine* e, const wt_grid* g, const int64_t* M, const int64_t* N,
+                              const int64_t* K, int64_t n, const wt_decisions* out, void* stream);
+
 /* End-to-end convenience over HOST buffers (the call an application makes):
  * queries M/N/K and the outputs macro/micro/latency live in host memory
  * (pinned for full overlap).  The batch is cut into chunks of `chunk`

@@ -92,7 +92,7 @@ class wt_build_result(C.Structure):
 # entry points declared in include/wavetune_c.h (tests check they all exist)
 EXPORTS = (
     "wt_last_error wt_version wt_abi_version wt_engine_create wt_engine_destroy wt_engine_info_get "
-    "wt_engine_config_index wt_engine_set_prune wt_engine_count_evals wt_engine_prune_masks wt_tune_batch wt_tune_grouped_batch wt_predict_batch wt_explain "
+    "wt_engine_config_index wt_engine_set_prune wt_engine_count_evals wt_engine_prune_masks wt_tune_batch wt_tune_batch_i64 wt_gather_batch_i64 wt_tune_grouped_batch wt_predict_batch wt_explain "
     "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_destroy wt_grid_storage wt_sweep wt_grid_finalize "
     "wt_fit_build_device wt_build_result_get wt_engine_create_from_build wt_gather_batch wt_decide_host_sync wt_decide_host_stream_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
     "wt_simulate_batch wt_profile_sim wt_tune_one wt_engine_set_resident wt_baseline_create "
@@ -300,6 +300,12 @@ class Engine:
         check(lib().wt_tune_batch(self.handle, vp(_ptr(M)), vp(_ptr(N)), vp(_ptr(K)), C.c_int64(M.numel()),
                                   C.byref(out), vp(_stream_ptr(stream))))
 
+    def tune_batch_i64(self, M, N, K, out: wt_decisions, stream=None):
+        """Queries with int64 dims (DenseGemm{i64 m, n, k}); dims >= 2^31 are
+        evaluated in 64-bit arithmetic (wt_tune_batch_i64)."""
+        check(lib().wt_tune_batch_i64(self.handle, vp(_ptr(M)), vp(_ptr(N)), vp(_ptr(K)), C.c_int64(M.numel()),
+                                      C.byref(out), vp(_stream_ptr(stream))))
+
     def tune_one(self, M, N, K) -> wt_decision_one:
         """One query, synchronously, at minimum latency (wt_tune_one)."""
         o = wt_decision_one()
@@ -421,6 +427,10 @@ class Grid:
     def gather(self, M, N, K, out: wt_decisions, stream=None):
         check(lib().wt_gather_batch(self.engine.handle, self.handle, vp(_ptr(M)), vp(_ptr(N)), vp(_ptr(K)),
                                     C.c_int64(M.numel()), C.byref(out), vp(_stream_ptr(stream))))
+
+    def gather_i64(self, M, N, K, out: wt_decisions, stream=None):
+        check(lib().wt_gather_batch_i64(self.engine.handle, self.handle, vp(_ptr(M)), vp(_ptr(N)), vp(_ptr(K)),
+                                        C.c_int64(M.numel()), C.byref(out), vp(_stream_ptr(stream))))
 
     def decide_host(self, M, N, K, macro, micro, lat, chunk=1 << 22, stream=None):
         """End-to-end over host (pinned) buffers: H2D, gather, D2H, pipelined;

@@ -8,13 +8,11 @@
 #include "wavetune_c.h"
 #include "wavetune_gemm.h"
 #include "wt_gemm.h"
-#include "wt_gemm_table.inc"
 
 namespace wtb::gemm {
 namespace {
 
-constexpr int kFamilySize = int(sizeof(kFamily) / sizeof(kFamily[0]));
-constexpr size_t kWorkspace = size_t(16) << 20;
+constexpr size_t kWorkspace = kWorkspaceBytes;
 
 struct DeviceState {
     void* workspace = nullptr;
@@ -31,6 +29,7 @@ int state(DeviceState** out) {
     DeviceState& s = g_dev[d];
     if (!s.workspace) {
         if (cudaMalloc(&s.workspace, kWorkspace) != cudaSuccess) return WT_CUDA_ERROR;
+        if (cudaMemset(s.workspace, 0, kWorkspace) != cudaSuccess) return WT_CUDA_ERROR;
         if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess) return WT_CUDA_ERROR;
         if (cudaEventCreate(&s.e0) != cudaSuccess || cudaEventCreate(&s.e1) != cudaSuccess) return WT_CUDA_ERROR;
     }
@@ -43,8 +42,9 @@ bool valid_swizzle(int s) { return s == 1 || s == 2 || s == 4 || s == 8; }
 int status_of(int rc) {
     switch (rc) {
         case 0: return WT_OK;
-        case 1: return WT_UNSUPPORTED;      // can_implement refused the shape
-        case 4: return WT_RUNTIME_ERROR;    // workspace too small
+        case 1: return WT_UNSUPPORTED;      // shape / alignment not supported by the kernel
+        case 2: return WT_RUNTIME_ERROR;    // setup (tensor maps, attributes, workspace)
+        case 4: return WT_RUNTIME_ERROR;
         default: return WT_CUDA_ERROR;
     }
 }

@@ -1487,6 +1487,65 @@ wt_status wt_gather_batch(const wt_engine* e, const wt_grid* g, const int32_t* M
     return WT_OK;
 }
 
+// i64 queries (wt_wide.cu): narrow -> the int32 path -> wide fix-up, all
+// stream-ordered on the caller's stream; scratch from the library pool.
+static wt_status i64_batch(const wt_engine* e, const wt_grid* g, const int64_t* M, const int64_t* N,
+                           const int64_t* K, int64_t n, const wt_decisions* out, void* stream, const char* what) {
+    NvtxRange nvtx_(what);
+    if (!e || !M || !N || !K) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    if (g && g->eng != e) return set_err(WT_INVALID_ARGUMENT, "grid was created for another engine");
+    wt_status st = check_out(out);
+    if (st) return st;
+    if (out->topk) return set_err(WT_UNSUPPORTED, "top-k is not offered for i64 queries");
+    if (n <= 0) return n == 0 ? WT_OK : set_err(WT_INVALID_ARGUMENT, "negative batch size");
+    if (!g && e->host.family == WT_FAMILY_GROUPED_GEMM)
+        return set_err(WT_INVALID_ARGUMENT, "dense_gemm workload needs gemm tiles");
+    DeviceGuard guard(e->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t a4 = (size_t(n) * 4 + 255) & ~size_t(255);
+    const size_t bytes = 3 * a4 + size_t(n) * 8 + 256;
+    char* p = nullptr;
+    cudaError_t ce = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), bytes, lib_pool(e->device), s);
+    if (ce != cudaSuccess) return cuda_err(ce, what);
+    WideArgs a{};
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.n = n;
+    a.M32 = reinterpret_cast<int32_t*>(p);
+    a.N32 = reinterpret_cast<int32_t*>(p + a4);
+    a.K32 = reinterpret_cast<int32_t*>(p + 2 * a4);
+    a.count = reinterpret_cast<unsigned long long*>(p + 3 * a4);
+    a.list = reinterpret_cast<int64_t*>(p + 3 * a4 + 256);
+    a.out = to_out(out);
+    ce = cudaMemsetAsync(a.count, 0, 8, s);
+    if (ce == cudaSuccess) ce = launch_narrow(a, s);
+    g_launches++;
+    if (ce == cudaSuccess) {
+        st = g ? wt_gather_batch(e, g, a.M32, a.N32, a.K32, n, out, stream)
+               : wt_tune_batch(e, a.M32, a.N32, a.K32, n, out, stream);
+        if (st == WT_OK) {
+            ce = launch_wide(e->dev, a, s);
+            g_launches++;
+        }
+    }
+    cudaFreeAsync(p, s);
+    if (st != WT_OK) return st;
+    if (ce != cudaSuccess) return cuda_err(ce, what);
+    return WT_OK;
+}
+
+wt_status wt_tune_batch_i64(const wt_engine* e, const int64_t* M, const int64_t* N, const int64_t* K, int64_t n,
+                            const wt_decisions* out, void* stream) {
+    return i64_batch(e, nullptr, M, N, K, n, out, stream, "wt_tune_batch_i64");
+}
+
+wt_status wt_gather_batch_i64(const wt_engine* e, const wt_grid* g, const int64_t* M, const int64_t* N,
+                              const int64_t* K, int64_t n, const wt_decisions* out, void* stream) {
+    if (!g) return set_err(WT_INVALID_ARGUMENT, "null grid");
+    return i64_batch(e, g, M, N, K, n, out, stream, "wt_gather_batch_i64");
+}
+
 wt_status wt_decide_host_sync(const wt_engine* e, const wt_grid* g, const int32_t* M,
                               const int32_t* N, const int32_t* K, int64_t n, int32_t* macro_id,
                               int32_t* micro_id, double* latency_us, int64_t chunk) {

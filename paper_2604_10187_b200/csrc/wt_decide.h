@@ -180,6 +180,22 @@ struct NearestArgs {
     int32_t* comps;
 };
 
+// 64-bit-dimension queries (wt_wide.cu): narrowed copies + the wide list
+struct WideArgs {
+    const int64_t* M;
+    const int64_t* N;
+    const int64_t* K;
+    int64_t n;
+    int32_t* M32;
+    int32_t* N32;
+    int32_t* K32;
+    int64_t* list;                // indices of queries with a dim >= 2^31
+    unsigned long long* count;    // wide list length (zeroed by the caller)
+    DecOut out;
+};
+cudaError_t launch_narrow(const WideArgs& a, cudaStream_t st);
+cudaError_t launch_wide(const DevImage& im, const WideArgs& a, cudaStream_t st);
+
 // Library-owned stream-ordered memory pool of a device (wt_capi.cu).
 cudaMemPool_t device_pool(int device);
 // Launch helpers for the current device, safe for concurrent host threads

@@ -551,22 +551,25 @@ struct Buckets {
     int32_t* degen;
 };
 
-constexpr int kQWarps = 4;   // warps per CTA (128 threads)
-constexpr int kQRows = 32;   // problems of <= 32 samples run in shared memory
-constexpr int kQScr = 5;     // global scratch doubles per sample (larger problems)
+constexpr int kQWarps = 4;    // warps per CTA of the bucket fit (128 threads)
+constexpr int kQRows = 32;    // bucket problems of <= 32 samples run in shared memory
+constexpr int kQPoolRows = 256;  // pooled (extrapolation / per-macro) problems: 1 warp per CTA, 80 KB slab
+constexpr int kQScr = 5;      // global scratch doubles per sample (problems above the slab)
 
 // fit_bucket over b.nb independent problems; quad p of warp w takes problem
-// 8w + p (grid-stride).  Shared slab per warp: [kQRows][32] column slots +
-// [kQRows][8] right-hand sides (40 KB per CTA).
-__global__ void __launch_bounds__(32 * kQWarps) k_qfit(const double* sg, const double* sl, const double* st,
-                                                       Buckets b, double* gscr) {
-    __shared__ double slab[kQWarps][kQRows * 40];
+// 8w + p (grid-stride).  Shared slab per warp (dynamic): [ROWS][32] column
+// slots + [ROWS][8] right-hand sides; problems of more than ROWS samples
+// work in their own global scratch (same operation order, bitwise equal).
+template <int ROWS, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS) k_qfit(const double* sg, const double* sl, const double* st,
+                                                     Buckets b, double* gscr) {
+    extern __shared__ double slab_dyn[];
     const int lane = threadIdx.x & 31, q = lane & 3, pq = lane >> 2;
     const unsigned m = 0xFu << (lane & ~3);
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    double* sA = slab[threadIdx.x >> 5];
-    double* sR = sA + kQRows * 32;
+    double* sA = slab_dyn + size_t(threadIdx.x >> 5) * ROWS * 40;
+    double* sR = sA + ROWS * 32;
     for (int64_t base = warp * 8; base < b.nb; base += nw * 8) {
         const int64_t pi = base + pq;
         if (pi >= b.nb) continue;
@@ -574,7 +577,7 @@ __global__ void __launch_bounds__(32 * kQWarps) k_qfit(const double* sg, const d
         if (n <= 0) continue;
         double *A, *R;
         int la, lr;
-        if (n <= kQRows) {
+        if (n <= ROWS) {
             A = sA + pq * 4;
             la = 32;
             R = sR + pq;
@@ -594,6 +597,32 @@ __global__ void __launch_bounds__(32 * kQWarps) k_qfit(const double* sg, const d
         }
         __syncwarp(m);  // the slab is reused by the quad's next problem
     }
+}
+
+template <int ROWS, int WARPS>
+constexpr size_t qfit_smem() {
+    return size_t(WARPS) * ROWS * 40 * sizeof(double);
+}
+
+// Bucket problems (<= kQRows samples mostly) on 4-warp CTAs; pooled problems
+// (extrapolation windows, per-macro baselines) on 1-warp CTAs with a
+// kQPoolRows slab.  grid: problems / 8 per warp, capped at 16 CTAs per SM.
+cudaError_t launch_qfit(bool pooled, const double* sg, const double* sl, const double* st, const Buckets& b,
+                        double* gscr, int nsm, cudaStream_t s) {
+    if (b.nb <= 0) return cudaSuccess;
+    if (!pooled) {
+        constexpr size_t sm = qfit_smem<kQRows, kQWarps>();
+        const int grid = int(std::max<int64_t>(1, std::min<int64_t>((b.nb + 8 * kQWarps - 1) / (8 * kQWarps),
+                                                                   int64_t(nsm) * 16)));
+        k_qfit<kQRows, kQWarps><<<grid, 32 * kQWarps, sm, s>>>(sg, sl, st, b, gscr);
+    } else {
+        constexpr size_t sm = qfit_smem<kQPoolRows, 1>();
+        const cudaError_t e = wtb::prepare_smem(reinterpret_cast<const void*>(k_qfit<kQPoolRows, 1>), sm);
+        if (e != cudaSuccess) return e;
+        const int grid = int(std::max<int64_t>(1, std::min<int64_t>((b.nb + 7) / 8, int64_t(nsm) * 16)));
+        k_qfit<kQPoolRows, 1><<<grid, 32, sm, s>>>(sg, sl, st, b, gscr);
+    }
+    return cudaGetLastError();
 }
 
 // ---- ablation baselines (tuner.cpp:168-220) from the selected samples.
@@ -759,59 +788,125 @@ __global__ void k_ext_prep(Rec rc, Buckets b, Groups gr, const int64_t* ordA, Ma
     m.next[q] = cnt;
 }
 
-__global__ void k_ext_vote(Rec rc, Groups gr, const int64_t* ordA, Macros m, const int64_t* elo, const int64_t* ehi,
-                           const int32_t* edeg) {
-    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+// Warp per macro.  The window's groups (w asc, l asc) carry (l, selected
+// micro); the per-l majority micro (ties -> smaller micro) is found with
+// O(n^2) lane-parallel counting over the window staged in shared memory
+// (n = groups in the window, <= kVoteCap; larger windows take the serial
+// scan on lane 0), then each l's winner is written at the rank of l among
+// the distinct l values.
+constexpr int kVoteWarps = 4;
+constexpr int kVoteCap = 256;
+__global__ void __launch_bounds__(32 * kVoteWarps)
+    k_ext_vote(Rec rc, Groups gr, const int64_t* ordA, Macros m, const int64_t* elo, const int64_t* ehi,
+               const int32_t* edeg) {
+    __shared__ int64_t sl[kVoteWarps][kVoteCap];
+    __shared__ int32_t sm[kVoteWarps][kVoteCap], sc[kVoteWarps][kVoteCap], sf[kVoteWarps][kVoteCap];
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const int64_t q = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (q >= m.nmac || ehi[q] <= elo[q]) return;
-    m.flags[q] = edeg[q] ? 1 : 0;
+    if (lane == 0) m.flags[q] = edeg[q] ? 1 : 0;
     const int64_t b0 = m.bstart[q], b1 = m.bstart[q + 1];
     const int w_lo = max(1, m.W - m.p + 1);
-    int64_t wb0 = -1, wb1 = -1;
-    for (int64_t k = b0; k < b1; ++k)
+    long long wb0 = LLONG_MAX, wb1 = -1;
+    for (int64_t k = b0 + lane; k < b1; k += 32)
         if (m.bw[k] >= w_lo && m.bw[k] <= m.W) {
-            if (wb0 < 0) wb0 = k;
-            wb1 = k + 1;
+            wb0 = min(wb0, (long long)k);
+            wb1 = max(wb1, (long long)k + 1);
         }
+    wb0 = __reduce_min_sync(FULL, int(min(wb0, (long long)INT_MAX)));
+    wb1 = __reduce_max_sync(FULL, int(wb1));
     const int64_t gslice = m.gstart_of_bucket[b0];
     const int64_t g0 = m.gstart_of_bucket[wb0], g1 = m.gstart_of_bucket[wb1];
-    int cnt = 0;
-    int64_t prev_l = 0;
-    bool have_prev = false;
-    for (;;) {  // distinct l ascending
-        bool found = false;
-        int64_t lv = 0;
-        for (int64_t k = g0; k < g1; ++k) {
-            const int64_t gl = rc.l[ordA[gr.start[k]]];
-            if ((!have_prev || gl > prev_l) && (!found || gl < lv)) {
-                lv = gl;
-                found = true;
-            }
-        }
-        if (!found) break;
-        int32_t best_micro = -1, best_count = -1, cur = INT_MIN;
-        for (;;) {
-            int32_t nxt = INT_MAX;
+    const int n = int(g1 - g0);
+    if (n > kVoteCap) {
+        if (lane != 0) return;
+        int cnt = 0;
+        int64_t prev_l = 0;
+        bool have_prev = false;
+        for (;;) {  // distinct l ascending
+            bool found = false;
+            int64_t lv = 0;
             for (int64_t k = g0; k < g1; ++k) {
                 const int64_t gl = rc.l[ordA[gr.start[k]]];
-                if (gl == lv && gr.micro[k] > cur && gr.micro[k] < nxt) nxt = gr.micro[k];
+                if ((!have_prev || gl > prev_l) && (!found || gl < lv)) {
+                    lv = gl;
+                    found = true;
+                }
             }
-            if (nxt == INT_MAX) break;
-            int32_t c = 0;
-            for (int64_t k = g0; k < g1; ++k)
-                if (rc.l[ordA[gr.start[k]]] == lv && gr.micro[k] == nxt) ++c;
-            if (c > best_count) {
-                best_count = c;
-                best_micro = nxt;
+            if (!found) break;
+            int32_t best_micro = -1, best_count = -1, cur = INT_MIN;
+            for (;;) {
+                int32_t nxt = INT_MAX;
+                for (int64_t k = g0; k < g1; ++k) {
+                    const int64_t gl = rc.l[ordA[gr.start[k]]];
+                    if (gl == lv && gr.micro[k] > cur && gr.micro[k] < nxt) nxt = gr.micro[k];
+                }
+                if (nxt == INT_MAX) break;
+                int32_t c = 0;
+                for (int64_t k = g0; k < g1; ++k)
+                    if (rc.l[ordA[gr.start[k]]] == lv && gr.micro[k] == nxt) ++c;
+                if (c > best_count) {
+                    best_count = c;
+                    best_micro = nxt;
+                }
+                cur = nxt;
             }
-            cur = nxt;
+            m.el[gslice + cnt] = lv;
+            m.em[gslice + cnt] = best_micro;
+            ++cnt;
+            prev_l = lv;
+            have_prev = true;
         }
-        m.el[gslice + cnt] = lv;
-        m.em[gslice + cnt] = best_micro;
-        ++cnt;
-        prev_l = lv;
-        have_prev = true;
+        m.next[q] = cnt;
+        return;
     }
-    m.next[q] = cnt;
+    int64_t* L = sl[wi];
+    int32_t* U = sm[wi];
+    int32_t* Cn = sc[wi];
+    int32_t* FL = sf[wi];
+    for (int k = lane; k < n; k += 32) {
+        L[k] = rc.l[ordA[gr.start[g0 + k]]];
+        U[k] = gr.micro[g0 + k];
+    }
+    __syncwarp();
+    // occurrences of (l, micro) (-1 marks a repeat of an earlier entry) and
+    // first occurrence of each l
+    for (int k = lane; k < n; k += 32) {
+        int c = 0;
+        bool first = true, firstl = true;
+        for (int j = 0; j < n; ++j)
+            if (L[j] == L[k]) {
+                if (j < k) firstl = false;
+                if (U[j] == U[k]) {
+                    ++c;
+                    if (j < k) first = false;
+                }
+            }
+        Cn[k] = first ? c : -1;
+        FL[k] = firstl;
+    }
+    __syncwarp();
+    int distinct = 0;
+    for (int k = lane; k < n; k += 32) {
+        const int64_t lk = L[k];
+        bool win = Cn[k] >= 0;
+        int rank = 0;  // distinct l values below lk
+        for (int j = 0; j < n; ++j) {
+            const int64_t lj = L[j];
+            if (lj == lk) {
+                if (Cn[j] > Cn[k] || (Cn[j] == Cn[k] && Cn[j] >= 0 && U[j] < U[k])) win = false;
+            } else if (lj < lk) {
+                rank += FL[j];
+            }
+        }
+        if (win) {
+            m.el[gslice + rank] = lk;
+            m.em[gslice + rank] = U[k];
+        }
+        distinct += FL[k];
+    }
+    distinct = __reduce_add_sync(FULL, distinct);
+    if (lane == 0) m.next[q] = distinct;
 }
 
 // Device-resident table CSR (wt_tables_desc layout, int32) from the fit's
@@ -1257,8 +1352,7 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     Buckets bk{NB, d_bslo, d_bshi, B->t_coeff_theta, B->d_r2, B->d_mape, bdegen};
     const int nsm = wtb::device_sms();
     trace("samples + meta");
-    const int qgrid = int(std::max<int64_t>(1, std::min<int64_t>((NB + 8 * kQWarps - 1) / (8 * kQWarps), nsm * 16)));
-    k_qfit<<<qgrid, 32 * kQWarps, 0, s>>>(sg, sl, stt, bk, scratch);
+    CK(launch_qfit(false, sg, sl, stt, bk, scratch, nsm, s));
     trace("k_qfit buckets");
     Macros mc{NM, d_mbs, d_bw, d_bgs, W, p, B->t_theta_ext, B->d_ext_flags, B->t_ext_cnt, B->t_ext_l, B->t_ext_micro};
     {
@@ -1269,9 +1363,9 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
         k_ext_prep<<<mblocks, 128, 0, s>>>(rc, bk, gr, ordA, mc, elo, ehi);
         // pooled window fits (model.cpp:171-176): theta_ext straight into the table
         Buckets ext{NM, elo, ehi, B->t_theta_ext, nullptr, nullptr, edeg};
-        const int egrid = int(std::max<int64_t>(1, std::min<int64_t>((NM + 8 * kQWarps - 1) / (8 * kQWarps), nsm * 16)));
-        k_qfit<<<egrid, 32 * kQWarps, 0, s>>>(sg, sl, stt, ext, scratch);
-        k_ext_vote<<<mblocks, 128, 0, s>>>(rc, gr, ordA, mc, elo, ehi, edeg);
+        CK(launch_qfit(true, sg, sl, stt, ext, scratch, nsm, s));
+        k_ext_vote<<<int((NM + kVoteWarps - 1) / kVoteWarps), 32 * kVoteWarps, 0, s>>>(rc, gr, ordA, mc, elo, ehi,
+                                                                                       edeg);
     }
     trace("extrapolation");
     {
@@ -1300,8 +1394,7 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
             return WT_CUDA_ERROR;
         }
         Buckets lin{NM, d_mslo, d_mshi, B->b_lin, B->b_lin_r2, B->b_lin_mape, B->b_lin_deg};
-        k_qfit<<<int(std::max<int64_t>(1, std::min<int64_t>((NM + 31) / 32, nsm * 16))), 32 * kQWarps, 0, s>>>(
-            sg, sl, stt, lin, scratch);
+        CK(launch_qfit(true, sg, sl, stt, lin, scratch, nsm, s));
         static const bool serial = std::getenv("WT_STEP_SERIAL") != nullptr;
         if (serial) {
             k_step<<<int((NM + 127) / 128), 128, 0, s>>>(NM, d_mbs, d_bgs, gw, gl, soff, gr.nsamp, stt, B->b_step_l,
@@ -1657,7 +1750,7 @@ wt_status wt_fit_bucket_batch(const double* g, const double* l, const double* t,
     CK(cudaMemcpy(hi, hhi.data(), nb * 8, cudaMemcpyHostToDevice));
     Buckets bk{nb, lo, hi, dalloc<double>(owned, nb * 4), dalloc<double>(owned, nb), dalloc<double>(owned, nb),
                dalloc<int32_t>(owned, nb)};
-    k_qfit<<<int(std::min<int64_t>((nb + 31) / 32, 148 * 16)), 32 * kQWarps>>>(dg, dl, dt, bk, scr);
+    launch_qfit(false, dg, dl, dt, bk, scr, wtb::device_sms(), nullptr);
     CK(cudaGetLastError());
     CK(cudaMemcpy(coeffs, bk.coeff, nb * 32, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(r2, bk.r2, nb * 8, cudaMemcpyDeviceToHost));

@@ -178,7 +178,9 @@ def test_gemm_family_symbols_and_registry(core):
     assert not [s for s in decl if not hasattr(lib, s)]
     fam = gemm.family()
     assert len(fam) == lib.wt_gemm_family_size() >= 10
-    assert all(bk == 64 and bm in (128, 256) for bm, bn, bk, st in fam)
+    # swap-AB small-M tiles (BM 32 / 64), 1-SM (128) and CTA-pair (256) tiles; whole 64-element swizzle atoms
+    assert all(bk in (64, 128) and bm in (32, 64, 128, 256) for bm, bn, bk, st in fam)
+    assert {bm for bm, *_ in fam} == {32, 64, 128, 256} and {bk for _, _, bk, _ in fam} == {64, 128}
     reg = core.gemm_registry()
     assert len(reg.feasible) == 4 * len(fam)
     for ma, mi in reg.feasible:

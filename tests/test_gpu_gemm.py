@@ -39,7 +39,10 @@ def _check(out, a, b):
     assert bad == 0, f"{bad} elements out of tolerance; max err {err.max().item():.4g}"
 
 
-@pytest.mark.parametrize("shape", [(512, 1024, 512), (333, 264, 200), (1, 8, 64), (1000, 4104, 1096)])
+# (24, 1024, 2048) and (40, 2056, 1024): decode-sized M -> the swap-AB tiles
+# split K (fp32 partials reduced in slice order by the last slice)
+@pytest.mark.parametrize("shape", [(512, 1024, 512), (333, 264, 200), (1, 8, 64), (1000, 4104, 1096),
+                                   (24, 1024, 2048), (40, 2056, 1024)])
 def test_family_numerics(gm, shape):
     M, N, K = shape
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
@@ -53,15 +56,18 @@ def test_family_numerics(gm, shape):
             _check(out, a, b)
 
 
-def test_family_bitwise_deterministic(gm):
+@pytest.mark.parametrize("M", [768, 24])
+def test_family_bitwise_deterministic(gm, M):
     """Same instantiation, same operands -> the same bits; swizzle only
-    reorders tiles, so it cannot change any output element either."""
-    a = torch.randn(768, 1024, device="cuda").bfloat16()
+    reorders tiles, so it cannot change any output element either (M = 24:
+    split-K, whose slices are summed in slice order whichever finishes last)."""
+    a = torch.randn(M, 1024, device="cuda").bfloat16()
     b = torch.randn(1536, 1024, device="cuda").bfloat16()
     for cfg in range(len(gm.family())):
         base = gm.matmul(a, b, cfg, 1)
         for swz in gm.SWIZZLES[1:]:
             assert torch.equal(gm.matmul(a, b, cfg, swz), base)
+        assert torch.equal(gm.matmul(a, b, cfg, 1), base)
 
 
 def test_measurement_entry_points(gm):

@@ -21,7 +21,7 @@
 
 #include <type_traits>
 
-#include "wt_gemm.h"
+#include "wt_gemm.h"  // paper_2604_10187_b200/csrc/gemm
 
 namespace wtb::gemm {
 

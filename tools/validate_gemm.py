@@ -47,6 +47,48 @@ def cublas_us(M, N, K, warmup, reps):
     return e0.elapsed_time(e1) * 1000.0 / reps
 
 
+def cutlass_xcheck_lib():
+    """tools/bin/libwtgemm_cutlass.so (make -C tools cutlass): the same C-ABI
+    over CUTLASS 4.5 sm100 collectives -- a cross-check of the hand-written
+    family's speed, never the product."""
+    import ctypes as C
+
+    p = os.path.join(ROOT, "tools", "bin", "libwtgemm_cutlass.so")
+    if not os.path.exists(p):
+        return None
+    L = C.CDLL(p)
+    i32p = C.POINTER(C.c_int32)
+    L.wt_gemm_family_size.restype = C.c_int
+    L.wt_gemm_config.argtypes = [C.c_int] + [C.POINTER(C.c_int)] * 4
+    L.wt_gemm_measure_batch.argtypes = [C.c_int] + [i32p] * 5 + [C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_double)]
+    return L
+
+
+def xcheck_best_us(L, M, N, K, warmup, reps):
+    """Fastest CUTLASS instantiation x swizzle on one shape (us) and its label."""
+    import ctypes as C
+
+    n = L.wt_gemm_family_size()
+    cfgs, labels = [], []
+    for c in range(n):
+        v = [C.c_int() for _ in range(4)]
+        L.wt_gemm_config(c, *[C.byref(x) for x in v])
+        for s in (1, 2, 4, 8):
+            cfgs.append((c, s))
+            labels.append(f"{v[0].value}x{v[1].value}x{v[2].value}/s{v[3].value}/w{s}")
+    arr = [np.ascontiguousarray(x, dtype=np.int32) for x in
+           ([c for c, _ in cfgs], [s for _, s in cfgs], [M] * len(cfgs), [N] * len(cfgs), [K] * len(cfgs))]
+    out = np.empty(len(cfgs), dtype=np.float64)
+    p = lambda a: a.ctypes.data_as(C.POINTER(C.c_int32))
+    rc = L.wt_gemm_measure_batch(len(cfgs), *[p(a) for a in arr], warmup, reps, 3,
+                                 out.ctypes.data_as(C.POINTER(C.c_double)))
+    if rc != 0:
+        return None, None
+    out[out <= 0] = np.inf
+    i = int(np.argmin(out))
+    return float(out[i]), labels[i]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--W", type=int, default=24)
@@ -55,12 +97,14 @@ def main():
     ap.add_argument("--anchors", default="16,64,128,224")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--no-xcheck", action="store_true", help="skip the CUTLASS cross-check timings")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "gemm_validation.json"))
     args = ap.parse_args()
 
     import torch
     from paper_2604_10187_b200 import _core as wt
 
+    xlib = cutlass_xcheck_lib() if not args.no_xcheck else None
     n_sm = torch.cuda.get_device_properties(0).multi_processor_count
     hw = wt.HardwareSpec(n_sm, 1, "b200")
     reg = wt.gemm_registry()
@@ -112,6 +156,7 @@ def main():
                 "oracle": (best, None),
                 "default": ((d_macro, d_micro), None),
             }
+            xc_us, xc_cfg = xcheck_best_us(xlib, M, N, K, args.warmup, args.reps) if xlib else (None, None)
             rows.append({
                 "methods": {k: {"config": label(*c), "measured_us": t_all[c], "predicted_us": pr}
                             for k, (c, pr) in methods.items()},
@@ -121,11 +166,13 @@ def main():
                 "extrapolated": bool(d.regime.extrapolated), "decide_us_host": t_decide,
                 "all_us": {label(*k): v for k, v in t_all.items()},
                 "cublas_us": cublas_us(M, N, K, args.warmup, args.reps),
+                "cutlass_best_us": xc_us, "cutlass_best": xc_cfg,
             })
             r = rows[-1]
             print(f"{layer:8s} M={M:6d}: oracle {r['oracle']:22s} {r['oracle_us']:9.1f} us | wavetune "
                   f"{r['wavetune']:22s} {r['wavetune_us']:9.1f} us (pred {r['predicted_us']:9.1f}) | "
-                  f"cuBLAS {r['cublas_us']:9.1f} us", flush=True)
+                  f"cuBLAS {r['cublas_us']:9.1f} us" + (f" | CUTLASS best {xc_us:9.1f} us" if xc_us else ""),
+                  flush=True)
 
     # eval.cpp:106-116: geomean speedup over the default heuristic, MAPE of
     # each method's predicted latency against the measured one
@@ -183,6 +230,12 @@ def main():
         "best_static": best_static,
         "wavetune_vs_cublas_geomean": geomean([r["cublas_us"] / r["wavetune_us"] for r in rows]),
         "oracle_vs_cublas_geomean": geomean([r["cublas_us"] / r["oracle_us"] for r in rows]),
+        "family_best_vs_cutlass_best_geomean": (geomean([r["cutlass_best_us"] / r["oracle_us"] for r in rows])
+                                                if all(r["cutlass_best_us"] for r in rows) else None),
+        "wavetune_vs_cutlass_best_geomean": (geomean([r["cutlass_best_us"] / r["wavetune_us"] for r in rows])
+                                             if all(r["cutlass_best_us"] for r in rows) else None),
+        "family_best_ge_cutlass_best_shapes": (int(sum(r["oracle_us"] <= r["cutlass_best_us"] * 1.0 for r in rows))
+                                               if all(r["cutlass_best_us"] for r in rows) else None),
         "decide_us_host_median": float(np.median([r["decide_us_host"] for r in rows])),
         "prediction_mape": float(np.mean([abs(r["predicted_us"] - r["wavetune_us"]) / r["wavetune_us"]
                                           for r in rows])),
