@@ -19,12 +19,14 @@
  * Reduction order.  Eigen's vectorised reductions have a build-dependent
  * association order, so bitwise parity with a real Eigen build is UNPINNED
  * (pinned only to 1e-9 by the reference's golden fits, test_model.cpp:23-61,
- * acceptance.cpp:313-323).  This restatement fixes ONE order that the GPU fit
- * kernel reproduces exactly: every sum over rows r in [r0, n) is a plain
- * ascending accumulation starting from +0.0 (products rounded first).  That
- * is what one lane computes when it owns a column of the least-squares
- * problem (the GPU fit gives each problem 4 lanes, one per design column),
- * so CPU and GPU agree bit for bit.
+ * acceptance.cpp:313-323).  This restatement fixes ONE order per problem
+ * size that the GPU fit kernels reproduce exactly (products rounded first,
+ * sums from +0.0): problems of <= 32 rows -- every (macro, wave) bucket --
+ * reduce rows in plain ascending order (one GPU lane per design column);
+ * larger problems (extrapolation windows, per-macro baselines) reduce the
+ * QR's dot products as eight interleaved ascending partials in a fixed tree
+ * (wtf_qsum; 8 GPU lanes per design column).  Diagnostics (R^2, MAPE) stay
+ * ascending.  CPU and GPU agree bit for bit.
  * All arithmetic is IEEE binary64 with no contraction (-ffp-contract=off).
  */
 #ifndef WT_FIT_CORE_H
@@ -42,10 +44,25 @@ static inline double wtf_sum(const double* v, int r0, int n) {
     return p;
 }
 
-/* dot(a[r0..n), b[r0..n)) with products rounded first. */
+/* Row sum of the QR's reductions over [r0, n) of an n-row problem.
+ * n <= 32: ascending (one GPU lane per design column).  n > 32: eight
+ * interleaved ascending partials p_j over the rows r = j (mod 8), combined
+ * as ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)) -- the GPU gives such problems a
+ * warp, 8 lanes per column (k_ofit). */
+static inline double wtf_qsum(const double* v, int r0, int n) {
+    if (n <= 32) return wtf_sum(v, r0, n);
+    double p[8];
+    for (int j = 0; j < 8; ++j) {
+        p[j] = 0.0;
+        for (int r = r0 + ((j - r0 % 8) % 8 + 8) % 8; r < n; r += 8) p[j] = p[j] + v[r];
+    }
+    return ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+}
+
+/* dot(a[r0..n), b[r0..n)) with products rounded first (n = problem rows). */
 static inline double wtf_dot(const double* a, const double* b, int r0, int n, double* scratch) {
     for (int r = r0; r < n; ++r) scratch[r] = a[r] * b[r];
-    return wtf_sum(scratch, r0, n);
+    return wtf_qsum(scratch, r0, n);
 }
 
 /* Householder reflector for x = col[k..n): Eigen makeHouseholderInPlace.

@@ -32,6 +32,10 @@
 //                  even when the GEMM's M is tiny; the epilogue writes the
 //                  transposed accumulator (lanes = n, columns = m).
 //   BK = 128       two 64-element swizzle atoms per stage.
+// TMA multicast (runtime, single-CTA tiles): clusters of 2 / 4 CTAs on
+// neighbouring n-blocks of one m-block load the shared operand once (each CTA
+// 1/mc of its rows, .multicast::cluster to all); commits release ring slots
+// in every CTA of the cluster, a producer tail drains them before exit.
 // Tile order: persistent CTAs (clusters) stride the tile list; tile index ->
 // (m block, n block) goes through a raster swizzle of `swizzle` m-blocks per
 // group (L2 reuse of B across neighbouring CTAs), a runtime knob.
@@ -56,6 +60,14 @@ struct Params {
     int splits;
     float* ws;
     int* cnt;
+    long long* trace;  // debug (WT_GEMM_TRACE): CTA 0's per-k-block clocks, else null
+    // TMA multicast (single-CTA tiles): clusters of `mc` CTAs take `mc`
+    // consecutive n-blocks of one m-block; the operand they share (A, or the
+    // activations of a swap-AB tile) is loaded once per cluster, each CTA
+    // fetching 1/mc of its rows and multicasting them to all; tiles counts
+    // cluster tiles (m_blocks x n_groups)
+    int mc, n_groups;
+    int nomma;  // debug (WT_GEMM_NOMMA): stream operands without issuing MMAs (timing experiments)
 };
 
 // ------------------------------------------------------------------ PTX
@@ -76,13 +88,15 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// the suspend-time hint parks the waiting thread in hardware until the
+// phase completes (no spin loop competing for issue slots)
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
-        "r"(parity)
+        "r"(parity), "r"(0x989680u)
         : "memory");
 }
 // arrive on the barrier at the same offset in CTA `rank` of the cluster
@@ -115,6 +129,17 @@ __device__ __forceinline__ void tma_load(const CUtensorMap* m, uint32_t dst, uin
             "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(x), "r"(y)
             : "memory");
     }
+}
+
+// multicast form: the box lands at the same offset in every CTA of `mask`,
+// completing bytes on the barrier at `bar`'s offset in each of them
+__device__ __forceinline__ void tma_load_mc(const CUtensorMap* m, uint32_t dst, uint32_t bar, int x, int y,
+                                            uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(x), "r"(y), "h"(mask)
+        : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -157,12 +182,21 @@ __device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_
             : "memory");
 }
 // completion of every prior MMA of this thread -> one arrive on `bar`
-// (CTA pair: on the barrier at that offset in both CTAs)
+// (CTA pair: on the barrier at that offset in both CTAs; mask != 0: in every
+// CTA of the multicast cluster)
 template <int CG>
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-    if constexpr (CG == 1)
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                     : "memory");
+__device__ __forceinline__ void umma_commit(uint32_t bar, uint16_t mask = 0) {
+    if constexpr (CG == 1) {
+        if (mask)
+            asm volatile(
+                "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::
+                    "r"(bar),
+                "h"(mask)
+                : "memory");
+        else
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                         : "memory");
+    }
     else
         asm volatile(
             "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -204,15 +238,16 @@ __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
     return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// tile index -> (m block, n block): groups of `sw` m-blocks walk n
-__device__ __forceinline__ void raster(int t, const Params& p, int* mb, int* nb) {
+// cluster tile index -> (m block, n block of multicast rank `crank`):
+// groups of `sw` m-blocks walk the n groups
+__device__ __forceinline__ void raster(int t, const Params& p, int crank, int* mb, int* nb) {
     const int sw = p.swizzle;
-    const int per = sw * p.n_blocks;
+    const int per = sw * p.n_groups;
     const int g = t / per, r = t - g * per;
     const int m0 = g * sw;
     const int gw = min(sw, p.m_blocks - m0);
     *mb = m0 + r % gw;
-    *nb = r / gw;
+    *nb = (r / gw) * p.mc + crank;
 }
 
 template <int BM, int BN, int BK, int ST, bool SWAP>
@@ -252,8 +287,12 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+    const int mc = CG == 1 ? p.mc : 1;
+    const bool clustered = CG == 2 || mc > 1;
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;           // CTA of the pair
+    const int crank = (CG == 1 && mc > 1) ? int(cluster_rank()) : 0;  // CTA of the multicast cluster
     const bool leader = rank == 0;
+    const uint16_t mc_mask = mc > 1 ? uint16_t((1u << mc) - 1u) : uint16_t(0);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
@@ -262,7 +301,7 @@ __global__ void __launch_bounds__(192, 1)
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < ST; ++s) {
             mbar_init(full0 + 8 * s, 1);
-            mbar_init(empty0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, uint32_t(mc));  // every consumer of the cluster frees the slot
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(tfull0 + 8 * s, 1);
@@ -272,15 +311,15 @@ __global__ void __launch_bounds__(192, 1)
     }
     if (warp == 2) tmem_alloc<CG>(smem_u32(tmem_slot), S::TMEM_COLS);
     tc_fence_before();
-    if constexpr (CG == 2)
+    if (clustered)
         cluster_sync();
     else
         __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    const int nclusters = gridDim.x / CG;
-    const int cid = blockIdx.x / CG;
+    const int nclusters = gridDim.x / (CG * mc);
+    const int cid = blockIdx.x / (CG * mc);
 
     if (warp == 0) {
         // ===== TMA producer
@@ -290,7 +329,7 @@ __global__ void __launch_bounds__(192, 1)
             for (int u = cid; u < p.tiles * p.splits; u += nclusters) {
                 const int t = u / p.splits, sl = u - t * p.splits;
                 int mb, nb;
-                raster(t, p, &mb, &nb);
+                raster(t, p, crank, &mb, &nb);
                 const int kb0 = int((long long)sl * p.k_blocks / p.splits);
                 const int kb1 = int((long long)(sl + 1) * p.k_blocks / p.splits);
                 // M-slot operand rows / N-slot operand rows of this CTA
@@ -300,6 +339,7 @@ __global__ void __launch_bounds__(192, 1)
                 const CUtensorMap* tb = SWAP ? &tmA : &tmB;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(empty0 + 8 * stage, phase ^ 1u);
+                    if (p.trace && blockIdx.x == 0 && u == cid && kb - kb0 < 512) p.trace[kb - kb0] = clock64();
                     const uint32_t fb = full0 + 8 * stage;
                     if (leader) mbar_expect_tx(fb, uint32_t(S::STAGE_BYTES * CG));
                     const uint32_t sa = smem_u32(ring + stage * S::STAGE_BYTES);
@@ -307,13 +347,37 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                     for (int j = 0; j < S::ATOMS; ++j) {
                         const int k0 = kb * BK + 64 * j;
-                        tma_load<CG == 2>(ta, sa + j * (S::A_ROWS * 128), fb, k0, ra);
-                        tma_load<CG == 2>(tb, sb + j * (S::B_ROWS * 128), fb, k0, rb);
+                        if (mc > 1) {
+                            // the m-block's operand: this CTA's 1/mc of its rows, to every CTA
+                            if constexpr (!SWAP) {
+                                const int sr = S::A_ROWS / mc;
+                                tma_load_mc(ta, sa + j * (S::A_ROWS * 128) + crank * sr * 128, fb, k0,
+                                            ra + crank * sr, mc_mask);
+                                tma_load<false>(tb, sb + j * (S::B_ROWS * 128), fb, k0, rb);
+                            } else {
+                                const int sr = S::B_ROWS / mc;
+                                tma_load<false>(ta, sa + j * (S::A_ROWS * 128), fb, k0, ra);
+                                tma_load_mc(tb, sb + j * (S::B_ROWS * 128) + crank * sr * 128, fb, k0,
+                                            rb + crank * sr, mc_mask);
+                            }
+                        } else {
+                            tma_load<CG == 2>(ta, sa + j * (S::A_ROWS * 128), fb, k0, ra);
+                            tma_load<CG == 2>(tb, sb + j * (S::B_ROWS * 128), fb, k0, rb);
+                        }
                     }
                     if (++stage == ST) {
                         stage = 0;
                         phase ^= 1u;
                     }
+                }
+            }
+            // producer tail: every slot released by every consumer of the
+            // cluster before this CTA may exit (peers' commits target our barriers)
+            for (int i = 0; i < ST; ++i) {
+                mbar_wait(empty0 + 8 * stage, phase ^ 1u);
+                if (++stage == ST) {
+                    stage = 0;
+                    phase ^= 1u;
                 }
             }
         }
@@ -335,6 +399,7 @@ __global__ void __launch_bounds__(192, 1)
                 const uint32_t d = tmem + uint32_t(acc * S::UN);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(full0 + 8 * stage, phase);
+                    if (p.trace && blockIdx.x == 0 && u == cid && kb - kb0 < 512) p.trace[512 + kb - kb0] = clock64();
                     tc_fence_after();
                     const uint32_t sa = smem_u32(ring + stage * S::STAGE_BYTES);
                     const uint32_t sb = sa + S::A_BYTES;
@@ -343,9 +408,9 @@ __global__ void __launch_bounds__(192, 1)
                         const int j = k >> 2, kk = k & 3;
                         const uint64_t ad = sdesc(sa + j * (S::A_ROWS * 128) + kk * 32);
                         const uint64_t bd = sdesc(sb + j * (S::B_ROWS * 128) + kk * 32);
-                        umma<CG>(d, ad, bd, idesc, ((kb - kb0) | k) != 0);
+                        if (!p.nomma) umma<CG>(d, ad, bd, idesc, ((kb - kb0) | k) != 0);
                     }
-                    umma_commit<CG>(empty0 + 8 * stage);
+                    umma_commit<CG>(empty0 + 8 * stage, mc_mask);
                     if (++stage == ST) {
                         stage = 0;
                         phase ^= 1u;
@@ -393,7 +458,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int u = cid; u < p.tiles * p.splits; u += nclusters, ++it) {
             const int t = u / p.splits;
             int mb, nb;
-            raster(t, p, &mb, &nb);
+            raster(t, p, crank, &mb, &nb);
             const int acc = it & 1;
             mbar_wait(tfull0 + 8 * acc, uint32_t(it >> 1) & 1u);
             tc_fence_after();
@@ -409,7 +474,7 @@ __global__ void __launch_bounds__(192, 1)
                     store(f, mb, nb, c);
                 }
             } else {
-                float* mine = p.ws + ((size_t(u) * CG + rank) * 128 + row) * S::UN;
+                float* mine = p.ws + (((size_t(u) * mc + crank) * CG + rank) * 128 + row) * S::UN;
 #pragma unroll 1
                 for (int c = 0; c < S::UN; c += 32) {
                     uint32_t v[32];
@@ -431,7 +496,7 @@ __global__ void __launch_bounds__(192, 1)
             if (p.splits > 1) {
                 __threadfence();
                 asm volatile("bar.sync 1, 128;" ::: "memory");
-                int* ctr = p.cnt + size_t(t) * CG + rank;
+                int* ctr = p.cnt + (size_t(t) * mc + crank) * CG + rank;
                 if (threadIdx.x == 64) last_flag = atomicAdd(ctr, 1) == p.splits - 1;
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 if (last_flag) {
@@ -443,7 +508,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
                         for (int sl = 0; sl < p.splits; ++sl) {
                             const float4* src = reinterpret_cast<const float4*>(
-                                p.ws + (((u0 + sl) * CG + rank) * 128 + row) * S::UN + c);
+                                p.ws + ((((u0 + sl) * mc + crank) * CG + rank) * 128 + row) * S::UN + c);
 #pragma unroll
                             for (int g = 0; g < 8; ++g) {
                                 const float4 x = __ldcg(src + g);
@@ -464,7 +529,7 @@ __global__ void __launch_bounds__(192, 1)
     }
 
     tc_fence_before();
-    if constexpr (CG == 2)
+    if (clustered)
         cluster_sync();
     else
         __syncthreads();

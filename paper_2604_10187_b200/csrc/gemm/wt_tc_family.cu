@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -83,10 +84,6 @@ int run_tc(const RunArgs& r, int warmup, int reps, cudaEvent_t e0, cudaEvent_t e
     if (r.K % 8 || r.N % 8 || r.M <= 0 || r.N <= 0 || r.K <= 0) return 1;
     if ((reinterpret_cast<uintptr_t>(r.A) | reinterpret_cast<uintptr_t>(r.B) | reinterpret_cast<uintptr_t>(r.C)) & 15)
         return 1;
-    CUtensorMap ta, tb;
-    const int a_rows = SWAP ? S::B_ROWS : S::A_ROWS;  // A = activations: N slot when swapped
-    const int b_rows = SWAP ? S::A_ROWS : S::B_ROWS;
-    if (!make_map(&ta, r.A, r.M, r.K, a_rows) || !make_map(&tb, r.B, r.N, r.K, b_rows)) return 2;
     tc::Params p{};
     p.M = r.M;
     p.N = r.N;
@@ -95,26 +92,53 @@ int run_tc(const RunArgs& r, int warmup, int reps, cudaEvent_t e0, cudaEvent_t e
     p.m_blocks = (r.M + BM - 1) / BM;
     p.n_blocks = (r.N + BN - 1) / BN;
     p.k_blocks = (r.K + BK - 1) / BK;
-    p.tiles = p.m_blocks * p.n_blocks;
+    // multicast cluster of the single-CTA tiles (WT_GEMM_MC = 2 / 4): CTAs on
+    // consecutive n-blocks share one load of the m-block's operand.  Off by
+    // default: measured on B200 it does not pay here (r02 probe: 128x4096x4096
+    // 25.1 -> 26.9 us, 4096^3 on 128x256 tiles 108 -> 156 us) -- L2 request
+    // volume is not what bounds these tiles.
+    p.mc = 1;
+    if (S::CG == 1) {
+        static const int mc_env = env_int("WT_GEMM_MC", 1);
+        const int want = mc_env;
+        p.mc = want >= 4 && p.n_blocks >= 4 ? 4 : want >= 2 && p.n_blocks >= 2 ? 2 : 1;
+    }
+    p.n_groups = (p.n_blocks + p.mc - 1) / p.mc;
+    p.tiles = p.m_blocks * p.n_groups;
     p.swizzle = std::max(1, r.swizzle);
+    CUtensorMap ta, tb;
+    // A = activations (M slot; N slot when swapped); the shared operand's box
+    // is the multicast slice
+    const int a_rows = SWAP ? S::B_ROWS : S::A_ROWS / p.mc;
+    const int b_rows = SWAP ? S::A_ROWS : S::B_ROWS;
+    const int a_box = SWAP ? a_rows / p.mc : a_rows;
+    if (!make_map(&ta, r.A, r.M, r.K, a_box) || !make_map(&tb, r.B, r.N, r.K, b_rows)) return 2;
     // split-K for the small-M (swap-AB) tiles when they leave more than half
     // of the SMs idle: slices of >= 4 k-blocks, at most one unit per SM, and
     // at most 64 KB of fp32 partials for the last slice to reduce (measured:
     // with 128-column accumulators the serial reduction costs more than the
     // extra SMs gain, so the wide tiles never split).  WT_GEMM_SPLITK=0: off.
-    const int avail = device_sms() / S::CG;
+    const int avail = device_sms() / (S::CG * p.mc);
     p.splits = 1;
     if (SWAP && splitk_enabled() && 2 * p.tiles <= avail)
         p.splits = std::max(1, std::min({avail / p.tiles, p.k_blocks / 4, (64 << 10) / (128 * S::UN * 4)}));
     if (p.splits > 1) {
-        const size_t need = kCounterBytes + size_t(p.tiles) * p.splits * S::CG * 128 * S::UN * 4;
-        if (!r.workspace || need > r.workspace_bytes || size_t(p.tiles) * S::CG * 4 > kCounterBytes)
+        // partial slots / counters per CTA tile (cluster tiles x mc)
+        const size_t ctas = size_t(p.tiles) * p.mc;
+        const size_t need = kCounterBytes + ctas * p.splits * S::CG * 128 * S::UN * 4;
+        if (!r.workspace || need > r.workspace_bytes || ctas * S::CG * 4 > kCounterBytes)
             p.splits = 1;
         else {
             p.cnt = static_cast<int*>(r.workspace);
             p.ws = reinterpret_cast<float*>(static_cast<char*>(r.workspace) + kCounterBytes);
         }
     }
+    static long long* trace_buf = nullptr;
+    if (env_int("WT_GEMM_TRACE", 0)) {
+        if (!trace_buf) cudaMalloc(&trace_buf, 1024 * sizeof(long long));
+        p.trace = trace_buf;
+    }
+    p.nomma = env_int("WT_GEMM_NOMMA", 0);
     auto kern = tc::k_tc_gemm<BM, BN, BK, ST, SWAP>;
     static bool attr_set[64] = {};
     int dev = 0;
@@ -124,22 +148,34 @@ int run_tc(const RunArgs& r, int warmup, int reps, cudaEvent_t e0, cudaEvent_t e
             return 2;
         attr_set[dev] = true;
     }
-    const int clusters = std::min(p.tiles * p.splits, avail);
+    static const bool nonpersist = env_int("WT_GEMM_NONPERSIST", 0) != 0;  // A/B: one tile per cluster
+    const int clusters = nonpersist ? p.tiles * p.splits : std::min(p.tiles * p.splits, avail);
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned(clusters * S::CG));
+    cfg.gridDim = dim3(unsigned(clusters * S::CG * p.mc));
     cfg.blockDim = dim3(S::THREADS);
     cfg.dynamicSmemBytes = S::SMEM;
     cfg.stream = static_cast<cudaStream_t>(r.stream);
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = S::CG;
+    at[0].val.clusterDim.x = S::CG * p.mc;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     static const bool nocluster = env_int("WT_GEMM_NOCLUSTER", 0) != 0;
-    cfg.numAttrs = (S::CG == 1 && nocluster) ? 0 : 1;
+    cfg.numAttrs = (S::CG == 1 && p.mc == 1 && nocluster) ? 0 : 1;
     auto launch = [&]() { return cudaLaunchKernelEx(&cfg, kern, ta, tb, p) == cudaSuccess; };
-    if (reps == 0) return launch() ? 0 : 3;
+    if (reps == 0) {
+        const bool ok = launch();
+        if (p.trace) {  // debug: CTA 0's producer issue / MMA full-wait clocks per k-block
+            long long h[1024];
+            cudaMemcpy(h, p.trace, sizeof(h), cudaMemcpyDeviceToHost);
+            const int nk = std::min(p.k_blocks / p.splits, 512);
+            for (int k = 0; k < nk; ++k)
+                std::fprintf(stderr, "kb %3d issue %8lld full %8lld lat %6lld\n", k, h[k] - h[0], h[512 + k] - h[0],
+                             h[512 + k] - h[k]);
+        }
+        return ok ? 0 : 3;
+    }
     for (int i = 0; i < warmup; ++i)
         if (!launch()) return 3;
     cudaEventRecord(e0, cfg.stream);

@@ -310,8 +310,10 @@ wt_status engine_build(wt_engine* e, const ImagePlan& P, const DevTables& T, cud
                  o_am = ar.take(size_t(n_pool) * 4), o_th2 = ar.take(C * R * 32), o_m2 = ar.take(C * R * 4),
                  o_th2t = ar.take(C * R * 32), o_m2t = ar.take(C * R * 4), o_smask = ar.take(NS * R * kLB * 4),
                  o_sor = ar.take(NS * R * 4), o_spec = ar.take(4);
-    cudaError_t ce = cudaMalloc(&e->mem, ar.used);
-    if (ce != cudaSuccess) return cuda_err(ce, "wt_engine_create: cudaMalloc");
+    // stream-ordered from the library pool (retained across engines: a
+    // rebuild costs no cudaMalloc); ordered before the image kernels on s
+    cudaError_t ce = cudaMallocFromPoolAsync(&e->mem, ar.used, lib_pool(e->device), s);
+    if (ce != cudaSuccess) return cuda_err(ce, "wt_engine_create: allocation");
     e->bytes = ar.used;
     char* base = static_cast<char*>(e->mem);
     std::vector<char> stage(plan_bytes, 0);
@@ -512,7 +514,10 @@ wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc*
     const wt_status bs = engine_build(e, P, T, s);
     cudaFreeAsync(tmp, s);
     if (bs != WT_OK) {
-        if (e->mem) cudaFree(e->mem);
+        if (e->mem) {
+            cudaStreamSynchronize(s);
+            cudaFreeAsync(e->mem, s);
+        }
         delete e;
         return bs;
     }
@@ -545,7 +550,10 @@ wt_status wt_engine_create_from_build(const wt_build* b, const wt_registry_desc*
     e->device = bt.device;
     const wt_status bs = engine_build(e, P, T, static_cast<cudaStream_t>(stream));
     if (bs != WT_OK) {
-        if (e->mem) cudaFree(e->mem);
+        if (e->mem) {
+            cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+            cudaFreeAsync(e->mem, static_cast<cudaStream_t>(stream));
+        }
         delete e;
         return bs;
     }
@@ -560,7 +568,11 @@ wt_status wt_engine_destroy(wt_engine* e) {
     if (e->one_st) cudaStreamDestroy(e->one_st);
     if (e->one_h) cudaFreeHost(e->one_h);
     if (e->mb_h) cudaFreeHost(e->mb_h);
-    cudaFree(e->mem);
+    // pool memory: free after every stream's use of the engine (the
+    // cudaFree this replaces synchronised the device too)
+    cudaDeviceSynchronize();
+    cudaFreeAsync(e->mem, nullptr);
+    cudaStreamSynchronize(nullptr);
     delete e;
     return WT_OK;
 }

@@ -61,46 +61,88 @@ constexpr unsigned FULL = 0xffffffffu;
 // global scratch (5 doubles per sample, la = 4).
 constexpr double kEps = DBL_EPSILON;
 
-__device__ __forceinline__ double qb(double v, int src, unsigned m) { return __shfl_sync(m, v, src, 4); }
-__device__ __forceinline__ int qbi(int v, int src, unsigned m) { return __shfl_sync(m, v, src, 4); }
+// Lane groups.  A problem is solved by 4*SUB lanes: column owner q (0..3)
+// holds sub-lanes j = 0..SUB-1.  SUB = 1 (problems of <= 32 rows: buckets):
+// every row reduction is one lane's ascending accumulation.  SUB = 8 (larger
+// problems: extrapolation windows, per-macro baselines): sub-lane j owns the
+// rows r = j (mod 8), accumulates them in ascending order, and the eight
+// partials combine as ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)) (xor butterfly --
+// exact, since each add is commutative).  oracle/wt_fit_core.h (wtf_dot /
+// wtf_qsum) fixes the same two orders by problem size, so GPU and CPU agree
+// bit for bit.  Elementwise row updates are split the same way.
+template <int SUB>
+struct Grp {
+    int q, j;     // column owner, sub-lane
+    unsigned m;   // the problem's lanes
+    unsigned mo;  // the owner's sub-lanes (reductions)
+    // broadcast from lane `src` of the group
+    __device__ __forceinline__ double bc(double v, int src) const { return __shfl_sync(m, v, src, 4 * SUB); }
+    __device__ __forceinline__ double own(double v, int col) const { return bc(v, col * SUB + j); }
+    __device__ __forceinline__ double red(double p) const {
+        if constexpr (SUB > 1) {
+            p = __dadd_rn(p, __shfl_xor_sync(mo, p, 1));
+            p = __dadd_rn(p, __shfl_xor_sync(mo, p, 2));
+            p = __dadd_rn(p, __shfl_xor_sync(mo, p, 4));
+        }
+        return p;
+    }
+    __device__ __forceinline__ void sync() const { __syncwarp(m); }
+    __device__ __forceinline__ void sync_own() const {
+        if constexpr (SUB > 1) __syncwarp(mo);
+    }
+    // first row >= r0 of this sub-lane
+    __device__ __forceinline__ int first(int r0) const {
+        if constexpr (SUB == 1) return r0;
+        return r0 + ((j - r0 % SUB) % SUB + SUB) % SUB;
+    }
+};
 
 // design column c of sample r (model.cpp:24-32): g*l, g, l, 1
 __device__ __forceinline__ double dcol(const double* g, const double* l, int c, int r) {
     return c == 0 ? __dmul_rn(g[r], l[r]) : c == 1 ? g[r] : c == 2 ? l[r] : 1.0;
 }
 
-// Householder reflector on rows [k, n) of column `col` (stride la):
-// makeHouseholderInPlace (wtf_house).  Returns tau; *beta = new diagonal.
-__device__ double q_house(double* col, int la, int k, int n, double* beta) {
+// Householder reflector on rows [k, n) of column `col` (stride la), by the
+// column owner's sub-lanes: makeHouseholderInPlace (wtf_house).  Returns tau;
+// *beta = new diagonal (written to col[k] by the caller).
+template <int SUB>
+__device__ double q_house(const Grp<SUB>& G, double* col, int la, int k, int n, double* beta) {
     const double c0 = col[k * la];
     double tailsq = 0.0;
-    if (n - k != 1)
-        for (int r = k + 1; r < n; ++r) tailsq = __dadd_rn(tailsq, __dmul_rn(col[r * la], col[r * la]));
+    if (n - k != 1) {
+        double p = 0.0;
+        for (int r = G.first(k + 1); r < n; r += SUB) p = __dadd_rn(p, __dmul_rn(col[r * la], col[r * la]));
+        tailsq = G.red(p);
+    }
     if (tailsq <= DBL_MIN) {
         *beta = c0;
-        for (int r = k + 1; r < n; ++r) col[r * la] = 0.0;
+        for (int r = G.first(k + 1); r < n; r += SUB) col[r * la] = 0.0;
         return 0.0;
     }
     double b = __dsqrt_rn(__dadd_rn(__dmul_rn(c0, c0), tailsq));
     if (c0 >= 0.0) b = -b;
     const double d = __dadd_rn(c0, -b);
-    for (int r = k + 1; r < n; ++r) col[r * la] = __ddiv_rn(col[r * la], d);
+    for (int r = G.first(k + 1); r < n; r += SUB) col[r * la] = __ddiv_rn(col[r * la], d);
     *beta = b;
     return __ddiv_rn(__dadd_rn(b, -c0), b);
 }
 
-// y[k..n) -= tau v (v . y), v = [1; ess[k+1..n)] (wtf_apply)
-__device__ void q_apply(const double* ess, int le, double tau, double* y, int ly, int k, int n) {
+// y[k..n) -= tau v (v . y), v = [1; ess[k+1..n)] (wtf_apply), by one owner's sub-lanes
+template <int SUB>
+__device__ void q_apply(const Grp<SUB>& G, const double* ess, int le, double tau, double* y, int ly, int k, int n) {
     if (n - k == 1) {
-        y[k * ly] = __dmul_rn(y[k * ly], __dadd_rn(1.0, -tau));
+        if (G.j == 0) y[k * ly] = __dmul_rn(y[k * ly], __dadd_rn(1.0, -tau));
         return;
     }
     if (tau == 0.0) return;
-    double tmp = 0.0;
-    for (int r = k + 1; r < n; ++r) tmp = __dadd_rn(tmp, __dmul_rn(ess[r * le], y[r * ly]));
+    double p = 0.0;
+    for (int r = G.first(k + 1); r < n; r += SUB) p = __dadd_rn(p, __dmul_rn(ess[r * le], y[r * ly]));
+    double tmp = G.red(p);
     tmp = __dadd_rn(tmp, y[k * ly]);
-    y[k * ly] = __dadd_rn(y[k * ly], -__dmul_rn(tau, tmp));
-    for (int r = k + 1; r < n; ++r) y[r * ly] = __dadd_rn(y[r * ly], -__dmul_rn(__dmul_rn(tau, ess[r * le]), tmp));
+    G.sync_own();  // every sub-lane has read y[k]
+    if (G.j == 0) y[k * ly] = __dadd_rn(y[k * ly], -__dmul_rn(tau, tmp));
+    for (int r = G.first(k + 1); r < n; r += SUB)
+        y[r * ly] = __dadd_rn(y[r * ly], -__dmul_rn(__dmul_rn(tau, ess[r * le]), tmp));
 }
 
 // upper back-substitution on rhs[0..m) with R column i at A + slot[i]
@@ -122,32 +164,46 @@ struct FitOut {
     int degenerate;
 };
 
-// One problem per quad: q = lane within the quad, m = the quad's mask.
-__device__ FitOut quad_fit(const double* g, const double* l, const double* t, int n, double* A, int la, double* rhs,
-                           int lr, int q, unsigned m) {
+// One problem per group (4*SUB lanes; lane = q*SUB + j).
+template <int SUB>
+__device__ FitOut group_fit(const double* g, const double* l, const double* t, int n, double* A, int la,
+                            double* rhs, int lr, const Grp<SUB>& G, bool diag) {
+    const int q = G.q, j = G.j;
     // 1. scaled design (model.cpp:36-41), right-hand side = t
-    double mxa = fabs(dcol(g, l, q, 0));
-    for (int r = 1; r < n; ++r) {
+    double mxa = 0.0;
+    bool have = false;
+    for (int r = G.first(0); r < n; r += SUB) {
         const double v = fabs(dcol(g, l, q, r));
-        if (v > mxa) mxa = v;
+        if (!have || v > mxa) mxa = v;
+        have = true;
+    }
+    if constexpr (SUB > 1) {  // max is order-free; design columns are finite
+#pragma unroll
+        for (int o = 1; o < SUB; o <<= 1) {
+            const double u = __shfl_xor_sync(G.mo, mxa, o);
+            const bool uh = __shfl_xor_sync(G.mo, int(have), o) != 0;
+            if (uh && (!have || u > mxa)) mxa = u;
+            have = have || uh;
+        }
     }
     const double sc = mxa > 0 ? mxa : 1.0;
     double nrm = 0.0;
-    for (int r = 0; r < n; ++r) {
+    for (int r = G.first(0); r < n; r += SUB) {
         const double v = __ddiv_rn(dcol(g, l, q, r), sc);
         A[r * la + q] = v;
         nrm = __dadd_rn(nrm, __dmul_rn(v, v));
     }
+    nrm = G.red(nrm);
     if (q == 0)
-        for (int r = 0; r < n; ++r) rhs[r * lr] = t[r];
+        for (int r = G.first(0); r < n; r += SUB) rhs[r * lr] = t[r];
     double scale[4], upd[4], direct[4];
     const double dn = __dsqrt_rn(nrm);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-        scale[c] = qb(sc, c, m);
-        direct[c] = upd[c] = qb(dn, c, m);
+        scale[c] = G.own(sc, c);
+        direct[c] = upd[c] = G.own(dn, c);
     }
-    __syncwarp(m);
+    G.sync();
     // 2. ColPivHouseholderQR (model.cpp:43-45): own[c] = slot of logical column c
     int own[4] = {0, 1, 2, 3};
     double mx = upd[0];
@@ -186,18 +242,18 @@ __device__ FitOut quad_fit(const double* g, const double* l, const double* t, in
             if (own[c] == q) lj = c;
         double tk = 0.0, bk = 0.0;
         if (lj == k) {
-            tk = q_house(A + q, la, k, n, &bk);
-            A[k * la + q] = bk;
+            tk = q_house(G, A + q, la, k, n, &bk);
+            if (j == 0) A[k * la + q] = bk;
         }
-        tk = qb(tk, own[k], m);
-        bk = qb(bk, own[k], m);
+        tk = G.own(tk, own[k]);
+        bk = G.own(bk, own[k]);
         if (fabs(bk) > maxpiv) maxpiv = fabs(bk);
-        __syncwarp(m);
+        G.sync();
         if (lj > k)
-            q_apply(A + own[k], la, tk, A + q, la, k, n);
+            q_apply(G, A + own[k], la, tk, A + q, la, k, n);
         else if (lj == k)
-            q_apply(A + q, la, tk, rhs, lr, k, n);  // H_k on the right-hand side, in step
-        __syncwarp(m);
+            q_apply(G, A + q, la, tk, rhs, lr, k, n);  // H_k on the right-hand side, in step
+        G.sync();
         double nu = upd[lj], nd = direct[lj];
         if (lj > k && nu != 0.0) {
             double tq = __ddiv_rn(fabs(A[k * la + q]), nu);
@@ -206,17 +262,17 @@ __device__ FitOut quad_fit(const double* g, const double* l, const double* t, in
             const double ratio = __ddiv_rn(nu, nd);
             const double t2 = __dmul_rn(tq, __dmul_rn(ratio, ratio));
             if (t2 <= downdate_th) {
-                double s = 0.0;
-                for (int r = k + 1; r < n; ++r) s = __dadd_rn(s, __dmul_rn(A[r * la + q], A[r * la + q]));
-                nd = __dsqrt_rn(s);
+                double sp = 0.0;
+                for (int r = G.first(k + 1); r < n; r += SUB) sp = __dadd_rn(sp, __dmul_rn(A[r * la + q], A[r * la + q]));
+                nd = __dsqrt_rn(G.red(sp));
                 nu = nd;
             } else {
                 nu = __dmul_rn(nu, __dsqrt_rn(tq));
             }
         }
-        for (int j = k + 1; j < 4; ++j) {
-            upd[j] = qb(nu, own[j], m);
-            direct[j] = qb(nd, own[j], m);
+        for (int c = k + 1; c < 4; ++c) {
+            upd[c] = G.own(nu, own[c]);
+            direct[c] = G.own(nd, own[c]);
         }
     }
     int perm[4] = {0, 1, 2, 3};
@@ -234,7 +290,7 @@ __device__ FitOut quad_fit(const double* g, const double* l, const double* t, in
     o.degenerate = 0;
     if (rank >= 4 && n >= 4) {
         // the right-hand side already carries H_0..H_3 (nz = 4 here)
-        if (q == 0) {
+        if (q == 0 && j == 0) {
             q_backsolve(A, la, own, nz, rhs, lr);
             for (int i = 0; i < nz; ++i) x[perm[i]] = rhs[i * lr];
         }
@@ -245,56 +301,61 @@ __device__ FitOut quad_fit(const double* g, const double* l, const double* t, in
         int keep = rank < n ? rank : n;
         if (keep < 1) keep = 1;
         const int hs = n < keep ? n : keep;
-        __syncwarp(m);  // every lane is done reading the pivoted QR
+        G.sync();  // every lane is done reading the pivoted QR
         if (q < keep)
-            for (int r = 0; r < n; ++r) A[r * la + q] = __ddiv_rn(dcol(g, l, perm[q], r), scale[perm[q]]);
+            for (int r = G.first(0); r < n; r += SUB) A[r * la + q] = __ddiv_rn(dcol(g, l, perm[q], r), scale[perm[q]]);
         if (q == 0)
-            for (int r = 0; r < n; ++r) rhs[r * lr] = t[r];
-        __syncwarp(m);
+            for (int r = G.first(0); r < n; r += SUB) rhs[r * lr] = t[r];
+        G.sync();
         for (int k = 0; k < hs; ++k) {
             double tk = 0.0, bk = 0.0;
             if (q == k) {
-                tk = q_house(A + q, la, k, n, &bk);
-                A[k * la + q] = bk;
+                tk = q_house(G, A + q, la, k, n, &bk);
+                if (j == 0) A[k * la + q] = bk;
             }
-            tk = qb(tk, k, m);
-            __syncwarp(m);
+            tk = G.own(tk, k);
+            G.sync();
             if (q > k && q < keep)
-                q_apply(A + k, la, tk, A + q, la, k, n);
+                q_apply(G, A + k, la, tk, A + q, la, k, n);
             else if (q == k)
-                q_apply(A + q, la, tk, rhs, lr, k, n);
-            __syncwarp(m);
+                q_apply(G, A + q, la, tk, rhs, lr, k, n);
+            G.sync();
         }
-        if (q == 0) {
+        if (q == 0 && j == 0) {
             const int id[4] = {0, 1, 2, 3};
             q_backsolve(A, la, id, hs, rhs, lr);
             for (int c = 0; c < hs; ++c) x[perm[c]] = rhs[c * lr];
         }
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) o.c[c] = __ddiv_rn(qb(x[c], 0, m), scale[c]);
-    // 3. diagnostics (model.cpp:64-75): lane 0 SS_res, lane 1 mean + SS_tot,
-    //    lane 2 MAPE -- each a sequential pass in sample order
+    for (int c = 0; c < 4; ++c) o.c[c] = __ddiv_rn(G.bc(x[c], 0), scale[c]);
+    // 3. diagnostics (model.cpp:64-75): lane (0,0) SS_res, (1,0) mean + SS_tot,
+    //    (2,0) MAPE -- each a sequential pass in sample order (skipped when
+    //    the caller keeps none: extrapolation windows)
     double acc = 0.0;
-    if (q == 1) {
-        for (int r = 0; r < n; ++r) acc = __dadd_rn(acc, t[r]);
-        const double mean = __ddiv_rn(acc, double(n));
-        acc = 0.0;
-        for (int r = 0; r < n; ++r) {
-            const double d = __dadd_rn(t[r], -mean);
-            acc = __dadd_rn(acc, __dmul_rn(d, d));
-        }
-    } else if (q != 3) {
-        for (int r = 0; r < n; ++r) {
-            double f = __dmul_rn(__dmul_rn(g[r], l[r]), o.c[0]);
-            f = __dadd_rn(f, __dmul_rn(g[r], o.c[1]));
-            f = __dadd_rn(f, __dmul_rn(l[r], o.c[2]));
-            f = __dadd_rn(f, __dmul_rn(1.0, o.c[3]));
-            const double d = __dadd_rn(t[r], -f);
-            acc = q == 0 ? __dadd_rn(acc, __dmul_rn(d, d)) : __dadd_rn(acc, __ddiv_rn(fabs(d), fabs(t[r])));
+    o.r2 = o.mape = 0.0;
+    if (!diag) return o;
+    if (j == 0) {
+        if (q == 1) {
+            for (int r = 0; r < n; ++r) acc = __dadd_rn(acc, t[r]);
+            const double mean = __ddiv_rn(acc, double(n));
+            acc = 0.0;
+            for (int r = 0; r < n; ++r) {
+                const double d = __dadd_rn(t[r], -mean);
+                acc = __dadd_rn(acc, __dmul_rn(d, d));
+            }
+        } else if (q != 3) {
+            for (int r = 0; r < n; ++r) {
+                double f = __dmul_rn(__dmul_rn(g[r], l[r]), o.c[0]);
+                f = __dadd_rn(f, __dmul_rn(g[r], o.c[1]));
+                f = __dadd_rn(f, __dmul_rn(l[r], o.c[2]));
+                f = __dadd_rn(f, __dmul_rn(1.0, o.c[3]));
+                const double d = __dadd_rn(t[r], -f);
+                acc = q == 0 ? __dadd_rn(acc, __dmul_rn(d, d)) : __dadd_rn(acc, __ddiv_rn(fabs(d), fabs(t[r])));
+            }
         }
     }
-    const double ss_res = qb(acc, 0, m), ss_tot = qb(acc, 1, m), mp = qb(acc, 2, m);
+    const double ss_res = G.bc(acc, 0), ss_tot = G.bc(acc, SUB), mp = G.bc(acc, 2 * SUB);
     o.r2 = ss_tot > 0 ? __dadd_rn(1.0, -__ddiv_rn(ss_res, ss_tot)) : (ss_res < 1e-18 ? 1.0 : 0.0);
     o.mape = __ddiv_rn(mp, double(n));
     return o;
@@ -310,8 +371,15 @@ struct Rec {
     const double* lat;
 };
 
+__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+// registry position of each record; per-macro smallest micro id (the sort
+// key carries micro - that, usually 0 bits wide)
 __global__ void k_mpos(Rec rc, int64_t n, const int32_t* ids_sorted, const int32_t* pos_sorted, int nm,
-                       int32_t* mpos, int32_t* valid, int32_t* has_rec) {
+                       int32_t* mpos, int32_t* valid, int32_t* has_rec, int32_t* umin_m) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int32_t id = rc.macro[i];
@@ -326,7 +394,10 @@ __global__ void k_mpos(Rec rc, int64_t n, const int32_t* ids_sorted, const int32
     const bool ok = lo < nm && ids_sorted[lo] == id;
     mpos[i] = ok ? pos_sorted[lo] : INT_MAX;
     valid[i] = ok ? 1 : 0;
-    if (ok) has_rec[pos_sorted[lo]] = 1;  // group_records finds this macro
+    if (ok) {
+        has_rec[pos_sorted[lo]] = 1;  // group_records finds this macro
+        atomicMin(umin_m + pos_sorted[lo], rc.micro[i]);
+    }
 }
 
 struct Ranges {
@@ -336,7 +407,10 @@ struct Ranges {
 
 // Field ranges for the sort-key packing: grid-stride, warp reductions, one
 // set of atomics per warp (a per-record atomic on 8 hot words serialises).
-__global__ void k_ranges(Rec rc, const int64_t* idx, int64_t n, Ranges* out) {
+// The micro field is micro - (smallest micro of the record's macro): umin =
+// 0, umax = its largest value over valid records.
+__global__ void k_ranges(Rec rc, const int64_t* idx, int64_t n, const int32_t* mpos, const int32_t* umin_m,
+                         Ranges* out) {
     unsigned long long gmin = ~0ULL, gmax = 0, lmin = ~0ULL, lmax = 0;
     int wmin = INT_MAX, wmax = INT_MIN, umin = INT_MAX, umax = INT_MIN;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
@@ -350,8 +424,12 @@ __global__ void k_ranges(Rec rc, const int64_t* idx, int64_t n, Ranges* out) {
         lmax = max(lmax, l);
         wmin = min(wmin, rc.w[r]);
         wmax = max(wmax, rc.w[r]);
-        umin = min(umin, rc.micro[r]);
-        umax = max(umax, rc.micro[r]);
+        const int32_t mp = mpos[r];
+        if (mp != INT_MAX) {
+            umin = 0;
+            const long long ur = (long long)rc.micro[r] - umin_m[mp];
+            umax = max(umax, int(ur < INT_MAX ? ur : INT_MAX));
+        }
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
@@ -387,7 +465,7 @@ struct Pass {
     int nf, bits;
 };
 
-__global__ void k_pack(Rec rc, const int32_t* mpos, const int64_t* perm, int64_t n, Pass ps,
+__global__ void k_pack(Rec rc, const int32_t* mpos, const int32_t* umin_m, const int64_t* perm, int64_t n, Pass ps,
                        unsigned long long* key) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -398,7 +476,7 @@ __global__ void k_pack(Rec rc, const int32_t* mpos, const int64_t* perm, int64_t
         unsigned long long v;
         switch (f.which) {
             case 0: v = ((unsigned long long)rc.g[r] ^ 0x8000000000000000ULL) - f.base; break;
-            case 1: v = (unsigned long long)(long long)(rc.micro[r]) - f.base; break;
+            case 1: v = (unsigned long long)((long long)rc.micro[r] - umin_m[mpos[r]]) - f.base; break;
             case 2: v = ((unsigned long long)rc.l[r] ^ 0x8000000000000000ULL) - f.base; break;
             case 3: v = (unsigned long long)(long long)(rc.w[r]) - f.base; break;
             default: v = (unsigned long long)mpos[r]; break;
@@ -551,77 +629,80 @@ struct Buckets {
     int32_t* degen;
 };
 
-constexpr int kQWarps = 4;    // warps per CTA of the bucket fit (128 threads)
-constexpr int kQRows = 32;    // bucket problems of <= 32 samples run in shared memory
-constexpr int kQPoolRows = 256;  // pooled (extrapolation / per-macro) problems: 1 warp per CTA, 80 KB slab
-constexpr int kQScr = 5;      // global scratch doubles per sample (problems above the slab)
+constexpr int kQWarps = 4;      // warps per CTA of the small-problem fit (128 threads)
+constexpr int kQRows = 32;      // problems of <= 32 samples: 4 lanes each, shared memory, sequential sums
+constexpr int kORows = 256;     // larger problems: a warp each (octet order), shared memory up to this size
+constexpr int kOWarps = 4;
+constexpr int kQScr = 5;        // global scratch doubles per sample (problems above kORows)
 
-// fit_bucket over b.nb independent problems; quad p of warp w takes problem
-// 8w + p (grid-stride).  Shared slab per warp (dynamic): [ROWS][32] column
-// slots + [ROWS][8] right-hand sides; problems of more than ROWS samples
-// work in their own global scratch (same operation order, bitwise equal).
-template <int ROWS, int WARPS>
-__global__ void __launch_bounds__(32 * WARPS) k_qfit(const double* sg, const double* sl, const double* st,
-                                                     Buckets b, double* gscr) {
-    extern __shared__ double slab_dyn[];
+// Problems of <= kQRows samples: quad p of warp w takes problem 8w + p
+// (grid-stride).  Shared slab per warp: [kQRows][32] column slots +
+// [kQRows][8] right-hand sides.  Larger problems are k_ofit's.
+__global__ void __launch_bounds__(32 * kQWarps, 6) k_qfit(const double* sg, const double* sl, const double* st,
+                                                       Buckets b) {
+    __shared__ double slab[kQWarps][kQRows * 40];
     const int lane = threadIdx.x & 31, q = lane & 3, pq = lane >> 2;
-    const unsigned m = 0xFu << (lane & ~3);
+    Grp<1> G{q, 0, 0xFu << (lane & ~3), 0u};
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    double* sA = slab_dyn + size_t(threadIdx.x >> 5) * ROWS * 40;
-    double* sR = sA + ROWS * 32;
+    double* sA = slab[threadIdx.x >> 5];
+    double* sR = sA + kQRows * 32;
     for (int64_t base = warp * 8; base < b.nb; base += nw * 8) {
         const int64_t pi = base + pq;
         if (pi >= b.nb) continue;
         const int64_t lo = b.slo[pi], n = b.shi[pi] - lo;
-        if (n <= 0) continue;
-        double *A, *R;
-        int la, lr;
-        if (n <= ROWS) {
-            A = sA + pq * 4;
-            la = 32;
-            R = sR + pq;
-            lr = 8;
-        } else {
-            A = gscr + kQScr * lo;
-            la = 4;
-            R = A + 4 * n;
-            lr = 1;
-        }
-        const FitOut o = quad_fit(sg + lo, sl + lo, st + lo, int(n), A, la, R, lr, q, m);
+        if (n <= 0 || n > kQRows) continue;
+        const FitOut o =
+            group_fit<1>(sg + lo, sl + lo, st + lo, int(n), sA + pq * 4, 32, sR + pq, 8, G, b.r2 || b.mape);
         if (q == 0) {
             for (int c = 0; c < 4; ++c) b.coeff[4 * pi + c] = o.c[c];
             if (b.r2) b.r2[pi] = o.r2;
             if (b.mape) b.mape[pi] = o.mape;
             b.degen[pi] = o.degenerate;
         }
-        __syncwarp(m);  // the slab is reused by the quad's next problem
+        __syncwarp(G.m);  // the slab is reused by the quad's next problem
     }
 }
 
-template <int ROWS, int WARPS>
-constexpr size_t qfit_smem() {
-    return size_t(WARPS) * ROWS * 40 * sizeof(double);
+// Problems of more than kQRows samples: a warp each (8 lanes per design
+// column, octet order), in a [kORows][5] shared slab or -- above kORows --
+// the problem's own global scratch (5 doubles per sample).
+__global__ void __launch_bounds__(32 * kOWarps) k_ofit(const double* sg, const double* sl, const double* st,
+                                                       Buckets b, double* gscr) {
+    __shared__ double slab[kOWarps][kORows * 5];
+    const int lane = threadIdx.x & 31;
+    Grp<8> G{lane >> 3, lane & 7, 0xffffffffu, 0xFFu << (lane & 24)};
+    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    double* sA = slab[threadIdx.x >> 5];
+    for (int64_t pi = warp; pi < b.nb; pi += nw) {
+        const int64_t lo = b.slo[pi], n = b.shi[pi] - lo;
+        if (n <= kQRows) continue;
+        double* A = n <= kORows ? sA : gscr + kQScr * lo;
+        const FitOut o = group_fit<8>(sg + lo, sl + lo, st + lo, int(n), A, 4, A + 4 * n, 1, G, b.r2 || b.mape);
+        if (lane == 0) {
+            for (int c = 0; c < 4; ++c) b.coeff[4 * pi + c] = o.c[c];
+            if (b.r2) b.r2[pi] = o.r2;
+            if (b.mape) b.mape[pi] = o.mape;
+            b.degen[pi] = o.degenerate;
+        }
+        __syncwarp();  // the slab is reused by the warp's next problem
+    }
 }
 
-// Bucket problems (<= kQRows samples mostly) on 4-warp CTAs; pooled problems
-// (extrapolation windows, per-macro baselines) on 1-warp CTAs with a
-// kQPoolRows slab.  grid: problems / 8 per warp, capped at 16 CTAs per SM.
+// fit_bucket over every problem of b: small ones on quads, large ones on
+// warps.  `pooled` = the list is mostly large problems (extrapolation
+// windows, per-macro baselines): the quad kernel is sized for few problems.
 cudaError_t launch_qfit(bool pooled, const double* sg, const double* sl, const double* st, const Buckets& b,
                         double* gscr, int nsm, cudaStream_t s) {
     if (b.nb <= 0) return cudaSuccess;
-    if (!pooled) {
-        constexpr size_t sm = qfit_smem<kQRows, kQWarps>();
-        const int grid = int(std::max<int64_t>(1, std::min<int64_t>((b.nb + 8 * kQWarps - 1) / (8 * kQWarps),
-                                                                   int64_t(nsm) * 16)));
-        k_qfit<kQRows, kQWarps><<<grid, 32 * kQWarps, sm, s>>>(sg, sl, st, b, gscr);
-    } else {
-        constexpr size_t sm = qfit_smem<kQPoolRows, 1>();
-        const cudaError_t e = wtb::prepare_smem(reinterpret_cast<const void*>(k_qfit<kQPoolRows, 1>), sm);
-        if (e != cudaSuccess) return e;
-        const int grid = int(std::max<int64_t>(1, std::min<int64_t>((b.nb + 7) / 8, int64_t(nsm) * 16)));
-        k_qfit<kQPoolRows, 1><<<grid, 32, sm, s>>>(sg, sl, st, b, gscr);
-    }
+    const int64_t cap = int64_t(nsm) * 16;
+    const int gq = int(std::max<int64_t>(1, std::min<int64_t>((b.nb + 8 * kQWarps - 1) / (8 * kQWarps),
+                                                              pooled ? int64_t(nsm) : cap)));
+    k_qfit<<<gq, 32 * kQWarps, 0, s>>>(sg, sl, st, b);
+    const int go = int(std::max<int64_t>(1, std::min<int64_t>((b.nb + kOWarps - 1) / kOWarps,
+                                                              pooled ? cap : int64_t(nsm) * 2)));
+    k_ofit<<<go, 32 * kOWarps, 0, s>>>(sg, sl, st, b, gscr);
     return cudaGetLastError();
 }
 
@@ -1068,12 +1149,12 @@ std::vector<Pass> plan_passes(const std::vector<Field>& fields) {
     return out;
 }
 
-wt_status run_sort(const Rec& rc, const int32_t* mpos, int64_t* perm, int64_t* perm_alt, int64_t n,
+wt_status run_sort(const Rec& rc, const int32_t* mpos, const int32_t* umin_m, int64_t* perm, int64_t* perm_alt, int64_t n,
                    const std::vector<Pass>& passes, unsigned long long* keys, unsigned long long* keys_alt,
                    void*& tmp, size_t& tmp_bytes, cudaStream_t s) {
     for (const Pass& ps : passes) {
         const int blocks = int((n + 255) / 256);
-        k_pack<<<blocks, 256, 0, s>>>(rc, mpos, perm, n, ps, keys);
+        k_pack<<<blocks, 256, 0, s>>>(rc, mpos, umin_m, perm, n, ps, keys);
         size_t need = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, need, keys, keys_alt, perm, perm_alt, n, 0,
                                         std::max(1, ps.bits), s);
@@ -1134,7 +1215,8 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     int32_t* mpos = dalloc<int32_t>(owned, n_all);
     int32_t* valid = dalloc<int32_t>(owned, n_all);
     int64_t* idx = dalloc<int64_t>(owned, n_all);
-    if (!dup || !drb || !mpos || !valid || !idx) {
+    int32_t* umin_m = dalloc<int32_t>(owned, n_macros);
+    if (!dup || !drb || !mpos || !valid || !idx || !umin_m) {
         g_fit_err = "cudaMalloc failed";
         return WT_CUDA_ERROR;
     }
@@ -1146,10 +1228,12 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     Head* dh = reinterpret_cast<Head*>(drb);
     int32_t* has_rec = reinterpret_cast<int32_t*>(drb + sizeof(Head));
     const int blocks_all = int((n_all + 255) / 256);
-    k_mpos<<<blocks_all, 256, 0, s>>>(rc, n_all, dup, dup + nid, nid, mpos, valid, has_rec);
+    k_fill_i32<<<(n_macros + 255) / 256, 256, 0, s>>>(umin_m, n_macros, INT_MAX);
+    k_mpos<<<blocks_all, 256, 0, s>>>(rc, n_all, dup, dup + nid, nid, mpos, valid, has_rec, umin_m);
     // key ranges over every record (a superset of the valid ones: packing
     // stays exact) and max w over ALL records (model.cpp:201-203)
-    k_ranges<<<int(std::min<int64_t>((n_all + 255) / 256, 148 * 4)), 256, 0, s>>>(rc, nullptr, n_all, &dh->r);
+    k_ranges<<<int(std::min<int64_t>((n_all + 255) / 256, 148 * 4)), 256, 0, s>>>(rc, nullptr, n_all, mpos, umin_m,
+                                                                                  &dh->r);
     {  // compact valid record indices, order preserved
         cub::CountingInputIterator<int64_t> it(0);
         size_t need = 0;
@@ -1180,9 +1264,9 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     // (the ranges' g / l / w / micro bounds cover every record)
     const int bits_g = bits_for(hr.gmax - hr.gmin), bits_l = bits_for(hr.lmax - hr.lmin);
     const int bits_w = bits_for((unsigned long long)((long long)hr.wmax - hr.wmin));
-    const int bits_u = bits_for((unsigned long long)((long long)hr.umax - hr.umin));
+    const int bits_u = hr.umax > 0 ? bits_for((unsigned long long)hr.umax) : 0;
     const int bits_m = bits_for((unsigned long long)std::max(1, n_macros));
-    Field fg{0, hr.gmin, bits_g, 0}, fu{1, (unsigned long long)(long long)hr.umin, bits_u, 0},
+    Field fg{0, hr.gmin, bits_g, 0}, fu{1, 0ULL, bits_u, 0},
         fl{2, hr.lmin, bits_l, 0}, fw{3, (unsigned long long)(long long)hr.wmin, bits_w, 0},
         fm{4, 0, bits_m, 0};
     auto passA = plan_passes({fg, fu, fl, fw, fm});
@@ -1203,10 +1287,16 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     CK(cudaMemcpyAsync(ordB, idx, n * 8, cudaMemcpyDeviceToDevice, s));
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
-    wt_status st = run_sort(rc, mpos, ordA, alt, n, passA, keys, keys2, tmp, tmp_bytes, s);
+    wt_status st = run_sort(rc, mpos, umin_m, ordA, alt, n, passA, keys, keys2, tmp, tmp_bytes, s);
     if (st) return st;
-    st = run_sort(rc, mpos, ordB, alt, n, passB, keys, keys2, tmp, tmp_bytes, s);
-    if (st) return st;
+    if (bits_u == 0) {
+        // one micro id per macro: order A (macro, w, l, micro, g) is order B
+        // (macro, w, l, g) -- one sort
+        CK(cudaMemcpyAsync(ordB, ordA, n * 8, cudaMemcpyDeviceToDevice, s));
+    } else {
+        st = run_sort(rc, mpos, umin_m, ordB, alt, n, passB, keys, keys2, tmp, tmp_bytes, s);
+        if (st) return st;
+    }
     if (tmp) cudaFreeAsync(tmp, s);
 
     trace("sorts");
