@@ -312,6 +312,12 @@ typedef struct {
 } wt_grid_entry;
 
 wt_status wt_grid_create(const wt_engine* e, const wt_grid_desc* desc, wt_grid** out);
+/* The same, stream-ordered on `stream`: storage from the library's memory
+ * pool and every upload queued on the stream (no host synchronisation), so a
+ * build chain fit -> engine -> grid -> sweep stays on one stream.  Use the
+ * grid on other streams only after ordering them behind `stream`.  Its
+ * storage is not IPC-exportable (wt_grid_ipc_handle: WT_UNSUPPORTED). */
+wt_status wt_grid_create_async(const wt_engine* e, const wt_grid_desc* desc, void* stream, wt_grid** out);
 wt_status wt_grid_destroy(wt_grid* g);
 /* Raw device storage (for collectives / inspection).  Taking it invalidates
  * the grid's run index (gathers then read the entries from L2) until the next
@@ -464,6 +470,27 @@ wt_status wt_build_result_get(wt_build* b, wt_build_result* result);
  * `stream` (ordered after the build); returns once the engine is ready. */
 wt_status wt_engine_create_from_build(const wt_build* b, const wt_registry_desc* registry, const wt_hw* hw,
                                       void* stream, wt_engine** out);
+
+/* ---- exchanging builds between ranks (multi-GPU build, dist.py) ----------
+ * A build fitted on one GPU for a contiguous slice of the registry (its shard
+ * of build_dual_table) is packed into one contiguous device blob; the blobs
+ * of all ranks travel in one collective (NCCL all-gather of equal-stride
+ * blobs) and every rank merges them, in registry order, into one build on
+ * its own device -- the same tables the single-GPU build of the whole
+ * registry produces (merge_tables on the device: CSR offsets rebased).
+ *
+ * wt_build_pack_info: counts[5] = {n_tables, n_buckets, n_groups, W, p} and
+ *   the packed size in bytes.
+ * wt_build_pack: packs into device memory dst (cap >= bytes), queued on
+ *   `stream` after the build's own work.
+ * wt_build_merge: parts are packed[r * stride], r < n_parts, with counts
+ *   [n_parts * 5] as wt_build_pack_info reported them (parts with zero
+ *   tables are skipped; W and p must agree).  The merged build has no
+ *   ablation baselines.  One host sync (the merged macro ids). */
+wt_status wt_build_pack_info(const wt_build* b, int64_t* counts, size_t* bytes);
+wt_status wt_build_pack(const wt_build* b, void* dst, size_t cap, void* stream);
+wt_status wt_build_merge(const void* packed, size_t stride, int32_t n_parts, const int64_t* counts, int device,
+                         void* stream, wt_build** out);
 
 /* fit_bucket over nb independent buckets in one launch: samples of bucket b
  * are [off[b], off[b+1]) of g/l/t (host arrays).  coeffs [nb*4]. */

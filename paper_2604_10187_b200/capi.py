@@ -93,8 +93,8 @@ class wt_build_result(C.Structure):
 EXPORTS = (
     "wt_last_error wt_version wt_abi_version wt_engine_create wt_engine_destroy wt_engine_info_get "
     "wt_engine_config_index wt_engine_set_prune wt_engine_count_evals wt_engine_prune_masks wt_tune_batch wt_tune_batch_i64 wt_gather_batch_i64 wt_tune_grouped_batch wt_predict_batch wt_explain "
-    "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_destroy wt_grid_storage wt_sweep wt_grid_finalize "
-    "wt_fit_build_device wt_build_result_get wt_engine_create_from_build wt_gather_batch wt_decide_host_sync wt_decide_host_stream_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
+    "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_create_async wt_grid_destroy wt_grid_storage wt_sweep wt_grid_finalize "
+    "wt_fit_build_device wt_build_result_get wt_build_pack_info wt_build_pack wt_build_merge wt_engine_create_from_build wt_gather_batch wt_decide_host_sync wt_decide_host_stream_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
     "wt_simulate_batch wt_profile_sim wt_tune_one wt_engine_set_resident wt_baseline_create "
     "wt_baseline_destroy wt_baseline_tune_batch wt_baseline_predict_batch wt_set_kernel_timing wt_kernel_time_ms "
     "wt_prune_plan wt_sweep_to wt_grid_ipc_handle wt_ipc_open wt_ipc_close").split()
@@ -373,13 +373,18 @@ class Baseline:
 class Grid:
     """A decision grid: tune() over n_pairs (N, K) x M in [m_lo, m_hi]."""
 
-    def __init__(self, engine: Engine, N, K, m_lo, m_hi, topk=0):
+    def __init__(self, engine: Engine, N, K, m_lo, m_hi, topk=0, stream=None):
+        """stream=None: synchronous create (IPC-exportable storage); a stream:
+        wt_grid_create_async (pool storage, uploads queued on the stream)."""
         self.engine = engine
         self._N = np.ascontiguousarray(N, np.int32)
         self._K = np.ascontiguousarray(K, np.int32)
         d = wt_grid_desc(len(self._N), self._N.ctypes.data, self._K.ctypes.data, m_lo, m_hi, topk)
         h = C.c_void_p()
-        check(lib().wt_grid_create(engine.handle, C.byref(d), C.byref(h)))
+        if stream is None:
+            check(lib().wt_grid_create(engine.handle, C.byref(d), C.byref(h)))
+        else:
+            check(lib().wt_grid_create_async(engine.handle, C.byref(d), vp(_stream_ptr(stream)), C.byref(h)))
         self.handle = h
         self.m_lo, self.m_hi, self.topk = m_lo, m_hi, topk
         ent, n = C.c_void_p(), C.c_int64()
@@ -576,6 +581,34 @@ class Build:
                                         vp(_stream_ptr(stream)), C.byref(h)))
         self.handle = h
         self.device = device
+
+    @classmethod
+    def _wrap(cls, handle, device):
+        b = cls.__new__(cls)
+        b.handle, b.device, b._ids = handle, device, None
+        return b
+
+    def pack_info(self):
+        """(counts [n_tables, n_buckets, n_groups, W, p] int64, packed bytes)."""
+        counts = np.zeros(5, np.int64)
+        nbytes = C.c_size_t()
+        check(lib().wt_build_pack_info(self.handle, vp(counts.ctypes.data), C.byref(nbytes)))
+        return counts, nbytes.value
+
+    def pack(self, dst, stream=None):
+        """Pack the device tables into `dst` (a uint8 device tensor)."""
+        check(lib().wt_build_pack(self.handle, vp(dst.data_ptr()), C.c_size_t(dst.numel()),
+                                  vp(_stream_ptr(stream))))
+
+    @classmethod
+    def merge(cls, packed, stride: int, counts, device: int = 0, stream=None):
+        """One build from n packed parts (packed: uint8 device tensor of
+        n * stride bytes, counts: [n, 5] as pack_info reported them)."""
+        counts = np.ascontiguousarray(counts, np.int64).reshape(-1, 5)
+        h = C.c_void_p()
+        check(lib().wt_build_merge(vp(packed.data_ptr()), C.c_size_t(stride), C.c_int32(len(counts)),
+                                   vp(counts.ctypes.data), C.c_int(device), vp(_stream_ptr(stream)), C.byref(h)))
+        return cls._wrap(h, device)
 
     def result(self) -> dict:
         """Host copies of the tables + diagnostics (wt_build_result_get)."""

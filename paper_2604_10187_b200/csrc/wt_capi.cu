@@ -192,6 +192,7 @@ struct wt_grid {
     bool wide = false;
     int sweep_chunk = 0;
     void* mem = nullptr;
+    bool pooled = false;    // mem from the library pool (wt_grid_create_async): not IPC-exportable
     int32_t* dN = nullptr;
     int32_t* dK = nullptr;
     uint64_t* dkeys = nullptr;
@@ -1095,8 +1096,11 @@ wt_status wt_nearest_anchor_batch(const int64_t* anchors, int32_t n_anchors, con
 }
 
 // ------------------------------------------------------------------ grid
-wt_status wt_grid_create(const wt_engine* e, const wt_grid_desc* desc, wt_grid** out) {
-    NvtxRange nvtx_("wt_grid_create");
+namespace {
+// pooled: storage from the library pool and every upload queued on `st` (no
+// host sync); otherwise cudaMalloc (IPC-exportable) and synchronous uploads.
+wt_status grid_create_impl(const wt_engine* e, const wt_grid_desc* desc, bool pooled, cudaStream_t st,
+                           wt_grid** out) {
     if (!e || !desc || !out) return set_err(WT_INVALID_ARGUMENT, "null argument");
     *out = nullptr;
     if (desc->n_pairs <= 0) return set_err(WT_INVALID_ARGUMENT, "grid needs at least one (N, K) pair");
@@ -1168,11 +1172,19 @@ wt_status wt_grid_create(const wt_engine* e, const wt_grid_desc* desc, wt_grid**
                  o_rbidx = ar.take(want_runs ? size_t(g->n_pairs) * nblk * 16 : 0),
                  o_rkey = ar.take(want_runs ? size_t(g->n_entries + 1) * 4 : 0),
                  o_rval = ar.take(want_runs ? size_t(g->n_entries) * 16 : 0);
-    cudaError_t ce = cudaMalloc(&g->mem, ar.used);
+    cudaError_t ce = pooled ? cudaMallocFromPoolAsync(&g->mem, ar.used, lib_pool(e->device), st)
+                            : cudaMalloc(&g->mem, ar.used);
     if (ce != cudaSuccess) {
         delete g;
         return cuda_err(ce, "wt_grid_create: cudaMalloc");
     }
+    g->pooled = pooled;
+    // uploads: synchronous, or queued on st (pageable sources are staged by
+    // the driver when the call returns, so the host vectors may go)
+    auto up = [&](void* dst, const void* src, size_t n) {
+        return pooled ? cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st)
+                      : cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
+    };
     char* base = static_cast<char*>(g->mem);
     g->dN = reinterpret_cast<int32_t*>(base + o_n);
     g->dK = reinterpret_cast<int32_t*>(base + o_k);
@@ -1182,7 +1194,7 @@ wt_status wt_grid_create(const wt_engine* e, const wt_grid_desc* desc, wt_grid**
     g->tk_macro = g->topk ? reinterpret_cast<int32_t*>(base + o_tkm) : nullptr;
     g->tk_lat = g->topk ? reinterpret_cast<double*>(base + o_tkl) : nullptr;
     g->dhash = htab.empty() ? nullptr : reinterpret_cast<int4*>(base + o_hash);
-    if (g->dhash) cudaMemcpy(g->dhash, htab.data(), htab.size() * sizeof(int4), cudaMemcpyHostToDevice);
+    if (g->dhash) up(g->dhash, htab.data(), htab.size() * sizeof(int4));
     if (want_runs) {
         g->runs.hdr = reinterpret_cast<int32_t*>(base + o_rhdr);
         g->runs.bhead = reinterpret_cast<int4*>(base + o_rbidx);
@@ -1191,7 +1203,8 @@ wt_status wt_grid_create(const wt_engine* e, const wt_grid_desc* desc, wt_grid**
         g->runs.nblk = int32_t(nblk);
         g->runs.nbtot = int32_t(int64_t(g->n_pairs) * nblk);
         g->runs.budget = runs_kb * 1024;
-        cudaMemset(g->runs.hdr, 0, 16);
+        if (pooled) cudaMemsetAsync(g->runs.hdr, 0, 16, st);
+        else cudaMemset(g->runs.hdr, 0, 16);
     }
     std::vector<uint64_t> kk;
     std::vector<int32_t> pid;
@@ -1199,12 +1212,17 @@ wt_status wt_grid_create(const wt_engine* e, const wt_grid_desc* desc, wt_grid**
         kk.push_back(k.first);
         pid.push_back(k.second);
     }
-    cudaMemcpy(g->dN, desc->N, size_t(g->n_pairs) * 4, cudaMemcpyHostToDevice);
-    cudaMemcpy(g->dK, desc->K, size_t(g->n_pairs) * 4, cudaMemcpyHostToDevice);
-    cudaMemcpy(g->dkeys, kk.data(), kk.size() * 8, cudaMemcpyHostToDevice);
-    ce = cudaMemcpy(g->dpid, pid.data(), pid.size() * 4, cudaMemcpyHostToDevice);
+    up(g->dN, desc->N, size_t(g->n_pairs) * 4);
+    up(g->dK, desc->K, size_t(g->n_pairs) * 4);
+    up(g->dkeys, kk.data(), kk.size() * 8);
+    ce = up(g->dpid, pid.data(), pid.size() * 4);
     if (ce != cudaSuccess) {
-        cudaFree(g->mem);
+        if (pooled) {
+            cudaFreeAsync(g->mem, st);
+            cudaStreamSynchronize(st);
+        } else {
+            cudaFree(g->mem);
+        }
         delete g;
         return cuda_err(ce, "wt_grid_create: upload");
     }
@@ -1213,11 +1231,29 @@ wt_status wt_grid_create(const wt_engine* e, const wt_grid_desc* desc, wt_grid**
     *out = g;
     return WT_OK;
 }
+}  // namespace
+
+wt_status wt_grid_create(const wt_engine* e, const wt_grid_desc* desc, wt_grid** out) {
+    NvtxRange nvtx_("wt_grid_create");
+    return grid_create_impl(e, desc, false, nullptr, out);
+}
+
+wt_status wt_grid_create_async(const wt_engine* e, const wt_grid_desc* desc, void* stream, wt_grid** out) {
+    NvtxRange nvtx_("wt_grid_create_async");
+    return grid_create_impl(e, desc, true, static_cast<cudaStream_t>(stream), out);
+}
 
 wt_status wt_grid_destroy(wt_grid* g) {
     if (!g) return WT_OK;
     DeviceGuard guard(g->eng->device);
-    cudaFree(g->mem);
+    if (g->pooled) {
+        // pool memory: released after every stream's use of the grid
+        cudaDeviceSynchronize();
+        cudaFreeAsync(g->mem, nullptr);
+        cudaStreamSynchronize(nullptr);
+    } else {
+        cudaFree(g->mem);
+    }
     delete g;
     return WT_OK;
 }
@@ -1323,6 +1359,7 @@ wt_status wt_sweep_to(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end
 
 wt_status wt_grid_ipc_handle(const wt_grid* g, void* handle, int64_t* offset) {
     if (!g || !handle || !offset) return set_err(WT_INVALID_ARGUMENT, "null argument");
+    if (g->pooled) return set_err(WT_UNSUPPORTED, "grid storage from wt_grid_create_async is not IPC-exportable");
     DeviceGuard guard(g->eng->device);
     cudaIpcMemHandle_t h;
     const cudaError_t ce = cudaIpcGetMemHandle(&h, g->mem);

@@ -1660,6 +1660,126 @@ struct DevRestore {
 
 }  // namespace
 
+// ------------------------------------------- build exchange between ranks
+// A build's device tables packed into one contiguous blob (wt_build_pack) so
+// that shards fitted on different GPUs travel in ONE collective (an NCCL
+// all-gather of equal-stride blobs), then merged back into one build in
+// registry order on every rank (wt_build_merge): the per-rank tables are
+// concatenated and the CSR offsets rebased -- coeff_off by the bucket count
+// of the ranks before, awave_aoff / ext_off by their group count.  This is
+// merge_tables (dist.py) on the device: shards are contiguous registry slices
+// and fit_core's outputs depend on a macro's own records only, so the merged
+// build equals the single-GPU build of the whole registry.
+namespace {
+
+enum PackArr {
+    PA_MACRO, PA_W, PA_COFF, PA_EOFF, PA_ECNT, PA_EFLAGS,         // per table (i32; COFF has NM + 1)
+    PA_CW, PA_AAOFF, PA_NSAMP, PA_DFLAGS, PA_DEGEN,               // per bucket (i32; AAOFF has NB + 1)
+    PA_AMICRO, PA_PART, PA_EMICRO,                                // per group (i32)
+    PA_TEXT, PA_CTH, PA_R2, PA_MAPE,                              // f64: 4 / table, 4 / bucket, 1, 1
+    PA_AL, PA_EL,                                                 // i64 per group
+    PA_N
+};
+constexpr uint64_t kPackMagic = 0x31424b5041505457ull;  // "WTPAPKB1"
+struct PackHead {
+    uint64_t magic;
+    int64_t NM, NB, G, W, p, bytes, pad;
+};
+struct PackLayout {
+    size_t off[PA_N], bytes[PA_N], total;
+};
+
+PackLayout pack_layout(int64_t NM, int64_t NB, int64_t G) {
+    const int64_t n[PA_N] = {NM, NM, NM + 1, NM, NM, NM, NB, NB + 1, NB, NB, NB, G, G, G,
+                             4 * NM, 4 * NB, NB, NB, G, G};
+    const int esz[PA_N] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 8, 8, 8, 8, 8, 8};
+    PackLayout L{};
+    Arena ar;
+    ar.take(sizeof(PackHead));
+    for (int a = 0; a < PA_N; ++a) {
+        L.bytes[a] = size_t(n[a]) * esz[a];
+        L.off[a] = ar.take(L.bytes[a]);
+    }
+    L.total = ar.used;
+    return L;
+}
+
+void* pack_ptr(const wt_build* B, int a) {
+    switch (a) {
+        case PA_MACRO: return B->t_macro;
+        case PA_W: return B->t_W;
+        case PA_COFF: return B->t_coeff_off;
+        case PA_EOFF: return B->t_ext_off;
+        case PA_ECNT: return B->t_ext_cnt;
+        case PA_EFLAGS: return B->d_ext_flags;
+        case PA_CW: return B->t_coeff_w;
+        case PA_AAOFF: return B->t_awave_aoff;
+        case PA_NSAMP: return B->d_nsamp;
+        case PA_DFLAGS: return B->d_dflags;
+        case PA_DEGEN: return B->d_degen;
+        case PA_AMICRO: return B->t_anchor_micro;
+        case PA_PART: return B->d_partial;
+        case PA_EMICRO: return B->t_ext_micro;
+        case PA_TEXT: return B->t_theta_ext;
+        case PA_CTH: return B->t_coeff_theta;
+        case PA_R2: return B->d_r2;
+        case PA_MAPE: return B->d_mape;
+        case PA_AL: return B->t_anchor_l;
+        case PA_EL: return B->t_ext_l;
+    }
+    return nullptr;
+}
+
+void set_pack_ptr(wt_build* B, int a, void* p) {
+    switch (a) {
+        case PA_MACRO: B->t_macro = static_cast<int32_t*>(p); break;
+        case PA_W: B->t_W = static_cast<int32_t*>(p); break;
+        case PA_COFF: B->t_coeff_off = static_cast<int32_t*>(p); break;
+        case PA_EOFF: B->t_ext_off = static_cast<int32_t*>(p); break;
+        case PA_ECNT: B->t_ext_cnt = static_cast<int32_t*>(p); break;
+        case PA_EFLAGS: B->d_ext_flags = static_cast<int32_t*>(p); break;
+        case PA_CW: B->t_coeff_w = static_cast<int32_t*>(p); break;
+        case PA_AAOFF: B->t_awave_aoff = static_cast<int32_t*>(p); break;
+        case PA_NSAMP: B->d_nsamp = static_cast<int32_t*>(p); break;
+        case PA_DFLAGS: B->d_dflags = static_cast<int32_t*>(p); break;
+        case PA_DEGEN: B->d_degen = static_cast<int32_t*>(p); break;
+        case PA_AMICRO: B->t_anchor_micro = static_cast<int32_t*>(p); break;
+        case PA_PART: B->d_partial = static_cast<int32_t*>(p); break;
+        case PA_EMICRO: B->t_ext_micro = static_cast<int32_t*>(p); break;
+        case PA_TEXT: B->t_theta_ext = static_cast<double*>(p); break;
+        case PA_CTH: B->t_coeff_theta = static_cast<double*>(p); break;
+        case PA_R2: B->d_r2 = static_cast<double*>(p); break;
+        case PA_MAPE: B->d_mape = static_cast<double*>(p); break;
+        case PA_AL: B->t_anchor_l = static_cast<int64_t*>(p); break;
+        case PA_EL: B->t_ext_l = static_cast<int64_t*>(p); break;
+    }
+}
+
+// One launch copies up to kMergeSegs (rank, array) segments as 32-bit words,
+// adding the segment's base to offset arrays (0 elsewhere: identity on the
+// bit pattern).  blockIdx.y = segment.
+constexpr int kMergeSegs = 96;
+struct MergeSeg {
+    const uint32_t* src;
+    uint32_t* dst;
+    int64_t words;
+    uint32_t add;
+    uint32_t pad;
+};
+struct MergeArgs {
+    int32_t nseg;
+    MergeSeg seg[kMergeSegs];
+};
+
+__global__ void __launch_bounds__(256) k_build_merge(const __grid_constant__ MergeArgs a) {
+    const MergeSeg sg = a.seg[blockIdx.y];
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < sg.words; i += stride)
+        sg.dst[i] = __ldg(sg.src + i) + sg.add;
+}
+
+}  // namespace
+
 // For wt_capi.cu: the device CSR of a build (engine creation without a
 // host round trip).
 namespace wtb {
@@ -1846,6 +1966,173 @@ wt_status wt_fit_bucket_batch(const double* g, const double* l, const double* t,
     CK(cudaMemcpy(r2, bk.r2, nb * 8, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(mape, bk.mape, nb * 8, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(degenerate, bk.degen, nb * 4, cudaMemcpyDeviceToHost));
+    return WT_OK;
+}
+
+
+wt_status wt_build_pack_info(const wt_build* b, int64_t* counts, size_t* bytes) {
+    if (!b || !counts || !bytes) {
+        g_fit_err = "null argument";
+        return WT_INVALID_ARGUMENT;
+    }
+    counts[0] = b->NM;
+    counts[1] = b->NB;
+    counts[2] = b->G;
+    counts[3] = b->W;
+    counts[4] = b->p;
+    *bytes = pack_layout(b->NM, b->NB, b->G).total;
+    return WT_OK;
+}
+
+wt_status wt_build_pack(const wt_build* b, void* dst, size_t cap, void* stream) {
+    if (!b || !dst) {
+        g_fit_err = "null argument";
+        return WT_INVALID_ARGUMENT;
+    }
+    const PackLayout L = pack_layout(b->NM, b->NB, b->G);
+    if (cap < L.total) {
+        g_fit_err = "wt_build_pack: destination smaller than the packed build";
+        return WT_INVALID_ARGUMENT;
+    }
+    int prev_dev = 0;
+    cudaGetDevice(&prev_dev);
+    cudaSetDevice(b->device);
+    DevRestore restore{prev_dev};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaStreamWaitEvent(s, b->done, 0));  // the build's stream may differ
+    char* d = static_cast<char*>(dst);
+    const PackHead h{kPackMagic, b->NM, b->NB, b->G, b->W, b->p, int64_t(L.total), 0};
+    CK(cudaMemcpyAsync(d, &h, sizeof(h), cudaMemcpyHostToDevice, s));  // pageable: staged before return
+    for (int a = 0; a < PA_N; ++a)
+        if (L.bytes[a]) CK(cudaMemcpyAsync(d + L.off[a], pack_ptr(b, a), L.bytes[a], cudaMemcpyDeviceToDevice, s));
+    return WT_OK;
+}
+
+wt_status wt_build_merge(const void* packed, size_t stride, int32_t n_parts, const int64_t* counts, int device,
+                         void* stream, wt_build** out) {
+    if (!packed || !counts || !out || n_parts <= 0) {
+        g_fit_err = "null argument";
+        return WT_INVALID_ARGUMENT;
+    }
+    *out = nullptr;
+    int64_t NM = 0, NB = 0, G = 0, W = -1, p = -1;
+    for (int r = 0; r < n_parts; ++r) {
+        const int64_t* c = counts + 5 * r;
+        if (c[0] < 0 || c[1] < 0 || c[2] < 0) {
+            g_fit_err = "wt_build_merge: negative count";
+            return WT_INVALID_ARGUMENT;
+        }
+        if (c[0] == 0) continue;  // a rank without macros
+        if (pack_layout(c[0], c[1], c[2]).total > stride) {
+            g_fit_err = "wt_build_merge: part larger than the stride";
+            return WT_INVALID_ARGUMENT;
+        }
+        if ((W >= 0 && c[3] != W) || (p >= 0 && c[4] != p)) {
+            g_fit_err = "wt_build_merge: parts fitted with different W / p";
+            return WT_INVALID_ARGUMENT;
+        }
+        W = c[3];
+        p = c[4];
+        NM += c[0];
+        NB += c[1];
+        G += c[2];
+    }
+    if (NM == 0) {
+        g_fit_err = "build_dual_table: no macro produced a table";
+        return WT_RUNTIME_ERROR;
+    }
+    if (NB >= INT32_MAX || G >= INT32_MAX) {
+        g_fit_err = "wt_build_merge: merged build exceeds 32-bit offsets";
+        return WT_UNSUPPORTED;
+    }
+    int prev_dev = 0;
+    cudaGetDevice(&prev_dev);
+    cudaSetDevice(device);
+    DevRestore restore{prev_dev};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto* B = new wt_build;
+    B->device = device;
+    struct Guard {
+        wt_build*& b;
+        cudaStream_t s;
+        bool ok = false;
+        ~Guard() {
+            if (ok || !b) return;
+            cudaStreamSynchronize(s);
+            build_release(b);
+            delete b;
+        }
+    } guard{B, s};
+    const PackLayout M = pack_layout(NM, NB, G);
+    {
+        void* blk = nullptr;
+        CK(cudaMallocFromPoolAsync(&blk, M.total, wtb::device_pool(device), s));
+        B->mem.push_back(blk);
+        for (int a = 0; a < PA_N; ++a) set_pack_ptr(B, a, static_cast<char*>(blk) + M.off[a]);
+    }
+    CK(cudaEventCreate(&B->ev0));
+    CK(cudaEventCreate(&B->ev1));
+    CK(cudaEventCreateWithFlags(&B->done, cudaEventDisableTiming));
+    CK(cudaEventRecord(B->ev0, s));
+    // segments: (part, array); offset arrays rebased, their closing entry
+    // taken from the last non-empty part only
+    int last = -1;
+    for (int r = 0; r < n_parts; ++r)
+        if (counts[5 * r] > 0) last = r;
+    std::vector<MergeSeg> segs;
+    int64_t bNM = 0, bNB = 0, bG = 0, max_words = 0;
+    for (int r = 0; r < n_parts; ++r) {
+        const int64_t* c = counts + 5 * r;
+        if (c[0] == 0) continue;
+        const PackLayout L = pack_layout(c[0], c[1], c[2]);
+        const char* src = static_cast<const char*>(packed) + size_t(r) * stride;
+        // destination element offsets of this part per array
+        const int64_t dst_el[PA_N] = {bNM, bNM, bNM, bNM, bNM, bNM, bNB, bNB, bNB, bNB, bNB, bG, bG, bG,
+                                      4 * bNM, 4 * bNB, bNB, bNB, bG, bG};
+        const int esz[PA_N] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 8, 8, 8, 8, 8, 8};
+        for (int a = 0; a < PA_N; ++a) {
+            int64_t bytes = int64_t(L.bytes[a]);
+            uint32_t add = 0;
+            if (a == PA_COFF || a == PA_AAOFF) {
+                if (r != last) bytes -= 4;  // the next part's first entry closes this part
+                add = uint32_t(a == PA_COFF ? bNB : bG);
+            } else if (a == PA_EOFF) {
+                add = uint32_t(bG);
+            }
+            if (bytes <= 0) continue;
+            MergeSeg sg{};
+            sg.src = reinterpret_cast<const uint32_t*>(src + L.off[a]);
+            sg.dst = reinterpret_cast<uint32_t*>(static_cast<char*>(B->mem[0]) + M.off[a] + dst_el[a] * esz[a]);
+            sg.words = bytes / 4;
+            sg.add = add;
+            segs.push_back(sg);
+            max_words = std::max(max_words, sg.words);
+        }
+        bNM += c[0];
+        bNB += c[1];
+        bG += c[2];
+    }
+    for (size_t i0 = 0; i0 < segs.size(); i0 += kMergeSegs) {
+        MergeArgs ma{};
+        ma.nseg = int32_t(std::min<size_t>(kMergeSegs, segs.size() - i0));
+        for (int i = 0; i < ma.nseg; ++i) ma.seg[i] = segs[i0 + i];
+        const int gx = int(std::min<int64_t>(64, std::max<int64_t>(1, (max_words + 255) / 256)));
+        k_build_merge<<<dim3(gx, ma.nseg), 256, 0, s>>>(ma);
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(B->ev1, s));
+    B->h_macro_id.resize(NM);
+    CK(cudaMemcpyAsync(B->h_macro_id.data(), B->t_macro, size_t(NM) * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));  // host macro ids (the engine plan needs them)
+    B->NM = int32_t(NM);
+    B->NB = NB;
+    B->G = G;
+    B->W = int32_t(W);
+    B->p = int32_t(p);
+    B->baselines = false;
+    CK(cudaEventRecord(B->done, s));
+    guard.ok = true;
+    *out = B;
     return WT_OK;
 }
 

@@ -39,7 +39,12 @@ def gather_grid(local_full: torch.Tensor, n_entries: int, group=None, fill=None)
     if hi > lo:
         mine[: hi - lo].copy_(local_full[lo:hi])
     # in-place all-gather: this rank's chunk already sits at its offset
-    dist.all_gather_into_tensor(staging, mine, group=group)
+    if staging.device.type == "cuda" and dist.get_backend(group) != "nccl":
+        host = staging.cpu()  # gloo with device tensors: through the host
+        dist.all_gather_into_tensor(host, host[rank * per: rank * per + per], group=group)
+        staging.copy_(host)
+    else:
+        dist.all_gather_into_tensor(staging, mine, group=group)
     local_full.copy_(staging[:n_entries])
     return staging
 
@@ -83,14 +88,17 @@ def fused_sharded_sweep(grid, group=None, stream=None):
 
 def sharded_sweep(grid, group=None, stream=None):
     """Fill `grid` (a capi.Grid, identical on every rank) cooperatively:
-    each rank sweeps its slice, then the NCCL all-gather replicates it."""
+    each rank sweeps its slice, then the NCCL all-gather replicates it.
+    Everything is ordered on `stream` (default: the current stream)."""
     ent = grid.entries_tensor()
+    st = stream if stream is not None else torch.cuda.current_stream(ent.device)
 
     def fill(lo, hi):
-        grid.sweep(lo, hi, stream=stream)
+        grid.sweep(lo, hi, stream=st)
 
-    gather_grid(ent, grid.n_entries, group=group, fill=fill)
-    grid.finalize(stream=stream)
+    with torch.cuda.stream(st):
+        gather_grid(ent, grid.n_entries, group=group, fill=fill)
+    grid.finalize(stream=st)
     return ent
 
 
@@ -190,3 +198,93 @@ def sharded_fit(records: dict, registry_ids, W: int = 0, p: int = 10, group=None
     parts = [None] * world
     dist.all_gather_object(parts, part, group=group)
     return merge_tables(parts)
+
+
+# ------------------------------------------------- device-resident sharded build
+# The multi-GPU build keeps the tables on the devices end to end: each rank
+# fits its registry slice from records resident in its HBM (wt_fit_build_
+# device), packs the tables into one blob (wt_build_pack), ONE all-gather
+# moves the blobs (NCCL over NVLink; equal strides, this rank's blob written
+# in place at its slot), and every rank merges them into the full build on
+# its device (wt_build_merge) and resolves its engine image there
+# (Engine.from_build).  Host traffic: two tiny all-gathers of counts/sizes
+# and the merged build's macro ids.
+
+PACK_ALIGN = 256
+
+
+def exchange_packed(nbytes: int, counts, pack, device, group=None):
+    """All-gather variable-size packed blobs.  `pack(dst)` writes this rank's
+    blob into the uint8 tensor `dst` (its slot of the gather buffer).
+    Returns (buffer [world * stride] uint8, stride, counts [world, 5]).
+    Ranks with nothing to send pass nbytes 0 and counts of zeros."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    nccl = dist.get_backend(group) == "nccl"
+    meta_dev = device if nccl else "cpu"
+    meta = torch.tensor([int(nbytes)] + [int(c) for c in counts], dtype=torch.int64, device=meta_dev)
+    allm = torch.empty((world, 6), dtype=torch.int64, device=meta_dev)
+    dist.all_gather_into_tensor(allm.view(-1), meta, group=group)
+    allm = allm.cpu()
+    stride = -(-int(allm[:, 0].max()) // PACK_ALIGN) * PACK_ALIGN
+    stride = max(stride, PACK_ALIGN)
+    buf = torch.empty(world * stride, dtype=torch.uint8, device=device)
+    mine = buf[rank * stride: (rank + 1) * stride]
+    if nbytes:
+        pack(mine)
+    if nccl:
+        dist.all_gather_into_tensor(buf, mine, group=group)  # in place
+    else:  # gloo (CPU tests; two processes on one GPU): staged through the host
+        host = buf.cpu() if buf.device.type != "cpu" else buf
+        dist.all_gather_into_tensor(host, host[rank * stride: (rank + 1) * stride], group=group)
+        if host is not buf:
+            buf.copy_(host)
+    return buf, stride, allm[:, 1:].numpy()
+
+
+def shard_records(records: dict, registry_ids, world: int, rank: int):
+    """This rank's macro slice and the records of those macros (host arrays)."""
+    ids = macro_shards(registry_ids, world)[rank]
+    return ids, records_of(records, ids)
+
+
+def sharded_build(records_dev: dict, shard_ids, W: int, p: int = 10, group=None, device: int = 0, stream=None):
+    """build_dual_table sharded by macro, tables kept on the devices.
+    `records_dev`: this rank's records (device tensors, capi.Build layout) of
+    the macros `shard_ids` (its contiguous registry slice, macro_shards).
+    W must be the global horizon (> 0; the reference's W <= 0 rule is a
+    global max -- resolve it first with global_w).  Returns the merged
+    capi.Build on this rank's device (the full registry's tables)."""
+    from . import capi
+
+    st = stream if stream is not None else torch.cuda.current_stream(device)
+    if W <= 0:
+        raise ValueError("sharded_build needs the global W (global_w)")
+    part = None
+    if len(shard_ids) and int(records_dev["g"].numel()):
+        part = capi.Build(records_dev, shard_ids, W, p, device=device, stream=st)
+    try:
+        if part is not None:
+            counts, nbytes = part.pack_info()
+        else:
+            counts, nbytes = [0, 0, 0, W, p], 0
+        with torch.cuda.stream(st):
+            buf, stride, allc = exchange_packed(nbytes, counts, lambda dst: part.pack(dst, stream=st),
+                                                torch.device("cuda", device), group=group)
+        return capi.Build.merge(buf, stride, allc, device=device, stream=st)
+    finally:
+        if part is not None:
+            part.close()
+
+
+def global_w(records_w, group=None, device=None):
+    """The reference's W for params.W <= 0: max r.w over ALL records
+    (model.cpp:201-203), an all-reduce(max) over the ranks' shards."""
+    import numpy as np
+
+    w = int(np.max(records_w)) if len(records_w) else 0
+    t = torch.tensor([w], dtype=torch.int64)
+    if dist.get_backend(group) == "nccl":
+        t = t.to(device if device is not None else "cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return int(t.item())

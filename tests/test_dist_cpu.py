@@ -67,3 +67,52 @@ def test_shard_bounds_cover_exactly():
                 assert hi - lo <= per
                 seen.extend(range(lo, hi))
             assert seen == list(range(n))
+
+
+# ---- build exchange protocol (dist.exchange_packed) on gloo -------------
+def _blob(rank):
+    # rank r sends 1000 * r + 37 bytes (rank 1 of 3 sends nothing), content
+    # a function of (rank, position); counts carry the rank
+    n = 0 if rank == 1 else 1000 * rank + 37
+    return n, torch.arange(n, dtype=torch.int64).mul(31).add(rank * 7).remainder(251).to(torch.uint8)
+
+
+def _xworker(rank, world, port, q):
+    from paper_2604_10187_b200.dist import PACK_ALIGN, exchange_packed
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, data = _blob(rank)
+        counts = [rank + 1, 2 * rank, 3 * rank, 40, 10] if n else [0, 0, 0, 40, 10]
+
+        def pack(dst):
+            assert dst.numel() >= n
+            dst[:n] = data
+
+        buf, stride, allc = exchange_packed(n, counts, pack, "cpu")
+        ok = stride % PACK_ALIGN == 0 and buf.numel() == world * stride
+        for r in range(world):
+            nr, dr = _blob(r)
+            ok = ok and stride >= nr and torch.equal(buf[r * stride: r * stride + nr], dr)
+            want = [r + 1, 2 * r, 3 * r, 40, 10] if nr else [0, 0, 0, 40, 10]
+            ok = ok and allc[r].tolist() == want
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_exchange_packed_blobs(world):
+    """Variable-size blobs (one rank empty) land at rank * stride on every
+    rank, with every rank's counts -- the layout wt_build_merge consumes."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_xworker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {r: True for r in range(world)}

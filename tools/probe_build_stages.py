@@ -27,7 +27,8 @@ for rep in range(6):
     e = capi.Engine.from_build(b, reg, n_sm=148)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
-    g = capi.Grid(e, [p[0] for p in p3], [p[1] for p in p3], 1, 65536)
+    g = capi.Grid(e, [p[0] for p in p3], [p[1] for p in p3], 1, 65536,
+                  stream=torch.cuda.current_stream() if os.environ.get("GRID_ASYNC") else None)
     torch.cuda.synchronize()
     t3 = time.perf_counter()
     g.sweep()
