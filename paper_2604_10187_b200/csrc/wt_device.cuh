@@ -234,7 +234,9 @@ __device__ __forceinline__ uint32_t eval_key(const DevImage& im, int32_t m, int3
                                              int64_t slot, int mode = 1) {
     uint32_t M, N, K;
     uint32_t key = 0;
-    if (!query_status(im, m, n, k, &M, &N, &K)) {
+    if (mode == 3) {  // no grouping (A/B): one key, list order kept chunk by chunk
+        key = 0;
+    } else if (!query_status(im, m, n, k, &M, &N, &K)) {
         int br = 1;
         while ((1 << br) < im.R) ++br;
         const uint32_t y2M = 2u * (M - 1u), y2N = 2u * (N - 1u);

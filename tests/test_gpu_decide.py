@@ -494,6 +494,7 @@ def test_sharded_sweep_equals_full(capi, synth256):
     {"WT_EVAL_KERNEL": "3"},
     {"WT_EVAL4_RPT": "4"},
     {"WT_EVAL4_RPT": "1"},
+    {"WT_EVAL_KEY_MODE": "3"},
     {"WT_BATCH_SLICE": "4100"},
     {"WT_SWEEP_SMEM_KB": "96"},
 ])
