@@ -150,6 +150,7 @@ struct EngineMeta {
     std::vector<int32_t> macro_id;  // ascending (config order)
     int32_t tm_min = 0, tn_min = 0;
     int64_t n_pool = 0;             // anchor pool entries
+    std::vector<int32_t> tm_vals;   // distinct t_m (ascending): grid M intervals
 };
 
 struct wt_engine {
@@ -193,6 +194,13 @@ struct wt_grid {
     int sweep_chunk = 0;
     void* mem = nullptr;
     bool pooled = false;    // mem from the library pool (wt_grid_create_async): not IPC-exportable
+    // M intervals on which every ceil(M / t_m) is constant: a grid entry
+    // depends on M only through those quotients (G = ceil(M/t_m) ceil(N/t_n)),
+    // so the sweep evaluates one representative M per interval and copies
+    // its entry over the interval (nrep = 0: plain sweep)
+    int32_t nrep = 0;
+    int32_t* d_mrep = nullptr;
+    std::vector<int32_t> h_mrep;
     int32_t* dN = nullptr;
     int32_t* dK = nullptr;
     uint64_t* dkeys = nullptr;
@@ -396,6 +404,10 @@ wt_status engine_build(wt_engine* e, const ImagePlan& P, const DevTables& T, cud
     h.special = special != 0;
     h.macro_id = P.macro_id;
     h.tm_min = P.tm_min;
+    h.tm_vals.clear();
+    for (size_t c = 0; c < C; ++c) h.tm_vals.push_back(P.tiles[4 * c]);
+    std::sort(h.tm_vals.begin(), h.tm_vals.end());
+    h.tm_vals.erase(std::unique(h.tm_vals.begin(), h.tm_vals.end()), h.tm_vals.end());
     h.tn_min = P.tn_min;
     h.n_pool = n_pool;
     DevImage& d = e->dev;
@@ -1159,6 +1171,30 @@ wt_status grid_create_impl(const wt_engine* e, const wt_grid_desc* desc, bool po
         g->hbits = bits;
     }
     const size_t o_hash = ar.take(htab.size() * sizeof(int4));
+    // M intervals: breakpoints at k * t_m + 1 for every distinct t_m; used
+    // when they cut the work by at least 4x
+    {
+        const int64_t mc = g->mcount;
+        std::vector<uint8_t> brk;
+        if (mc >= 64 && mc <= (int64_t(1) << 26) && !e->host.tm_vals.empty()) {
+            brk.assign(size_t(mc), 0);
+            brk[0] = 1;
+            for (int32_t tm : e->host.tm_vals) {
+                // M = k * tm + 1 >= m_lo + 1
+                int64_t k = (int64_t(desc->m_lo) + tm - 1) / tm;
+                for (int64_t M = k * tm + 1; M <= desc->m_hi; M += tm) brk[size_t(M - desc->m_lo)] = 1;
+            }
+            int64_t nb = 0;
+            for (uint8_t b : brk) nb += b;
+            if (nb * 4 <= mc && nb < INT32_MAX) {
+                g->h_mrep.reserve(size_t(nb));
+                for (int64_t i = 0; i < mc; ++i)
+                    if (brk[size_t(i)]) g->h_mrep.push_back(int32_t(desc->m_lo + i));
+                g->nrep = int32_t(nb);
+            }
+        }
+    }
+    const size_t o_mrep = ar.take(size_t(g->nrep) * 4);
     // run index storage (worst case: every entry its own run) when its block
     // table alone leaves room in the shared-memory budget
     static const int runs_kb = [] {
@@ -1194,6 +1230,10 @@ wt_status grid_create_impl(const wt_engine* e, const wt_grid_desc* desc, bool po
     g->tk_macro = g->topk ? reinterpret_cast<int32_t*>(base + o_tkm) : nullptr;
     g->tk_lat = g->topk ? reinterpret_cast<double*>(base + o_tkl) : nullptr;
     g->dhash = htab.empty() ? nullptr : reinterpret_cast<int4*>(base + o_hash);
+    if (g->nrep) {
+        g->d_mrep = reinterpret_cast<int32_t*>(base + o_mrep);
+        up(g->d_mrep, g->h_mrep.data(), g->h_mrep.size() * 4);
+    }
     if (g->dhash) up(g->dhash, htab.data(), htab.size() * sizeof(int4));
     if (want_runs) {
         g->runs.hdr = reinterpret_cast<int32_t*>(base + o_rhdr);
@@ -1294,8 +1334,45 @@ wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, v
     a.topk_lat = g->tk_lat;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t ce;
+    static const bool dedup = [] {
+        const char* v = std::getenv("WT_SWEEP_DEDUP");
+        return !v || std::atoi(v) != 0;
+    }();
     if (g->topk > 0) {
         ce = launch_sweep(e->dev, a, g->wide, s);
+    } else if (dedup && g->nrep > 0) {
+        // representatives of the intervals meeting [begin, end), swept into a
+        // scratch list, then copied over their intervals
+        auto rep_of = [&](int64_t flat) {
+            const int64_t p = flat / g->mcount;
+            const int32_t M = int32_t(g->m_lo + (flat - p * g->mcount));
+            const int64_t i = int64_t(std::upper_bound(g->h_mrep.begin(), g->h_mrep.end(), M) - g->h_mrep.begin()) - 1;
+            return p * g->nrep + i;
+        };
+        const int64_t rb = rep_of(begin), re = rep_of(end - 1) + 1;
+        SweepArgs ra = a;
+        ra.mcount = g->nrep;
+        ra.mrep = g->d_mrep;
+        ra.begin = rb;
+        ra.end = re;
+        static const int sweep_w = [] {
+            const char* v = std::getenv("WT_SWEEP_W");
+            return v ? std::atoi(v) : 1;
+        }();
+        const size_t eb = (size_t(re - rb) * sizeof(wt_grid_entry) + 255) & ~size_t(255);
+        const size_t sb = sweep_w ? 0 : sweep2_scratch_bytes(e->dev, ra);
+        void* scratch = nullptr;
+        ce = cudaMallocFromPoolAsync(&scratch, eb + sb, lib_pool(e->device), s);
+        if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep: scratch");
+        wt_grid_entry* rep = static_cast<wt_grid_entry*>(scratch);
+        // the sweep writes entry r at ra.entries + r: offset the list by -rb
+        ra.entries = rep - rb;
+        ce = sweep_w ? launch_sweep_w(e->dev, ra, s)
+                     : launch_sweep2(e->dev, ra, g->wide, sb ? static_cast<char*>(scratch) + eb : nullptr, s);
+        if (ce == cudaSuccess)
+            ce = launch_expand(g->entries, rep, rb, re, begin, end, g->m_lo, g->mcount, g->d_mrep, g->nrep, s);
+        cudaFreeAsync(scratch, s);
+        g_launches += sb ? 2 : 1;
     } else {
         void* scratch = nullptr;
         const size_t sb = sweep2_scratch_bytes(e->dev, a);

@@ -33,7 +33,10 @@ struct SweepArgs {
     const int32_t* N;  // [n_pairs] device
     const int32_t* K;
     int32_t m_lo;
-    int64_t mcount;    // M values per pair
+    int64_t mcount;    // M values per pair (representative sweep: intervals per pair)
+    // representative sweep (wt_sweep over M intervals): shape i of a pair has
+    // M = mrep[i] instead of m_lo + i; null = every M of [m_lo, m_lo + mcount)
+    const int32_t* mrep;
     int64_t begin, end;
     int32_t chunk;     // configs per shared-memory chunk
     wt_grid_entry* entries;
@@ -274,6 +277,14 @@ cudaError_t launch_serve(const DevImage& im, int64_t n_anchor, Mailbox* mb, uint
                          cudaStream_t st);
 size_t sweep2_scratch_bytes(const DevImage& im, const SweepArgs& a);
 cudaError_t launch_sweep2(const DevImage& im, const SweepArgs& a, bool wide, void* scratch, cudaStream_t st);
+// Warp-per-shape sweep (representative sweeps; no top-k).
+cudaError_t launch_sweep_w(const DevImage& im, const SweepArgs& a, cudaStream_t st);
+// Copies representative entries rep[r - rb], r in [rb, re), onto every grid
+// entry of their M interval inside the flat range [begin, end): interval i
+// of a pair covers M in [mrep[i], mrep[i + 1]) (the last up to m_lo + mcount).
+cudaError_t launch_expand(wt_grid_entry* entries, const wt_grid_entry* rep, int64_t rb, int64_t re, int64_t begin,
+                          int64_t end, int32_t m_lo, int64_t mcount, const int32_t* mrep, int32_t nrep,
+                          cudaStream_t st);
 cudaError_t launch_eval2(const DevImage& im, const EvalArgs& a, int grid, cudaStream_t st);
 // row-grouped list evaluation (wt_eval3.cu): key + histogram, scan, scatter,
 // evaluation; scratch of eval3_scratch_bytes(a.n) (a.n = host upper bound)

@@ -53,6 +53,11 @@ __device__ __forceinline__ bool lex_less(double a, int ia, double b, int ib) {
 
 constexpr double kInf = __builtin_huge_val();
 
+// M of shape `off` of a pair: consecutive M, or the interval representative
+__device__ __forceinline__ uint32_t sweep_M(const SweepArgs& a, int64_t off) {
+    return a.mrep ? uint32_t(__ldg(a.mrep + off)) : uint32_t(a.m_lo + off);
+}
+
 }  // namespace
 
 struct Part {  // per-split partial argmins, [S][n]
@@ -89,8 +94,8 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
         const int32_t p = int32_t(seg0 / a.mcount);
         const int64_t seg_end = min(t1, int64_t(p + 1) * a.mcount);
         const uint32_t Np = uint32_t(a.N[p]), Kp = uint32_t(a.K[p]);
-        const uint32_t Mlo = uint32_t(a.m_lo + (seg0 - int64_t(p) * a.mcount));
-        const uint32_t Mhi = uint32_t(a.m_lo + (seg_end - 1 - int64_t(p) * a.mcount));
+        const uint32_t Mlo = sweep_M(a, seg0 - int64_t(p) * a.mcount);
+        const uint32_t Mhi = sweep_M(a, seg_end - 1 - int64_t(p) * a.mcount);
 
         double best[RPT];
         int bc[RPT];
@@ -98,7 +103,7 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
             const int64_t idx = seg0 + int64_t(j) * kT2 + tid;
-            const uint32_t M = idx < seg_end ? uint32_t(a.m_lo + (idx - int64_t(p) * a.mcount)) : Mlo;
+            const uint32_t M = idx < seg_end ? sweep_M(a, idx - int64_t(p) * a.mcount) : Mlo;
             y2[j] = 2u * (M - 1u);
             best[j] = kInf;
             bc[j] = -1;
@@ -295,6 +300,129 @@ __global__ void __launch_bounds__(kT2) k_sweep2(DevImage im, SweepArgs a, int ca
     }
 }
 
+// Warp-per-shape sweep (the representative sweep: few shapes, many
+// configs): the 32 lanes take the tile-class segments in turn -- wave row,
+// L bucket and pruning mask per (shape, segment), every surviving config of
+// the segment evaluated (coefficient rows from theta2t) -- then a warp-shuffle
+// argmin on (latency, config index), i.e. tune()'s ascending strict-< scan
+// (tuner.cpp:135-149; +inf and NaN never win), and lane 0 runs Stage II and
+// stores the entry.
+template <bool SPECIAL>
+__global__ void __launch_bounds__(256) k_sweep_w(DevImage im, SweepArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const int C = im.C, R = im.R;
+    for (int64_t idx = a.begin + ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); idx < a.end; idx += nw) {
+        const int32_t p = int32_t(idx / a.mcount);
+        const uint32_t M = sweep_M(a, idx - int64_t(p) * a.mcount);
+        const uint32_t Np = uint32_t(__ldg(a.N + p)), Kp = uint32_t(__ldg(a.K + p));
+        const uint32_t y2M = 2u * (M - 1u), y2N = 2u * (Np - 1u), y2K = 2u * (Kp - 1u);
+        double best = kInf;
+        int bc = INT32_MAX;
+        uint32_t acc = 0;
+        for (int s = lane; s < im.nseg; s += 32) {
+            const uint4 mg = __ldg(im.seg_magic + s);
+            const int4 st = __ldg(im.seg_tiles + s);
+            const int pos = __ldg(im.seg_pos + s);
+            uint64_t g;
+            const uint32_t row = row_for(im, y2M, y2N, mg, &g);
+            const uint32_t L = mdiv2(y2K, mg.z, (mg.w >> 16) & 0xffu) + 1u;
+            const uint32_t lb = uint32_t(min(31 - __clz(int(L)), kLB - 1));
+            uint32_t m = st.w >= 32 ? 0xffffffffu : ((1u << st.w) - 1u);
+            if (im.prune) m &= __ldg(im.segmask + (size_t(s) * R + row) * kLB + lb);
+            if (SPECIAL) acc |= __ldg(im.segor + size_t(s) * R + row);
+            if (im.eval_count) atomicAdd(im.eval_count, (unsigned long long)__popc(m));
+            const double gd = u64_to_f64(g), ld = u32_to_f64(L);
+            const double4* tp = im.theta2t + size_t(row) * C + pos;
+            for (; m; m &= m - 1u) {
+                const int c = __ffs(int(m)) - 1;
+                const double4 th = ldg_row(tp + c);
+                const double t = bilinear(th.x, th.y, __dmul_rn(th.z, ld), th.w, gd, ld);
+                const int ci = __ldg(im.cls_cfg + pos + c);
+                if (t < best || (t == best && ci < bc && bc != INT32_MAX)) {
+                    best = t;
+                    bc = ci;
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+            const int oc = __shfl_xor_sync(0xffffffffu, bc, off);
+            acc |= __shfl_xor_sync(0xffffffffu, acc, off);
+            if (oc != INT32_MAX && (bc == INT32_MAX || ob < best || (ob == best && oc < bc))) {
+                best = ob;
+                bc = oc;
+            }
+        }
+        if (lane != 0) continue;
+        const int c = bc != INT32_MAX ? bc : -1;
+        uint64_t g = 0;
+        int64_t l = 0;
+        if (c >= 0) {
+            const int4 tl4 = __ldg(im.tiles + c);
+            g = uint64_t((M + uint32_t(tl4.x) - 1) / uint32_t(tl4.x)) *
+                uint64_t((uint64_t(Np) + uint32_t(tl4.y) - 1) / uint32_t(tl4.y));
+            l = int64_t((uint64_t(Kp) + uint32_t(tl4.z) - 1) / uint32_t(tl4.z));
+        }
+        const Final f = finish(im, c, 0.0, g, l, acc);
+        const bool ok = (f.flags >> 24) == 0;
+        const double lat = ok ? best : __longlong_as_double(0x7ff8000000000000LL);
+        int4 lo, hi;
+        lo.x = __double2loint(lat);
+        lo.y = __double2hiint(lat);
+        lo.z = f.macro;
+        lo.w = f.micro;
+        hi.x = f.wave;
+        hi.y = int(f.flags);
+        hi.z = f.comps;
+        hi.w = __float_as_int(f.tail);
+        store_entry(a, idx, lo, hi);
+    }
+}
+
+cudaError_t launch_sweep_w(const DevImage& im, const SweepArgs& a, cudaStream_t st) {
+    const int64_t n = a.end - a.begin;
+    if (n <= 0) return cudaSuccess;
+    const int grid = int(std::min<int64_t>((n + 7) / 8, int64_t(device_sms()) * 8));
+    if (im.special) k_sweep_w<true><<<grid, 256, 0, st>>>(im, a);
+    else k_sweep_w<false><<<grid, 256, 0, st>>>(im, a);
+    return cudaGetLastError();
+}
+
+// Representative sweep expansion: one warp per M interval copies the
+// interval's entry (32 bytes, loaded once) onto every M of the interval that
+// lies in [begin, end) -- consecutive lanes, consecutive entries.
+__global__ void __launch_bounds__(256) k_expand(wt_grid_entry* entries, const wt_grid_entry* rep, int64_t rb,
+                                                int64_t re, int64_t begin, int64_t end, int32_t m_lo,
+                                                int64_t mcount, const int32_t* mrep, int32_t nrep) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t r = rb + ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); r < re; r += nw) {
+        const int64_t p = r / nrep;
+        const int32_t i = int32_t(r - p * nrep);
+        const int64_t lo = max(begin, p * mcount + (__ldg(mrep + i) - m_lo));
+        const int64_t hi = min(end, i + 1 < nrep ? p * mcount + (__ldg(mrep + i + 1) - m_lo) : (p + 1) * mcount);
+        const int4* src = reinterpret_cast<const int4*>(rep + (r - rb));
+        const int4 e0 = __ldg(src), e1 = __ldg(src + 1);
+        for (int64_t x = lo + lane; x < hi; x += 32) {
+            int4* d = reinterpret_cast<int4*>(entries + x);
+            d[0] = e0;
+            d[1] = e1;
+        }
+    }
+}
+
+cudaError_t launch_expand(wt_grid_entry* entries, const wt_grid_entry* rep, int64_t rb, int64_t re, int64_t begin,
+                          int64_t end, int32_t m_lo, int64_t mcount, const int32_t* mrep, int32_t nrep,
+                          cudaStream_t st) {
+    if (re <= rb) return cudaSuccess;
+    const int64_t warps = re - rb;
+    const int grid = int(std::min<int64_t>((warps + 7) / 8, int64_t(device_sms()) * 8));
+    k_expand<<<grid, 256, 0, st>>>(entries, rep, rb, re, begin, end, m_lo, mcount, mrep, nrep);
+    return cudaGetLastError();
+}
+
 // Merge of the config splits + Stage II epilogue (grid mode).
 __global__ void k_sweep_merge(DevImage im, SweepArgs a, Part part) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -315,7 +443,7 @@ __global__ void k_sweep_merge(DevImage im, SweepArgs a, Part part) {
     }
     const int64_t idx = a.begin + i;
     const int32_t p = int32_t(idx / a.mcount);
-    const uint32_t M = uint32_t(a.m_lo + (idx - int64_t(p) * a.mcount));
+    const uint32_t M = sweep_M(a, idx - int64_t(p) * a.mcount);
     const uint32_t Np = uint32_t(a.N[p]), Kp = uint32_t(a.K[p]);
     uint64_t g = 0;
     int64_t l = 0;

@@ -553,7 +553,9 @@ __global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval
                     tt = __dadd_rn(tt, __dmul_rn(th[j].y, gd[j]));
                     tt = __dadd_rn(tt, __dmul_rn(th[j].z, ld[j]));
                     tt = __dadd_rn(tt, th[j].w);
-                    if (tt < best[j] || (tt == best[j] && ci < bci[j])) {
+                    // ties go to the smaller index only between real winners:
+                    // +inf never wins (tune() starts from +inf with strict <)
+                    if (tt < best[j] || (tt == best[j] && ci < bci[j] && bci[j] != INT32_MAX)) {
                         best[j] = tt;
                         bci[j] = ci;
                     }

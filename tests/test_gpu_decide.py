@@ -400,6 +400,33 @@ def test_empty_coeff_table_is_runtime_error(capi, orc, synth256):
     assert want["status"][0] == 2  # w <= W for table 3 -> runtime_error
 
 
+def test_all_infinite_candidates_are_runtime_error(capi, orc, synth256):
+    """Coefficients that overflow: for large shapes every config predicts
+    +inf, and tune() -- best_latency starts at +inf, strict < -- finds no
+    winner (the reference dereferences null; the restatement reports
+    runtime_error).  Small shapes keep finite candidates.  Grid (sweep +
+    gather) and list paths must agree with the restatement."""
+    from paper_2604_10187_b200 import synthetic as S
+
+    cfg, t, reg = synth256
+    t2 = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in t.items()}
+    t2["coeff_theta"][0::4] = 1e308
+    t2["theta_ext"][0::4] = 1e308
+    eng = capi.Engine(t2, reg, n_sm=148)
+    pairs = S.LLAMA3_8B[:2]
+    grid = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], 1, 600)
+    grid.sweep()
+    rng = np.random.default_rng(4)
+    M = np.concatenate([rng.integers(1, 600, 3000), rng.integers(1, 40, 1000)]).astype(np.int32)
+    N = np.concatenate([np.full(3000, pairs[0][0]), rng.integers(1, 70, 1000)]).astype(np.int32)
+    K = np.concatenate([np.full(3000, pairs[0][1]), rng.integers(1, 70, 1000)]).astype(np.int32)
+    tiles = {int(i): (int(a), int(b), int(c)) for i, a, b, c in zip(cfg["id"], cfg["t_m"], cfg["t_n"], cfg["t_k"])}
+    want = orc.tune(po.FlatTables(U.pytables_from_arrays(t2), tiles), 148, 1, M, N, K)
+    assert (want["status"] == 2).any() and (want["status"] == 0).any()
+    assert_same(tune_gpu(capi, eng, M, N, K, grid=grid), want)
+    assert_same(tune_gpu(capi, eng, M, N, K), want)
+
+
 def test_attention_family(capi, orc):
     """FlashAttention registries: g = n_heads*ceil(s_q/t_q), l = ceil(s_kv/t_kv)
     (kernel_map.cpp:258-263) -- the oracle evaluates it as dense with t_n=1."""
@@ -477,6 +504,45 @@ def test_sharded_sweep_equals_full(capi, synth256):
     assert torch.equal(g1.entries_tensor(), g2.entries_tensor())
 
 
+@pytest.mark.parametrize("m_lo,m_hi", [(1, 5000), (37, 4133), (129, 129 + 63)])
+def test_partial_sweep_writes_only_its_range(capi, orc, synth256, m_lo, m_hi):
+    """The representative sweep (one M per interval of constant ceil(M/t_m),
+    copied over the interval) writes exactly [begin, end): entries outside a
+    partial range keep their poison, entries inside equal the full sweep and
+    the restatement, for M ranges that start off the t_m multiples."""
+    from paper_2604_10187_b200 import synthetic as S
+
+    cfg, t, reg = synth256
+    eng = capi.Engine(t, reg, n_sm=148)
+    pairs = S.LLAMA3_8B[:3]
+    full = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], m_lo, m_hi)
+    full.sweep()
+    part = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], m_lo, m_hi)
+    n = part.n_entries
+    rng = np.random.default_rng(m_lo)
+    for _ in range(4):
+        a, b = sorted(int(x) for x in rng.integers(0, n + 1, 2))
+        ent = part.entries_tensor()
+        ent.fill_(-7)
+        torch.cuda.synchronize()
+        part.sweep(a, b)
+        torch.cuda.synchronize()
+        got = part.entries_tensor()
+        assert bool((got[:a] == -7).all()) and bool((got[b:] == -7).all())
+        assert torch.equal(got[a:b], full.entries_tensor()[a:b])
+    # every full-grid entry against the restatement
+    M = np.tile(np.arange(m_lo, m_hi + 1, dtype=np.int32), len(pairs))
+    N = np.repeat(np.array([p[0] for p in pairs], np.int32), m_hi - m_lo + 1)
+    K = np.repeat(np.array([p[1] for p in pairs], np.int32), m_hi - m_lo + 1)
+    tiles = {int(i): (int(x), int(y), int(z)) for i, x, y, z in zip(cfg["id"], cfg["t_m"], cfg["t_n"], cfg["t_k"])}
+    want = orc.tune(po.FlatTables(U.pytables_from_arrays(t), tiles), 148, 1, M, N, K)
+    e = full.entries_tensor().cpu().numpy()
+    lat = e[:, :2].copy().view(np.float64).ravel()
+    np.testing.assert_array_equal(e[:, 2], want["macro"])
+    np.testing.assert_array_equal(e[:, 3], want["micro"])
+    np.testing.assert_array_equal(lat.view(np.int64), want["lat"].view(np.int64))
+
+
 @pytest.mark.parametrize("env", [
     {"WT_SWEEP_RPT": "2", "WT_EVAL_RPT": "2"},
     {"WT_SWEEP_SMEM_KB": "24", "WT_EVAL_SMEM_KB": "64"},
@@ -497,6 +563,8 @@ def test_sharded_sweep_equals_full(capi, synth256):
     {"WT_EVAL_KEY_MODE": "3"},
     {"WT_BATCH_SLICE": "4100"},
     {"WT_SWEEP_SMEM_KB": "96"},
+    {"WT_SWEEP_DEDUP": "0"},
+    {"WT_SWEEP_W": "0"},
 ])
 def test_launch_variants(capi, env):
     """Every launch shape the tuning knobs can select stays bit-exact."""
