@@ -668,16 +668,22 @@ __global__ void __launch_bounds__(32 * kQWarps, 6) k_qfit(const double* sg, cons
 // column, octet order), in a [kORows][5] shared slab or -- above kORows --
 // the problem's own global scratch (5 doubles per sample).
 __global__ void __launch_bounds__(32 * kOWarps) k_ofit(const double* sg, const double* sl, const double* st,
-                                                       Buckets b, double* gscr) {
+                                                       Buckets b, double* gscr, int span) {
     __shared__ double slab[kOWarps][kORows * 5];
     const int lane = threadIdx.x & 31;
     Grp<8> G{lane >> 3, lane & 7, 0xffffffffu, 0xFFu << (lane & 24)};
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
     double* sA = slab[threadIdx.x >> 5];
-    for (int64_t pi = warp; pi < b.nb; pi += nw) {
+    // the warp scans `span` (<= 32) problems at a time (one per lane) and
+    // solves the large ones among them in ascending order: span 32 when few
+    // problems are large (buckets), 1 when most are (pooled windows)
+    for (int64_t base = warp * span; base < b.nb; base += nw * span) {
+      const int64_t mine = base + lane;
+      const bool big = lane < span && mine < b.nb && b.shi[mine] - b.slo[mine] > kQRows;
+      for (unsigned todo = __ballot_sync(0xffffffffu, big); todo; todo &= todo - 1u) {
+        const int64_t pi = base + (__ffs(int(todo)) - 1);
         const int64_t lo = b.slo[pi], n = b.shi[pi] - lo;
-        if (n <= kQRows) continue;
         double* A = n <= kORows ? sA : gscr + kQScr * lo;
         const FitOut o = group_fit<8>(sg + lo, sl + lo, st + lo, int(n), A, 4, A + 4 * n, 1, G, b.r2 || b.mape);
         if (lane == 0) {
@@ -687,6 +693,7 @@ __global__ void __launch_bounds__(32 * kOWarps) k_ofit(const double* sg, const d
             b.degen[pi] = o.degenerate;
         }
         __syncwarp();  // the slab is reused by the warp's next problem
+      }
     }
 }
 
@@ -700,9 +707,10 @@ cudaError_t launch_qfit(bool pooled, const double* sg, const double* sl, const d
     const int gq = int(std::max<int64_t>(1, std::min<int64_t>((b.nb + 8 * kQWarps - 1) / (8 * kQWarps),
                                                               pooled ? int64_t(nsm) : cap)));
     k_qfit<<<gq, 32 * kQWarps, 0, s>>>(sg, sl, st, b);
-    const int go = int(std::max<int64_t>(1, std::min<int64_t>((b.nb + kOWarps - 1) / kOWarps,
+    const int span = pooled ? 1 : 32;
+    const int go = int(std::max<int64_t>(1, std::min<int64_t>((b.nb + span * kOWarps - 1) / (span * kOWarps),
                                                               pooled ? cap : int64_t(nsm) * 2)));
-    k_ofit<<<go, 32 * kOWarps, 0, s>>>(sg, sl, st, b, gscr);
+    k_ofit<<<go, 32 * kOWarps, 0, s>>>(sg, sl, st, b, gscr, span);
     return cudaGetLastError();
 }
 
