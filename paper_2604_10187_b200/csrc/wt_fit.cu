@@ -679,21 +679,21 @@ __global__ void __launch_bounds__(32 * kOWarps) k_ofit(const double* sg, const d
     // solves the large ones among them in ascending order: span 32 when few
     // problems are large (buckets), 1 when most are (pooled windows)
     for (int64_t base = warp * span; base < b.nb; base += nw * span) {
-      const int64_t mine = base + lane;
-      const bool big = lane < span && mine < b.nb && b.shi[mine] - b.slo[mine] > kQRows;
-      for (unsigned todo = __ballot_sync(0xffffffffu, big); todo; todo &= todo - 1u) {
-        const int64_t pi = base + (__ffs(int(todo)) - 1);
-        const int64_t lo = b.slo[pi], n = b.shi[pi] - lo;
-        double* A = n <= kORows ? sA : gscr + kQScr * lo;
-        const FitOut o = group_fit<8>(sg + lo, sl + lo, st + lo, int(n), A, 4, A + 4 * n, 1, G, b.r2 || b.mape);
-        if (lane == 0) {
-            for (int c = 0; c < 4; ++c) b.coeff[4 * pi + c] = o.c[c];
-            if (b.r2) b.r2[pi] = o.r2;
-            if (b.mape) b.mape[pi] = o.mape;
-            b.degen[pi] = o.degenerate;
+        const int64_t mine = base + lane;
+        const bool big = lane < span && mine < b.nb && b.shi[mine] - b.slo[mine] > kQRows;
+        for (unsigned todo = __ballot_sync(0xffffffffu, big); todo; todo &= todo - 1u) {
+            const int64_t pi = base + (__ffs(int(todo)) - 1);
+            const int64_t lo = b.slo[pi], n = b.shi[pi] - lo;
+            double* A = n <= kORows ? sA : gscr + kQScr * lo;
+            const FitOut o = group_fit<8>(sg + lo, sl + lo, st + lo, int(n), A, 4, A + 4 * n, 1, G, b.r2 || b.mape);
+            if (lane == 0) {
+                for (int c = 0; c < 4; ++c) b.coeff[4 * pi + c] = o.c[c];
+                if (b.r2) b.r2[pi] = o.r2;
+                if (b.mape) b.mape[pi] = o.mape;
+                b.degen[pi] = o.degenerate;
+            }
+            __syncwarp();  // the slab is reused by the warp's next problem
         }
-        __syncwarp();  // the slab is reused by the warp's next problem
-      }
     }
 }
 
