@@ -327,6 +327,12 @@ wt_status wt_grid_destroy(wt_grid* g);
  * use an index built for earlier entries, whatever stream built it. */
 wt_status wt_grid_storage(const wt_grid* g, wt_grid_entry** entries, int64_t* n_entries,
                           int32_t** topk_macro, double** topk_latency);
+/* Shapes a full sweep of the grid actually evaluates: a grid entry depends
+ * on M only through ceil(M / t_m) for the engine's tile heights, so the sweep
+ * takes one representative M per interval of constant quotients and copies
+ * its entry over the interval (n_pairs * intervals; equals n_entries when the
+ * intervals do not cut the work at least 4x and every M is evaluated). */
+int64_t wt_grid_representatives(const wt_grid* g);
 /* Fills entries [begin, end) (flattened index) -- one shard of the sweep.
  * A full-range sweep also rebuilds the grid's run index (below); a partial
  * one invalidates it until wt_grid_finalize. */

@@ -93,7 +93,7 @@ class wt_build_result(C.Structure):
 EXPORTS = (
     "wt_last_error wt_version wt_abi_version wt_engine_create wt_engine_destroy wt_engine_info_get "
     "wt_engine_config_index wt_engine_set_prune wt_engine_count_evals wt_engine_prune_masks wt_tune_batch wt_tune_batch_i64 wt_gather_batch_i64 wt_tune_grouped_batch wt_predict_batch wt_explain "
-    "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_create_async wt_grid_destroy wt_grid_storage wt_sweep wt_grid_finalize "
+    "wt_engine_anchor_map wt_nearest_anchor_batch wt_grid_create wt_grid_create_async wt_grid_destroy wt_grid_representatives wt_grid_storage wt_sweep wt_grid_finalize "
     "wt_fit_build_device wt_build_result_get wt_build_pack_info wt_build_pack wt_build_merge wt_engine_create_from_build wt_gather_batch wt_decide_host_sync wt_decide_host_stream_sync wt_launch_count wt_fit_build wt_build_free wt_fit_bucket_batch "
     "wt_simulate_batch wt_profile_sim wt_tune_one wt_engine_set_resident wt_baseline_create "
     "wt_baseline_destroy wt_baseline_tune_batch wt_baseline_predict_batch wt_set_kernel_timing wt_kernel_time_ms "
@@ -113,6 +113,7 @@ def lib():
         L.wt_launch_count.restype = C.c_int64
         L.wt_engine_config_index.restype = C.c_int32
         L.wt_engine_anchor_map.restype = C.c_int32
+        L.wt_grid_representatives.restype = C.c_int64
         _lib = L
     return _lib
 
@@ -391,6 +392,7 @@ class Grid:
         tkm, tkl = C.c_void_p(), C.c_void_p()
         check(lib().wt_grid_storage(h, C.byref(ent), C.byref(n), C.byref(tkm), C.byref(tkl)))
         self.entries_ptr, self.n_entries = ent.value, n.value
+        self.n_representatives = int(lib().wt_grid_representatives(h))
         self.topk_macro_ptr, self.topk_lat_ptr = tkm.value, tkl.value
 
     def close(self):

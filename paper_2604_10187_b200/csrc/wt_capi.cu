@@ -1298,6 +1298,11 @@ wt_status wt_grid_destroy(wt_grid* g) {
     return WT_OK;
 }
 
+int64_t wt_grid_representatives(const wt_grid* g) {
+    if (!g) return 0;
+    return g->nrep > 0 ? int64_t(g->nrep) * g->n_pairs : g->n_entries;
+}
+
 wt_status wt_grid_storage(const wt_grid* g, wt_grid_entry** entries, int64_t* n_entries,
                           int32_t** topk_macro, double** topk_latency) {
     if (!g) return set_err(WT_INVALID_ARGUMENT, "null grid");

@@ -519,6 +519,7 @@ def test_partial_sweep_writes_only_its_range(capi, orc, synth256, m_lo, m_hi):
     full.sweep()
     part = capi.Grid(eng, [p[0] for p in pairs], [p[1] for p in pairs], m_lo, m_hi)
     n = part.n_entries
+    assert full.n_representatives * 4 <= n  # the sweep evaluates one M per interval
     rng = np.random.default_rng(m_lo)
     for _ in range(4):
         a, b = sorted(int(x) for x in rng.integers(0, n + 1, 2))
