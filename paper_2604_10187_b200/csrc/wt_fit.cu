@@ -405,32 +405,44 @@ struct Ranges {
     int wmin, wmax, umin, umax;
 };
 
-// Field ranges for the sort-key packing: grid-stride, warp reductions, one
-// set of atomics per warp (a per-record atomic on 8 hot words serialises).
-// The micro field is micro - (smallest micro of the record's macro): umin =
-// 0, umax = its largest value over valid records.
-__global__ void k_ranges(Rec rc, const int64_t* idx, int64_t n, const int32_t* mpos, const int32_t* umin_m,
-                         Ranges* out) {
+// Field ranges for the sort-key packing: a full-occupancy grid, four
+// records per thread per trip (independent loads in flight), warp then
+// block reductions, one set of atomics per block (a per-record atomic on 8
+// hot words serialises).  The micro field is micro - (smallest micro of the
+// record's macro): umin = 0, umax = its largest value over valid records.
+__global__ void __launch_bounds__(256) k_ranges(Rec rc, const int64_t* idx, int64_t n, const int32_t* mpos,
+                                                const int32_t* umin_m, Ranges* out) {
     unsigned long long gmin = ~0ULL, gmax = 0, lmin = ~0ULL, lmax = 0;
     int wmin = INT_MAX, wmax = INT_MIN, umin = INT_MAX, umax = INT_MIN;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t r = idx ? idx[i] : i;  // idx == null: every record
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    auto take = [&](int64_t r) {
         // offset by 2^63 so signed order becomes unsigned order
         const unsigned long long g = (unsigned long long)rc.g[r] ^ 0x8000000000000000ULL;
         const unsigned long long l = (unsigned long long)rc.l[r] ^ 0x8000000000000000ULL;
+        const int w = rc.w[r];
+        const int32_t mp = mpos[r];
+        const int32_t mu = rc.micro[r];
         gmin = min(gmin, g);
         gmax = max(gmax, g);
         lmin = min(lmin, l);
         lmax = max(lmax, l);
-        wmin = min(wmin, rc.w[r]);
-        wmax = max(wmax, rc.w[r]);
-        const int32_t mp = mpos[r];
+        wmin = min(wmin, w);
+        wmax = max(wmax, w);
         if (mp != INT_MAX) {
             umin = 0;
-            const long long ur = (long long)rc.micro[r] - umin_m[mp];
+            const long long ur = (long long)mu - umin_m[mp];
             umax = max(umax, int(ur < INT_MAX ? ur : INT_MAX));
         }
+    };
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n; i += 4 * stride) {
+        int64_t r[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = idx ? idx[i + k * stride] : i + k * stride;  // idx == null: every record
+#pragma unroll
+        for (int k = 0; k < 4; ++k) take(r[k]);
     }
+    for (; i < n; i += stride) take(idx ? idx[i] : i);
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
         gmin = min(gmin, __shfl_xor_sync(FULL, gmin, off));
@@ -442,19 +454,33 @@ __global__ void k_ranges(Rec rc, const int64_t* idx, int64_t n, const int32_t* m
     wmax = __reduce_max_sync(FULL, wmax);
     umin = __reduce_min_sync(FULL, umin);
     umax = __reduce_max_sync(FULL, umax);
-    if ((threadIdx.x & 31) == 0) {
-        atomicMin(&out->gmin, gmin);
-        atomicMax(&out->gmax, gmax);
-        atomicMin(&out->lmin, lmin);
-        atomicMax(&out->lmax, lmax);
-        atomicMin(&out->wmin, wmin);
-        atomicMax(&out->wmax, wmax);
-        atomicMin(&out->umin, umin);
-        atomicMax(&out->umax, umax);
+    __shared__ Ranges part[8];
+    const int wid = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) part[wid] = Ranges{gmin, gmax, lmin, lmax, wmin, wmax, umin, umax};
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Ranges t = part[0];
+        for (int k = 1; k < int(blockDim.x >> 5); ++k) {
+            t.gmin = min(t.gmin, part[k].gmin);
+            t.gmax = max(t.gmax, part[k].gmax);
+            t.lmin = min(t.lmin, part[k].lmin);
+            t.lmax = max(t.lmax, part[k].lmax);
+            t.wmin = min(t.wmin, part[k].wmin);
+            t.wmax = max(t.wmax, part[k].wmax);
+            t.umin = min(t.umin, part[k].umin);
+            t.umax = max(t.umax, part[k].umax);
+        }
+        atomicMin(&out->gmin, t.gmin);
+        atomicMax(&out->gmax, t.gmax);
+        atomicMin(&out->lmin, t.lmin);
+        atomicMax(&out->lmax, t.lmax);
+        atomicMin(&out->wmin, t.wmin);
+        atomicMax(&out->wmax, t.wmax);
+        atomicMin(&out->umin, t.umin);
+        atomicMax(&out->umax, t.umax);
     }
 }
 
-// One key field: value - base, `bits` wide, placed at `shift`.
 struct Field {
     int which;  // 0 g, 1 micro, 2 l, 3 w, 4 mpos
     unsigned long long base;
@@ -494,6 +520,14 @@ __global__ void k_group_flags(Rec rc, const int32_t* mpos, const int64_t* ordA, 
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     gflag[i] = (i == 0 || !same_group(rc, mpos, ordA[i], ordA[i - 1])) ? 1 : 0;
+}
+
+// The same from order A's sorted packed keys (one packing pass): records
+// are in one group iff their keys agree above the l field's shift.
+__global__ void k_group_flags_k(const unsigned long long* keys, int64_t n, int shift_l, int32_t* gflag) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    gflag[i] = (i == 0 || (keys[i] >> shift_l) != (keys[i - 1] >> shift_l)) ? 1 : 0;
 }
 
 __global__ void k_group_starts(const int32_t* gflag, const int32_t* gid, int64_t n, int64_t* gstart) {
@@ -586,6 +620,35 @@ __global__ void k_group_meta(Rec rc, const int32_t* mpos, const int64_t* ordA, i
         const int64_t r0 = ordA[gr.start[q - 1]];
         nm = mpos[r0] != mpos[r];
         nb = nm || rc.w[r0] != rc.w[r];
+    }
+    bflag[q] = nb;
+    mflag[q] = nm;
+}
+
+struct KeyFields {  // order A's single packing pass: shift / width / base of l, w, macro position
+    int sl, bl, sw, bw, sm, bm;
+    unsigned long long base_l, base_w;
+};
+__device__ __forceinline__ unsigned long long kfield(unsigned long long k, int shift, int bits) {
+    return bits >= 64 ? k >> shift : (k >> shift) & ((1ULL << bits) - 1ULL);
+}
+
+// k_group_meta from the sorted keys (the group's first record's key)
+__global__ void k_group_meta_k(const unsigned long long* keys, KeyFields kf, int64_t G, Groups gr, int64_t* gm,
+                               int64_t* gw, int64_t* gl, int32_t* bflag, int32_t* mflag) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= G) return;
+    const unsigned long long k = keys[gr.start[q]];
+    const int64_t m = int64_t(kfield(k, kf.sm, kf.bm));
+    const int64_t w = (long long)(kfield(k, kf.sw, kf.bw) + kf.base_w);
+    gm[q] = m;
+    gw[q] = w;
+    gl[q] = (long long)((kfield(k, kf.sl, kf.bl) + kf.base_l) ^ 0x8000000000000000ULL);
+    int nb = 1, nm = 1;
+    if (q > 0) {
+        const unsigned long long k0 = keys[gr.start[q - 1]];
+        nm = int64_t(kfield(k0, kf.sm, kf.bm)) != m;
+        nb = nm || (long long)(kfield(k0, kf.sw, kf.bw) + kf.base_w) != w;
     }
     bflag[q] = nb;
     mflag[q] = nm;
@@ -1157,8 +1220,11 @@ std::vector<Pass> plan_passes(const std::vector<Field>& fields) {
     return out;
 }
 
-wt_status run_sort(const Rec& rc, const int32_t* mpos, const int32_t* umin_m, int64_t* perm, int64_t* perm_alt, int64_t n,
-                   const std::vector<Pass>& passes, unsigned long long* keys, unsigned long long* keys_alt,
+// Stable LSD sort of `perm` by the packed fields; after each pass the
+// permutation buffers swap (no copy back): on return `perm` holds the order
+// and `keys_alt` the last pass's sorted keys.
+wt_status run_sort(const Rec& rc, const int32_t* mpos, const int32_t* umin_m, int64_t*& perm, int64_t*& perm_alt,
+                   int64_t n, const std::vector<Pass>& passes, unsigned long long* keys, unsigned long long* keys_alt,
                    void*& tmp, size_t& tmp_bytes, cudaStream_t s) {
     for (const Pass& ps : passes) {
         const int blocks = int((n + 255) / 256);
@@ -1173,7 +1239,7 @@ wt_status run_sort(const Rec& rc, const int32_t* mpos, const int32_t* umin_m, in
         }
         CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_alt, perm, perm_alt, n, 0,
                                            std::max(1, ps.bits), s));
-        CK(cudaMemcpyAsync(perm, perm_alt, size_t(n) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+        std::swap(perm, perm_alt);
     }
     return WT_OK;
 }
@@ -1240,7 +1306,7 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     k_mpos<<<blocks_all, 256, 0, s>>>(rc, n_all, dup, dup + nid, nid, mpos, valid, has_rec, umin_m);
     // key ranges over every record (a superset of the valid ones: packing
     // stays exact) and max w over ALL records (model.cpp:201-203)
-    k_ranges<<<int(std::min<int64_t>((n_all + 255) / 256, 148 * 4)), 256, 0, s>>>(rc, nullptr, n_all, mpos, umin_m,
+    k_ranges<<<int(std::min<int64_t>((n_all + 255) / 256, int64_t(wtb::device_sms()) * 8)), 256, 0, s>>>(rc, nullptr, n_all, mpos, umin_m,
                                                                                   &dh->r);
     {  // compact valid record indices, order preserved
         cub::CountingInputIterator<int64_t> it(0);
@@ -1286,33 +1352,54 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     CK(cudaEventRecord(B->ev0, s));
     trace("registry + ranges");
     // 2. stable sorts
-    int64_t* ordA = dalloc<int64_t>(owned, n);
-    int64_t* ordB = dalloc<int64_t>(owned, n);
+    // ordA starts as the compacted index list itself (the sort swaps buffers)
+    int64_t* ordA = idx;
     int64_t* alt = dalloc<int64_t>(owned, n);
     unsigned long long* keys = dalloc<unsigned long long>(owned, n);
     unsigned long long* keys2 = dalloc<unsigned long long>(owned, n);
-    CK(cudaMemcpyAsync(ordA, idx, n * 8, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(ordB, idx, n * 8, cudaMemcpyDeviceToDevice, s));
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
-    wt_status st = run_sort(rc, mpos, umin_m, ordA, alt, n, passA, keys, keys2, tmp, tmp_bytes, s);
-    if (st) return st;
-    if (bits_u == 0) {
+    int64_t* ordB = nullptr;
+    {
+        // order B's sort runs first from a copy of the index list, so that
+        // order A's sorted keys (its single pass) survive for the group kernels
+        if (bits_u != 0) {
+            ordB = dalloc<int64_t>(owned, n);
+            int64_t* altB = dalloc<int64_t>(owned, n);
+            CK(cudaMemcpyAsync(ordB, idx, n * 8, cudaMemcpyDeviceToDevice, s));
+            wt_status sb = run_sort(rc, mpos, umin_m, ordB, altB, n, passB, keys, keys2, tmp, tmp_bytes, s);
+            if (sb) return sb;
+        }
+        wt_status sa = run_sort(rc, mpos, umin_m, ordA, alt, n, passA, keys, keys2, tmp, tmp_bytes, s);
+        if (sa) return sa;
         // one micro id per macro: order A (macro, w, l, micro, g) is order B
         // (macro, w, l, g) -- one sort
-        CK(cudaMemcpyAsync(ordB, ordA, n * 8, cudaMemcpyDeviceToDevice, s));
-    } else {
-        st = run_sort(rc, mpos, umin_m, ordB, alt, n, passB, keys, keys2, tmp, tmp_bytes, s);
-        if (st) return st;
+        if (bits_u == 0) ordB = ordA;
     }
     if (tmp) cudaFreeAsync(tmp, s);
+    // with one packing pass, order A's sorted keys hold (macro, w, l, micro,
+    // g) of every sorted record: group boundaries and group keys come from
+    // them instead of gathers through the permutation
+    const unsigned long long* keysA = passA.size() == 1 ? keys2 : nullptr;
+    KeyFields kf{};
+    if (keysA) {
+        for (int q = 0; q < passA[0].nf; ++q) {
+            const Field& f = passA[0].f[q];
+            if (f.which == 2) { kf.sl = f.shift; kf.bl = f.bits; kf.base_l = f.base; }
+            if (f.which == 3) { kf.sw = f.shift; kf.bw = f.bits; kf.base_w = f.base; }
+            if (f.which == 4) { kf.sm = f.shift; kf.bm = f.bits; }
+        }
+    }
 
     trace("sorts");
     // 3. groups
     const int blocks = int((n + 255) / 256);
     int32_t* gflag = dalloc<int32_t>(owned, n);
     int32_t* gid = dalloc<int32_t>(owned, n);
-    k_group_flags<<<blocks, 256, 0, s>>>(rc, mpos, ordA, n, gflag);
+    if (keysA)
+        k_group_flags_k<<<blocks, 256, 0, s>>>(keysA, n, kf.sl, gflag);
+    else
+        k_group_flags<<<blocks, 256, 0, s>>>(rc, mpos, ordA, n, gflag);
     {
         size_t need = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, need, gflag, gid, n, s);
@@ -1372,7 +1459,10 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     int32_t* mflag = dalloc<int32_t>(owned, G);
     int32_t* bid = dalloc<int32_t>(owned, G);
     int32_t* mid = dalloc<int32_t>(owned, G);
-    k_group_meta<<<gblocks, 128, 0, s>>>(rc, mpos, ordA, G, gr, gm, gw, gl, bflag, mflag);
+    if (keysA)
+        k_group_meta_k<<<gblocks, 128, 0, s>>>(keysA, kf, G, gr, gm, gw, gl, bflag, mflag);
+    else
+        k_group_meta<<<gblocks, 128, 0, s>>>(rc, mpos, ordA, G, gr, gm, gw, gl, bflag, mflag);
     for (auto [in, out] : {std::pair<int32_t*, int32_t*>{bflag, bid}, std::pair<int32_t*, int32_t*>{mflag, mid}}) {
         size_t need = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, need, in, out, G, s);

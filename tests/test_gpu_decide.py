@@ -545,9 +545,10 @@ def test_partial_sweep_writes_only_its_range(capi, orc, synth256, m_lo, m_hi):
 
 
 @pytest.mark.parametrize("env", [
-    {"WT_SWEEP_RPT": "2", "WT_EVAL_RPT": "2"},
-    {"WT_SWEEP_SMEM_KB": "24", "WT_EVAL_SMEM_KB": "64"},
-    {"WT_SWEEP_RPT": "2", "WT_SWEEP_SMEM_KB": "160", "WT_EVAL_RPT": "4", "WT_EVAL_SMEM_KB": "160"},
+    {"WT_SWEEP_RPT": "2", "WT_EVAL_RPT": "2", "WT_SWEEP_DEDUP": "0"},
+    {"WT_SWEEP_SMEM_KB": "24", "WT_EVAL_SMEM_KB": "64", "WT_SWEEP_DEDUP": "0"},
+    {"WT_SWEEP_RPT": "2", "WT_SWEEP_SMEM_KB": "160", "WT_EVAL_RPT": "4", "WT_EVAL_SMEM_KB": "160",
+     "WT_SWEEP_DEDUP": "0"},
     {"WT_GATHER_VARIANT": "1"},
     {"WT_EVAL_RPT": "2", "WT_GATHER_VARIANT": "2"},
     {"WT_GATHER_VARIANT": "3"},
@@ -563,8 +564,9 @@ def test_partial_sweep_writes_only_its_range(capi, orc, synth256, m_lo, m_hi):
     {"WT_EVAL4_RPT": "1"},
     {"WT_EVAL_KEY_MODE": "3"},
     {"WT_BATCH_SLICE": "4100"},
-    {"WT_SWEEP_SMEM_KB": "96"},
+    {"WT_SWEEP_SMEM_KB": "96", "WT_SWEEP_DEDUP": "0"},
     {"WT_SWEEP_DEDUP": "0"},
+    {"WT_SWEEP_DEDUP": "0", "WT_PRUNE": "0"},
     {"WT_SWEEP_W": "0"},
 ])
 def test_launch_variants(capi, env):

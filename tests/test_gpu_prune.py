@@ -81,7 +81,9 @@ def test_pruning_is_exact_on_adversarial_tables():
 
 
 def test_pruning_matches_unpruned_run():
-    """Same decisions with WT_PRUNE=0 (every config evaluated)."""
+    """Same decisions with WT_PRUNE=0 (every config evaluated) and with the
+    every-M grid sweep (WT_SWEEP_DEDUP=0: k_sweep2 with pruning) instead of
+    the representative sweep."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     script = (
@@ -92,17 +94,18 @@ def test_pruning_matches_unpruned_run():
         "np.savez(sys.argv[1], gm=r['grid'][0], gl=r['grid'][2], lm=r['list'][0], ll=r['list'][2])"
     ) % (os.path.dirname(HERE), os.path.join(os.path.dirname(HERE), "oracle"), HERE)
     outs = []
-    for prune in ("1", "0"):
-        f = os.path.join("/tmp", f"wt_prune_{prune}_{os.getpid()}.npz")
-        r = subprocess.run([sys.executable, "-c", script, f], env={**os.environ, "WT_PRUNE": prune},
+    for i, env in enumerate(({"WT_PRUNE": "1"}, {"WT_PRUNE": "0"}, {"WT_PRUNE": "1", "WT_SWEEP_DEDUP": "0"})):
+        f = os.path.join("/tmp", f"wt_prune_{i}_{os.getpid()}.npz")
+        r = subprocess.run([sys.executable, "-c", script, f], env={**os.environ, **env},
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-3000:]
         outs.append(np.load(f))
         os.unlink(f)
-    for k in ("gm", "lm"):
-        np.testing.assert_array_equal(outs[0][k], outs[1][k])
-    for k in ("gl", "ll"):
-        np.testing.assert_array_equal(outs[0][k].view(np.int64), outs[1][k].view(np.int64))
+    for o in outs[1:]:
+        for k in ("gm", "lm"):
+            np.testing.assert_array_equal(outs[0][k], o[k])
+        for k in ("gl", "ll"):
+            np.testing.assert_array_equal(outs[0][k].view(np.int64), o[k].view(np.int64))
 
 
 def test_many_tile_classes_list_and_grid():
