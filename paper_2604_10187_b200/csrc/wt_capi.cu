@@ -1317,6 +1317,56 @@ wt_status wt_grid_storage(const wt_grid* g, wt_grid_entry** entries, int64_t* n_
     return WT_OK;
 }
 
+namespace {
+bool sweep_dedup() {
+    static const bool d = [] {
+        const char* v = std::getenv("WT_SWEEP_DEDUP");
+        return !v || std::atoi(v) != 0;
+    }();
+    return d;
+}
+
+// The representative sweep of [a.begin, a.end): one M per interval of
+// constant ceil(M / t_m) (k_sweep_w, or k_sweep2 with WT_SWEEP_W=0) into a
+// scratch list, then k_expand copies every interval's entry over its M
+// values in the range, into each destination grid.
+cudaError_t rep_sweep(const wt_engine* e, const wt_grid* g, const SweepArgs& a, const ExpandDst& dst,
+                      cudaStream_t s) {
+    static const int sweep_w = [] {
+        const char* v = std::getenv("WT_SWEEP_W");
+        return v ? std::atoi(v) : 1;
+    }();
+    auto rep_of = [&](int64_t flat) {
+        const int64_t p = flat / g->mcount;
+        const int32_t M = int32_t(g->m_lo + (flat - p * g->mcount));
+        const int64_t i = int64_t(std::upper_bound(g->h_mrep.begin(), g->h_mrep.end(), M) - g->h_mrep.begin()) - 1;
+        return p * g->nrep + i;
+    };
+    const int64_t rb = rep_of(a.begin), re = rep_of(a.end - 1) + 1;
+    SweepArgs ra = a;
+    ra.mcount = g->nrep;
+    ra.mrep = g->d_mrep;
+    ra.begin = rb;
+    ra.end = re;
+    ra.ndst = 0;
+    const size_t eb = (size_t(re - rb) * sizeof(wt_grid_entry) + 255) & ~size_t(255);
+    const size_t sb = sweep_w ? 0 : sweep2_scratch_bytes(e->dev, ra);
+    void* scratch = nullptr;
+    cudaError_t ce = cudaMallocFromPoolAsync(&scratch, eb + sb, lib_pool(e->device), s);
+    if (ce != cudaSuccess) return ce;
+    wt_grid_entry* rep = static_cast<wt_grid_entry*>(scratch);
+    // the sweep writes representative r at ra.entries + r: offset the list by -rb
+    ra.entries = rep - rb;
+    ce = sweep_w ? launch_sweep_w(e->dev, ra, s)
+                 : launch_sweep2(e->dev, ra, g->wide, sb ? static_cast<char*>(scratch) + eb : nullptr, s);
+    if (ce == cudaSuccess)
+        ce = launch_expand(dst, rep, rb, re, a.begin, a.end, g->m_lo, g->mcount, g->d_mrep, g->nrep, s);
+    cudaFreeAsync(scratch, s);
+    g_launches += sb ? 3 : 2;
+    return ce;
+}
+}  // namespace
+
 wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, void* stream) {
     NvtxRange nvtx_("wt_sweep");
     if (!e || !g) return set_err(WT_INVALID_ARGUMENT, "null argument");
@@ -1339,45 +1389,15 @@ wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, v
     a.topk_lat = g->tk_lat;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t ce;
-    static const bool dedup = [] {
-        const char* v = std::getenv("WT_SWEEP_DEDUP");
-        return !v || std::atoi(v) != 0;
-    }();
+    const bool dedup = sweep_dedup();
     if (g->topk > 0) {
         ce = launch_sweep(e->dev, a, g->wide, s);
+        g_launches++;
     } else if (dedup && g->nrep > 0) {
-        // representatives of the intervals meeting [begin, end), swept into a
-        // scratch list, then copied over their intervals
-        auto rep_of = [&](int64_t flat) {
-            const int64_t p = flat / g->mcount;
-            const int32_t M = int32_t(g->m_lo + (flat - p * g->mcount));
-            const int64_t i = int64_t(std::upper_bound(g->h_mrep.begin(), g->h_mrep.end(), M) - g->h_mrep.begin()) - 1;
-            return p * g->nrep + i;
-        };
-        const int64_t rb = rep_of(begin), re = rep_of(end - 1) + 1;
-        SweepArgs ra = a;
-        ra.mcount = g->nrep;
-        ra.mrep = g->d_mrep;
-        ra.begin = rb;
-        ra.end = re;
-        static const int sweep_w = [] {
-            const char* v = std::getenv("WT_SWEEP_W");
-            return v ? std::atoi(v) : 1;
-        }();
-        const size_t eb = (size_t(re - rb) * sizeof(wt_grid_entry) + 255) & ~size_t(255);
-        const size_t sb = sweep_w ? 0 : sweep2_scratch_bytes(e->dev, ra);
-        void* scratch = nullptr;
-        ce = cudaMallocFromPoolAsync(&scratch, eb + sb, lib_pool(e->device), s);
-        if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep: scratch");
-        wt_grid_entry* rep = static_cast<wt_grid_entry*>(scratch);
-        // the sweep writes entry r at ra.entries + r: offset the list by -rb
-        ra.entries = rep - rb;
-        ce = sweep_w ? launch_sweep_w(e->dev, ra, s)
-                     : launch_sweep2(e->dev, ra, g->wide, sb ? static_cast<char*>(scratch) + eb : nullptr, s);
-        if (ce == cudaSuccess)
-            ce = launch_expand(g->entries, rep, rb, re, begin, end, g->m_lo, g->mcount, g->d_mrep, g->nrep, s);
-        cudaFreeAsync(scratch, s);
-        g_launches += sb ? 2 : 1;
+        ExpandDst dst{};
+        dst.d[0] = g->entries;
+        dst.n = 1;
+        ce = rep_sweep(e, g, a, dst, s);  // counts its launches
     } else {
         void* scratch = nullptr;
         const size_t sb = sweep2_scratch_bytes(e->dev, a);
@@ -1387,9 +1407,8 @@ wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, v
         }
         ce = launch_sweep2(e->dev, a, g->wide, scratch, s);
         if (scratch) cudaFreeAsync(scratch, s);
-        if (sb) g_launches++;  // split merge
+        g_launches += sb ? 2 : 1;  // (+ split merge)
     }
-    g_launches++;
     if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep");
     // the run index follows the entries: rebuilt after a full sweep,
     // invalidated by a partial one (wt_grid_finalize rebuilds it)
@@ -1425,14 +1444,22 @@ wt_status wt_sweep_to(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end
     for (int d = 0; d < n_dests; ++d) a.dst[d] = dests[d];
     a.ndst = n_dests;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    void* scratch = nullptr;
-    const size_t sb = sweep2_scratch_bytes(e->dev, a);
     cudaError_t ce = cudaSuccess;
-    if (sb) ce = cudaMallocFromPoolAsync(&scratch, sb, lib_pool(e->device), s);
-    if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep_to: scratch");
-    ce = launch_sweep2(e->dev, a, g->wide, scratch, s);
-    if (scratch) cudaFreeAsync(scratch, s);
-    g_launches += sb ? 2 : 1;
+    if (sweep_dedup() && g->nrep > 0) {
+        // representative sweep; the expansion stores into every destination
+        ExpandDst dst{};
+        for (int d = 0; d < n_dests; ++d) dst.d[d] = dests[d];
+        dst.n = n_dests;
+        ce = rep_sweep(e, g, a, dst, s);
+    } else {
+        void* scratch = nullptr;
+        const size_t sb = sweep2_scratch_bytes(e->dev, a);
+        if (sb) ce = cudaMallocFromPoolAsync(&scratch, sb, lib_pool(e->device), s);
+        if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep_to: scratch");
+        ce = launch_sweep2(e->dev, a, g->wide, scratch, s);
+        if (scratch) cudaFreeAsync(scratch, s);
+        g_launches += sb ? 2 : 1;
+    }
     if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep_to");
     // this grid's own run index is stale until the caller finalizes it
     g->invalidate_runs();

@@ -282,7 +282,11 @@ cudaError_t launch_sweep_w(const DevImage& im, const SweepArgs& a, cudaStream_t 
 // Copies representative entries rep[r - rb], r in [rb, re), onto every grid
 // entry of their M interval inside the flat range [begin, end): interval i
 // of a pair covers M in [mrep[i], mrep[i + 1]) (the last up to m_lo + mcount).
-cudaError_t launch_expand(wt_grid_entry* entries, const wt_grid_entry* rep, int64_t rb, int64_t re, int64_t begin,
+struct ExpandDst {
+    wt_grid_entry* d[8];
+    int32_t n;
+};
+cudaError_t launch_expand(const ExpandDst& dst, const wt_grid_entry* rep, int64_t rb, int64_t re, int64_t begin,
                           int64_t end, int32_t m_lo, int64_t mcount, const int32_t* mrep, int32_t nrep,
                           cudaStream_t st);
 cudaError_t launch_eval2(const DevImage& im, const EvalArgs& a, int grid, cudaStream_t st);

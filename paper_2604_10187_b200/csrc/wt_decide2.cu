@@ -393,7 +393,7 @@ cudaError_t launch_sweep_w(const DevImage& im, const SweepArgs& a, cudaStream_t 
 // Representative sweep expansion: one warp per M interval copies the
 // interval's entry (32 bytes, loaded once) onto every M of the interval that
 // lies in [begin, end) -- consecutive lanes, consecutive entries.
-__global__ void __launch_bounds__(256) k_expand(wt_grid_entry* entries, const wt_grid_entry* rep, int64_t rb,
+__global__ void __launch_bounds__(256) k_expand(ExpandDst dst, const wt_grid_entry* rep, int64_t rb,
                                                 int64_t re, int64_t begin, int64_t end, int32_t m_lo,
                                                 int64_t mcount, const int32_t* mrep, int32_t nrep) {
     const int lane = threadIdx.x & 31;
@@ -405,21 +405,22 @@ __global__ void __launch_bounds__(256) k_expand(wt_grid_entry* entries, const wt
         const int64_t hi = min(end, i + 1 < nrep ? p * mcount + (__ldg(mrep + i + 1) - m_lo) : (p + 1) * mcount);
         const int4* src = reinterpret_cast<const int4*>(rep + (r - rb));
         const int4 e0 = __ldg(src), e1 = __ldg(src + 1);
-        for (int64_t x = lo + lane; x < hi; x += 32) {
-            int4* d = reinterpret_cast<int4*>(entries + x);
-            d[0] = e0;
-            d[1] = e1;
-        }
+        for (int64_t x = lo + lane; x < hi; x += 32)
+            for (int k = 0; k < dst.n; ++k) {  // every destination grid (fused multi-GPU sweep: peers)
+                int4* d = reinterpret_cast<int4*>(dst.d[k] + x);
+                d[0] = e0;
+                d[1] = e1;
+            }
     }
 }
 
-cudaError_t launch_expand(wt_grid_entry* entries, const wt_grid_entry* rep, int64_t rb, int64_t re, int64_t begin,
+cudaError_t launch_expand(const ExpandDst& dst, const wt_grid_entry* rep, int64_t rb, int64_t re, int64_t begin,
                           int64_t end, int32_t m_lo, int64_t mcount, const int32_t* mrep, int32_t nrep,
                           cudaStream_t st) {
     if (re <= rb) return cudaSuccess;
     const int64_t warps = re - rb;
     const int grid = int(std::min<int64_t>((warps + 7) / 8, int64_t(device_sms()) * 8));
-    k_expand<<<grid, 256, 0, st>>>(entries, rep, rb, re, begin, end, m_lo, mcount, mrep, nrep);
+    k_expand<<<grid, 256, 0, st>>>(dst, rep, rb, re, begin, end, m_lo, mcount, mrep, nrep);
     return cudaGetLastError();
 }
 
