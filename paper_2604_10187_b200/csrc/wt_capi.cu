@@ -1510,7 +1510,7 @@ wt_status wt_grid_finalize(const wt_engine* e, wt_grid* g, void* stream) {
     if (ce != cudaSuccess) return cuda_err(ce, "wt_grid_finalize: scratch");
     ce = launch_runs_build(g->entries, g->n_entries, g->mcount, g->runs_now(), temp, s);
     cudaFreeAsync(temp, s);
-    g_launches += 5;
+    g_launches += 3 + scan_launches(g->n_entries);  // flags, scan, scatter, heads
     if (ce != cudaSuccess) return cuda_err(ce, "wt_grid_finalize");
     return WT_OK;
 }

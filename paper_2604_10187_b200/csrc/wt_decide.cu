@@ -17,7 +17,6 @@
 // reference's C++ (SURVEY.md Appendix A).
 #include <cuda_runtime.h>
 
-#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cstdint>
@@ -880,10 +879,7 @@ __global__ void k_runheads(int64_t mcount, const uint32_t* flags, const uint32_t
 }
 
 size_t runs_temp_bytes(int64_t n) {
-    size_t b = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, b, static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
-                                  int(n));
-    return b + 2 * ((size_t(n) * 4 + 255) & ~size_t(255));
+    return scan_scratch_bytes(n) + 2 * ((size_t(n) * 4 + 255) & ~size_t(255));
 }
 
 cudaError_t launch_runs_build(const wt_grid_entry* entries, int64_t n, int64_t mcount, const RunIndex& ri,
@@ -896,9 +892,7 @@ cudaError_t launch_runs_build(const wt_grid_entry* entries, int64_t n, int64_t m
     cudaError_t e = cudaMemsetAsync(ri.hdr, 0, 16, st);
     if (e != cudaSuccess) return e;
     k_runflags<<<g, 256, 0, st>>>(entries, n, mcount, flags, ri.hdr);
-    size_t b = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, b, flags, ids, int(n), st);
-    e = cub::DeviceScan::ExclusiveSum(t + 2 * arr, b, flags, ids, int(n), st);
+    e = scan_exclusive_u32(flags, ids, n, t + 2 * arr, st);
     if (e != cudaSuccess) return e;
     k_runscatter<<<g, 256, 0, st>>>(entries, n, flags, ids, ri);
     k_runheads<<<unsigned((ri.nbtot + 255) / 256), 256, 0, st>>>(mcount, flags, ids, ri);

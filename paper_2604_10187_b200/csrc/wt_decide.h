@@ -277,6 +277,10 @@ cudaError_t launch_serve(const DevImage& im, int64_t n_anchor, Mailbox* mb, uint
                          cudaStream_t st);
 size_t sweep2_scratch_bytes(const DevImage& im, const SweepArgs& a);
 cudaError_t launch_sweep2(const DevImage& im, const SweepArgs& a, bool wide, void* scratch, cudaStream_t st);
+// Exclusive prefix sum of n u32 (wt_scan.cu); scratch of scan_scratch_bytes(n).
+size_t scan_scratch_bytes(int64_t n);
+int scan_launches(int64_t n);
+cudaError_t scan_exclusive_u32(const uint32_t* in, uint32_t* out, int64_t n, void* scratch, cudaStream_t st);
 // Warp-per-shape sweep (representative sweeps; no top-k).
 cudaError_t launch_sweep_w(const DevImage& im, const SweepArgs& a, cudaStream_t st);
 // Copies representative entries rep[r - rb], r in [rb, re), onto every grid
@@ -303,7 +307,7 @@ struct Eval3Bufs {
 Eval3Bufs eval3_bufs(void* scratch, int64_t n);
 // keys_ready: hist / keys were filled by the gather's compaction
 cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, bool keys_ready, cudaStream_t st);
-constexpr int kEval3Launches = 5;  // key, scan (2), scatter, eval
+constexpr int kEval3Launches = 6;  // key, scan (3: 2^20 buckets), scatter, eval
 int eval2_tile();
 cudaError_t launch_explain(const DevImage& im, const ExplainArgs& a, cudaStream_t st);
 cudaError_t launch_nearest(const NearestArgs& a, cudaStream_t st);

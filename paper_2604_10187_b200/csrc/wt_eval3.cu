@@ -27,7 +27,6 @@
 // segments = "first minimum in ascending macro_id" (tuner.cpp:135-149).
 #include <cuda_runtime.h>
 
-#include <cub/device/device_scan.cuh>
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
@@ -611,9 +610,7 @@ int key_mode() {
 
 size_t eval3_scratch_bytes(int64_t n) {
     const size_t nb = size_t(1) << (key_bits() + kSpreadBits);
-    size_t scan = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, scan, static_cast<const uint32_t*>(nullptr),
-                                  static_cast<uint32_t*>(nullptr), int(nb));
+    const size_t scan = scan_scratch_bytes(int64_t(nb));
     const size_t un = size_t(std::max<int64_t>(n, 1));
     return al256(nb * 4) * 2 + al256(un * 4) + al256(un * 16) + al256(un * 4) + al256(scan);
 }
@@ -661,9 +658,7 @@ cudaError_t launch_eval3(const DevImage& im, const EvalArgs& a, void* scratch, b
         if (e != cudaSuccess) return e;
         k_ekey<<<gk, kT3, 0, st>>>(im, a, bits, key_mode(), keys, hist);
     }
-    size_t sb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, sb, hist, offs, int(nb), st);
-    e = cub::DeviceScan::ExclusiveSum(tmp, sb, hist, offs, int(nb), st);
+    e = scan_exclusive_u32(hist, offs, int64_t(nb), tmp, st);
     if (e != cudaSuccess) return e;
     const int gs = int(std::max<int64_t>(1, std::min<int64_t>((a.n + kT3 * kScPer - 1) / (kT3 * kScPer),
                                                               int64_t(sms) * 4)));
