@@ -57,6 +57,19 @@ def gather_traffic(n_decisions):
     return d["dram_bytes_per_decision"] * n_decisions, os.path.relpath(caps[-1], ROOT)
 
 
+def pattern_ceiling():
+    """Measured DRAM ceiling of the gather's own traffic pattern (12 B read +
+    16 B written per query, no lookups: tools/micro/rw_stream.cu), committed
+    under profiles/."""
+    import glob
+
+    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_rw_stream.json")))
+    if not caps:
+        return None, None
+    with open(caps[-1]) as f:
+        return json.load(f)["best_gather_pattern_gbs"], os.path.relpath(caps[-1], ROOT)
+
+
 def fp64_peak():
     """Measured FP64 rates of this B200 pool (tools/micro/fp64_peak.cu: DMUL
     and DADD chains, no FMA, and the 4 DMUL : 3 DADD mix of one bilinear
@@ -623,6 +636,7 @@ def run_wavetune(args):
             cpu = {"value": rate, "unit": "queries/s", "cores": thr, "kind": "reference", "cpu_model": cpu_model(),
                    "sample": f"{sample} queries of this stream, reference tune() (oracle/_ref) on {thr} threads; "
                              f"rate extrapolated linearly to the 1e8-query stream (queries are independent)"}
+        pc, pc_src = pattern_ceiling()
         line = {
             "metric": "queries/s", "value": value, "unit": "queries/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True, "scaling": "weak",
@@ -637,7 +651,11 @@ def run_wavetune(args):
                          "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                          "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peaks_kind,
                          "alg_bytes_per_launch": alg_bytes, "launch_ms": gather_ms,
-                         "share_of_step": gather_ms / t_ms},
+                         "share_of_step": gather_ms / t_ms,
+                         "pattern_ceiling": ({"gbs": pc, "frac": achieved / pc, "source": pc_src,
+                                              "what": "the same 12 B read + 16 B written per query with no "
+                                                      "lookups (16-byte streaming loads / stores)"}
+                                             if pc else None)},
             "offgrid_eval": {"queries": n_off, "ms": eval_ms, "share_of_step": eval_ms / t_ms,
                              "evals": n_off * eng.n_configs,
                              "evals_per_s": n_off * eng.n_configs / (eval_ms * 1e-3),
