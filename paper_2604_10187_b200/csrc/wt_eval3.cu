@@ -388,16 +388,16 @@ __global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval
     // Per-warp plan of 32 segments, built lane-parallel (lane = segment) from
     // lane 0's first query: its wave row and L bucket, the pruning mask of
     // that cell and the rows of its first two surviving configs, all loaded
-    // at once.  A segment whose 128 queries all share that (row, L bucket)
-    // -- checked exactly per segment -- then reads mask and rows from shared
-    // memory instead of two dependent global round trips.
+    // at once.  A segment whose queries all share that (row, L bucket) --
+    // known per (t_m, t_n) group and per t_k, see inplan below -- then reads
+    // mask and rows from shared memory instead of two dependent global round
+    // trips.
     __shared__ __align__(16) double4 pth[kT3 / 32][32][2];
-    __shared__ uint32_t pmask[kT3 / 32][32], pcell[kT3 / 32][32];
+    __shared__ uint32_t pmask[kT3 / 32][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     // this warp's plan slices, addressed once (not re-derived per segment)
     double4 (*const my_pth)[2] = pth[wid];
     uint32_t* const my_pmask = pmask[wid];
-    uint32_t* const my_pcell = pcell[wid];
     for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < nt; base += stride) {
         const int64_t t = base + threadIdx.x;
         uint32_t y2M[RPT], y2N[RPT], y2K[RPT], status[RPT], acc[RPT];
@@ -431,6 +431,9 @@ __global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval
         uint32_t tagA = 0xffffffffu, tagB = 0xffffffffu;
         double ldA[RPT] = {}, ldB[RPT] = {};
         uint32_t lbA = 0, lbB = 0;
+        // per cache slot: every query of the warp in lane 0's L bucket (the
+        // plan's), decided once when the slot fills
+        bool luA = false, luB = false;
         bool nextA = true;
         const uint32_t y2M0 = __shfl_sync(0xffffffffu, y2M[0], 0), y2N0 = __shfl_sync(0xffffffffu, y2N[0], 0),
                        y2K0 = __shfl_sync(0xffffffffu, y2K[0], 0);
@@ -438,7 +441,7 @@ __global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval
             if ((s & 31) == 0) {  // plan segments [s, s + 32)
                 __syncwarp();     // the previous plan is no longer read
                 const int sg = s + lane;
-                uint32_t m = 0, cell = 0xffffffffu;
+                uint32_t m = 0;
                 if (sg < im.nseg) {
                     const uint4 mq = Ms[sg];
                     uint64_t g;
@@ -448,14 +451,12 @@ __global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval
                     const int nq = Ts[sg].w;
                     m = im.prune ? __ldg(im.segmask + (size_t(sg) * R + r) * kLB + lb) : 0xffffffffu;
                     m &= nq >= 32 ? 0xffffffffu : ((1u << nq) - 1u);
-                    cell = r | (lb << 24);
                     const double4* tp = im.theta2t + size_t(r) * C + Ps[sg];
                     if (m) my_pth[lane][0] = ldg_row(tp + (__ffs(int(m)) - 1));
                     const uint32_t m2 = m & (m - 1u);
                     if (m2) my_pth[lane][1] = ldg_row(tp + (__ffs(int(m2)) - 1));
                 }
                 my_pmask[lane] = m;
-                my_pcell[lane] = cell;
                 __syncwarp();
             }
             const uint4 mg = Ms[s];
@@ -488,12 +489,19 @@ __global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval
                     ld[j] = u32_to_f64(L);
                     lb |= uint32_t(min(31 - __clz(int(L)), kLB - 1)) << (8 * j);
                 }
+                const uint32_t lb0 = __shfl_sync(0xffffffffu, lb & 0xffu, 0);
+                bool lsame = true;
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) lsame = lsame && ((lb >> (8 * j)) & 0xffu) == lb0;
+                const bool lu = __all_sync(0xffffffffu, lsame);
                 if (nextA) {
                     tagA = tag;
                     lbA = lb;
+                    luA = lu;
                 } else {
                     tagB = tag;
                     lbB = lb;
+                    luB = lu;
                 }
                 nextA = !nextA;
             }
@@ -503,12 +511,11 @@ __global__ void __launch_bounds__(kT3, RPT == 4 ? 2 : (RPT == 2 ? 3 : 4)) k_eval
             for (int j = 0; j < RPT; ++j) ld[j] = useA ? ldA[j] : ldB[j];
             const uint32_t lbp = useA ? lbA : lbB;
             // does the whole warp sit in the planned (row, L bucket) cell?
-            const uint32_t cell = my_pcell[s & 31];
-            bool lbu = true;
-#pragma unroll
-            for (int j = 1; j < RPT; ++j) lbu = lbu && ((lbp >> (8 * j)) & 0xffu) == (lbp & 0xffu);
-            const bool inplan = __all_sync(0xffffffffu, uni && row[0] == (cell & 0xffffffu) && lbu &&
-                                                            (lbp & 0xffu) == (cell >> 24));
+            // The plan is lane 0's first query's cell, so: every query's row
+            // equals lane 0's (uni, per (t_m, t_n)) and every L bucket equals
+            // lane 0's (per t_k slot) -- both warp-uniform, decided when they
+            // were computed, no per-segment vote
+            const bool inplan = uni && (useA ? luA : luB);
             uint32_t live;
             if (inplan) {
                 live = my_pmask[s & 31];
