@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <chrono>
 #include <map>
 #include <tuple>
 #include <mutex>
@@ -389,10 +390,17 @@ wt_status engine_build(wt_engine* e, const ImagePlan& P, const DevTables& T, cud
     pa.meta2 = ra.meta2;
     pa.segmask = static_cast<uint32_t*>(at(o_smask));
     pa.segor = static_cast<uint32_t*>(at(o_sor));
+    static const bool tr = std::getenv("WT_TRACE_ENGINE") != nullptr;
+    const auto tq = std::chrono::steady_clock::now();
     ce = launch_image_build(T.tv, ra, pa, s);
     g_launches += 2;
     uint32_t special = 0;
     if (ce == cudaSuccess) ce = cudaMemcpyAsync(&special, at(o_spec), 4, cudaMemcpyDeviceToHost, s);
+    if (tr) {
+        cudaStreamSynchronize(s);
+        std::fprintf(stderr, "[engine]   image kernels done %.3f ms after queueing\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq).count());
+    }
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
     if (ce != cudaSuccess) return cuda_err(ce, "wt_engine_create: image build");
 
@@ -543,6 +551,8 @@ wt_status wt_engine_create_from_build(const wt_build* b, const wt_registry_desc*
     NvtxRange nvtx_("wt_engine_create_from_build");
     if (!b || !registry || !hw || !out) return set_err(WT_INVALID_ARGUMENT, "null argument");
     *out = nullptr;
+    static const bool tr = std::getenv("WT_TRACE_ENGINE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     BuildTables bt{};
     if (build_device_tables(b, &bt) != WT_OK) return set_err(WT_INVALID_ARGUMENT, "invalid build");
     std::vector<int32_t> W(bt.n_tables, bt.W);
@@ -550,6 +560,9 @@ wt_status wt_engine_create_from_build(const wt_build* b, const wt_registry_desc*
     std::string err;
     const wt_status st = plan_image(bt.macro_id_host, W.data(), bt.n_tables, *registry, *hw, &P, &err);
     if (st != WT_OK) return set_err(st, err);
+    if (tr)
+        std::fprintf(stderr, "[engine] plan_image %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     DeviceGuard guard(bt.device);
     DevTables T;
     T.tv = bt.tv;
@@ -562,6 +575,9 @@ wt_status wt_engine_create_from_build(const wt_build* b, const wt_registry_desc*
     auto* e = new wt_engine;
     e->device = bt.device;
     const wt_status bs = engine_build(e, P, T, static_cast<cudaStream_t>(stream));
+    if (tr)
+        std::fprintf(stderr, "[engine] + engine_build %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     if (bs != WT_OK) {
         if (e->mem) {
             cudaStreamSynchronize(static_cast<cudaStream_t>(stream));

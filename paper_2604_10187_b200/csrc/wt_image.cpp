@@ -13,12 +13,14 @@
 // pruning masks are resolved by the shared functions of wt_rows.h -- on the
 // device for engines (wt_image_dev.cu), on the host here for the plan.
 #include <algorithm>
+#include <array>
 #include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <map>
 #include <numeric>
 #include <tuple>
+#include <unordered_map>
 
 #include "wt_internal.h"
 #include "wt_rows.h"
@@ -44,9 +46,17 @@ wt_status plan_image(const int32_t* macro_id, const int32_t* W, int32_t n, const
         return fail(err, WT_UNSUPPORTED, "slots = n_sm * blocks_per_sm exceeds the device path's range");
 
     ImagePlan& P = *out;
+    // ascending macro_id (duplicates are rejected below, so any sort that
+    // breaks ties by position is the stable order): one sort of packed keys
     P.order.resize(n);
-    std::iota(P.order.begin(), P.order.end(), 0);
-    std::stable_sort(P.order.begin(), P.order.end(), [&](int32_t a, int32_t b) { return macro_id[a] < macro_id[b]; });
+    if (std::is_sorted(macro_id, macro_id + n)) {  // the usual case: tables in ascending id order
+        std::iota(P.order.begin(), P.order.end(), 0);
+    } else {
+        std::vector<uint64_t> key(n);
+        for (int32_t i = 0; i < n; ++i) key[i] = (uint64_t(uint32_t(macro_id[i]) ^ 0x80000000u) << 32) | uint32_t(i);
+        std::sort(key.begin(), key.end());
+        for (int32_t i = 0; i < n; ++i) P.order[i] = int32_t(uint32_t(key[i]));
+    }
     for (int32_t i = 1; i < n; ++i)
         if (macro_id[P.order[i]] == macro_id[P.order[i - 1]])
             return fail(err, WT_INVALID_ARGUMENT,
@@ -64,7 +74,8 @@ wt_status plan_image(const int32_t* macro_id, const int32_t* W, int32_t n, const
     // registry.macro(id): first macro with that id wins (linear scan order)
     std::vector<std::pair<int32_t, int32_t>> ids(reg.n_macros);
     for (int32_t i = 0; i < reg.n_macros; ++i) ids[i] = {reg.id[i], i};
-    std::stable_sort(ids.begin(), ids.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    if (!std::is_sorted(reg.id, reg.id + reg.n_macros))
+        std::sort(ids.begin(), ids.end());  // (id, position): the first occurrence of an id sorts first
 
     const int32_t C = n;
     P.macro_id.resize(C);
@@ -72,13 +83,15 @@ wt_status plan_image(const int32_t* macro_id, const int32_t* W, int32_t n, const
     P.magic.assign(size_t(C) * 4, 0);
     P.tm_min = INT32_MAX;
     P.tn_min = INT32_MAX;
+    std::vector<std::pair<uint32_t, Magic>> mcache;
+    size_t k = 0;  // merge walk: tables and registry ids both ascend
     for (int32_t c = 0; c < C; ++c) {
         const int32_t id = macro_id[P.order[c]];
         P.macro_id[c] = id;
-        auto it = std::lower_bound(ids.begin(), ids.end(), std::make_pair(id, INT32_MIN));
-        if (it == ids.end() || it->first != id)
+        while (k < ids.size() && ids[k].first < id) ++k;
+        if (k == ids.size() || ids[k].first != id)
             return fail(err, WT_OUT_OF_RANGE, "no macro config with id " + std::to_string(id));
-        const int32_t rp = it->second;
+        const int32_t rp = ids[k].second;  // first occurrence of the id
         int64_t tm = reg.t_m[rp], tn = reg.t_n[rp], tk = reg.t_k[rp];
         if (reg.family == WT_FAMILY_FLASH_ATTENTION) tn = 1;  // g = n_heads * ceil(s_q / t_q)
         if (tm < 1 || tn < 1 || tk < 1) return fail(err, WT_INVALID_ARGUMENT, "tile dims must be >= 1");
@@ -87,7 +100,15 @@ wt_status plan_image(const int32_t* macro_id, const int32_t* W, int32_t n, const
         P.tiles[4 * c + 0] = int32_t(tm);
         P.tiles[4 * c + 1] = int32_t(tn);
         P.tiles[4 * c + 2] = int32_t(tk);
-        const Magic a = make_magic(uint32_t(tm)), b = make_magic(uint32_t(tn)), k = make_magic(uint32_t(tk));
+        // tile dims take few distinct values: memoised magic numbers
+        auto magic = [&](uint32_t d) {
+            for (const auto& x : mcache)
+                if (x.first == d) return x.second;
+            const Magic mg = make_magic(d);
+            mcache.push_back({d, mg});
+            return mg;
+        };
+        const Magic a = magic(uint32_t(tm)), b = magic(uint32_t(tn)), k = magic(uint32_t(tk));
         P.magic[4 * c + 0] = a.m;
         P.magic[4 * c + 1] = b.m;
         P.magic[4 * c + 2] = k.m;
@@ -102,11 +123,51 @@ wt_status plan_image(const int32_t* macro_id, const int32_t* W, int32_t n, const
     // most seg_cfg configs (all R rows of a segment fit a 48 KB staging
     // budget: list mode stages every row), ascending macro_id inside.
     std::vector<int32_t> byc(C);
-    std::iota(byc.begin(), byc.end(), 0);
-    std::stable_sort(byc.begin(), byc.end(), [&](int32_t x, int32_t y) {
-        return std::tie(P.tiles[4 * x], P.tiles[4 * x + 1], P.tiles[4 * x + 2]) <
-               std::tie(P.tiles[4 * y], P.tiles[4 * y + 1], P.tiles[4 * y + 2]);
-    });
+    {
+        // the stable order by tile: bucket the configs by their (t_m, t_n,
+        // t_k) class (few distinct classes; consecutive configs usually share
+        // one), order the classes, then a counting sort in config order
+        bool packable = true;
+        for (int32_t c = 0; c < C && packable; ++c)
+            for (int q = 0; q < 3; ++q) packable = packable && P.tiles[4 * c + q] < (1 << 21);
+        if (packable) {
+            auto pack = [&](int32_t c) {
+                return (uint64_t(P.tiles[4 * c]) << 42) | (uint64_t(P.tiles[4 * c + 1]) << 21) |
+                       uint64_t(P.tiles[4 * c + 2]);
+            };
+            std::unordered_map<uint64_t, int32_t> cid;
+            std::vector<uint64_t> ckey;
+            std::vector<int32_t> cls(C);
+            uint64_t lastk = ~uint64_t(0);
+            int32_t lastc = -1;
+            for (int32_t c = 0; c < C; ++c) {
+                const uint64_t kk = pack(c);
+                if (kk != lastk) {
+                    auto it = cid.find(kk);
+                    if (it == cid.end()) it = cid.emplace(kk, int32_t(ckey.size())).first, ckey.push_back(kk);
+                    lastk = kk;
+                    lastc = it->second;
+                }
+                cls[c] = lastc;
+            }
+            const int32_t K = int32_t(ckey.size());
+            std::vector<int32_t> rank(K), cnt(K + 1, 0);
+            {
+                std::vector<int32_t> o(K);
+                std::iota(o.begin(), o.end(), 0);
+                std::sort(o.begin(), o.end(), [&](int32_t a, int32_t b) { return ckey[a] < ckey[b]; });
+                for (int32_t r = 0; r < K; ++r) rank[o[r]] = r;
+            }
+            for (int32_t c = 0; c < C; ++c) ++cnt[rank[cls[c]] + 1];
+            for (int32_t r = 0; r < K; ++r) cnt[r + 1] += cnt[r];
+            for (int32_t c = 0; c < C; ++c) byc[cnt[rank[cls[c]]]++] = c;
+        } else {
+            std::vector<std::array<int32_t, 4>> key(C);
+            for (int32_t c = 0; c < C; ++c) key[c] = {P.tiles[4 * c], P.tiles[4 * c + 1], P.tiles[4 * c + 2], c};
+            std::sort(key.begin(), key.end());
+            for (int32_t c = 0; c < C; ++c) byc[c] = key[c][3];
+        }
+    }
     P.seg_cfg = int32_t(std::clamp<int64_t>(48 * 1024 / (int64_t(P.R) * 36), 1, kSegCfg));
     P.cls_cfg.clear();
     P.seg_tiles.clear();

@@ -32,8 +32,8 @@ struct Magic {
 inline Magic make_magic(uint32_t d) {
     uint32_t s = 0;
     while ((uint64_t(1) << s) < d) ++s;
-    unsigned __int128 num = (unsigned __int128)1 << (31 + s);
-    uint64_t m = (uint64_t)((num + d - 1) / d);
+    const uint64_t num = uint64_t(1) << (31 + s);  // s <= 31: fits 64 bits
+    const uint64_t m = (num + d - 1) / d;
     return Magic{(uint32_t)m, s};
 }
 
