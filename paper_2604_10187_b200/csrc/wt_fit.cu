@@ -522,6 +522,24 @@ __global__ void k_group_flags(Rec rc, const int32_t* mpos, const int64_t* ordA, 
     gflag[i] = (i == 0 || !same_group(rc, mpos, ordA[i], ordA[i - 1])) ? 1 : 0;
 }
 
+struct KeyFields {  // order A's single packing pass: shift / width / base of g, micro, l, w, macro position
+    int sg, bg, su, bu, sl, bl, sw, bw, sm, bm;
+    unsigned long long base_g, base_l, base_w;
+};
+__device__ __forceinline__ unsigned long long kfield(unsigned long long k, int shift, int bits) {
+    return bits >= 64 ? k >> shift : (k >> shift) & ((1ULL << bits) - 1ULL);
+}
+__device__ __forceinline__ int64_t key_g(unsigned long long k, const KeyFields& f) {
+    return (long long)((kfield(k, f.sg, f.bg) + f.base_g) ^ 0x8000000000000000ULL);
+}
+__device__ __forceinline__ int64_t key_l(unsigned long long k, const KeyFields& f) {
+    return (long long)((kfield(k, f.sl, f.bl) + f.base_l) ^ 0x8000000000000000ULL);
+}
+// micro id: the key holds micro - (smallest micro of the record's macro)
+__device__ __forceinline__ int32_t key_micro(unsigned long long k, const KeyFields& f, const int32_t* umin_m) {
+    return int32_t(kfield(k, f.su, f.bu)) + umin_m[kfield(k, f.sm, f.bm)];
+}
+
 // The same from order A's sorted packed keys (one packing pass): records
 // are in one group iff their keys agree above the l field's shift.
 __global__ void k_group_flags_k(const unsigned long long* keys, int64_t n, int shift_l, int32_t* gflag) {
@@ -607,6 +625,73 @@ __global__ void k_samples(Rec rc, const int64_t* ordA, int64_t G, Groups gr, con
         }
 }
 
+// k_select / k_samples with g and micro read from order A's sorted keys
+// (one packing pass, one micro id per macro: order B = order A): only the
+// latencies are gathered through the permutation.  Same operations, same
+// order -- bit-identical.
+__global__ void k_select_k(Rec rc, const unsigned long long* keys, KeyFields kf, const int32_t* umin_m,
+                           const int64_t* ordA, int64_t G, Groups gr) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= G) return;
+    const int64_t s = gr.start[q], e = gr.start[q + 1];
+    int32_t n_g = 0;  // |all_g|
+    for (int64_t i = s; i < e; ++i)
+        if (i == s || key_g(keys[i], kf) != key_g(keys[i - 1], kf)) ++n_g;
+    int32_t best_micro = -1, best_cover = 0, part = 0;
+    int64_t blo = s, bhi = s;
+    for (int pass = 0; pass < 2 && best_micro < 0; ++pass) {
+        const bool full = pass == 0;
+        double best_mean = 0.0;
+        for (int64_t i = s; i < e;) {
+            const int32_t mu = key_micro(keys[i], kf, umin_m);
+            int64_t j = i;
+            while (j < e && key_micro(keys[j], kf, umin_m) == mu) ++j;
+            int32_t cover = 0;
+            double mean = 0.0;
+            for (int64_t k = i; k < j; ++k)
+                if (k + 1 == j || key_g(keys[k + 1], kf) != key_g(keys[k], kf)) {  // last write of this g
+                    mean = __dadd_rn(mean, rc.lat[ordA[k]]);
+                    ++cover;
+                }
+            mean = __ddiv_rn(mean, double(cover));
+            if (!(full && cover != n_g)) {
+                const bool better = best_micro < 0 || (full ? mean < best_mean : cover > best_cover);
+                if (better) {
+                    best_micro = mu;
+                    best_mean = mean;
+                    best_cover = cover;
+                    blo = i;
+                    bhi = j;
+                }
+            }
+            i = j;
+        }
+        part = full ? 0 : 1;
+    }
+    gr.micro[q] = best_micro;
+    gr.partial[q] = part;
+    gr.sel_lo[q] = blo;
+    gr.sel_hi[q] = bhi;
+    gr.nsamp[q] = best_cover;
+}
+
+__global__ void k_samples_k(Rec rc, const unsigned long long* keys, KeyFields kf, const int64_t* ordA, int64_t G,
+                            Groups gr, const int64_t* soff, double* sg, double* sl, double* st) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= G) return;
+    int64_t o = soff[q];
+    const int64_t lo = gr.sel_lo[q], hi = gr.sel_hi[q];
+    for (int64_t k = lo; k < hi; ++k) {
+        const unsigned long long kk = keys[k];
+        if (k + 1 == hi || key_g(keys[k + 1], kf) != key_g(kk, kf)) {
+            sg[o] = double(key_g(kk, kf));
+            sl[o] = double(key_l(kk, kf));
+            st[o] = rc.lat[ordA[k]];
+            ++o;
+        }
+    }
+}
+
 __global__ void k_group_meta(Rec rc, const int32_t* mpos, const int64_t* ordA, int64_t G, Groups gr, int64_t* gm,
                              int64_t* gw, int64_t* gl, int32_t* bflag, int32_t* mflag) {
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -623,14 +708,6 @@ __global__ void k_group_meta(Rec rc, const int32_t* mpos, const int64_t* ordA, i
     }
     bflag[q] = nb;
     mflag[q] = nm;
-}
-
-struct KeyFields {  // order A's single packing pass: shift / width / base of l, w, macro position
-    int sl, bl, sw, bw, sm, bm;
-    unsigned long long base_l, base_w;
-};
-__device__ __forceinline__ unsigned long long kfield(unsigned long long k, int shift, int bits) {
-    return bits >= 64 ? k >> shift : (k >> shift) & ((1ULL << bits) - 1ULL);
 }
 
 // k_group_meta from the sorted keys (the group's first record's key)
@@ -1385,6 +1462,8 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     if (keysA) {
         for (int q = 0; q < passA[0].nf; ++q) {
             const Field& f = passA[0].f[q];
+            if (f.which == 0) { kf.sg = f.shift; kf.bg = f.bits; kf.base_g = f.base; }
+            if (f.which == 1) { kf.su = f.shift; kf.bu = f.bits; }
             if (f.which == 2) { kf.sl = f.shift; kf.bl = f.bits; kf.base_l = f.base; }
             if (f.which == 3) { kf.sw = f.shift; kf.bw = f.bits; kf.base_w = f.base; }
             if (f.which == 4) { kf.sm = f.shift; kf.bm = f.bits; }
@@ -1436,7 +1515,11 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     Groups gr{gstart, B->t_anchor_micro, B->d_partial, dalloc<int64_t>(owned, G), dalloc<int64_t>(owned, G),
               dalloc<int32_t>(owned, G)};
     const int gblocks = int((G + 127) / 128);
-    k_select<<<gblocks, 128, 0, s>>>(rc, ordA, ordB, G, gr);
+    const bool sel_keys = keysA && ordB == ordA;  // g / micro from the sorted keys
+    if (sel_keys)
+        k_select_k<<<gblocks, 128, 0, s>>>(rc, keysA, kf, umin_m, ordA, G, gr);
+    else
+        k_select<<<gblocks, 128, 0, s>>>(rc, ordA, ordB, G, gr);
     // sample offsets
     int64_t* soff = dalloc<int64_t>(owned, G + 1);
     {
@@ -1527,7 +1610,10 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
         g_fit_err = "cudaMalloc failed (fit scratch)";
         return WT_CUDA_ERROR;
     }
-    k_samples<<<gblocks, 128, 0, s>>>(rc, ordA, G, gr, soff, sg, sl, stt);
+    if (keysA)
+        k_samples_k<<<gblocks, 128, 0, s>>>(rc, keysA, kf, ordA, G, gr, soff, sg, sl, stt);
+    else
+        k_samples<<<gblocks, 128, 0, s>>>(rc, ordA, G, gr, soff, sg, sl, stt);
     int64_t* d_bslo = dalloc<int64_t>(owned, NB);
     int64_t* d_bshi = dalloc<int64_t>(owned, NB);
     int64_t* d_bgs = dalloc<int64_t>(owned, NB + 1);
