@@ -495,7 +495,7 @@ __global__ void k_pack(Rec rc, const int32_t* mpos, const int32_t* umin_m, const
                        unsigned long long* key) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int64_t r = perm[i];
+    const int64_t r = perm ? perm[i] : i;
     unsigned long long k = 0;
     for (int q = 0; q < ps.nf; ++q) {
         const Field& f = ps.f[q];
@@ -542,10 +542,12 @@ __device__ __forceinline__ int32_t key_micro(unsigned long long k, const KeyFiel
 
 // The same from order A's sorted packed keys (one packing pass): records
 // are in one group iff their keys agree above the l field's shift.
-__global__ void k_group_flags_k(const unsigned long long* keys, int64_t n, int shift_l, int32_t* gflag) {
+__global__ void k_group_flags_k(const unsigned long long* keys, int64_t n, int shift_grp, int32_t* gflag) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    gflag[i] = (i == 0 || (keys[i] >> shift_l) != (keys[i - 1] >> shift_l)) ? 1 : 0;
+    // shift_grp = bits of the (g, micro) fields below (l, w, macro); 64: one group
+    const bool same = i > 0 && (shift_grp >= 64 || (keys[i] >> shift_grp) == (keys[i - 1] >> shift_grp));
+    gflag[i] = same ? 0 : 1;
 }
 
 __global__ void k_group_starts(const int32_t* gflag, const int32_t* gid, int64_t n, int64_t* gstart) {
@@ -1285,6 +1287,7 @@ std::vector<Pass> plan_passes(const std::vector<Field>& fields) {
     cur.bits = 0;
     for (const Field& f0 : fields) {
         Field f = f0;
+        if (f.bits == 0) continue;  // constant field: orders nothing, costs loads
         if (cur.bits + f.bits > 64 && cur.nf > 0) {
             out.push_back(cur);
             cur = Pass{};
@@ -1300,12 +1303,16 @@ std::vector<Pass> plan_passes(const std::vector<Field>& fields) {
 // Stable LSD sort of `perm` by the packed fields; after each pass the
 // permutation buffers swap (no copy back): on return `perm` holds the order
 // and `keys_alt` the last pass's sorted keys.
+// identity: perm starts as 0..n-1 (every record valid), so the first pass
+// packs record i directly.
 wt_status run_sort(const Rec& rc, const int32_t* mpos, const int32_t* umin_m, int64_t*& perm, int64_t*& perm_alt,
                    int64_t n, const std::vector<Pass>& passes, unsigned long long* keys, unsigned long long* keys_alt,
-                   void*& tmp, size_t& tmp_bytes, cudaStream_t s) {
+                   void*& tmp, size_t& tmp_bytes, cudaStream_t s, bool identity = false) {
+    bool first = true;
     for (const Pass& ps : passes) {
         const int blocks = int((n + 255) / 256);
-        k_pack<<<blocks, 256, 0, s>>>(rc, mpos, umin_m, perm, n, ps, keys);
+        k_pack<<<blocks, 256, 0, s>>>(rc, mpos, umin_m, first && identity ? nullptr : perm, n, ps, keys);
+        first = false;
         size_t need = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, need, keys, keys_alt, perm, perm_alt, n, 0,
                                         std::max(1, ps.bits), s);
@@ -1444,10 +1451,11 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
             ordB = dalloc<int64_t>(owned, n);
             int64_t* altB = dalloc<int64_t>(owned, n);
             CK(cudaMemcpyAsync(ordB, idx, n * 8, cudaMemcpyDeviceToDevice, s));
-            wt_status sb = run_sort(rc, mpos, umin_m, ordB, altB, n, passB, keys, keys2, tmp, tmp_bytes, s);
+            wt_status sb = run_sort(rc, mpos, umin_m, ordB, altB, n, passB, keys, keys2, tmp, tmp_bytes, s,
+                                    n == n_all);
             if (sb) return sb;
         }
-        wt_status sa = run_sort(rc, mpos, umin_m, ordA, alt, n, passA, keys, keys2, tmp, tmp_bytes, s);
+        wt_status sa = run_sort(rc, mpos, umin_m, ordA, alt, n, passA, keys, keys2, tmp, tmp_bytes, s, n == n_all);
         if (sa) return sa;
         // one micro id per macro: order A (macro, w, l, micro, g) is order B
         // (macro, w, l, g) -- one sort
@@ -1460,12 +1468,17 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     const unsigned long long* keysA = passA.size() == 1 ? keys2 : nullptr;
     KeyFields kf{};
     if (keysA) {
+        // bases from the field definitions (a constant field is not in the
+        // pass: width 0, its value is the base); shifts from the pass
+        kf.base_g = fg.base;
+        kf.base_l = fl.base;
+        kf.base_w = fw.base;
         for (int q = 0; q < passA[0].nf; ++q) {
             const Field& f = passA[0].f[q];
-            if (f.which == 0) { kf.sg = f.shift; kf.bg = f.bits; kf.base_g = f.base; }
+            if (f.which == 0) { kf.sg = f.shift; kf.bg = f.bits; }
             if (f.which == 1) { kf.su = f.shift; kf.bu = f.bits; }
-            if (f.which == 2) { kf.sl = f.shift; kf.bl = f.bits; kf.base_l = f.base; }
-            if (f.which == 3) { kf.sw = f.shift; kf.bw = f.bits; kf.base_w = f.base; }
+            if (f.which == 2) { kf.sl = f.shift; kf.bl = f.bits; }
+            if (f.which == 3) { kf.sw = f.shift; kf.bw = f.bits; }
             if (f.which == 4) { kf.sm = f.shift; kf.bm = f.bits; }
         }
     }
@@ -1476,7 +1489,7 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     int32_t* gflag = dalloc<int32_t>(owned, n);
     int32_t* gid = dalloc<int32_t>(owned, n);
     if (keysA)
-        k_group_flags_k<<<blocks, 256, 0, s>>>(keysA, n, kf.sl, gflag);
+        k_group_flags_k<<<blocks, 256, 0, s>>>(keysA, n, kf.bg + kf.bu, gflag);
     else
         k_group_flags<<<blocks, 256, 0, s>>>(rc, mpos, ordA, n, gflag);
     {

@@ -133,6 +133,35 @@ def test_build_edge_records(capi, orc):
         compare_build(gpu, want)
 
 
+@pytest.mark.parametrize("const", ["l", "g", "w", "macro", "all_valid", "one_micro"])
+def test_build_constant_fields(capi, orc, const):
+    """Sort-key fields that are constant over the records pack to zero bits
+    and drop out of the radix sort; the group / select / sample kernels then
+    decode the remaining fields from the sorted keys (one packing pass).
+    Every such case against the restatement."""
+    rng = np.random.default_rng(23)
+    rows = []
+    for macro in range(1 if const == "macro" else 5):
+        for w in ([3] if const == "w" else range(1, 6)):
+            for l in ([16] if const == "l" else (8, 16, 32)):
+                for gi in range(1 if const == "g" else 3):
+                    g = 250 if const == "g" else (w - 1) * 100 + 10 + 20 * gi
+                    for micro in range(1 if const == "one_micro" else 2):
+                        t = (5 + micro + 0.3 * macro) * w * (1 + l / 50) * (1 + 0.01 * rng.random())
+                        rows.append((g, l, w, macro, 10 * macro + micro, t))
+    if const != "all_valid":
+        rows.append((10, 8, 1, 99, 0, 5.0))  # a record of an unknown macro (not every record valid)
+    r = np.array(rows, dtype=object)
+    rec = dict(g=r[:, 0].astype(np.int64), l=r[:, 1].astype(np.int64), w=r[:, 2].astype(np.int32),
+               macro=r[:, 3].astype(np.int32), micro=r[:, 4].astype(np.int32), lat=r[:, 5].astype(np.float64))
+    order = list(range(5))
+    for W in (0, 4):
+        gpu = capi.fit_build(rec, order, W, 4)
+        st, want = orc.build(rec, order, W, 4)
+        assert st == 0
+        compare_build(gpu, want)
+
+
 def test_build_config4_scale_subset_parity(capi, orc):
     """Config 4 (4608 configs x 131 plan points x 5 anchors ~ 3.0M records):
     the full GPU build, checked bit for bit against the oracle on a 48-macro
