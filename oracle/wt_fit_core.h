@@ -21,7 +21,8 @@
  * (pinned only to 1e-9 by the reference's golden fits, test_model.cpp:23-61,
  * acceptance.cpp:313-323).  This restatement fixes ONE order per problem
  * size that the GPU fit kernels reproduce exactly (products rounded first,
- * sums from +0.0): problems of <= 32 rows -- every (macro, wave) bucket --
+ * sums from +0.0): problems of <= WTF_QROWS (24) rows -- every (macro, wave)
+ * bucket of the synthetic plans --
  * reduce rows in plain ascending order (one GPU lane per design column);
  * larger problems (extrapolation windows, per-macro baselines) reduce the
  * QR's dot products as eight interleaved ascending partials in a fixed tree
@@ -44,13 +45,18 @@ static inline double wtf_sum(const double* v, int r0, int n) {
     return p;
 }
 
+/* Problems of up to WTF_QROWS rows reduce in ascending order (the GPU's
+ * quad kernel k_qfit: one lane per design column, the problem in a
+ * WTF_QROWS-row shared slab); larger ones in the octet order (k_ofit). */
+#define WTF_QROWS 24
+
 /* Row sum of the QR's reductions over [r0, n) of an n-row problem.
- * n <= 32: ascending (one GPU lane per design column).  n > 32: eight
+ * n <= WTF_QROWS: ascending (one GPU lane per design column).  Otherwise eight
  * interleaved ascending partials p_j over the rows r = j (mod 8), combined
  * as ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)) -- the GPU gives such problems a
  * warp, 8 lanes per column (k_ofit). */
 static inline double wtf_qsum(const double* v, int r0, int n) {
-    if (n <= 32) return wtf_sum(v, r0, n);
+    if (n <= WTF_QROWS) return wtf_sum(v, r0, n);
     double p[8];
     for (int j = 0; j < 8; ++j) {
         p[j] = 0.0;

@@ -62,7 +62,7 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr double kEps = DBL_EPSILON;
 
 // Lane groups.  A problem is solved by 4*SUB lanes: column owner q (0..3)
-// holds sub-lanes j = 0..SUB-1.  SUB = 1 (problems of <= 32 rows: buckets):
+// holds sub-lanes j = 0..SUB-1.  SUB = 1 (problems of <= kQRows rows: buckets):
 // every row reduction is one lane's ascending accumulation.  SUB = 8 (larger
 // problems: extrapolation windows, per-macro baselines): sub-lane j owns the
 // rows r = j (mod 8), accumulates them in ascending order, and the eight
@@ -772,7 +772,8 @@ struct Buckets {
 };
 
 constexpr int kQWarps = 4;      // warps per CTA of the small-problem fit (128 threads)
-constexpr int kQRows = 32;      // problems of <= 32 samples: 4 lanes each, shared memory, sequential sums
+constexpr int kQRows = 24;      // problems of <= 24 samples: 4 lanes each, shared memory, sequential sums
+                                // (= WTF_QROWS of oracle/wt_fit_core.h: the two orders switch there)
 constexpr int kORows = 256;     // larger problems: a warp each (octet order), shared memory up to this size
 constexpr int kOWarps = 4;
 constexpr int kQScr = 5;        // global scratch doubles per sample (problems above kORows)
