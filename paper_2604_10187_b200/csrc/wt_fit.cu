@@ -827,8 +827,15 @@ __global__ void __launch_bounds__(32 * kOWarps) k_ofit(const double* sg, const d
         for (unsigned todo = __ballot_sync(0xffffffffu, big); todo; todo &= todo - 1u) {
             const int64_t pi = base + (__ffs(int(todo)) - 1);
             const int64_t lo = b.slo[pi], n = b.shi[pi] - lo;
-            double* A = n <= kORows ? sA : gscr + kQScr * lo;
-            const FitOut o = group_fit<8>(sg + lo, sl + lo, st + lo, int(n), A, 4, A + 4 * n, 1, G, b.r2 || b.mape);
+            // two call sites: the shared slab's loads compile to LDS (a
+            // pointer that may be either space would take generic loads)
+            FitOut o;
+            if (n <= kORows) {
+                o = group_fit<8>(sg + lo, sl + lo, st + lo, int(n), sA, 4, sA + 4 * n, 1, G, b.r2 || b.mape);
+            } else {
+                double* A = gscr + kQScr * lo;
+                o = group_fit<8>(sg + lo, sl + lo, st + lo, int(n), A, 4, A + 4 * n, 1, G, b.r2 || b.mape);
+            }
             if (lane == 0) {
                 for (int c = 0; c < 4; ++c) b.coeff[4 * pi + c] = o.c[c];
                 if (b.r2) b.r2[pi] = o.r2;
