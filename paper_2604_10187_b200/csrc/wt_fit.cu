@@ -243,6 +243,7 @@ __device__ FitOut group_fit(const double* g, const double* l, const double* t, i
         double tk = 0.0, bk = 0.0;
         if (lj == k) {
             tk = q_house(G, A + q, la, k, n, &bk);
+            G.sync_own();  // every sub-lane has read col[k] (c0) before it is overwritten
             if (j == 0) A[k * la + q] = bk;
         }
         tk = G.own(tk, own[k]);
@@ -311,6 +312,7 @@ __device__ FitOut group_fit(const double* g, const double* l, const double* t, i
             double tk = 0.0, bk = 0.0;
             if (q == k) {
                 tk = q_house(G, A + q, la, k, n, &bk);
+                G.sync_own();  // every sub-lane has read col[k] before it is overwritten
                 if (j == 0) A[k * la + q] = bk;
             }
             tk = G.own(tk, k);
