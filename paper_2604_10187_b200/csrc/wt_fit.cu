@@ -1351,18 +1351,52 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     // WT_FIT_TRACE=1 prints a synchronised wall-clock breakdown of the stages
     const bool tr = std::getenv("WT_FIT_TRACE") != nullptr;
     auto t_start = std::chrono::steady_clock::now();
+    // WT_FIT_TRACE=2: no syncs -- an event per stage and the host clock when
+    // the stage was queued; printed at the end (device reached vs host queued)
+    const bool tr2 = tr && std::getenv("WT_FIT_TRACE")[0] == '2';
+    struct Mark {
+        const char* what;
+        cudaEvent_t ev;
+        double host_ms;
+    };
+    std::vector<Mark> marks;
     auto trace = [&](const char* what) {
         if (!tr) return;
-        cudaStreamSynchronize(s);
         const double ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
-        std::fprintf(stderr, "[wt_fit] %-28s %9.3f ms\n", what, ms);
+        if (tr2) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            cudaEventRecord(e, s);
+            marks.push_back({what, e, ms});
+            return;
+        }
+        cudaStreamSynchronize(s);
+        std::fprintf(stderr, "[wt_fit] %-28s %9.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
     };
+    struct MarkDump {
+        std::vector<Mark>* m;
+        cudaStream_t s;
+        ~MarkDump() {
+            if (m->empty()) return;
+            cudaStreamSynchronize(s);
+            for (const Mark& k : *m) {
+                float d = 0.f;
+                cudaEventElapsedTime(&d, m->front().ev, k.ev);
+                std::fprintf(stderr, "[wt_fit] %-28s queued %8.3f ms  device +%8.3f ms\n", k.what, k.host_ms,
+                             double(d) + m->front().host_ms);
+            }
+            for (const Mark& k : *m) cudaEventDestroy(k.ev);
+        }
+    } mark_dump{&marks, s};
+    trace("start");
 
     // 1. registry positions (first occurrence of a duplicated id wins)
-    std::vector<std::pair<int32_t, int32_t>> ids;
-    for (int32_t i = 0; i < n_macros; ++i) ids.push_back({registry_ids[i], i});
-    std::stable_sort(ids.begin(), ids.end(), [](auto& a, auto& b) { return a.first < b.first; });
+    std::vector<std::pair<int32_t, int32_t>> ids(n_macros);
+    for (int32_t i = 0; i < n_macros; ++i) ids[i] = {registry_ids[i], i};
+    if (!std::is_sorted(registry_ids, registry_ids + n_macros))  // usual registries ascend already
+        std::sort(ids.begin(), ids.end());  // (id, position): the stable order by id
     ids.erase(std::unique(ids.begin(), ids.end(), [](auto& a, auto& b) { return a.first == b.first; }), ids.end());
     const int nid = int(ids.size());
     // one upload: sorted ids | their registry positions | registry ids (order)
