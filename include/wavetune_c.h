@@ -133,8 +133,9 @@ typedef struct {
 
 /* Validates like the reference (duplicate ids -> INVALID_ARGUMENT, table id
  * absent from the registry -> OUT_OF_RANGE "no macro config with id N",
- * no tables -> INVALID_ARGUMENT "no dual tables provided") and uploads.
- * Synchronous (host -> device copies complete on return). */
+ * no tables -> INVALID_ARGUMENT "no dual tables provided") and uploads (the
+ * host arrays may be released on return).  The device image is built
+ * asynchronously; the first call that uses the engine waits for it. */
 wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc* registry,
                            const wt_hw* hw, int device, wt_engine** out);
 wt_status wt_engine_destroy(wt_engine* e);
@@ -473,7 +474,9 @@ wt_status wt_build_result_get(wt_build* b, wt_build_result* result);
 /* Engine from a build's device-resident tables (registry = the one the build
  * was fitted against): the image -- rows, tile classes, pruning masks -- is
  * resolved on the device, the tables never cross PCIe.  Work is queued on
- * `stream` (ordered after the build); returns once the engine is ready. */
+ * `stream` (ordered after the build) and not waited for: the first call that
+ * uses the engine waits for the image (so the host can meanwhile, e.g.,
+ * create a grid).  wt_build_free waits for all device work. */
 wt_status wt_engine_create_from_build(const wt_build* b, const wt_registry_desc* registry, const wt_hw* hw,
                                       void* stream, wt_engine** out);
 

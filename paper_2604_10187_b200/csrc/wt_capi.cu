@@ -157,7 +157,38 @@ struct EngineMeta {
 struct wt_engine {
     int device = 0;
     EngineMeta host;
-    DevImage dev{};
+    // The device image.  Creation only queues its build (no host sync); the
+    // first call that uses the engine waits for it (ready_ev) and reads the
+    // one data-dependent host fact, the special-row flag -- so the host can
+    // go on (e.g. create a grid) while the image kernels run.
+    DevImage dev_{};
+    mutable std::atomic<bool> ready{true};
+    mutable std::mutex ready_mu;
+    cudaEvent_t ready_ev = nullptr;
+    const uint32_t* spec_d = nullptr;  // device word: OR of the rows' special bits
+    const DevImage& dev() const {
+        if (!ready.load(std::memory_order_acquire)) resolve();
+        return dev_;
+    }
+    DevImage& dev_mut() {
+        dev();
+        return dev_;
+    }
+    void resolve() const {
+        std::lock_guard<std::mutex> lk(ready_mu);
+        if (ready.load(std::memory_order_relaxed)) return;
+        auto* self = const_cast<wt_engine*>(this);
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        uint32_t special = 0;
+        cudaEventSynchronize(ready_ev);
+        cudaMemcpy(&special, spec_d, 4, cudaMemcpyDeviceToHost);
+        cudaSetDevice(prev);
+        self->host.special = special != 0;
+        self->dev_.special = special != 0 ? 1 : 0;
+        ready.store(true, std::memory_order_release);
+    }
     void* mem = nullptr;
     size_t bytes = 0;
     int eval_chunk = 0;
@@ -192,7 +223,6 @@ struct wt_grid {
     int64_t mcount = 0, n_entries = 0;
     int32_t topk = 0;
     bool wide = false;
-    int sweep_chunk = 0;
     void* mem = nullptr;
     bool pooled = false;    // mem from the library pool (wt_grid_create_async): not IPC-exportable
     // M intervals on which every ceil(M / t_m) is constant: a grid entry
@@ -394,22 +424,24 @@ wt_status engine_build(wt_engine* e, const ImagePlan& P, const DevTables& T, cud
     const auto tq = std::chrono::steady_clock::now();
     ce = launch_image_build(T.tv, ra, pa, s);
     g_launches += 2;
-    uint32_t special = 0;
-    if (ce == cudaSuccess) ce = cudaMemcpyAsync(&special, at(o_spec), 4, cudaMemcpyDeviceToHost, s);
+    // no host sync: the first use of the engine waits on this event
+    if (ce == cudaSuccess && !e->ready_ev) ce = cudaEventCreateWithFlags(&e->ready_ev, cudaEventDisableTiming);
+    if (ce == cudaSuccess) ce = cudaEventRecord(e->ready_ev, s);
     if (tr) {
         cudaStreamSynchronize(s);
         std::fprintf(stderr, "[engine]   image kernels done %.3f ms after queueing\n",
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq).count());
     }
-    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
     if (ce != cudaSuccess) return cuda_err(ce, "wt_engine_create: image build");
+    e->spec_d = static_cast<const uint32_t*>(at(o_spec));
+    e->ready.store(false, std::memory_order_release);
 
     EngineMeta& h = e->host;
     h.C = P.C;
     h.R = P.R;
     h.S = P.S;
     h.family = P.family;
-    h.special = special != 0;
+    h.special = false;  // resolved at first use (wt_engine::resolve)
     h.macro_id = P.macro_id;
     h.tm_min = P.tm_min;
     h.tm_vals.clear();
@@ -418,7 +450,7 @@ wt_status engine_build(wt_engine* e, const ImagePlan& P, const DevTables& T, cud
     h.tm_vals.erase(std::unique(h.tm_vals.begin(), h.tm_vals.end()), h.tm_vals.end());
     h.tn_min = P.tn_min;
     h.n_pool = n_pool;
-    DevImage& d = e->dev;
+    DevImage& d = e->dev_;
     d.C = P.C;
     d.R = P.R;
     d.S = P.S;
@@ -426,7 +458,7 @@ wt_status engine_build(wt_engine* e, const ImagePlan& P, const DevTables& T, cud
     const Magic ms = make_magic(uint32_t(P.S));
     d.mS = ms.m;
     d.sS = ms.s;
-    d.special = h.special ? 1 : 0;
+    d.special = 0;  // resolved at first use
     d.macro_id = static_cast<const int32_t*>(at(o_mid));
     d.tiles = static_cast<const int4*>(at(o_til));
     d.magic = static_cast<const uint4*>(at(o_mag));
@@ -595,6 +627,7 @@ wt_status wt_engine_destroy(wt_engine* e) {
     DeviceGuard guard(e->device);
     stop_server(e);
     if (e->one_st) cudaStreamDestroy(e->one_st);
+    if (e->ready_ev) cudaEventDestroy(e->ready_ev);
     if (e->one_h) cudaFreeHost(e->one_h);
     if (e->mb_h) cudaFreeHost(e->mb_h);
     // pool memory: free after every stream's use of the engine (the
@@ -612,7 +645,7 @@ wt_status wt_engine_info_get(const wt_engine* e, wt_engine_info* out) {
     out->n_rows = e->host.R;
     out->slots = e->host.S;
     out->family = e->host.family;
-    out->has_fallback_rows = e->host.special ? 1 : 0;
+    out->has_fallback_rows = e->dev().special ? 1 : 0;
     out->device = e->device;
     out->device_bytes = e->bytes;
     return WT_OK;
@@ -620,23 +653,23 @@ wt_status wt_engine_info_get(const wt_engine* e, wt_engine_info* out) {
 
 wt_status wt_engine_prune_masks(const wt_engine* e, uint32_t* masks, int64_t n) {
     if (!e || !masks) return set_err(WT_INVALID_ARGUMENT, "null argument");
-    const int64_t want = int64_t(e->dev.nseg) * e->dev.R * kLB;
+    const int64_t want = int64_t(e->dev().nseg) * e->dev().R * kLB;
     if (n != want) return set_err(WT_INVALID_ARGUMENT, "masks must hold n_seg * R * 16 words");
     DeviceGuard guard(e->device);
-    const cudaError_t ce = cudaMemcpy(masks, e->dev.segmask, size_t(n) * 4, cudaMemcpyDeviceToHost);
+    const cudaError_t ce = cudaMemcpy(masks, e->dev().segmask, size_t(n) * 4, cudaMemcpyDeviceToHost);
     if (ce != cudaSuccess) return cuda_err(ce, "wt_engine_prune_masks");
     return WT_OK;
 }
 
 wt_status wt_engine_count_evals(wt_engine* e, unsigned long long* counter) {
     if (!e) return set_err(WT_INVALID_ARGUMENT, "null argument");
-    e->dev.eval_count = counter;
+    e->dev_mut().eval_count = counter;
     return WT_OK;
 }
 
 wt_status wt_engine_set_prune(wt_engine* e, int32_t enable) {
     if (!e) return set_err(WT_INVALID_ARGUMENT, "null argument");
-    e->dev.prune = enable ? 1 : 0;
+    e->dev_mut().prune = enable ? 1 : 0;
     return WT_OK;
 }
 
@@ -661,17 +694,17 @@ int32_t wt_engine_anchor_map(const wt_engine* e, int32_t config, int32_t wave, i
     uint32_t meta = 0;
     int2 am{0, 0};
     int32_t fb = -1;
-    if (cudaMemcpy(&meta, e->dev.rowmeta + rr, 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
-        cudaMemcpy(&am, e->dev.amap + rr, 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
-        cudaMemcpy(&fb, e->dev.afb + rr, 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+    if (cudaMemcpy(&meta, e->dev().rowmeta + rr, 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(&am, e->dev().amap + rr, 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(&fb, e->dev().afb + rr, 4, cudaMemcpyDeviceToHost) != cudaSuccess)
         return -1;
     if (meta & ROW_NO_ANCHOR) return -1;
     const int32_t n = std::min(am.y, std::max(cap, 0));
     if (n > 0 && anchors &&
-        cudaMemcpy(anchors, e->dev.anchor_l + am.x, size_t(n) * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+        cudaMemcpy(anchors, e->dev().anchor_l + am.x, size_t(n) * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
         return -1;
     if (n > 0 && micros &&
-        cudaMemcpy(micros, e->dev.anchor_micro + am.x, size_t(n) * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+        cudaMemcpy(micros, e->dev().anchor_micro + am.x, size_t(n) * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
         return -1;
     if (fallback_wave) fallback_wave[0] = fb;
     return am.y;
@@ -718,13 +751,13 @@ static cudaError_t run_list_eval(const wt_engine* e, const EvalArgs& a, cudaStre
     if (eval_mode() == 2) {
         const int64_t tiles = (a.n + eval2_tile() - 1) / eval2_tile();
         g_launches++;
-        return launch_eval2(e->dev, a, int(std::min<int64_t>(tiles, e->eval_grid2)), s);
+        return launch_eval2(e->dev(), a, int(std::min<int64_t>(tiles, e->eval_grid2)), s);
     }
     const bool own = scratch == nullptr;
     cudaError_t ce = cudaSuccess;
     if (own) ce = cudaMallocFromPoolAsync(&scratch, eval3_scratch_bytes(a.n), lib_pool(e->device), s);
     if (ce != cudaSuccess) return ce;
-    ce = launch_eval3(e->dev, a, scratch, !own, s);
+    ce = launch_eval3(e->dev(), a, scratch, !own, s);
     if (own) cudaFreeAsync(scratch, s);
     g_launches += own ? kEval3Launches : kEval3Launches - 1;
     return ce;
@@ -780,7 +813,7 @@ wt_status wt_tune_batch(const wt_engine* e, const int32_t* M, const int32_t* N, 
     cudaError_t ce;
     if (a.out.topk > 0) {  // per-config order kernel keeps the top-k list
         const int64_t tiles = (n + kEvalThreads - 1) / kEvalThreads;
-        ce = launch_eval(e->dev, a, int(std::min<int64_t>(tiles, e->eval_grid)), static_cast<cudaStream_t>(stream));
+        ce = launch_eval(e->dev(), a, int(std::min<int64_t>(tiles, e->eval_grid)), static_cast<cudaStream_t>(stream));
         g_launches++;
     } else {
         ce = cudaSuccess;
@@ -845,7 +878,7 @@ wt_status wt_tune_one(const wt_engine* e, int32_t M, int32_t N, int32_t K, wt_de
                 std::atomic_thread_fence(std::memory_order_acquire);
                 if (answered()) break;
                 mb->alive = 1;
-                ce = launch_serve(e->dev, n_anchor, e->mb_d, seq - 1, e->idle_ns, e->one_st);
+                ce = launch_serve(e->dev(), n_anchor, e->mb_d, seq - 1, e->idle_ns, e->one_st);
                 g_launches++;
                 if (ce != cudaSuccess) {
                     mb->alive = 0;
@@ -879,7 +912,7 @@ wt_status wt_tune_one(const wt_engine* e, int32_t M, int32_t N, int32_t K, wt_de
         out->tail_frac = double(tail);
         return WT_OK;
     }
-    ce = launch_one(e->dev, M, N, K, e->one_d, seq, e->one_st);
+    ce = launch_one(e->dev(), M, N, K, e->one_d, seq, e->one_st);
     g_launches++;
     if (ce != cudaSuccess) return cuda_err(ce, "wt_tune_one");
     // poll the mailbox; every 4096 spins ask the stream whether the kernel
@@ -1035,7 +1068,7 @@ wt_status wt_baseline_tune_batch(const wt_engine* e, const wt_baseline* b, const
     a.K = K;
     a.n = n;
     a.out = to_out(out);
-    const cudaError_t ce = launch_btune(e->dev, b->img, a, static_cast<cudaStream_t>(stream));
+    const cudaError_t ce = launch_btune(e->dev(), b->img, a, static_cast<cudaStream_t>(stream));
     g_launches++;
     if (ce != cudaSuccess) return cuda_err(ce, "wt_baseline_tune_batch");
     return WT_OK;
@@ -1078,7 +1111,7 @@ wt_status wt_tune_grouped_batch(const wt_engine* e, const int64_t* row_off, cons
     a.n = n;
     a.out = to_out(out);
     const int grid = int(std::min<int64_t>((n * 32 + 255) / 256, int64_t(sm_count(e->device)) * 8));
-    cudaError_t ce = launch_grouped(e->dev, a, grid, static_cast<cudaStream_t>(stream));
+    cudaError_t ce = launch_grouped(e->dev(), a, grid, static_cast<cudaStream_t>(stream));
     g_launches++;
     if (ce != cudaSuccess) return cuda_err(ce, "wt_tune_grouped_batch");
     return WT_OK;
@@ -1091,7 +1124,7 @@ wt_status wt_predict_batch(const wt_engine* e, const int32_t* config, const int6
     if (n <= 0) return WT_OK;
     DeviceGuard guard(e->device);
     PredictArgs a{config, g, l, n, latency_us, wave, extrapolated, used_w, status};
-    cudaError_t ce = launch_predict(e->dev, a, static_cast<cudaStream_t>(stream));
+    cudaError_t ce = launch_predict(e->dev(), a, static_cast<cudaStream_t>(stream));
     g_launches++;
     if (ce != cudaSuccess) return cuda_err(ce, "wt_predict_batch");
     return WT_OK;
@@ -1106,7 +1139,7 @@ wt_status wt_explain(const wt_engine* e, int64_t M, int64_t N, int64_t K, int64_
         return set_err(WT_UNSUPPORTED, "dims above 2^31-1 are outside the device path's range");
     DeviceGuard guard(e->device);
     ExplainArgs a{M, N, K, g, l, wave, used_w, latency_us, status};
-    cudaError_t ce = launch_explain(e->dev, a, static_cast<cudaStream_t>(stream));
+    cudaError_t ce = launch_explain(e->dev(), a, static_cast<cudaStream_t>(stream));
     g_launches++;
     if (ce != cudaSuccess) return cuda_err(ce, "wt_explain");
     return WT_OK;
@@ -1282,8 +1315,6 @@ wt_status grid_create_impl(const wt_engine* e, const wt_grid_desc* desc, bool po
         delete g;
         return cuda_err(ce, "wt_grid_create: upload");
     }
-    const size_t per_cfg = size_t(e->host.R) * (32 + (e->host.special ? 4 : 0)) + 24;
-    g->sweep_chunk = int(std::max<size_t>(1, std::min<size_t>(e->host.C, 49152 / per_cfg)));
     *out = g;
     return WT_OK;
 }
@@ -1366,15 +1397,15 @@ cudaError_t rep_sweep(const wt_engine* e, const wt_grid* g, const SweepArgs& a, 
     ra.end = re;
     ra.ndst = 0;
     const size_t eb = (size_t(re - rb) * sizeof(wt_grid_entry) + 255) & ~size_t(255);
-    const size_t sb = sweep_w ? 0 : sweep2_scratch_bytes(e->dev, ra);
+    const size_t sb = sweep_w ? 0 : sweep2_scratch_bytes(e->dev(), ra);
     void* scratch = nullptr;
     cudaError_t ce = cudaMallocFromPoolAsync(&scratch, eb + sb, lib_pool(e->device), s);
     if (ce != cudaSuccess) return ce;
     wt_grid_entry* rep = static_cast<wt_grid_entry*>(scratch);
     // the sweep writes representative r at ra.entries + r: offset the list by -rb
     ra.entries = rep - rb;
-    ce = sweep_w ? launch_sweep_w(e->dev, ra, s)
-                 : launch_sweep2(e->dev, ra, g->wide, sb ? static_cast<char*>(scratch) + eb : nullptr, s);
+    ce = sweep_w ? launch_sweep_w(e->dev(), ra, s)
+                 : launch_sweep2(e->dev(), ra, g->wide, sb ? static_cast<char*>(scratch) + eb : nullptr, s);
     if (ce == cudaSuccess)
         ce = launch_expand(dst, rep, rb, re, a.begin, a.end, g->m_lo, g->mcount, g->d_mrep, g->nrep, s);
     cudaFreeAsync(scratch, s);
@@ -1398,7 +1429,10 @@ wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, v
     a.mcount = g->mcount;
     a.begin = begin;
     a.end = end;
-    a.chunk = g->sweep_chunk;
+    {  // configs per shared-memory chunk of the top-k sweep
+        const size_t per_cfg = size_t(e->host.R) * (32 + (e->dev().special ? 4 : 0)) + 24;
+        a.chunk = int(std::max<size_t>(1, std::min<size_t>(e->host.C, 49152 / per_cfg)));
+    }
     a.entries = g->entries;
     a.topk = g->topk;
     a.topk_macro = g->tk_macro;
@@ -1407,7 +1441,7 @@ wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, v
     cudaError_t ce;
     const bool dedup = sweep_dedup();
     if (g->topk > 0) {
-        ce = launch_sweep(e->dev, a, g->wide, s);
+        ce = launch_sweep(e->dev(), a, g->wide, s);
         g_launches++;
     } else if (dedup && g->nrep > 0) {
         ExpandDst dst{};
@@ -1416,12 +1450,12 @@ wt_status wt_sweep(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end, v
         ce = rep_sweep(e, g, a, dst, s);  // counts its launches
     } else {
         void* scratch = nullptr;
-        const size_t sb = sweep2_scratch_bytes(e->dev, a);
+        const size_t sb = sweep2_scratch_bytes(e->dev(), a);
         if (sb) {
             ce = cudaMallocFromPoolAsync(&scratch, sb, lib_pool(e->device), s);
             if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep: scratch");
         }
-        ce = launch_sweep2(e->dev, a, g->wide, scratch, s);
+        ce = launch_sweep2(e->dev(), a, g->wide, scratch, s);
         if (scratch) cudaFreeAsync(scratch, s);
         g_launches += sb ? 2 : 1;  // (+ split merge)
     }
@@ -1455,7 +1489,6 @@ wt_status wt_sweep_to(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end
     a.mcount = g->mcount;
     a.begin = begin;
     a.end = end;
-    a.chunk = g->sweep_chunk;
     a.entries = g->entries;
     for (int d = 0; d < n_dests; ++d) a.dst[d] = dests[d];
     a.ndst = n_dests;
@@ -1469,10 +1502,10 @@ wt_status wt_sweep_to(const wt_engine* e, wt_grid* g, int64_t begin, int64_t end
         ce = rep_sweep(e, g, a, dst, s);
     } else {
         void* scratch = nullptr;
-        const size_t sb = sweep2_scratch_bytes(e->dev, a);
+        const size_t sb = sweep2_scratch_bytes(e->dev(), a);
         if (sb) ce = cudaMallocFromPoolAsync(&scratch, sb, lib_pool(e->device), s);
         if (ce != cudaSuccess) return cuda_err(ce, "wt_sweep_to: scratch");
-        ce = launch_sweep2(e->dev, a, g->wide, scratch, s);
+        ce = launch_sweep2(e->dev(), a, g->wide, scratch, s);
         if (scratch) cudaFreeAsync(scratch, s);
         g_launches += sb ? 2 : 1;
     }
@@ -1600,7 +1633,7 @@ static wt_status gather_impl(const wt_engine* e, const wt_grid* g, const int32_t
     const int grid = int(std::min<int64_t>((n + kGatherThreads - 1) / kGatherThreads,
                                            int64_t(sm_count(e->device)) * 8));
     timing_mark(0, s);
-    ce = launch_gather(e->dev, a, grid, s);
+    ce = launch_gather(e->dev(), a, grid, s);
     timing_mark(1, s);
     timing_mark(2, s);
     g_launches++;
@@ -1622,7 +1655,7 @@ static wt_status gather_impl(const wt_engine* e, const wt_grid* g, const int32_t
             ea.inputs_compact = 1;
         }
         if (ea.out.topk > 0) {
-            ce = launch_eval(e->dev, ea, e->eval_grid, s);
+            ce = launch_eval(e->dev(), ea, e->eval_grid, s);
             g_launches++;
         } else {
             ce = run_list_eval(e, ea, s, escratch);
@@ -1699,7 +1732,7 @@ static wt_status i64_batch(const wt_engine* e, const wt_grid* g, const int64_t* 
         st = g ? wt_gather_batch(e, g, a.M32, a.N32, a.K32, n, out, stream)
                : wt_tune_batch(e, a.M32, a.N32, a.K32, n, out, stream);
         if (st == WT_OK) {
-            ce = launch_wide(e->dev, a, s);
+            ce = launch_wide(e->dev(), a, s);
             g_launches++;
         }
     }

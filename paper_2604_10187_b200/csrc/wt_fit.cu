@@ -1750,7 +1750,10 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
 }
 
 void build_release(wt_build* b) {
-    if (b->done) cudaEventSynchronize(b->done);
+    // engines made from this build read its tables from their own streams
+    // until their first use (wt_engine_create_from_build does not wait):
+    // all device work completes before the tables go back to the pool
+    cudaDeviceSynchronize();
     for (void* q : b->mem) cudaFreeAsync(q, nullptr);
     if (!b->mem.empty()) cudaStreamSynchronize(nullptr);
     b->mem.clear();
