@@ -34,6 +34,8 @@
 #include <cstdlib>
 #include <climits>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -996,9 +998,15 @@ struct Macros {
 // highest wave's fit and anchors (ext_insufficient_waves).  k_ext_vote
 // (thread / macro) then takes the fit's degenerate flag and the per-l
 // majority micro (ties -> smaller micro id).
+// fallback = false: the window bounds only (fallback macros get elo = ehi =
+// 0 and wait for k_ext_prep(fallback = true) after the bucket fits, whose
+// coefficients they copy) -- so the window fits can run beside the bucket
+// fits.  fallback = true: only macros with elo == ehi.
+template <bool FALLBACK>
 __global__ void k_ext_prep(Rec rc, Buckets b, Groups gr, const int64_t* ordA, Macros m, int64_t* elo, int64_t* ehi) {
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= m.nmac) return;
+    if (FALLBACK && ehi[q] > elo[q]) return;  // a window macro (done beside the bucket fits)
     const int64_t b0 = m.bstart[q], b1 = m.bstart[q + 1];
     const int w_lo = max(1, m.W - m.p + 1);
     int64_t wb0 = -1, wb1 = -1;
@@ -1015,6 +1023,7 @@ __global__ void k_ext_prep(Rec rc, Buckets b, Groups gr, const int64_t* ordA, Ma
         return;
     }
     elo[q] = ehi[q] = 0;
+    if (!FALLBACK) return;
     // fewer than two window waves: the highest wave's fit and anchors
     const int64_t top = b1 - 1, gslice = m.gstart_of_bucket[b0];
     for (int c = 0; c < 4; ++c) m.theta[4 * q + c] = b.coeff[4 * top + c];
@@ -1254,6 +1263,19 @@ namespace {
 // hundreds of MB per build costs milliseconds of host time).
 thread_local cudaStream_t t_alloc_stream = nullptr;
 thread_local cudaMemPool_t t_alloc_pool = nullptr;
+
+// a second stream per device for work that overlaps within one build
+cudaStream_t aux_stream(int device) {
+    static std::mutex mu;
+    static std::map<int, cudaStream_t> st;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = st.find(device);
+    if (it != st.end()) return it->second;
+    cudaStream_t x = nullptr;
+    cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+    st[device] = x;
+    return x;
+}
 
 // cub temporaries: the library pool too (the default pool releases its
 // memory at every synchronisation and re-maps it on the next allocation)
@@ -1683,20 +1705,45 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     Buckets bk{NB, d_bslo, d_bshi, B->t_coeff_theta, B->d_r2, B->d_mape, bdegen};
     const int nsm = wtb::device_sms();
     trace("samples + meta");
-    CK(launch_qfit(false, sg, sl, stt, bk, scratch, nsm, s));
-    trace("k_qfit buckets");
     Macros mc{NM, d_mbs, d_bw, d_bgs, W, p, B->t_theta_ext, B->d_ext_flags, B->t_ext_cnt, B->t_ext_l, B->t_ext_micro};
     {
+        // the extrapolation windows (model.cpp:140-192) need the samples
+        // only: their pooled fits and anchor votes run on a second stream
+        // beside the bucket fits; macros without a two-wave window copy their
+        // top bucket's fit after the join
         int64_t* elo = dalloc<int64_t>(owned, NM);
         int64_t* ehi = dalloc<int64_t>(owned, NM);
         int32_t* edeg = dalloc<int32_t>(owned, NM);
+        double* scratch2 = dalloc<double>(owned, kQScr * S_total);  // the window fits' own scratch
+        if (!elo || !ehi || !edeg || !scratch2) {
+            g_fit_err = "cudaMalloc failed (extrapolation)";
+            return WT_CUDA_ERROR;
+        }
         const int mblocks = int((NM + 127) / 128);
-        k_ext_prep<<<mblocks, 128, 0, s>>>(rc, bk, gr, ordA, mc, elo, ehi);
+        cudaStream_t ax = aux_stream(device);
+        cudaEvent_t fork = nullptr, join = nullptr;
+        CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+        struct Evs {
+            cudaEvent_t a, b;
+            ~Evs() {
+                cudaEventDestroy(a);
+                cudaEventDestroy(b);
+            }
+        } evs{fork, join};
+        CK(cudaEventRecord(fork, s));
+        CK(cudaStreamWaitEvent(ax, fork, 0));
+        k_ext_prep<false><<<mblocks, 128, 0, ax>>>(rc, bk, gr, ordA, mc, elo, ehi);
         // pooled window fits (model.cpp:171-176): theta_ext straight into the table
         Buckets ext{NM, elo, ehi, B->t_theta_ext, nullptr, nullptr, edeg};
-        CK(launch_qfit(true, sg, sl, stt, ext, scratch, nsm, s));
-        k_ext_vote<<<int((NM + kVoteWarps - 1) / kVoteWarps), 32 * kVoteWarps, 0, s>>>(rc, gr, ordA, mc, elo, ehi,
-                                                                                       edeg);
+        CK(launch_qfit(true, sg, sl, stt, ext, scratch2, nsm, ax));
+        k_ext_vote<<<int((NM + kVoteWarps - 1) / kVoteWarps), 32 * kVoteWarps, 0, ax>>>(rc, gr, ordA, mc, elo, ehi,
+                                                                                        edeg);
+        CK(cudaEventRecord(join, ax));
+        CK(launch_qfit(false, sg, sl, stt, bk, scratch, nsm, s));
+        trace("k_qfit buckets");
+        CK(cudaStreamWaitEvent(s, join, 0));
+        k_ext_prep<true><<<mblocks, 128, 0, s>>>(rc, bk, gr, ordA, mc, elo, ehi);
     }
     trace("extrapolation");
     {
