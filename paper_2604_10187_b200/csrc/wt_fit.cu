@@ -404,6 +404,23 @@ __global__ void k_mpos(Rec rc, int64_t n, const int32_t* ids_sorted, const int32
     }
 }
 
+// The same with a dense id -> registry position table (ids in [0, nt)):
+// one load per record instead of a binary search.
+__global__ void k_mpos_dense(Rec rc, int64_t n, const int32_t* table, int nt, int32_t* mpos, int32_t* valid,
+                             int32_t* has_rec, int32_t* umin_m) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t id = rc.macro[i];
+    const int32_t p = (id >= 0 && id < nt) ? table[id] : -1;
+    const bool ok = p >= 0;
+    mpos[i] = ok ? p : INT_MAX;
+    valid[i] = ok ? 1 : 0;
+    if (ok) {
+        has_rec[p] = 1;  // group_records finds this macro
+        atomicMin(umin_m + p, rc.micro[i]);
+    }
+}
+
 struct Ranges {
     unsigned long long gmin, gmax, lmin, lmax;
     int wmin, wmax, umin, umax;
@@ -1428,6 +1445,15 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
         hup[nid + i] = ids[i].second;
     }
     std::copy(registry_ids, registry_ids + n_macros, hup.begin() + 2 * nid);
+    // small non-negative ids (the usual registry): a dense id -> position
+    // table after the upload block replaces the per-record binary search
+    const int32_t id_min = nid ? ids.front().first : 0, id_max = nid ? ids.back().first : -1;
+    const bool dense = nid > 0 && id_min >= 0 && int64_t(id_max) < std::max<int64_t>(4096, 8 * int64_t(nid));
+    const size_t dense_off = hup.size();
+    if (dense) {
+        hup.resize(dense_off + size_t(id_max) + 1, -1);
+        for (int i = 0; i < nid; ++i) hup[dense_off + size_t(ids[i].first)] = ids[i].second;
+    }
     int32_t* dup = dalloc<int32_t>(owned, hup.size());
     // read-back block: nvalid (i64) | ranges | has_rec[n_macros]
     struct Head {
@@ -1453,7 +1479,10 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     int32_t* has_rec = reinterpret_cast<int32_t*>(drb + sizeof(Head));
     const int blocks_all = int((n_all + 255) / 256);
     k_fill_i32<<<(n_macros + 255) / 256, 256, 0, s>>>(umin_m, n_macros, INT_MAX);
-    k_mpos<<<blocks_all, 256, 0, s>>>(rc, n_all, dup, dup + nid, nid, mpos, valid, has_rec, umin_m);
+    if (dense)
+        k_mpos_dense<<<blocks_all, 256, 0, s>>>(rc, n_all, dup + dense_off, id_max + 1, mpos, valid, has_rec, umin_m);
+    else
+        k_mpos<<<blocks_all, 256, 0, s>>>(rc, n_all, dup, dup + nid, nid, mpos, valid, has_rec, umin_m);
     // key ranges over every record (a superset of the valid ones: packing
     // stays exact) and max w over ALL records (model.cpp:201-203)
     k_ranges<<<int(std::min<int64_t>((n_all + 255) / 256, int64_t(wtb::device_sms()) * 8)), 256, 0, s>>>(rc, nullptr, n_all, mpos, umin_m,
@@ -1467,6 +1496,7 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
         CK(cub::DeviceSelect::Flagged(t, need, it, valid, idx, &dh->nvalid, n_all, s));
         cudaFreeAsync(t, s);
     }
+    trace("registry + ranges queued");
     std::vector<char> hrb(rb_bytes);
     CK(cudaMemcpyAsync(hrb.data(), drb, rb_bytes, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
