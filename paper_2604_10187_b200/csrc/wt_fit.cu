@@ -1294,6 +1294,36 @@ cudaStream_t aux_stream(int device) {
     return x;
 }
 
+// Pinned host words for the build's scalar read-backs (one per host thread;
+// a pageable D2H is staged and costs several times a pinned one).
+void* pinned_words(size_t bytes) {
+    thread_local void* p = nullptr;
+    thread_local size_t cap = 0;
+    if (bytes > cap) {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(bytes, 64 << 10);
+        if (cudaMallocHost(&p, want) != cudaSuccess) return nullptr;
+        cap = want;
+    }
+    return p;
+}
+
+// last element of each of up to 6 device arrays into one small block (one
+// read-back instead of six); w32[k] != 0: an int32 array, else int64
+struct Tails {
+    const void* a[6];
+    int32_t w32[6];
+    int32_t n;
+};
+__global__ void k_tails(Tails t, int64_t idx, int64_t* out) {
+    const int k = threadIdx.x;
+    if (k >= t.n) return;
+    out[k] = t.w32[k] ? int64_t(static_cast<const int32_t*>(t.a[k])[idx])
+                      : static_cast<const int64_t*>(t.a[k])[idx];
+}
+
 // cub temporaries: the library pool too (the default pool releases its
 // memory at every synchronisation and re-maps it on the next allocation)
 cudaError_t talloc(void** p, size_t bytes, cudaStream_t s) {
@@ -1497,9 +1527,15 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
         cudaFreeAsync(t, s);
     }
     trace("registry + ranges queued");
-    std::vector<char> hrb(rb_bytes);
-    CK(cudaMemcpyAsync(hrb.data(), drb, rb_bytes, cudaMemcpyDeviceToHost, s));
+    char* hrbp = static_cast<char*>(pinned_words(rb_bytes));
+    std::vector<char> hrb_fallback;
+    if (!hrbp) {
+        hrb_fallback.resize(rb_bytes);
+        hrbp = hrb_fallback.data();
+    }
+    CK(cudaMemcpyAsync(hrbp, drb, rb_bytes, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    const std::vector<char> hrb(hrbp, hrbp + rb_bytes);  // the pinned words are reused below
     Head hh;
     std::memcpy(&hh, hrb.data(), sizeof(Head));
     const int64_t n = hh.nvalid;
@@ -1596,11 +1632,17 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
         CK(cub::DeviceScan::ExclusiveSum(t, need, gflag, gid, n, s));
         cudaFreeAsync(t, s);
     }
-    int32_t last2[2] = {0, 0};
-    CK(cudaMemcpyAsync(&last2[0], gid + n - 1, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&last2[1], gflag + n - 1, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    const int64_t G = int64_t(last2[0]) + last2[1];
+    int64_t* dtail = dalloc<int64_t>(owned, 8);
+    int64_t* htail = static_cast<int64_t*>(pinned_words(64));
+    int64_t htail_fb[8];
+    if (!htail) htail = htail_fb;
+    {
+        Tails t{{gid, gflag}, {1, 1}, 2};
+        k_tails<<<1, 32, 0, s>>>(t, n - 1, dtail);
+        CK(cudaMemcpyAsync(htail, dtail, 2 * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    const int64_t G = htail[0] + htail[1];
     // G-sized outputs (anchors = groups; ext-anchor slices live at each
     // macro's first group) in one block owned by the build
     {
@@ -1663,18 +1705,14 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
         CK(cub::DeviceScan::ExclusiveSum(t, need, in, out, G, s));
         cudaFreeAsync(t, s);
     }
-    int32_t tail4[4];
-    int64_t tail_soff = 0;
-    int32_t last_ns = 0;
-    CK(cudaMemcpyAsync(&tail4[0], bid + G - 1, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&tail4[1], bflag + G - 1, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&tail4[2], mid + G - 1, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&tail4[3], mflag + G - 1, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&tail_soff, soff + G - 1, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&last_ns, gr.nsamp + G - 1, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    const int64_t NB = int64_t(tail4[0]) + tail4[1], NM = int64_t(tail4[2]) + tail4[3];
-    const int64_t S_total = tail_soff + last_ns;
+    {
+        Tails t{{bid, bflag, mid, mflag, soff, gr.nsamp}, {1, 1, 1, 1, 0, 1}, 6};
+        k_tails<<<1, 32, 0, s>>>(t, G - 1, dtail);
+        CK(cudaMemcpyAsync(htail, dtail, 6 * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    const int64_t NB = htail[0] + htail[1], NM = htail[2] + htail[3];
+    const int64_t S_total = htail[4] + htail[5];
     if (NM != int64_t(B->h_macro_id.size())) {
         g_fit_err = "build_dual_table: macro count mismatch";
         return WT_RUNTIME_ERROR;
