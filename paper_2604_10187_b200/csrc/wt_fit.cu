@@ -1500,10 +1500,23 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
         g_fit_err = "cudaMalloc failed";
         return WT_CUDA_ERROR;
     }
-    CK(cudaMemcpyAsync(dup, hup.data(), hup.size() * 4, cudaMemcpyHostToDevice, s));
     Head h0{};
     h0.r = Ranges{~0ULL, 0ULL, ~0ULL, 0ULL, INT_MAX, INT_MIN, INT_MAX, INT_MIN};
-    CK(cudaMemcpyAsync(drb, &h0, sizeof(Head), cudaMemcpyHostToDevice, s));
+    {
+        // both uploads from the pinned words (no staging copy); the first
+        // read-back below syncs the stream before the words are reused
+        const size_t hb = (hup.size() * 4 + 255) & ~size_t(255);
+        char* pw = static_cast<char*>(pinned_words(hb + sizeof(Head)));
+        if (pw) {
+            std::memcpy(pw, hup.data(), hup.size() * 4);
+            std::memcpy(pw + hb, &h0, sizeof(Head));
+            CK(cudaMemcpyAsync(dup, pw, hup.size() * 4, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(drb, pw + hb, sizeof(Head), cudaMemcpyHostToDevice, s));
+        } else {
+            CK(cudaMemcpyAsync(dup, hup.data(), hup.size() * 4, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(drb, &h0, sizeof(Head), cudaMemcpyHostToDevice, s));
+        }
+    }
     CK(cudaMemsetAsync(drb + sizeof(Head), 0, size_t(n_macros) * 4, s));
     Head* dh = reinterpret_cast<Head*>(drb);
     int32_t* has_rec = reinterpret_cast<int32_t*>(drb + sizeof(Head));
