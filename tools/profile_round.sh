@@ -20,7 +20,7 @@ ncu --set full --clock-control none --import-source on -k regex:k_escatter -s 2 
 # the build (config 3/4, records in HBM -> grid): representative sweep, bucket fit, pruning masks
 ncu --set full --clock-control none --import-source on -k regex:k_sweep_w -s 1 -c 1 -o $O/ncu_sweepw_$TAG -f \
     python tools/prof_kernels.py build > /dev/null 2>&1; echo "sweep_w $?"
-ncu --set full --clock-control none --import-source on -k regex:k_qfit -s 2 -c 1 -o $O/ncu_qfit_$TAG -f \
+ncu --set full --clock-control none --import-source on -k regex:k_qfit -s 3 -c 1 -o $O/ncu_qfit_$TAG -f \
     python tools/prof_kernels.py build > /dev/null 2>&1; echo "qfit $?"
 ncu --set full --clock-control none --import-source on -k regex:k_img_prune -s 1 -c 1 -o $O/ncu_prune_$TAG -f \
     python tools/prof_kernels.py build > /dev/null 2>&1; echo "prune $?"
