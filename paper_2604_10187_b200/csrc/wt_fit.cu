@@ -175,7 +175,9 @@ __device__ FitOut group_fit(const double* g, const double* l, const double* t, i
     double mxa = 0.0;
     bool have = false;
     for (int r = G.first(0); r < n; r += SUB) {
-        const double v = fabs(dcol(g, l, q, r));
+        const double d = dcol(g, l, q, r);
+        A[r * la + q] = d;  // the raw column, scaled in place below (one read of g / l per row)
+        const double v = fabs(d);
         if (!have || v > mxa) mxa = v;
         have = true;
     }
@@ -191,7 +193,7 @@ __device__ FitOut group_fit(const double* g, const double* l, const double* t, i
     const double sc = mxa > 0 ? mxa : 1.0;
     double nrm = 0.0;
     for (int r = G.first(0); r < n; r += SUB) {
-        const double v = __ddiv_rn(dcol(g, l, q, r), sc);
+        const double v = __ddiv_rn(A[r * la + q], sc);
         A[r * la + q] = v;
         nrm = __dadd_rn(nrm, __dmul_rn(v, v));
     }
