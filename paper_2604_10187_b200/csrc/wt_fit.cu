@@ -377,6 +377,12 @@ struct Rec {
     const double* lat;
 };
 
+// 32-bit sort permutation -> the 64-bit order the later kernels index with
+__global__ void k_widen(const uint32_t* in, int64_t n, int64_t* out) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = int64_t(in[i]);
+}
+
 __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -514,11 +520,11 @@ struct Pass {
     int nf, bits;
 };
 
-__global__ void k_pack(Rec rc, const int32_t* mpos, const int32_t* umin_m, const int64_t* perm, int64_t n, Pass ps,
+__global__ void k_pack(Rec rc, const int32_t* mpos, const int32_t* umin_m, const uint32_t* perm, int64_t n, Pass ps,
                        unsigned long long* key) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int64_t r = perm ? perm[i] : i;
+    const int64_t r = perm ? int64_t(perm[i]) : i;
     unsigned long long k = 0;
     for (int q = 0; q < ps.nf; ++q) {
         const Field& f = ps.f[q];
@@ -1386,7 +1392,7 @@ std::vector<Pass> plan_passes(const std::vector<Field>& fields) {
 // and `keys_alt` the last pass's sorted keys.
 // identity: perm starts as 0..n-1 (every record valid), so the first pass
 // packs record i directly.
-wt_status run_sort(const Rec& rc, const int32_t* mpos, const int32_t* umin_m, int64_t*& perm, int64_t*& perm_alt,
+wt_status run_sort(const Rec& rc, const int32_t* mpos, const int32_t* umin_m, uint32_t*& perm, uint32_t*& perm_alt,
                    int64_t n, const std::vector<Pass>& passes, unsigned long long* keys, unsigned long long* keys_alt,
                    void*& tmp, size_t& tmp_bytes, cudaStream_t s, bool identity = false) {
     bool first = true;
@@ -1415,6 +1421,10 @@ wt_status run_sort(const Rec& rc, const int32_t* mpos, const int32_t* umin_m, in
 // presence; group count; bucket / sample counts).  Outputs land in B.
 wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, int32_t n_macros, int32_t W,
                    int32_t p, bool baselines, int device, cudaStream_t s, wt_build* B) {
+    if (n_all >= (int64_t(1) << 31)) {  // the sorts permute 32-bit record indices
+        g_fit_err = "build_dual_table: 2^31 or more records are outside the device path's range";
+        return WT_UNSUPPORTED;
+    }
     t_alloc_stream = s;
     t_alloc_pool = wtb::device_pool(device);
     std::vector<void*> owned;
@@ -1496,7 +1506,7 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     char* drb = dalloc<char>(owned, rb_bytes);
     int32_t* mpos = dalloc<int32_t>(owned, n_all);
     int32_t* valid = dalloc<int32_t>(owned, n_all);
-    int64_t* idx = dalloc<int64_t>(owned, n_all);
+    uint32_t* idx = dalloc<uint32_t>(owned, n_all);  // record indices (< 2^31: 32-bit sort values)
     int32_t* umin_m = dalloc<int32_t>(owned, n_macros);
     if (!dup || !drb || !mpos || !valid || !idx || !umin_m) {
         g_fit_err = "cudaMalloc failed";
@@ -1533,7 +1543,7 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     k_ranges<<<int(std::min<int64_t>((n_all + 255) / 256, int64_t(wtb::device_sms()) * 8)), 256, 0, s>>>(rc, nullptr, n_all, mpos, umin_m,
                                                                                   &dh->r);
     {  // compact valid record indices, order preserved
-        cub::CountingInputIterator<int64_t> it(0);
+        cub::CountingInputIterator<uint32_t> it(0);
         size_t need = 0;
         cub::DeviceSelect::Flagged(nullptr, need, it, valid, idx, &dh->nvalid, n_all, s);
         void* t = nullptr;
@@ -1583,9 +1593,12 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     CK(cudaEventRecord(B->ev0, s));
     trace("registry + ranges");
     // 2. stable sorts
-    // ordA starts as the compacted index list itself (the sort swaps buffers)
-    int64_t* ordA = idx;
-    int64_t* alt = dalloc<int64_t>(owned, n);
+    // the sorts permute 32-bit record indices (12 bytes per element and pass
+    // with the key instead of 16); order A starts as the compacted index list
+    // itself (the passes swap buffers) and is widened to 64 bits afterwards
+    uint32_t* permA = idx;
+    uint32_t* alt = dalloc<uint32_t>(owned, n);
+    int64_t* ordA = dalloc<int64_t>(owned, n);
     unsigned long long* keys = dalloc<unsigned long long>(owned, n);
     unsigned long long* keys2 = dalloc<unsigned long long>(owned, n);
     void* tmp = nullptr;
@@ -1594,16 +1607,20 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     {
         // order B's sort runs first from a copy of the index list, so that
         // order A's sorted keys (its single pass) survive for the group kernels
+        const int wblocks = int((n + 255) / 256);
         if (bits_u != 0) {
+            uint32_t* permB = dalloc<uint32_t>(owned, n);
+            uint32_t* altB = dalloc<uint32_t>(owned, n);
             ordB = dalloc<int64_t>(owned, n);
-            int64_t* altB = dalloc<int64_t>(owned, n);
-            CK(cudaMemcpyAsync(ordB, idx, n * 8, cudaMemcpyDeviceToDevice, s));
-            wt_status sb = run_sort(rc, mpos, umin_m, ordB, altB, n, passB, keys, keys2, tmp, tmp_bytes, s,
+            CK(cudaMemcpyAsync(permB, idx, n * 4, cudaMemcpyDeviceToDevice, s));
+            wt_status sb = run_sort(rc, mpos, umin_m, permB, altB, n, passB, keys, keys2, tmp, tmp_bytes, s,
                                     n == n_all);
             if (sb) return sb;
+            k_widen<<<wblocks, 256, 0, s>>>(permB, n, ordB);
         }
-        wt_status sa = run_sort(rc, mpos, umin_m, ordA, alt, n, passA, keys, keys2, tmp, tmp_bytes, s, n == n_all);
+        wt_status sa = run_sort(rc, mpos, umin_m, permA, alt, n, passA, keys, keys2, tmp, tmp_bytes, s, n == n_all);
         if (sa) return sa;
+        k_widen<<<wblocks, 256, 0, s>>>(permA, n, ordA);
         // one micro id per macro: order A (macro, w, l, micro, g) is order B
         // (macro, w, l, g) -- one sort
         if (bits_u == 0) ordB = ordA;
