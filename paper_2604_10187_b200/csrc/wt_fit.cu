@@ -525,16 +525,21 @@ __global__ void k_pack(Rec rc, const int32_t* mpos, const int32_t* umin_m, const
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int64_t r = perm ? int64_t(perm[i]) : i;
+    // the record's fields, loaded together (the field loop below only shifts)
+    const unsigned long long g = (unsigned long long)rc.g[r] ^ 0x8000000000000000ULL;
+    const unsigned long long l = (unsigned long long)rc.l[r] ^ 0x8000000000000000ULL;
+    const int32_t w = rc.w[r];
+    const int32_t mp = mpos[r];
     unsigned long long k = 0;
     for (int q = 0; q < ps.nf; ++q) {
         const Field& f = ps.f[q];
         unsigned long long v;
         switch (f.which) {
-            case 0: v = ((unsigned long long)rc.g[r] ^ 0x8000000000000000ULL) - f.base; break;
-            case 1: v = (unsigned long long)((long long)rc.micro[r] - umin_m[mpos[r]]) - f.base; break;
-            case 2: v = ((unsigned long long)rc.l[r] ^ 0x8000000000000000ULL) - f.base; break;
-            case 3: v = (unsigned long long)(long long)(rc.w[r]) - f.base; break;
-            default: v = (unsigned long long)mpos[r]; break;
+            case 0: v = g - f.base; break;
+            case 1: v = (unsigned long long)((long long)rc.micro[r] - umin_m[mp]) - f.base; break;
+            case 2: v = l - f.base; break;
+            case 3: v = (unsigned long long)(long long)(w) - f.base; break;
+            default: v = (unsigned long long)mp; break;
         }
         k |= v << f.shift;
     }
