@@ -377,12 +377,6 @@ struct Rec {
     const double* lat;
 };
 
-// 32-bit sort permutation -> the 64-bit order the later kernels index with
-__global__ void k_widen(const uint32_t* in, int64_t n, int64_t* out) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = int64_t(in[i]);
-}
-
 __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -550,7 +544,7 @@ __device__ __forceinline__ bool same_group(const Rec& rc, const int32_t* mpos, i
     return mpos[a] == mpos[b] && rc.w[a] == rc.w[b] && rc.l[a] == rc.l[b];
 }
 
-__global__ void k_group_flags(Rec rc, const int32_t* mpos, const int64_t* ordA, int64_t n, int32_t* gflag) {
+__global__ void k_group_flags(Rec rc, const int32_t* mpos, const uint32_t* ordA, int64_t n, int32_t* gflag) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     gflag[i] = (i == 0 || !same_group(rc, mpos, ordA[i], ordA[i - 1])) ? 1 : 0;
@@ -600,7 +594,7 @@ struct Groups {
 };
 
 // select_shared_micro (model.cpp:81-120) on group q = [start[q], start[q+1])
-__global__ void k_select(Rec rc, const int64_t* ordA, const int64_t* ordB, int64_t G, Groups gr) {
+__global__ void k_select(Rec rc, const uint32_t* ordA, const uint32_t* ordB, int64_t G, Groups gr) {
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= G) return;
     const int64_t s = gr.start[q], e = gr.start[q + 1];
@@ -645,7 +639,7 @@ __global__ void k_select(Rec rc, const int64_t* ordA, const int64_t* ordB, int64
     gr.nsamp[q] = best_cover;
 }
 
-__global__ void k_samples(Rec rc, const int64_t* ordA, int64_t G, Groups gr, const int64_t* soff, double* sg,
+__global__ void k_samples(Rec rc, const uint32_t* ordA, int64_t G, Groups gr, const int64_t* soff, double* sg,
                           double* sl, double* st) {
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= G) return;
@@ -666,7 +660,7 @@ __global__ void k_samples(Rec rc, const int64_t* ordA, int64_t G, Groups gr, con
 // latencies are gathered through the permutation.  Same operations, same
 // order -- bit-identical.
 __global__ void k_select_k(Rec rc, const unsigned long long* keys, KeyFields kf, const int32_t* umin_m,
-                           const int64_t* ordA, int64_t G, Groups gr) {
+                           const uint32_t* ordA, int64_t G, Groups gr) {
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= G) return;
     const int64_t s = gr.start[q], e = gr.start[q + 1];
@@ -711,7 +705,7 @@ __global__ void k_select_k(Rec rc, const unsigned long long* keys, KeyFields kf,
     gr.nsamp[q] = best_cover;
 }
 
-__global__ void k_samples_k(Rec rc, const unsigned long long* keys, KeyFields kf, const int64_t* ordA, int64_t G,
+__global__ void k_samples_k(Rec rc, const unsigned long long* keys, KeyFields kf, const uint32_t* ordA, int64_t G,
                             Groups gr, const int64_t* soff, double* sg, double* sl, double* st) {
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= G) return;
@@ -728,7 +722,7 @@ __global__ void k_samples_k(Rec rc, const unsigned long long* keys, KeyFields kf
     }
 }
 
-__global__ void k_group_meta(Rec rc, const int32_t* mpos, const int64_t* ordA, int64_t G, Groups gr, int64_t* gm,
+__global__ void k_group_meta(Rec rc, const int32_t* mpos, const uint32_t* ordA, int64_t G, Groups gr, int64_t* gm,
                              int64_t* gw, int64_t* gl, int32_t* bflag, int32_t* mflag) {
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= G) return;
@@ -1033,7 +1027,7 @@ struct Macros {
 // coefficients they copy) -- so the window fits can run beside the bucket
 // fits.  fallback = true: only macros with elo == ehi.
 template <bool FALLBACK>
-__global__ void k_ext_prep(Rec rc, Buckets b, Groups gr, const int64_t* ordA, Macros m, int64_t* elo, int64_t* ehi) {
+__global__ void k_ext_prep(Rec rc, Buckets b, Groups gr, const uint32_t* ordA, Macros m, int64_t* elo, int64_t* ehi) {
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= m.nmac) return;
     if (FALLBACK && ehi[q] > elo[q]) return;  // a window macro (done beside the bucket fits)
@@ -1077,7 +1071,7 @@ __global__ void k_ext_prep(Rec rc, Buckets b, Groups gr, const int64_t* ordA, Ma
 constexpr int kVoteWarps = 4;
 constexpr int kVoteCap = 256;
 __global__ void __launch_bounds__(32 * kVoteWarps)
-    k_ext_vote(Rec rc, Groups gr, const int64_t* ordA, Macros m, const int64_t* elo, const int64_t* ehi,
+    k_ext_vote(Rec rc, Groups gr, const uint32_t* ordA, Macros m, const int64_t* elo, const int64_t* ehi,
                const int32_t* edeg) {
     __shared__ int64_t sl[kVoteWarps][kVoteCap];
     __shared__ int32_t sm[kVoteWarps][kVoteCap], sc[kVoteWarps][kVoteCap], sf[kVoteWarps][kVoteCap];
@@ -1600,32 +1594,30 @@ wt_status fit_core(const Rec& rc, int64_t n_all, const int32_t* registry_ids, in
     // 2. stable sorts
     // the sorts permute 32-bit record indices (12 bytes per element and pass
     // with the key instead of 16); order A starts as the compacted index list
-    // itself (the passes swap buffers) and is widened to 64 bits afterwards
+    // itself (the passes swap buffers); the later kernels index with it as is
     uint32_t* permA = idx;
     uint32_t* alt = dalloc<uint32_t>(owned, n);
-    int64_t* ordA = dalloc<int64_t>(owned, n);
     unsigned long long* keys = dalloc<unsigned long long>(owned, n);
     unsigned long long* keys2 = dalloc<unsigned long long>(owned, n);
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
-    int64_t* ordB = nullptr;
+    uint32_t* ordB = nullptr;
+    uint32_t* ordA = nullptr;
     {
         // order B's sort runs first from a copy of the index list, so that
         // order A's sorted keys (its single pass) survive for the group kernels
-        const int wblocks = int((n + 255) / 256);
         if (bits_u != 0) {
             uint32_t* permB = dalloc<uint32_t>(owned, n);
             uint32_t* altB = dalloc<uint32_t>(owned, n);
-            ordB = dalloc<int64_t>(owned, n);
             CK(cudaMemcpyAsync(permB, idx, n * 4, cudaMemcpyDeviceToDevice, s));
             wt_status sb = run_sort(rc, mpos, umin_m, permB, altB, n, passB, keys, keys2, tmp, tmp_bytes, s,
                                     n == n_all);
             if (sb) return sb;
-            k_widen<<<wblocks, 256, 0, s>>>(permB, n, ordB);
+            ordB = permB;
         }
         wt_status sa = run_sort(rc, mpos, umin_m, permA, alt, n, passA, keys, keys2, tmp, tmp_bytes, s, n == n_all);
         if (sa) return sa;
-        k_widen<<<wblocks, 256, 0, s>>>(permA, n, ordA);
+        ordA = permA;
         // one micro id per macro: order A (macro, w, l, micro, g) is order B
         // (macro, w, l, g) -- one sort
         if (bits_u == 0) ordB = ordA;
