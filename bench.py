@@ -620,6 +620,9 @@ def run_wavetune(args):
     step()
     torch.cuda.synchronize(dev)
     assert torch.equal(macp, mac.cpu()) and torch.equal(latp.view(torch.int64), lat.cpu().view(torch.int64))
+    # what bounds e2e: the same pinned copies, same chunking and slot streams,
+    # no decisions (the host buffers are not read after this)
+    copy_s = copy_ceiling_s(torch, dev, (Mp, Np, Kp), (macp, micp, latp), e2e_steps)
 
     # secondary: the build path (configs 3 and 4) -- records in HBM -> grid
     sec = {}
@@ -646,7 +649,11 @@ def run_wavetune(args):
                        "queries_per_rank": n, "configs": eng.n_configs, "grid_shapes": grid.n_entries,
                        "l2": "inputs 1.2 GB/rank > L2 (no flush needed)", "parallelism": f"replicas x{ws}"},
             "e2e": {"value": ws * n / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": 12 * n,
-                    "d2h_bytes_per_step": 16 * n},
+                    "d2h_bytes_per_step": 16 * n,
+                    "copy_ceiling": {"value": ws * n / copy_s, "frac": copy_s / e2e_s,
+                                     "what": "the step's pinned H2D + D2H copies alone (4 slot streams, "
+                                             "4 Mi-query chunks, both copy engines), no decisions: "
+                                             "the PCIe bound of the e2e number"}},
             "roofline": {"kernel": "k_gather", "bound": "hbm", "achieved": achieved,
                          "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                          "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peaks_kind,
@@ -671,6 +678,33 @@ def run_wavetune(args):
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def copy_ceiling_s(torch, dev, hin, hout, steps, chunk=1 << 22, slots=4):
+    """Seconds per step of the e2e path's copies alone: H2D of the (M, N, K)
+    chunks and D2H of the (macro, micro, latency) chunks on `slots` streams,
+    the chunking wt_decide_host_stream_sync uses (wall clock, like e2e)."""
+    n = hin[0].numel()
+    chunk = min(chunk, n)
+    st = [torch.cuda.Stream(dev) for _ in range(slots)]
+    din = [[torch.empty(chunk, dtype=h.dtype, device=dev) for h in hin] for _ in range(slots)]
+    dout = [[torch.empty(chunk, dtype=h.dtype, device=dev) for h in hout] for _ in range(slots)]
+
+    def once():
+        for k, i in enumerate(range(0, n, chunk)):
+            s, m = k % slots, min(chunk, n - i)
+            with torch.cuda.stream(st[s]):
+                for d, h in zip(din[s], hin):
+                    d[:m].copy_(h[i:i + m], non_blocking=True)
+                for d, h in zip(dout[s], hout):
+                    h[i:i + m].copy_(d[:m], non_blocking=True)
+        torch.cuda.synchronize(dev)
+
+    once()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        once()
+    return (time.perf_counter() - t0) / steps
 
 
 def main():
