@@ -99,6 +99,11 @@ struct Grp {
     }
 };
 
+// dcol (below) through the read-only path, for the batched first pass
+__device__ __forceinline__ double dcol_ldg(const double* g, const double* l, int c, int r) {
+    return c == 0 ? __dmul_rn(__ldg(g + r), __ldg(l + r)) : c == 1 ? __ldg(g + r) : c == 2 ? __ldg(l + r) : 1.0;
+}
+
 // design column c of sample r (model.cpp:24-32): g*l, g, l, 1
 __device__ __forceinline__ double dcol(const double* g, const double* l, int c, int r) {
     return c == 0 ? __dmul_rn(g[r], l[r]) : c == 1 ? g[r] : c == 2 ? l[r] : 1.0;
@@ -125,6 +130,31 @@ __device__ double q_house(const Grp<SUB>& G, double* col, int la, int k, int n, 
     if (c0 >= 0.0) b = -b;
     const double d = __dadd_rn(c0, -b);
     for (int r = G.first(k + 1); r < n; r += SUB) col[r * la] = __ddiv_rn(col[r * la], d);
+    *beta = b;
+    return __ddiv_rn(__dadd_rn(b, -c0), b);
+}
+
+// q_house's scalars for one lane (SUB = 1): tau, *beta, the divisor *d of
+// the tail rows, *zero = the tail is zeroed instead (tailsq <= DBL_MIN).
+// The caller divides (or zeroes) rows [k+1, n) and writes beta to col[k].
+__device__ double q_house_scalars(const double* col, int la, int k, int n, double* beta, double* d, int* zero) {
+    const double c0 = col[k * la];
+    double tailsq = 0.0;
+    if (n - k != 1) {
+        double p = 0.0;
+        for (int r = k + 1; r < n; ++r) p = __dadd_rn(p, __dmul_rn(col[r * la], col[r * la]));
+        tailsq = p;
+    }
+    if (tailsq <= DBL_MIN) {
+        *beta = c0;
+        *d = 1.0;
+        *zero = 1;
+        return 0.0;
+    }
+    double b = __dsqrt_rn(__dadd_rn(__dmul_rn(c0, c0), tailsq));
+    if (c0 >= 0.0) b = -b;
+    *d = __dadd_rn(c0, -b);
+    *zero = 0;
     *beta = b;
     return __ddiv_rn(__dadd_rn(b, -c0), b);
 }
@@ -174,12 +204,27 @@ __device__ FitOut group_fit(const double* g, const double* l, const double* t, i
     // 1. scaled design (model.cpp:36-41), right-hand side = t
     double mxa = 0.0;
     bool have = false;
-    for (int r = G.first(0); r < n; r += SUB) {
-        const double d = dcol(g, l, q, r);
-        A[r * la + q] = d;  // the raw column, scaled in place below (one read of g / l per row)
-        const double v = fabs(d);
-        if (!have || v > mxa) mxa = v;
-        have = true;
+    // rows in batches of 8: the batch's global loads are issued together
+    // (one memory latency per batch, not per row), then stored / maxed in
+    // row order
+    constexpr int kB = SUB == 1 ? 16 : 8;  // rows per batch and lane
+    for (int r0 = G.first(0); r0 < n; r0 += kB * SUB) {
+        double dv[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            const int r = r0 + u * SUB;
+            dv[u] = r < n ? dcol_ldg(g, l, q, r) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            const int r = r0 + u * SUB;
+            if (r < n) {
+                A[r * la + q] = dv[u];  // the raw column, scaled in place below (one read of g / l per row)
+                const double v = fabs(dv[u]);
+                if (!have || v > mxa) mxa = v;
+                have = true;
+            }
+        }
     }
     if constexpr (SUB > 1) {  // max is order-free; design columns are finite
 #pragma unroll
@@ -199,7 +244,14 @@ __device__ FitOut group_fit(const double* g, const double* l, const double* t, i
     }
     nrm = G.red(nrm);
     if (q == 0)
-        for (int r = G.first(0); r < n; r += SUB) rhs[r * lr] = t[r];
+        for (int r0 = G.first(0); r0 < n; r0 += 8 * SUB) {
+            double tv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) tv[u] = r0 + u * SUB < n ? __ldg(t + r0 + u * SUB) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (r0 + u * SUB < n) rhs[(r0 + u * SUB) * lr] = tv[u];
+        }
     double scale[4], upd[4], direct[4];
     const double dn = __dsqrt_rn(nrm);
 #pragma unroll
@@ -245,10 +297,25 @@ __device__ FitOut group_fit(const double* g, const double* l, const double* t, i
         for (int c = 0; c < 4; ++c)
             if (own[c] == q) lj = c;
         double tk = 0.0, bk = 0.0;
-        if (lj == k) {
-            tk = q_house(G, A + q, la, k, n, &bk);
-            G.sync_own();  // every sub-lane has read col[k] (c0) before it is overwritten
-            if (j == 0) A[k * la + q] = bk;
+        if constexpr (SUB == 1) {
+            // the owner forms the reflector's scalars; the quad's four lanes
+            // divide the tail rows (k+1+q, step 4) -- elementwise, so the
+            // same correctly rounded quotients as one lane's loop
+            double dk = 0.0;
+            int zero = 0;
+            if (lj == k) tk = q_house_scalars(A + q, la, k, n, &bk, &dk, &zero);
+            dk = G.own(dk, own[k]);
+            zero = __shfl_sync(G.m, zero, own[k], 4);
+            G.sync();
+            double* ck = A + own[k];
+            for (int r = k + 1 + q; r < n; r += 4) ck[r * la] = zero ? 0.0 : __ddiv_rn(ck[r * la], dk);
+            if (lj == k) A[k * la + q] = bk;  // row k: disjoint from the tail rows
+        } else {
+            if (lj == k) {
+                tk = q_house(G, A + q, la, k, n, &bk);
+                G.sync_own();  // every sub-lane has read col[k] (c0) before it is overwritten
+                if (j == 0) A[k * la + q] = bk;
+            }
         }
         tk = G.own(tk, own[k]);
         bk = G.own(bk, own[k]);
@@ -333,8 +400,20 @@ __device__ FitOut group_fit(const double* g, const double* l, const double* t, i
             for (int c = 0; c < hs; ++c) x[perm[c]] = rhs[c * lr];
         }
     }
+    {  // coefficient c = x[c] / scale[c], divided once by column c's owner
+        double xq = 0.0, sq = 1.0;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) o.c[c] = __ddiv_rn(G.bc(x[c], 0), scale[c]);
+        for (int c = 0; c < 4; ++c) {
+            const double xc = G.bc(x[c], 0);
+            if (c == q) {
+                xq = xc;
+                sq = scale[c];
+            }
+        }
+        const double cq = __ddiv_rn(xq, sq);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) o.c[c] = G.own(cq, c);
+    }
     // 3. diagnostics (model.cpp:64-75): lane (0,0) SS_res, (1,0) mean + SS_tot,
     //    (2,0) MAPE -- each a sequential pass in sample order (skipped when
     //    the caller keeps none: extrapolation windows)
@@ -342,22 +421,51 @@ __device__ FitOut group_fit(const double* g, const double* l, const double* t, i
     o.r2 = o.mape = 0.0;
     if (!diag) return o;
     if (j == 0) {
+        // rows in batches (8 / 4) whose loads issue together; sums stay in
+        // ascending row order
         if (q == 1) {
-            for (int r = 0; r < n; ++r) acc = __dadd_rn(acc, t[r]);
+            for (int r0 = 0; r0 < n; r0 += 8) {
+                double tv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) tv[u] = r0 + u < n ? __ldg(t + r0 + u) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (r0 + u < n) acc = __dadd_rn(acc, tv[u]);
+            }
             const double mean = __ddiv_rn(acc, double(n));
             acc = 0.0;
-            for (int r = 0; r < n; ++r) {
-                const double d = __dadd_rn(t[r], -mean);
-                acc = __dadd_rn(acc, __dmul_rn(d, d));
+            for (int r0 = 0; r0 < n; r0 += 8) {
+                double tv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) tv[u] = r0 + u < n ? __ldg(t + r0 + u) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (r0 + u < n) {
+                        const double d = __dadd_rn(tv[u], -mean);
+                        acc = __dadd_rn(acc, __dmul_rn(d, d));
+                    }
             }
         } else if (q != 3) {
-            for (int r = 0; r < n; ++r) {
-                double f = __dmul_rn(__dmul_rn(g[r], l[r]), o.c[0]);
-                f = __dadd_rn(f, __dmul_rn(g[r], o.c[1]));
-                f = __dadd_rn(f, __dmul_rn(l[r], o.c[2]));
-                f = __dadd_rn(f, __dmul_rn(1.0, o.c[3]));
-                const double d = __dadd_rn(t[r], -f);
-                acc = q == 0 ? __dadd_rn(acc, __dmul_rn(d, d)) : __dadd_rn(acc, __ddiv_rn(fabs(d), fabs(t[r])));
+            for (int r0 = 0; r0 < n; r0 += 4) {
+                double gv[4], lv[4], tv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const bool in = r0 + u < n;
+                    gv[u] = in ? __ldg(g + r0 + u) : 0.0;
+                    lv[u] = in ? __ldg(l + r0 + u) : 0.0;
+                    tv[u] = in ? __ldg(t + r0 + u) : 1.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (r0 + u < n) {
+                        double f = __dmul_rn(__dmul_rn(gv[u], lv[u]), o.c[0]);
+                        f = __dadd_rn(f, __dmul_rn(gv[u], o.c[1]));
+                        f = __dadd_rn(f, __dmul_rn(lv[u], o.c[2]));
+                        f = __dadd_rn(f, __dmul_rn(1.0, o.c[3]));
+                        const double d = __dadd_rn(tv[u], -f);
+                        acc = q == 0 ? __dadd_rn(acc, __dmul_rn(d, d))
+                                     : __dadd_rn(acc, __ddiv_rn(fabs(d), fabs(tv[u])));
+                    }
             }
         }
     }
