@@ -219,9 +219,7 @@ class Engine:
         self.handle = h
         self.device = device
         self._keep = []
-        info = wt_engine_info()
-        check(L.wt_engine_info_get(h, C.byref(info)))
-        self.info = info
+        self._info = None
 
     @classmethod
     def from_build(cls, build: "Build", registry: dict, n_sm: int, blocks_per_sm: int = 1, stream=None):
@@ -236,10 +234,19 @@ class Engine:
         self.handle = h
         self.device = build.device
         self._keep = []
-        info = wt_engine_info()
-        check(lib().wt_engine_info_get(h, C.byref(info)))
-        self.info = info
+        self._info = None
         return self
+
+    @property
+    def info(self):
+        """wt_engine_info, read on first access: it resolves the special-row
+        flag, which waits for the device image -- creation itself stays
+        asynchronous, so a Grid built next overlaps the image kernels."""
+        if self._info is None:
+            info = wt_engine_info()
+            check(lib().wt_engine_info_get(self.handle, C.byref(info)))
+            self._info = info
+        return self._info
 
     def close(self):
         if getattr(self, "handle", None):

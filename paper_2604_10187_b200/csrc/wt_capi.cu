@@ -334,6 +334,42 @@ struct DevTables {
 // Allocates the engine's arena, uploads the plan (one H2D copy), builds the
 // rows, class views and pruning masks on the device from `T`, copies the
 // anchor pool, and reads back the special-row flag (the only host sync).
+// Pinned staging for the plan upload (one buffer per host thread): a
+// pageable H2D of this size blocks the host until the stream reaches the
+// copy, i.e. until the fit's tail has run, which serialised the host's image
+// preparation behind it.  Before the buffer is rewritten, the previous copy
+// out of it is waited for (its event; normally long complete).
+struct PinnedStage {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t done = nullptr;  // recorded after the last copy out of p
+    int done_dev = -1;  // (kept for the thread's life, like the fit's pinned words)
+};
+static void* pinned_stage(PinnedStage& ps, size_t bytes) {
+    if (ps.done) cudaEventSynchronize(ps.done);
+    if (bytes > ps.cap) {
+        if (ps.p) cudaFreeHost(ps.p);
+        ps.p = nullptr;
+        ps.cap = 0;
+        const size_t want = std::max<size_t>(bytes, 256 << 10);
+        if (cudaMallocHost(&ps.p, want) != cudaSuccess) return nullptr;
+        ps.cap = want;
+    }
+    return ps.p;
+}
+static void pinned_stage_mark(PinnedStage& ps, int device, cudaStream_t s) {
+    if (ps.done && ps.done_dev != device) {
+        cudaEventDestroy(ps.done);
+        ps.done = nullptr;
+    }
+    if (!ps.done && cudaEventCreateWithFlags(&ps.done, cudaEventDisableTiming) != cudaSuccess) {
+        ps.done = nullptr;
+        return;
+    }
+    ps.done_dev = device;
+    cudaEventRecord(ps.done, s);
+}
+
 wt_status engine_build(wt_engine* e, const ImagePlan& P, const DevTables& T, cudaStream_t s) {
     const size_t C = P.C, R = P.R, NS = P.seg_pos.size(), NCLS = P.cls_seg.size() - 1;
     const int64_t n_pool = std::max<int64_t>(1, T.n_anchor + T.n_ext);
@@ -356,9 +392,13 @@ wt_status engine_build(wt_engine* e, const ImagePlan& P, const DevTables& T, cud
     if (ce != cudaSuccess) return cuda_err(ce, "wt_engine_create: allocation");
     e->bytes = ar.used;
     char* base = static_cast<char*>(e->mem);
-    std::vector<char> stage(plan_bytes, 0);
+    thread_local PinnedStage pstage;
+    char* pin = static_cast<char*>(pinned_stage(pstage, plan_bytes));
+    std::vector<char> stage(pin ? 0 : plan_bytes, 0);
+    char* sbuf = pin ? pin : stage.data();
+    if (pin) std::memset(pin, 0, plan_bytes);
     auto put = [&](size_t off, const void* src, size_t n) {
-        if (n) std::memcpy(stage.data() + off, src, n);
+        if (n) std::memcpy(sbuf + off, src, n);
     };
     put(o_mid, P.macro_id.data(), C * 4);
     put(o_til, P.tiles.data(), C * 16);
@@ -370,7 +410,8 @@ wt_status engine_build(wt_engine* e, const ImagePlan& P, const DevTables& T, cud
     put(o_ord, P.order.data(), C * 4);
     put(o_cp, P.cfg_pos.data(), C * 4);
     put(o_cs, P.cls_seg.data(), (NCLS + 1) * 4);
-    ce = cudaMemcpyAsync(base, stage.data(), plan_bytes, cudaMemcpyHostToDevice, s);
+    ce = cudaMemcpyAsync(base, sbuf, plan_bytes, cudaMemcpyHostToDevice, s);
+    if (ce == cudaSuccess && pin) pinned_stage_mark(pstage, e->device, s);
     if (ce == cudaSuccess) ce = cudaMemsetAsync(base + o_spec, 0, 4, s);
     auto at = [&](size_t off) { return static_cast<void*>(base + off); };
     if (ce == cudaSuccess && T.n_anchor > 0) {
