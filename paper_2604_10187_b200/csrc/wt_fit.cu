@@ -786,11 +786,24 @@ __global__ void k_select_k(Rec rc, const unsigned long long* keys, KeyFields kf,
             while (j < e && key_micro(keys[j], kf, umin_m) == mu) ++j;
             int32_t cover = 0;
             double mean = 0.0;
-            for (int64_t k = i; k < j; ++k)
-                if (k + 1 == j || key_g(keys[k + 1], kf) != key_g(keys[k], kf)) {  // last write of this g
-                    mean = __dadd_rn(mean, rc.lat[ordA[k]]);
-                    ++cover;
+            // last write of each g, in batches of 8 whose latency gathers
+            // issue together; the sum stays in ascending record order
+            for (int64_t k0 = i; k0 < j; k0 += 8) {
+                double lv[8];
+                bool take[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int64_t k = k0 + u;
+                    take[u] = k < j && (k + 1 == j || key_g(keys[k + 1], kf) != key_g(keys[k], kf));
+                    lv[u] = take[u] ? __ldg(rc.lat + __ldg(ordA + k)) : 0.0;
                 }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (take[u]) {
+                        mean = __dadd_rn(mean, lv[u]);
+                        ++cover;
+                    }
+            }
             mean = __ddiv_rn(mean, double(cover));
             if (!(full && cover != n_g)) {
                 const bool better = best_micro < 0 || (full ? mean < best_mean : cover > best_cover);
@@ -819,14 +832,28 @@ __global__ void k_samples_k(Rec rc, const unsigned long long* keys, KeyFields kf
     if (q >= G) return;
     int64_t o = soff[q];
     const int64_t lo = gr.sel_lo[q], hi = gr.sel_hi[q];
-    for (int64_t k = lo; k < hi; ++k) {
-        const unsigned long long kk = keys[k];
-        if (k + 1 == hi || key_g(keys[k + 1], kf) != key_g(kk, kf)) {
-            sg[o] = double(key_g(kk, kf));
-            sl[o] = double(key_l(kk, kf));
-            st[o] = rc.lat[ordA[k]];
-            ++o;
+    // batches of 8 records: keys and the latency gathers issue together,
+    // the samples are appended in record order
+    for (int64_t k0 = lo; k0 < hi; k0 += 8) {
+        unsigned long long kv[9];
+#pragma unroll
+        for (int u = 0; u < 9; ++u) kv[u] = k0 + u < hi ? __ldg(keys + k0 + u) : 0ull;
+        bool take[8];
+        double lv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t k = k0 + u;
+            take[u] = k < hi && (k + 1 == hi || key_g(kv[u + 1], kf) != key_g(kv[u], kf));
+            lv[u] = take[u] ? __ldg(rc.lat + __ldg(ordA + k)) : 0.0;
         }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (take[u]) {
+                sg[o] = double(key_g(kv[u], kf));
+                sl[o] = double(key_l(kv[u], kf));
+                st[o] = lv[u];
+                ++o;
+            }
     }
 }
 
