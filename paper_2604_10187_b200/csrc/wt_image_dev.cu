@@ -58,7 +58,7 @@ __device__ __forceinline__ bool lex_less(double v, int32_t p, double w, int32_t 
     return v < w || (v == w && p < q);
 }
 
-__global__ void k_img_prune(ImgPruneArgs a) {
+__global__ void __launch_bounds__(256) k_img_prune(ImgPruneArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t cell = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (cell >= a.ncells) return;
@@ -99,15 +99,22 @@ __global__ void k_img_prune(ImgPruneArgs a) {
                 bp[q] = op;
             }
         }
-    double lt[4][4];
+    // the four leaders' rows in shared memory (warp-uniform, read as
+    // broadcasts): 32 registers fewer per lane, more resident warps
+    __shared__ double slt[8][4][4];
+    double(*const lt)[4] = slt[threadIdx.x >> 5];
+    if (lane < 4) {
+        int32_t pq = bp[0];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const double4 t4 = bp[q] >= 0 ? *row(bp[q]) : make_double4(0.0, 0.0, 0.0, 0.0);
-        lt[q][0] = t4.x;
-        lt[q][1] = t4.y;
-        lt[q][2] = t4.z;
-        lt[q][3] = t4.w;
+        for (int q = 1; q < 4; ++q)
+            if (lane == q) pq = bp[q];
+        const double4 t4 = pq >= 0 ? *row(pq) : make_double4(0.0, 0.0, 0.0, 0.0);
+        lt[lane][0] = t4.x;
+        lt[lane][1] = t4.y;
+        lt[lane][2] = t4.z;
+        lt[lane][3] = t4.w;
     }
+    __syncwarp();
     for (int32_t s = s0; s < s1; ++s) {
         const int32_t ps = a.seg_pos[s], cnt = a.seg_tiles[s].w;
         bool keep = false;
