@@ -139,6 +139,9 @@ typedef struct {
 wt_status wt_engine_create(const wt_tables_desc* tables, const wt_registry_desc* registry,
                            const wt_hw* hw, int device, wt_engine** out);
 wt_status wt_engine_destroy(wt_engine* e);
+/* Counts and flags of the engine.  has_fallback_rows is resolved from the
+ * device image, so this call is a first use: it waits for the image build
+ * (call it after queueing the work that should overlap the build). */
 wt_status wt_engine_info_get(const wt_engine* e, wt_engine_info* out);
 /* Host-only (no device needed): the exact pruning plan an engine built from
  * (tables, registry, hw) would use -- for tests and inspection.  Segments
